@@ -1,0 +1,305 @@
+"""CPU oracle for the BrainPy hot path -- TEST INFRASTRUCTURE ONLY.
+
+Thin numpy/ctypes wrapper around ``liboracle.so`` (built from
+``oracle/bp_oracle.c``) plus the network time loop of rule S1 written out in
+Python.  Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package; the
+product package ``paper_2311_05106_b200`` never does, and the two share no
+code.
+
+Spike vectors here are plain ``uint8`` arrays, one entry per neuron, exactly
+the ``events`` of Listing S1/S2.  Conversion from the
+product's bit-packed words is done by the tests, not here.
+
+Parity status per function:
+  philox / conn_len / jit_row / jit_event_mv / event_csrmv /
+  lif_step / hh_step / expf / run_network: pinned (tests/test_oracle_*.py).
+  run_network firing *rates*: parity unpinned by the paper (reading R23) --
+  the paper prints no COBA statistics; rasters are pinned only through the
+  closed-form w = 0 network and the per-step primitives.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "bp_oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+
+OUT_F64, OUT_FIX, OUT_F32 = 0, 1, 2
+LAW_HOMO, LAW_UNIFORM, LAW_NORMAL = 0, 1, 2
+LAWS = {"homo": LAW_HOMO, "uniform": LAW_UNIFORM, "normal": LAW_NORMAL}
+
+BUILD_CMD = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math",
+             "-fPIC", "-shared", "-o", _LIB_PATH, _SRC, "-lm"]
+
+
+def build() -> str:
+    """Compile liboracle.so (gcc, -ffp-contract=off) if it is missing or stale."""
+    if (not os.path.exists(_LIB_PATH)
+            or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC)):
+        subprocess.check_call(BUILD_CMD)
+    return _LIB_PATH
+
+
+class LifParams(ctypes.Structure):
+    _fields_ = [("v_rest", ctypes.c_float), ("v_reset", ctypes.c_float),
+                ("v_th", ctypes.c_float), ("r", ctypes.c_float),
+                ("i_ext", ctypes.c_float), ("e_exc", ctypes.c_float),
+                ("e_inh", ctypes.c_float), ("alpha_v", ctypes.c_float),
+                ("alpha_e", ctypes.c_double), ("alpha_i", ctypes.c_double),
+                ("ref_steps", ctypes.c_int32), ("pad_", ctypes.c_int32)]
+
+
+class HHParams(ctypes.Structure):
+    _fields_ = [(name, ctypes.c_float) for name in
+                ("c_m", "g_l", "e_l", "g_na", "e_na", "g_k", "e_k", "v_t",
+                 "e_exc", "e_inh", "i_ext", "dt", "v_spike", "pad_")] + \
+               [("alpha_e", ctypes.c_double), ("alpha_i", ctypes.c_double)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        P = ctypes.c_void_p
+        u32, u64, i64, f32, f64, i32 = (ctypes.c_uint32, ctypes.c_uint64,
+                                        ctypes.c_int64, ctypes.c_float,
+                                        ctypes.c_double, ctypes.c_int)
+        _lib.or_philox4x32_10.argtypes = [P, P, P]
+        _lib.or_word.argtypes = [u64, u32, u32, u32, u32]
+        _lib.or_word.restype = u32
+        _lib.or_conn_len.argtypes = [f64]
+        _lib.or_conn_len.restype = u32
+        _lib.or_quantize.argtypes = [f32]
+        _lib.or_quantize.restype = i64
+        _lib.or_jit_row.argtypes = [u64, u32, u32, i64, i32, f32, f32, u32,
+                                    i64, i64, P, P, i64]
+        _lib.or_jit_row.restype = i64
+        _lib.or_event_csrmv.argtypes = [P, P, P, f32, i64, P, i32, P, P]
+        _lib.or_jit_event_mv.argtypes = [u64, u32, u32, i32, f32, f32, i64,
+                                         i64, i64, i64, P, i32, P, P]
+        _lib.or_lif_step.argtypes = [ctypes.POINTER(LifParams), i64, P, P, P,
+                                     i32, P, P]
+        _lib.or_hh_step.argtypes = [ctypes.POINTER(HHParams), i64, P, P, P, P,
+                                    P, P, i32, P]
+        _lib.or_expf.argtypes = [f32]
+        _lib.or_expf.restype = f32
+    return _lib
+
+
+def _p(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+# --------------------------------------------------------------------------
+# RNG and connectivity rules (J1-J7)
+# --------------------------------------------------------------------------
+
+def philox(ctr, key) -> np.ndarray:
+    c = np.asarray(ctr, dtype=np.uint32)
+    k = np.asarray(key, dtype=np.uint32)
+    out = np.zeros(4, dtype=np.uint32)
+    lib().or_philox4x32_10(_p(c), _p(k), _p(out))
+    return out
+
+
+def word(seed: int, tag: int, row: int, seg: int, j: int) -> int:
+    return int(lib().or_word(seed, tag, row, seg, j))
+
+
+def conn_len(p: float) -> int:
+    return int(lib().or_conn_len(float(p)))
+
+
+def quantize(w: float) -> int:
+    return int(lib().or_quantize(float(w)))
+
+
+def expf(x: float) -> float:
+    return float(lib().or_expf(float(x)))
+
+
+@dataclass(frozen=True)
+class JitSpec:
+    """Rule J-spec: (seed, K, L) fix the matrix; (law, w0, w1) the weights."""
+    seed: int
+    K: int
+    L: int  # seg_len; the segment grid is part of the connectivity (rule J4)
+    law: int = LAW_HOMO
+    w0: float = 1.0
+    w1: float = 0.0
+
+
+def jit_row(spec: JitSpec, n_cols: int, row: int, seg_first: int = 0,
+            seg_last: int | None = None):
+    """(positions int32, weights float32) of one row, segments seg_first..seg_last."""
+    if seg_last is None:
+        seg_last = (n_cols - 1) // spec.L
+    cap = 64
+    while True:
+        pos = np.empty(cap, np.int32)
+        w = np.empty(cap, np.float32)
+        n = lib().or_jit_row(spec.seed, spec.K, spec.L, n_cols, spec.law,
+                             spec.w0, spec.w1, row, seg_first, seg_last,
+                             _p(pos), _p(w), cap)
+        if n <= cap:
+            return pos[:n].copy(), w[:n].copy()
+        cap = int(n)
+
+
+def jit_materialize(spec: JitSpec, n_rows: int, n_cols: int):
+    """CSR (indptr int64, indices int32, data float32) of the implied matrix."""
+    rows = [jit_row(spec, n_cols, r) for r in range(n_rows)]
+    indptr = np.zeros(n_rows + 1, np.int64)
+    indptr[1:] = np.cumsum([len(p) for p, _ in rows])
+    indices = (np.concatenate([p for p, _ in rows]) if n_rows else
+               np.zeros(0, np.int32)).astype(np.int32)
+    data = (np.concatenate([w for _, w in rows]) if n_rows else
+            np.zeros(0, np.float32)).astype(np.float32)
+    return indptr, indices, data
+
+
+def _out_buf(n: int, out_kind: int):
+    return np.zeros(n, {OUT_F64: np.float64, OUT_FIX: np.int64,
+                        OUT_F32: np.float32}[out_kind])
+
+
+def event_csrmv(indptr, indices, data, w_homo, n_rows, n_cols, events,
+                out_kind=OUT_F64, out=None, with_abs=False):
+    """Listing S1 (indices[j] reading). Returns out (and sum|w| if with_abs)."""
+    indptr = np.ascontiguousarray(indptr, np.int64)
+    indices = np.ascontiguousarray(indices, np.int32)
+    data = None if data is None else np.ascontiguousarray(data, np.float32)
+    ev = np.ascontiguousarray(events, np.uint8)
+    assert ev.shape[0] == n_rows
+    if out is None:
+        out = _out_buf(n_cols, out_kind)
+    absd = np.zeros(n_cols, np.float64) if with_abs else None
+    lib().or_event_csrmv(_p(indptr), _p(indices), _p(data), float(w_homo),
+                         n_rows, _p(ev), out_kind, _p(out), _p(absd))
+    return (out, absd) if with_abs else out
+
+
+def jit_event_mv(spec: JitSpec, n_rows, n_cols, events, col_begin=0,
+                 col_end=None, out_kind=OUT_F64, out=None, with_abs=False):
+    """Listing S2 / rule J9 over columns [col_begin, col_end)."""
+    if col_end is None:
+        col_end = n_cols
+    ev = np.ascontiguousarray(events, np.uint8)
+    assert ev.shape[0] == n_rows
+    if out is None:
+        out = _out_buf(col_end - col_begin, out_kind)
+    absd = np.zeros(col_end - col_begin, np.float64) if with_abs else None
+    lib().or_jit_event_mv(spec.seed, spec.K, spec.L, spec.law, spec.w0,
+                          spec.w1, n_rows, n_cols, col_begin, col_end,
+                          _p(ev), out_kind, _p(out), _p(absd))
+    return (out, absd) if with_abs else out
+
+
+# --------------------------------------------------------------------------
+# Neuron rules N1 / H1
+# --------------------------------------------------------------------------
+
+def lif_params(dt=0.1, tau=20.0, tau_e=5.0, tau_i=10.0, v_rest=-60.0,
+               v_reset=-60.0, v_th=-50.0, r=1.0, i_ext=20.0, e_exc=0.0,
+               e_inh=-80.0, tau_ref=5.0) -> LifParams:
+    """Listing S3 constants; alphas evaluated once, fp64."""
+    return LifParams(v_rest, v_reset, v_th, r, i_ext, e_exc, e_inh,
+                     np.float32(math.exp(-dt / tau)), math.exp(-dt / tau_e),
+                     math.exp(-dt / tau_i), int(round(tau_ref / dt)), 0)
+
+
+def hh_params(dt=0.1, tau_e=5.0, tau_i=10.0, i_ext=0.0) -> HHParams:
+    """Rule H1 constants (Brette et al. 2007 COBAHH; EXTERNAL)."""
+    return HHParams(200.0, 10.0, -60.0, 20000.0, 50.0, 6000.0, -90.0, -63.0,
+                    0.0, -80.0, i_ext, dt, -20.0, 0.0,
+                    math.exp(-dt / tau_e), math.exp(-dt / tau_i))
+
+
+def lif_step(params: LifParams, v, g_e, g_i, ref):
+    """In-place rule N1 on numpy arrays; returns the uint8 spike vector."""
+    n = v.shape[0]
+    g_kind = 1 if g_e.dtype == np.int64 else 0
+    ev = np.zeros(n, np.uint8)
+    lib().or_lif_step(ctypes.byref(params), n, _p(v), _p(g_e), _p(g_i),
+                      g_kind, _p(ref), _p(ev))
+    return ev
+
+
+def hh_step(params: HHParams, v, m, h, nk, g_e, g_i):
+    n = v.shape[0]
+    g_kind = 1 if g_e.dtype == np.int64 else 0
+    ev = np.zeros(n, np.uint8)
+    lib().or_hh_step(ctypes.byref(params), n, _p(v), _p(m), _p(h), _p(nk),
+                     _p(g_e), _p(g_i), g_kind, _p(ev))
+    return ev
+
+
+# --------------------------------------------------------------------------
+# Rule S1: the network time loop (Listing S3 update())
+# --------------------------------------------------------------------------
+
+@dataclass
+class Projection:
+    """Rows = presynaptic neurons [row0, row0 + n_rows); cols = all N posts."""
+    row0: int
+    n_rows: int
+    jit: JitSpec | None = None
+    csr: tuple | None = None        # (indptr, indices, data or None)
+    w_homo: float = 0.0             # CSR homogeneous weight when data is None
+
+
+def run_network(model: str, params, state: dict, proj_e: Projection,
+                proj_i: Projection, n_steps: int, col_begin: int = 0,
+                col_end: int | None = None, record=True):
+    """Rule S1, for n = 0 .. n_steps-1:
+        1. read spikes_{n-1} (state['spikes'], all false at n = 0)
+        2. E rows add into g_E and I rows into g_I (a2/a4)
+        3. neuron rule N1 (LIF) or H1 (HH) -> spikes_n
+        4. store spikes_n
+    `state` holds numpy arrays (v, g_e, g_i, ref | m, h, n) over the
+    postsynaptic columns [col_begin, col_end) and 'spikes' (uint8, all N).
+    g dtype int64 selects fixed point (rule F1), float32 selects fp32.
+    Returns the raster (n_steps x N uint8) when record, else spike counts.
+    """
+    n_total = state["spikes"].shape[0]
+    if col_end is None:
+        col_end = n_total
+    fixed = state["g_e"].dtype == np.int64
+    kind = OUT_FIX if fixed else OUT_F32
+    raster = np.zeros((n_steps, col_end - col_begin), np.uint8) if record else None
+    counts = np.zeros(n_steps, np.int64)
+    for step in range(n_steps):
+        spikes = state["spikes"]
+        for proj, g in ((proj_e, state["g_e"]), (proj_i, state["g_i"])):
+            ev = spikes[proj.row0:proj.row0 + proj.n_rows]
+            if proj.jit is not None:
+                jit_event_mv(proj.jit, proj.n_rows, n_total, ev, col_begin,
+                             col_end, kind, out=g)
+            else:
+                ip, ix, dat = proj.csr
+                event_csrmv(ip, ix, dat, proj.w_homo, proj.n_rows,
+                            col_end - col_begin, ev, kind, out=g)
+        if model == "lif":
+            local = lif_step(params, state["v"], state["g_e"], state["g_i"],
+                             state["ref"])
+        else:
+            local = hh_step(params, state["v"], state["m"], state["h"],
+                            state["n"], state["g_e"], state["g_i"])
+        new = np.zeros(n_total, np.uint8)
+        new[col_begin:col_end] = local
+        state["spikes"] = new
+        counts[step] = int(local.sum())
+        if record:
+            raster[step] = local
+    return raster if record else counts

@@ -1,0 +1,202 @@
+"""Pins for the oracle's JIT connectivity (App. C, Listing S2; rules J4-J9).
+
+The jitconn result has no closed form (it is an RNG-driven encoding of a
+random matrix), so the oracle is pinned by what the paper and probability
+fix: K = 1 gives a dense matrix, each column is connected with probability
+2/(K+1) (the paper's "expectation is 1/p", when 2/p - 1 is an
+integer), gaps have mean (K+1)/2, the connectivity does not depend on the
+events ("synaptic weights remain unchanged during simulation"; P:345
+caption: "consistency of matrix regeneration across multiple invocations"),
+and two independent oracle paths (materialise -> Listing S1 vs Listing S2
+directly) agree.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2311_05106_b200 import inputs
+
+
+def _spec(orc, p, seed=7, L=None, n_cols=None, law="homo", w0=0.6, w1=0.0):
+    K = orc.conn_len(p)
+    return orc.JitSpec(seed=seed, K=K, L=L or n_cols, law=orc.LAWS[law],
+                       w0=w0, w1=w1)
+
+
+def test_dense_when_k_is_one(orc):
+    spec = _spec(orc, 1.0, n_cols=37, L=37)
+    assert spec.K == 1
+    for r in range(50):
+        pos, w = orc.jit_row(spec, 37, r)
+        assert pos.tolist() == list(range(37))
+        assert np.all(w == np.float32(0.6))
+    # y = w * #active exactly for a dense homogeneous matrix
+    ev = inputs.spike_pattern(50, 0.3, 3)
+    y = orc.jit_event_mv(spec, 50, 37, ev, out_kind=orc.OUT_F64)
+    assert np.all(y == float(np.float32(0.6)) * ev.sum())
+
+
+def test_positions_strictly_increasing_and_in_range(orc):
+    for p, n_cols, L in [(0.1, 500, 500), (0.05, 1000, 128), (0.3, 77, 10)]:
+        spec = _spec(orc, p, n_cols=n_cols, L=L)
+        for r in range(200):
+            pos, _ = orc.jit_row(spec, n_cols, r)
+            assert np.all(np.diff(pos) > 0)
+            assert pos.size == 0 or (pos[0] >= 0 and pos[-1] < n_cols)
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 5, 19])
+def test_first_offset_is_stationary(orc, K):
+    """Rule J5: P(first = j) = 2(K-j)/(K(K+1)), the equilibrium residual of a
+    U[1,K] renewal process; chi-square-style 4-sigma check per bin."""
+    n_rows = 40_000
+    spec = orc.JitSpec(seed=11, K=K, L=4 * K + 8)
+    n_cols = spec.L
+    counts = np.zeros(K, np.int64)
+    for r in range(n_rows):
+        pos, _ = orc.jit_row(spec, n_cols, r, 0, 0)
+        counts[pos[0]] += 1
+    for j in range(K):
+        pj = 2.0 * (K - j) / (K * (K + 1))
+        sd = math.sqrt(n_rows * pj * (1 - pj)) + 1e-9
+        assert abs(counts[j] - n_rows * pj) <= 4 * sd + 1, (j, counts)
+
+
+@pytest.mark.parametrize("p,L", [(0.1, 200), (0.1, 50), (0.02, 400)])
+def test_every_column_connected_with_p_eff(orc, p, L):
+    """Each column, including column 0 and every segment start, is connected
+    with probability p_eff = 2/(K+1) (Listing S2's randint(1,K) start never
+    connects column 0 -- reading R6)."""
+    n_cols = 400
+    spec = _spec(orc, p, n_cols=n_cols, L=L)
+    p_eff = 2.0 / (spec.K + 1)
+    n_rows = 6000
+    hits = np.zeros(n_cols, np.int64)
+    for r in range(n_rows):
+        pos, _ = orc.jit_row(spec, n_cols, r)
+        hits[pos] += 1
+    sd = math.sqrt(n_rows * p_eff * (1 - p_eff))
+    dev = np.abs(hits - n_rows * p_eff) / sd
+    assert dev.max() < 5.0, (dev.argmax(), dev.max())
+    # segment starts are not special
+    starts = np.arange(0, n_cols, L)
+    assert np.abs(hits[starts] - n_rows * p_eff).mean() < 2.5 * sd
+
+
+def test_mean_gap(orc):
+    spec = _spec(orc, 0.1, n_cols=100_000)
+    gaps = []
+    for r in range(1000):
+        pos, _ = orc.jit_row(spec, 100_000, r)
+        gaps.append(np.diff(pos))
+    g = np.concatenate(gaps)
+    assert abs(g.mean() - (spec.K + 1) / 2) < 0.01 * (spec.K + 1) / 2
+    assert g.min() == 1 and g.max() == spec.K
+
+
+@pytest.mark.parametrize("p", [0.01, 0.05, 0.1])
+def test_density_2000x2000(orc, p):
+    """empirical density within 4 binomial sigma of 2/(K+1)."""
+    spec = _spec(orc, p, n_cols=2000)
+    ip, _, _ = orc.jit_materialize(spec, 2000, 2000)
+    cells = 2000 * 2000
+    p_eff = 2.0 / (spec.K + 1)
+    sd = math.sqrt(cells * p_eff * (1 - p_eff))
+    assert abs(ip[-1] - cells * p_eff) < 4 * sd
+
+
+@pytest.mark.parametrize("law", ["homo", "uniform", "normal"])
+@pytest.mark.parametrize("L", [None, 64, 100])
+def test_materialised_csr_equals_direct(orc, law, L):
+    """Two independent oracle paths: materialise -> Listing S1 vs Listing S2."""
+    n_rows, n_cols = 300, 500
+    w0, w1 = {"homo": (0.6, 0.0), "uniform": (-0.1, 0.1),
+              "normal": (0.0, 0.5)}[law]
+    spec = _spec(orc, 0.05, seed=99, n_cols=n_cols, L=L, law=law, w0=w0, w1=w1)
+    ip, ix, dat = orc.jit_materialize(spec, n_rows, n_cols)
+    for density in (0.01, 0.1, 0.5):
+        ev = inputs.spike_pattern(n_rows, density, 5)
+        for kind in (orc.OUT_F64, orc.OUT_FIX):
+            a = orc.event_csrmv(ip, ix, dat, 0.0, n_rows, n_cols, ev, kind)
+            b = orc.jit_event_mv(spec, n_rows, n_cols, ev, out_kind=kind)
+            if kind == orc.OUT_FIX:
+                assert np.array_equal(a, b)
+            else:
+                np.testing.assert_allclose(a, b, rtol=0, atol=1e-12)
+
+
+def test_partition_is_a_slice(orc):
+    n_rows, n_cols, L = 200, 640, 64
+    spec = _spec(orc, 0.05, seed=3, n_cols=n_cols, L=L, law="uniform",
+                 w0=-1.0, w1=1.0)
+    ev = inputs.spike_pattern(n_rows, 0.2, 8)
+    full = orc.jit_event_mv(spec, n_rows, n_cols, ev, out_kind=orc.OUT_FIX)
+    for cb, ce in [(0, 64), (64, 320), (320, 640), (128, 130), (600, 640)]:
+        part = orc.jit_event_mv(spec, n_rows, n_cols, ev, cb, ce,
+                                out_kind=orc.OUT_FIX)
+        assert np.array_equal(part, full[cb:ce])
+
+
+def test_connectivity_independent_of_events(orc):
+    """Union of single-spike probes == the full event pattern."""
+    n_rows, n_cols = 64, 300
+    spec = _spec(orc, 0.1, seed=1234, n_cols=n_cols, law="normal", w0=0.0, w1=1.0)
+    ev = inputs.spike_pattern(n_rows, 0.5, 2)
+    full = orc.jit_event_mv(spec, n_rows, n_cols, ev, out_kind=orc.OUT_FIX)
+    acc = np.zeros(n_cols, np.int64)
+    for r in np.nonzero(ev)[0]:
+        probe = np.zeros(n_rows, np.uint8)
+        probe[r] = 1
+        acc += orc.jit_event_mv(spec, n_rows, n_cols, probe, out_kind=orc.OUT_FIX)
+    assert np.array_equal(acc, full)
+
+
+def test_indices_identical_across_laws(orc):
+    n_cols = 1000
+    rows = {}
+    for law, w0, w1 in [("homo", 0.6, 0), ("uniform", -1, 1), ("normal", 0, 1)]:
+        spec = _spec(orc, 0.02, seed=5, n_cols=n_cols, L=250, law=law, w0=w0, w1=w1)
+        rows[law] = [orc.jit_row(spec, n_cols, r)[0] for r in range(100)]
+    for r in range(100):
+        assert np.array_equal(rows["homo"][r], rows["uniform"][r])
+        assert np.array_equal(rows["homo"][r], rows["normal"][r])
+
+
+def test_uniform_weight_moments(orc):
+    lo, hi = -0.1, 0.1   # Table S1 input scale s = 0.1
+    spec = _spec(orc, 0.5, seed=21, n_cols=2000, law="uniform", w0=lo, w1=hi)
+    w = np.concatenate([orc.jit_row(spec, 2000, r)[1] for r in range(200)])
+    assert w.size > 100_000
+    assert w.min() >= np.float32(lo) and w.max() < np.float32(hi)
+    mean, var = (lo + hi) / 2, (hi - lo) ** 2 / 12
+    n = w.size
+    assert abs(w.mean() - mean) < 4 * math.sqrt(var / n)
+    # var of the sample variance of U: (mu4 - var^2)/n with mu4 = (hi-lo)^4/80
+    mu4 = (hi - lo) ** 4 / 80
+    assert abs(w.var() - var) < 4 * math.sqrt((mu4 - var * var) / n)
+
+
+def test_normal_weight_moments(orc):
+    mu, sigma = 0.25, 2.0
+    spec = _spec(orc, 0.5, seed=22, n_cols=2000, law="normal", w0=mu, w1=sigma)
+    w = np.concatenate([orc.jit_row(spec, 2000, r)[1] for r in range(200)]).astype(np.float64)
+    n = w.size
+    assert n > 100_000
+    assert abs(w.mean() - mu) < 4 * sigma / math.sqrt(n)
+    assert abs(w.var() - sigma ** 2) < 4 * sigma ** 2 * math.sqrt(2.0 / n)
+    # tails: fraction beyond 2 sigma = 0.0455
+    frac = np.mean(np.abs(w - mu) > 2 * sigma)
+    assert abs(frac - 0.0455) < 4 * math.sqrt(0.0455 * 0.9545 / n)
+    z3 = np.mean(((w - mu) / sigma) ** 3)
+    assert abs(z3) < 4 * math.sqrt(15.0 / n)
+
+
+def test_empty_and_degenerate(orc):
+    spec = _spec(orc, 0.1, n_cols=10)
+    ev = np.zeros(5, np.uint8)
+    assert not orc.jit_event_mv(spec, 5, 10, ev, out_kind=orc.OUT_FIX).any()
+    # zero-width partition produces nothing
+    out = orc.jit_event_mv(spec, 5, 10, np.ones(5, np.uint8), 4, 4,
+                           out_kind=orc.OUT_FIX)
+    assert out.size == 0

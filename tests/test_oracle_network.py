@@ -1,0 +1,126 @@
+"""Pins for the oracle's network loop (rule S1, Listing S3 update()).
+
+* A w = 0 network is a set of unconnected LIF neurons: each raster row has a
+  closed form (first passage from V0, then period 189 steps).
+* Fixed-point g after T steps equals the fp64 recursion
+  g_n = alpha g_{n-1} + sum_{r in spikes_{n-1}} w D[r, c] recomputed in
+  numpy from the oracle's own raster and an independent densified matrix,
+  within the F1 rounding bound.
+* The JIT network equals the network over its materialised CSR.
+* Refractory contract and determinism.
+Firing *rates* of the coupled network are not printed in the paper
+(Fig 2C elided): parity for rates is unpinned (reading R23).
+"""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2311_05106_b200 import inputs
+
+
+def _coba(orc, n=4000, fixed=True, w_e=0.6, w_i=6.7, seed_e=0x5EED0001,
+          seed_i=0x5EED0002, conn="jit"):
+    n_exc = n * 4 // 5
+    K = orc.conn_len(80.0 / n)
+    pe = orc.Projection(0, n_exc, jit=orc.JitSpec(seed_e, K, n, orc.LAW_HOMO, w_e))
+    pi = orc.Projection(n_exc, n - n_exc, jit=orc.JitSpec(seed_i, K, n, orc.LAW_HOMO, w_i))
+    if conn == "csr":
+        ip, ix, _ = orc.jit_materialize(pe.jit, n_exc, n)
+        pe = orc.Projection(0, n_exc, csr=(ip, ix, None), w_homo=w_e)
+        ip, ix, _ = orc.jit_materialize(pi.jit, n - n_exc, n)
+        pi = orc.Projection(n_exc, n - n_exc, csr=(ip, ix, None), w_homo=w_i)
+    g_dtype = np.int64 if fixed else np.float32
+    state = dict(v=inputs.lif_v0(n), g_e=np.zeros(n, g_dtype),
+                 g_i=np.zeros(n, g_dtype), ref=np.zeros(n, np.uint8),
+                 spikes=np.zeros(n, np.uint8))
+    return state, pe, pi
+
+
+def test_zero_weight_network_closed_form(orc):
+    n = 800
+    state, pe, pi = _coba(orc, n=n, w_e=0.0, w_i=0.0)
+    v0 = state["v"].astype(np.float64).copy()
+    raster = orc.run_network("lif", orc.lif_params(), state, pe, pi, 700)
+    alpha = math.exp(-0.1 / 20.0)
+    checked = 0
+    for i in range(n):
+        # V_m = -40 + (V0 + 40) alpha^m; first m >= 1 with V_m > -50
+        ratio = 10.0 / (-40.0 - v0[i])
+        m_real = math.log(ratio) / math.log(alpha) if ratio < 1 else 0.0
+        if abs(m_real - round(m_real)) < 0.05:
+            continue          # fp32 rounding could move a near-integer crossing
+        m1 = max(1, math.floor(m_real) + 1)
+        want = list(range(m1 - 1, 700, 189))
+        got = np.nonzero(raster[:, i])[0].tolist()
+        assert got == want, i
+        checked += 1
+    assert checked > 700
+
+
+def test_fixed_point_g_equals_fp64_recursion(orc):
+    n, T = 4000, 300
+    state, pe, pi = _coba(orc, n=n)
+    raster = orc.run_network("lif", orc.lif_params(), state, pe, pi, T)
+    assert raster.sum() > 0
+    # independent dense matrices from the oracle's materialised rows
+    d_e = np.zeros((pe.n_rows, n))
+    for r in range(pe.n_rows):
+        d_e[r, orc.jit_row(pe.jit, n, r)[0]] = float(np.float32(0.6))
+    d_i = np.zeros((pi.n_rows, n))
+    for r in range(pi.n_rows):
+        d_i[r, orc.jit_row(pi.jit, n, r)[0]] = float(np.float32(6.7))
+    a_e, a_i = math.exp(-0.1 / 5.0), math.exp(-0.1 / 10.0)
+    g_e = np.zeros(n); g_i = np.zeros(n)
+    prev = np.zeros(n)
+    for step in range(T):
+        g_e = a_e * g_e + prev[:pe.n_rows] @ d_e      # decay, then add (R12)
+        g_i = a_i * g_i + prev[pe.n_rows:] @ d_i
+        prev = raster[step].astype(np.float64)
+    # the stored state is pre-decayed after the last update
+    g_e *= a_e
+    g_i *= a_i
+    got_e = state["g_e"] / 2.0 ** 32
+    got_i = state["g_i"] / 2.0 ** 32
+    # per step <= 1 unit of 2^-32 from llrint(decay) + 0.5/term: << 2^-20
+    assert np.max(np.abs(got_e - g_e)) < 2.0 ** -20 * max(1.0, g_e.max())
+    assert np.max(np.abs(got_i - g_i)) < 2.0 ** -20 * max(1.0, g_i.max())
+
+
+def test_jit_network_equals_materialised_csr_network(orc):
+    n, T = 2000, 200
+    s1, pe1, pi1 = _coba(orc, n=n)
+    s2, pe2, pi2 = _coba(orc, n=n, conn="csr")
+    r1 = orc.run_network("lif", orc.lif_params(), s1, pe1, pi1, T)
+    r2 = orc.run_network("lif", orc.lif_params(), s2, pe2, pi2, T)
+    assert np.array_equal(r1, r2)
+    assert np.array_equal(s1["v"].view(np.uint32), s2["v"].view(np.uint32))
+    assert np.array_equal(s1["g_e"], s2["g_e"])
+
+
+def test_refractory_contract_and_determinism(orc):
+    n, T = 4000, 400
+    s1, pe, pi = _coba(orc, n=n)
+    r1 = orc.run_network("lif", orc.lif_params(), s1, pe, pi, T)
+    s2, pe, pi = _coba(orc, n=n)
+    r2 = orc.run_network("lif", orc.lif_params(), s2, pe, pi, T)
+    assert np.array_equal(r1, r2)
+    for i in range(n):
+        t = np.nonzero(r1[:, i])[0]
+        assert np.all(np.diff(t) >= 51)
+
+
+@pytest.mark.parametrize("fixed", [True, False])
+def test_hh_network_runs_finite(orc, fixed):
+    n = 1000
+    n_exc = 800
+    K = orc.conn_len(80.0 / n)
+    pe = orc.Projection(0, n_exc, jit=orc.JitSpec(1, K, n, orc.LAW_HOMO, 6.0))
+    pi = orc.Projection(n_exc, n - n_exc, jit=orc.JitSpec(2, K, n, orc.LAW_HOMO, 67.0))
+    v, m, h, nk = inputs.hh_init(n)
+    g_dtype = np.int64 if fixed else np.float32
+    state = dict(v=v, m=m, h=h, n=nk, g_e=np.zeros(n, g_dtype),
+                 g_i=np.zeros(n, g_dtype), spikes=np.zeros(n, np.uint8))
+    raster = orc.run_network("hh", orc.hh_params(), state, pe, pi, 300)
+    assert np.all(np.isfinite(state["v"]))
+    assert raster.sum() > 0
