@@ -1,0 +1,369 @@
+"""bench.py -- synaptic events/s and simulated-s per wall-s of the COBA E/I
+network on 1/2/4/8 B200 (BASELINE.json metric, config 5 shape).
+
+Workload (default, `--workload coba_lif_jit`): Listing S3's COBA-LIF E/I
+network with JIT connectivity (event_mv_prob_homo), fan-in
+80 (p = 80/N), 12.5 M neurons per GPU (weak scaling: N = 12.5M x G),
+dt = 0.1 ms, fixed-point int64 conductances (rule F1).  One "step" = one
+0.1 ms timestep of the whole hot path: spike delivery (JIT regeneration +
+scatter), fused Expon + COBA + LIF update, spike compaction, and for G > 1
+the bit-packed spike all-gather.  State per GPU is 525 MB > 126 MB L2, so
+no L2 flush is needed between steps (inputs larger than L2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DT_MS = 0.1
+N_PER_GPU = 12_500_000
+METRIC = "synaptic events/sec & sim-sec per wall-sec, COBA E/I at 1/2/4/8 B200"
+UNIT = "synaptic events/s"
+# rule F1 state bytes per neuron per step for the LIF update (algorithmic):
+# V r+w (8) + g_E, g_I int64 r+w (32) + refractory counter r+w (2)
+LIF_BYTES_PER_NEURON = 42
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": mx or None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle leg (cpu_baseline and --impl reference): the oracle as it stands
+# ---------------------------------------------------------------------------
+
+def oracle_sample_steps(n_total: int, n_steps: int, fraction: float, seed: int = 7):
+    """Time the oracle on a bounded sample of the same workload: each step
+    delivers the spikes of `fraction` of the presynaptic rows (all of their
+    events, E and I projections, Bernoulli(22 Hz * dt) activity -- the
+    oracle network's measured rate) and updates `fraction` of the neurons.
+    Returns (seconds, events, neuron_updates)."""
+    import numpy as np
+
+    import oracle
+    from paper_2311_05106_b200 import inputs
+    from paper_2311_05106_b200.network import SEED_E, SEED_I
+    oracle.build()
+    n_exc = n_total * 4 // 5
+    K = oracle.conn_len(80.0 / n_total)
+    je = oracle.JitSpec(SEED_E, K, n_total, oracle.LAW_HOMO, 0.6)
+    ji = oracle.JitSpec(SEED_I, K, n_total, oracle.LAW_HOMO, 6.7)
+    n_rows_e = max(1, int(n_exc * fraction))
+    n_rows_i = max(1, int((n_total - n_exc) * fraction))
+    n_upd = max(32, int(n_total * fraction))
+    v = inputs.lif_v0(n_upd)
+    ref = np.zeros(n_upd, np.uint8)
+    g_e = np.zeros(n_total, np.int64)
+    g_i = np.zeros(n_total, np.int64)
+    params = oracle.lif_params()
+    density = 22.0 * DT_MS * 1e-3
+    patterns = [(inputs.spike_pattern(n_rows_e, density, seed + 2 * k),
+                 inputs.spike_pattern(n_rows_i, density, seed + 2 * k + 1))
+                for k in range(min(n_steps, 8))]
+    t0 = time.perf_counter()
+    for k in range(n_steps):
+        ev_e, ev_i = patterns[k % len(patterns)]
+        oracle.jit_event_mv(je, n_rows_e, n_total, ev_e, out_kind=oracle.OUT_FIX, out=g_e)
+        oracle.jit_event_mv(ji, n_rows_i, n_total, ev_i, out_kind=oracle.OUT_FIX, out=g_i)
+        oracle.lif_step(params, v, g_e[:n_upd], g_i[:n_upd], ref)
+    secs = time.perf_counter() - t0
+    # events delivered (outside the timed region): fan-out of every active row
+    events = 0
+    for k in range(n_steps):
+        ev_e, ev_i = patterns[k % len(patterns)]
+        for spec, ev in ((je, ev_e), (ji, ev_i)):
+            for r in np.nonzero(ev)[0]:
+                events += len(oracle.jit_row(spec, n_total, int(r))[0])
+    return secs, events, n_upd * n_steps
+
+
+def cpu_baseline(n_total: int, budget_s: float = 15.0):
+    fraction = 1.0 / 32
+    secs, events, _ = oracle_sample_steps(n_total, 2, fraction)   # calibrate
+    per_step = max(secs / 2, 1e-3)
+    steps = max(2, min(200, int(budget_s / per_step)))
+    secs, events, upd = oracle_sample_steps(n_total, steps, fraction)
+    return {"value": events / secs, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": (f"{steps} steps of the {n_total:,}-neuron network with 1/32 of "
+                       f"presynaptic rows active-eligible (Bernoulli 22 Hz x dt) and 1/32 "
+                       f"of neurons updated per step; {events:,} events in {secs:.1f} s, "
+                       f"single-threaded C oracle"),
+            "sim_s_per_wall_s_equiv": (steps * DT_MS * 1e-3 * fraction) / secs}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n_total = N_PER_GPU * args.gpus
+    fraction = 1.0 / 64
+    _, _, _ = oracle_sample_steps(n_total, max(1, args.warmup), fraction)
+    secs, events, upd = oracle_sample_steps(n_total, args.steps, fraction)
+    value = events / secs
+    sample = (f"each step: 1/64 of the presynaptic rows (Bernoulli 22 Hz x dt) of the "
+              f"{n_total:,}-neuron network delivered through the oracle's Listing S2 "
+              f"loop + 1/64 of the neurons updated (rule N1)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32+i64fix",
+            "data": "synthetic",
+            "config": {"workload": "coba_lif_jit", "n_per_gpu": N_PER_GPU,
+                       "n_total": n_total, "fan_in": 80, "dt_ms": DT_MS},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import __graft_entry__ as ge
+    ge.build_lib()
+    from paper_2311_05106_b200.network import CobaNetwork
+
+    world = args.gpus
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n_total = N_PER_GPU * world
+    fixed = not args.f32
+
+    net = CobaNetwork(n_total, conn="jit", fixed=fixed, rank=rank, world=world, device=dev)
+    n_local = net.part.col_end - net.part.col_begin
+    stream = torch.cuda.current_stream()
+
+    def steps(k):
+        if world == 1:
+            net.run(k)
+        else:
+            for _ in range(k):
+                net.step_distributed()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up (untimed)
+    steps(args.warmup)
+    barrier()
+    sp0, ev0 = net.counters()
+
+    # timed region: exactly K steps, CUDA events on the launching stream
+    if world == 1:
+        net.net.profile_begin(args.steps)
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        start.record(stream)
+        steps(args.steps)
+        stop.record(stream)
+        barrier()
+    ms = start.elapsed_time(stop)
+    sp1, ev1 = net.counters()
+    prof = net.net.profile_end() if world == 1 else None
+    events_local = ev1 - ev0
+    spikes_seen = sp1 - sp0
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        e = torch.tensor([events_local], dtype=torch.float64, device=dev)
+        dist.all_reduce(e, op=dist.ReduceOp.SUM)
+        events_total = float(e.item())
+    else:
+        events_total = float(events_local)
+    secs = ms / 1e3
+    value = events_total / secs
+    sim_ratio = args.steps * DT_MS * 1e-3 / secs
+
+    # end-to-end through the public API with host buffers: initial state H2D
+    # from pinned memory inside the timed region, every step's spike count
+    # D2H into pinned memory (the step's population-rate result).
+    e2e = None
+    if world == 1:
+        e2e = run_e2e(args, fixed, dev, net.state)
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peaks, peak_kind = _peaks()
+    roofline = None
+    if prof is not None:
+        sc_ms, up_ms, nrec = prof
+        upd_s = up_ms / 1e3 / max(nrec, 1)
+        bytes_per_launch = LIF_BYTES_PER_NEURON * n_local + n_local / 8
+        achieved = bytes_per_launch / upd_s / 1e9
+        roofline = {"kernel": "k_lif<fix64> (fused Expon+COBA+LIF update + spike compaction)",
+                    "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                    "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                    "traffic": None, "peak_source": peak_kind,
+                    "algorithmic_bytes_per_launch": bytes_per_launch,
+                    "avg_launch_us": upd_s * 1e6,
+                    "share_of_step": up_ms / (sc_ms + up_ms) if (sc_ms + up_ms) else None,
+                    "scatter_avg_us": sc_ms / 1e3 / max(nrec, 1) * 1e6}
+    cpu = cpu_baseline(n_total) if (world == 1 and not args.no_cpu) else None
+    clocks = clk.summary()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "i64fix+f32" if fixed else "f32", "data": "synthetic",
+        "config": {"workload": "coba_lif_jit", "n_per_gpu": N_PER_GPU, "n_total": n_total,
+                   "fan_in": 80, "p": 80.0 / n_total, "conn_len_K": net.net.desc.jit_exc.conn_len,
+                   "dt_ms": DT_MS, "g": "int64 fixed point 2^-32" if fixed else "fp32",
+                   "parallelism": f"postsynaptic partition x{world}",
+                   "l2": "state 525 MB/GPU > 126 MB L2: no flush needed",
+                   "spikes_delivered": spikes_seen, "events": events_total},
+        "sim_s_per_wall_s": sim_ratio,
+        "events_per_step": events_total / args.steps,
+        # libbp kernels in the timed region: scatter + update per step (world 1);
+        # compaction + scatter + update per step (world > 1; NCCL not counted)
+        "gpu_launches": (2 if world == 1 else 3) * args.steps,
+        "clocks": clocks,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(args, fixed, dev, template_state):
+    """Same metric through the public API with host buffers."""
+    import torch
+
+    from paper_2311_05106_b200 import inputs
+    from paper_2311_05106_b200.network import CobaNetwork
+    n = N_PER_GPU
+    net = CobaNetwork(n, conn="jit", fixed=fixed, device=dev)
+    host = {k: torch.empty_like(v, device="cpu").pin_memory() for k, v in net.state.items()}
+    host["v"].copy_(torch.from_numpy(inputs.lif_v0(n)))
+    for k in ("g_e", "g_i", "ref"):
+        host[k].zero_()
+    counts = torch.zeros(args.steps, dtype=torch.int32).pin_memory()
+    h2d = sum(t.numel() * t.element_size() for t in host.values())
+    stream = torch.cuda.current_stream()
+    net.run(args.warmup)
+    torch.cuda.synchronize()
+    sp0, ev0 = net.counters()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    start.record(stream)
+    for k, t in host.items():
+        net.state[k].copy_(t, non_blocking=True)
+    net.run(args.steps, counts=counts)
+    stop.record(stream)
+    stop.synchronize()
+    ms = start.elapsed_time(stop)
+    sp1, ev1 = net.counters()
+    return {"value": (ev1 - ev0) / (ms / 1e3), "unit": UNIT,
+            "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": 4,
+            "note": "initial state H2D (pinned) amortised over the K steps; per-step "
+                    "spike count D2H into pinned memory; ms=%.3f" % ms,
+            "spikes_total": int(counts.sum().item())}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10_000)
+    ap.add_argument("--warmup", type=int, default=200)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--f32", action="store_true", help="fp32 conductances (fp32 atomics)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,266 @@
+/*
+ * bp.h -- C ABI of the B200-native BrainPy hot path (libbp.so).
+ *
+ * The operations follow the paper's statement of the operators
+ * (arxiv 2311.05106, PAPER.md; "P:n" = line n):
+ *   bp_compact_spikes        -- spike vector -> active-row list; "computes only
+ *                               at positions where the spike in v is True"
+ *                               (App. B)                   [SURVEY 8(a) a1]
+ *   bp_event_csrmv           -- brainpy.math.event.csrmv, Listing S1
+ *                               (App. B)                         [a2]
+ *   bp_jitconn_event_mv_*    -- brainpy.math.jitconn.event_mv_prob_{homo,
+ *                               uniform,normal}, Listing S2 (App. C;
+ *                               P:192)                       [a3, a4]
+ *   bp_neuron_step           -- Expon + COBA + LIF
+ *                               or COBA-HH (rule H1, EXTERNAL)   [a5, a6]
+ *   bp_network_*             -- Listing S3's update() loop: 1-step
+ *                               delayed spikes -> scatter -> neuron update [a7]
+ * Rule names (J1..J9, F1, N1, H1, S1, R-numbered readings) refer to DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *  - Every pointer argument is a DEVICE pointer owned by the caller unless
+ *    stated otherwise; the library allocates no device memory per call.
+ *  - Every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy
+ *    default stream) and returns after enqueueing.  Arguments are validated
+ *    synchronously before any launch.
+ *  - Spike vectors are bit-packed: neuron r is bit (r & 31) of 32-bit word
+ *    r >> 5, little-endian bit order; bits past the vector length are ignored
+ *    on input and written 0 on output.
+ *  - CSR rows are PRESYNAPTIC (the event index) and columns POSTSYNAPTIC (the
+ *    output index): Listing S1 iterates `events` over rows and scatters into
+ *    `outs`.  indptr int64[n_rows+1], indices int32[nnz] sorted
+ *    within a row, data float32[nnz] or NULL for one homogeneous weight.
+ *  - Output accumulators (bp_out_kind): BP_OUT_F32 = float32 with fp32
+ *    atomics (summation order unspecified); BP_OUT_FIX64 = int64 fixed point
+ *    with 32 fractional bits, each weight quantised as llrint(w * 2^32)
+ *    (rule F1) -- bit-reproducible for any launch configuration.
+ *  - Unless BP_ACCUMULATE is set in `flags`, the output is zeroed first.
+ *  - Errors: a non-zero bp_status; bp_last_error() gives a thread-local
+ *    message.  Faults raised asynchronously by a kernel surface at the
+ *    caller's next synchronisation and are reported as BP_ERR_CUDA by the
+ *    next call.  The library never aborts the process.
+ *  - Only sm_100 devices are supported (BP_ERR_UNSUPPORTED otherwise).
+ */
+#ifndef BP_H_
+#define BP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void *bp_stream; /* cudaStream_t */
+
+typedef enum {
+  BP_OK = 0,
+  BP_ERR_INVALID_ARG = 1, /* null pointer, p outside (0,1], NaN, sigma < 0 ... */
+  BP_ERR_SHAPE = 2,       /* sizes <= 0 or >= 2^31, partition not aligned      */
+  BP_ERR_UNSUPPORTED = 3, /* not an sm_100 device, K too large for 32-bit pos  */
+  BP_ERR_WORKSPACE = 4,   /* workspace NULL, misaligned or too small           */
+  BP_ERR_CUDA = 5         /* a CUDA runtime error (launch or sticky)           */
+} bp_status;
+
+typedef enum { BP_OUT_F32 = 0, BP_OUT_FIX64 = 1 } bp_out_kind;
+
+#define BP_ACCUMULATE 1u
+
+typedef enum { BP_LAW_HOMO = 0, BP_LAW_UNIFORM = 1, BP_LAW_NORMAL = 2 } bp_law;
+typedef enum { BP_MODEL_LIF = 0, BP_MODEL_HH = 1 } bp_model;
+typedef enum { BP_CONN_JIT = 0, BP_CONN_CSR = 1 } bp_conn;
+
+int bp_abi_version(void); /* 1 */
+const char *bp_status_string(int status);
+const char *bp_last_error(void);
+
+/* Rule J1: K = floor(2/p - 1), snapped to the nearest integer when
+ * within 1e-9 relative of it, K >= 1.  Returns 0 when p is not in (0, 1].
+ * Host function. */
+uint32_t bp_conn_len(double prob);
+
+/* Bytes of caller-provided workspace the stateless scatter calls need for an
+ * input of n_rows presynaptic neurons (active-row list + counter).  Host. */
+size_t bp_workspace_bytes(int64_t n_rows);
+
+/* a1: active = { r < n : bit r of spikes set }, written to active[0..count)
+ * in unspecified order (a set); *count (device int32) receives its size.
+ * active must hold n entries. */
+bp_status bp_compact_spikes(const uint32_t *spikes, int64_t n, int32_t *active,
+                            int32_t *count, bp_stream stream);
+
+/* a2: event_csrmv, Listing S1 with indices[j] (the listing's indices[i] is a
+ * typo):  for r with bit r set, for k in [indptr[r], indptr[r+1]):
+ *     out[indices[k]] += (data ? data[k] : w_homo)
+ * out: n_cols float32 (BP_OUT_F32) or int64 (BP_OUT_FIX64), 16-byte aligned.
+ * ws: >= bp_workspace_bytes(n_rows) bytes, 256-byte aligned. */
+bp_status bp_event_csrmv(const int64_t *indptr, const int32_t *indices,
+                         const float *data, float w_homo, int64_t n_rows,
+                         int64_t n_cols, const uint32_t *spikes, void *out,
+                         int out_kind, uint32_t flags, void *ws,
+                         size_t ws_bytes, bp_stream stream);
+
+/* JIT connectivity (App. C; the "four scalars (p, mu, sigma, s)"
+ * of P:192).  The matrix is a pure function of (seed, K, seg_len, n_rows,
+ * n_cols): row r's targets in segment s = [s*L, min((s+1)L, n_cols)) are
+ * pos_0 = s*L + a(r,s) (stationary first offset, rule J5) and
+ * pos_{e+1} = pos_e + U[1,K](Philox word e), rules J2-J6.  No connectivity
+ * memory is used or stored. */
+typedef struct {
+  uint64_t seed;
+  double prob;       /* connection probability p in (0, 1]                  */
+  uint32_t conn_len; /* K; 0 => bp_conn_len(prob)                           */
+  uint32_t seg_len;  /* L; 0 => n_cols (one segment per row)                */
+} bp_jitconn;
+
+/* a3+a4: out[c - col_begin] += sum over active rows r of w_e(r) for every
+ * generated edge (r, c) with c in [col_begin, col_end).  col_begin must be a
+ * multiple of seg_len and col_end a multiple of seg_len or equal to n_cols
+ * (a postsynaptic partition).  Requires
+ * n_cols + 128 * K < 2^32 (32-bit positions), else BP_ERR_UNSUPPORTED.
+ *   homo    : w_e = weight                                  (Listing S2)
+ *   uniform : w_e ~ U[w_low, w_high)                         (rule J7)
+ *   normal  : w_e ~ N(w_mu, w_sigma^2), Box-Muller           (rule J7)
+ * out: (col_end - col_begin) float32 / int64; ws as for bp_event_csrmv. */
+bp_status bp_jitconn_event_mv_homo(const bp_jitconn *spec, float weight,
+                                   const uint32_t *spikes, int64_t n_rows,
+                                   int64_t n_cols, int64_t col_begin,
+                                   int64_t col_end, void *out, int out_kind,
+                                   uint32_t flags, void *ws, size_t ws_bytes,
+                                   bp_stream stream);
+bp_status bp_jitconn_event_mv_uniform(const bp_jitconn *spec, float w_low,
+                                      float w_high, const uint32_t *spikes,
+                                      int64_t n_rows, int64_t n_cols,
+                                      int64_t col_begin, int64_t col_end,
+                                      void *out, int out_kind, uint32_t flags,
+                                      void *ws, size_t ws_bytes,
+                                      bp_stream stream);
+bp_status bp_jitconn_event_mv_normal(const bp_jitconn *spec, float w_mu,
+                                     float w_sigma, const uint32_t *spikes,
+                                     int64_t n_rows, int64_t n_cols,
+                                     int64_t col_begin, int64_t col_end,
+                                     void *out, int out_kind, uint32_t flags,
+                                     void *ws, size_t ws_bytes,
+                                     bp_stream stream);
+
+/* Debug/inspection: materialise the implied matrix with the KERNEL's own
+ * generator.  row_counts: counts[r] = number of edges of row r (int64[n_rows]).
+ * materialize: given indptr (exclusive prefix sum of the counts, int64
+ * [n_rows+1]) write indices[indptr[r]..) ascending and data (nullable) with
+ * the weights of `law` (w0, w1) = (weight, -) | (w_low, w_high) | (mu, sigma). */
+bp_status bp_jitconn_row_counts(const bp_jitconn *spec, int64_t n_rows,
+                                int64_t n_cols, int64_t *counts,
+                                bp_stream stream);
+bp_status bp_jitconn_materialize(const bp_jitconn *spec, int law, float w0,
+                                 float w1, int64_t n_rows, int64_t n_cols,
+                                 const int64_t *indptr, int32_t *indices,
+                                 float *data, bp_stream stream);
+
+/* Neuron parameters.  LIF (rule N1, Listing S3): alpha_v =
+ * fl32(exp(-dt/tau)), alpha_e/alpha_i = exp(-dt/tau_syn) in fp64, ref_steps
+ * = tau_ref/dt.  HH (rule H1): Traub-Miles COBAHH constants (mV, ms, nS, pF).
+ * Both: E_exc/E_inh reversal potentials, i_ext constant input. */
+typedef struct {
+  int32_t model; /* bp_model */
+  int32_t ref_steps;
+  float v_rest, v_reset, v_th, r, i_ext, e_exc, e_inh, alpha_v;
+  double alpha_e, alpha_i;
+  /* HH only */
+  float c_m, g_l, e_l, g_na, e_na, g_k, e_k, v_t, dt, v_spike;
+} bp_neuron_params;
+
+/* State of n neurons (device arrays of n entries).  g_exc/g_inh are float32
+ * or int64 fixed point (g_kind); they hold alpha*g_{n-1} + increments on entry
+ * and are pre-decayed on exit (reading R12).  LIF uses v, ref; HH uses v, m,
+ * h, n_gate. */
+typedef struct {
+  float *v;
+  void *g_exc;
+  void *g_inh;
+  int32_t g_kind; /* bp_out_kind */
+  int32_t reserved;
+  uint8_t *ref;
+  float *m, *h, *n_gate;
+} bp_neuron_state;
+
+/* a5+a6: one step for neurons [0, n).  spikes_out: ceil(n/32) words (bit set
+ * = spike).  active_out (nullable, n entries) receives the spiking indices
+ * plus `active_base`, appended at *count_out (device int32, which the caller
+ * zeroes). */
+bp_status bp_neuron_step(const bp_neuron_params *params,
+                         const bp_neuron_state *state, int64_t n,
+                         uint32_t *spikes_out, int32_t *active_out,
+                         int32_t *count_out, int64_t active_base,
+                         bp_stream stream);
+
+/* ---------------------------------------------------------------------
+ * Network: Listing S3.  Neurons [0, n_exc) are excitatory
+ * (projection E, rows 0..n_exc-1), [n_exc, n) inhibitory (projection I,
+ * rows 0..n-n_exc-1); both project onto all n neurons.  This
+ * process owns postsynaptic neurons [col_begin, col_end);
+ * col_begin must be a multiple of 32 and of both seg_lens.
+ * Per step (rule S1): scatter(spikes_{n-1}) into g, neuron update ->
+ * spikes_n.  With several processes the caller all-gathers the bit-packed
+ * spike vector between bp_network_update and the next bp_network_scatter.
+ * --------------------------------------------------------------------- */
+typedef struct {
+  int32_t model;  /* bp_model */
+  int32_t conn;   /* bp_conn  */
+  int32_t g_kind; /* bp_out_kind of state.g_exc / g_inh */
+  int32_t reserved;
+  int64_t n, n_exc;
+  int64_t col_begin, col_end;
+  bp_jitconn jit_exc, jit_inh; /* conn == BP_CONN_JIT                       */
+  float w_exc, w_inh;          /* homogeneous weights (both conn kinds)     */
+  /* conn == BP_CONN_CSR: column-sliced CSR of each projection, indices local
+   * to [col_begin, col_end); data NULL => homogeneous w_exc / w_inh.       */
+  const int64_t *exc_indptr;
+  const int32_t *exc_indices;
+  const float *exc_data;
+  const int64_t *inh_indptr;
+  const int32_t *inh_indices;
+  const float *inh_data;
+  bp_neuron_params params;
+  bp_neuron_state state; /* local neurons, col_end - col_begin entries     */
+  uint32_t *spikes;      /* global bit vector, >= ceil(n/32) words; holds
+                            spikes_{n-1} on entry to a step               */
+  void *ws;              /* >= bp_network_workspace_bytes(desc), 256-aligned */
+  size_t ws_bytes;
+} bp_network_desc;
+
+typedef struct bp_network bp_network; /* opaque; not thread-safe */
+
+size_t bp_network_workspace_bytes(const bp_network_desc *desc);
+/* Copies *desc (all buffers stay owned by the caller), initialises the
+ * workspace on `stream` from desc->spikes. */
+bp_status bp_network_create(const bp_network_desc *desc, bp_stream stream,
+                            bp_network **out);
+/* n_steps full steps on one device (no exchange).  raster_out (nullable,
+ * device): n_steps x ceil((col_end-col_begin)/32) words of local spikes.
+ * counts_out (nullable; device or page-locked host memory): n_steps int32,
+ * the number of local spikes emitted in each step (copied asynchronously). */
+bp_status bp_network_step(bp_network *net, int64_t n_steps,
+                          uint32_t *raster_out, int32_t *counts_out,
+                          bp_stream stream);
+/* The two halves of a step for multi-process runs. */
+bp_status bp_network_scatter(bp_network *net, bp_stream stream);
+bp_status bp_network_update(bp_network *net, uint32_t *raster_row,
+                            bp_stream stream);
+/* Device counters since create: [0] = local spikes, [1] = synaptic events
+ * delivered into local neurons.  Copies into host uint64[2]; synchronises
+ * `stream`. */
+bp_status bp_network_counters(bp_network *net, uint64_t *host_out,
+                              bp_stream stream);
+/* Per-kernel timing of the next bp_network_step calls (at most max_steps
+ * steps): CUDA events are recorded on `stream` around every scatter and
+ * neuron-update launch.  _end synchronises and returns the summed device
+ * milliseconds of each kernel kind and the number of steps recorded. */
+bp_status bp_network_profile_begin(bp_network *net, int64_t max_steps);
+bp_status bp_network_profile_end(bp_network *net, double *scatter_ms,
+                                 double *update_ms, int64_t *steps);
+void bp_network_destroy(bp_network *net);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BP_H_ */

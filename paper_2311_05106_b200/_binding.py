@@ -1,0 +1,383 @@
+"""ctypes binding of libbp.so (include/bp.h) -- argument marshalling only.
+
+Every function takes torch tensors that live on the current CUDA device and
+passes their data pointers, sizes and the current stream to the C ABI; all
+computation happens in the library's sm_100a kernels.  There is no CPU
+fallback: if libbp.so is missing or the device is not sm_100, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbp.so")
+
+OUT_F32, OUT_FIX64 = 0, 1
+ACCUMULATE = 1
+LAW_HOMO, LAW_UNIFORM, LAW_NORMAL = 0, 1, 2
+MODEL_LIF, MODEL_HH = 0, 1
+CONN_JIT, CONN_CSR = 0, 1
+
+EXPORTED = [
+    "bp_abi_version", "bp_status_string", "bp_last_error", "bp_conn_len",
+    "bp_workspace_bytes", "bp_compact_spikes", "bp_event_csrmv",
+    "bp_jitconn_event_mv_homo", "bp_jitconn_event_mv_uniform",
+    "bp_jitconn_event_mv_normal", "bp_jitconn_row_counts",
+    "bp_jitconn_materialize", "bp_neuron_step", "bp_network_workspace_bytes",
+    "bp_network_create", "bp_network_step", "bp_network_scatter",
+    "bp_network_update", "bp_network_counters", "bp_network_profile_begin",
+    "bp_network_profile_end", "bp_network_destroy",
+]
+
+
+class BpError(RuntimeError):
+    pass
+
+
+class JitConn(ctypes.Structure):
+    _fields_ = [("seed", ctypes.c_uint64), ("prob", ctypes.c_double),
+                ("conn_len", ctypes.c_uint32), ("seg_len", ctypes.c_uint32)]
+
+
+_F = ctypes.c_float
+
+
+class NeuronParams(ctypes.Structure):
+    _fields_ = ([("model", ctypes.c_int32), ("ref_steps", ctypes.c_int32)] +
+                [(n, _F) for n in ("v_rest", "v_reset", "v_th", "r", "i_ext",
+                                   "e_exc", "e_inh", "alpha_v")] +
+                [("alpha_e", ctypes.c_double), ("alpha_i", ctypes.c_double)] +
+                [(n, _F) for n in ("c_m", "g_l", "e_l", "g_na", "e_na", "g_k",
+                                   "e_k", "v_t", "dt", "v_spike")])
+
+
+class NeuronState(ctypes.Structure):
+    _fields_ = [("v", ctypes.c_void_p), ("g_exc", ctypes.c_void_p),
+                ("g_inh", ctypes.c_void_p), ("g_kind", ctypes.c_int32),
+                ("reserved", ctypes.c_int32), ("ref", ctypes.c_void_p),
+                ("m", ctypes.c_void_p), ("h", ctypes.c_void_p),
+                ("n_gate", ctypes.c_void_p)]
+
+
+class NetworkDesc(ctypes.Structure):
+    _fields_ = [("model", ctypes.c_int32), ("conn", ctypes.c_int32),
+                ("g_kind", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("n", ctypes.c_int64), ("n_exc", ctypes.c_int64),
+                ("col_begin", ctypes.c_int64), ("col_end", ctypes.c_int64),
+                ("jit_exc", JitConn), ("jit_inh", JitConn),
+                ("w_exc", _F), ("w_inh", _F),
+                ("exc_indptr", ctypes.c_void_p), ("exc_indices", ctypes.c_void_p),
+                ("exc_data", ctypes.c_void_p), ("inh_indptr", ctypes.c_void_p),
+                ("inh_indices", ctypes.c_void_p), ("inh_data", ctypes.c_void_p),
+                ("params", NeuronParams), ("state", NeuronState),
+                ("spikes", ctypes.c_void_p), ("ws", ctypes.c_void_p),
+                ("ws_bytes", ctypes.c_size_t)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libbp.so; raise loudly if it was not built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise BpError(f"{LIB_PATH} not built: run __graft_entry__.build()")
+        L = ctypes.CDLL(LIB_PATH)
+        P, i64, u32, f32, i32 = (ctypes.c_void_p, ctypes.c_int64,
+                                 ctypes.c_uint32, ctypes.c_float, ctypes.c_int)
+        sz = ctypes.c_size_t
+        L.bp_status_string.restype = ctypes.c_char_p
+        L.bp_last_error.restype = ctypes.c_char_p
+        L.bp_conn_len.argtypes = [ctypes.c_double]
+        L.bp_conn_len.restype = u32
+        L.bp_workspace_bytes.argtypes = [i64]
+        L.bp_workspace_bytes.restype = sz
+        L.bp_compact_spikes.argtypes = [P, i64, P, P, P]
+        L.bp_event_csrmv.argtypes = [P, P, P, f32, i64, i64, P, P, i32, u32, P, sz, P]
+        jit_tail = [P, i64, i64, i64, i64, P, i32, u32, P, sz, P]
+        L.bp_jitconn_event_mv_homo.argtypes = [ctypes.POINTER(JitConn), f32] + jit_tail
+        L.bp_jitconn_event_mv_uniform.argtypes = [ctypes.POINTER(JitConn), f32, f32] + jit_tail
+        L.bp_jitconn_event_mv_normal.argtypes = [ctypes.POINTER(JitConn), f32, f32] + jit_tail
+        L.bp_jitconn_row_counts.argtypes = [ctypes.POINTER(JitConn), i64, i64, P, P]
+        L.bp_jitconn_materialize.argtypes = [ctypes.POINTER(JitConn), i32, f32, f32,
+                                             i64, i64, P, P, P, P]
+        L.bp_neuron_step.argtypes = [ctypes.POINTER(NeuronParams),
+                                     ctypes.POINTER(NeuronState), i64, P, P, P, i64, P]
+        L.bp_network_workspace_bytes.argtypes = [ctypes.POINTER(NetworkDesc)]
+        L.bp_network_workspace_bytes.restype = sz
+        L.bp_network_create.argtypes = [ctypes.POINTER(NetworkDesc), P,
+                                        ctypes.POINTER(ctypes.c_void_p)]
+        L.bp_network_step.argtypes = [P, i64, P, P, P]
+        L.bp_network_profile_begin.argtypes = [P, i64]
+        L.bp_network_profile_end.argtypes = [P, P, P, P]
+        L.bp_network_scatter.argtypes = [P, P]
+        L.bp_network_update.argtypes = [P, P, P]
+        L.bp_network_counters.argtypes = [P, P, P]
+        L.bp_network_destroy.argtypes = [P]
+        L.bp_network_destroy.restype = None
+        for name in EXPORTED:
+            if name not in ("bp_network_destroy", "bp_status_string",
+                            "bp_last_error", "bp_conn_len", "bp_workspace_bytes",
+                            "bp_network_workspace_bytes", "bp_abi_version"):
+                getattr(L, name).restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        L = lib()
+        raise BpError(f"{L.bp_status_string(status).decode()}: "
+                      f"{L.bp_last_error().decode()}")
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _out_kind(out: torch.Tensor) -> int:
+    if out.dtype == torch.float32:
+        return OUT_F32
+    if out.dtype == torch.int64:
+        return OUT_FIX64
+    raise BpError(f"output dtype {out.dtype}: float32 or int64 (fixed point)")
+
+
+def _cuda(*ts):
+    for t in ts:
+        if t is not None and (not t.is_cuda or not t.is_contiguous()):
+            raise BpError("inputs must be contiguous CUDA tensors")
+
+
+# ------------------------------------------------------------------ helpers
+
+def conn_len(prob: float) -> int:
+    return int(lib().bp_conn_len(float(prob)))
+
+
+def workspace_bytes(n_rows: int) -> int:
+    return int(lib().bp_workspace_bytes(int(n_rows)))
+
+
+def workspace(n_rows: int, device=None) -> torch.Tensor:
+    return torch.empty(workspace_bytes(n_rows), dtype=torch.uint8,
+                       device=device or torch.cuda.current_device())
+
+
+def jitconn_spec(seed: int, prob: float, conn_len: int = 0, seg_len: int = 0) -> JitConn:
+    return JitConn(int(seed) & (2 ** 64 - 1), float(prob), int(conn_len), int(seg_len))
+
+
+# ------------------------------------------------------------- operators
+
+def compact_spikes(spikes: torch.Tensor, n: int, active: torch.Tensor,
+                   count: torch.Tensor, stream=None):
+    _cuda(spikes, active, count)
+    _check(lib().bp_compact_spikes(_ptr(spikes), int(n), _ptr(active),
+                                   _ptr(count), _stream(stream)))
+
+
+def event_csrmv(indptr, indices, data, w_homo, n_rows, n_cols, spikes, out,
+                accumulate=False, ws=None, stream=None):
+    """brainpy.math.event.csrmv (Listing S1) -> out[n_cols] (f32 or fix64)."""
+    _cuda(indptr, indices, data, spikes, out)
+    ws = ws if ws is not None else workspace(n_rows, out.device)
+    _check(lib().bp_event_csrmv(
+        _ptr(indptr), _ptr(indices), _ptr(data), float(w_homo), int(n_rows),
+        int(n_cols), _ptr(spikes), _ptr(out), _out_kind(out),
+        ACCUMULATE if accumulate else 0, _ptr(ws), ws.numel(), _stream(stream)))
+    return out
+
+
+def jitconn_event_mv(law: int, spec: JitConn, w0: float, w1: float, spikes,
+                     n_rows, n_cols, out, col_begin=0, col_end=None,
+                     accumulate=False, ws=None, stream=None):
+    """brainpy.math.jitconn.event_mv_prob_{homo,uniform,normal} (Listing S2)."""
+    _cuda(spikes, out)
+    col_end = n_cols if col_end is None else col_end
+    ws = ws if ws is not None else workspace(n_rows, out.device)
+    flags = ACCUMULATE if accumulate else 0
+    tail = (_ptr(spikes), int(n_rows), int(n_cols), int(col_begin), int(col_end),
+            _ptr(out), _out_kind(out), flags, _ptr(ws), ws.numel(), _stream(stream))
+    L = lib()
+    if law == LAW_HOMO:
+        st = L.bp_jitconn_event_mv_homo(ctypes.byref(spec), float(w0), *tail)
+    elif law == LAW_UNIFORM:
+        st = L.bp_jitconn_event_mv_uniform(ctypes.byref(spec), float(w0), float(w1), *tail)
+    elif law == LAW_NORMAL:
+        st = L.bp_jitconn_event_mv_normal(ctypes.byref(spec), float(w0), float(w1), *tail)
+    else:
+        raise BpError(f"unknown law {law}")
+    _check(st)
+    return out
+
+
+def jitconn_event_mv_homo(spec, weight, spikes, n_rows, n_cols, out, **kw):
+    return jitconn_event_mv(LAW_HOMO, spec, weight, 0.0, spikes, n_rows, n_cols, out, **kw)
+
+
+def jitconn_event_mv_uniform(spec, w_low, w_high, spikes, n_rows, n_cols, out, **kw):
+    return jitconn_event_mv(LAW_UNIFORM, spec, w_low, w_high, spikes, n_rows, n_cols, out, **kw)
+
+
+def jitconn_event_mv_normal(spec, w_mu, w_sigma, spikes, n_rows, n_cols, out, **kw):
+    return jitconn_event_mv(LAW_NORMAL, spec, w_mu, w_sigma, spikes, n_rows, n_cols, out, **kw)
+
+
+def jitconn_materialize(spec: JitConn, n_rows: int, n_cols: int, law=LAW_HOMO,
+                        w0=1.0, w1=0.0, with_data=True, device=None, stream=None):
+    """CSR of the implied matrix, generated by the kernels' own generator."""
+    device = device or torch.cuda.current_device()
+    counts = torch.empty(n_rows, dtype=torch.int64, device=device)
+    _check(lib().bp_jitconn_row_counts(ctypes.byref(spec), int(n_rows), int(n_cols),
+                                       _ptr(counts), _stream(stream)))
+    indptr = torch.zeros(n_rows + 1, dtype=torch.int64, device=device)
+    torch.cumsum(counts, 0, out=indptr[1:])
+    nnz = int(indptr[-1].item())
+    indices = torch.empty(max(nnz, 1), dtype=torch.int32, device=device)
+    data = torch.empty(max(nnz, 1), dtype=torch.float32, device=device) if with_data else None
+    _check(lib().bp_jitconn_materialize(ctypes.byref(spec), int(law), float(w0),
+                                        float(w1), int(n_rows), int(n_cols),
+                                        _ptr(indptr), _ptr(indices), _ptr(data),
+                                        _stream(stream)))
+    return indptr, indices[:nnz], (data[:nnz] if data is not None else None)
+
+
+# ------------------------------------------------------------- neurons
+
+def lif_params(dt=0.1, tau=20.0, tau_e=5.0, tau_i=10.0, v_rest=-60.0,
+               v_reset=-60.0, v_th=-50.0, r=1.0, i_ext=20.0, e_exc=0.0,
+               e_inh=-80.0, tau_ref=5.0) -> NeuronParams:
+    """LifRef + Expon + COBA of Listing S3, I_ext = 20."""
+    p = NeuronParams()
+    p.model = MODEL_LIF
+    p.ref_steps = int(round(tau_ref / dt))
+    p.v_rest, p.v_reset, p.v_th, p.r = v_rest, v_reset, v_th, r
+    p.i_ext, p.e_exc, p.e_inh = i_ext, e_exc, e_inh
+    p.alpha_v = float(ctypes.c_float(math.exp(-dt / tau)).value)
+    p.alpha_e, p.alpha_i = math.exp(-dt / tau_e), math.exp(-dt / tau_i)
+    return p
+
+
+def hh_params(dt=0.1, tau_e=5.0, tau_i=10.0, i_ext=0.0) -> NeuronParams:
+    """COBA-HH (Brette et al. 2007 benchmark 3; rule H1, EXTERNAL)."""
+    p = NeuronParams()
+    p.model = MODEL_HH
+    p.c_m, p.g_l, p.e_l = 200.0, 10.0, -60.0
+    p.g_na, p.e_na, p.g_k, p.e_k, p.v_t = 20000.0, 50.0, 6000.0, -90.0, -63.0
+    p.e_exc, p.e_inh, p.i_ext, p.dt, p.v_spike = 0.0, -80.0, i_ext, dt, -20.0
+    p.alpha_e, p.alpha_i = math.exp(-dt / tau_e), math.exp(-dt / tau_i)
+    return p
+
+
+def _state_struct(state: dict) -> NeuronState:
+    g = state["g_e"]
+    s = NeuronState()
+    s.v = state["v"].data_ptr()
+    s.g_exc = g.data_ptr()
+    s.g_inh = state["g_i"].data_ptr()
+    s.g_kind = _out_kind(g)
+    for k, f in (("ref", "ref"), ("m", "m"), ("h", "h"), ("n", "n_gate")):
+        if state.get(k) is not None:
+            setattr(s, f, state[k].data_ptr())
+    return s
+
+
+def neuron_step(params: NeuronParams, state: dict, spikes_out: torch.Tensor,
+                active=None, count=None, active_base=0, stream=None):
+    """One fused Expon + COBA + LIF/HH step of all neurons in `state`."""
+    n = state["v"].numel()
+    _check(lib().bp_neuron_step(ctypes.byref(params), ctypes.byref(_state_struct(state)),
+                                n, _ptr(spikes_out), _ptr(active), _ptr(count),
+                                int(active_base), _stream(stream)))
+
+
+class Network:
+    """Handle over bp_network_* (Listing S3's update loop, rule S1).
+
+    Keeps references to every tensor whose pointer it passed to the library.
+    """
+
+    def __init__(self, *, model, conn, n, n_exc, state: dict, spikes, params,
+                 col_begin=0, col_end=None, jit_exc=None, jit_inh=None,
+                 w_exc=0.6, w_inh=6.7, csr_exc=None, csr_inh=None, stream=None):
+        col_end = n if col_end is None else col_end
+        d = NetworkDesc()
+        d.model, d.conn = model, conn
+        d.g_kind = _out_kind(state["g_e"])
+        d.n, d.n_exc, d.col_begin, d.col_end = n, n_exc, col_begin, col_end
+        if jit_exc is not None:
+            d.jit_exc = jit_exc
+        if jit_inh is not None:
+            d.jit_inh = jit_inh
+        d.w_exc, d.w_inh = w_exc, w_inh
+        self._keep = [state, spikes, csr_exc, csr_inh]
+        for side, csr in (("exc", csr_exc), ("inh", csr_inh)):
+            if csr is not None:
+                ip, ix, dat = csr
+                setattr(d, f"{side}_indptr", ip.data_ptr())
+                setattr(d, f"{side}_indices", ix.data_ptr())
+                if dat is not None:
+                    setattr(d, f"{side}_data", dat.data_ptr())
+        d.params = params
+        d.state = _state_struct(state)
+        d.spikes = spikes.data_ptr()
+        nbytes = int(lib().bp_network_workspace_bytes(ctypes.byref(d)))
+        self.ws = torch.zeros(nbytes, dtype=torch.uint8, device=spikes.device)
+        d.ws, d.ws_bytes = self.ws.data_ptr(), nbytes
+        self.desc = d
+        self.state, self.spikes = state, spikes
+        self.n_local = col_end - col_begin
+        self.local_words = (self.n_local + 31) // 32
+        handle = ctypes.c_void_p()
+        _check(lib().bp_network_create(ctypes.byref(d), _stream(stream),
+                                       ctypes.byref(handle)))
+        self._h = handle
+
+    def step(self, n_steps: int, raster=None, counts=None, stream=None):
+        """counts: device tensor or pinned host tensor of n_steps int32."""
+        _check(lib().bp_network_step(self._h, int(n_steps), _ptr(raster), _ptr(counts),
+                                     _stream(stream)))
+
+    def profile_begin(self, max_steps: int):
+        _check(lib().bp_network_profile_begin(self._h, int(max_steps)))
+
+    def profile_end(self):
+        """-> (scatter_ms_total, update_ms_total, steps) over the recorded steps."""
+        sc, up, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+        _check(lib().bp_network_profile_end(self._h, ctypes.byref(sc), ctypes.byref(up),
+                                            ctypes.byref(n)))
+        return sc.value, up.value, n.value
+
+    def scatter(self, stream=None):
+        _check(lib().bp_network_scatter(self._h, _stream(stream)))
+
+    def update(self, raster_row=None, stream=None):
+        _check(lib().bp_network_update(self._h, _ptr(raster_row), _stream(stream)))
+
+    def counters(self, stream=None):
+        out = (ctypes.c_uint64 * 2)()
+        _check(lib().bp_network_counters(self._h, ctypes.cast(out, ctypes.c_void_p),
+                                         _stream(stream)))
+        return int(out[0]), int(out[1])
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().bp_network_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,779 @@
+// bp_api.cu -- host side of libbp.so: argument validation, launch geometry
+// and the per-step orchestration of the network (include/bp.h).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <new>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/bp.h"
+#include "neuron.cuh"
+#include "scatter.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+bp_status fail(bp_status s, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+bp_status fail(bp_status s, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return s;
+}
+
+#define BP_CHECK(cond, status, ...) \
+  do {                              \
+    if (!(cond)) return fail(status, __VA_ARGS__); \
+  } while (0)
+
+#define BP_CUDA(call)                                                       \
+  do {                                                                      \
+    cudaError_t e_ = (call);                                                \
+    if (e_ != cudaSuccess)                                                  \
+      return fail(BP_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_));    \
+  } while (0)
+
+struct DeviceInfo {
+  int checked = 0;
+  int ok = 0;
+  int sms = 148;
+};
+DeviceInfo g_dev[64];
+
+// Sticky-error check + sm_100 check, cached per device.
+bp_status device_ready(int *sms) {
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess)
+    return fail(BP_ERR_CUDA, "pending CUDA error: %s", cudaGetErrorString(e));
+  int dev = 0;
+  BP_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail(BP_ERR_UNSUPPORTED, "device id %d", dev);
+  DeviceInfo &d = g_dev[dev];
+  if (!d.checked) {
+    int major = 0, minor = 0;
+    BP_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
+    BP_CUDA(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
+    BP_CUDA(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev));
+    d.ok = (major == 10 && minor == 0);
+    d.checked = 1;
+  }
+  if (!d.ok) return fail(BP_ERR_UNSUPPORTED, "libbp is built for sm_100a only");
+  if (sms) *sms = d.sms;
+  return BP_OK;
+}
+
+bp_status launched() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    return fail(BP_ERR_CUDA, "launch failed: %s", cudaGetErrorString(e));
+  return BP_OK;
+}
+
+inline cudaStream_t as_stream(bp_stream s) { return static_cast<cudaStream_t>(s); }
+inline bool aligned(const void *p, size_t a) {
+  return (reinterpret_cast<uintptr_t>(p) % a) == 0;
+}
+constexpr int64_t kMaxDim = (int64_t{1} << 31) - 1;
+
+size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Workspace of the stateless scatter calls: [count int32 | pad to 256]
+// [active int32[n_rows]].
+struct Ws {
+  int32_t *count;
+  int32_t *active;
+};
+bp_status carve_ws(void *ws, size_t ws_bytes, int64_t n_rows, Ws *out) {
+  BP_CHECK(ws != nullptr, BP_ERR_WORKSPACE, "workspace is NULL");
+  BP_CHECK(aligned(ws, 256), BP_ERR_WORKSPACE, "workspace must be 256-byte aligned");
+  BP_CHECK(ws_bytes >= bp_workspace_bytes(n_rows), BP_ERR_WORKSPACE,
+           "workspace %zu bytes < %zu required", ws_bytes, bp_workspace_bytes(n_rows));
+  out->count = static_cast<int32_t *>(ws);
+  out->active = reinterpret_cast<int32_t *>(static_cast<char *>(ws) + 256);
+  return BP_OK;
+}
+
+int grid_for_items(int64_t items_upper, int sms) {
+  // one warp per item; at most 8 resident 256-thread blocks per SM
+  const int64_t warps_per_block = bp::kScatterThreads / 32;
+  int64_t blocks = (items_upper + warps_per_block - 1) / warps_per_block;
+  const int64_t cap = static_cast<int64_t>(sms) * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  return static_cast<int>(blocks);
+}
+
+int grid_for_words(int64_t n_words, int sms) {
+  int64_t blocks = (n_words + 255) / 256;
+  const int64_t cap = static_cast<int64_t>(sms) * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  return static_cast<int>(blocks);
+}
+
+void launch_compact(const uint32_t *spikes, int64_t n, int32_t *active,
+                    int32_t *count, int sms, cudaStream_t st) {
+  const int64_t words = (n + 31) / 32;
+  bp::k_compact<<<grid_for_words(words, sms), 256, 0, st>>>(spikes, n, active,
+                                                            count, 0);
+}
+
+// ------------------------------------------------------------- JIT helpers
+struct JitResolved {
+  uint32_t K, L;
+};
+
+bp_status resolve_jit(const bp_jitconn *spec, int64_t n_cols, JitResolved *r) {
+  BP_CHECK(spec != nullptr, BP_ERR_INVALID_ARG, "jitconn spec is NULL");
+  uint32_t K = spec->conn_len;
+  if (K == 0) {
+    BP_CHECK(spec->prob > 0.0 && spec->prob <= 1.0, BP_ERR_INVALID_ARG,
+             "prob %g not in (0, 1]", spec->prob);
+    K = bp_conn_len(spec->prob);
+  }
+  BP_CHECK(K >= 1 && K < (1u << 31), BP_ERR_INVALID_ARG, "conn_len %u invalid", K);
+  const uint64_t reach = static_cast<uint64_t>(n_cols) + 128ull * K;
+  BP_CHECK(reach < (1ull << 32), BP_ERR_UNSUPPORTED,
+           "n_cols + 128*K = %llu exceeds 32-bit positions",
+           static_cast<unsigned long long>(reach));
+  uint32_t L = spec->seg_len ? spec->seg_len : static_cast<uint32_t>(n_cols);
+  BP_CHECK(L >= 1, BP_ERR_INVALID_ARG, "seg_len 0 with n_cols 0");
+  r->K = K;
+  r->L = L;
+  return BP_OK;
+}
+
+bp::JitSide jit_side(const bp_jitconn *spec, const JitResolved &jr, int law,
+                     float w0, float w1, int64_t col_begin, int64_t col_end,
+                     void *out) {
+  bp::JitSide s{};
+  s.seed = spec->seed;
+  s.K = jr.K;
+  s.L = jr.L;
+  s.seg_first = static_cast<uint32_t>(col_begin / jr.L);
+  const int64_t seg_last = col_end > col_begin ? (col_end - 1) / jr.L : -1;
+  s.n_seg = col_end > col_begin ? static_cast<uint32_t>(seg_last - s.seg_first + 1) : 0u;
+  s.w0 = w0;
+  s.w1 = (law == BP_LAW_UNIFORM) ? (w1 - w0) : w1;   // uniform: fp32 span
+  s.q = llrint(static_cast<double>(w0) * 4294967296.0);
+  s.out = out;
+  return s;
+}
+
+template <int LAW>
+void launch_jit_law(const bp::JitScatterArgs &a, int kind, int grid,
+                    cudaStream_t st) {
+  if (kind == BP_OUT_FIX64)
+    bp::k_jit_scatter<LAW, 1><<<grid, bp::kScatterThreads, 0, st>>>(a);
+  else
+    bp::k_jit_scatter<LAW, 0><<<grid, bp::kScatterThreads, 0, st>>>(a);
+}
+
+void launch_jit(const bp::JitScatterArgs &a, int law, int kind, int grid,
+                cudaStream_t st) {
+  if (law == BP_LAW_HOMO) launch_jit_law<0>(a, kind, grid, st);
+  else if (law == BP_LAW_UNIFORM) launch_jit_law<1>(a, kind, grid, st);
+  else launch_jit_law<2>(a, kind, grid, st);
+}
+
+void launch_csr(const bp::CsrScatterArgs &a, int kind, int grid, cudaStream_t st) {
+  if (kind == BP_OUT_FIX64)
+    bp::k_csr_scatter<1><<<grid, bp::kScatterThreads, 0, st>>>(a);
+  else
+    bp::k_csr_scatter<0><<<grid, bp::kScatterThreads, 0, st>>>(a);
+}
+
+bp_status check_out(void *out, int out_kind) {
+  BP_CHECK(out != nullptr, BP_ERR_INVALID_ARG, "out is NULL");
+  BP_CHECK(out_kind == BP_OUT_F32 || out_kind == BP_OUT_FIX64, BP_ERR_INVALID_ARG,
+           "out_kind %d", out_kind);
+  BP_CHECK(aligned(out, out_kind == BP_OUT_FIX64 ? 8 : 4), BP_ERR_INVALID_ARG,
+           "out misaligned");
+  return BP_OK;
+}
+
+bp_status jit_event_mv(int law, const bp_jitconn *spec, float w0, float w1,
+                       const uint32_t *spikes, int64_t n_rows, int64_t n_cols,
+                       int64_t col_begin, int64_t col_end, void *out,
+                       int out_kind, uint32_t flags, void *ws, size_t ws_bytes,
+                       bp_stream stream) {
+  int sms = 0;
+  bp_status s = device_ready(&sms);
+  if (s != BP_OK) return s;
+  BP_CHECK(n_rows >= 0 && n_rows <= kMaxDim && n_cols >= 1 && n_cols <= kMaxDim,
+           BP_ERR_SHAPE, "n_rows=%lld n_cols=%lld", (long long)n_rows, (long long)n_cols);
+  BP_CHECK(col_begin >= 0 && col_begin <= col_end && col_end <= n_cols, BP_ERR_SHAPE,
+           "partition [%lld, %lld) outside [0, %lld)", (long long)col_begin,
+           (long long)col_end, (long long)n_cols);
+  BP_CHECK(n_rows == 0 || spikes != nullptr, BP_ERR_INVALID_ARG, "spikes is NULL");
+  if (col_end > col_begin) {
+    s = check_out(out, out_kind);
+    if (s != BP_OK) return s;
+  }
+  BP_CHECK(!std::isnan(w0) && !std::isnan(w1), BP_ERR_INVALID_ARG, "NaN weight parameter");
+  if (law == BP_LAW_UNIFORM)
+    BP_CHECK(w0 <= w1, BP_ERR_INVALID_ARG, "w_low %g > w_high %g", w0, w1);
+  if (law == BP_LAW_NORMAL)
+    BP_CHECK(w1 >= 0.0f, BP_ERR_INVALID_ARG, "w_sigma %g < 0", w1);
+  JitResolved jr;
+  s = resolve_jit(spec, n_cols, &jr);
+  if (s != BP_OK) return s;
+  BP_CHECK(col_begin % jr.L == 0 && (col_end % jr.L == 0 || col_end == n_cols),
+           BP_ERR_SHAPE, "partition [%lld, %lld) not aligned to seg_len %u",
+           (long long)col_begin, (long long)col_end, jr.L);
+  Ws w;
+  s = carve_ws(ws, ws_bytes, n_rows, &w);
+  if (s != BP_OK) return s;
+  cudaStream_t st = as_stream(stream);
+  const size_t elt = out_kind == BP_OUT_FIX64 ? 8 : 4;
+  if (!(flags & BP_ACCUMULATE) && col_end > col_begin)
+    BP_CUDA(cudaMemsetAsync(out, 0, elt * (col_end - col_begin), st));
+  if (n_rows == 0 || col_end == col_begin) return launched();
+  BP_CUDA(cudaMemsetAsync(w.count, 0, sizeof(int32_t), st));
+  launch_compact(spikes, n_rows, w.active, w.count, sms, st);
+  bp::JitScatterArgs a{};
+  a.e = jit_side(spec, jr, law, w0, w1, col_begin, col_end, out);
+  a.i = a.e;
+  a.split = n_rows;
+  a.n_seg_max = a.e.n_seg;
+  a.n_cols = static_cast<uint32_t>(n_cols);
+  a.col_begin = static_cast<uint32_t>(col_begin);
+  a.col_end = static_cast<uint32_t>(col_end);
+  a.active = w.active;
+  a.count = w.count;
+  launch_jit(a, law, out_kind, grid_for_items(n_rows * a.n_seg_max, sms), st);
+  return launched();
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+int bp_abi_version(void) { return 1; }
+
+const char *bp_status_string(int status) {
+  switch (status) {
+    case BP_OK: return "BP_OK";
+    case BP_ERR_INVALID_ARG: return "BP_ERR_INVALID_ARG";
+    case BP_ERR_SHAPE: return "BP_ERR_SHAPE";
+    case BP_ERR_UNSUPPORTED: return "BP_ERR_UNSUPPORTED";
+    case BP_ERR_WORKSPACE: return "BP_ERR_WORKSPACE";
+    case BP_ERR_CUDA: return "BP_ERR_CUDA";
+    default: return "BP_ERR_UNKNOWN";
+  }
+}
+
+const char *bp_last_error(void) { return g_last_error.c_str(); }
+
+uint32_t bp_conn_len(double prob) {
+  // Rule J1: floor(2/p - 1), snapped to the nearest integer within
+  // 1e-9 relative, at least 1; 0 for p outside (0, 1].
+  if (!(prob > 0.0) || !(prob <= 1.0)) return 0;
+  const double x = 2.0 / prob - 1.0;
+  const double nearest = std::nearbyint(x);
+  const double tol = 1e-9 * (std::fabs(x) > 1.0 ? std::fabs(x) : 1.0);
+  double k = std::fabs(x - nearest) <= tol ? nearest : std::floor(x);
+  if (k < 1.0) k = 1.0;
+  if (k > 2147483647.0) return 0;
+  return static_cast<uint32_t>(k);
+}
+
+size_t bp_workspace_bytes(int64_t n_rows) {
+  if (n_rows < 0) n_rows = 0;
+  return 256 + round_up(static_cast<size_t>(n_rows) * sizeof(int32_t), 256);
+}
+
+bp_status bp_compact_spikes(const uint32_t *spikes, int64_t n, int32_t *active,
+                            int32_t *count, bp_stream stream) {
+  int sms = 0;
+  bp_status s = device_ready(&sms);
+  if (s != BP_OK) return s;
+  BP_CHECK(n >= 0 && n <= kMaxDim, BP_ERR_SHAPE, "n=%lld", (long long)n);
+  BP_CHECK(count != nullptr && (n == 0 || (spikes && active)), BP_ERR_INVALID_ARG,
+           "NULL pointer");
+  cudaStream_t st = as_stream(stream);
+  BP_CUDA(cudaMemsetAsync(count, 0, sizeof(int32_t), st));
+  if (n > 0) launch_compact(spikes, n, active, count, sms, st);
+  return launched();
+}
+
+bp_status bp_event_csrmv(const int64_t *indptr, const int32_t *indices,
+                         const float *data, float w_homo, int64_t n_rows,
+                         int64_t n_cols, const uint32_t *spikes, void *out,
+                         int out_kind, uint32_t flags, void *ws,
+                         size_t ws_bytes, bp_stream stream) {
+  int sms = 0;
+  bp_status s = device_ready(&sms);
+  if (s != BP_OK) return s;
+  BP_CHECK(n_rows >= 0 && n_rows <= kMaxDim && n_cols >= 1 && n_cols <= kMaxDim,
+           BP_ERR_SHAPE, "n_rows=%lld n_cols=%lld", (long long)n_rows, (long long)n_cols);
+  BP_CHECK(n_rows == 0 || (indptr && indices && spikes), BP_ERR_INVALID_ARG,
+           "NULL indptr/indices/spikes");
+  s = check_out(out, out_kind);
+  if (s != BP_OK) return s;
+  Ws w;
+  s = carve_ws(ws, ws_bytes, n_rows, &w);
+  if (s != BP_OK) return s;
+  cudaStream_t st = as_stream(stream);
+  const size_t elt = out_kind == BP_OUT_FIX64 ? 8 : 4;
+  if (!(flags & BP_ACCUMULATE)) BP_CUDA(cudaMemsetAsync(out, 0, elt * n_cols, st));
+  if (n_rows == 0) return launched();
+  BP_CUDA(cudaMemsetAsync(w.count, 0, sizeof(int32_t), st));
+  launch_compact(spikes, n_rows, w.active, w.count, sms, st);
+  bp::CsrScatterArgs a{};
+  a.e.indptr = indptr;
+  a.e.indices = indices;
+  a.e.data = data;
+  a.e.w = w_homo;
+  a.e.q = llrint(static_cast<double>(w_homo) * 4294967296.0);
+  a.e.out = out;
+  a.i = a.e;
+  a.split = n_rows;
+  a.active = w.active;
+  a.count = w.count;
+  launch_csr(a, out_kind, grid_for_items(n_rows, sms), st);
+  return launched();
+}
+
+bp_status bp_jitconn_event_mv_homo(const bp_jitconn *spec, float weight,
+                                   const uint32_t *spikes, int64_t n_rows,
+                                   int64_t n_cols, int64_t col_begin,
+                                   int64_t col_end, void *out, int out_kind,
+                                   uint32_t flags, void *ws, size_t ws_bytes,
+                                   bp_stream stream) {
+  return jit_event_mv(BP_LAW_HOMO, spec, weight, 0.0f, spikes, n_rows, n_cols,
+                      col_begin, col_end, out, out_kind, flags, ws, ws_bytes,
+                      stream);
+}
+
+bp_status bp_jitconn_event_mv_uniform(const bp_jitconn *spec, float w_low,
+                                      float w_high, const uint32_t *spikes,
+                                      int64_t n_rows, int64_t n_cols,
+                                      int64_t col_begin, int64_t col_end,
+                                      void *out, int out_kind, uint32_t flags,
+                                      void *ws, size_t ws_bytes,
+                                      bp_stream stream) {
+  return jit_event_mv(BP_LAW_UNIFORM, spec, w_low, w_high, spikes, n_rows,
+                      n_cols, col_begin, col_end, out, out_kind, flags, ws,
+                      ws_bytes, stream);
+}
+
+bp_status bp_jitconn_event_mv_normal(const bp_jitconn *spec, float w_mu,
+                                     float w_sigma, const uint32_t *spikes,
+                                     int64_t n_rows, int64_t n_cols,
+                                     int64_t col_begin, int64_t col_end,
+                                     void *out, int out_kind, uint32_t flags,
+                                     void *ws, size_t ws_bytes,
+                                     bp_stream stream) {
+  return jit_event_mv(BP_LAW_NORMAL, spec, w_mu, w_sigma, spikes, n_rows,
+                      n_cols, col_begin, col_end, out, out_kind, flags, ws,
+                      ws_bytes, stream);
+}
+
+bp_status bp_jitconn_row_counts(const bp_jitconn *spec, int64_t n_rows,
+                                int64_t n_cols, int64_t *counts,
+                                bp_stream stream) {
+  int sms = 0;
+  bp_status s = device_ready(&sms);
+  if (s != BP_OK) return s;
+  BP_CHECK(n_rows >= 0 && n_rows <= kMaxDim && n_cols >= 1 && n_cols <= kMaxDim,
+           BP_ERR_SHAPE, "bad shape");
+  BP_CHECK(n_rows == 0 || counts, BP_ERR_INVALID_ARG, "counts is NULL");
+  JitResolved jr;
+  s = resolve_jit(spec, n_cols, &jr);
+  if (s != BP_OK) return s;
+  if (n_rows == 0) return BP_OK;
+  bp::JitSide side = jit_side(spec, jr, BP_LAW_HOMO, 0.f, 0.f, 0, n_cols, nullptr);
+  bp::k_jit_rows<<<grid_for_items(n_rows, sms), bp::kScatterThreads, 0,
+                   as_stream(stream)>>>(side, n_rows, static_cast<uint32_t>(n_cols),
+                                        BP_LAW_HOMO, nullptr, counts, nullptr, nullptr);
+  return launched();
+}
+
+bp_status bp_jitconn_materialize(const bp_jitconn *spec, int law, float w0,
+                                 float w1, int64_t n_rows, int64_t n_cols,
+                                 const int64_t *indptr, int32_t *indices,
+                                 float *data, bp_stream stream) {
+  int sms = 0;
+  bp_status s = device_ready(&sms);
+  if (s != BP_OK) return s;
+  BP_CHECK(n_rows >= 0 && n_rows <= kMaxDim && n_cols >= 1 && n_cols <= kMaxDim,
+           BP_ERR_SHAPE, "bad shape");
+  BP_CHECK(law >= 0 && law <= 2, BP_ERR_INVALID_ARG, "law %d", law);
+  BP_CHECK(n_rows == 0 || (indptr && indices), BP_ERR_INVALID_ARG, "NULL indptr/indices");
+  JitResolved jr;
+  s = resolve_jit(spec, n_cols, &jr);
+  if (s != BP_OK) return s;
+  if (n_rows == 0) return BP_OK;
+  bp::JitSide side = jit_side(spec, jr, law, w0, w1, 0, n_cols, nullptr);
+  bp::k_jit_rows<<<grid_for_items(n_rows, sms), bp::kScatterThreads, 0,
+                   as_stream(stream)>>>(side, n_rows, static_cast<uint32_t>(n_cols),
+                                        law, indptr, nullptr, indices, data);
+  return launched();
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ neuron step
+namespace {
+
+bp_status fill_neuron_args(const bp_neuron_params *p, const bp_neuron_state *st,
+                           int64_t n, bp::NeuronArgs *a) {
+  BP_CHECK(p != nullptr && st != nullptr, BP_ERR_INVALID_ARG, "NULL params/state");
+  BP_CHECK(p->model == BP_MODEL_LIF || p->model == BP_MODEL_HH, BP_ERR_INVALID_ARG,
+           "model %d", p->model);
+  BP_CHECK(st->g_kind == BP_OUT_F32 || st->g_kind == BP_OUT_FIX64, BP_ERR_INVALID_ARG,
+           "g_kind %d", st->g_kind);
+  BP_CHECK(n >= 0 && n <= kMaxDim, BP_ERR_SHAPE, "n=%lld", (long long)n);
+  if (n > 0) {
+    BP_CHECK(st->v && st->g_exc && st->g_inh, BP_ERR_INVALID_ARG, "NULL v/g");
+    if (p->model == BP_MODEL_LIF)
+      BP_CHECK(st->ref != nullptr, BP_ERR_INVALID_ARG, "NULL ref");
+    else
+      BP_CHECK(st->m && st->h && st->n_gate, BP_ERR_INVALID_ARG, "NULL m/h/n");
+    BP_CHECK(aligned(st->g_exc, st->g_kind == BP_OUT_FIX64 ? 8 : 4) &&
+                 aligned(st->g_inh, st->g_kind == BP_OUT_FIX64 ? 8 : 4),
+             BP_ERR_INVALID_ARG, "g misaligned");
+  }
+  BP_CHECK(p->ref_steps >= 0 && p->ref_steps <= 255, BP_ERR_INVALID_ARG,
+           "ref_steps %d not in [0, 255]", p->ref_steps);
+  *a = bp::NeuronArgs{};
+  a->v_rest = p->v_rest; a->v_reset = p->v_reset; a->v_th = p->v_th; a->r = p->r;
+  a->i_ext = p->i_ext; a->e_exc = p->e_exc; a->e_inh = p->e_inh; a->alpha_v = p->alpha_v;
+  a->alpha_e = p->alpha_e; a->alpha_i = p->alpha_i;
+  a->alpha_e32 = static_cast<float>(p->alpha_e);
+  a->alpha_i32 = static_cast<float>(p->alpha_i);
+  a->ref_steps = p->ref_steps;
+  a->c_m = p->c_m; a->g_l = p->g_l; a->e_l = p->e_l; a->g_na = p->g_na; a->e_na = p->e_na;
+  a->g_k = p->g_k; a->e_k = p->e_k; a->v_t = p->v_t; a->dt = p->dt; a->v_spike = p->v_spike;
+  a->v = st->v; a->g_e = st->g_exc; a->g_i = st->g_inh; a->ref = st->ref;
+  a->m = st->m; a->h = st->h; a->nk = st->n_gate;
+  a->n = n;
+  return BP_OK;
+}
+
+void launch_neuron(const bp::NeuronArgs &a, int model, int g_kind, cudaStream_t st) {
+  if (a.n == 0) return;
+  const int blocks = static_cast<int>((a.n + 255) / 256);
+  if (model == BP_MODEL_LIF) {
+    if (g_kind == BP_OUT_FIX64) bp::k_lif<1><<<blocks, 256, 0, st>>>(a);
+    else bp::k_lif<0><<<blocks, 256, 0, st>>>(a);
+  } else {
+    if (g_kind == BP_OUT_FIX64) bp::k_hh<1><<<blocks, 256, 0, st>>>(a);
+    else bp::k_hh<0><<<blocks, 256, 0, st>>>(a);
+  }
+}
+
+}  // namespace
+
+extern "C" bp_status bp_neuron_step(const bp_neuron_params *params,
+                                    const bp_neuron_state *state, int64_t n,
+                                    uint32_t *spikes_out, int32_t *active_out,
+                                    int32_t *count_out, int64_t active_base,
+                                    bp_stream stream) {
+  bp_status s = device_ready(nullptr);
+  if (s != BP_OK) return s;
+  bp::NeuronArgs a;
+  s = fill_neuron_args(params, state, n, &a);
+  if (s != BP_OK) return s;
+  BP_CHECK(n == 0 || spikes_out != nullptr, BP_ERR_INVALID_ARG, "spikes_out is NULL");
+  BP_CHECK(active_out == nullptr || count_out != nullptr, BP_ERR_INVALID_ARG,
+           "active_out without count_out");
+  BP_CHECK(active_base >= 0 && active_base + n <= kMaxDim, BP_ERR_SHAPE, "active_base");
+  a.spikes = spikes_out;
+  a.active = active_out;
+  a.count = count_out;
+  a.active_base = static_cast<int32_t>(active_base);
+  launch_neuron(a, params->model, state->g_kind, as_stream(stream));
+  return launched();
+}
+
+// ================================================================ network
+struct bp_network {
+  bp_network_desc d;
+  int sms;
+  int64_t n_local, local_words, global_words;
+  JitResolved jr_e, jr_i;
+  unsigned long long *counters;   // [0] spikes delivered, [1] events
+  int32_t *count;                 // [2] ping-pong active counts
+  int32_t *active[2];             // ping-pong active lists (n entries each)
+  int parity;                     // list holding spikes_{n-1}
+  bp::NeuronArgs neuron;
+  // profiling: 3 events per step (before scatter, between, after update)
+  cudaEvent_t *prof_ev = nullptr;
+  int64_t prof_cap = 0, prof_used = 0;
+};
+
+namespace {
+
+size_t network_ws_layout(const bp_network_desc *d, size_t *off_active0,
+                         size_t *off_active1) {
+  const size_t list = round_up(static_cast<size_t>(d->n) * sizeof(int32_t), 256);
+  *off_active0 = 256;
+  *off_active1 = 256 + list;
+  return 256 + 2 * list;
+}
+
+bp_status validate_network(const bp_network_desc *d) {
+  BP_CHECK(d != nullptr, BP_ERR_INVALID_ARG, "desc is NULL");
+  BP_CHECK(d->n >= 1 && d->n <= kMaxDim && d->n_exc >= 0 && d->n_exc <= d->n,
+           BP_ERR_SHAPE, "n=%lld n_exc=%lld", (long long)d->n, (long long)d->n_exc);
+  BP_CHECK(d->col_begin >= 0 && d->col_begin < d->col_end && d->col_end <= d->n,
+           BP_ERR_SHAPE, "partition [%lld, %lld)", (long long)d->col_begin,
+           (long long)d->col_end);
+  BP_CHECK(d->col_begin % 32 == 0, BP_ERR_SHAPE, "col_begin not a multiple of 32");
+  BP_CHECK(d->col_end % 32 == 0 || d->col_end == d->n, BP_ERR_SHAPE,
+           "col_end must be a multiple of 32 or n");
+  BP_CHECK(d->conn == BP_CONN_JIT || d->conn == BP_CONN_CSR, BP_ERR_INVALID_ARG,
+           "conn %d", d->conn);
+  BP_CHECK(d->spikes != nullptr && aligned(d->spikes, 4), BP_ERR_INVALID_ARG,
+           "spikes NULL/misaligned");
+  BP_CHECK(d->params.model == d->model, BP_ERR_INVALID_ARG, "params.model != model");
+  BP_CHECK(d->state.g_kind == d->g_kind, BP_ERR_INVALID_ARG, "state.g_kind != g_kind");
+  if (d->conn == BP_CONN_CSR) {
+    BP_CHECK(d->n_exc == 0 || (d->exc_indptr && d->exc_indices), BP_ERR_INVALID_ARG,
+             "NULL excitatory CSR");
+    BP_CHECK(d->n_exc == d->n || (d->inh_indptr && d->inh_indices), BP_ERR_INVALID_ARG,
+             "NULL inhibitory CSR");
+  }
+  BP_CHECK(d->ws != nullptr && aligned(d->ws, 256), BP_ERR_WORKSPACE,
+           "workspace NULL or not 256-byte aligned");
+  BP_CHECK(d->ws_bytes >= bp_network_workspace_bytes(d), BP_ERR_WORKSPACE,
+           "workspace too small");
+  return BP_OK;
+}
+
+bp_status network_scatter_launch(bp_network *net, const int32_t *active,
+                                 const int32_t *count, int32_t *zero_count,
+                                 cudaStream_t st) {
+  const bp_network_desc &d = net->d;
+  const int grid_cap_items = static_cast<int>(d.n);
+  if (d.conn == BP_CONN_JIT) {
+    bp::JitScatterArgs a{};
+    a.e = jit_side(&d.jit_exc, net->jr_e, BP_LAW_HOMO, d.w_exc, 0.f, d.col_begin,
+                   d.col_end, d.state.g_exc);
+    a.i = jit_side(&d.jit_inh, net->jr_i, BP_LAW_HOMO, d.w_inh, 0.f, d.col_begin,
+                   d.col_end, d.state.g_inh);
+    a.split = d.n_exc;
+    a.n_seg_max = a.e.n_seg > a.i.n_seg ? a.e.n_seg : a.i.n_seg;
+    a.n_cols = static_cast<uint32_t>(d.n);
+    a.col_begin = static_cast<uint32_t>(d.col_begin);
+    a.col_end = static_cast<uint32_t>(d.col_end);
+    a.active = active;
+    a.count = count;
+    a.zero_count = zero_count;
+    a.events = net->counters + 1;
+    a.spikes = net->counters;
+    launch_jit(a, BP_LAW_HOMO, d.g_kind,
+               grid_for_items(static_cast<int64_t>(grid_cap_items) * a.n_seg_max, net->sms), st);
+  } else {
+    bp::CsrScatterArgs a{};
+    a.e.indptr = d.exc_indptr; a.e.indices = d.exc_indices; a.e.data = d.exc_data;
+    a.e.w = d.w_exc; a.e.q = llrint(static_cast<double>(d.w_exc) * 4294967296.0);
+    a.e.out = d.state.g_exc;
+    a.i.indptr = d.inh_indptr; a.i.indices = d.inh_indices; a.i.data = d.inh_data;
+    a.i.w = d.w_inh; a.i.q = llrint(static_cast<double>(d.w_inh) * 4294967296.0);
+    a.i.out = d.state.g_inh;
+    a.split = d.n_exc;
+    a.active = active;
+    a.count = count;
+    a.zero_count = zero_count;
+    a.events = net->counters + 1;
+    a.spikes = net->counters;
+    launch_csr(a, d.g_kind, grid_for_items(grid_cap_items, net->sms), st);
+  }
+  return launched();
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t bp_network_workspace_bytes(const bp_network_desc *desc) {
+  if (desc == nullptr || desc->n < 0) return 0;
+  size_t a0, a1;
+  return network_ws_layout(desc, &a0, &a1);
+}
+
+bp_status bp_network_create(const bp_network_desc *desc, bp_stream stream,
+                            bp_network **out) {
+  int sms = 0;
+  bp_status s = device_ready(&sms);
+  if (s != BP_OK) return s;
+  BP_CHECK(out != nullptr, BP_ERR_INVALID_ARG, "out is NULL");
+  s = validate_network(desc);
+  if (s != BP_OK) return s;
+  bp_network *net = new (std::nothrow) bp_network();
+  BP_CHECK(net != nullptr, BP_ERR_INVALID_ARG, "out of host memory");
+  net->d = *desc;
+  net->sms = sms;
+  net->n_local = desc->col_end - desc->col_begin;
+  net->local_words = (net->n_local + 31) / 32;
+  net->global_words = (desc->n + 31) / 32;
+  if (desc->conn == BP_CONN_JIT) {
+    s = resolve_jit(&desc->jit_exc, desc->n, &net->jr_e);
+    if (s == BP_OK) s = resolve_jit(&desc->jit_inh, desc->n, &net->jr_i);
+    if (s == BP_OK &&
+        (desc->col_begin % net->jr_e.L || desc->col_begin % net->jr_i.L ||
+         (desc->col_end != desc->n &&
+          (desc->col_end % net->jr_e.L || desc->col_end % net->jr_i.L))))
+      s = fail(BP_ERR_SHAPE, "partition not aligned to seg_len");
+    if (s != BP_OK) {
+      delete net;
+      return s;
+    }
+  }
+  s = fill_neuron_args(&desc->params, &desc->state, net->n_local, &net->neuron);
+  if (s != BP_OK) {
+    delete net;
+    return s;
+  }
+  size_t a0, a1;
+  network_ws_layout(desc, &a0, &a1);
+  char *ws = static_cast<char *>(desc->ws);
+  net->counters = reinterpret_cast<unsigned long long *>(ws);
+  net->count = reinterpret_cast<int32_t *>(ws + 64);
+  net->active[0] = reinterpret_cast<int32_t *>(ws + a0);
+  net->active[1] = reinterpret_cast<int32_t *>(ws + a1);
+  net->parity = 0;
+  cudaStream_t st = as_stream(stream);
+  cudaError_t e = cudaMemsetAsync(ws, 0, 256, st);
+  if (e == cudaSuccess) {
+    launch_compact(desc->spikes, desc->n, net->active[0], net->count, sms, st);
+    e = cudaGetLastError();
+  }
+  if (e != cudaSuccess) {
+    delete net;
+    return fail(BP_ERR_CUDA, "network init: %s", cudaGetErrorString(e));
+  }
+  net->neuron.spikes = desc->spikes + desc->col_begin / 32;
+  net->neuron.active_base = static_cast<int32_t>(desc->col_begin);
+  *out = net;
+  return BP_OK;
+}
+
+bp_status bp_network_step(bp_network *net, int64_t n_steps, uint32_t *raster_out,
+                          int32_t *counts_out, bp_stream stream) {
+  bp_status s = device_ready(nullptr);
+  if (s != BP_OK) return s;
+  BP_CHECK(net != nullptr && n_steps >= 0, BP_ERR_INVALID_ARG, "bad net/n_steps");
+  cudaStream_t st = as_stream(stream);
+  for (int64_t k = 0; k < n_steps; ++k) {
+    const int cur = net->parity, nxt = cur ^ 1;
+    cudaEvent_t *ev = nullptr;
+    if (net->prof_ev && net->prof_used < net->prof_cap)
+      ev = net->prof_ev + 3 * net->prof_used++;
+    if (ev) BP_CUDA(cudaEventRecord(ev[0], st));
+    s = network_scatter_launch(net, net->active[cur], net->count + cur,
+                               net->count + nxt, st);
+    if (s != BP_OK) return s;
+    if (ev) BP_CUDA(cudaEventRecord(ev[1], st));
+    bp::NeuronArgs a = net->neuron;
+    a.active = net->active[nxt];
+    a.count = net->count + nxt;
+    a.raster = raster_out ? raster_out + k * net->local_words : nullptr;
+    launch_neuron(a, net->d.model, net->d.g_kind, st);
+    s = launched();
+    if (s != BP_OK) return s;
+    if (ev) BP_CUDA(cudaEventRecord(ev[2], st));
+    if (counts_out)
+      BP_CUDA(cudaMemcpyAsync(counts_out + k, net->count + nxt, sizeof(int32_t),
+                              cudaMemcpyDefault, st));
+    net->parity = nxt;
+  }
+  return BP_OK;
+}
+
+bp_status bp_network_profile_begin(bp_network *net, int64_t max_steps) {
+  BP_CHECK(net != nullptr && max_steps >= 0, BP_ERR_INVALID_ARG, "bad arguments");
+  BP_CHECK(net->prof_ev == nullptr, BP_ERR_INVALID_ARG, "profiling already active");
+  net->prof_ev = new (std::nothrow) cudaEvent_t[3 * max_steps + 1];
+  BP_CHECK(net->prof_ev != nullptr, BP_ERR_INVALID_ARG, "out of host memory");
+  for (int64_t i = 0; i < 3 * max_steps; ++i)
+    BP_CUDA(cudaEventCreate(&net->prof_ev[i]));
+  net->prof_cap = max_steps;
+  net->prof_used = 0;
+  return BP_OK;
+}
+
+bp_status bp_network_profile_end(bp_network *net, double *scatter_ms,
+                                 double *update_ms, int64_t *steps) {
+  BP_CHECK(net != nullptr && net->prof_ev != nullptr, BP_ERR_INVALID_ARG,
+           "profiling not active");
+  double sc = 0.0, up = 0.0;
+  bp_status s = BP_OK;
+  for (int64_t k = 0; k < net->prof_used && s == BP_OK; ++k) {
+    cudaEvent_t *ev = net->prof_ev + 3 * k;
+    float a = 0.f, b = 0.f;
+    cudaError_t e = cudaEventSynchronize(ev[2]);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&a, ev[0], ev[1]);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&b, ev[1], ev[2]);
+    if (e != cudaSuccess) s = fail(BP_ERR_CUDA, "profile: %s", cudaGetErrorString(e));
+    sc += a;
+    up += b;
+  }
+  for (int64_t i = 0; i < 3 * net->prof_cap; ++i) cudaEventDestroy(net->prof_ev[i]);
+  delete[] net->prof_ev;
+  net->prof_ev = nullptr;
+  if (scatter_ms) *scatter_ms = sc;
+  if (update_ms) *update_ms = up;
+  if (steps) *steps = net->prof_used;
+  net->prof_cap = net->prof_used = 0;
+  return s;
+}
+
+bp_status bp_network_scatter(bp_network *net, bp_stream stream) {
+  bp_status s = device_ready(nullptr);
+  if (s != BP_OK) return s;
+  BP_CHECK(net != nullptr, BP_ERR_INVALID_ARG, "net is NULL");
+  cudaStream_t st = as_stream(stream);
+  // The spike vector may have been rewritten by an exchange: rebuild the
+  // active list of spikes_{n-1} from the global bit vector.
+  const int cur = net->parity;
+  BP_CUDA(cudaMemsetAsync(net->count + cur, 0, sizeof(int32_t), st));
+  launch_compact(net->d.spikes, net->d.n, net->active[cur], net->count + cur,
+                 net->sms, st);
+  s = launched();
+  if (s != BP_OK) return s;
+  return network_scatter_launch(net, net->active[cur], net->count + cur, nullptr, st);
+}
+
+bp_status bp_network_update(bp_network *net, uint32_t *raster_row, bp_stream stream) {
+  bp_status s = device_ready(nullptr);
+  if (s != BP_OK) return s;
+  BP_CHECK(net != nullptr, BP_ERR_INVALID_ARG, "net is NULL");
+  bp::NeuronArgs a = net->neuron;
+  a.active = nullptr;
+  a.raster = raster_row;
+  launch_neuron(a, net->d.model, net->d.g_kind, as_stream(stream));
+  return launched();
+}
+
+bp_status bp_network_counters(bp_network *net, uint64_t *host_out, bp_stream stream) {
+  bp_status s = device_ready(nullptr);
+  if (s != BP_OK) return s;
+  BP_CHECK(net != nullptr && host_out != nullptr, BP_ERR_INVALID_ARG, "NULL argument");
+  cudaStream_t st = as_stream(stream);
+  BP_CUDA(cudaMemcpyAsync(host_out, net->counters, 2 * sizeof(uint64_t),
+                          cudaMemcpyDeviceToHost, st));
+  BP_CUDA(cudaStreamSynchronize(st));
+  return BP_OK;
+}
+
+void bp_network_destroy(bp_network *net) {
+  if (net && net->prof_ev) {
+    for (int64_t i = 0; i < 3 * net->prof_cap; ++i) cudaEventDestroy(net->prof_ev[i]);
+    delete[] net->prof_ev;
+  }
+  delete net;
+}
+
+}  // extern "C"

@@ -1,0 +1,95 @@
+// rng.cuh -- counter-based randomness of the JIT connectivity (DESIGN.md
+// rules J2, J3, J5, J7), written for sm_100a.
+//
+// Philox4x32-10: 10 rounds of two 32x32->64 multiplies (IMAD.WIDE.U32 /
+// IMAD.HI) and xors with a Weyl-sequence key schedule.  A JIT row is a pure
+// function of (seed, row, segment, draw index), so any lane can regenerate
+// any edge with no connectivity memory (App. C).
+#pragma once
+#include <cstdint>
+
+namespace bp {
+
+struct u32x4 {
+  uint32_t x, y, z, w;
+};
+
+__device__ __forceinline__ u32x4 philox4x32_10(uint32_t c0, uint32_t c1,
+                                               uint32_t c2, uint32_t c3,
+                                               uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int round = 0; round < 10; ++round) {
+    const uint32_t lo0 = 0xD2511F53u * c0;
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0);
+    const uint32_t lo1 = 0xCD9E8D57u * c2;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2);
+    const uint32_t n0 = hi1 ^ c1 ^ k0;
+    const uint32_t n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return {c0, c1, c2, c3};
+}
+
+// Block of 4 words j = 4*blk .. 4*blk+3 of stream (tag, row, seg):
+// counter = (blk, row, seg, tag), key = (lo32(seed), hi32(seed)).
+__device__ __forceinline__ u32x4 philox_block(uint64_t seed, uint32_t tag,
+                                              uint32_t row, uint32_t seg,
+                                              uint32_t blk) {
+  return philox4x32_10(blk, row, seg, tag, static_cast<uint32_t>(seed),
+                       static_cast<uint32_t>(seed >> 32));
+}
+
+__device__ __forceinline__ uint32_t word_of(const u32x4 &b, uint32_t k) {
+  return k == 0 ? b.x : (k == 1 ? b.y : (k == 2 ? b.z : b.w));
+}
+
+// Rule J3: lo + floor(x * (hi - lo + 1) / 2^32).
+__device__ __forceinline__ uint32_t bounded(uint32_t lo, uint32_t span,
+                                            uint32_t x) {
+  return lo + __umulhi(x, span);
+}
+// span == 2^32 cannot occur: K < 2^31.
+
+enum : uint32_t { kTagGap = 0, kTagWeight = 1, kTagFirst = 2 };
+
+// Rule J5: stationary first offset a in [0, K) of (row, seg):
+// a = U[0,K-1](w0), b = U[0,K](w1), b <= a -> a = K-1-a.
+__device__ __forceinline__ uint32_t first_offset(uint64_t seed, uint32_t K,
+                                                 uint32_t row, uint32_t seg) {
+  const u32x4 b = philox_block(seed, kTagFirst, row, seg, 0);
+  uint32_t a = bounded(0u, K, b.x);
+  const uint32_t c = bounded(0u, K + 1u, b.y);
+  if (c <= a) a = K - 1u - a;
+  return a;
+}
+
+// Rule J7 weights.  uniform: u = (x >> 8) 2^-24, w = fmaf(u, hi - lo, lo).
+__device__ __forceinline__ float uniform_weight(uint32_t x, float lo,
+                                                float span) {
+  const float u = __uint2float_rn(x >> 8) * 0x1p-24f;
+  return __fmaf_rn(u, span, lo);
+}
+
+// normal: u1 = ((x1 >> 8) + 1) 2^-24 in (0,1], u2 = (x2 >> 8) 2^-24;
+// z = sqrt(-2 ln u1) cos(2 pi u2) evaluated in fp64, w = fmaf(sigma, (float)z, mu).
+__device__ __forceinline__ float normal_weight(uint32_t x1, uint32_t x2,
+                                               float mu, float sigma) {
+  const float u1 = __uint2float_rn((x1 >> 8) + 1u) * 0x1p-24f;
+  const float u2 = __uint2float_rn(x2 >> 8) * 0x1p-24f;
+  const double radius = sqrt(__dmul_rn(-2.0, log(static_cast<double>(u1))));
+  const double z =
+      __dmul_rn(radius, cos(__dmul_rn(6.283185307179586, static_cast<double>(u2))));
+  return __fmaf_rn(sigma, __double2float_rn(z), mu);
+}
+
+// Rule F1: q(w) = round-half-even(w * 2^32) as int64.
+__device__ __forceinline__ long long quantize(float w) {
+  return __double2ll_rn(__dmul_rn(static_cast<double>(w), 4294967296.0));
+}
+
+}  // namespace bp

@@ -1,0 +1,347 @@
+// scatter.cuh -- spike compaction (a1), CSR event scatter (a2) and JIT
+// connectivity regeneration + scatter (a3, a4) for sm_100a.
+//
+// Design:
+//  * compaction: one thread per 32-bit spike word; warp inclusive scan of
+//    popcounts, one atomicAdd per warp claims a slice of the active list.
+//  * CSR: one warp per active row (grid-stride).  A row's indices/data are
+//    read as 128-byte coalesced warp loads, 4 loads in flight per lane, and
+//    every synaptic event is one fire-and-forget RED (no return value).
+//  * JIT: one warp per (active row, segment).  Lane l of chunk c owns gap
+//    draws 128c+4l..128c+4l+3 (one Philox block), a warp scan turns gaps into
+//    positions, and each lane scatters its (up to) 4 edges.  No connectivity
+//    bytes are read at all.
+#pragma once
+#include <cstdint>
+
+#include "rng.cuh"
+
+namespace bp {
+
+constexpr int kScatterThreads = 256;
+
+__device__ __forceinline__ void add_f32(void *out, int64_t c, float w) {
+  atomicAdd(static_cast<float *>(out) + c, w);
+}
+__device__ __forceinline__ void add_fix(void *out, int64_t c, long long q) {
+  atomicAdd(reinterpret_cast<unsigned long long *>(out) + c,
+            static_cast<unsigned long long>(q));
+}
+
+// Block-wide sum of per-thread event counts, one atomic per block.
+__device__ __forceinline__ void count_events(unsigned long long *counter,
+                                             unsigned long long mine) {
+  if (counter == nullptr) return;
+  __shared__ unsigned long long block_sum;
+  if (threadIdx.x == 0) block_sum = 0;
+  __syncthreads();
+  mine = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(mine));
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&block_sum, mine);
+  __syncthreads();
+  if (threadIdx.x == 0 && block_sum) atomicAdd(counter, block_sum);
+}
+
+// ---------------------------------------------------------------- a1
+__global__ void __launch_bounds__(256)
+k_compact(const uint32_t *__restrict__ spikes, int64_t n,
+          int32_t *__restrict__ active, int32_t *__restrict__ count,
+          int32_t id_base) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n_words = (n + 31) >> 5;
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t base = warp0 * 32; base < n_words; base += n_warps * 32) {
+    const int64_t wi = base + lane;
+    uint32_t word = 0;
+    if (wi < n_words) {
+      word = __ldg(spikes + wi);
+      const int64_t valid = n - (wi << 5);
+      if (valid < 32) word &= (1u << valid) - 1u;
+    }
+    const int c = __popc(word);
+    int incl = c;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += t;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) continue;
+    int slot = 0;
+    if (lane == 31) slot = atomicAdd(count, total);
+    slot = __shfl_sync(0xffffffffu, slot, 31) + incl - c;
+    while (word) {
+      const int b = __ffs(word) - 1;
+      active[slot++] = id_base + static_cast<int32_t>((wi << 5) + b);
+      word &= word - 1u;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- a2
+struct CsrSide {
+  const int64_t *indptr;
+  const int32_t *indices;
+  const float *data;  // nullptr -> homogeneous w
+  float w;
+  long long q;        // quantize(w)
+  void *out;
+};
+
+struct CsrScatterArgs {
+  CsrSide e, i;          // rows < split -> e (row), else i (row - split)
+  int64_t split;
+  const int32_t *active;
+  const int32_t *count;
+  int32_t *zero_count;   // nullable; set to 0 by thread 0 (ping-pong list)
+  unsigned long long *events;   // nullable
+  unsigned long long *spikes;   // nullable; += *count once
+};
+
+// Field-wise select keeps the chosen projection in registers (a runtime
+// reference into the kernel-parameter struct would spill it to local memory).
+__device__ __forceinline__ CsrSide pick(bool second, const CsrSide &x,
+                                        const CsrSide &y) {
+  CsrSide s;
+  s.indptr = second ? y.indptr : x.indptr;
+  s.indices = second ? y.indices : x.indices;
+  s.data = second ? y.data : x.data;
+  s.w = second ? y.w : x.w;
+  s.q = second ? y.q : x.q;
+  s.out = second ? y.out : x.out;
+  return s;
+}
+
+template <int KIND>
+__device__ __forceinline__ void csr_emit(const CsrSide &s, int32_t c, float w) {
+  if (KIND == 0) add_f32(s.out, c, w);
+  else add_fix(s.out, c, s.data ? quantize(w) : s.q);
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kScatterThreads)
+k_csr_scatter(CsrScatterArgs a) {
+  const int n_active = *a.count;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (a.zero_count) *a.zero_count = 0;
+    if (a.spikes) atomicAdd(a.spikes, static_cast<unsigned long long>(n_active));
+  }
+  const int lane = threadIdx.x & 31;
+  const int warp0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int n_warps = (gridDim.x * blockDim.x) >> 5;
+  unsigned long long ev = 0;
+  for (int k = warp0; k < n_active; k += n_warps) {
+    const int64_t r = a.active[k];
+    const bool inh = r >= a.split;
+    const CsrSide s = pick(inh, a.e, a.i);
+    const int64_t row = inh ? r - a.split : r;
+    const int64_t begin = __ldg(s.indptr + row);
+    const int64_t end = __ldg(s.indptr + row + 1);
+    if (lane == 0) ev += static_cast<unsigned long long>(end - begin);
+    int64_t j = begin + lane;
+    // 4 independent 128-byte warp loads in flight before the REDs.
+    for (; j + 96 < end; j += 128) {
+      const int32_t c0 = __ldg(s.indices + j), c1 = __ldg(s.indices + j + 32);
+      const int32_t c2 = __ldg(s.indices + j + 64), c3 = __ldg(s.indices + j + 96);
+      float w0 = s.w, w1 = s.w, w2 = s.w, w3 = s.w;
+      if (s.data) {
+        w0 = __ldg(s.data + j); w1 = __ldg(s.data + j + 32);
+        w2 = __ldg(s.data + j + 64); w3 = __ldg(s.data + j + 96);
+      }
+      csr_emit<KIND>(s, c0, w0); csr_emit<KIND>(s, c1, w1);
+      csr_emit<KIND>(s, c2, w2); csr_emit<KIND>(s, c3, w3);
+    }
+    for (; j < end; j += 32) {
+      const int32_t c = __ldg(s.indices + j);
+      csr_emit<KIND>(s, c, s.data ? __ldg(s.data + j) : s.w);
+    }
+  }
+  count_events(a.events, ev);
+}
+
+// ---------------------------------------------------------------- a3 + a4
+struct JitSide {
+  uint64_t seed;
+  uint32_t K, L;
+  uint32_t seg_first, n_seg;   // local segments [seg_first, seg_first + n_seg)
+  float w0, w1;                // homo: (w, -); uniform: (lo, hi-lo); normal: (mu, sigma)
+  long long q;                 // quantize(w0) for homo
+  void *out;                   // indexed c - col_begin
+};
+
+struct JitScatterArgs {
+  JitSide e, i;
+  int64_t split;
+  uint32_t n_seg_max;
+  uint32_t n_cols, col_begin, col_end;
+  const int32_t *active;
+  const int32_t *count;
+  int32_t *zero_count;
+  unsigned long long *events;
+  unsigned long long *spikes;
+};
+
+__device__ __forceinline__ JitSide pick(bool second, const JitSide &x,
+                                        const JitSide &y) {
+  JitSide s;
+  s.seed = second ? y.seed : x.seed;
+  s.K = second ? y.K : x.K;
+  s.L = second ? y.L : x.L;
+  s.seg_first = second ? y.seg_first : x.seg_first;
+  s.n_seg = second ? y.n_seg : x.n_seg;
+  s.w0 = second ? y.w0 : x.w0;
+  s.w1 = second ? y.w1 : x.w1;
+  s.q = second ? y.q : x.q;
+  s.out = second ? y.out : x.out;
+  return s;
+}
+
+template <int LAW, int KIND>
+__device__ __forceinline__ void jit_emit(const JitSide &s, uint32_t pos,
+                                         uint32_t col_begin, float w) {
+  const int64_t c = static_cast<int64_t>(pos) - col_begin;
+  if (KIND == 0) add_f32(s.out, c, w);
+  else add_fix(s.out, c, LAW == 0 ? s.q : quantize(w));
+}
+
+template <int LAW, int KIND>
+__global__ void __launch_bounds__(kScatterThreads)
+k_jit_scatter(JitScatterArgs a) {
+  const int n_active = *a.count;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (a.zero_count) *a.zero_count = 0;
+    if (a.spikes) atomicAdd(a.spikes, static_cast<unsigned long long>(n_active));
+  }
+  const uint32_t lane = threadIdx.x & 31;
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t n_items = static_cast<int64_t>(n_active) * a.n_seg_max;
+  unsigned long long ev = 0;
+  for (int64_t item = warp0; item < n_items; item += n_warps) {
+    const int64_t r = a.active[item / a.n_seg_max];
+    const uint32_t sidx = static_cast<uint32_t>(item % a.n_seg_max);
+    const bool inh = r >= a.split;
+    const JitSide s = pick(inh, a.e, a.i);
+    if (sidx >= s.n_seg) continue;
+    const uint32_t row = static_cast<uint32_t>(inh ? r - a.split : r);
+    const uint32_t seg = s.seg_first + sidx;
+    const uint32_t seg_begin = seg * s.L;
+    const uint32_t seg_end = min(seg_begin + s.L, a.n_cols);
+    uint32_t start = seg_begin + first_offset(s.seed, s.K, row, seg);
+    uint32_t chunk = 0;
+    while (start < seg_end) {                      // warp-uniform
+      const uint32_t blk = chunk * 32u + lane;
+      const u32x4 g = philox_block(s.seed, kTagGap, row, seg, blk);
+      const uint32_t g0 = bounded(1u, s.K, g.x), g1 = bounded(1u, s.K, g.y);
+      const uint32_t g2 = bounded(1u, s.K, g.z), g3 = bounded(1u, s.K, g.w);
+      const uint32_t p1 = g0, p2 = g0 + g1, p3 = p2 + g2, t = p3 + g3;
+      uint32_t incl = t;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= static_cast<uint32_t>(off)) incl += v;
+      }
+      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      const uint32_t pos0 = start + (incl - t);
+      if (pos0 < seg_end) {
+        const uint32_t pos[4] = {pos0, pos0 + p1, pos0 + p2, pos0 + p3};
+        float w[4] = {s.w0, s.w0, s.w0, s.w0};
+        if (LAW == 1) {
+          const u32x4 x = philox_block(s.seed, kTagWeight, row, seg, blk);
+          w[0] = uniform_weight(x.x, s.w0, s.w1); w[1] = uniform_weight(x.y, s.w0, s.w1);
+          w[2] = uniform_weight(x.z, s.w0, s.w1); w[3] = uniform_weight(x.w, s.w0, s.w1);
+        } else if (LAW == 2) {
+          const u32x4 x = philox_block(s.seed, kTagWeight, row, seg, 2u * blk);
+          w[0] = normal_weight(x.x, x.y, s.w0, s.w1);
+          if (pos[1] < seg_end) w[1] = normal_weight(x.z, x.w, s.w0, s.w1);
+          if (pos[2] < seg_end) {
+            const u32x4 y = philox_block(s.seed, kTagWeight, row, seg, 2u * blk + 1u);
+            w[2] = normal_weight(y.x, y.y, s.w0, s.w1);
+            if (pos[3] < seg_end) w[3] = normal_weight(y.z, y.w, s.w0, s.w1);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (pos[k] < seg_end && pos[k] >= a.col_begin && pos[k] < a.col_end) {
+            jit_emit<LAW, KIND>(s, pos[k], a.col_begin, w[k]);
+            ++ev;
+          }
+        }
+      }
+      start += total;
+      ++chunk;
+    }
+  }
+  count_events(a.events, ev);
+}
+
+// Row counts / materialisation with the kernel's own generator (debug).
+__global__ void __launch_bounds__(kScatterThreads)
+k_jit_rows(JitSide s, int64_t n_rows, uint32_t n_cols, int law,
+           const int64_t *__restrict__ indptr, int64_t *__restrict__ counts,
+           int32_t *__restrict__ indices, float *__restrict__ data) {
+  const uint32_t lane = threadIdx.x & 31;
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = warp0; r < n_rows; r += n_warps) {
+    const uint32_t row = static_cast<uint32_t>(r);
+    int64_t out = indptr ? indptr[r] : 0;
+    for (uint32_t seg = 0; seg < s.n_seg; ++seg) {
+      const uint32_t seg_begin = seg * s.L;
+      const uint32_t seg_end = min(seg_begin + s.L, n_cols);
+      uint32_t start = seg_begin + first_offset(s.seed, s.K, row, seg);
+      uint32_t chunk = 0;
+      while (start < seg_end) {
+        const uint32_t blk = chunk * 32u + lane;
+        const u32x4 g = philox_block(s.seed, kTagGap, row, seg, blk);
+        const uint32_t g0 = bounded(1u, s.K, g.x), g1 = bounded(1u, s.K, g.y);
+        const uint32_t g2 = bounded(1u, s.K, g.z), g3 = bounded(1u, s.K, g.w);
+        const uint32_t p1 = g0, p2 = g0 + g1, p3 = p2 + g2, t = p3 + g3;
+        uint32_t incl = t;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= static_cast<uint32_t>(off)) incl += v;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t pos0 = start + (incl - t);
+        const uint32_t pos[4] = {pos0, pos0 + p1, pos0 + p2, pos0 + p3};
+        int nv = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) nv += pos[k] < seg_end;
+        // edges before this lane in this chunk
+        uint32_t nv_incl = nv;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t v = __shfl_up_sync(0xffffffffu, nv_incl, off);
+          if (lane >= static_cast<uint32_t>(off)) nv_incl += v;
+        }
+        const uint32_t nv_total = __shfl_sync(0xffffffffu, nv_incl, 31);
+        if (indices) {
+          int64_t o = out + (nv_incl - nv);
+          float w[4] = {s.w0, s.w0, s.w0, s.w0};
+          if (nv > 0 && law == 1) {
+            const u32x4 x = philox_block(s.seed, kTagWeight, row, seg, blk);
+            w[0] = uniform_weight(x.x, s.w0, s.w1); w[1] = uniform_weight(x.y, s.w0, s.w1);
+            w[2] = uniform_weight(x.z, s.w0, s.w1); w[3] = uniform_weight(x.w, s.w0, s.w1);
+          } else if (nv > 0 && law == 2) {
+            const u32x4 x = philox_block(s.seed, kTagWeight, row, seg, 2u * blk);
+            const u32x4 y = philox_block(s.seed, kTagWeight, row, seg, 2u * blk + 1u);
+            w[0] = normal_weight(x.x, x.y, s.w0, s.w1); w[1] = normal_weight(x.z, x.w, s.w0, s.w1);
+            w[2] = normal_weight(y.x, y.y, s.w0, s.w1); w[3] = normal_weight(y.z, y.w, s.w0, s.w1);
+          }
+          for (int k = 0; k < nv; ++k) {
+            indices[o + k] = static_cast<int32_t>(pos[k]);
+            if (data) data[o + k] = w[k];
+          }
+        }
+        out += nv_total;
+        start += total;
+        ++chunk;
+      }
+    }
+    if (counts && lane == 0) counts[r] = out;
+  }
+}
+
+}  // namespace bp

@@ -1,0 +1,177 @@
+"""COBA E/I networks of Listing S3 on the C ABI, one process per GPU.
+
+Host logic only: building the state tensors, the postsynaptic partition of
+SURVEY 8(e) (rank g owns neurons [lo_g, hi_g)), and the per-step bit-packed
+spike all-gather over torch.distributed (NCCL on GPUs, gloo in the CPU
+tests).  Every arithmetic step of the simulation runs in libbp.so.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _binding as B
+from . import inputs
+
+# Listing S3: 80 % excitatory, p = 80 / N, w_E = 0.6, w_I = 6.7.
+SEED_E, SEED_I = 0x5EED0001, 0x5EED0002
+W_E_LIF, W_I_LIF = 0.6, 6.7
+W_E_HH, W_I_HH = 6.0, 67.0          # COBA-HH nS (rule H1, EXTERNAL)
+
+
+@dataclass(frozen=True)
+class Partition:
+    """Postsynaptic slice [col_begin, col_end) of rank `rank` out of `world`.
+    Every rank owns `local` neurons (the last one possibly fewer); `local`
+    is a multiple of `align` (32-bit spike words, JIT segments)."""
+    rank: int
+    world: int
+    n: int
+    local: int
+
+    @property
+    def col_begin(self) -> int:
+        return min(self.n, self.rank * self.local)
+
+    @property
+    def col_end(self) -> int:
+        return min(self.n, (self.rank + 1) * self.local)
+
+    @property
+    def local_words(self) -> int:
+        return self.local // 32
+
+    @property
+    def padded_words(self) -> int:
+        """Length of the all-gathered spike vector in words (world * local/32)."""
+        return self.world * self.local_words
+
+
+def partition(n: int, world: int, rank: int, align: int = 32) -> Partition:
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"rank {rank} of world {world}")
+    align = math.lcm(32, int(align))
+    local = -(-n // world)
+    local = -(-local // align) * align
+    return Partition(rank, world, n, local)
+
+
+def exchange_spikes(words: torch.Tensor, part: Partition, group=None,
+                    send: torch.Tensor | None = None) -> torch.Tensor:
+    """All-gather the bit-packed spike vector: rank g contributes its words
+    [g*local/32, (g+1)*local/32) of `words` (length part.padded_words) and
+    receives everybody else's (a8; "gather only non-zero spikes",
+    realised as bit packing).  Works with NCCL and gloo."""
+    import torch.distributed as dist
+    lw = part.local_words
+    mine = words[part.rank * lw:(part.rank + 1) * lw]
+    if send is None:
+        send = mine.clone()
+    else:
+        send.copy_(mine)
+    dist.all_gather_into_tensor(words, send, group=group)
+    return words
+
+
+class CobaNetwork:
+    """One rank's share of the Listing S3 E/I network (COBA-LIF or COBA-HH).
+
+    conn='jit': connectivity regenerated each step from (seed, p) -- the
+    EventJitFPHomoLinear / event_mv_prob_homo projection of P:973-981.
+    conn='csr': stored CSR (event_csrmv, Listing S1); `csr` gives the full
+    (indptr, indices) of the E rows and the I rows (torch CPU or CUDA), and
+    this rank keeps the columns it owns.
+    """
+
+    def __init__(self, n: int, *, model: str = "lif", conn: str = "jit",
+                 fixed: bool = True, p: float | None = None, seg_len: int | None = None,
+                 rank: int = 0, world: int = 1, device=None, csr=None,
+                 w_exc: float | None = None, w_inh: float | None = None,
+                 seed_e: int = SEED_E, seed_i: int = SEED_I, v0=None,
+                 init_seed: int = inputs.V0_SEED, spikes: torch.Tensor | None = None):
+        device = torch.device(device or "cuda")
+        self.n = n
+        self.n_exc = n * 4 // 5
+        self.model, self.conn, self.fixed = model, conn, fixed
+        self.p = 80.0 / n if p is None else p
+        if seg_len is None:
+            # one JIT segment per rank: the partition is the segment (8(e))
+            seg_len = partition(n, world, rank).local if world > 1 else n
+        self.seg_len = seg_len
+        self.part = partition(n, world, rank, align=seg_len if conn == "jit" and world > 1 else 32)
+        lo, hi = self.part.col_begin, self.part.col_end
+        n_local = hi - lo
+        if model == "lif":
+            w_exc = W_E_LIF if w_exc is None else w_exc
+            w_inh = W_I_LIF if w_inh is None else w_inh
+            params = B.lif_params()
+        else:
+            w_exc = W_E_HH if w_exc is None else w_exc
+            w_inh = W_I_HH if w_inh is None else w_inh
+            params = B.hh_params()
+        self.w_exc, self.w_inh, self.params = w_exc, w_inh, params
+        g_dtype = torch.int64 if fixed else torch.float32
+        st = {"g_e": torch.zeros(n_local, dtype=g_dtype, device=device),
+              "g_i": torch.zeros(n_local, dtype=g_dtype, device=device)}
+        if model == "lif":
+            v_all = inputs.lif_v0(n, init_seed) if v0 is None else v0
+            st["v"] = torch.as_tensor(v_all[lo:hi]).to(device).contiguous()
+            st["ref"] = torch.zeros(n_local, dtype=torch.uint8, device=device)
+        else:
+            v, m, h, nk = inputs.hh_init(n, init_seed) if v0 is None else v0
+            for k, a in (("v", v), ("m", m), ("h", h), ("n", nk)):
+                st[k] = torch.as_tensor(a[lo:hi]).to(device).contiguous()
+        self.state = st
+        # bit-packed spike vector (int32 storage of the uint32 words); a
+        # caller may share one vector between partitions on one device
+        words = self.part.padded_words if world > 1 else (n + 31) // 32
+        self.spikes = (torch.zeros(words, dtype=torch.int32, device=device)
+                       if spikes is None else spikes)
+        kw = {}
+        if conn == "jit":
+            K = B.conn_len(self.p)
+            kw["jit_exc"] = B.jitconn_spec(seed_e, self.p, K, seg_len)
+            kw["jit_inh"] = B.jitconn_spec(seed_i, self.p, K, seg_len)
+        else:
+            (ip_e, ix_e), (ip_i, ix_i) = csr
+            kw["csr_exc"] = _slice_csr(ip_e, ix_e, lo, hi, device)
+            kw["csr_inh"] = _slice_csr(ip_i, ix_i, lo, hi, device)
+        self.net = B.Network(model=B.MODEL_LIF if model == "lif" else B.MODEL_HH,
+                             conn=B.CONN_JIT if conn == "jit" else B.CONN_CSR,
+                             n=n, n_exc=self.n_exc, state=st, spikes=self.spikes,
+                             params=params, col_begin=lo, col_end=hi,
+                             w_exc=w_exc, w_inh=w_inh, **kw)
+        self._send = None
+
+    # single device: the whole loop runs in the library
+    def run(self, n_steps: int, raster: torch.Tensor | None = None, counts=None):
+        self.net.step(n_steps, raster, counts)
+
+    # several devices: scatter -> update -> all-gather, per step
+    def step_distributed(self, group=None, raster_row=None):
+        self.net.scatter()
+        self.net.update(raster_row)
+        if self._send is None:
+            self._send = torch.empty(self.part.local_words, dtype=torch.int32,
+                                     device=self.spikes.device)
+        exchange_spikes(self.spikes, self.part, group, self._send)
+
+    def counters(self):
+        return self.net.counters()
+
+
+def _slice_csr(indptr, indices, lo, hi, device):
+    """Keep the columns [lo, hi) of a row-major CSR, rebased to 0 (8(e))."""
+    ip = torch.as_tensor(indptr).to(torch.int64).cpu()
+    ix = torch.as_tensor(indices).to(torch.int32).cpu()
+    n_rows = ip.numel() - 1
+    if lo == 0 and hi >= int(ix.max().item() if ix.numel() else 0) + 1:
+        return ip.to(device), ix.to(device), None
+    rows = torch.repeat_interleave(torch.arange(n_rows), ip[1:] - ip[:-1])
+    keep = (ix >= lo) & (ix < hi)
+    rows, cols = rows[keep], ix[keep] - lo
+    new_ip = torch.zeros(n_rows + 1, dtype=torch.int64)
+    new_ip[1:] = torch.cumsum(torch.bincount(rows, minlength=n_rows), 0)
+    return new_ip.to(device), cols.to(torch.int32).contiguous().to(device), None

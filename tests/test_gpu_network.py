@@ -1,0 +1,150 @@
+"""GPU parity of the network step (rule S1: Listing S3's update loop) against
+the oracle's run_network.
+
+Fixed-point mode (BP_OUT_FIX64) is the primary parity mode: rasters, V bits
+and g are bit-exact for every step.  fp32 mode (fp32 atomics) follows rule
+T3: rasters identical over the first 200 steps and the population rate
+within 1 % over 1 s (north_star).
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_2311_05106_b200 import inputs
+from paper_2311_05106_b200.network import SEED_E, SEED_I, CobaNetwork
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import __graft_entry__ as ge
+    ge.build_lib()
+    torch.cuda.set_device(0)
+
+
+def _oracle_lif(orc, n, fixed, csr=None):
+    n_exc = n * 4 // 5
+    K = orc.conn_len(80.0 / n)
+    if csr is None:
+        pe = orc.Projection(0, n_exc, jit=orc.JitSpec(SEED_E, K, n, orc.LAW_HOMO, 0.6))
+        pi = orc.Projection(n_exc, n - n_exc, jit=orc.JitSpec(SEED_I, K, n, orc.LAW_HOMO, 6.7))
+    else:
+        (ipe, ixe), (ipi, ixi) = csr
+        pe = orc.Projection(0, n_exc, csr=(ipe, ixe, None), w_homo=0.6)
+        pi = orc.Projection(n_exc, n - n_exc, csr=(ipi, ixi, None), w_homo=6.7)
+    g = np.int64 if fixed else np.float32
+    st = dict(v=inputs.lif_v0(n), g_e=np.zeros(n, g), g_i=np.zeros(n, g),
+              ref=np.zeros(n, np.uint8), spikes=np.zeros(n, np.uint8))
+    return st, pe, pi
+
+
+def _raster(r, n):
+    return np.stack([inputs.unpack_bits(row, n) for row in r.cpu().numpy().view(np.uint32)])
+
+
+@pytest.mark.parametrize("n,steps", [(4000, 2000), (1000, 500), (12_345, 300)])
+def test_coba_lif_jit_fixed_bit_exact(orc, n, steps):
+    net = CobaNetwork(n, conn="jit", fixed=True)
+    raster = torch.zeros((steps, (n + 31) // 32), dtype=torch.int32, device="cuda")
+    net.run(steps, raster)
+    st, pe, pi = _oracle_lif(orc, n, True)
+    want = orc.run_network("lif", orc.lif_params(), st, pe, pi, steps)
+    got = _raster(raster, n)
+    assert want.sum() > 0
+    assert np.array_equal(got, want)
+    assert np.array_equal(net.state["v"].cpu().numpy().view(np.uint32), st["v"].view(np.uint32))
+    assert np.array_equal(net.state["g_e"].cpu().numpy(), st["g_e"])
+    assert np.array_equal(net.state["g_i"].cpu().numpy(), st["g_i"])
+    assert np.array_equal(net.state["ref"].cpu().numpy(), st["ref"])
+    spikes, events = net.counters()
+    assert spikes == int(want[:-1].sum())       # spikes of the last step not yet delivered
+    assert events > 0
+
+
+def test_coba_lif_csr_fixed_bit_exact(orc):
+    n, steps = 4000, 1000
+    n_exc = 3200
+    ipe, ixe, _ = inputs.random_csr(n_exc, n, 0.02, seed=1)
+    ipi, ixi, _ = inputs.random_csr(n - n_exc, n, 0.02, seed=2)
+    csr = ((ipe, ixe), (ipi, ixi))
+    net = CobaNetwork(n, conn="csr", fixed=True, csr=csr)
+    raster = torch.zeros((steps, n // 32), dtype=torch.int32, device="cuda")
+    net.run(steps, raster)
+    st, pe, pi = _oracle_lif(orc, n, True, csr=csr)
+    want = orc.run_network("lif", orc.lif_params(), st, pe, pi, steps)
+    assert want.sum() > 0
+    assert np.array_equal(_raster(raster, n), want)
+    assert np.array_equal(net.state["v"].cpu().numpy().view(np.uint32), st["v"].view(np.uint32))
+
+
+def test_coba_lif_f32_rule_t3(orc):
+    """T3: identical rasters for 200 steps, rate within 1 % over 1 s."""
+    n, steps = 4000, 10_000
+    net = CobaNetwork(n, conn="jit", fixed=False)
+    raster = torch.zeros((steps, n // 32), dtype=torch.int32, device="cuda")
+    net.run(steps, raster)
+    st, pe, pi = _oracle_lif(orc, n, False)
+    want = orc.run_network("lif", orc.lif_params(), st, pe, pi, steps)
+    got = _raster(raster, n)
+    assert np.array_equal(got[:200], want[:200])
+    rate_got, rate_want = got.sum() / n, want.sum() / n
+    assert abs(rate_got - rate_want) <= 0.01 * rate_want
+
+
+@pytest.mark.parametrize("fixed", [True, False])
+def test_coba_hh_csr(orc, fixed):
+    n, steps = 4000, 400
+    n_exc = 3200
+    ipe, ixe, _ = inputs.random_csr(n_exc, n, 0.02, seed=11)
+    ipi, ixi, _ = inputs.random_csr(n - n_exc, n, 0.02, seed=12)
+    net = CobaNetwork(n, model="hh", conn="csr", fixed=fixed, csr=((ipe, ixe), (ipi, ixi)))
+    raster = torch.zeros((steps, n // 32), dtype=torch.int32, device="cuda")
+    net.run(steps, raster)
+    v, m, h, nk = inputs.hh_init(n)
+    g = np.int64 if fixed else np.float32
+    st = dict(v=v, m=m, h=h, n=nk, g_e=np.zeros(n, g), g_i=np.zeros(n, g),
+              spikes=np.zeros(n, np.uint8))
+    pe = orc.Projection(0, n_exc, csr=(ipe, ixe, None), w_homo=6.0)
+    pi = orc.Projection(n_exc, n - n_exc, csr=(ipi, ixi, None), w_homo=67.0)
+    want = orc.run_network("hh", orc.hh_params(), st, pe, pi, steps)
+    got = _raster(raster, n)
+    assert want.sum() > 0
+    if fixed:
+        assert np.array_equal(got, want)
+        assert np.array_equal(net.state["v"].cpu().numpy().view(np.uint32), st["v"].view(np.uint32))
+    else:
+        assert np.array_equal(got[:200], want[:200])
+
+
+def test_split_step_equals_fused_step(orc):
+    """bp_network_scatter + bp_network_update (the multi-GPU halves, with no
+    exchange at world 1) reproduce bp_network_step."""
+    n, steps = 3000, 300
+    a = CobaNetwork(n, conn="jit", fixed=True)
+    b = CobaNetwork(n, conn="jit", fixed=True)
+    a.run(steps)
+    for _ in range(steps):
+        b.net.scatter()
+        b.net.update()
+    assert np.array_equal(a.state["v"].cpu().numpy(), b.state["v"].cpu().numpy())
+    assert np.array_equal(a.state["g_e"].cpu().numpy(), b.state["g_e"].cpu().numpy())
+
+
+def test_partitions_emulated_on_one_gpu_equal_whole(orc):
+    """G postsynaptic partitions stepped one after another on one device,
+    with the all-gather emulated by sharing one spike vector, give the
+    single-partition network bit for bit."""
+    n, steps, world = 4096, 300, 4
+    whole = CobaNetwork(n, conn="jit", fixed=True, seg_len=1024)
+    whole.run(steps)
+    shared = torch.zeros(n // 32, dtype=torch.int32, device="cuda")
+    parts = [CobaNetwork(n, conn="jit", fixed=True, seg_len=1024, rank=r, world=world,
+                         spikes=shared) for r in range(world)]
+    for _ in range(steps):
+        for q in parts:          # every rank scatters spikes_{n-1} first ...
+            q.net.scatter()
+        for q in parts:          # ... then all update (the exchange is the shared vector)
+            q.net.update()
+    v = np.concatenate([q.state["v"].cpu().numpy() for q in parts])
+    assert np.array_equal(v.view(np.uint32), whole.state["v"].cpu().numpy().view(np.uint32))

@@ -1,0 +1,280 @@
+"""GPU parity of the stateless C-ABI operators against the CPU oracle.
+
+Bars: index sets, positions and every BP_OUT_FIX64
+output are bit-exact; BP_OUT_F32 outputs satisfy rule T2,
+|y_gpu - y_f64| <= 1e-5 * sum|w| + 1e-30 per output (order-free bound for
+fp32 atomics); normal-law weights (fp64 log/cos on both sides, rounded to
+fp32) may differ by 1 ulp from the oracle's in a vanishing fraction of
+edges, so their fixed-point sums are compared within that allowance.
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_2311_05106_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def bp():
+    import __graft_entry__ as ge
+    ge.build_lib()
+    import paper_2311_05106_b200 as bp
+    torch.cuda.set_device(0)
+    return bp
+
+
+def _dev_spikes(ev):
+    return torch.from_numpy(inputs.pack_bits(ev).view(np.int32)).cuda()
+
+
+def _t(a):
+    return None if a is None else torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+# ------------------------------------------------------------------ a1
+@pytest.mark.parametrize("n", [1, 31, 32, 33, 1000, 100_003, 3_000_017])
+@pytest.mark.parametrize("density", [0.0, 0.001, 0.3, 1.0])
+def test_compact_is_the_active_set(bp, n, density):
+    ev = inputs.spike_pattern(n, density, seed=n)
+    spikes = _dev_spikes(ev)
+    active = torch.full((n,), -1, dtype=torch.int32, device="cuda")
+    count = torch.zeros(1, dtype=torch.int32, device="cuda")
+    bp.compact_spikes(spikes, n, active, count)
+    c = int(count.item())
+    got = np.sort(active[:c].cpu().numpy())
+    assert np.array_equal(got, np.nonzero(ev)[0].astype(np.int32))
+
+
+def test_compact_ignores_tail_bits(bp):
+    words = torch.full((2,), -1, dtype=torch.int32, device="cuda")   # 64 set bits
+    active = torch.zeros(40, dtype=torch.int32, device="cuda")
+    count = torch.zeros(1, dtype=torch.int32, device="cuda")
+    bp.compact_spikes(words, 40, active, count)
+    assert int(count.item()) == 40
+
+
+# ------------------------------------------------------------------ a2
+CSR_CASES = [
+    # n_rows, n_cols, p, weights, density
+    (1, 1, 1.0, "homo", 1.0),
+    (50, 70, 0.2, "homo", 0.5),
+    (300, 5000, 0.05, "uniform", 0.1),    # rows of ~250: several 128-wide chunks + tail
+    (2000, 3000, 0.01, "normal", 0.01),
+    (4000, 4000, 0.02, "homo", 0.002),
+    (1000, 100_000, 0.05, "uniform", 0.05),   # fan-out 5000 (config 2 row shape)
+]
+
+
+@pytest.mark.parametrize("case", CSR_CASES)
+def test_event_csrmv(bp, orc, case):
+    n_rows, n_cols, p, law, density = case
+    ip, ix, dat = inputs.random_csr(n_rows, n_cols, p, seed=n_rows + n_cols,
+                                    weights=law, w0=-0.5 if law != "homo" else 1.0,
+                                    w1=0.5 if law != "homo" else 0.0)
+    w_homo = 0.6
+    ev = inputs.spike_pattern(n_rows, density, seed=3)
+    spikes = _dev_spikes(ev)
+    tip, tix, tdat = _t(ip), _t(ix), _t(dat)
+    # fixed point: bit-exact
+    out = torch.zeros(n_cols, dtype=torch.int64, device="cuda")
+    bp.event_csrmv(tip, tix, tdat, w_homo, n_rows, n_cols, spikes, out)
+    want = orc.event_csrmv(ip, ix, dat, w_homo, n_rows, n_cols, ev, orc.OUT_FIX)
+    assert np.array_equal(out.cpu().numpy(), want)
+    # fp32 atomics: rule T2
+    out32 = torch.full((n_cols,), 7.0, dtype=torch.float32, device="cuda")
+    bp.event_csrmv(tip, tix, tdat, w_homo, n_rows, n_cols, spikes, out32)
+    ref, absw = orc.event_csrmv(ip, ix, dat, w_homo, n_rows, n_cols, ev, orc.OUT_F64,
+                                with_abs=True)
+    err = np.abs(out32.cpu().numpy().astype(np.float64) - ref)
+    assert np.all(err <= 1e-5 * absw + 1e-30)
+
+
+def test_event_csrmv_accumulate_and_empty(bp, orc):
+    ip, ix, _ = inputs.random_csr(100, 64, 0.3, seed=1)
+    ev = inputs.spike_pattern(100, 0.2, 2)
+    out = torch.full((64,), 5 * 2 ** 32, dtype=torch.int64, device="cuda")
+    bp.event_csrmv(_t(ip), _t(ix), None, 1.5, 100, 64, _dev_spikes(ev), out, accumulate=True)
+    want = orc.event_csrmv(ip, ix, None, 1.5, 100, 64, ev, orc.OUT_FIX)
+    assert np.array_equal(out.cpu().numpy(), want + 5 * 2 ** 32)
+    # all-false events and n_rows = 0 leave a zeroed output
+    out.fill_(123)
+    bp.event_csrmv(_t(ip), _t(ix), None, 1.5, 100, 64,
+                   _dev_spikes(np.zeros(100, np.uint8)), out)
+    assert not out.any()
+    out.fill_(123)
+    bp.event_csrmv(_t(np.zeros(1, np.int64)), _t(np.zeros(1, np.int32)), None, 1.0,
+                   0, 64, _dev_spikes(np.zeros(1, np.uint8)), out)
+    assert not out.any()
+
+
+def test_event_csrmv_rejects_bad_arguments(bp):
+    out = torch.zeros(8, dtype=torch.float64, device="cuda")
+    with pytest.raises(bp.BpError):
+        bp.event_csrmv(_t(np.zeros(2, np.int64)), _t(np.zeros(1, np.int32)), None,
+                       1.0, 1, 8, _dev_spikes(np.ones(1, np.uint8)), out)
+    with pytest.raises(bp.BpError, match="WORKSPACE"):
+        bp.event_csrmv(_t(np.zeros(2, np.int64)), _t(np.zeros(1, np.int32)), None,
+                       1.0, 1, 8, _dev_spikes(np.ones(1, np.uint8)),
+                       torch.zeros(8, device="cuda"),
+                       ws=torch.zeros(16, dtype=torch.uint8, device="cuda"))
+
+
+# ------------------------------------------------------------------ a3 + a4
+JIT_CASES = [
+    # n_rows, n_cols, p, seg_len, density
+    (64, 37, 1.0, 0, 0.5),             # K = 1: dense rows
+    (500, 3000, 0.05, 0, 0.1),         # fan-out 150 > 128: two chunks
+    (300, 10_000, 0.1, 1000, 0.2),     # 10 segments
+    (1000, 100_000, 0.05, 0, 0.01),    # fan-out 5000 (config 2 row shape)
+    (4000, 4000, 0.02, 0, 0.01),       # COBA-4000 projection shape
+    (3, 2**20, 80 / 2**20, 0, 1.0),    # huge K = 26213
+]
+
+
+@pytest.mark.parametrize("case", JIT_CASES)
+@pytest.mark.parametrize("law", ["homo", "uniform", "normal"])
+def test_jitconn_event_mv(bp, orc, case, law):
+    n_rows, n_cols, p, seg_len, density = case
+    w0, w1 = {"homo": (0.6, 0.0), "uniform": (-0.1, 0.1), "normal": (0.0, 0.3)}[law]
+    seed = 0xC0FFEE + n_rows
+    K = orc.conn_len(p)
+    L = seg_len or n_cols
+    ospec = orc.JitSpec(seed, K, L, orc.LAWS[law], w0, w1)
+    spec = bp.jitconn_spec(seed, p, 0, seg_len)
+    ev = inputs.spike_pattern(n_rows, density, seed=9)
+    spikes = _dev_spikes(ev)
+    fn = {"homo": lambda o: bp.jitconn_event_mv_homo(spec, w0, spikes, n_rows, n_cols, o),
+          "uniform": lambda o: bp.jitconn_event_mv_uniform(spec, w0, w1, spikes, n_rows, n_cols, o),
+          "normal": lambda o: bp.jitconn_event_mv_normal(spec, w0, w1, spikes, n_rows, n_cols, o)}[law]
+    out = torch.zeros(n_cols, dtype=torch.int64, device="cuda")
+    fn(out)
+    want = orc.jit_event_mv(ospec, n_rows, n_cols, ev, out_kind=orc.OUT_FIX)
+    got = out.cpu().numpy()
+    if law == "normal":
+        # a 1-ulp weight difference moves a fixed-point sum by <= ulp(w) * 2^32
+        diff = np.abs(got - want)
+        assert np.mean(diff != 0) < 1e-3
+        assert np.all(diff <= 2 ** 32 * 2.0 ** -22 * (abs(w1) * 6 + 1))
+    else:
+        assert np.array_equal(got, want)
+    out32 = torch.zeros(n_cols, dtype=torch.float32, device="cuda")
+    fn(out32)
+    ref, absw = orc.jit_event_mv(ospec, n_rows, n_cols, ev, out_kind=orc.OUT_F64,
+                                 with_abs=True)
+    err = np.abs(out32.cpu().numpy().astype(np.float64) - ref)
+    assert np.all(err <= 1e-5 * absw + 1e-6 * (law == "normal") * absw + 1e-30)
+
+
+@pytest.mark.parametrize("bounds", [(0, 1000), (1000, 5000), (9000, 10_000), (2000, 2000)])
+def test_jitconn_partition(bp, orc, bounds):
+    n_rows, n_cols, L = 400, 10_000, 1000
+    cb, ce = bounds
+    spec = bp.jitconn_spec(77, 0.02, 0, L)
+    ospec = orc.JitSpec(77, orc.conn_len(0.02), L, orc.LAW_UNIFORM, -1.0, 1.0)
+    ev = inputs.spike_pattern(n_rows, 0.3, seed=4)
+    out = torch.zeros(ce - cb, dtype=torch.int64, device="cuda")
+    bp.jitconn_event_mv_uniform(spec, -1.0, 1.0, _dev_spikes(ev), n_rows, n_cols, out,
+                                col_begin=cb, col_end=ce)
+    want = orc.jit_event_mv(ospec, n_rows, n_cols, ev, cb, ce, orc.OUT_FIX)
+    assert np.array_equal(out.cpu().numpy(), want)
+
+
+def test_jitconn_rejects_unaligned_partition(bp):
+    spec = bp.jitconn_spec(1, 0.1, 0, 100)
+    out = torch.zeros(50, dtype=torch.float32, device="cuda")
+    with pytest.raises(bp.BpError, match="SHAPE"):
+        bp.jitconn_event_mv_homo(spec, 1.0, _dev_spikes(np.ones(10, np.uint8)), 10, 1000,
+                                 out, col_begin=50, col_end=100)
+    with pytest.raises(bp.BpError, match="INVALID"):
+        bp.jitconn_event_mv_homo(bp.jitconn_spec(1, 1.5), 1.0,
+                                 _dev_spikes(np.ones(10, np.uint8)), 10, 1000,
+                                 torch.zeros(1000, device="cuda"))
+
+
+@pytest.mark.parametrize("law", ["homo", "uniform", "normal"])
+@pytest.mark.parametrize("shape", [(200, 5000, 0.05, 0), (100, 4000, 0.1, 300), (50, 37, 1.0, 0)])
+def test_materialize_positions_bit_exact(bp, orc, law, shape):
+    """The kernel's generator yields exactly the oracle's positions (J4-J6)."""
+    n_rows, n_cols, p, seg_len = shape
+    w0, w1 = {"homo": (0.6, 0.0), "uniform": (-1.0, 1.0), "normal": (0.5, 2.0)}[law]
+    L = seg_len or n_cols
+    seed = 4242
+    ip, ix, dat = bp.jitconn_materialize(bp.jitconn_spec(seed, p, 0, seg_len), n_rows,
+                                         n_cols, law=orc.LAWS[law], w0=w0, w1=w1)
+    ip, ix, dat = ip.cpu().numpy(), ix.cpu().numpy(), dat.cpu().numpy()
+    ospec = orc.JitSpec(seed, orc.conn_len(p), L, orc.LAWS[law], w0, w1)
+    oip, oix, odat = orc.jit_materialize(ospec, n_rows, n_cols)
+    assert np.array_equal(ip, oip)
+    assert np.array_equal(ix, oix)
+    if law == "normal":
+        ulp = np.spacing(np.abs(odat).astype(np.float32))
+        assert np.all(np.abs(dat - odat) <= ulp)
+        assert np.mean(dat != odat) < 1e-3
+    else:
+        assert np.array_equal(dat.view(np.uint32), odat.view(np.uint32))
+
+
+# ------------------------------------------------------------------ a5 + a6
+def _rand_lif_state(n, fixed, seed):
+    rng = np.random.default_rng(seed)
+    v = rng.uniform(-70, -45, n).astype(np.float32)
+    if fixed:
+        ge = rng.integers(0, 5 * 2 ** 32, n).astype(np.int64)
+        gi = rng.integers(0, 40 * 2 ** 32, n).astype(np.int64)
+    else:
+        ge = rng.uniform(0, 5, n).astype(np.float32)
+        gi = rng.uniform(0, 40, n).astype(np.float32)
+    ref = rng.integers(0, 51, n).astype(np.uint8)
+    ref[rng.random(n) < 0.6] = 0
+    return dict(v=v, g_e=ge, g_i=gi, ref=ref)
+
+
+@pytest.mark.parametrize("n", [1, 33, 4000, 100_003])
+@pytest.mark.parametrize("fixed", [True, False])
+def test_lif_step_bit_exact(bp, orc, n, fixed):
+    st = _rand_lif_state(n, fixed, seed=n)
+    dev = {k: _t(a) for k, a in st.items()}
+    spikes = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+    active = torch.zeros(n, dtype=torch.int32, device="cuda")
+    count = torch.zeros(1, dtype=torch.int32, device="cuda")
+    params = bp.lif_params()
+    bp.neuron_step(params, dev, spikes, active, count, active_base=1000)
+    ev = orc.lif_step(orc.lif_params(), st["v"], st["g_e"], st["g_i"], st["ref"])
+    assert np.array_equal(dev["v"].cpu().numpy().view(np.uint32), st["v"].view(np.uint32))
+    assert np.array_equal(dev["ref"].cpu().numpy(), st["ref"])
+    assert np.array_equal(dev["g_e"].cpu().numpy().view(np.uint32 if not fixed else np.int64),
+                          st["g_e"].view(np.uint32 if not fixed else np.int64))
+    assert np.array_equal(dev["g_i"].cpu().numpy().view(np.uint32 if not fixed else np.int64),
+                          st["g_i"].view(np.uint32 if not fixed else np.int64))
+    got = inputs.unpack_bits(spikes.cpu().numpy().view(np.uint32), n)
+    assert np.array_equal(got, ev)
+    c = int(count.item())
+    assert np.array_equal(np.sort(active[:c].cpu().numpy()), np.nonzero(ev)[0] + 1000)
+
+
+@pytest.mark.parametrize("n", [1, 1000, 65_537])
+@pytest.mark.parametrize("fixed", [True, False])
+def test_hh_step_bit_exact(bp, orc, n, fixed):
+    rng = np.random.default_rng(n)
+    v = rng.uniform(-80, 40, n).astype(np.float32)
+    v[:3] = np.float32([-50.0, -48.0, -23.0])[: min(3, n)]     # rate singularities
+    m = rng.uniform(0, 1, n).astype(np.float32)
+    h = rng.uniform(0, 1, n).astype(np.float32)
+    nk = rng.uniform(0, 1, n).astype(np.float32)
+    if fixed:
+        ge = rng.integers(0, 50 * 2 ** 32, n).astype(np.int64)
+        gi = rng.integers(0, 300 * 2 ** 32, n).astype(np.int64)
+    else:
+        ge = rng.uniform(0, 50, n).astype(np.float32)
+        gi = rng.uniform(0, 300, n).astype(np.float32)
+    st = dict(v=v, m=m, h=h, n=nk, g_e=ge, g_i=gi)
+    dev = {k: _t(a) for k, a in st.items()}
+    spikes = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
+    for _ in range(3):
+        bp.neuron_step(bp.hh_params(), dev, spikes)
+        ev = orc.hh_step(orc.hh_params(), st["v"], st["m"], st["h"], st["n"], st["g_e"], st["g_i"])
+        for k in ("v", "m", "h", "n"):
+            assert np.array_equal(dev[k].cpu().numpy().view(np.uint32), st[k].view(np.uint32)), k
+        assert np.array_equal(inputs.unpack_bits(spikes.cpu().numpy().view(np.uint32), n), ev)
