@@ -136,12 +136,14 @@ def oracle_sample_steps(n_total: int, n_steps: int, fraction: float, seed: int =
         oracle.lif_step(params, v, g_e[:n_upd], g_i[:n_upd], ref)
     secs = time.perf_counter() - t0
     # events delivered (outside the timed region): fan-out of every active row
-    events = 0
-    for k in range(n_steps):
-        ev_e, ev_i = patterns[k % len(patterns)]
+    per_pattern = []
+    for ev_e, ev_i in patterns:
+        e = 0
         for spec, ev in ((je, ev_e), (ji, ev_i)):
             for r in np.nonzero(ev)[0]:
-                events += len(oracle.jit_row(spec, n_total, int(r))[0])
+                e += len(oracle.jit_row(spec, n_total, int(r))[0])
+        per_pattern.append(e)
+    events = sum(per_pattern[k % len(patterns)] for k in range(n_steps))
     return secs, events, n_upd * n_steps
 
 
