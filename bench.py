@@ -31,9 +31,14 @@ DT_MS = 0.1
 N_PER_GPU = 12_500_000
 METRIC = "synaptic events/sec & sim-sec per wall-sec, COBA E/I at 1/2/4/8 B200"
 UNIT = "synaptic events/s"
-# rule F1 state bytes per neuron per step for the LIF update (algorithmic):
-# V r+w (8) + g_E, g_I int64 r+w (32) + refractory counter r+w (2)
-LIF_BYTES_PER_NEURON = 42
+# algorithmic bytes of the fused step kernel (k_step): per neuron V r+w (8),
+# refractory counter r (1), g_E + g_I r+w (32 fixed point / 16 fp32); per
+# synaptic event one 4-byte bucket record written and read back (8); per
+# neuron 1/8 byte of spike bits.
+def step_bytes(n_local, events_per_step, fixed):
+    """k_step: state r+w + the 4-byte bucket record of every incoming event."""
+    per_neuron = 8 + 1 + (32 if fixed else 16) + 0.125
+    return per_neuron * n_local + 4 * events_per_step
 
 
 def _peaks():
@@ -262,7 +267,7 @@ def run_ours(args):
     # from pinned memory inside the timed region, every step's spike count
     # D2H into pinned memory (the step's population-rate result).
     e2e = None
-    if world == 1:
+    if world == 1 and not args.no_e2e:
         e2e = run_e2e(args, fixed, dev, net.state)
 
     if rank != 0:
@@ -276,16 +281,17 @@ def run_ours(args):
     if prof is not None:
         sc_ms, up_ms, nrec = prof
         upd_s = up_ms / 1e3 / max(nrec, 1)
-        bytes_per_launch = LIF_BYTES_PER_NEURON * n_local + n_local / 8
+        bytes_per_launch = step_bytes(n_local, events_total / args.steps, fixed)
         achieved = bytes_per_launch / upd_s / 1e9
-        roofline = {"kernel": "k_lif<fix64> (fused Expon+COBA+LIF update + spike compaction)",
+        roofline = {"kernel": "k_step<LIF,%s> (fused: bucket counts -> Expon+COBA+LIF -> "
+                              "spike bits + active list)" % ("fix64" if fixed else "f32"),
                     "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
                     "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                     "traffic": None, "peak_source": peak_kind,
                     "algorithmic_bytes_per_launch": bytes_per_launch,
                     "avg_launch_us": upd_s * 1e6,
                     "share_of_step": up_ms / (sc_ms + up_ms) if (sc_ms + up_ms) else None,
-                    "scatter_avg_us": sc_ms / 1e3 / max(nrec, 1) * 1e6}
+                    "bin_kernel_avg_us": sc_ms / 1e3 / max(nrec, 1) * 1e6}
     cpu = cpu_baseline(n_total) if (world == 1 and not args.no_cpu) else None
     clocks = clk.summary()
     line = {
@@ -358,6 +364,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--f32", action="store_true", help="fp32 conductances (fp32 atomics)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -252,9 +252,11 @@ bp_status bp_network_update(bp_network *net, uint32_t *raster_row,
 bp_status bp_network_counters(bp_network *net, uint64_t *host_out,
                               bp_stream stream);
 /* Per-kernel timing of the next bp_network_step calls (at most max_steps
- * steps): CUDA events are recorded on `stream` around every scatter and
- * neuron-update launch.  _end synchronises and returns the summed device
- * milliseconds of each kernel kind and the number of steps recorded. */
+ * steps): CUDA events are recorded on `stream` before the neuron-update
+ * kernel, between it and the event-binning kernel, and after the latter.
+ * _end synchronises and returns the summed device milliseconds of the
+ * update kernels (update_ms) and of the binning kernels (scatter_ms) and
+ * the number of steps recorded. */
 bp_status bp_network_profile_begin(bp_network *net, int64_t max_steps);
 bp_status bp_network_profile_end(bp_network *net, double *scatter_ms,
                                  double *update_ms, int64_t *steps);

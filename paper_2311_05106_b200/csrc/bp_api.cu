@@ -6,12 +6,14 @@
 #include <cstdarg>
 #include <new>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
 #include "../../include/bp.h"
 #include "neuron.cuh"
 #include "scatter.cuh"
+#include "step.cuh"
 
 namespace {
 
@@ -510,6 +512,14 @@ struct bp_network {
   // profiling: 3 events per step (before scatter, between, after update)
   cudaEvent_t *prof_ev = nullptr;
   int64_t prof_cap = 0, prof_used = 0;
+  float keep_frac = 0.f;          // L2 evict_last fraction of g (cache.cuh)
+  // fused-step event buckets (step.cuh), two parities, owned by the network
+  uint32_t n_tiles = 0, cap = 0;
+  bp::Buckets bk[2] = {};
+  void *bk_mem = nullptr;
+  int bpar = 0;                   // bucket parity holding the next step's input
+  int64_t steps_done = 0;
+  bp::ConnArgs conn{};
 };
 
 namespace {
@@ -551,46 +561,147 @@ bp_status validate_network(const bp_network_desc *d) {
   return BP_OK;
 }
 
-bp_status network_scatter_launch(bp_network *net, const int32_t *active,
-                                 const int32_t *count, int32_t *zero_count,
-                                 cudaStream_t st) {
+}  // namespace
+
+namespace {
+
+bp::ConnArgs make_conn(const bp_network *net) {
   const bp_network_desc &d = net->d;
-  const int grid_cap_items = static_cast<int>(d.n);
+  bp::ConnArgs c{};
+  c.conn = d.conn;
+  c.split = d.n_exc;
+  c.n_cols = static_cast<uint32_t>(d.n);
   if (d.conn == BP_CONN_JIT) {
-    bp::JitScatterArgs a{};
-    a.e = jit_side(&d.jit_exc, net->jr_e, BP_LAW_HOMO, d.w_exc, 0.f, d.col_begin,
-                   d.col_end, d.state.g_exc);
-    a.i = jit_side(&d.jit_inh, net->jr_i, BP_LAW_HOMO, d.w_inh, 0.f, d.col_begin,
-                   d.col_end, d.state.g_inh);
-    a.split = d.n_exc;
-    a.n_seg_max = a.e.n_seg > a.i.n_seg ? a.e.n_seg : a.i.n_seg;
-    a.n_cols = static_cast<uint32_t>(d.n);
-    a.col_begin = static_cast<uint32_t>(d.col_begin);
-    a.col_end = static_cast<uint32_t>(d.col_end);
-    a.active = active;
-    a.count = count;
-    a.zero_count = zero_count;
-    a.events = net->counters + 1;
-    a.spikes = net->counters;
-    launch_jit(a, BP_LAW_HOMO, d.g_kind,
-               grid_for_items(static_cast<int64_t>(grid_cap_items) * a.n_seg_max, net->sms), st);
+    c.je = jit_side(&d.jit_exc, net->jr_e, BP_LAW_HOMO, d.w_exc, 0.f, d.col_begin,
+                    d.col_end, d.state.g_exc);
+    c.ji = jit_side(&d.jit_inh, net->jr_i, BP_LAW_HOMO, d.w_inh, 0.f, d.col_begin,
+                    d.col_end, d.state.g_inh);
   } else {
-    bp::CsrScatterArgs a{};
-    a.e.indptr = d.exc_indptr; a.e.indices = d.exc_indices; a.e.data = d.exc_data;
-    a.e.w = d.w_exc; a.e.q = llrint(static_cast<double>(d.w_exc) * 4294967296.0);
-    a.e.out = d.state.g_exc;
-    a.i.indptr = d.inh_indptr; a.i.indices = d.inh_indices; a.i.data = d.inh_data;
-    a.i.w = d.w_inh; a.i.q = llrint(static_cast<double>(d.w_inh) * 4294967296.0);
-    a.i.out = d.state.g_inh;
-    a.split = d.n_exc;
-    a.active = active;
-    a.count = count;
-    a.zero_count = zero_count;
-    a.events = net->counters + 1;
-    a.spikes = net->counters;
-    launch_csr(a, d.g_kind, grid_for_items(grid_cap_items, net->sms), st);
+    c.ce.indptr = d.exc_indptr; c.ce.indices = d.exc_indices; c.ce.data = d.exc_data;
+    c.ci.indptr = d.inh_indptr; c.ci.indices = d.inh_indices; c.ci.data = d.inh_data;
   }
+  return c;
+}
+
+bp::BinTarget bin_target(const bp_network *net, int parity) {
+  bp::BinTarget b{};
+  b.out = net->bk[parity];
+  b.cap = net->cap;
+  b.n_local = static_cast<uint32_t>(net->n_local);
+  b.col_begin = static_cast<uint32_t>(net->d.col_begin);
+  return b;
+}
+
+// Mean events per postsynaptic neuron per presynaptic spike wave: fan-in.
+double fan_in_estimate(const bp_network *net, cudaStream_t st) {
+  const bp_network_desc &d = net->d;
+  if (d.conn == BP_CONN_JIT)
+    return static_cast<double>(d.n_exc) * 2.0 / (net->jr_e.K + 1.0) +
+           static_cast<double>(d.n - d.n_exc) * 2.0 / (net->jr_i.K + 1.0);
+  int64_t nnz_e = 0, nnz_i = 0;
+  if (d.n_exc > 0)
+    cudaMemcpyAsync(&nnz_e, d.exc_indptr + d.n_exc, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+  if (d.n > d.n_exc)
+    cudaMemcpyAsync(&nnz_i, d.inh_indptr + (d.n - d.n_exc), sizeof(int64_t),
+                    cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  return static_cast<double>(nnz_e + nnz_i) / static_cast<double>(net->n_local);
+}
+
+// Buckets sized for 5 % of the presynaptic neurons spiking in one step
+// (500 Hz at dt = 0.1 ms); more events spill exactly (step.cuh).
+bp_status alloc_buckets(bp_network *net, cudaStream_t st) {
+  net->n_tiles = static_cast<uint32_t>((net->n_local + bp::kTile - 1) / bp::kTile);
+  double expect = bp::kTile * fan_in_estimate(net, st) * 0.05;
+  uint32_t cap = static_cast<uint32_t>(round_up(static_cast<size_t>(expect) + 1024, 1024));
+  if (const char *env = std::getenv("BP_BUCKET_CAP")) cap = static_cast<uint32_t>(std::atoi(env));
+  if (cap < 1) cap = 1;
+  net->cap = cap;
+  const size_t cnt_b = round_up(static_cast<size_t>(net->n_tiles) * bp::kCntStride *
+                                    sizeof(int32_t), 256);
+  const size_t buf_b = round_up(static_cast<size_t>(net->n_tiles) * cap * sizeof(uint32_t), 256);
+  const size_t spill_b = round_up(2 * static_cast<size_t>(net->n_local) * sizeof(int32_t), 256);
+  const size_t per = 2 * cnt_b + buf_b + spill_b;     // cnt, flag, buf, spill
+  BP_CUDA(cudaMalloc(&net->bk_mem, 2 * per));
+  char *m = static_cast<char *>(net->bk_mem);
+  for (int p = 0; p < 2; ++p) {
+    char *b = m + p * per;
+    net->bk[p].cnt = reinterpret_cast<int32_t *>(b);
+    net->bk[p].flag = reinterpret_cast<int32_t *>(b + cnt_b);
+    net->bk[p].buf = reinterpret_cast<uint32_t *>(b + 2 * cnt_b);
+    net->bk[p].spill = reinterpret_cast<int32_t *>(b + 2 * cnt_b + buf_b);
+    BP_CUDA(cudaMemsetAsync(b, 0, 2 * cnt_b, st));
+    BP_CUDA(cudaMemsetAsync(net->bk[p].spill, 0, spill_b, st));
+  }
+  return BP_OK;
+}
+
+// Bin the events of the spikes in words [w_begin, w_end) of the global
+// vector (neurons [32 w_begin, min(32 w_end, n))) into bucket parity `par`.
+bp_status bin_spike_range(bp_network *net, int64_t w_begin, int64_t w_end, int par,
+                          cudaStream_t st) {
+  if (w_end <= w_begin) return BP_OK;
+  const int64_t first = w_begin * 32;
+  const int64_t last = w_end * 32 < net->d.n ? w_end * 32 : net->d.n;
+  if (last <= first) return BP_OK;
+  int32_t *active = net->active[0];
+  int32_t *count = net->count;
+  BP_CUDA(cudaMemsetAsync(count, 0, sizeof(int32_t), st));
+  bp::k_compact<<<grid_for_words(w_end - w_begin, net->sms), 256, 0, st>>>(
+      net->d.spikes + w_begin, last - first, active, count, static_cast<int32_t>(first));
+  bp_status s = launched();
+  if (s != BP_OK) return s;
+  bp::k_bin_rows<<<grid_for_items(last - first, net->sms), bp::kScatterThreads, 0, st>>>(
+      net->conn, bin_target(net, par), active, count, net->counters + 1);
   return launched();
+}
+
+bp_status launch_step(bp_network *net, uint32_t *raster, cudaStream_t st,
+                      int32_t *step_spikes = nullptr, cudaEvent_t mid = nullptr) {
+  const bp_network_desc &d = net->d;
+  bp::StepArgs a{};
+  a.nrn = net->neuron;
+  a.nrn.raster = raster;
+  a.nrn.active = nullptr;
+  a.model = d.model;
+  a.conn = net->conn;
+  a.w_e = d.w_exc;
+  a.w_i = d.w_inh;
+  a.q_e = llrint(static_cast<double>(d.w_exc) * 4294967296.0);
+  a.q_i = llrint(static_cast<double>(d.w_inh) * 4294967296.0);
+  a.in = net->bk[net->bpar];
+  a.out = bin_target(net, net->bpar ^ 1);
+  a.n_tiles = net->n_tiles;
+  a.reverse = static_cast<int>(net->steps_done & 1);
+  a.events = net->counters + 1;
+  a.spikes = net->counters;
+  a.step_spikes = step_spikes;
+  const int out_par = net->bpar ^ 1;
+  // ping-pong list counters: this step appends at count[2 + p] and zeroes
+  // count[2 + (p ^ 1)] for the next step (its reader finished last step)
+  const int cp = static_cast<int>(net->steps_done & 1);
+  a.active = net->active[1];
+  a.active_count = net->count + 2 + cp;
+  a.zero_count = net->count + 2 + (cp ^ 1);
+  const int grid = static_cast<int>(net->n_tiles);
+  if (d.model == BP_MODEL_LIF) {
+    if (d.g_kind == BP_OUT_FIX64) bp::k_step<0, 1><<<grid, bp::kStepThreads, 0, st>>>(a);
+    else bp::k_step<0, 0><<<grid, bp::kStepThreads, 0, st>>>(a);
+  } else {
+    if (d.g_kind == BP_OUT_FIX64) bp::k_step<1, 1><<<grid, bp::kStepThreads, 0, st>>>(a);
+    else bp::k_step<1, 0><<<grid, bp::kStepThreads, 0, st>>>(a);
+  }
+  bp_status s = launched();
+  if (s != BP_OK) return s;
+  if (mid) BP_CUDA(cudaEventRecord(mid, st));
+  bp::k_bin_rows<<<grid_for_items(net->n_local, net->sms), bp::kScatterThreads, 0, st>>>(
+      net->conn, bin_target(net, out_par), net->active[1], net->count + 2 + cp,
+      net->counters + 1);
+  s = launched();
+  if (s != BP_OK) return s;
+  net->bpar = out_par;
+  net->steps_done += 1;
+  return BP_OK;
 }
 
 }  // namespace
@@ -646,16 +757,39 @@ bp_status bp_network_create(const bp_network_desc *desc, bp_stream stream,
   net->parity = 0;
   cudaStream_t st = as_stream(stream);
   cudaError_t e = cudaMemsetAsync(ws, 0, 256, st);
-  if (e == cudaSuccess) {
-    launch_compact(desc->spikes, desc->n, net->active[0], net->count, sms, st);
-    e = cudaGetLastError();
-  }
   if (e != cudaSuccess) {
     delete net;
     return fail(BP_ERR_CUDA, "network init: %s", cudaGetErrorString(e));
   }
+  // L2 residency of g across steps: evict_last on the fraction of the g
+  // lines that fits ~72 % of the L2 (BP_L2_KEEP_MB overrides the budget;
+  // 0 disables the hints).
+  {
+    int dev = 0, l2 = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    double budget = 0.72 * static_cast<double>(l2);
+    if (const char *env = std::getenv("BP_L2_KEEP_MB")) budget = std::atof(env) * 1048576.0;
+    const double g_bytes = 2.0 * static_cast<double>(net->n_local) *
+                           (desc->g_kind == BP_OUT_FIX64 ? 8.0 : 4.0);
+    double f = g_bytes > 0 ? budget / g_bytes : 0.0;
+    if (f > 1.0) f = 1.0;
+    if (f < 0.0) f = 0.0;
+    net->keep_frac = static_cast<float>(f);
+    net->neuron.keep_frac = net->keep_frac;
+  }
   net->neuron.spikes = desc->spikes + desc->col_begin / 32;
   net->neuron.active_base = static_cast<int32_t>(desc->col_begin);
+  net->conn = make_conn(net);
+  s = alloc_buckets(net, st);
+  // the local part of the initial spike vector (spikes_{-1}) is delivered
+  // into the first step; remote parts arrive through bp_network_scatter
+  if (s == BP_OK)
+    s = bin_spike_range(net, desc->col_begin / 32, (desc->col_end + 31) / 32, net->bpar, st);
+  if (s != BP_OK) {
+    bp_network_destroy(net);
+    return s;
+  }
   *out = net;
   return BP_OK;
 }
@@ -667,27 +801,18 @@ bp_status bp_network_step(bp_network *net, int64_t n_steps, uint32_t *raster_out
   BP_CHECK(net != nullptr && n_steps >= 0, BP_ERR_INVALID_ARG, "bad net/n_steps");
   cudaStream_t st = as_stream(stream);
   for (int64_t k = 0; k < n_steps; ++k) {
-    const int cur = net->parity, nxt = cur ^ 1;
     cudaEvent_t *ev = nullptr;
     if (net->prof_ev && net->prof_used < net->prof_cap)
       ev = net->prof_ev + 3 * net->prof_used++;
+    if (counts_out) BP_CUDA(cudaMemsetAsync(net->count + 1, 0, sizeof(int32_t), st));
     if (ev) BP_CUDA(cudaEventRecord(ev[0], st));
-    s = network_scatter_launch(net, net->active[cur], net->count + cur,
-                               net->count + nxt, st);
-    if (s != BP_OK) return s;
-    if (ev) BP_CUDA(cudaEventRecord(ev[1], st));
-    bp::NeuronArgs a = net->neuron;
-    a.active = net->active[nxt];
-    a.count = net->count + nxt;
-    a.raster = raster_out ? raster_out + k * net->local_words : nullptr;
-    launch_neuron(a, net->d.model, net->d.g_kind, st);
-    s = launched();
+    s = launch_step(net, raster_out ? raster_out + k * net->local_words : nullptr, st,
+                    counts_out ? net->count + 1 : nullptr, ev ? ev[1] : nullptr);
     if (s != BP_OK) return s;
     if (ev) BP_CUDA(cudaEventRecord(ev[2], st));
     if (counts_out)
-      BP_CUDA(cudaMemcpyAsync(counts_out + k, net->count + nxt, sizeof(int32_t),
+      BP_CUDA(cudaMemcpyAsync(counts_out + k, net->count + 1, sizeof(int32_t),
                               cudaMemcpyDefault, st));
-    net->parity = nxt;
   }
   return BP_OK;
 }
@@ -717,8 +842,8 @@ bp_status bp_network_profile_end(bp_network *net, double *scatter_ms,
     if (e == cudaSuccess) e = cudaEventElapsedTime(&a, ev[0], ev[1]);
     if (e == cudaSuccess) e = cudaEventElapsedTime(&b, ev[1], ev[2]);
     if (e != cudaSuccess) s = fail(BP_ERR_CUDA, "profile: %s", cudaGetErrorString(e));
-    sc += a;
-    up += b;
+    up += a;   // neuron update (k_step)
+    sc += b;   // event regeneration + binning (k_bin_rows)
   }
   for (int64_t i = 0; i < 3 * net->prof_cap; ++i) cudaEventDestroy(net->prof_ev[i]);
   delete[] net->prof_ev;
@@ -735,26 +860,21 @@ bp_status bp_network_scatter(bp_network *net, bp_stream stream) {
   if (s != BP_OK) return s;
   BP_CHECK(net != nullptr, BP_ERR_INVALID_ARG, "net is NULL");
   cudaStream_t st = as_stream(stream);
-  // The spike vector may have been rewritten by an exchange: rebuild the
-  // active list of spikes_{n-1} from the global bit vector.
-  const int cur = net->parity;
-  BP_CUDA(cudaMemsetAsync(net->count + cur, 0, sizeof(int32_t), st));
-  launch_compact(net->d.spikes, net->d.n, net->active[cur], net->count + cur,
-                 net->sms, st);
-  s = launched();
+  // Deliver the spikes of the OTHER partitions (words outside this rank's
+  // slice) into the buckets the next bp_network_update consumes; local
+  // spikes were binned by the update that produced them.
+  const int64_t lw0 = net->d.col_begin / 32;
+  const int64_t lw1 = (net->d.col_end + 31) / 32;
+  s = bin_spike_range(net, 0, lw0, net->bpar, st);
   if (s != BP_OK) return s;
-  return network_scatter_launch(net, net->active[cur], net->count + cur, nullptr, st);
+  return bin_spike_range(net, lw1, net->global_words, net->bpar, st);
 }
 
 bp_status bp_network_update(bp_network *net, uint32_t *raster_row, bp_stream stream) {
   bp_status s = device_ready(nullptr);
   if (s != BP_OK) return s;
   BP_CHECK(net != nullptr, BP_ERR_INVALID_ARG, "net is NULL");
-  bp::NeuronArgs a = net->neuron;
-  a.active = nullptr;
-  a.raster = raster_row;
-  launch_neuron(a, net->d.model, net->d.g_kind, as_stream(stream));
-  return launched();
+  return launch_step(net, raster_row, as_stream(stream));
 }
 
 bp_status bp_network_counters(bp_network *net, uint64_t *host_out, bp_stream stream) {
@@ -769,6 +889,7 @@ bp_status bp_network_counters(bp_network *net, uint64_t *host_out, bp_stream str
 }
 
 void bp_network_destroy(bp_network *net) {
+  if (net && net->bk_mem) cudaFree(net->bk_mem);
   if (net && net->prof_ev) {
     for (int64_t i = 0; i < 3 * net->prof_cap; ++i) cudaEventDestroy(net->prof_ev[i]);
     delete[] net->prof_ev;

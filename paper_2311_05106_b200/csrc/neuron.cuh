@@ -12,6 +12,8 @@
 #pragma once
 #include <cstdint>
 
+#include "cache.cuh"
+
 namespace bp {
 
 struct NeuronArgs {
@@ -33,26 +35,28 @@ struct NeuronArgs {
   int32_t *active;       // nullable
   int32_t *count;
   int32_t active_base;
+  float keep_frac;       // L2 evict_last fraction for g (0: no hints)
 };
 
 template <int KIND>
-__device__ __forceinline__ float g_load(const void *g, int64_t i) {
+__device__ __forceinline__ float g_load(const void *g, int64_t i, uint64_t pol) {
   if (KIND == 1) {
-    const long long q = static_cast<const long long *>(g)[i];
+    const long long q = ld_s64(static_cast<const long long *>(g) + i, pol);
     return __double2float_rn(__dmul_rn(__ll2double_rn(q), 0x1p-32));
   }
-  return static_cast<const float *>(g)[i];
+  return ld_f32(static_cast<const float *>(g) + i, pol);
 }
 
+// g' = decay(g): fixed point llrint(g * alpha) in fp64 (rule F1), fp32 g * fl32(alpha).
 template <int KIND>
-__device__ __forceinline__ void g_decay(void *g, int64_t i, double a64,
-                                        float a32) {
+__device__ __forceinline__ void g_decay(void *g, int64_t i, double a64, float a32,
+                                        uint64_t pol) {
   if (KIND == 1) {
-    long long *q = static_cast<long long *>(g);
-    q[i] = __double2ll_rn(__dmul_rn(__ll2double_rn(q[i]), a64));
+    long long *q = static_cast<long long *>(g) + i;
+    st_s64(q, __double2ll_rn(__dmul_rn(__ll2double_rn(ld_s64(q, pol)), a64)), pol);
   } else {
-    float *f = static_cast<float *>(g);
-    f[i] = __fmul_rn(f[i], a32);
+    float *f = static_cast<float *>(g) + i;
+    st_f32(f, __fmul_rn(ld_f32(f, pol), a32), pol);
   }
 }
 
@@ -79,26 +83,47 @@ __device__ __forceinline__ void emit_spikes(const NeuronArgs &a, int64_t i,
 template <int KIND>
 __global__ void __launch_bounds__(256) k_lif(NeuronArgs a) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const Policies pol = make_policies(a.keep_frac);
   bool spike = false;
   if (i < a.n) {
-    const float V = a.v[i];
-    const float gE = g_load<KIND>(a.g_e, i);
-    const float gI = g_load<KIND>(a.g_i, i);
+    const float V = ld_f32(a.v + i, pol.stream);
+    const uint32_t ref = ld_u8(a.ref + i, pol.stream);
+    // g is read once and written once: load both, then store the decayed values
+    float gE, gI;
+    long long qE = 0, qI = 0;
+    float fE = 0.f, fI = 0.f;
+    if (KIND == 1) {
+      qE = ld_s64(static_cast<const long long *>(a.g_e) + i, pol.keep);
+      qI = ld_s64(static_cast<const long long *>(a.g_i) + i, pol.keep);
+      gE = __double2float_rn(__dmul_rn(__ll2double_rn(qE), 0x1p-32));
+      gI = __double2float_rn(__dmul_rn(__ll2double_rn(qI), 0x1p-32));
+    } else {
+      fE = ld_f32(static_cast<const float *>(a.g_e) + i, pol.keep);
+      fI = ld_f32(static_cast<const float *>(a.g_i) + i, pol.keep);
+      gE = fE;
+      gI = fI;
+    }
     const float I = __fmaf_rn(gI, a.e_inh - V, __fmaf_rn(gE, a.e_exc - V, a.i_ext));
     const float Vinf = __fmaf_rn(a.r, I, a.v_rest);
     const float Vc = __fmaf_rn(V - Vinf, a.alpha_v, Vinf);
-    const uint8_t ref = a.ref[i];
     if (ref > 0) {
-      a.ref[i] = static_cast<uint8_t>(ref - 1);   // hold V while refractory
-    } else if (Vc > a.v_th) {                     // strict '>'
-      a.v[i] = a.v_reset;
-      a.ref[i] = static_cast<uint8_t>(a.ref_steps);
+      st_u8(a.ref + i, ref - 1u, pol.stream);      // hold V while refractory
+    } else if (Vc > a.v_th) {                      // strict '>'
+      st_f32(a.v + i, a.v_reset, pol.stream);
+      st_u8(a.ref + i, static_cast<uint32_t>(a.ref_steps), pol.stream);
       spike = true;
     } else {
-      a.v[i] = Vc;
+      st_f32(a.v + i, Vc, pol.stream);
     }
-    g_decay<KIND>(a.g_e, i, a.alpha_e, a.alpha_e32);
-    g_decay<KIND>(a.g_i, i, a.alpha_i, a.alpha_i32);
+    if (KIND == 1) {
+      st_s64(static_cast<long long *>(a.g_e) + i,
+             __double2ll_rn(__dmul_rn(__ll2double_rn(qE), a.alpha_e)), pol.keep);
+      st_s64(static_cast<long long *>(a.g_i) + i,
+             __double2ll_rn(__dmul_rn(__ll2double_rn(qI), a.alpha_i)), pol.keep);
+    } else {
+      st_f32(static_cast<float *>(a.g_e) + i, __fmul_rn(fE, a.alpha_e32), pol.keep);
+      st_f32(static_cast<float *>(a.g_i) + i, __fmul_rn(fI, a.alpha_i32), pol.keep);
+    }
   }
   emit_spikes(a, i, spike);
 }
@@ -132,11 +157,12 @@ __device__ __forceinline__ float hh_efrac(float u, float k) {
 template <int KIND>
 __global__ void __launch_bounds__(256) k_hh(NeuronArgs a) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const Policies pol = make_policies(a.keep_frac);
   bool spike = false;
   if (i < a.n) {
     const float V = a.v[i], M = a.m[i], H = a.h[i], Nk = a.nk[i];
-    const float gE = g_load<KIND>(a.g_e, i);
-    const float gI = g_load<KIND>(a.g_i, i);
+    const float gE = g_load<KIND>(a.g_e, i, pol.keep);
+    const float gI = g_load<KIND>(a.g_i, i, pol.keep);
     const float x = V - a.v_t;
     const float am = 0.32f * hh_efrac(13.0f - x, 4.0f);
     const float bm = 0.28f * hh_efrac(x - 40.0f, 5.0f);
@@ -162,8 +188,8 @@ __global__ void __launch_bounds__(256) k_hh(NeuronArgs a) {
     a.m[i] = m_new;
     a.h[i] = h_new;
     a.nk[i] = n_new;
-    g_decay<KIND>(a.g_e, i, a.alpha_e, a.alpha_e32);
-    g_decay<KIND>(a.g_i, i, a.alpha_i, a.alpha_i32);
+    g_decay<KIND>(a.g_e, i, a.alpha_e, a.alpha_e32, pol.keep);
+    g_decay<KIND>(a.g_i, i, a.alpha_i, a.alpha_i32, pol.keep);
   }
   emit_spikes(a, i, spike);
 }

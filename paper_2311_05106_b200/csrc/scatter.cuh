@@ -14,18 +14,19 @@
 #pragma once
 #include <cstdint>
 
+#include "cache.cuh"
 #include "rng.cuh"
 
 namespace bp {
 
 constexpr int kScatterThreads = 256;
 
-__device__ __forceinline__ void add_f32(void *out, int64_t c, float w) {
-  atomicAdd(static_cast<float *>(out) + c, w);
+__device__ __forceinline__ void add_f32(void *out, int64_t c, float w, uint64_t pol) {
+  red_add_f32(static_cast<float *>(out) + c, w, pol);
 }
-__device__ __forceinline__ void add_fix(void *out, int64_t c, long long q) {
-  atomicAdd(reinterpret_cast<unsigned long long *>(out) + c,
-            static_cast<unsigned long long>(q));
+__device__ __forceinline__ void add_fix(void *out, int64_t c, long long q, uint64_t pol) {
+  red_add_u64(reinterpret_cast<unsigned long long *>(out) + c,
+              static_cast<unsigned long long>(q), pol);
 }
 
 // Block-wide sum of per-thread event counts, one atomic per block.
@@ -96,6 +97,7 @@ struct CsrScatterArgs {
   int32_t *zero_count;   // nullable; set to 0 by thread 0 (ping-pong list)
   unsigned long long *events;   // nullable
   unsigned long long *spikes;   // nullable; += *count once
+  float keep_frac;              // L2 evict_last fraction of the outputs (0: none)
 };
 
 // Field-wise select keeps the chosen projection in registers (a runtime
@@ -113,9 +115,10 @@ __device__ __forceinline__ CsrSide pick(bool second, const CsrSide &x,
 }
 
 template <int KIND>
-__device__ __forceinline__ void csr_emit(const CsrSide &s, int32_t c, float w) {
-  if (KIND == 0) add_f32(s.out, c, w);
-  else add_fix(s.out, c, s.data ? quantize(w) : s.q);
+__device__ __forceinline__ void csr_emit(const CsrSide &s, int32_t c, float w,
+                                         uint64_t pol) {
+  if (KIND == 0) add_f32(s.out, c, w, pol);
+  else add_fix(s.out, c, s.data ? quantize(w) : s.q, pol);
 }
 
 template <int KIND>
@@ -129,6 +132,7 @@ k_csr_scatter(CsrScatterArgs a) {
   const int lane = threadIdx.x & 31;
   const int warp0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int n_warps = (gridDim.x * blockDim.x) >> 5;
+  const uint64_t pol = make_policies(a.keep_frac).keep;
   unsigned long long ev = 0;
   for (int k = warp0; k < n_active; k += n_warps) {
     const int64_t r = a.active[k];
@@ -148,12 +152,12 @@ k_csr_scatter(CsrScatterArgs a) {
         w0 = __ldg(s.data + j); w1 = __ldg(s.data + j + 32);
         w2 = __ldg(s.data + j + 64); w3 = __ldg(s.data + j + 96);
       }
-      csr_emit<KIND>(s, c0, w0); csr_emit<KIND>(s, c1, w1);
-      csr_emit<KIND>(s, c2, w2); csr_emit<KIND>(s, c3, w3);
+      csr_emit<KIND>(s, c0, w0, pol); csr_emit<KIND>(s, c1, w1, pol);
+      csr_emit<KIND>(s, c2, w2, pol); csr_emit<KIND>(s, c3, w3, pol);
     }
     for (; j < end; j += 32) {
       const int32_t c = __ldg(s.indices + j);
-      csr_emit<KIND>(s, c, s.data ? __ldg(s.data + j) : s.w);
+      csr_emit<KIND>(s, c, s.data ? __ldg(s.data + j) : s.w, pol);
     }
   }
   count_events(a.events, ev);
@@ -179,6 +183,7 @@ struct JitScatterArgs {
   int32_t *zero_count;
   unsigned long long *events;
   unsigned long long *spikes;
+  float keep_frac;
 };
 
 __device__ __forceinline__ JitSide pick(bool second, const JitSide &x,
@@ -198,10 +203,10 @@ __device__ __forceinline__ JitSide pick(bool second, const JitSide &x,
 
 template <int LAW, int KIND>
 __device__ __forceinline__ void jit_emit(const JitSide &s, uint32_t pos,
-                                         uint32_t col_begin, float w) {
+                                         uint32_t col_begin, float w, uint64_t pol) {
   const int64_t c = static_cast<int64_t>(pos) - col_begin;
-  if (KIND == 0) add_f32(s.out, c, w);
-  else add_fix(s.out, c, LAW == 0 ? s.q : quantize(w));
+  if (KIND == 0) add_f32(s.out, c, w, pol);
+  else add_fix(s.out, c, LAW == 0 ? s.q : quantize(w), pol);
 }
 
 template <int LAW, int KIND>
@@ -216,6 +221,7 @@ k_jit_scatter(JitScatterArgs a) {
   const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   const int64_t n_items = static_cast<int64_t>(n_active) * a.n_seg_max;
+  const uint64_t pol = make_policies(a.keep_frac).keep;
   unsigned long long ev = 0;
   for (int64_t item = warp0; item < n_items; item += n_warps) {
     const int64_t r = a.active[item / a.n_seg_max];
@@ -227,11 +233,13 @@ k_jit_scatter(JitScatterArgs a) {
     const uint32_t seg = s.seg_first + sidx;
     const uint32_t seg_begin = seg * s.L;
     const uint32_t seg_end = min(seg_begin + s.L, a.n_cols);
+    // The first gap block does not depend on the first offset: issue both
+    // Philox evaluations back to back so their 10-round chains overlap.
+    u32x4 g = philox_block(s.seed, kTagGap, row, seg, lane);
     uint32_t start = seg_begin + first_offset(s.seed, s.K, row, seg);
     uint32_t chunk = 0;
     while (start < seg_end) {                      // warp-uniform
       const uint32_t blk = chunk * 32u + lane;
-      const u32x4 g = philox_block(s.seed, kTagGap, row, seg, blk);
       const uint32_t g0 = bounded(1u, s.K, g.x), g1 = bounded(1u, s.K, g.y);
       const uint32_t g2 = bounded(1u, s.K, g.z), g3 = bounded(1u, s.K, g.w);
       const uint32_t p1 = g0, p2 = g0 + g1, p3 = p2 + g2, t = p3 + g3;
@@ -263,13 +271,14 @@ k_jit_scatter(JitScatterArgs a) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           if (pos[k] < seg_end && pos[k] >= a.col_begin && pos[k] < a.col_end) {
-            jit_emit<LAW, KIND>(s, pos[k], a.col_begin, w[k]);
+            jit_emit<LAW, KIND>(s, pos[k], a.col_begin, w[k], pol);
             ++ev;
           }
         }
       }
       start += total;
       ++chunk;
+      if (start < seg_end) g = philox_block(s.seed, kTagGap, row, seg, chunk * 32u + lane);
     }
   }
   count_events(a.events, ev);
