@@ -576,6 +576,12 @@ bp::ConnArgs make_conn(const bp_network *net) {
                     d.col_end, d.state.g_exc);
     c.ji = jit_side(&d.jit_inh, net->jr_i, BP_LAW_HOMO, d.w_inh, 0.f, d.col_begin,
                     d.col_end, d.state.g_inh);
+    // expected events of one row in one segment: L * 2 / (K + 1)
+    const double fe = net->jr_e.L * 2.0 / (net->jr_e.K + 1.0);
+    const double fi = net->jr_i.L * 2.0 / (net->jr_i.K + 1.0);
+    // one lane per row only on request: measured slower at 186 rows per SM
+    // (too few warps to hide the Philox chain latency), see DESIGN.md
+    c.lane_rows = (fe <= 512.0 && fi <= 512.0 && std::getenv("BP_BIN_LANE_ROWS")) ? 1 : 0;
   } else {
     c.ce.indptr = d.exc_indptr; c.ce.indices = d.exc_indices; c.ce.data = d.exc_data;
     c.ci.indptr = d.inh_indptr; c.ci.indices = d.inh_indices; c.ci.data = d.inh_data;
@@ -636,6 +642,27 @@ bp_status alloc_buckets(bp_network *net, cudaStream_t st) {
   return BP_OK;
 }
 
+// Bin the rows active[0..*count) into bucket parity `par`: block-aggregated
+// when the tile table fits in shared memory, else one atomic per event.
+bp_status launch_bin(bp_network *net, const int32_t *active, const int32_t *count, int par,
+                     int64_t max_rows, cudaStream_t st) {
+  const size_t smem = (2 * static_cast<size_t>(bp::kBinStage) + 2 * net->n_tiles) * 4;
+  if (net->n_tiles <= 8192 && smem <= 200 * 1024 && !std::getenv("BP_BIN_PER_EVENT")) {
+    static bool attr_set = false;
+    if (!attr_set) {
+      BP_CUDA(cudaFuncSetAttribute(bp::k_bin_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   200 * 1024));
+      attr_set = true;
+    }
+    bp::k_bin_sorted<<<net->sms, bp::kBinThreads, smem, st>>>(
+        net->conn, bin_target(net, par), active, count, net->counters + 1, net->n_tiles);
+  } else {
+    bp::k_bin_rows<<<grid_for_items(max_rows, net->sms), bp::kScatterThreads, 0, st>>>(
+        net->conn, bin_target(net, par), active, count, net->counters + 1);
+  }
+  return launched();
+}
+
 // Bin the events of the spikes in words [w_begin, w_end) of the global
 // vector (neurons [32 w_begin, min(32 w_end, n))) into bucket parity `par`.
 bp_status bin_spike_range(bp_network *net, int64_t w_begin, int64_t w_end, int par,
@@ -651,9 +678,7 @@ bp_status bin_spike_range(bp_network *net, int64_t w_begin, int64_t w_end, int p
       net->d.spikes + w_begin, last - first, active, count, static_cast<int32_t>(first));
   bp_status s = launched();
   if (s != BP_OK) return s;
-  bp::k_bin_rows<<<grid_for_items(last - first, net->sms), bp::kScatterThreads, 0, st>>>(
-      net->conn, bin_target(net, par), active, count, net->counters + 1);
-  return launched();
+  return launch_bin(net, active, count, par, last - first, st);
 }
 
 bp_status launch_step(bp_network *net, uint32_t *raster, cudaStream_t st,
@@ -694,10 +719,7 @@ bp_status launch_step(bp_network *net, uint32_t *raster, cudaStream_t st,
   bp_status s = launched();
   if (s != BP_OK) return s;
   if (mid) BP_CUDA(cudaEventRecord(mid, st));
-  bp::k_bin_rows<<<grid_for_items(net->n_local, net->sms), bp::kScatterThreads, 0, st>>>(
-      net->conn, bin_target(net, out_par), net->active[1], net->count + 2 + cp,
-      net->counters + 1);
-  s = launched();
+  s = launch_bin(net, net->active[1], net->count + 2 + cp, out_par, net->n_local, st);
   if (s != BP_OK) return s;
   net->bpar = out_par;
   net->steps_done += 1;

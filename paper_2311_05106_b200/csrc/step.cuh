@@ -87,6 +87,7 @@ struct ConnArgs {
   CsrSide ce, ci;           // CSR: column-sliced rows, indices local
   int64_t split;            // n_exc: rows >= split belong to projection I
   uint32_t n_cols;          // all neurons (columns of both projections)
+  int lane_rows;            // JIT fan-out per segment small: one lane per row
 };
 
 // Regenerate (JIT) or read (CSR) the local targets of presynaptic neuron r
@@ -284,6 +285,168 @@ __device__ __forceinline__ void st4(float *p, const float *v, uint64_t pol) {
 }
 
 // ---------------------------------------------------------------- kernel
+// The state of 4 consecutive neurons (one thread, one pass of 1024).
+template <int MODEL, int KIND>
+struct Pass {
+  bool full;            // all 4 neurons exist (else the scalar tail path)
+  float4 V;
+  uint32_t R;           // LIF refractory counters, 4 x u8
+  float4 M, H, N;       // HH gates
+  GVec<KIND> ge, gi;
+};
+
+template <int MODEL, int KIND>
+__device__ __forceinline__ void pass_load(Pass<MODEL, KIND> &p, const NeuronArgs &nr,
+                                          int64_t i0, const Policies &pol) {
+  p.full = i0 + 4 <= nr.n;
+  if (!p.full) return;
+  p.ge.load(nr.g_e, i0, pol.keep);
+  p.gi.load(nr.g_i, i0, pol.keep);
+  p.V = ld4(nr.v + i0, pol.stream);
+  if constexpr (MODEL == 0) {
+    asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;"
+                 : "=r"(p.R) : "l"(nr.ref + i0), "l"(pol.stream));
+  } else {
+    p.M = ld4(nr.m + i0, pol.stream);
+    p.H = ld4(nr.h + i0, pol.stream);
+    p.N = ld4(nr.nk + i0, pol.stream);
+  }
+}
+
+// Update the 4 neurons of pass p (offset j0 in the tile, local index i0);
+// returns their spike nibble.
+template <int MODEL, int KIND>
+__device__ __forceinline__ uint32_t pass_update(Pass<MODEL, KIND> &p, const StepArgs &a,
+                                                const int32_t *cnt_e, const int32_t *cnt_i,
+                                                int j0, int64_t i0, const Policies &pol) {
+  const NeuronArgs &nr = a.nrn;
+  uint32_t nib = 0;
+  if (i0 >= nr.n) return 0;
+  if (p.full) {
+    float gEf[4], gIf[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if constexpr (KIND == 1) {
+        gEf[q] = g_fold(p.ge.v[q], cnt_e[j0 + q], a.q_e);
+        gIf[q] = g_fold(p.gi.v[q], cnt_i[j0 + q], a.q_i);
+      } else {
+        gEf[q] = g_fold(p.ge.v[q], cnt_e[j0 + q], a.w_e);
+        gIf[q] = g_fold(p.gi.v[q], cnt_i[j0 + q], a.w_i);
+      }
+      g_after(p.ge.v[q], nr.alpha_e, nr.alpha_e32);
+      g_after(p.gi.v[q], nr.alpha_i, nr.alpha_i32);
+    }
+    float V[4] = {p.V.x, p.V.y, p.V.z, p.V.w};
+    if constexpr (MODEL == 0) {
+      uint32_t Rn = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t r = (p.R >> (8 * q)) & 0xFFu;
+        if (lif_one(nr, V[q], r, gEf[q], gIf[q])) nib |= 1u << q;
+        Rn |= r << (8 * q);
+      }
+      if (Rn != p.R)
+        asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;"
+                     ::"l"(nr.ref + i0), "r"(Rn), "l"(pol.stream) : "memory");
+    } else {
+      float M[4] = {p.M.x, p.M.y, p.M.z, p.M.w}, H[4] = {p.H.x, p.H.y, p.H.z, p.H.w};
+      float Nn[4] = {p.N.x, p.N.y, p.N.z, p.N.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (hh_one(nr, V[q], M[q], H[q], Nn[q], gEf[q], gIf[q])) nib |= 1u << q;
+      st4(nr.m + i0, M, pol.stream);
+      st4(nr.h + i0, H, pol.stream);
+      st4(nr.nk + i0, Nn, pol.stream);
+    }
+    st4(nr.v + i0, V, pol.stream);
+    p.ge.store(nr.g_e, i0, pol.keep);
+    p.gi.store(nr.g_i, i0, pol.keep);
+    return nib;
+  }
+  // ragged tail of the last tile: scalar path
+  for (int q = 0; q < 4 && i0 + q < nr.n; ++q) {
+    const int64_t i = i0 + q;
+    float gEf, gIf;
+    if constexpr (KIND == 1) {
+      long long *pe = static_cast<long long *>(nr.g_e) + i;
+      long long *pi = static_cast<long long *>(nr.g_i) + i;
+      long long ge = *pe, gi = *pi;
+      gEf = g_fold(ge, cnt_e[j0 + q], a.q_e);
+      gIf = g_fold(gi, cnt_i[j0 + q], a.q_i);
+      g_after(ge, nr.alpha_e, 0.f);
+      g_after(gi, nr.alpha_i, 0.f);
+      *pe = ge;
+      *pi = gi;
+    } else {
+      float *pe = static_cast<float *>(nr.g_e) + i;
+      float *pi = static_cast<float *>(nr.g_i) + i;
+      float ge = *pe, gi = *pi;
+      gEf = g_fold(ge, cnt_e[j0 + q], a.w_e);
+      gIf = g_fold(gi, cnt_i[j0 + q], a.w_i);
+      g_after(ge, 0.0, nr.alpha_e32);
+      g_after(gi, 0.0, nr.alpha_i32);
+      *pe = ge;
+      *pi = gi;
+    }
+    float V = nr.v[i];
+    if constexpr (MODEL == 0) {
+      uint32_t r = nr.ref[i];
+      if (lif_one(nr, V, r, gEf, gIf)) nib |= 1u << q;
+      nr.ref[i] = static_cast<uint8_t>(r);
+    } else {
+      float M = nr.m[i], H = nr.h[i], Nk = nr.nk[i];
+      if (hh_one(nr, V, M, H, Nk, gEf, gIf)) nib |= 1u << q;
+      nr.m[i] = M;
+      nr.h[i] = H;
+      nr.nk[i] = Nk;
+    }
+    nr.v[i] = V;
+  }
+  return nib;
+}
+
+// Spike words of one pass (lanes 8w..8w+7 hold the 32 neurons of word w)
+// and the active-list append (one atomic per warp with spikes).
+__device__ __forceinline__ void pass_emit(const StepArgs &a, uint32_t nib, int64_t base,
+                                          int pass, uint32_t &my_sp) {
+  const NeuronArgs &nr = a.nrn;
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint32_t word = nib << (4u * (lane & 7u));
+  word |= __shfl_xor_sync(0xffffffffu, word, 1);
+  word |= __shfl_xor_sync(0xffffffffu, word, 2);
+  word |= __shfl_xor_sync(0xffffffffu, word, 4);
+  const int64_t wi = (base + pass * 1024 + warp * 128) / 32 + (lane >> 3);
+  if ((lane & 7u) == 0 && wi * 32 < nr.n) {
+    nr.spikes[wi] = word;
+    if (nr.raster) nr.raster[wi] = word;
+  }
+  const uint32_t c = __popc(nib);
+  my_sp += c;
+  const uint32_t warp_sp = __reduce_add_sync(0xffffffffu, c);
+  if (warp_sp) {
+    uint32_t incl = c;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= static_cast<uint32_t>(off)) incl += v;
+    }
+    int slot = 0;
+    if (lane == 0) slot = atomicAdd(a.active_count, static_cast<int>(warp_sp));
+    slot = __shfl_sync(0xffffffffu, slot, 0) + static_cast<int>(incl - c);
+    const int64_t i0 = base + pass * 1024 + 4 * static_cast<int64_t>(threadIdx.x);
+    uint32_t bits = nib;
+    while (bits) {
+      const int q = __ffs(bits) - 1;
+      bits &= bits - 1u;
+      a.active[slot++] = nr.active_base + static_cast<int32_t>(i0 + q);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- kernel
+// The first two passes' state loads are issued before the bucket-counting
+// phase so their DRAM latency overlaps it; passes 2 and 3 are loaded while
+// 0 and 1 compute (register double buffering).
 template <int MODEL, int KIND>
 __global__ void __launch_bounds__(kStepThreads)
 k_step(StepArgs a) {
@@ -291,11 +454,15 @@ k_step(StepArgs a) {
   __shared__ int32_t cnt_i[kTile];
   __shared__ unsigned long long block_sp;
   const int tid = threadIdx.x;
-  const uint32_t lane = tid & 31u, warp = tid >> 5;
+  const uint32_t lane = tid & 31u;
   const uint32_t tile = a.reverse ? a.n_tiles - 1u - blockIdx.x : blockIdx.x;
   const int64_t base = static_cast<int64_t>(tile) << kTileShift;
   const NeuronArgs &nr = a.nrn;
   const Policies pol = make_policies(nr.keep_frac);
+
+  Pass<MODEL, KIND> pa, pb;
+  pass_load(pa, nr, base + 4 * tid, pol);
+  pass_load(pb, nr, base + 1024 + 4 * tid, pol);
 
   // 1. count this tile's incoming events (bucket + rare spill)
   for (int j = tid; j < kTile; j += kStepThreads) { cnt_e[j] = 0; cnt_i[j] = 0; }
@@ -326,136 +493,24 @@ k_step(StepArgs a) {
 
   // 2. update the tile: 4 passes of 1024 neurons, 4 consecutive per thread
   uint32_t my_sp = 0;
-  for (int pass = 0; pass < kTile / 1024; ++pass) {
-    const int j0 = pass * 1024 + 4 * tid;               // offset in tile
-    const int64_t i0 = base + j0;                        // local neuron
-    uint32_t nib = 0;
-    if (i0 < nr.n) {
-      if (i0 + 4 <= nr.n) {
-        GVec<KIND> ge, gi;
-        ge.load(nr.g_e, i0, pol.keep);
-        gi.load(nr.g_i, i0, pol.keep);
-        float gEf[4], gIf[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if constexpr (KIND == 1) {
-            gEf[q] = g_fold(reinterpret_cast<long long &>(ge.v[q]), cnt_e[j0 + q], a.q_e);
-            gIf[q] = g_fold(reinterpret_cast<long long &>(gi.v[q]), cnt_i[j0 + q], a.q_i);
-          } else {
-            gEf[q] = g_fold(reinterpret_cast<float &>(ge.v[q]), cnt_e[j0 + q], a.w_e);
-            gIf[q] = g_fold(reinterpret_cast<float &>(gi.v[q]), cnt_i[j0 + q], a.w_i);
-          }
-          g_after(ge.v[q], nr.alpha_e, nr.alpha_e32);
-          g_after(gi.v[q], nr.alpha_i, nr.alpha_i32);
-        }
-        const float4 V4 = ld4(nr.v + i0, pol.stream);
-        float V[4] = {V4.x, V4.y, V4.z, V4.w};
-        if constexpr (MODEL == 0) {
-          uint32_t R4;
-          asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;"
-                       : "=r"(R4) : "l"(nr.ref + i0), "l"(pol.stream));
-          uint32_t Rn = 0;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint32_t r = (R4 >> (8 * q)) & 0xFFu;
-            if (lif_one(nr, V[q], r, gEf[q], gIf[q])) nib |= 1u << q;
-            Rn |= r << (8 * q);
-          }
-          if (Rn != R4)
-            asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;"
-                         ::"l"(nr.ref + i0), "r"(Rn), "l"(pol.stream) : "memory");
-        } else {
-          const float4 M4 = ld4(nr.m + i0, pol.stream), H4 = ld4(nr.h + i0, pol.stream);
-          const float4 N4 = ld4(nr.nk + i0, pol.stream);
-          float M[4] = {M4.x, M4.y, M4.z, M4.w}, H[4] = {H4.x, H4.y, H4.z, H4.w};
-          float Nn[4] = {N4.x, N4.y, N4.z, N4.w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (hh_one(nr, V[q], M[q], H[q], Nn[q], gEf[q], gIf[q])) nib |= 1u << q;
-          st4(nr.m + i0, M, pol.stream);
-          st4(nr.h + i0, H, pol.stream);
-          st4(nr.nk + i0, Nn, pol.stream);
-        }
-        st4(nr.v + i0, V, pol.stream);
-        ge.store(nr.g_e, i0, pol.keep);
-        gi.store(nr.g_i, i0, pol.keep);
-      } else {
-        // ragged tail of the last tile: scalar path
-        for (int q = 0; q < 4 && i0 + q < nr.n; ++q) {
-          const int64_t i = i0 + q;
-          float gEf, gIf;
-          if constexpr (KIND == 1) {
-            long long *pe = static_cast<long long *>(nr.g_e) + i;
-            long long *pi = static_cast<long long *>(nr.g_i) + i;
-            long long ge = *pe, gi = *pi;
-            gEf = g_fold(ge, cnt_e[j0 + q], a.q_e);
-            gIf = g_fold(gi, cnt_i[j0 + q], a.q_i);
-            g_after(ge, nr.alpha_e, 0.f); g_after(gi, nr.alpha_i, 0.f);
-            *pe = ge; *pi = gi;
-          } else {
-            float *pe = static_cast<float *>(nr.g_e) + i;
-            float *pi = static_cast<float *>(nr.g_i) + i;
-            float ge = *pe, gi = *pi;
-            gEf = g_fold(ge, cnt_e[j0 + q], a.w_e);
-            gIf = g_fold(gi, cnt_i[j0 + q], a.w_i);
-            g_after(ge, 0.0, nr.alpha_e32); g_after(gi, 0.0, nr.alpha_i32);
-            *pe = ge; *pi = gi;
-          }
-          float V = nr.v[i];
-          if constexpr (MODEL == 0) {
-            uint32_t r = nr.ref[i];
-            if (lif_one(nr, V, r, gEf, gIf)) nib |= 1u << q;
-            nr.ref[i] = static_cast<uint8_t>(r);
-          } else {
-            float M = nr.m[i], H = nr.h[i], Nk = nr.nk[i];
-            if (hh_one(nr, V, M, H, Nk, gEf, gIf)) nib |= 1u << q;
-            nr.m[i] = M; nr.h[i] = H; nr.nk[i] = Nk;
-          }
-          nr.v[i] = V;
-        }
-      }
-    }
-    // 3. spike words: lanes 8w..8w+7 of this warp hold the 32 neurons of word w
-    uint32_t word = nib << (4u * (lane & 7u));
-    word |= __shfl_xor_sync(0xffffffffu, word, 1);
-    word |= __shfl_xor_sync(0xffffffffu, word, 2);
-    word |= __shfl_xor_sync(0xffffffffu, word, 4);
-    const int64_t wi = (base + pass * 1024 + warp * 128) / 32 + (lane >> 3);
-    if ((lane & 7u) == 0 && wi * 32 < nr.n) {
-      nr.spikes[wi] = word;
-      if (nr.raster) nr.raster[wi] = word;
-    }
-    my_sp += __popc(nib);
-    // 4. append the new spikes to the active list (one atomic per warp);
-    //    k_bin_rows regenerates their rows and bins the events
-    const uint32_t warp_sp = __reduce_add_sync(0xffffffffu, __popc(nib));
-    if (warp_sp) {
-      uint32_t incl = __popc(nib);
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= static_cast<uint32_t>(off)) incl += v;
-      }
-      int slot = 0;
-      if (lane == 0) slot = atomicAdd(a.active_count, static_cast<int>(warp_sp));
-      slot = __shfl_sync(0xffffffffu, slot, 0) + static_cast<int>(incl - __popc(nib));
-      uint32_t bits = nib;
-      while (bits) {
-        const int q = __ffs(bits) - 1;
-        bits &= bits - 1u;
-        a.active[slot++] = nr.active_base + static_cast<int32_t>(i0 + q);
-      }
-    }
-  }
-  // 5. counters
+  uint32_t nib = pass_update(pa, a, cnt_e, cnt_i, 4 * tid, base + 4 * tid, pol);
+  pass_load(pa, nr, base + 2048 + 4 * tid, pol);
+  pass_emit(a, nib, base, 0, my_sp);
+  nib = pass_update(pb, a, cnt_e, cnt_i, 1024 + 4 * tid, base + 1024 + 4 * tid, pol);
+  pass_load(pb, nr, base + 3072 + 4 * tid, pol);
+  pass_emit(a, nib, base, 1, my_sp);
+  nib = pass_update(pa, a, cnt_e, cnt_i, 2048 + 4 * tid, base + 2048 + 4 * tid, pol);
+  pass_emit(a, nib, base, 2, my_sp);
+  nib = pass_update(pb, a, cnt_e, cnt_i, 3072 + 4 * tid, base + 3072 + 4 * tid, pol);
+  pass_emit(a, nib, base, 3, my_sp);
+
+  // 3. counters
   my_sp = __reduce_add_sync(0xffffffffu, my_sp);
   if (lane == 0 && my_sp) atomicAdd(&block_sp, static_cast<unsigned long long>(my_sp));
   __syncthreads();
-  if (tid == 0) {
-    if (block_sp) {
-      atomicAdd(a.spikes, block_sp);
-      if (a.step_spikes) atomicAdd(a.step_spikes, static_cast<int32_t>(block_sp));
-    }
+  if (tid == 0 && block_sp) {
+    atomicAdd(a.spikes, block_sp);
+    if (a.step_spikes) atomicAdd(a.step_spikes, static_cast<int32_t>(block_sp));
   }
 }
 
@@ -470,6 +525,352 @@ k_bin_rows(ConnArgs conn, BinTarget out, const int32_t *active, const int32_t *c
   unsigned long long ev = 0;
   for (int64_t k = warp0; k < n_active; k += n_warps) ev += deliver_row(conn, out, active[k]);
   count_events(events, ev);
+}
+
+// ---------------------------------------------------------------------------
+// Block-aggregated binning (one 1024-thread block per SM).  A block's share
+// of the active rows is regenerated into shared memory, counting-sorted by
+// tile there, and then each non-empty tile costs ONE global slot-claiming
+// atomic per block and its records leave as a contiguous run -- ~5x fewer L2
+// atomics and sectors than one atomic + one 4-byte store per event.
+// Events that do not fit the shared staging area take the per-event path.
+constexpr int kBinThreads = 1024;
+constexpr int kBinStage = 12288;          // staged records per block
+
+__device__ __forceinline__ uint32_t stage_record(uint32_t proj, uint32_t loc) {
+  return (proj ? kProjBit : 0u) | loc;    // loc < 2^31
+}
+
+// Generate the local targets of row r into the block's staging area (or the
+// global per-event path when it is full).  Whole warp, warp-uniform r.
+__device__ __forceinline__ uint32_t stage_row(const ConnArgs &c, const BinTarget &b, int64_t r,
+                                              uint32_t *staged, int32_t *n_staged,
+                                              int32_t *hist) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const bool inh = r >= c.split;
+  const uint32_t proj = inh ? 1u : 0u;
+  const int64_t row64 = inh ? r - c.split : r;
+  uint32_t ev = 0;
+  // emit up to 4 locs per lane (valid[k]) through one warp-wide slot claim
+  auto emit = [&](const uint32_t *loc, const bool *valid) {
+    uint32_t mine = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) mine += valid[k];
+    uint32_t incl = mine;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= static_cast<uint32_t>(off)) incl += v;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) return;
+    int base = 0;
+    if (lane == 31) base = atomicAdd(n_staged, static_cast<int>(total));
+    base = __shfl_sync(0xffffffffu, base, 31);
+    int slot = base + static_cast<int>(incl - mine);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (!valid[k]) continue;
+      if (slot < kBinStage) {
+        staged[slot] = stage_record(proj, loc[k]);
+        atomicAdd(hist + (loc[k] >> kTileShift), 1);
+      } else {
+        bin_event(b, proj, loc[k]);
+      }
+      ++slot;
+      ++ev;
+    }
+  };
+  if (c.conn == 1) {
+    const CsrSide s = pick(inh, c.ce, c.ci);
+    const int64_t begin = __ldg(s.indptr + row64), end = __ldg(s.indptr + row64 + 1);
+    for (int64_t j0 = begin; j0 < end; j0 += 128) {
+      uint32_t loc[4];
+      bool valid[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t j = j0 + k * 32 + lane;
+        valid[k] = j < end;
+        loc[k] = valid[k] ? static_cast<uint32_t>(__ldg(s.indices + j)) : 0u;
+      }
+      emit(loc, valid);
+    }
+    return ev;
+  }
+  const JitSide s = pick(inh, c.je, c.ji);
+  const uint32_t row = static_cast<uint32_t>(row64);
+  for (uint32_t sidx = 0; sidx < s.n_seg; ++sidx) {
+    const uint32_t seg = s.seg_first + sidx;
+    const uint32_t seg_begin = seg * s.L;
+    const uint32_t seg_end = min(seg_begin + s.L, c.n_cols);
+    u32x4 g = philox_block(s.seed, kTagGap, row, seg, lane);
+    uint32_t start = seg_begin + first_offset(s.seed, s.K, row, seg);
+    uint32_t chunk = 0;
+    while (start < seg_end) {                      // warp-uniform
+      const uint32_t g0 = bounded(1u, s.K, g.x), g1 = bounded(1u, s.K, g.y);
+      const uint32_t g2 = bounded(1u, s.K, g.z), g3 = bounded(1u, s.K, g.w);
+      const uint32_t p1 = g0, p2 = g0 + g1, p3 = p2 + g2, t = p3 + g3;
+      uint32_t incl = t;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= static_cast<uint32_t>(off)) incl += v;
+      }
+      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      const uint32_t pos0 = start + (incl - t);
+      const uint32_t pos[4] = {pos0, pos0 + p1, pos0 + p2, pos0 + p3};
+      uint32_t loc[4];
+      bool valid[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        valid[k] = pos[k] < seg_end;
+        loc[k] = pos[k] - b.col_begin;
+      }
+      emit(loc, valid);
+      start += total;
+      ++chunk;
+      if (start < seg_end) g = philox_block(s.seed, kTagGap, row, seg, chunk * 32u + lane);
+    }
+  }
+  return ev;
+}
+
+// JIT rows active[k0 + 32 i] (i < 32, k0 + 32 i < k_end) for one warp.  Lane l first
+// computes the stationary first offset of row k0+l (one Philox per lane
+// instead of one per row), then the warp walks the rows one by one: one
+// Philox block of 4 gaps per lane per chunk of 128 gaps.  Positions grow
+// with (lane, k), so the valid events are a prefix of that order and their
+// staging slots follow from four ballots -- no second scan.
+__device__ __forceinline__ uint32_t stage_rows_jit(const ConnArgs &c, const BinTarget &b,
+                                                   const int32_t *active, int k0, int k_end,
+                                                   uint32_t *staged, int32_t *n_staged,
+                                                   int32_t *hist) {
+  const uint32_t lane = threadIdx.x & 31u;
+  // rows k0, k0 + 32, k0 + 64, ... (stride = warps per block)
+  const int nrows = min(32, (k_end - k0 + 31) / 32);
+  const int64_t r_l = lane < static_cast<uint32_t>(nrows) ? active[k0 + 32 * lane] : 0;
+  const bool inh_l = r_l >= c.split;
+  const uint32_t row_l = static_cast<uint32_t>(inh_l ? r_l - c.split : r_l);
+  const uint32_t n_seg_max = max(c.je.n_seg, c.ji.n_seg);
+  uint32_t ev = 0;
+  for (uint32_t sidx = 0; sidx < n_seg_max; ++sidx) {
+    // lane-parallel first offsets of the 32 rows in this segment
+    const JitSide sl = pick(inh_l, c.je, c.ji);
+    uint32_t first_l = 0;
+    if (lane < static_cast<uint32_t>(nrows) && sidx < sl.n_seg)
+      first_l = (sl.seg_first + sidx) * sl.L + first_offset(sl.seed, sl.K, row_l, sl.seg_first + sidx);
+    for (int j = 0; j < nrows; ++j) {
+      const bool inh = __shfl_sync(0xffffffffu, static_cast<int>(inh_l), j) != 0;
+      const JitSide s = pick(inh, c.je, c.ji);
+      if (sidx >= s.n_seg) continue;                       // warp-uniform
+      const uint32_t row = __shfl_sync(0xffffffffu, row_l, j);
+      const uint32_t proj = inh ? 1u : 0u;
+      const uint32_t seg = s.seg_first + sidx;
+      const uint32_t seg_end = min(seg * s.L + s.L, c.n_cols);
+      uint32_t start = __shfl_sync(0xffffffffu, first_l, j);
+      uint32_t chunk = 0;
+      while (start < seg_end) {                            // warp-uniform
+        const u32x4 g = philox_block(s.seed, kTagGap, row, seg, chunk * 32u + lane);
+        const uint32_t g0 = bounded(1u, s.K, g.x), g1 = bounded(1u, s.K, g.y);
+        const uint32_t g2 = bounded(1u, s.K, g.z), g3 = bounded(1u, s.K, g.w);
+        const uint32_t p1 = g0, p2 = g0 + g1, p3 = p2 + g2, t = p3 + g3;
+        uint32_t incl = t;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= static_cast<uint32_t>(off)) incl += v;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t pos0 = start + (incl - t);
+        const uint32_t pos[4] = {pos0, pos0 + p1, pos0 + p2, pos0 + p3};
+        uint32_t n_valid = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) n_valid += __popc(__ballot_sync(0xffffffffu, pos[k] < seg_end));
+        int base = 0;
+        if (lane == 0) base = atomicAdd(n_staged, static_cast<int>(n_valid));
+        base = __shfl_sync(0xffffffffu, base, 0);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (pos[k] >= seg_end) continue;
+          const uint32_t loc = pos[k] - b.col_begin;
+          const int slot = base + static_cast<int>(4 * lane) + k;
+          if (slot < kBinStage) {
+            staged[slot] = stage_record(proj, loc);
+            atomicAdd(hist + (loc >> kTileShift), 1);
+          } else {
+            bin_event(b, proj, loc);
+          }
+          ++ev;
+        }
+        start += total;
+        ++chunk;
+      }
+    }
+  }
+  return ev;
+}
+
+// JIT rows with a small fan-out per segment (the network's ~80): ONE LANE
+// per row.  The lane walks its row's gap chain itself, two Philox blocks
+// (8 gaps) per iteration; the blocks do not depend on the running position,
+// so their 10-round chains overlap (ILP) and no cross-lane scan is needed.
+__device__ __forceinline__ uint32_t stage_row_lane(const ConnArgs &c, const BinTarget &b,
+                                                   int64_t r, uint32_t *staged,
+                                                   int32_t *n_staged, int32_t *hist) {
+  const bool inh = r >= c.split;
+  const uint32_t proj = inh ? 1u : 0u;
+  const JitSide s = pick(inh, c.je, c.ji);
+  const uint32_t row = static_cast<uint32_t>(inh ? r - c.split : r);
+  uint32_t ev = 0;
+  for (uint32_t sidx = 0; sidx < s.n_seg; ++sidx) {
+    const uint32_t seg = s.seg_first + sidx;
+    const uint32_t seg_end = min(seg * s.L + s.L, c.n_cols);
+    uint32_t pos = seg * s.L + first_offset(s.seed, s.K, row, seg);
+    for (uint32_t blk = 0; pos < seg_end; blk += 2) {
+      const u32x4 x = philox_block(s.seed, kTagGap, row, seg, blk);
+      const u32x4 y = philox_block(s.seed, kTagGap, row, seg, blk + 1);
+      uint32_t e[8];
+      e[0] = pos;
+      e[1] = e[0] + bounded(1u, s.K, x.x);
+      e[2] = e[1] + bounded(1u, s.K, x.y);
+      e[3] = e[2] + bounded(1u, s.K, x.z);
+      e[4] = e[3] + bounded(1u, s.K, x.w);
+      e[5] = e[4] + bounded(1u, s.K, y.x);
+      e[6] = e[5] + bounded(1u, s.K, y.y);
+      e[7] = e[6] + bounded(1u, s.K, y.z);
+      pos = e[7] + bounded(1u, s.K, y.w);
+      int nv = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) nv += e[k] < seg_end;
+      int slot = atomicAdd(n_staged, nv);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (e[k] >= seg_end) break;
+        const uint32_t loc = e[k] - b.col_begin;
+        if (slot < kBinStage) {
+          staged[slot] = stage_record(proj, loc);
+          atomicAdd(hist + (loc >> kTileShift), 1);
+        } else {
+          bin_event(b, proj, loc);
+        }
+        ++slot;
+        ++ev;
+      }
+    }
+  }
+  return ev;
+}
+
+// Exclusive scan of v[0..n) in place (block-wide, kBinThreads threads);
+// returns the total.
+__device__ __forceinline__ int32_t block_exclusive_scan(int32_t *v, int n, int32_t *warp_sums) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int per = (n + kBinThreads - 1) / kBinThreads;
+  const int lo = min(n, tid * per), hi = min(n, lo + per);
+  int32_t sum = 0;
+  for (int i = lo; i < hi; ++i) sum += v[i];
+  int32_t incl = sum;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int32_t t = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += t;
+  }
+  if (lane == 31) warp_sums[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int32_t w = warp_sums[lane];
+    int32_t wi = w;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int32_t t = __shfl_up_sync(0xffffffffu, wi, off);
+      if (lane >= off) wi += t;
+    }
+    warp_sums[lane] = wi - w;          // exclusive warp offsets
+    if (lane == 31) warp_sums[32] = wi;
+  }
+  __syncthreads();
+  int32_t run = warp_sums[warp] + incl - sum;
+  for (int i = lo; i < hi; ++i) {
+    const int32_t x = v[i];
+    v[i] = run;
+    run += x;
+  }
+  const int32_t total = warp_sums[32];
+  __syncthreads();
+  return total;
+}
+
+__global__ void __launch_bounds__(kBinThreads, 1)
+k_bin_sorted(ConnArgs conn, BinTarget out, const int32_t *active, const int32_t *count,
+             unsigned long long *events, uint32_t n_tiles) {
+  extern __shared__ uint32_t smem[];
+  uint32_t *staged = smem;                                  // [kBinStage]
+  uint32_t *sorted = staged + kBinStage;                    // [kBinStage]
+  int32_t *hist = reinterpret_cast<int32_t *>(sorted + kBinStage);   // [n_tiles]
+  int32_t *gbase = hist + n_tiles;                          // [n_tiles]
+  __shared__ int32_t n_staged;
+  __shared__ int32_t warp_sums[33];
+  __shared__ unsigned long long block_ev;
+  const int tid = threadIdx.x;
+  const uint32_t lane = tid & 31u, warp = tid >> 5;
+  const int n_active = *count;
+  // this block's contiguous share of the active rows
+  const int per = (n_active + gridDim.x - 1) / gridDim.x;
+  const int r_lo = min(n_active, static_cast<int>(blockIdx.x) * per);
+  const int r_hi = min(n_active, r_lo + per);
+  if (r_lo >= r_hi) return;
+  for (uint32_t t = tid; t < n_tiles; t += kBinThreads) hist[t] = 0;
+  if (tid == 0) { n_staged = 0; block_ev = 0; }
+  __syncthreads();
+
+  // A. regenerate this block's rows into shared memory + tile histogram
+  uint32_t ev = 0;
+  if (conn.conn == 1) {
+    for (int k = r_lo + static_cast<int>(warp); k < r_hi; k += kBinThreads / 32)
+      ev += stage_row(conn, out, active[k], staged, &n_staged, hist);
+  } else if (conn.lane_rows) {
+    for (int k = r_lo + tid; k < r_hi; k += kBinThreads)
+      ev += stage_row_lane(conn, out, active[k], staged, &n_staged, hist);
+  } else {
+    // warp w takes rows r_lo + w + 32 i (i = 0, 1, ...), 32 rows per batch
+    for (int k0 = r_lo + static_cast<int>(warp); k0 < r_hi; k0 += kBinThreads)
+      ev += stage_rows_jit(conn, out, active, k0, r_hi, staged, &n_staged, hist);
+  }
+  __syncthreads();
+  const int ns = min(n_staged, kBinStage);
+
+  // B. tile offsets; one global slot claim per non-empty tile
+  block_exclusive_scan(hist, static_cast<int>(n_tiles), warp_sums);
+  for (uint32_t t = tid; t < n_tiles; t += kBinThreads) {
+    const int32_t begin = hist[t];
+    const int32_t end = (t + 1 < n_tiles) ? hist[t + 1] : ns;
+    gbase[t] = end > begin ? atomicAdd(out.out.cnt + t * kCntStride, end - begin) : 0;
+  }
+  __syncthreads();
+
+  // C. counting sort by tile (hist[] becomes the running cursor)
+  for (int i = tid; i < ns; i += kBinThreads) {
+    const uint32_t rec = staged[i];
+    const uint32_t t = (rec & ~kProjBit) >> kTileShift;
+    sorted[atomicAdd(hist + t, 1)] = rec;
+  }
+  __syncthreads();
+
+  // D. write the runs.  After the sort hist[t] is the END of tile t's run in
+  //    sorted[], so the run begins at hist[t-1] (tiles are in order).
+  for (int i = tid; i < ns; i += kBinThreads) {
+    const uint32_t rec = sorted[i];
+    const uint32_t loc = rec & ~kProjBit;
+    const uint32_t t = loc >> kTileShift;
+    const int32_t run_begin = (t == 0) ? 0 : hist[t - 1];
+    const int32_t slot = gbase[t] + (i - run_begin);
+    bin_store(out, (rec & kProjBit) ? 1u : 0u, loc, slot);
+  }
+  // events counter
+  ev = __reduce_add_sync(0xffffffffu, ev);
+  if (lane == 0 && ev) atomicAdd(&block_ev, static_cast<unsigned long long>(ev));
+  __syncthreads();
+  if (tid == 0 && block_ev && events) atomicAdd(events, block_ev);
 }
 
 }  // namespace bp
