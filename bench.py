@@ -156,7 +156,7 @@ def cpu_baseline(n_total: int, budget_s: float = 15.0):
     fraction = 1.0 / 32
     secs, events, _ = oracle_sample_steps(n_total, 2, fraction)   # calibrate
     per_step = max(secs / 2, 1e-3)
-    steps = max(2, min(200, int(budget_s / per_step)))
+    steps = max(2, min(5000, int(budget_s / per_step)))
     secs, events, upd = oracle_sample_steps(n_total, steps, fraction)
     return {"value": events / secs, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": (f"{steps} steps of the {n_total:,}-neuron network with 1/32 of "
