@@ -356,6 +356,122 @@ def run_e2e(args, fixed, dev, template_state):
             "spikes_total": int(counts.sum().item())}
 
 
+# ---------------------------------------------------------------------------
+# config 2: event_csrmv / jitconn event_mv microbenchmark, 100k x 100k
+# ---------------------------------------------------------------------------
+# Algorithmic integer ops per JIT event (homo law): Philox4x32-10 = 10 rounds
+# x (2 IMAD.WIDE + 2 LOP3 + 2 key IADD) = 60 ops per 4 gap words -> 15;
+# bounded draw 2; running position 1; share of the 5-step warp scan 2.5;
+# RED 1.  Uniform adds 15 + 2 (weight word + fma), normal 30 + ~40 (fp64
+# log/cos/sqrt, counted as 40).  Issue peak: 148 SMs x 4 schedulers x 32
+# lanes x 1 warp-instruction per cycle at the sampled SM clock.
+JIT_OPS_PER_EVENT = {"homo": 21.5, "uniform": 38.5, "normal": 91.5}
+
+
+def run_micro(args):
+    import numpy as np
+    import torch
+
+    import __graft_entry__ as ge
+    ge.build_lib()
+    import paper_2311_05106_b200 as bp
+    from paper_2311_05106_b200 import inputs
+
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    n = 100_000
+    p, d, kind = args.p, args.density, args.workload
+    fixed = args.fix
+    law = args.law
+    n_pat = 64
+    pats = [inputs.spike_pattern(n, d, 7000 + k) for k in range(n_pat)]
+    spikes = [torch.from_numpy(inputs.pack_bits(e).view(np.int32)).to(dev) for e in pats]
+    out = torch.zeros(n, dtype=torch.int64 if fixed else torch.float32, device=dev)
+    ws = bp.workspace(n, dev)
+    seed = 0xBE7C4
+    spec = bp.jitconn_spec(seed, p)
+    w0, w1 = {"homo": (0.6, 0.0), "uniform": (-0.1, 0.1),
+              "normal": (0.0, 1.0 / np.sqrt(n * p))}[law]     # Table S1 scales
+    if kind == "csrmv":
+        ip, ix, dat = bp.jitconn_materialize(spec, n, n, law=bp.LAW_UNIFORM, w0=-0.1, w1=0.1,
+                                             with_data=(law != "homo"), device=dev)
+        row_nnz = (ip[1:] - ip[:-1]).cpu().numpy()
+        data = dat if law != "homo" else None
+        call = lambda s: bp.event_csrmv(ip, ix, data, 0.6, n, n, s, out, ws=ws)
+        ev_per_pat = [int(row_nnz[e.astype(bool)].sum()) for e in pats]
+        bytes_per_event = 8 if law != "homo" else 4
+        nnz = int(ip[-1].item())
+        working_set = nnz * bytes_per_event + ip.numel() * 8
+    else:
+        fn = {"homo": bp.jitconn_event_mv_homo, "uniform": bp.jitconn_event_mv_uniform,
+              "normal": bp.jitconn_event_mv_normal}[law]
+        if law == "homo":
+            call = lambda s: fn(spec, w0, s, n, n, out, ws=ws)
+        else:
+            call = lambda s: fn(spec, w0, w1, s, n, n, out, ws=ws)
+        counts = torch.empty(n, dtype=torch.int64, device=dev)
+        bp.lib().bp_jitconn_row_counts(bp._binding.ctypes.byref(spec), n, n,
+                                       bp._binding._ptr(counts), bp._binding._stream())
+        torch.cuda.synchronize()
+        row_nnz = counts.cpu().numpy()
+        ev_per_pat = [int(row_nnz[e.astype(bool)].sum()) for e in pats]
+        working_set = n * out.element_size()
+    l2 = 126 * 2 ** 20
+    flush = working_set < 2 * l2
+    scratch = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev) if flush else None
+    stream = torch.cuda.current_stream()
+    for k in range(args.warmup):
+        call(spikes[k % n_pat])
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    with ClockSampler(0) as clk:
+        for k in range(args.steps):
+            if flush:
+                scratch.fill_(k & 0xFF)           # evict the working set from L2
+            evs[k][0].record(stream)
+            call(spikes[k % n_pat])
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+    ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = sum(ms)
+    events = sum(ev_per_pat[k % n_pat] for k in range(args.steps))
+    value = events / (total_ms / 1e3)
+    peaks, peak_kind = _peaks()
+    clocks = clk.summary()
+    active = sum(int(pats[k % n_pat].sum()) for k in range(args.steps)) / args.steps
+    if kind == "csrmv":
+        per_call = (events / args.steps) * bytes_per_event + 16 * active + n / 8 + \
+            n * out.element_size()
+        achieved = per_call / (total_ms / args.steps / 1e3) / 1e9
+        roof = {"kernel": "k_compact + k_csr_scatter", "bound": "hbm", "achieved": achieved,
+                "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                "traffic": None, "peak_source": peak_kind,
+                "algorithmic_bytes_per_launch": per_call}
+    else:
+        sm_mhz = clocks.get("sm_mhz") or 1965.0
+        peak_ops = 148 * 4 * 32 * sm_mhz * 1e6
+        ops = JIT_OPS_PER_EVENT[law] * events / (total_ms / 1e3)
+        roof = {"kernel": "k_compact + k_jit_scatter<%s>" % law, "bound": "alu",
+                "achieved": ops / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s (int32 lane ops)",
+                "frac": ops / peak_ops, "traffic": None,
+                "peak_source": "derived: 148 SMs x 4 schedulers x 32 lanes x sampled SM clock",
+                "ops_per_event": JIT_OPS_PER_EVENT[law]}
+    line = {"metric": "synaptic events/sec (event_mv microbenchmark, config 2)",
+            "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "none", "vs_baseline": None,
+            "dtype": "i64fix" if fixed else "f32", "data": "synthetic",
+            "config": {"workload": f"{kind}_{law}", "shape": [n, n], "p": p, "density": d,
+                       "K": bp.conn_len(p), "events_per_call": events / args.steps,
+                       "active_rows_per_call": active,
+                       "l2": ("flushed between calls (256 MB write)" if flush
+                              else "working set %.0f MB > 2 x L2" % (working_set / 1e6))},
+            "gpu_launches": 2 * args.steps, "clocks": clocks, "roofline": roof,
+            "call_us": {"median": float(np.median(ms)) * 1e3, "min": float(np.min(ms)) * 1e3}}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -365,11 +481,19 @@ def main():
     ap.add_argument("--f32", action="store_true", help="fp32 conductances (fp32 atomics)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
+    ap.add_argument("--workload", choices=["coba_lif_jit", "csrmv", "jitmv"],
+                    default="coba_lif_jit")
+    ap.add_argument("--p", type=float, default=0.05, help="microbench connection probability")
+    ap.add_argument("--density", type=float, default=0.1, help="microbench spike density")
+    ap.add_argument("--law", choices=["homo", "uniform", "normal"], default="uniform")
+    ap.add_argument("--fix", action="store_true", help="microbench int64 fixed-point output")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload != "coba_lif_jit":
+        run_micro(args)
     else:
         run_ours(args)
 

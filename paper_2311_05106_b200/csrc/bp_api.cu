@@ -341,6 +341,34 @@ bp_status bp_event_csrmv(const int64_t *indptr, const int32_t *indices,
   a.split = n_rows;
   a.active = w.active;
   a.count = w.count;
+  // Column-tiled shared-memory aggregation when the output fits <= 4 tiles
+  // of <= 200 KB (scatter.cuh, k_csr_tiled); else one RED per event.
+  const size_t acc = out_kind == BP_OUT_FIX64 ? 8 : 4;
+  const int64_t tile_cols = static_cast<int64_t>(200 * 1000 / acc);
+  const int64_t n_tiles = (n_cols + tile_cols - 1) / tile_cols;
+  if (n_tiles <= 4 && !std::getenv("BP_CSR_DIRECT")) {
+    bp::CsrTiledArgs t{};
+    t.indptr = indptr; t.indices = indices; t.data = data; t.w = w_homo;
+    t.q = a.e.q; t.out = out; t.n_cols = n_cols;
+    t.tile_cols = static_cast<int32_t>(n_cols < tile_cols ? n_cols : tile_cols);
+    t.groups = static_cast<int32_t>(sms / n_tiles > 0 ? sms / n_tiles : 1);
+    t.active = w.active; t.count = w.count;
+    const size_t smem = static_cast<size_t>(t.tile_cols) * acc;
+    static bool attr_set[2] = {false, false};
+    if (!attr_set[out_kind]) {
+      if (out_kind == BP_OUT_FIX64)
+        BP_CUDA(cudaFuncSetAttribute(bp::k_csr_tiled<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     200 * 1000 + 1024));
+      else
+        BP_CUDA(cudaFuncSetAttribute(bp::k_csr_tiled<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     200 * 1000 + 1024));
+      attr_set[out_kind] = true;
+    }
+    const int grid = static_cast<int>(n_tiles * t.groups);
+    if (out_kind == BP_OUT_FIX64) bp::k_csr_tiled<1><<<grid, bp::kTiledThreads, smem, st>>>(t);
+    else bp::k_csr_tiled<0><<<grid, bp::kTiledThreads, smem, st>>>(t);
+    return launched();
+  }
   launch_csr(a, out_kind, grid_for_items(n_rows, sms), st);
   return launched();
 }

@@ -163,6 +163,140 @@ k_csr_scatter(CsrScatterArgs a) {
   count_events(a.events, ev);
 }
 
+
+// ---------------------------------------------------------------- a2, tiled
+// Column-tiled CSR scatter for outputs that fit a few shared-memory tiles
+// (config 2: 100k columns = two 50k-float tiles).  Random global REDs run at
+// ~0.19 T/s on B200 while shared-memory atomics run at 0.7 (f32 CAS) to 1.5
+// (int32) T/s (tools/probes/probe_atomics.cu), so each CTA owns one column
+// tile in shared memory, walks its share of the active rows, and adds only
+// the entries inside its tile -- the row's sub-range is found with a
+// 32-way warp search (<= 3 dependent loads for rows of 5000) -- then flushes
+// the tile with coalesced REDs (skipping untouched zeros).
+constexpr int kTiledThreads = 1024;
+
+// First j in [lo, hi) with idx[j] >= x (idx ascending); warp-cooperative.
+__device__ __forceinline__ int64_t warp_lower_bound(const int32_t *__restrict__ idx, int64_t lo,
+                                                    int64_t hi, int32_t x) {
+  const int lane = threadIdx.x & 31;
+  while (hi - lo > 32) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t j = lo + lane * step;
+    const bool ge = j < hi ? (__ldg(idx + j) >= x) : true;
+    const unsigned m = __ballot_sync(0xffffffffu, ge);
+    if (m == 0u) {                       // every probe < x: answer after the last probe
+      lo = lo + 31 * step + 1;
+      continue;
+    }
+    const int f = __ffs(m) - 1;
+    if (f == 0) return lo;               // idx[lo] >= x
+    const int64_t nlo = lo + (f - 1) * step + 1;
+    const int64_t nhi = lo + f * step;   // idx[nhi] >= x (or nhi >= hi)
+    lo = nlo;
+    hi = nhi < hi ? nhi : hi;
+  }
+  const int64_t j = lo + lane;
+  const bool ge = j < hi ? (__ldg(idx + j) >= x) : true;
+  const unsigned m = __ballot_sync(0xffffffffu, ge);
+  return m ? lo + (__ffs(m) - 1) : hi;
+}
+
+struct CsrTiledArgs {
+  const int64_t *indptr;
+  const int32_t *indices;
+  const float *data;          // nullptr -> homogeneous w
+  float w;
+  long long q;
+  void *out;
+  int64_t n_cols;
+  int32_t tile_cols;
+  int32_t groups;             // CTAs per tile
+  const int32_t *active;
+  const int32_t *count;
+};
+
+template <int KIND>
+__global__ void __launch_bounds__(kTiledThreads, 1)
+k_csr_tiled(CsrTiledArgs a) {
+  extern __shared__ unsigned char tile_raw[];
+  const int tile = blockIdx.x / a.groups, group = blockIdx.x % a.groups;
+  const int64_t c0 = static_cast<int64_t>(tile) * a.tile_cols;
+  const int64_t c1 = min(c0 + a.tile_cols, a.n_cols);
+  const int width = static_cast<int>(c1 - c0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float *accf = reinterpret_cast<float *>(tile_raw);
+  unsigned long long *accq = reinterpret_cast<unsigned long long *>(tile_raw);
+  for (int c = tid; c < width; c += kTiledThreads) {
+    if (KIND == 0) accf[c] = 0.f; else accq[c] = 0ull;
+  }
+  __syncthreads();
+  const int n_active = *a.count;
+  // Work unit = (active row, quarter of its in-tile range); units are dealt
+  // to the CTAs of the tile first, so a few long rows still spread over
+  // many SMs instead of queueing on one warp.
+  constexpr int kChunks = 4;
+  const int nwarp = a.groups * (kTiledThreads / 32);
+  const int64_t n_units = static_cast<int64_t>(n_active) * kChunks;
+  for (int64_t u = static_cast<int64_t>(warp) * a.groups + group; u < n_units; u += nwarp) {
+    const int64_t r = a.active[u / kChunks];
+    const int chunk = static_cast<int>(u % kChunks);
+    int64_t lo = __ldg(a.indptr + r), hi = __ldg(a.indptr + r + 1);
+    if (c0 > 0) lo = warp_lower_bound(a.indices, lo, hi, static_cast<int32_t>(c0));
+    if (c1 < a.n_cols) hi = warp_lower_bound(a.indices, lo, hi, static_cast<int32_t>(c1));
+    const int64_t span = hi - lo;
+    hi = lo + span * (chunk + 1) / kChunks;
+    lo = lo + span * chunk / kChunks;
+    int64_t j = lo + lane;
+    // 8 independent loads in flight per lane (latency-bound long rows)
+    for (; j + 224 < hi; j += 256) {
+      int32_t c[8];
+      float w[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        c[u] = __ldg(a.indices + j + 32 * u) - static_cast<int32_t>(c0);
+        w[u] = a.data ? __ldg(a.data + j + 32 * u) : a.w;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (KIND == 0) atomicAdd(accf + c[u], w[u]);
+        else atomicAdd(accq + c[u], static_cast<unsigned long long>(a.data ? quantize(w[u]) : a.q));
+      }
+    }
+    for (; j < hi; j += 32) {
+      const int32_t c = __ldg(a.indices + j) - static_cast<int32_t>(c0);
+      const float w = a.data ? __ldg(a.data + j) : a.w;
+      if (KIND == 0) atomicAdd(accf + c, w);
+      else atomicAdd(accq + c, static_cast<unsigned long long>(a.data ? quantize(w) : a.q));
+    }
+  }
+  __syncthreads();
+  if (KIND == 0 && (c0 & 3) == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0) {
+    // 16-byte vector REDs (red.global.add.v4.f32), all-zero quads skipped
+    float *out = static_cast<float *>(a.out) + c0;
+    const int quads = width / 4;
+    for (int qd = tid; qd < quads; qd += kTiledThreads) {
+      const float4 v = reinterpret_cast<const float4 *>(accf)[qd];
+      if (v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f)
+        asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};"
+                     ::"l"(out + 4 * qd), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+    }
+    for (int c = 4 * quads + tid; c < width; c += kTiledThreads) {
+      const float v = accf[c];
+      if (v != 0.f) atomicAdd(out + c, v);
+    }
+    return;
+  }
+  for (int c = tid; c < width; c += kTiledThreads) {
+    if (KIND == 0) {
+      const float v = accf[c];
+      if (v != 0.f) atomicAdd(static_cast<float *>(a.out) + c0 + c, v);
+    } else {
+      const unsigned long long v = accq[c];
+      if (v != 0ull) atomicAdd(static_cast<unsigned long long *>(a.out) + c0 + c, v);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- a3 + a4
 struct JitSide {
   uint64_t seed;

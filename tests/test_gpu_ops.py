@@ -64,11 +64,16 @@ CSR_CASES = [
     (2000, 3000, 0.01, "normal", 0.01),
     (4000, 4000, 0.02, "homo", 0.002),
     (1000, 100_000, 0.05, "uniform", 0.05),   # fan-out 5000 (config 2 row shape)
+    (300, 500_000, 0.01, "uniform", 0.3),     # > 4 shared-memory tiles: direct path
 ]
 
 
+@pytest.mark.parametrize("direct", [False, True])
 @pytest.mark.parametrize("case", CSR_CASES)
-def test_event_csrmv(bp, orc, case):
+def test_event_csrmv(bp, orc, case, direct, monkeypatch):
+    """direct=False: column-tiled shared-memory kernel; True: one RED per event."""
+    if direct:
+        monkeypatch.setenv("BP_CSR_DIRECT", "1")
     n_rows, n_cols, p, law, density = case
     ip, ix, dat = inputs.random_csr(n_rows, n_cols, p, seed=n_rows + n_cols,
                                     weights=law, w0=-0.5 if law != "homo" else 1.0,
