@@ -226,16 +226,23 @@ k_csr_tiled(CsrTiledArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   float *accf = reinterpret_cast<float *>(tile_raw);
   unsigned long long *accq = reinterpret_cast<unsigned long long *>(tile_raw);
+  // homogeneous weight: count the events per column (native int32 ATOMS)
+  // and scale once at the flush -- count * q(w) equals the fixed-point sum;
+  // fl32(count * w) is within rule T2 of the fp32 sum
+  unsigned *accc = reinterpret_cast<unsigned *>(tile_raw);
+  const bool homo = a.data == nullptr;
   for (int c = tid; c < width; c += kTiledThreads) {
-    if (KIND == 0) accf[c] = 0.f; else accq[c] = 0ull;
+    if (homo) accc[c] = 0u;
+    else if (KIND == 0) accf[c] = 0.f;
+    else accq[c] = 0ull;
   }
   __syncthreads();
   const int n_active = *a.count;
   // Work unit = (active row, quarter of its in-tile range); units are dealt
   // to the CTAs of the tile first, so a few long rows still spread over
   // many SMs instead of queueing on one warp.
-  constexpr int kChunks = 4;
   const int nwarp = a.groups * (kTiledThreads / 32);
+  const int kChunks = n_active >= nwarp ? 1 : 4;     // split rows only when rows are few
   const int64_t n_units = static_cast<int64_t>(n_active) * kChunks;
   for (int64_t u = static_cast<int64_t>(warp) * a.groups + group; u < n_units; u += nwarp) {
     const int64_t r = a.active[u / kChunks];
@@ -258,18 +265,35 @@ k_csr_tiled(CsrTiledArgs a) {
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        if (KIND == 0) atomicAdd(accf + c[u], w[u]);
-        else atomicAdd(accq + c[u], static_cast<unsigned long long>(a.data ? quantize(w[u]) : a.q));
+        if (homo) atomicAdd(accc + c[u], 1u);          // native ATOMS.ADD
+        else if (KIND == 0) atomicAdd(accf + c[u], w[u]);
+        else atomicAdd(accq + c[u], static_cast<unsigned long long>(quantize(w[u])));
       }
     }
     for (; j < hi; j += 32) {
       const int32_t c = __ldg(a.indices + j) - static_cast<int32_t>(c0);
-      const float w = a.data ? __ldg(a.data + j) : a.w;
-      if (KIND == 0) atomicAdd(accf + c, w);
-      else atomicAdd(accq + c, static_cast<unsigned long long>(a.data ? quantize(w) : a.q));
+      if (homo) {
+        atomicAdd(accc + c, 1u);
+      } else {
+        const float w = __ldg(a.data + j);
+        if (KIND == 0) atomicAdd(accf + c, w);
+        else atomicAdd(accq + c, static_cast<unsigned long long>(quantize(w)));
+      }
     }
   }
   __syncthreads();
+  if (homo) {
+    for (int c = tid; c < width; c += kTiledThreads) {
+      const unsigned n = accc[c];
+      if (n == 0u) continue;
+      if (KIND == 0)
+        atomicAdd(static_cast<float *>(a.out) + c0 + c, __fmul_rn(__uint2float_rn(n), a.w));
+      else
+        atomicAdd(static_cast<unsigned long long *>(a.out) + c0 + c,
+                  static_cast<unsigned long long>(static_cast<long long>(n) * a.q));
+    }
+    return;
+  }
   if (KIND == 0 && (c0 & 3) == 0 && (reinterpret_cast<uintptr_t>(a.out) & 15) == 0) {
     // 16-byte vector REDs (red.global.add.v4.f32), all-zero quads skipped
     float *out = static_cast<float *>(a.out) + c0;
