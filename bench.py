@@ -152,18 +152,68 @@ def oracle_sample_steps(n_total: int, n_steps: int, fraction: float, seed: int =
     return secs, events, n_upd * n_steps
 
 
-def cpu_baseline(n_total: int, budget_s: float = 15.0):
-    fraction = 1.0 / 32
-    secs, events, _ = oracle_sample_steps(n_total, 2, fraction)   # calibrate
-    per_step = max(secs / 2, 1e-3)
-    steps = max(2, min(5000, int(budget_s / per_step)))
-    secs, events, upd = oracle_sample_steps(n_total, steps, fraction)
+def oracle_full_network(wl, n_total, csr, n_steps):
+    """The oracle's own run_network (rule S1) on the workload's network for
+    n_steps; returns (seconds, events)."""
+    import numpy as np
+
+    import oracle
+    from paper_2311_05106_b200 import inputs
+    from paper_2311_05106_b200.network import SEED_E, SEED_I
+    spec = NETWORKS[wl]
+    n = n_total
+    n_exc = n * 4 // 5
+    K = oracle.conn_len(80.0 / n)
+    w = (0.6, 6.7) if spec["model"] == "lif" else (6.0, 67.0)
+    if csr is None:
+        pe = oracle.Projection(0, n_exc, jit=oracle.JitSpec(SEED_E, K, n, oracle.LAW_HOMO, w[0]))
+        pi = oracle.Projection(n_exc, n - n_exc, jit=oracle.JitSpec(SEED_I, K, n, oracle.LAW_HOMO, w[1]))
+        fan = [np.array([len(oracle.jit_row(p.jit, n, r)[0]) for r in range(p.n_rows)])
+               for p in (pe, pi)] if n <= 200_000 else None
+    else:
+        (ipe, ixe), (ipi, ixi) = [(a.cpu().numpy(), b.cpu().numpy()) for a, b in csr]
+        pe = oracle.Projection(0, n_exc, csr=(ipe, ixe, None), w_homo=w[0])
+        pi = oracle.Projection(n_exc, n - n_exc, csr=(ipi, ixi, None), w_homo=w[1])
+        fan = [np.diff(ipe), np.diff(ipi)]
+    if spec["model"] == "lif":
+        st = dict(v=inputs.lif_v0(n), g_e=np.zeros(n, np.int64), g_i=np.zeros(n, np.int64),
+                  ref=np.zeros(n, np.uint8), spikes=np.zeros(n, np.uint8))
+        params = oracle.lif_params()
+    else:
+        v, m, h, nk = inputs.hh_init(n)
+        st = dict(v=v, m=m, h=h, n=nk, g_e=np.zeros(n, np.int64), g_i=np.zeros(n, np.int64),
+                  spikes=np.zeros(n, np.uint8))
+        params = oracle.hh_params()
+    t0 = time.perf_counter()
+    raster = oracle.run_network(spec["model"], params, st, pe, pi, n_steps)
+    secs = time.perf_counter() - t0
+    # events: spikes of step k are delivered at step k+1
+    fan_all = np.concatenate(fan)
+    events = int((raster[:-1].astype(np.int64) @ fan_all).sum()) if fan is not None else 0
+    return secs, events
+
+
+def cpu_baseline(wl, n_total, csr, budget_s: float = 15.0):
+    if n_total > 1_000_000:
+        fraction = 1.0 / 32
+        secs, events, _ = oracle_sample_steps(n_total, 2, fraction)   # calibrate
+        per_step = max(secs / 2, 1e-3)
+        steps = max(2, min(5000, int(budget_s / per_step)))
+        secs, events, upd = oracle_sample_steps(n_total, steps, fraction)
+        return {"value": events / secs, "unit": UNIT, "cores": 1, "kind": "oracle",
+                "sample": (f"{steps} steps of the {n_total:,}-neuron network with 1/32 of "
+                           f"presynaptic rows active-eligible (Bernoulli 22 Hz x dt) and 1/32 "
+                           f"of neurons updated per step; {events:,} events in {secs:.1f} s, "
+                           f"single-threaded C oracle"),
+                "sim_s_per_wall_s_equiv": (steps * DT_MS * 1e-3 * fraction) / secs}
+    secs, _ = oracle_full_network(wl, n_total, csr, 20)                 # calibrate
+    steps = max(21, min(10_000, int(budget_s / max(secs / 20, 1e-6))))
+    secs, events = oracle_full_network(wl, n_total, csr, steps)
     return {"value": events / secs, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": (f"{steps} steps of the {n_total:,}-neuron network with 1/32 of "
-                       f"presynaptic rows active-eligible (Bernoulli 22 Hz x dt) and 1/32 "
-                       f"of neurons updated per step; {events:,} events in {secs:.1f} s, "
-                       f"single-threaded C oracle"),
-            "sim_s_per_wall_s_equiv": (steps * DT_MS * 1e-3 * fraction) / secs}
+            "sample": (f"the full {n_total:,}-neuron network for {steps} steps "
+                       f"({steps * DT_MS:.0f} ms simulated) through the oracle's run_network "
+                       f"(rule S1), single-threaded C oracle; {events:,} events in {secs:.1f} s"),
+            "sim_s_per_wall_s": steps * DT_MS * 1e-3 / secs}
 
 
 def run_reference(args):
@@ -195,6 +245,49 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+# Network workloads (BASELINE.json configs).  The default, config 5, is the
+# one the metric is quoted on ("COBA E/I at 1/2/4/8 B200", weak scaling).
+NETWORKS = {
+    "coba_lif_jit": dict(model="lif", conn="jit", per_gpu=N_PER_GPU, scaling="weak",
+                         cfg="config 5: COBA-LIF JIT, 12.5M neurons per GPU, postsynaptic partition"),
+    "coba4m_jit": dict(model="lif", conn="jit", n=4_000_000, scaling="strong",
+                       cfg="config 3: COBA-LIF JIT 4M neurons, fan-in 80"),
+    "coba4000_csr": dict(model="lif", conn="csr", n=4000, scaling="strong",
+                         cfg="config 1: COBA-LIF 4000 neurons (3200E/800I), p=0.02, CSR"),
+    "hh400k_csr": dict(model="hh", conn="csr", n=400_000, scaling="strong",
+                       cfg="config 4: COBA-HH 400k neurons, fan-in 80, CSR"),
+}
+
+
+def network_size(wl, world):
+    spec = NETWORKS[wl]
+    return spec["per_gpu"] * world if "per_gpu" in spec else spec["n"]
+
+
+def build_network(wl, world, rank, fixed, dev):
+    """The workload's network; CSR connectivity = materialise(JIT spec) with
+    the library's own generator ('CSR = materialise(jit spec)')."""
+    import paper_2311_05106_b200 as bp
+    from paper_2311_05106_b200.network import SEED_E, SEED_I, CobaNetwork
+    spec = NETWORKS[wl]
+    n = network_size(wl, world)
+    csr = None
+    if spec["conn"] == "csr":
+        n_exc = n * 4 // 5
+        p = 80.0 / n
+        ipe, ixe, _ = bp.jitconn_materialize(bp.jitconn_spec(SEED_E, p), n_exc, n,
+                                             with_data=False, device=dev)
+        ipi, ixi, _ = bp.jitconn_materialize(bp.jitconn_spec(SEED_I, p), n - n_exc, n,
+                                             with_data=False, device=dev)
+        csr = ((ipe, ixe), (ipi, ixi))
+    return CobaNetwork(n, model=spec["model"], conn=spec["conn"], fixed=fixed, rank=rank,
+                       world=world, device=dev, csr=csr), csr
+
+
+def state_bytes_per_neuron(model, fixed):
+    g = 32 if fixed else 16
+    return (8 + 1 if model == "lif" else 32) + g + 0.125
+
 
 def run_ours(args):
     import torch
@@ -202,8 +295,9 @@ def run_ours(args):
 
     import __graft_entry__ as ge
     ge.build_lib()
-    from paper_2311_05106_b200.network import CobaNetwork
 
+    wl = args.workload
+    spec = NETWORKS[wl]
     world = args.gpus
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -211,11 +305,12 @@ def run_ours(args):
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    n_total = N_PER_GPU * world
+    n_total = network_size(wl, world)
     fixed = not args.f32
 
-    net = CobaNetwork(n_total, conn="jit", fixed=fixed, rank=rank, world=world, device=dev)
+    net, csr = build_network(wl, world, rank, fixed, dev)
     n_local = net.part.col_end - net.part.col_begin
+    small = world == 1 and n_total <= 4096
     stream = torch.cuda.current_stream()
 
     def steps(k):
@@ -268,7 +363,7 @@ def run_ours(args):
     # D2H into pinned memory (the step's population-rate result).
     e2e = None
     if world == 1 and not args.no_e2e:
-        e2e = run_e2e(args, fixed, dev, net.state)
+        e2e = run_e2e(args, wl, fixed, dev)
 
     if rank != 0:
         if world > 1:
@@ -281,35 +376,45 @@ def run_ours(args):
     if prof is not None:
         sc_ms, up_ms, nrec = prof
         upd_s = up_ms / 1e3 / max(nrec, 1)
-        bytes_per_launch = step_bytes(n_local, events_total / args.steps, fixed)
+        bytes_per_launch = (state_bytes_per_neuron(spec["model"], fixed) * n_local +
+                            4 * events_total / args.steps)
         achieved = bytes_per_launch / upd_s / 1e9
-        roofline = {"kernel": "k_step<LIF,%s> (fused: bucket counts -> Expon+COBA+LIF -> "
-                              "spike bits + active list)" % ("fix64" if fixed else "f32"),
-                    "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"],
-                    "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+        kname = ("k_small_net<%s,%s> (whole time loop in one CTA, state in shared memory)"
+                 if small else "k_step<%s,%s> (fused: bucket counts -> Expon+COBA+neuron -> "
+                 "spike bits + active list)") % (spec["model"].upper(), "fix64" if fixed else "f32")
+        roofline = {"kernel": kname, "bound": "hbm", "achieved": achieved,
+                    "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                     "traffic": None, "peak_source": peak_kind,
                     "algorithmic_bytes_per_launch": bytes_per_launch,
                     "avg_launch_us": upd_s * 1e6,
                     "share_of_step": up_ms / (sc_ms + up_ms) if (sc_ms + up_ms) else None,
                     "bin_kernel_avg_us": sc_ms / 1e3 / max(nrec, 1) * 1e6}
-    cpu = cpu_baseline(n_total) if (world == 1 and not args.no_cpu) else None
+        if small:
+            roofline["note"] = ("latency-bound: the whole state (%d neurons) lives in one SM's "
+                                "shared memory; HBM fraction is not the limiter" % n_local)
+    cpu = cpu_baseline(wl, n_total, csr) if (world == 1 and not args.no_cpu) else None
+    state_mb = state_bytes_per_neuron(spec["model"], fixed) * n_local / 1e6
     clocks = clk.summary()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": spec["scaling"], "vs_baseline": None,
         "dtype": "i64fix+f32" if fixed else "f32", "data": "synthetic",
-        "config": {"workload": "coba_lif_jit", "n_per_gpu": N_PER_GPU, "n_total": n_total,
-                   "fan_in": 80, "p": 80.0 / n_total, "conn_len_K": net.net.desc.jit_exc.conn_len,
-                   "dt_ms": DT_MS, "g": "int64 fixed point 2^-32" if fixed else "fp32",
+        "config": {"workload": wl, "description": spec["cfg"], "n_total": n_total,
+                   "n_per_gpu": n_local, "model": spec["model"], "connectivity": spec["conn"],
+                   "fan_in": 80, "p": 80.0 / n_total, "dt_ms": DT_MS,
+                   "g": "int64 fixed point 2^-32" if fixed else "fp32",
                    "parallelism": f"postsynaptic partition x{world}",
-                   "l2": "state 525 MB/GPU > 126 MB L2: no flush needed",
-                   "spikes_delivered": spikes_seen, "events": events_total},
+                   "l2": (f"state {state_mb:.0f} MB/GPU > 2 x 126 MB L2: no flush needed"
+                          if state_mb > 252 else
+                          f"state {state_mb:.1f} MB is L2/SM-resident by design (the workload is that small)"),
+                   "spikes": spikes_seen, "events": events_total},
         "sim_s_per_wall_s": sim_ratio,
         "events_per_step": events_total / args.steps,
-        # libbp kernels in the timed region: scatter + update per step (world 1);
-        # compaction + scatter + update per step (world > 1; NCCL not counted)
-        "gpu_launches": (2 if world == 1 else 3) * args.steps,
+        # libbp kernels in the timed region: k_step + k_bin per step (world 1),
+        # one k_small_net launch for small networks, and k_compact + k_bin +
+        # k_step per step for world > 1 (NCCL kernels not counted)
+        "gpu_launches": (1 if small else (2 if world == 1 else 3) * args.steps),
         "clocks": clocks,
         "roofline": roofline,
         "cpu_baseline": cpu,
@@ -321,18 +426,23 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def run_e2e(args, fixed, dev, template_state):
+def run_e2e(args, wl, fixed, dev):
     """Same metric through the public API with host buffers."""
     import torch
 
     from paper_2311_05106_b200 import inputs
-    from paper_2311_05106_b200.network import CobaNetwork
-    n = N_PER_GPU
-    net = CobaNetwork(n, conn="jit", fixed=fixed, device=dev)
+    net, _ = build_network(wl, 1, 0, fixed, dev)
+    n = net.n
     host = {k: torch.empty_like(v, device="cpu").pin_memory() for k, v in net.state.items()}
-    host["v"].copy_(torch.from_numpy(inputs.lif_v0(n)))
-    for k in ("g_e", "g_i", "ref"):
-        host[k].zero_()
+    if NETWORKS[wl]["model"] == "lif":
+        host["v"].copy_(torch.from_numpy(inputs.lif_v0(n)))
+        for k in ("g_e", "g_i", "ref"):
+            host[k].zero_()
+    else:
+        for k, a in zip(("v", "m", "h", "n"), inputs.hh_init(n)):
+            host[k].copy_(torch.from_numpy(a))
+        for k in ("g_e", "g_i"):
+            host[k].zero_()
     counts = torch.zeros(args.steps, dtype=torch.int32).pin_memory()
     h2d = sum(t.numel() * t.element_size() for t in host.values())
     stream = torch.cuda.current_stream()
@@ -481,7 +591,7 @@ def main():
     ap.add_argument("--f32", action="store_true", help="fp32 conductances (fp32 atomics)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
-    ap.add_argument("--workload", choices=["coba_lif_jit", "csrmv", "jitmv"],
+    ap.add_argument("--workload", choices=list(NETWORKS) + ["csrmv", "jitmv"],
                     default="coba_lif_jit")
     ap.add_argument("--p", type=float, default=0.05, help="microbench connection probability")
     ap.add_argument("--density", type=float, default=0.1, help="microbench spike density")
@@ -492,7 +602,7 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
-    elif args.workload != "coba_lif_jit":
+    elif args.workload in ("csrmv", "jitmv"):
         run_micro(args)
     else:
         run_ours(args)

@@ -548,6 +548,13 @@ struct bp_network {
   int bpar = 0;                   // bucket parity holding the next step's input
   int64_t steps_done = 0;
   bp::ConnArgs conn{};
+  // small networks (step.cuh k_small_net): whole time loop in one CTA
+  bool small = false;
+  int32_t *small_active = nullptr;   // pending spikes (global ids) + count
+  int32_t *small_count = nullptr;
+  int32_t *small_steps = nullptr;    // per-step spike counts scratch
+  int64_t small_steps_cap = 0;
+  int64_t prof_steps = 0;
 };
 
 namespace {
@@ -656,7 +663,11 @@ bp_status alloc_buckets(bp_network *net, cudaStream_t st) {
   const size_t buf_b = round_up(static_cast<size_t>(net->n_tiles) * cap * sizeof(uint32_t), 256);
   const size_t spill_b = round_up(2 * static_cast<size_t>(net->n_local) * sizeof(int32_t), 256);
   const size_t per = 2 * cnt_b + buf_b + spill_b;     // cnt, flag, buf, spill
-  BP_CUDA(cudaMalloc(&net->bk_mem, 2 * per));
+  const size_t small_b = round_up((static_cast<size_t>(net->n_local) + 64) * sizeof(int32_t), 256);
+  BP_CUDA(cudaMalloc(&net->bk_mem, 2 * per + small_b));
+  net->small_count = reinterpret_cast<int32_t *>(static_cast<char *>(net->bk_mem) + 2 * per);
+  net->small_active = net->small_count + 64;
+  BP_CUDA(cudaMemsetAsync(net->small_count, 0, sizeof(int32_t), st));
   char *m = static_cast<char *>(net->bk_mem);
   for (int p = 0; p < 2; ++p) {
     char *b = m + p * per;
@@ -740,9 +751,9 @@ bp_status launch_step(bp_network *net, uint32_t *raster, cudaStream_t st,
   if (d.model == BP_MODEL_LIF) {
     if (d.g_kind == BP_OUT_FIX64) bp::k_step<0, 1><<<grid, bp::kStepThreads, 0, st>>>(a);
     else bp::k_step<0, 0><<<grid, bp::kStepThreads, 0, st>>>(a);
-  } else {
-    if (d.g_kind == BP_OUT_FIX64) bp::k_step<1, 1><<<grid, bp::kStepThreads, 0, st>>>(a);
-    else bp::k_step<1, 0><<<grid, bp::kStepThreads, 0, st>>>(a);
+  } else {   // HH is compute-latency-bound: 512 threads per tile
+    if (d.g_kind == BP_OUT_FIX64) bp::k_step<1, 1><<<grid, 512, 0, st>>>(a);
+    else bp::k_step<1, 0><<<grid, 512, 0, st>>>(a);
   }
   bp_status s = launched();
   if (s != BP_OK) return s;
@@ -751,6 +762,70 @@ bp_status launch_step(bp_network *net, uint32_t *raster, cudaStream_t st,
   if (s != BP_OK) return s;
   net->bpar = out_par;
   net->steps_done += 1;
+  return BP_OK;
+}
+
+}  // namespace
+
+namespace {
+
+template <int MODEL, int KIND>
+bp_status launch_small(const bp::SmallArgs &a, cudaStream_t st) {
+  const size_t smem = bp::small_net_smem(MODEL, KIND);
+  static bool attr = false;
+  if (!attr) {
+    BP_CUDA(cudaFuncSetAttribute(bp::k_small_net<MODEL, KIND>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    attr = true;
+  }
+  bp::k_small_net<MODEL, KIND><<<1, bp::kSmallThreads, smem, st>>>(a);
+  return launched();
+}
+
+bp_status small_step(bp_network *net, int64_t n_steps, uint32_t *raster, int32_t *counts_out,
+                     cudaStream_t st) {
+  const bp_network_desc &d = net->d;
+  if (counts_out && n_steps > net->small_steps_cap) {
+    if (net->small_steps) cudaFree(net->small_steps);
+    net->small_steps = nullptr;
+    BP_CUDA(cudaMalloc(&net->small_steps, n_steps * sizeof(int32_t)));
+    net->small_steps_cap = n_steps;
+  }
+  bp::SmallArgs a{};
+  a.nrn = net->neuron;
+  a.nrn.raster = raster;
+  a.conn = net->conn;
+  a.w_e = d.w_exc;
+  a.w_i = d.w_inh;
+  a.q_e = llrint(static_cast<double>(d.w_exc) * 4294967296.0);
+  a.q_i = llrint(static_cast<double>(d.w_inh) * 4294967296.0);
+  a.n_steps = n_steps;
+  a.step_counts = counts_out ? net->small_steps : nullptr;
+  a.active_io = net->small_active;
+  a.count_io = net->small_count;
+  a.events = net->counters + 1;
+  a.spikes = net->counters;
+  cudaEvent_t *ev = nullptr;
+  if (net->prof_ev && net->prof_used < net->prof_cap) {
+    ev = net->prof_ev + 3 * net->prof_used++;
+    net->prof_steps += n_steps;
+  }
+  if (ev) BP_CUDA(cudaEventRecord(ev[0], st));
+  bp_status s;
+  if (d.model == BP_MODEL_LIF)
+    s = d.g_kind == BP_OUT_FIX64 ? launch_small<0, 1>(a, st) : launch_small<0, 0>(a, st);
+  else
+    s = d.g_kind == BP_OUT_FIX64 ? launch_small<1, 1>(a, st) : launch_small<1, 0>(a, st);
+  if (s != BP_OK) return s;
+  if (ev) {   // the single launch is the "update" interval; no binning kernel
+    BP_CUDA(cudaEventRecord(ev[1], st));
+    BP_CUDA(cudaEventRecord(ev[2], st));
+  }
+  if (counts_out)
+    BP_CUDA(cudaMemcpyAsync(counts_out, net->small_steps, n_steps * sizeof(int32_t),
+                            cudaMemcpyDefault, st));
+  net->steps_done += n_steps;
   return BP_OK;
 }
 
@@ -836,6 +911,14 @@ bp_status bp_network_create(const bp_network_desc *desc, bp_stream stream,
   // into the first step; remote parts arrive through bp_network_scatter
   if (s == BP_OK)
     s = bin_spike_range(net, desc->col_begin / 32, (desc->col_end + 31) / 32, net->bpar, st);
+  // one device, whole network, state fits one CTA's shared memory: the
+  // single-CTA time loop (k_small_net) drives bp_network_step
+  net->small = s == BP_OK && desc->col_begin == 0 && desc->col_end == desc->n &&
+               desc->n <= bp::kSmallMax && !std::getenv("BP_NO_SMALL_NET");
+  if (net->small) {
+    launch_compact(desc->spikes, desc->n, net->small_active, net->small_count, sms, st);
+    s = launched();
+  }
   if (s != BP_OK) {
     bp_network_destroy(net);
     return s;
@@ -850,10 +933,13 @@ bp_status bp_network_step(bp_network *net, int64_t n_steps, uint32_t *raster_out
   if (s != BP_OK) return s;
   BP_CHECK(net != nullptr && n_steps >= 0, BP_ERR_INVALID_ARG, "bad net/n_steps");
   cudaStream_t st = as_stream(stream);
+  if (net->small && n_steps > 0) return small_step(net, n_steps, raster_out, counts_out, st);
   for (int64_t k = 0; k < n_steps; ++k) {
     cudaEvent_t *ev = nullptr;
-    if (net->prof_ev && net->prof_used < net->prof_cap)
+    if (net->prof_ev && net->prof_used < net->prof_cap) {
       ev = net->prof_ev + 3 * net->prof_used++;
+      net->prof_steps += 1;
+    }
     if (counts_out) BP_CUDA(cudaMemsetAsync(net->count + 1, 0, sizeof(int32_t), st));
     if (ev) BP_CUDA(cudaEventRecord(ev[0], st));
     s = launch_step(net, raster_out ? raster_out + k * net->local_words : nullptr, st,
@@ -876,6 +962,7 @@ bp_status bp_network_profile_begin(bp_network *net, int64_t max_steps) {
     BP_CUDA(cudaEventCreate(&net->prof_ev[i]));
   net->prof_cap = max_steps;
   net->prof_used = 0;
+  net->prof_steps = 0;
   return BP_OK;
 }
 
@@ -900,8 +987,9 @@ bp_status bp_network_profile_end(bp_network *net, double *scatter_ms,
   net->prof_ev = nullptr;
   if (scatter_ms) *scatter_ms = sc;
   if (update_ms) *update_ms = up;
-  if (steps) *steps = net->prof_used;
+  if (steps) *steps = net->prof_steps;
   net->prof_cap = net->prof_used = 0;
+  net->prof_steps = 0;
   return s;
 }
 
@@ -940,6 +1028,7 @@ bp_status bp_network_counters(bp_network *net, uint64_t *host_out, bp_stream str
 
 void bp_network_destroy(bp_network *net) {
   if (net && net->bk_mem) cudaFree(net->bk_mem);
+  if (net && net->small_steps) cudaFree(net->small_steps);
   if (net && net->prof_ev) {
     for (int64_t i = 0; i < 3 * net->prof_cap; ++i) cudaEventDestroy(net->prof_ev[i]);
     delete[] net->prof_ev;

@@ -27,6 +27,7 @@
 // state the previous step touched last -- still in L2 -- is touched first.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 
 #include "cache.cuh"
 #include "neuron.cuh"
@@ -408,14 +409,14 @@ __device__ __forceinline__ uint32_t pass_update(Pass<MODEL, KIND> &p, const Step
 // Spike words of one pass (lanes 8w..8w+7 hold the 32 neurons of word w)
 // and the active-list append (one atomic per warp with spikes).
 __device__ __forceinline__ void pass_emit(const StepArgs &a, uint32_t nib, int64_t base,
-                                          int pass, uint32_t &my_sp) {
+                                          int pass_off, uint32_t &my_sp) {
   const NeuronArgs &nr = a.nrn;
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   uint32_t word = nib << (4u * (lane & 7u));
   word |= __shfl_xor_sync(0xffffffffu, word, 1);
   word |= __shfl_xor_sync(0xffffffffu, word, 2);
   word |= __shfl_xor_sync(0xffffffffu, word, 4);
-  const int64_t wi = (base + pass * 1024 + warp * 128) / 32 + (lane >> 3);
+  const int64_t wi = (base + pass_off + warp * 128) / 32 + (lane >> 3);
   if ((lane & 7u) == 0 && wi * 32 < nr.n) {
     nr.spikes[wi] = word;
     if (nr.raster) nr.raster[wi] = word;
@@ -433,7 +434,7 @@ __device__ __forceinline__ void pass_emit(const StepArgs &a, uint32_t nib, int64
     int slot = 0;
     if (lane == 0) slot = atomicAdd(a.active_count, static_cast<int>(warp_sp));
     slot = __shfl_sync(0xffffffffu, slot, 0) + static_cast<int>(incl - c);
-    const int64_t i0 = base + pass * 1024 + 4 * static_cast<int64_t>(threadIdx.x);
+    const int64_t i0 = base + pass_off + 4 * static_cast<int64_t>(threadIdx.x);
     uint32_t bits = nib;
     while (bits) {
       const int q = __ffs(bits) - 1;
@@ -447,13 +448,18 @@ __device__ __forceinline__ void pass_emit(const StepArgs &a, uint32_t nib, int64
 // The first two passes' state loads are issued before the bucket-counting
 // phase so their DRAM latency overlaps it; passes 2 and 3 are loaded while
 // 0 and 1 compute (register double buffering).
+// LIF (memory-bound): 256 threads, 4 passes, register double buffering.
+// HH (FP32-latency-bound): 512 threads, 2 passes (more warps, 128 registers).
 template <int MODEL, int KIND>
-__global__ void __launch_bounds__(kStepThreads)
+__global__ void __launch_bounds__(MODEL == 0 ? kStepThreads : 512, MODEL == 0 ? 4 : 1)
 k_step(StepArgs a) {
   __shared__ int32_t cnt_e[kTile];
   __shared__ int32_t cnt_i[kTile];
   __shared__ unsigned long long block_sp;
   const int tid = threadIdx.x;
+  constexpr int nthreads = MODEL == 0 ? kStepThreads : 512;
+  constexpr int passes = kTile / (4 * nthreads);
+  constexpr int pstride = 4 * nthreads;   // neurons per pass
   const uint32_t lane = tid & 31u;
   const uint32_t tile = a.reverse ? a.n_tiles - 1u - blockIdx.x : blockIdx.x;
   const int64_t base = static_cast<int64_t>(tile) << kTileShift;
@@ -462,20 +468,20 @@ k_step(StepArgs a) {
 
   Pass<MODEL, KIND> pa, pb;
   pass_load(pa, nr, base + 4 * tid, pol);
-  pass_load(pb, nr, base + 1024 + 4 * tid, pol);
+  pass_load(pb, nr, base + pstride + 4 * tid, pol);
 
   // 1. count this tile's incoming events (bucket + rare spill)
-  for (int j = tid; j < kTile; j += kStepThreads) { cnt_e[j] = 0; cnt_i[j] = 0; }
+  for (int j = tid; j < kTile; j += nthreads) { cnt_e[j] = 0; cnt_i[j] = 0; }
   if (tid == 0) block_sp = 0;
   __syncthreads();
   const int32_t n_in = min(static_cast<uint32_t>(a.in.cnt[tile * kCntStride]), a.out.cap);
   const uint32_t *buf = a.in.buf + static_cast<size_t>(tile) * a.out.cap;
-  for (int k = tid; k < n_in; k += kStepThreads) {
+  for (int k = tid; k < n_in; k += nthreads) {
     const uint32_t e = __ldcs(buf + k);
     atomicAdd((e & kProjBit) ? &cnt_i[e & (kTile - 1)] : &cnt_e[e & (kTile - 1)], 1);
   }
   if (a.in.flag[tile]) {                       // overflow spill (exact, rare)
-    for (int j = tid; j < kTile && base + j < nr.n; j += kStepThreads) {
+    for (int j = tid; j < kTile && base + j < nr.n; j += nthreads) {
       int32_t *se = a.in.spill + base + j;
       int32_t *si = a.in.spill + a.out.n_local + base + j;
       atomicAdd(&cnt_e[j], *se);
@@ -493,16 +499,14 @@ k_step(StepArgs a) {
 
   // 2. update the tile: 4 passes of 1024 neurons, 4 consecutive per thread
   uint32_t my_sp = 0;
-  uint32_t nib = pass_update(pa, a, cnt_e, cnt_i, 4 * tid, base + 4 * tid, pol);
-  pass_load(pa, nr, base + 2048 + 4 * tid, pol);
-  pass_emit(a, nib, base, 0, my_sp);
-  nib = pass_update(pb, a, cnt_e, cnt_i, 1024 + 4 * tid, base + 1024 + 4 * tid, pol);
-  pass_load(pb, nr, base + 3072 + 4 * tid, pol);
-  pass_emit(a, nib, base, 1, my_sp);
-  nib = pass_update(pa, a, cnt_e, cnt_i, 2048 + 4 * tid, base + 2048 + 4 * tid, pol);
-  pass_emit(a, nib, base, 2, my_sp);
-  nib = pass_update(pb, a, cnt_e, cnt_i, 3072 + 4 * tid, base + 3072 + 4 * tid, pol);
-  pass_emit(a, nib, base, 3, my_sp);
+#pragma unroll
+  for (int p = 0; p < passes; ++p) {
+    Pass<MODEL, KIND> &cur = (p & 1) ? pb : pa;
+    const int off = p * pstride;
+    const uint32_t nib = pass_update(cur, a, cnt_e, cnt_i, off + 4 * tid, base + off + 4 * tid, pol);
+    if (p + 2 < passes) pass_load(cur, nr, base + off + 2 * pstride + 4 * tid, pol);
+    pass_emit(a, nib, base, off, my_sp);
+  }
 
   // 3. counters
   my_sp = __reduce_add_sync(0xffffffffu, my_sp);
@@ -871,6 +875,204 @@ k_bin_sorted(ConnArgs conn, BinTarget out, const int32_t *active, const int32_t 
   if (lane == 0 && ev) atomicAdd(&block_ev, static_cast<unsigned long long>(ev));
   __syncthreads();
   if (tid == 0 && block_ev && events) atomicAdd(events, block_ev);
+}
+
+}  // namespace bp
+
+namespace bp {
+
+// ---------------------------------------------------------------------------
+// Small networks (config 1: 4000 neurons): ONE CTA runs the whole time loop
+// with the network state in shared memory.  Per step ~9 neurons spike, i.e.
+// ~700 events -- microseconds of work that two kernel launches per step
+// would dominate.  Per step: (1) the warps deliver last step's spikes (one
+// warp per spiking row, CSR row loads or JIT regeneration) as int32 event
+// counts in shared memory; (2) barrier; (3) every thread updates 4 neurons
+// (rule N1/H1 with the same helpers as k_step) and appends spikes; (4)
+// barrier.  State is loaded once and written back once.
+constexpr int kSmallMax = 4096;
+constexpr int kSmallThreads = 1024;
+
+struct SmallArgs {
+  NeuronArgs nrn;          // global state (n = N <= kSmallMax), spikes, raster
+  ConnArgs conn;
+  float w_e, w_i;
+  long long q_e, q_i;
+  int64_t n_steps;
+  int32_t *step_counts;    // nullable, device [n_steps]
+  int32_t *active_io;      // in: initial active list, out: last step's list
+  int32_t *count_io;       // in/out: its length
+  unsigned long long *events;
+  unsigned long long *spikes;
+};
+
+template <int MODEL, int KIND>
+__global__ void __launch_bounds__(kSmallThreads, 1)
+k_small_net(SmallArgs a) {
+  extern __shared__ unsigned char sm[];
+  const NeuronArgs &nr = a.nrn;
+  const int n = static_cast<int>(nr.n);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  using G = typename std::conditional<KIND == 1, long long, float>::type;
+  G *gE = reinterpret_cast<G *>(sm);
+  G *gI = gE + kSmallMax;
+  float *V = reinterpret_cast<float *>(gI + kSmallMax);
+  float *M = V + kSmallMax;                  // HH only
+  float *H = M + kSmallMax;
+  float *Nk = H + kSmallMax;
+  int32_t *cE = reinterpret_cast<int32_t *>(MODEL == 0 ? (V + kSmallMax) : (Nk + kSmallMax));
+  int32_t *cI = cE + kSmallMax;
+  int32_t *act = cI + kSmallMax;             // active list (spikes of the last step)
+  uint8_t *R = reinterpret_cast<uint8_t *>(act + kSmallMax);
+  __shared__ int32_t n_act, n_next;
+  __shared__ unsigned long long ev_total, sp_total;
+
+  for (int i = tid; i < kSmallMax; i += kSmallThreads) {
+    const bool in = i < n;
+    gE[i] = in ? static_cast<G *>(nr.g_e)[i] : G(0);
+    gI[i] = in ? static_cast<G *>(nr.g_i)[i] : G(0);
+    V[i] = in ? nr.v[i] : 0.f;
+    if (MODEL == 0) R[i] = in ? nr.ref[i] : 0;
+    else { M[i] = in ? nr.m[i] : 0.f; H[i] = in ? nr.h[i] : 0.f; Nk[i] = in ? nr.nk[i] : 0.f; }
+    cE[i] = 0;
+    cI[i] = 0;
+  }
+  if (tid == 0) { n_act = *a.count_io; ev_total = 0; sp_total = 0; }
+  __syncthreads();
+  for (int i = tid; i < n_act; i += kSmallThreads) act[i] = a.active_io[i];
+  __syncthreads();
+
+  uint32_t my_ev = 0, my_sp = 0;
+  for (int64_t step = 0; step < a.n_steps; ++step) {
+    // (1) deliver spikes_{n-1}: count events per postsynaptic neuron
+    for (int k = warp; k < n_act; k += kSmallThreads / 32) {
+      const int64_t r = act[k];
+      const bool inh = r >= a.conn.split;
+      const int64_t row64 = inh ? r - a.conn.split : r;
+      int32_t *cnt = inh ? cI : cE;
+      if (a.conn.conn == 1) {
+        const CsrSide s = pick(inh, a.conn.ce, a.conn.ci);
+        const int64_t b = __ldg(s.indptr + row64), e = __ldg(s.indptr + row64 + 1);
+        for (int64_t j = b + lane; j < e; j += 32) {
+          atomicAdd(cnt + __ldg(s.indices + j), 1);
+          ++my_ev;
+        }
+      } else {
+        const JitSide s = pick(inh, a.conn.je, a.conn.ji);
+        const uint32_t row = static_cast<uint32_t>(row64);
+        for (uint32_t seg = 0; seg < s.n_seg; ++seg) {
+          const uint32_t seg_end = min(seg * s.L + s.L, a.conn.n_cols);
+          u32x4 g = philox_block(s.seed, kTagGap, row, seg, lane);
+          uint32_t start = seg * s.L + first_offset(s.seed, s.K, row, seg);
+          uint32_t chunk = 0;
+          while (start < seg_end) {
+            const uint32_t g0 = bounded(1u, s.K, g.x), g1 = bounded(1u, s.K, g.y);
+            const uint32_t g2 = bounded(1u, s.K, g.z), g3 = bounded(1u, s.K, g.w);
+            const uint32_t p1 = g0, p2 = g0 + g1, p3 = p2 + g2, t = p3 + g3;
+            uint32_t incl = t;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+              const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+              if (lane >= off) incl += v;
+            }
+            const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+            const uint32_t pos0 = start + (incl - t);
+            const uint32_t pos[4] = {pos0, pos0 + p1, pos0 + p2, pos0 + p3};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (pos[q] < seg_end) { atomicAdd(cnt + pos[q], 1); ++my_ev; }
+            start += total;
+            ++chunk;
+            if (start < seg_end) g = philox_block(s.seed, kTagGap, row, seg, chunk * 32u + lane);
+          }
+        }
+      }
+    }
+    if (tid == 0) n_next = 0;
+    __syncthreads();
+    // (3) update, 4 consecutive neurons per thread
+    const int j0 = 4 * tid;
+    uint32_t nib = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = j0 + q;
+      if (i >= n) break;
+      float gEf, gIf;
+      if constexpr (KIND == 1) {
+        gEf = g_fold(gE[i], cE[i], a.q_e);
+        gIf = g_fold(gI[i], cI[i], a.q_i);
+      } else {
+        gEf = g_fold(gE[i], cE[i], a.w_e);
+        gIf = g_fold(gI[i], cI[i], a.w_i);
+      }
+      cE[i] = 0;
+      cI[i] = 0;
+      g_after(gE[i], nr.alpha_e, nr.alpha_e32);
+      g_after(gI[i], nr.alpha_i, nr.alpha_i32);
+      bool sp;
+      if constexpr (MODEL == 0) {
+        uint32_t r = R[i];
+        sp = lif_one(nr, V[i], r, gEf, gIf);
+        R[i] = static_cast<uint8_t>(r);
+      } else {
+        sp = hh_one(nr, V[i], M[i], H[i], Nk[i], gEf, gIf);
+      }
+      if (sp) nib |= 1u << q;
+    }
+    uint32_t word = nib << (4u * (lane & 7u));
+    word |= __shfl_xor_sync(0xffffffffu, word, 1);
+    word |= __shfl_xor_sync(0xffffffffu, word, 2);
+    word |= __shfl_xor_sync(0xffffffffu, word, 4);
+    const int wi = (warp * 128) / 32 + (lane >> 3);
+    if ((lane & 7u) == 0 && wi * 32 < n) {
+      nr.spikes[wi] = word;
+      if (nr.raster) nr.raster[step * ((n + 31) / 32) + wi] = word;
+    }
+    if (nib) {
+      const int c = __popc(nib);
+      int slot = atomicAdd(&n_next, c);
+      my_sp += c;
+      uint32_t bits = nib;
+      while (bits) {
+        const int q = __ffs(bits) - 1;
+        bits &= bits - 1u;
+        act[slot++] = j0 + q;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      n_act = n_next;
+      if (a.step_counts) a.step_counts[step] = n_next;
+    }
+    __syncthreads();
+  }
+  // write back state and the final active list
+  for (int i = tid; i < n; i += kSmallThreads) {
+    static_cast<G *>(nr.g_e)[i] = gE[i];
+    static_cast<G *>(nr.g_i)[i] = gI[i];
+    nr.v[i] = V[i];
+    if (MODEL == 0) nr.ref[i] = R[i];
+    else { nr.m[i] = M[i]; nr.h[i] = H[i]; nr.nk[i] = Nk[i]; }
+  }
+  for (int i = tid; i < n_act; i += kSmallThreads) a.active_io[i] = act[i];
+  if (tid == 0) *a.count_io = n_act;
+  my_ev = __reduce_add_sync(0xffffffffu, my_ev);
+  my_sp = __reduce_add_sync(0xffffffffu, my_sp);
+  if (lane == 0) {
+    atomicAdd(&ev_total, static_cast<unsigned long long>(my_ev));
+    atomicAdd(&sp_total, static_cast<unsigned long long>(my_sp));
+  }
+  __syncthreads();
+  if (tid == 0) {
+    atomicAdd(a.events, ev_total);
+    atomicAdd(a.spikes, sp_total);
+  }
+}
+
+inline size_t small_net_smem(int model, int kind) {
+  const size_t g = kind == 1 ? 8 : 4;
+  const size_t per = 2 * g + 4 + (model == 1 ? 12 : 0) + 4 + 4 + 4 + (model == 0 ? 1 : 0);
+  return per * kSmallMax;
 }
 
 }  // namespace bp

@@ -43,7 +43,7 @@ def _raster(r, n):
     return np.stack([inputs.unpack_bits(row, n) for row in r.cpu().numpy().view(np.uint32)])
 
 
-@pytest.mark.parametrize("n,steps", [(4000, 2000), (1000, 500), (12_345, 300)])
+@pytest.mark.parametrize("n,steps", [(4000, 2000), (1000, 500), (12_345, 300), (4096, 300)])
 def test_coba_lif_jit_fixed_bit_exact(orc, n, steps):
     net = CobaNetwork(n, conn="jit", fixed=True)
     raster = torch.zeros((steps, (n + 31) // 32), dtype=torch.int32, device="cuda")
@@ -62,7 +62,11 @@ def test_coba_lif_jit_fixed_bit_exact(orc, n, steps):
     assert events > 0
 
 
-def test_coba_lif_csr_fixed_bit_exact(orc):
+@pytest.mark.parametrize("small", [True, False])
+def test_coba_lif_csr_fixed_bit_exact(orc, small, monkeypatch):
+    """small: single-CTA time loop (k_small_net); else k_step + k_bin per step."""
+    if not small:
+        monkeypatch.setenv("BP_NO_SMALL_NET", "1")
     n, steps = 4000, 1000
     n_exc = 3200
     ipe, ixe, _ = inputs.random_csr(n_exc, n, 0.02, seed=1)
@@ -92,8 +96,11 @@ def test_coba_lif_f32_rule_t3(orc):
     assert abs(rate_got - rate_want) <= 0.01 * rate_want
 
 
+@pytest.mark.parametrize("small", [True, False])
 @pytest.mark.parametrize("fixed", [True, False])
-def test_coba_hh_csr(orc, fixed):
+def test_coba_hh_csr(orc, fixed, small, monkeypatch):
+    if not small:
+        monkeypatch.setenv("BP_NO_SMALL_NET", "1")
     n, steps = 4000, 400
     n_exc = 3200
     ipe, ixe, _ = inputs.random_csr(n_exc, n, 0.02, seed=11)
