@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <new>
+#include <utility>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -681,6 +682,25 @@ bp_status alloc_buckets(bp_network *net, cudaStream_t st) {
   return BP_OK;
 }
 
+// Launch with programmatic stream serialization (PDL): the kernel may be
+// scheduled while its predecessor drains; it waits (griddepcontrol.wait)
+// before reading the predecessor's results (step.cuh).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, size_t smem,
+                       cudaStream_t st, Args &&...args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = std::getenv("BP_NO_PDL") ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 // Bin the rows active[0..*count) into bucket parity `par`: block-aggregated
 // when the tile table fits in shared memory, else one atomic per event.
 bp_status launch_bin(bp_network *net, const int32_t *active, const int32_t *count, int par,
@@ -693,8 +713,8 @@ bp_status launch_bin(bp_network *net, const int32_t *active, const int32_t *coun
                                    200 * 1024));
       attr_set = true;
     }
-    bp::k_bin_sorted<<<net->sms, bp::kBinThreads, smem, st>>>(
-        net->conn, bin_target(net, par), active, count, net->counters + 1, net->n_tiles);
+    BP_CUDA(launch_pdl(bp::k_bin_sorted, net->sms, bp::kBinThreads, smem, st, net->conn,
+                       bin_target(net, par), active, count, net->counters + 1, net->n_tiles));
   } else {
     bp::k_bin_rows<<<grid_for_items(max_rows, net->sms), bp::kScatterThreads, 0, st>>>(
         net->conn, bin_target(net, par), active, count, net->counters + 1);
@@ -749,11 +769,11 @@ bp_status launch_step(bp_network *net, uint32_t *raster, cudaStream_t st,
   a.zero_count = net->count + 2 + (cp ^ 1);
   const int grid = static_cast<int>(net->n_tiles);
   if (d.model == BP_MODEL_LIF) {
-    if (d.g_kind == BP_OUT_FIX64) bp::k_step<0, 1><<<grid, bp::kStepThreads, 0, st>>>(a);
-    else bp::k_step<0, 0><<<grid, bp::kStepThreads, 0, st>>>(a);
+    if (d.g_kind == BP_OUT_FIX64) BP_CUDA(launch_pdl(bp::k_step<0, 1>, grid, bp::kStepThreads, 0, st, a));
+    else BP_CUDA(launch_pdl(bp::k_step<0, 0>, grid, bp::kStepThreads, 0, st, a));
   } else {   // HH is compute-latency-bound: 512 threads per tile
-    if (d.g_kind == BP_OUT_FIX64) bp::k_step<1, 1><<<grid, 512, 0, st>>>(a);
-    else bp::k_step<1, 0><<<grid, 512, 0, st>>>(a);
+    if (d.g_kind == BP_OUT_FIX64) BP_CUDA(launch_pdl(bp::k_step<1, 1>, grid, 512, 0, st, a));
+    else BP_CUDA(launch_pdl(bp::k_step<1, 0>, grid, 512, 0, st, a));
   }
   bp_status s = launched();
   if (s != BP_OK) return s;

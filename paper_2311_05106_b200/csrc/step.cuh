@@ -36,6 +36,15 @@
 
 namespace bp {
 
+// Programmatic dependent launch (sm_90+): let the next kernel in the stream
+// be scheduled while this one drains, and wait for the previous kernel's
+// completion + memory flush before touching its outputs.  No-ops when the
+// kernel was launched without the PDL attribute.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 constexpr int kTileShift = 12;
 constexpr int kTile = 1 << kTileShift;   // postsynaptic neurons per tile/block
 constexpr int kStepThreads = 256;        // 16 neurons per thread
@@ -466,6 +475,8 @@ k_step(StepArgs a) {
   const NeuronArgs &nr = a.nrn;
   const Policies pol = make_policies(nr.keep_frac);
 
+  pdl_trigger();
+  pdl_wait();               // state and buckets of the previous kernels are final
   Pass<MODEL, KIND> pa, pb;
   pass_load(pa, nr, base + 4 * tid, pol);
   pass_load(pb, nr, base + pstride + 4 * tid, pol);
@@ -540,6 +551,20 @@ k_bin_rows(ConnArgs conn, BinTarget out, const int32_t *active, const int32_t *c
 // Events that do not fit the shared staging area take the per-event path.
 constexpr int kBinThreads = 1024;
 constexpr int kBinStage = 12288;          // staged records per block
+
+#ifdef BP_BIN_TIMING
+__device__ unsigned long long g_bin_t[1024][6];
+#define BP_BIN_MARK(k)                                                       \
+  do {                                                                       \
+    if (threadIdx.x == 0) {                                                  \
+      unsigned long long t_;                                                 \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                \
+      g_bin_t[blockIdx.x][k] = t_;                                           \
+    }                                                                        \
+  } while (0)
+#else
+#define BP_BIN_MARK(k) do {} while (0)
+#endif
 
 __device__ __forceinline__ uint32_t stage_record(uint32_t proj, uint32_t loc) {
   return (proj ? kProjBit : 0u) | loc;    // loc < 2^31
@@ -817,11 +842,14 @@ k_bin_sorted(ConnArgs conn, BinTarget out, const int32_t *active, const int32_t 
   __shared__ unsigned long long block_ev;
   const int tid = threadIdx.x;
   const uint32_t lane = tid & 31u, warp = tid >> 5;
+  pdl_trigger();
+  pdl_wait();               // the active list of the producing kernel is final
   const int n_active = *count;
   // this block's contiguous share of the active rows
   const int per = (n_active + gridDim.x - 1) / gridDim.x;
   const int r_lo = min(n_active, static_cast<int>(blockIdx.x) * per);
   const int r_hi = min(n_active, r_lo + per);
+  BP_BIN_MARK(0);
   if (r_lo >= r_hi) return;
   for (uint32_t t = tid; t < n_tiles; t += kBinThreads) hist[t] = 0;
   if (tid == 0) { n_staged = 0; block_ev = 0; }
@@ -841,6 +869,7 @@ k_bin_sorted(ConnArgs conn, BinTarget out, const int32_t *active, const int32_t 
       ev += stage_rows_jit(conn, out, active, k0, r_hi, staged, &n_staged, hist);
   }
   __syncthreads();
+  BP_BIN_MARK(1);
   const int ns = min(n_staged, kBinStage);
 
   // B. tile offsets; one global slot claim per non-empty tile
@@ -852,6 +881,7 @@ k_bin_sorted(ConnArgs conn, BinTarget out, const int32_t *active, const int32_t 
   }
   __syncthreads();
 
+  BP_BIN_MARK(2);
   // C. counting sort by tile (hist[] becomes the running cursor)
   for (int i = tid; i < ns; i += kBinThreads) {
     const uint32_t rec = staged[i];
@@ -860,6 +890,7 @@ k_bin_sorted(ConnArgs conn, BinTarget out, const int32_t *active, const int32_t 
   }
   __syncthreads();
 
+  BP_BIN_MARK(3);
   // D. write the runs.  After the sort hist[t] is the END of tile t's run in
   //    sorted[], so the run begins at hist[t-1] (tiles are in order).
   for (int i = tid; i < ns; i += kBinThreads) {
@@ -874,6 +905,7 @@ k_bin_sorted(ConnArgs conn, BinTarget out, const int32_t *active, const int32_t 
   ev = __reduce_add_sync(0xffffffffu, ev);
   if (lane == 0 && ev) atomicAdd(&block_ev, static_cast<unsigned long long>(ev));
   __syncthreads();
+  BP_BIN_MARK(4);
   if (tid == 0 && block_ev && events) atomicAdd(events, block_ev);
 }
 

@@ -1,6 +1,6 @@
 # quick bench summary lines: fixed and fp32 modes
 for m in "" "--f32"; do
-  python bench.py --steps ${STEPS:-2000} --warmup 200 --no-cpu --no-e2e $m > gpurun_out/b$m.log 2>&1
+  python bench.py --steps ${STEPS:-2000} --warmup 200 --no-cpu --no-e2e $m $EXTRA > gpurun_out/b$m.log 2>&1
   python - "$m" <<'PY'
 import json, sys
 m = sys.argv[1]
