@@ -712,25 +712,41 @@ __device__ __forceinline__ uint32_t stage_rows_jit(const ConnArgs &c, const BinT
         const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
         const uint32_t pos0 = start + (incl - t);
         const uint32_t pos[4] = {pos0, pos0 + p1, pos0 + p2, pos0 + p3};
+        bool v[4];
         uint32_t n_valid = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) n_valid += __popc(__ballot_sync(0xffffffffu, pos[k] < seg_end));
+        for (int k = 0; k < 4; ++k) {
+          v[k] = pos[k] < seg_end;
+          n_valid += __popc(__ballot_sync(0xffffffffu, v[k]));
+        }
         int base = 0;
         if (lane == 0) base = atomicAdd(n_staged, static_cast<int>(n_valid));
-        base = __shfl_sync(0xffffffffu, base, 0);
+        base = __shfl_sync(0xffffffffu, base, 0) + static_cast<int>(4 * lane);
+        const uint32_t pbit = proj ? kProjBit : 0u;
+        if (base - static_cast<int>(4 * lane) + static_cast<int>(n_valid) <= kBinStage) {
+          // common case, warp-uniform: predicated stores + histogram atomics
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (pos[k] >= seg_end) continue;
-          const uint32_t loc = pos[k] - b.col_begin;
-          const int slot = base + static_cast<int>(4 * lane) + k;
-          if (slot < kBinStage) {
-            staged[slot] = stage_record(proj, loc);
-            atomicAdd(hist + (loc >> kTileShift), 1);
-          } else {
-            bin_event(b, proj, loc);
+          for (int k = 0; k < 4; ++k) {
+            if (v[k]) {
+              const uint32_t loc = pos[k] - b.col_begin;
+              staged[base + k] = pbit | loc;
+              atomicAdd(hist + (loc >> kTileShift), 1);
+            }
           }
-          ++ev;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (!v[k]) continue;
+            const uint32_t loc = pos[k] - b.col_begin;
+            if (base + k < kBinStage) {
+              staged[base + k] = pbit | loc;
+              atomicAdd(hist + (loc >> kTileShift), 1);
+            } else {
+              bin_event(b, proj, loc);
+            }
+          }
         }
+        ev += static_cast<uint32_t>(v[0]) + v[1] + v[2] + v[3];
         start += total;
         ++chunk;
       }
@@ -874,10 +890,23 @@ k_bin_sorted(ConnArgs conn, BinTarget out, const int32_t *active, const int32_t 
 
   // B. tile offsets; one global slot claim per non-empty tile
   block_exclusive_scan(hist, static_cast<int>(n_tiles), warp_sums);
-  for (uint32_t t = tid; t < n_tiles; t += kBinThreads) {
-    const int32_t begin = hist[t];
-    const int32_t end = (t + 1 < n_tiles) ? hist[t + 1] : ns;
-    gbase[t] = end > begin ? atomicAdd(out.out.cnt + t * kCntStride, end - begin) : 0;
+  BP_BIN_MARK(5);
+  // a thread's slot claims are independent: issue 4 before using any result
+  for (uint32_t t0 = tid; t0 < n_tiles; t0 += 4 * kBinThreads) {
+    int32_t base[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t t = t0 + u * kBinThreads;
+      base[u] = 0;
+      if (t < n_tiles) {
+        const int32_t begin = hist[t];
+        const int32_t end = (t + 1 < n_tiles) ? hist[t + 1] : ns;
+        if (end > begin) base[u] = atomicAdd(out.out.cnt + t * kCntStride, end - begin);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (t0 + u * kBinThreads < n_tiles) gbase[t0 + u * kBinThreads] = base[u];
   }
   __syncthreads();
 

@@ -40,6 +40,8 @@ int main() {
       ph[k] += v / 148; mx[k] = std::max(mx[k], v);
     }
     double end = 0; for (int i = 0; i < 148; ++i) end = std::max(end, (double)(t[i][4] - t0) / 1e3);
+    double scan = 0; for (int i = 0; i < 148; ++i) scan += (double)(t[i][5] - t[i][1]) / 1e3 / 148;
+    printf("scan %.1f us | ", scan);
     printf("event %.1f us | last block end %.1f us | start-skew avg %.1f max %.1f | A %.1f/%.1f B %.1f/%.1f C %.1f/%.1f D %.1f/%.1f (avg/max us)\n",
            ms * 1e3, end, ph[0], mx[0], ph[1], mx[1], ph[2], mx[2], ph[3], mx[3], ph[4], mx[4]);
   }
