@@ -285,7 +285,7 @@ def build_network(wl, world, rank, fixed, dev):
 
 
 def state_bytes_per_neuron(model, fixed):
-    g = 32 if fixed else 16
+    g = 32 if fixed is True else 16
     return (8 + 1 if model == "lif" else 32) + g + 0.125
 
 
@@ -306,7 +306,7 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     n_total = network_size(wl, world)
-    fixed = not args.f32
+    fixed = {"fix64": True, "fix32": "fix32", "f32": False}[args.g]
 
     net, csr = build_network(wl, world, rank, fixed, dev)
     n_local = net.part.col_end - net.part.col_begin
@@ -328,7 +328,7 @@ def run_ours(args):
     # warm-up (untimed)
     steps(args.warmup)
     barrier()
-    sp0, ev0 = net.counters()
+    sp0, ev0, _ = net.counters()
 
     # timed region: exactly K steps, CUDA events on the launching stream
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -339,7 +339,7 @@ def run_ours(args):
         stop.record(stream)
         barrier()
     ms = start.elapsed_time(stop)
-    sp1, ev1 = net.counters()
+    sp1, ev1, sat1 = net.counters()
     # per-kernel durations: an instrumented window of K more steps right after
     # (events recorded between the two kernels of a step; they also disable
     # the programmatic-launch overlap, so this window is slightly slower)
@@ -386,7 +386,7 @@ def run_ours(args):
         achieved = bytes_per_launch / upd_s / 1e9
         kname = ("k_small_net<%s,%s> (whole time loop in one CTA, state in shared memory)"
                  if small else "k_step<%s,%s> (fused: bucket counts -> Expon+COBA+neuron -> "
-                 "spike bits + active list)") % (spec["model"].upper(), "fix64" if fixed else "f32")
+                 "spike bits + active list)") % (spec["model"].upper(), args.g)
         roofline = {"kernel": kname, "bound": "hbm", "achieved": achieved,
                     "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                     "traffic": None, "peak_source": peak_kind,
@@ -405,11 +405,15 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": spec["scaling"], "vs_baseline": None,
-        "dtype": "i64fix+f32" if fixed else "f32", "data": "synthetic",
+        "dtype": {"fix64": "i64fix+f32", "fix32": "i32fix+f32", "f32": "f32"}[args.g],
+        "data": "synthetic",
         "config": {"workload": wl, "description": spec["cfg"], "n_total": n_total,
                    "n_per_gpu": n_local, "model": spec["model"], "connectivity": spec["conn"],
                    "fan_in": 80, "p": 80.0 / n_total, "dt_ms": DT_MS,
-                   "g": "int64 fixed point 2^-32" if fixed else "fp32",
+                   "g": {"fix64": "int64 fixed point 2^-32 (rule F1)",
+                         "fix32": "int32 fixed point 2^-%d (rule F2), saturations: %d" % (
+                             20 if spec["model"] == "lif" else 16, sat1),
+                         "f32": "fp32 (rule T3)"}[args.g],
                    "parallelism": f"postsynaptic partition x{world}",
                    "l2": (f"state {state_mb:.0f} MB/GPU > 2 x 126 MB L2: no flush needed"
                           if state_mb > 252 else
@@ -439,7 +443,8 @@ def run_e2e(args, wl, fixed, dev):
     from paper_2311_05106_b200 import inputs
     net, _ = build_network(wl, 1, 0, fixed, dev)
     n = net.n
-    host = {k: torch.empty_like(v, device="cpu").pin_memory() for k, v in net.state.items()}
+    host = {k: torch.empty_like(v, device="cpu").pin_memory() for k, v in net.state.items()
+            if isinstance(v, torch.Tensor)}
     if NETWORKS[wl]["model"] == "lif":
         host["v"].copy_(torch.from_numpy(inputs.lif_v0(n)))
         for k in ("g_e", "g_i", "ref"):
@@ -454,7 +459,7 @@ def run_e2e(args, wl, fixed, dev):
     stream = torch.cuda.current_stream()
     net.run(args.warmup)
     torch.cuda.synchronize()
-    sp0, ev0 = net.counters()
+    sp0, ev0, _ = net.counters()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     start.record(stream)
@@ -464,7 +469,7 @@ def run_e2e(args, wl, fixed, dev):
     stop.record(stream)
     stop.synchronize()
     ms = start.elapsed_time(stop)
-    sp1, ev1 = net.counters()
+    sp1, ev1, sat1 = net.counters()
     return {"value": (ev1 - ev0) / (ms / 1e3), "unit": UNIT,
             "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": 4,
             "note": "initial state H2D (pinned) amortised over the K steps; per-step "
@@ -594,7 +599,10 @@ def main():
     ap.add_argument("--steps", type=int, default=10_000)
     ap.add_argument("--warmup", type=int, default=200)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--f32", action="store_true", help="fp32 conductances (fp32 atomics)")
+    ap.add_argument("--g", choices=["fix64", "fix32", "f32"], default="fix32",
+                    help="conductance representation: int64 2^-32 (rule F1), int32 "
+                         "2^-F (rule F2) or fp32 (rule T3 parity)")
+    ap.add_argument("--f32", action="store_true", help="alias of --g f32")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
     ap.add_argument("--workload", choices=list(NETWORKS) + ["csrmv", "jitmv"],
@@ -606,6 +614,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.f32:
+        args.g = "f32"
     if args.impl == "reference":
         run_reference(args)
     elif args.workload in ("csrmv", "jitmv"):

@@ -62,7 +62,10 @@ typedef enum {
   BP_ERR_CUDA = 5         /* a CUDA runtime error (launch or sticky)           */
 } bp_status;
 
-typedef enum { BP_OUT_F32 = 0, BP_OUT_FIX64 = 1 } bp_out_kind;
+/* Output / state accumulator kinds.  BP_OUT_FIX32 is a STATE kind only
+ * (network and neuron conductances): int32 with g_frac_bits fractional bits,
+ * a step's increments summed exactly and added with saturation (rule F2). */
+typedef enum { BP_OUT_F32 = 0, BP_OUT_FIX64 = 1, BP_OUT_FIX32 = 2 } bp_out_kind;
 
 #define BP_ACCUMULATE 1u
 
@@ -177,8 +180,8 @@ typedef struct {
   float *v;
   void *g_exc;
   void *g_inh;
-  int32_t g_kind; /* bp_out_kind */
-  int32_t reserved;
+  int32_t g_kind;      /* bp_out_kind */
+  int32_t g_frac_bits; /* BP_OUT_FIX32 only: fractional bits F (0 => 20) */
   uint8_t *ref;
   float *m, *h, *n_gate;
 } bp_neuron_state;
@@ -247,8 +250,9 @@ bp_status bp_network_scatter(bp_network *net, bp_stream stream);
 bp_status bp_network_update(bp_network *net, uint32_t *raster_row,
                             bp_stream stream);
 /* Device counters since create: [0] = local spikes, [1] = synaptic events
- * delivered into local neurons.  Copies into host uint64[2]; synchronises
- * `stream`. */
+ * delivered into local neurons, [2] = saturated BP_OUT_FIX32 conductance
+ * updates (0 in a well-scaled run).  Copies into host uint64[3];
+ * synchronises `stream`. */
 bp_status bp_network_counters(bp_network *net, uint64_t *host_out,
                               bp_stream stream);
 /* Per-kernel timing of the next bp_network_step calls (at most max_steps

@@ -32,7 +32,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "bp_oracle.c")
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
-OUT_F64, OUT_FIX, OUT_F32 = 0, 1, 2
+OUT_F64, OUT_FIX, OUT_F32, OUT_FIX32 = 0, 1, 2, 3
 LAW_HOMO, LAW_UNIFORM, LAW_NORMAL = 0, 1, 2
 LAWS = {"homo": LAW_HOMO, "uniform": LAW_UNIFORM, "normal": LAW_NORMAL}
 
@@ -94,6 +94,9 @@ def lib():
                                     P, P, i32, P]
         _lib.or_expf.argtypes = [f32]
         _lib.or_expf.restype = f32
+        _lib.or_set_fix32_bits.argtypes = [i32]
+        _lib.or_fix32_add.argtypes = [P, P, i64]
+        _lib.or_fix32_add.restype = i64
     return _lib
 
 
@@ -171,7 +174,18 @@ def jit_materialize(spec: JitSpec, n_rows: int, n_cols: int):
 
 def _out_buf(n: int, out_kind: int):
     return np.zeros(n, {OUT_F64: np.float64, OUT_FIX: np.int64,
-                        OUT_F32: np.float32}[out_kind])
+                        OUT_F32: np.float32, OUT_FIX32: np.int64}[out_kind])
+
+
+def set_fix32_bits(bits: int):
+    """Rule F2: fractional bits of the 32-bit fixed-point conductances."""
+    lib().or_set_fix32_bits(int(bits))
+
+
+def fix32_add(g: np.ndarray, inc: np.ndarray) -> int:
+    """Rule F2: g (int32) += inc (int64, exact step sum) with saturation."""
+    assert g.dtype == np.int32 and inc.dtype == np.int64
+    return int(lib().or_fix32_add(_p(g), _p(inc), g.shape[0]))
 
 
 def event_csrmv(indptr, indices, data, w_homo, n_rows, n_cols, events,
@@ -229,7 +243,7 @@ def hh_params(dt=0.1, tau_e=5.0, tau_i=10.0, i_ext=0.0) -> HHParams:
 def lif_step(params: LifParams, v, g_e, g_i, ref):
     """In-place rule N1 on numpy arrays; returns the uint8 spike vector."""
     n = v.shape[0]
-    g_kind = 1 if g_e.dtype == np.int64 else 0
+    g_kind = {np.dtype(np.int64): 1, np.dtype(np.int32): 2}.get(g_e.dtype, 0)
     ev = np.zeros(n, np.uint8)
     lib().or_lif_step(ctypes.byref(params), n, _p(v), _p(g_e), _p(g_i),
                       g_kind, _p(ref), _p(ev))
@@ -238,7 +252,7 @@ def lif_step(params: LifParams, v, g_e, g_i, ref):
 
 def hh_step(params: HHParams, v, m, h, nk, g_e, g_i):
     n = v.shape[0]
-    g_kind = 1 if g_e.dtype == np.int64 else 0
+    g_kind = {np.dtype(np.int64): 1, np.dtype(np.int32): 2}.get(g_e.dtype, 0)
     ev = np.zeros(n, np.uint8)
     lib().or_hh_step(ctypes.byref(params), n, _p(v), _p(m), _p(h), _p(nk),
                      _p(g_e), _p(g_i), g_kind, _p(ev))
@@ -275,21 +289,27 @@ def run_network(model: str, params, state: dict, proj_e: Projection,
     n_total = state["spikes"].shape[0]
     if col_end is None:
         col_end = n_total
+    fix32 = state["g_e"].dtype == np.int32
     fixed = state["g_e"].dtype == np.int64
-    kind = OUT_FIX if fixed else OUT_F32
+    kind = OUT_FIX32 if fix32 else (OUT_FIX if fixed else OUT_F32)
     raster = np.zeros((n_steps, col_end - col_begin), np.uint8) if record else None
     counts = np.zeros(n_steps, np.int64)
     for step in range(n_steps):
         spikes = state["spikes"]
         for proj, g in ((proj_e, state["g_e"]), (proj_i, state["g_i"])):
             ev = spikes[proj.row0:proj.row0 + proj.n_rows]
+            # rule F2: the step's increments are summed exactly, then added
+            # to the int32 conductance with saturation
+            acc = np.zeros(g.shape[0], np.int64) if fix32 else g
             if proj.jit is not None:
                 jit_event_mv(proj.jit, proj.n_rows, n_total, ev, col_begin,
-                             col_end, kind, out=g)
+                             col_end, kind, out=acc)
             else:
                 ip, ix, dat = proj.csr
                 event_csrmv(ip, ix, dat, proj.w_homo, proj.n_rows,
-                            col_end - col_begin, ev, kind, out=g)
+                            col_end - col_begin, ev, kind, out=acc)
+            if fix32:
+                fix32_add(g, acc)
         if model == "lif":
             local = lif_step(params, state["v"], state["g_e"], state["g_i"],
                              state["ref"])

@@ -29,6 +29,11 @@
 #define OR_OUT_F64 0   /* accumulate (double)w                               */
 #define OR_OUT_FIX 1   /* accumulate llrint(w * 2^32) into int64 (rule F1)   */
 #define OR_OUT_F32 2   /* accumulate w in float, sequentially (network f32)  */
+#define OR_OUT_FIX32 3 /* accumulate llrint(w * 2^F) into int64 (rule F2)    */
+
+/* Rule F2 (32-bit fixed point): F fractional bits, set per run. */
+static int g_fix32_bits = 20;
+void or_set_fix32_bits(int bits) { g_fix32_bits = bits; }
 
 #define OR_LAW_HOMO 0
 #define OR_LAW_UNIFORM 1
@@ -177,6 +182,8 @@ static void accumulate(int out_kind, void *out, double *abs_out, int64_t c,
     ((double *)out)[c] += (double)w;
   } else if (out_kind == OR_OUT_FIX) {
     ((int64_t *)out)[c] += or_quantize(w);
+  } else if (out_kind == OR_OUT_FIX32) {
+    ((int64_t *)out)[c] += llrint(ldexp((double)w, g_fix32_bits));
   } else {
     ((float *)out)[c] += w;
   }
@@ -250,6 +257,23 @@ void or_jit_event_mv(uint64_t seed, uint32_t K, uint32_t L, int law, float w0,
 }
 
 /* ------------------------------------------------------------------------
+ * Rule F2: a step's increments (summed exactly in int64, OR_OUT_FIX32) are
+ * added to the int32 conductance with saturation at the int32 range.
+ * Returns the number of saturated entries (a diagnostic; 0 in any sane run).
+ * Pinned by: fixed-point vs fp64 recursion bound and the saturation test.
+ * ---------------------------------------------------------------------- */
+int64_t or_fix32_add(int32_t *g, const int64_t *inc, int64_t n) {
+  int64_t sat = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t v = (int64_t)g[i] + inc[i];
+    if (v > INT32_MAX) { v = INT32_MAX; ++sat; }
+    if (v < INT32_MIN) { v = INT32_MIN; ++sat; }
+    g[i] = (int32_t)v;
+  }
+  return sat;
+}
+
+/* ------------------------------------------------------------------------
  * Rule N1: one step of exponential synapse (AlignPost) + COBA + LIF with
  * refractory period for neurons [0, n).
  *   LIF: tau dV/dt = -(V - V_rest) + R G;  spike if V > V_th,
@@ -265,6 +289,8 @@ void or_jit_event_mv(uint64_t seed, uint32_t K, uint32_t L, int law, float w0,
  *   Vc   = fmaf(V - Vinf, alpha_V, Vinf)
  * g_kind 1 (fixed point, rule F1): g = (float)ldexp((double)g_fix, -32);
  *   g_fix' = llrint((double)g_fix * alpha_d).   g_kind 0: g' = g*(float)alpha.
+ * g_kind 2 (32-bit fixed point, rule F2): g = (float)ldexp((double)g, -F);
+ *   g' = (g * A + 2^31) >> 32 with A = llrint(alpha_d * 2^32).
  * Writes events[i] = 1 for a spike, else 0.
  * Pinned by: subthreshold closed form V_n = V_rest + (V0-V_rest) alpha^n,
  * the 139-step first passage and 189-step period of an unconnected neuron,
@@ -280,6 +306,7 @@ typedef struct {
 
 static float g_read(int g_kind, const void *g, int64_t i) {
   if (g_kind == 1) return (float)ldexp((double)((const int64_t *)g)[i], -32);
+  if (g_kind == 2) return (float)ldexp((double)((const int32_t *)g)[i], -g_fix32_bits);
   return ((const float *)g)[i];
 }
 
@@ -287,6 +314,12 @@ static void g_decay(int g_kind, void *g, int64_t i, double alpha) {
   if (g_kind == 1) {
     int64_t *gf = (int64_t *)g;
     gf[i] = llrint((double)gf[i] * alpha);
+  } else if (g_kind == 2) {
+    /* rule F2 decay: A = llrint(alpha * 2^32); g' = (g * A + 2^31) >> 32
+     * (integer multiply-shift, round half up; arithmetic shift) */
+    int32_t *gf = (int32_t *)g;
+    int64_t A = llrint(alpha * 4294967296.0);
+    gf[i] = (int32_t)(((int64_t)gf[i] * A + ((int64_t)1 << 31)) >> 32);
   } else {
     float *gs = (float *)g;
     gs[i] = gs[i] * (float)alpha;

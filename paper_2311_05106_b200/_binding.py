@@ -16,7 +16,7 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libbp.so")
 
-OUT_F32, OUT_FIX64 = 0, 1
+OUT_F32, OUT_FIX64, OUT_FIX32 = 0, 1, 2
 ACCUMULATE = 1
 LAW_HOMO, LAW_UNIFORM, LAW_NORMAL = 0, 1, 2
 MODEL_LIF, MODEL_HH = 0, 1
@@ -58,7 +58,7 @@ class NeuronParams(ctypes.Structure):
 class NeuronState(ctypes.Structure):
     _fields_ = [("v", ctypes.c_void_p), ("g_exc", ctypes.c_void_p),
                 ("g_inh", ctypes.c_void_p), ("g_kind", ctypes.c_int32),
-                ("reserved", ctypes.c_int32), ("ref", ctypes.c_void_p),
+                ("g_frac_bits", ctypes.c_int32), ("ref", ctypes.c_void_p),
                 ("m", ctypes.c_void_p), ("h", ctypes.c_void_p),
                 ("n_gate", ctypes.c_void_p)]
 
@@ -150,7 +150,9 @@ def _out_kind(out: torch.Tensor) -> int:
         return OUT_F32
     if out.dtype == torch.int64:
         return OUT_FIX64
-    raise BpError(f"output dtype {out.dtype}: float32 or int64 (fixed point)")
+    if out.dtype == torch.int32:
+        return OUT_FIX32            # conductance state only (rule F2)
+    raise BpError(f"output dtype {out.dtype}: float32, int64 or int32 (fixed point)")
 
 
 def _cuda(*ts):
@@ -287,6 +289,7 @@ def _state_struct(state: dict) -> NeuronState:
     s.g_exc = g.data_ptr()
     s.g_inh = state["g_i"].data_ptr()
     s.g_kind = _out_kind(g)
+    s.g_frac_bits = int(state.get("frac_bits", 0))
     for k, f in (("ref", "ref"), ("m", "m"), ("h", "h"), ("n", "n_gate")):
         if state.get(k) is not None:
             setattr(s, f, state[k].data_ptr())
@@ -366,10 +369,11 @@ class Network:
         _check(lib().bp_network_update(self._h, _ptr(raster_row), _stream(stream)))
 
     def counters(self, stream=None):
-        out = (ctypes.c_uint64 * 2)()
+        """-> (local spikes, synaptic events delivered, saturated FIX32 updates)."""
+        out = (ctypes.c_uint64 * 3)()
         _check(lib().bp_network_counters(self._h, ctypes.cast(out, ctypes.c_void_p),
                                          _stream(stream)))
-        return int(out[0]), int(out[1])
+        return int(out[0]), int(out[1]), int(out[2])
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:

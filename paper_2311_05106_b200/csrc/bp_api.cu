@@ -461,8 +461,10 @@ bp_status fill_neuron_args(const bp_neuron_params *p, const bp_neuron_state *st,
   BP_CHECK(p != nullptr && st != nullptr, BP_ERR_INVALID_ARG, "NULL params/state");
   BP_CHECK(p->model == BP_MODEL_LIF || p->model == BP_MODEL_HH, BP_ERR_INVALID_ARG,
            "model %d", p->model);
-  BP_CHECK(st->g_kind == BP_OUT_F32 || st->g_kind == BP_OUT_FIX64, BP_ERR_INVALID_ARG,
-           "g_kind %d", st->g_kind);
+  BP_CHECK(st->g_kind == BP_OUT_F32 || st->g_kind == BP_OUT_FIX64 || st->g_kind == BP_OUT_FIX32,
+           BP_ERR_INVALID_ARG, "g_kind %d", st->g_kind);
+  BP_CHECK(st->g_kind != BP_OUT_FIX32 || (st->g_frac_bits >= 0 && st->g_frac_bits <= 30),
+           BP_ERR_INVALID_ARG, "g_frac_bits %d not in [0, 30]", st->g_frac_bits);
   BP_CHECK(n >= 0 && n <= kMaxDim, BP_ERR_SHAPE, "n=%lld", (long long)n);
   if (n > 0) {
     BP_CHECK(st->v && st->g_exc && st->g_inh, BP_ERR_INVALID_ARG, "NULL v/g");
@@ -488,6 +490,11 @@ bp_status fill_neuron_args(const bp_neuron_params *p, const bp_neuron_state *st,
   a->v = st->v; a->g_e = st->g_exc; a->g_i = st->g_inh; a->ref = st->ref;
   a->m = st->m; a->h = st->h; a->nk = st->n_gate;
   a->n = n;
+  a->frac_bits = st->g_frac_bits ? st->g_frac_bits : 20;
+  a->inv_scale = std::ldexp(1.0, -a->frac_bits);
+  a->inv_scale32 = static_cast<float>(a->inv_scale);
+  a->a_e_q = llrint(p->alpha_e * 4294967296.0);   // rule F2 decay factors
+  a->a_i_q = llrint(p->alpha_i * 4294967296.0);
   return BP_OK;
 }
 
@@ -496,9 +503,11 @@ void launch_neuron(const bp::NeuronArgs &a, int model, int g_kind, cudaStream_t 
   const int blocks = static_cast<int>((a.n + 255) / 256);
   if (model == BP_MODEL_LIF) {
     if (g_kind == BP_OUT_FIX64) bp::k_lif<1><<<blocks, 256, 0, st>>>(a);
+    else if (g_kind == BP_OUT_FIX32) bp::k_lif<2><<<blocks, 256, 0, st>>>(a);
     else bp::k_lif<0><<<blocks, 256, 0, st>>>(a);
   } else {
     if (g_kind == BP_OUT_FIX64) bp::k_hh<1><<<blocks, 256, 0, st>>>(a);
+    else if (g_kind == BP_OUT_FIX32) bp::k_hh<2><<<blocks, 256, 0, st>>>(a);
     else bp::k_hh<0><<<blocks, 256, 0, st>>>(a);
   }
 }
@@ -740,6 +749,13 @@ bp_status bin_spike_range(bp_network *net, int64_t w_begin, int64_t w_end, int p
   return launch_bin(net, active, count, par, last - first, st);
 }
 
+// Quantised homogeneous weight of the network's conductance kind.
+long long net_q(const bp_network *net, float w) {
+  if (net->d.g_kind == BP_OUT_FIX32)
+    return llrint(std::ldexp(static_cast<double>(w), net->neuron.frac_bits));
+  return llrint(static_cast<double>(w) * 4294967296.0);
+}
+
 bp_status launch_step(bp_network *net, uint32_t *raster, cudaStream_t st,
                       int32_t *step_spikes = nullptr, cudaEvent_t mid = nullptr) {
   const bp_network_desc &d = net->d;
@@ -751,8 +767,9 @@ bp_status launch_step(bp_network *net, uint32_t *raster, cudaStream_t st,
   a.conn = net->conn;
   a.w_e = d.w_exc;
   a.w_i = d.w_inh;
-  a.q_e = llrint(static_cast<double>(d.w_exc) * 4294967296.0);
-  a.q_i = llrint(static_cast<double>(d.w_inh) * 4294967296.0);
+  a.q_e = net_q(net, d.w_exc);
+  a.q_i = net_q(net, d.w_inh);
+  a.saturated = net->counters + 2;
   a.in = net->bk[net->bpar];
   a.out = bin_target(net, net->bpar ^ 1);
   a.n_tiles = net->n_tiles;
@@ -770,9 +787,11 @@ bp_status launch_step(bp_network *net, uint32_t *raster, cudaStream_t st,
   const int grid = static_cast<int>(net->n_tiles);
   if (d.model == BP_MODEL_LIF) {
     if (d.g_kind == BP_OUT_FIX64) BP_CUDA(launch_pdl(bp::k_step<0, 1>, grid, bp::kStepThreads, 0, st, a));
+    else if (d.g_kind == BP_OUT_FIX32) BP_CUDA(launch_pdl(bp::k_step<0, 2>, grid, bp::kStepThreads, 0, st, a));
     else BP_CUDA(launch_pdl(bp::k_step<0, 0>, grid, bp::kStepThreads, 0, st, a));
   } else {   // HH is compute-latency-bound: 512 threads per tile
     if (d.g_kind == BP_OUT_FIX64) BP_CUDA(launch_pdl(bp::k_step<1, 1>, grid, 512, 0, st, a));
+    else if (d.g_kind == BP_OUT_FIX32) BP_CUDA(launch_pdl(bp::k_step<1, 2>, grid, 512, 0, st, a));
     else BP_CUDA(launch_pdl(bp::k_step<1, 0>, grid, 512, 0, st, a));
   }
   bp_status s = launched();
@@ -818,8 +837,9 @@ bp_status small_step(bp_network *net, int64_t n_steps, uint32_t *raster, int32_t
   a.conn = net->conn;
   a.w_e = d.w_exc;
   a.w_i = d.w_inh;
-  a.q_e = llrint(static_cast<double>(d.w_exc) * 4294967296.0);
-  a.q_i = llrint(static_cast<double>(d.w_inh) * 4294967296.0);
+  a.q_e = net_q(net, d.w_exc);
+  a.q_i = net_q(net, d.w_inh);
+  a.saturated = net->counters + 2;
   a.n_steps = n_steps;
   a.step_counts = counts_out ? net->small_steps : nullptr;
   a.active_io = net->small_active;
@@ -834,9 +854,13 @@ bp_status small_step(bp_network *net, int64_t n_steps, uint32_t *raster, int32_t
   if (ev) BP_CUDA(cudaEventRecord(ev[0], st));
   bp_status s;
   if (d.model == BP_MODEL_LIF)
-    s = d.g_kind == BP_OUT_FIX64 ? launch_small<0, 1>(a, st) : launch_small<0, 0>(a, st);
+    s = d.g_kind == BP_OUT_FIX64   ? launch_small<0, 1>(a, st)
+        : d.g_kind == BP_OUT_FIX32 ? launch_small<0, 2>(a, st)
+                                   : launch_small<0, 0>(a, st);
   else
-    s = d.g_kind == BP_OUT_FIX64 ? launch_small<1, 1>(a, st) : launch_small<1, 0>(a, st);
+    s = d.g_kind == BP_OUT_FIX64   ? launch_small<1, 1>(a, st)
+        : d.g_kind == BP_OUT_FIX32 ? launch_small<1, 2>(a, st)
+                                   : launch_small<1, 0>(a, st);
   if (s != BP_OK) return s;
   if (ev) {   // the single launch is the "update" interval; no binning kernel
     BP_CUDA(cudaEventRecord(ev[1], st));
@@ -1040,7 +1064,7 @@ bp_status bp_network_counters(bp_network *net, uint64_t *host_out, bp_stream str
   if (s != BP_OK) return s;
   BP_CHECK(net != nullptr && host_out != nullptr, BP_ERR_INVALID_ARG, "NULL argument");
   cudaStream_t st = as_stream(stream);
-  BP_CUDA(cudaMemcpyAsync(host_out, net->counters, 2 * sizeof(uint64_t),
+  BP_CUDA(cudaMemcpyAsync(host_out, net->counters, 3 * sizeof(uint64_t),
                           cudaMemcpyDeviceToHost, st));
   BP_CUDA(cudaStreamSynchronize(st));
   return BP_OK;

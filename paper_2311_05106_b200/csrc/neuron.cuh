@@ -36,24 +36,48 @@ struct NeuronArgs {
   int32_t *count;
   int32_t active_base;
   float keep_frac;       // L2 evict_last fraction for g (0: no hints)
+  int32_t frac_bits;     // BP_OUT_FIX32: fractional bits F
+  double inv_scale;      // 2^-F
+  float inv_scale32;     // 2^-F (exact in fp32)
+  long long a_e_q, a_i_q;  // rule F2 decay: llrint(alpha * 2^32)
 };
 
+// Rule F2 decay: g' = (g * A + 2^31) >> 32 (round half up).  With
+// A = 2^32 + A' (A' = A - 2^32 < 0 fits int32) this is exactly
+// g + hi32(g * A' + 2^31): one IMAD.WIDE (s32 x s32) and a 64-bit add.
+__device__ __forceinline__ int32_t fix32_decay(int32_t g, long long A) {
+  const int32_t a_m = static_cast<int32_t>(A - (1ll << 32));
+  const long long p = static_cast<long long>(g) * a_m + (1ll << 31);
+  return g + static_cast<int32_t>(p >> 32);
+}
+
+// Rule F2 read: fl32(g * 2^-F) = fl32(g) * 2^-F (power-of-two scaling is
+// exact for F <= 30), so one I2F + one FMUL instead of fp64.
+__device__ __forceinline__ float fix32_read(int32_t g, float inv_scale32) {
+  return __fmul_rn(__int2float_rn(g), inv_scale32);
+}
+
 template <int KIND>
-__device__ __forceinline__ float g_load(const void *g, int64_t i, uint64_t pol) {
+__device__ __forceinline__ float g_load(const void *g, int64_t i, uint64_t pol,
+                                        float inv_scale = 0.f) {
   if (KIND == 1) {
     const long long q = ld_s64(static_cast<const long long *>(g) + i, pol);
     return __double2float_rn(__dmul_rn(__ll2double_rn(q), 0x1p-32));
   }
+  if (KIND == 2) return fix32_read(static_cast<const int32_t *>(g)[i], inv_scale);
   return ld_f32(static_cast<const float *>(g) + i, pol);
 }
 
 // g' = decay(g): fixed point llrint(g * alpha) in fp64 (rule F1), fp32 g * fl32(alpha).
 template <int KIND>
 __device__ __forceinline__ void g_decay(void *g, int64_t i, double a64, float a32,
-                                        uint64_t pol) {
+                                        long long a_q, uint64_t pol) {
   if (KIND == 1) {
     long long *q = static_cast<long long *>(g) + i;
     st_s64(q, __double2ll_rn(__dmul_rn(__ll2double_rn(ld_s64(q, pol)), a64)), pol);
+  } else if (KIND == 2) {
+    int32_t *q = static_cast<int32_t *>(g) + i;
+    *q = fix32_decay(*q, a_q);
   } else {
     float *f = static_cast<float *>(g) + i;
     st_f32(f, __fmul_rn(ld_f32(f, pol), a32), pol);
@@ -97,6 +121,11 @@ __global__ void __launch_bounds__(256) k_lif(NeuronArgs a) {
       qI = ld_s64(static_cast<const long long *>(a.g_i) + i, pol.keep);
       gE = __double2float_rn(__dmul_rn(__ll2double_rn(qE), 0x1p-32));
       gI = __double2float_rn(__dmul_rn(__ll2double_rn(qI), 0x1p-32));
+    } else if (KIND == 2) {
+      qE = static_cast<const int32_t *>(a.g_e)[i];
+      qI = static_cast<const int32_t *>(a.g_i)[i];
+      gE = fix32_read(static_cast<int32_t>(qE), a.inv_scale32);
+      gI = fix32_read(static_cast<int32_t>(qI), a.inv_scale32);
     } else {
       fE = ld_f32(static_cast<const float *>(a.g_e) + i, pol.keep);
       fI = ld_f32(static_cast<const float *>(a.g_i) + i, pol.keep);
@@ -120,6 +149,9 @@ __global__ void __launch_bounds__(256) k_lif(NeuronArgs a) {
              __double2ll_rn(__dmul_rn(__ll2double_rn(qE), a.alpha_e)), pol.keep);
       st_s64(static_cast<long long *>(a.g_i) + i,
              __double2ll_rn(__dmul_rn(__ll2double_rn(qI), a.alpha_i)), pol.keep);
+    } else if (KIND == 2) {
+      static_cast<int32_t *>(a.g_e)[i] = fix32_decay(static_cast<int32_t>(qE), a.a_e_q);
+      static_cast<int32_t *>(a.g_i)[i] = fix32_decay(static_cast<int32_t>(qI), a.a_i_q);
     } else {
       st_f32(static_cast<float *>(a.g_e) + i, __fmul_rn(fE, a.alpha_e32), pol.keep);
       st_f32(static_cast<float *>(a.g_i) + i, __fmul_rn(fI, a.alpha_i32), pol.keep);
@@ -161,8 +193,8 @@ __global__ void __launch_bounds__(256) k_hh(NeuronArgs a) {
   bool spike = false;
   if (i < a.n) {
     const float V = a.v[i], M = a.m[i], H = a.h[i], Nk = a.nk[i];
-    const float gE = g_load<KIND>(a.g_e, i, pol.keep);
-    const float gI = g_load<KIND>(a.g_i, i, pol.keep);
+    const float gE = g_load<KIND>(a.g_e, i, pol.keep, a.inv_scale32);
+    const float gI = g_load<KIND>(a.g_i, i, pol.keep, a.inv_scale32);
     const float x = V - a.v_t;
     const float am = 0.32f * hh_efrac(13.0f - x, 4.0f);
     const float bm = 0.28f * hh_efrac(x - 40.0f, 5.0f);
@@ -188,8 +220,8 @@ __global__ void __launch_bounds__(256) k_hh(NeuronArgs a) {
     a.m[i] = m_new;
     a.h[i] = h_new;
     a.nk[i] = n_new;
-    g_decay<KIND>(a.g_e, i, a.alpha_e, a.alpha_e32, pol.keep);
-    g_decay<KIND>(a.g_i, i, a.alpha_i, a.alpha_i32, pol.keep);
+    g_decay<KIND>(a.g_e, i, a.alpha_e, a.alpha_e32, a.a_e_q, pol.keep);
+    g_decay<KIND>(a.g_i, i, a.alpha_i, a.alpha_i32, a.a_i_q, pol.keep);
   }
   emit_spikes(a, i, spike);
 }

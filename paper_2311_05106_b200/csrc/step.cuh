@@ -168,7 +168,8 @@ struct StepArgs {
   int model;                // BP_MODEL_LIF / BP_MODEL_HH
   ConnArgs conn;
   float w_e, w_i;           // homogeneous weights (fp32 mode)
-  long long q_e, q_i;       // quantised weights (fixed point)
+  long long q_e, q_i;       // quantised weights (fixed point: 2^32 or 2^F scale)
+  unsigned long long *saturated;   // rule F2 saturations
   Buckets in;               // events for this step (consumed, then cleared)
   BinTarget out;            // events for the next step
   uint32_t n_tiles;
@@ -218,6 +219,33 @@ struct GVec<1> {
                  ::"l"(p + 2), "l"(v[2]), "l"(v[3]), "l"(pol) : "memory");
   }
 };
+
+template <>
+struct GVec<2> {
+  int32_t v[4];
+  __device__ __forceinline__ void load(const void *g, int64_t i, uint64_t pol) {
+    const int32_t *p = static_cast<const int32_t *>(g) + i;
+    asm volatile("ld.global.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "l"(p), "l"(pol));
+  }
+  __device__ __forceinline__ void store(void *g, int64_t i, uint64_t pol) const {
+    int32_t *p = static_cast<int32_t *>(g) + i;
+    asm volatile("st.global.L2::cache_hint.v4.s32 [%0], {%1,%2,%3,%4}, %5;"
+                 ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "l"(pol) : "memory");
+  }
+};
+
+// Rule F2: g32 += cnt * q with saturation at the int32 range (counted).
+__device__ __forceinline__ float g_fold32(int32_t &g, int32_t cnt, long long q,
+                                          float inv_scale, uint32_t &sat) {
+  // branch-free: cnt * q fits int64; clamp to the int32 range, count clamps
+  const long long v = static_cast<long long>(g) + static_cast<long long>(cnt) * q;
+  const long long c = v > 2147483647ll ? 2147483647ll : (v < -2147483648ll ? -2147483648ll : v);
+  sat += c != v;
+  g = static_cast<int32_t>(c);
+  return fix32_read(g, inv_scale);
+}
+__device__ __forceinline__ void g_after32(int32_t &g, long long a_q) { g = fix32_decay(g, a_q); }
 
 // g_n = (pre-decayed g) + increments of this step; returns the fp32 value
 // the neuron update reads, leaves the state value in `g` (rule F1 / fp32).
@@ -328,7 +356,8 @@ __device__ __forceinline__ void pass_load(Pass<MODEL, KIND> &p, const NeuronArgs
 template <int MODEL, int KIND>
 __device__ __forceinline__ uint32_t pass_update(Pass<MODEL, KIND> &p, const StepArgs &a,
                                                 const int32_t *cnt_e, const int32_t *cnt_i,
-                                                int j0, int64_t i0, const Policies &pol) {
+                                                int j0, int64_t i0, const Policies &pol,
+                                                uint32_t &sat) {
   const NeuronArgs &nr = a.nrn;
   uint32_t nib = 0;
   if (i0 >= nr.n) return 0;
@@ -336,15 +365,23 @@ __device__ __forceinline__ uint32_t pass_update(Pass<MODEL, KIND> &p, const Step
     float gEf[4], gIf[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      if constexpr (KIND == 1) {
+      if constexpr (KIND == 2) {
+        gEf[q] = g_fold32(p.ge.v[q], cnt_e[j0 + q], a.q_e, nr.inv_scale32, sat);
+        gIf[q] = g_fold32(p.gi.v[q], cnt_i[j0 + q], a.q_i, nr.inv_scale32, sat);
+      } else if constexpr (KIND == 1) {
         gEf[q] = g_fold(p.ge.v[q], cnt_e[j0 + q], a.q_e);
         gIf[q] = g_fold(p.gi.v[q], cnt_i[j0 + q], a.q_i);
       } else {
         gEf[q] = g_fold(p.ge.v[q], cnt_e[j0 + q], a.w_e);
         gIf[q] = g_fold(p.gi.v[q], cnt_i[j0 + q], a.w_i);
       }
-      g_after(p.ge.v[q], nr.alpha_e, nr.alpha_e32);
-      g_after(p.gi.v[q], nr.alpha_i, nr.alpha_i32);
+      if constexpr (KIND == 2) {
+        g_after32(p.ge.v[q], nr.a_e_q);
+        g_after32(p.gi.v[q], nr.a_i_q);
+      } else {
+        g_after(p.ge.v[q], nr.alpha_e, nr.alpha_e32);
+        g_after(p.gi.v[q], nr.alpha_i, nr.alpha_i32);
+      }
     }
     float V[4] = {p.V.x, p.V.y, p.V.z, p.V.w};
     if constexpr (MODEL == 0) {
@@ -377,7 +414,17 @@ __device__ __forceinline__ uint32_t pass_update(Pass<MODEL, KIND> &p, const Step
   for (int q = 0; q < 4 && i0 + q < nr.n; ++q) {
     const int64_t i = i0 + q;
     float gEf, gIf;
-    if constexpr (KIND == 1) {
+    if constexpr (KIND == 2) {
+      int32_t *pe = static_cast<int32_t *>(nr.g_e) + i;
+      int32_t *pi = static_cast<int32_t *>(nr.g_i) + i;
+      int32_t ge = *pe, gi = *pi;
+      gEf = g_fold32(ge, cnt_e[j0 + q], a.q_e, nr.inv_scale32, sat);
+      gIf = g_fold32(gi, cnt_i[j0 + q], a.q_i, nr.inv_scale32, sat);
+      g_after32(ge, nr.a_e_q);
+      g_after32(gi, nr.a_i_q);
+      *pe = ge;
+      *pi = gi;
+    } else if constexpr (KIND == 1) {
       long long *pe = static_cast<long long *>(nr.g_e) + i;
       long long *pi = static_cast<long long *>(nr.g_i) + i;
       long long ge = *pe, gi = *pi;
@@ -509,17 +556,19 @@ k_step(StepArgs a) {
   }
 
   // 2. update the tile: 4 passes of 1024 neurons, 4 consecutive per thread
-  uint32_t my_sp = 0;
+  uint32_t my_sp = 0, sat = 0;
 #pragma unroll
   for (int p = 0; p < passes; ++p) {
     Pass<MODEL, KIND> &cur = (p & 1) ? pb : pa;
     const int off = p * pstride;
-    const uint32_t nib = pass_update(cur, a, cnt_e, cnt_i, off + 4 * tid, base + off + 4 * tid, pol);
+    const uint32_t nib = pass_update(cur, a, cnt_e, cnt_i, off + 4 * tid, base + off + 4 * tid, pol,
+                                     sat);
     if (p + 2 < passes) pass_load(cur, nr, base + off + 2 * pstride + 4 * tid, pol);
     pass_emit(a, nib, base, off, my_sp);
   }
 
   // 3. counters
+  if (KIND == 2 && sat) atomicAdd(a.saturated, static_cast<unsigned long long>(sat));
   my_sp = __reduce_add_sync(0xffffffffu, my_sp);
   if (lane == 0 && my_sp) atomicAdd(&block_sp, static_cast<unsigned long long>(my_sp));
   __syncthreads();
@@ -965,6 +1014,7 @@ struct SmallArgs {
   int32_t *count_io;       // in/out: its length
   unsigned long long *events;
   unsigned long long *spikes;
+  unsigned long long *saturated;
 };
 
 template <int MODEL, int KIND>
@@ -974,7 +1024,8 @@ k_small_net(SmallArgs a) {
   const NeuronArgs &nr = a.nrn;
   const int n = static_cast<int>(nr.n);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  using G = typename std::conditional<KIND == 1, long long, float>::type;
+  using G = typename std::conditional<KIND == 1, long long,
+                                      typename std::conditional<KIND == 2, int32_t, float>::type>::type;
   G *gE = reinterpret_cast<G *>(sm);
   G *gI = gE + kSmallMax;
   float *V = reinterpret_cast<float *>(gI + kSmallMax);
@@ -1003,7 +1054,7 @@ k_small_net(SmallArgs a) {
   for (int i = tid; i < n_act; i += kSmallThreads) act[i] = a.active_io[i];
   __syncthreads();
 
-  uint32_t my_ev = 0, my_sp = 0;
+  uint32_t my_ev = 0, my_sp = 0, sat = 0;
   for (int64_t step = 0; step < a.n_steps; ++step) {
     // (1) deliver spikes_{n-1}: count events per postsynaptic neuron
     for (int k = warp; k < n_act; k += kSmallThreads / 32) {
@@ -1059,7 +1110,10 @@ k_small_net(SmallArgs a) {
       const int i = j0 + q;
       if (i >= n) break;
       float gEf, gIf;
-      if constexpr (KIND == 1) {
+      if constexpr (KIND == 2) {
+        gEf = g_fold32(gE[i], cE[i], a.q_e, nr.inv_scale32, sat);
+        gIf = g_fold32(gI[i], cI[i], a.q_i, nr.inv_scale32, sat);
+      } else if constexpr (KIND == 1) {
         gEf = g_fold(gE[i], cE[i], a.q_e);
         gIf = g_fold(gI[i], cI[i], a.q_i);
       } else {
@@ -1068,8 +1122,13 @@ k_small_net(SmallArgs a) {
       }
       cE[i] = 0;
       cI[i] = 0;
-      g_after(gE[i], nr.alpha_e, nr.alpha_e32);
-      g_after(gI[i], nr.alpha_i, nr.alpha_i32);
+      if constexpr (KIND == 2) {
+        g_after32(gE[i], nr.a_e_q);
+        g_after32(gI[i], nr.a_i_q);
+      } else {
+        g_after(gE[i], nr.alpha_e, nr.alpha_e32);
+        g_after(gI[i], nr.alpha_i, nr.alpha_i32);
+      }
       bool sp;
       if constexpr (MODEL == 0) {
         uint32_t r = R[i];
@@ -1128,10 +1187,11 @@ k_small_net(SmallArgs a) {
     atomicAdd(a.events, ev_total);
     atomicAdd(a.spikes, sp_total);
   }
+  if (KIND == 2 && sat) atomicAdd(a.saturated, static_cast<unsigned long long>(sat));
 }
 
 inline size_t small_net_smem(int model, int kind) {
-  const size_t g = kind == 1 ? 8 : 4;
+  const size_t g = kind == 1 ? 8 : 4;   // f32 and FIX32: 4 bytes
   const size_t per = 2 * g + 4 + (model == 1 ? 12 : 0) + 4 + 4 + 4 + (model == 0 ? 1 : 0);
   return per * kSmallMax;
 }

@@ -19,6 +19,8 @@ from . import inputs
 SEED_E, SEED_I = 0x5EED0001, 0x5EED0002
 W_E_LIF, W_I_LIF = 0.6, 6.7
 W_E_HH, W_I_HH = 6.0, 67.0          # COBA-HH nS (rule H1, EXTERNAL)
+# rule F2 fractional bits: LIF g stays < 2^11 (range 2048), HH g (nS) < 2^15
+FIX32_BITS = {"lif": 20, "hh": 16}
 
 
 @dataclass(frozen=True)
@@ -90,7 +92,8 @@ class CobaNetwork:
                  rank: int = 0, world: int = 1, device=None, csr=None,
                  w_exc: float | None = None, w_inh: float | None = None,
                  seed_e: int = SEED_E, seed_i: int = SEED_I, v0=None,
-                 init_seed: int = inputs.V0_SEED, spikes: torch.Tensor | None = None):
+                 init_seed: int = inputs.V0_SEED, spikes: torch.Tensor | None = None,
+                 frac_bits: int | None = None):
         device = torch.device(device or "cuda")
         self.n = n
         self.n_exc = n * 4 // 5
@@ -112,9 +115,17 @@ class CobaNetwork:
             w_inh = W_I_HH if w_inh is None else w_inh
             params = B.hh_params()
         self.w_exc, self.w_inh, self.params = w_exc, w_inh, params
-        g_dtype = torch.int64 if fixed else torch.float32
+        # conductance kind: fixed=True/"fix64" -> int64 2^-32 (rule F1),
+        # "fix32" -> int32 2^-F (rule F2; F = 20 LIF, 16 HH), False/"f32" -> fp32
+        mode = {True: "fix64", False: "f32"}.get(fixed, fixed)
+        if mode not in ("fix64", "fix32", "f32"):
+            raise ValueError(f"fixed={fixed!r}")
+        self.mode = mode
+        g_dtype = {"fix64": torch.int64, "fix32": torch.int32, "f32": torch.float32}[mode]
         st = {"g_e": torch.zeros(n_local, dtype=g_dtype, device=device),
               "g_i": torch.zeros(n_local, dtype=g_dtype, device=device)}
+        if mode == "fix32":
+            st["frac_bits"] = FIX32_BITS[model] if frac_bits is None else frac_bits
         if model == "lif":
             v_all = inputs.lif_v0(n, init_seed) if v0 is None else v0
             st["v"] = torch.as_tensor(v_all[lo:hi]).to(device).contiguous()

@@ -23,6 +23,11 @@ def _built():
     torch.cuda.set_device(0)
 
 
+def _g_dtype(fixed):
+    return {True: np.int64, "fix64": np.int64, "fix32": np.int32, False: np.float32,
+            "f32": np.float32}[fixed]
+
+
 def _oracle_lif(orc, n, fixed, csr=None):
     n_exc = n * 4 // 5
     K = orc.conn_len(80.0 / n)
@@ -33,7 +38,8 @@ def _oracle_lif(orc, n, fixed, csr=None):
         (ipe, ixe), (ipi, ixi) = csr
         pe = orc.Projection(0, n_exc, csr=(ipe, ixe, None), w_homo=0.6)
         pi = orc.Projection(n_exc, n - n_exc, csr=(ipi, ixi, None), w_homo=6.7)
-    g = np.int64 if fixed else np.float32
+    g = _g_dtype(fixed)
+    orc.set_fix32_bits(20)
     st = dict(v=inputs.lif_v0(n), g_e=np.zeros(n, g), g_i=np.zeros(n, g),
               ref=np.zeros(n, np.uint8), spikes=np.zeros(n, np.uint8))
     return st, pe, pi
@@ -43,12 +49,13 @@ def _raster(r, n):
     return np.stack([inputs.unpack_bits(row, n) for row in r.cpu().numpy().view(np.uint32)])
 
 
+@pytest.mark.parametrize("mode", ["fix64", "fix32"])
 @pytest.mark.parametrize("n,steps", [(4000, 2000), (1000, 500), (12_345, 300), (4096, 300)])
-def test_coba_lif_jit_fixed_bit_exact(orc, n, steps):
-    net = CobaNetwork(n, conn="jit", fixed=True)
+def test_coba_lif_jit_fixed_bit_exact(orc, n, steps, mode):
+    net = CobaNetwork(n, conn="jit", fixed=mode)
     raster = torch.zeros((steps, (n + 31) // 32), dtype=torch.int32, device="cuda")
     net.run(steps, raster)
-    st, pe, pi = _oracle_lif(orc, n, True)
+    st, pe, pi = _oracle_lif(orc, n, mode)
     want = orc.run_network("lif", orc.lif_params(), st, pe, pi, steps)
     got = _raster(raster, n)
     assert want.sum() > 0
@@ -57,13 +64,14 @@ def test_coba_lif_jit_fixed_bit_exact(orc, n, steps):
     assert np.array_equal(net.state["g_e"].cpu().numpy(), st["g_e"])
     assert np.array_equal(net.state["g_i"].cpu().numpy(), st["g_i"])
     assert np.array_equal(net.state["ref"].cpu().numpy(), st["ref"])
-    spikes, events = net.counters()
+    spikes, events, saturated = net.counters()
     assert spikes == int(want.sum())            # local spikes emitted (bp_network_counters)
     assert events > 0
 
 
+@pytest.mark.parametrize("mode", ["fix64", "fix32"])
 @pytest.mark.parametrize("small", [True, False])
-def test_coba_lif_csr_fixed_bit_exact(orc, small, monkeypatch):
+def test_coba_lif_csr_fixed_bit_exact(orc, small, mode, monkeypatch):
     """small: single-CTA time loop (k_small_net); else k_step + k_bin per step."""
     if not small:
         monkeypatch.setenv("BP_NO_SMALL_NET", "1")
@@ -72,10 +80,10 @@ def test_coba_lif_csr_fixed_bit_exact(orc, small, monkeypatch):
     ipe, ixe, _ = inputs.random_csr(n_exc, n, 0.02, seed=1)
     ipi, ixi, _ = inputs.random_csr(n - n_exc, n, 0.02, seed=2)
     csr = ((ipe, ixe), (ipi, ixi))
-    net = CobaNetwork(n, conn="csr", fixed=True, csr=csr)
+    net = CobaNetwork(n, conn="csr", fixed=mode, csr=csr)
     raster = torch.zeros((steps, n // 32), dtype=torch.int32, device="cuda")
     net.run(steps, raster)
-    st, pe, pi = _oracle_lif(orc, n, True, csr=csr)
+    st, pe, pi = _oracle_lif(orc, n, mode, csr=csr)
     want = orc.run_network("lif", orc.lif_params(), st, pe, pi, steps)
     assert want.sum() > 0
     assert np.array_equal(_raster(raster, n), want)
@@ -97,11 +105,12 @@ def test_coba_lif_f32_rule_t3(orc):
 
 
 @pytest.mark.parametrize("small", [True, False])
-@pytest.mark.parametrize("fixed", [True, False])
+@pytest.mark.parametrize("fixed", ["fix64", "fix32", "f32"])
 def test_coba_hh_csr(orc, fixed, small, monkeypatch):
     if not small:
         monkeypatch.setenv("BP_NO_SMALL_NET", "1")
     n, steps = 4000, 400
+    orc.set_fix32_bits(16)
     n_exc = 3200
     ipe, ixe, _ = inputs.random_csr(n_exc, n, 0.02, seed=11)
     ipi, ixi, _ = inputs.random_csr(n - n_exc, n, 0.02, seed=12)
@@ -109,15 +118,17 @@ def test_coba_hh_csr(orc, fixed, small, monkeypatch):
     raster = torch.zeros((steps, n // 32), dtype=torch.int32, device="cuda")
     net.run(steps, raster)
     v, m, h, nk = inputs.hh_init(n)
-    g = np.int64 if fixed else np.float32
+    g = _g_dtype(fixed)
     st = dict(v=v, m=m, h=h, n=nk, g_e=np.zeros(n, g), g_i=np.zeros(n, g),
               spikes=np.zeros(n, np.uint8))
     pe = orc.Projection(0, n_exc, csr=(ipe, ixe, None), w_homo=6.0)
     pi = orc.Projection(n_exc, n - n_exc, csr=(ipi, ixi, None), w_homo=67.0)
     want = orc.run_network("hh", orc.hh_params(), st, pe, pi, steps)
+    orc.set_fix32_bits(20)
     got = _raster(raster, n)
     assert want.sum() > 0
-    if fixed:
+    assert net.counters()[2] == 0          # no FIX32 saturation
+    if fixed != "f32":
         assert np.array_equal(got, want)
         assert np.array_equal(net.state["v"].cpu().numpy().view(np.uint32), st["v"].view(np.uint32))
     else:

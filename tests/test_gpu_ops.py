@@ -225,7 +225,10 @@ def test_materialize_positions_bit_exact(bp, orc, law, shape):
 def _rand_lif_state(n, fixed, seed):
     rng = np.random.default_rng(seed)
     v = rng.uniform(-70, -45, n).astype(np.float32)
-    if fixed:
+    if fixed == "fix32":
+        ge = rng.integers(0, 5 * 2 ** 20, n).astype(np.int32)
+        gi = rng.integers(0, 40 * 2 ** 20, n).astype(np.int32)
+    elif fixed:
         ge = rng.integers(0, 5 * 2 ** 32, n).astype(np.int64)
         gi = rng.integers(0, 40 * 2 ** 32, n).astype(np.int64)
     else:
@@ -237,10 +240,13 @@ def _rand_lif_state(n, fixed, seed):
 
 
 @pytest.mark.parametrize("n", [1, 33, 4000, 100_003])
-@pytest.mark.parametrize("fixed", [True, False])
+@pytest.mark.parametrize("fixed", [True, False, "fix32"])
 def test_lif_step_bit_exact(bp, orc, n, fixed):
     st = _rand_lif_state(n, fixed, seed=n)
     dev = {k: _t(a) for k, a in st.items()}
+    if fixed == "fix32":
+        dev["frac_bits"] = 20
+        orc.set_fix32_bits(20)
     spikes = torch.zeros((n + 31) // 32, dtype=torch.int32, device="cuda")
     active = torch.zeros(n, dtype=torch.int32, device="cuda")
     count = torch.zeros(1, dtype=torch.int32, device="cuda")
@@ -249,10 +255,8 @@ def test_lif_step_bit_exact(bp, orc, n, fixed):
     ev = orc.lif_step(orc.lif_params(), st["v"], st["g_e"], st["g_i"], st["ref"])
     assert np.array_equal(dev["v"].cpu().numpy().view(np.uint32), st["v"].view(np.uint32))
     assert np.array_equal(dev["ref"].cpu().numpy(), st["ref"])
-    assert np.array_equal(dev["g_e"].cpu().numpy().view(np.uint32 if not fixed else np.int64),
-                          st["g_e"].view(np.uint32 if not fixed else np.int64))
-    assert np.array_equal(dev["g_i"].cpu().numpy().view(np.uint32 if not fixed else np.int64),
-                          st["g_i"].view(np.uint32 if not fixed else np.int64))
+    assert np.array_equal(dev["g_e"].cpu().numpy(), st["g_e"])
+    assert np.array_equal(dev["g_i"].cpu().numpy(), st["g_i"])
     got = inputs.unpack_bits(spikes.cpu().numpy().view(np.uint32), n)
     assert np.array_equal(got, ev)
     c = int(count.item())

@@ -87,6 +87,52 @@ def test_fixed_point_g_equals_fp64_recursion(orc):
     assert np.max(np.abs(got_i - g_i)) < 2.0 ** -20 * max(1.0, g_i.max())
 
 
+def test_fix32_g_within_bound_of_fp64_recursion(orc):
+    """Rule F2 (int32, F = 20 fractional bits): the conductance stays within
+    the accumulated rounding bound of the exact recursion."""
+    n, T, F = 4000, 300, 20
+    orc.set_fix32_bits(F)
+    state, pe, pi = _coba(orc, n=n)
+    state["g_e"] = np.zeros(n, np.int32)
+    state["g_i"] = np.zeros(n, np.int32)
+    raster = orc.run_network("lif", orc.lif_params(), state, pe, pi, T)
+    assert raster.sum() > 0
+    d_e = np.zeros((pe.n_rows, n))
+    for r in range(pe.n_rows):
+        d_e[r, orc.jit_row(pe.jit, n, r)[0]] = float(np.float32(0.6))
+    d_i = np.zeros((pi.n_rows, n))
+    for r in range(pi.n_rows):
+        d_i[r, orc.jit_row(pi.jit, n, r)[0]] = float(np.float32(6.7))
+    a_e, a_i = math.exp(-0.1 / 5.0), math.exp(-0.1 / 10.0)
+    g_e = np.zeros(n); g_i = np.zeros(n); prev = np.zeros(n)
+    events_e = np.zeros(n); events_i = np.zeros(n)
+    for step in range(T):
+        inc_e = prev[:pe.n_rows] @ (d_e > 0)
+        inc_i = prev[pe.n_rows:] @ (d_i > 0)
+        events_e = np.maximum(events_e, inc_e)
+        events_i = np.maximum(events_i, inc_i)
+        g_e = a_e * g_e + prev[:pe.n_rows] @ d_e
+        g_i = a_i * g_i + prev[pe.n_rows:] @ d_i
+        prev = raster[step].astype(np.float64)
+    g_e *= a_e
+    g_i *= a_i
+    # per step: <= 1/2 ulp from the decay + 1/2 ulp per quantised event;
+    # errors contract by alpha, so the stationary bound is that / (1 - alpha)
+    ulp = 2.0 ** -F
+    bound_e = (0.5 + 0.5 * events_e.max()) * ulp / (1 - a_e) + ulp
+    bound_i = (0.5 + 0.5 * events_i.max()) * ulp / (1 - a_i) + ulp
+    assert np.max(np.abs(state["g_e"] * ulp - g_e)) <= bound_e
+    assert np.max(np.abs(state["g_i"] * ulp - g_i)) <= bound_i
+    orc.set_fix32_bits(20)
+
+
+def test_fix32_saturation(orc):
+    g = np.array([2 ** 31 - 10, -(2 ** 31) + 5, 7], np.int32)
+    sat = orc.fix32_add(g, np.array([100, -100, 3], np.int64))
+    assert sat == 2
+    assert g.tolist() == [2 ** 31 - 1, -(2 ** 31), 10]
+
+
 def test_jit_network_equals_materialised_csr_network(orc):
     n, T = 2000, 200
     s1, pe1, pi1 = _coba(orc, n=n)
