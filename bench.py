@@ -413,7 +413,7 @@ def run_ours(args):
                    "g": {"fix64": "int64 fixed point 2^-32 (rule F1)",
                          "fix32": "int32 fixed point 2^-%d (rule F2), saturations: %d" % (
                              20 if spec["model"] == "lif" else 16, sat1),
-                         "f32": "fp32 (rule T3)"}[args.g],
+                         "f32": "fp32, increments fl32(count*w) (rule N1-f32), bit-exact vs oracle"}[args.g],
                    "parallelism": f"postsynaptic partition x{world}",
                    "l2": (f"state {state_mb:.0f} MB/GPU > 2 x 126 MB L2: no flush needed"
                           if state_mb > 252 else
@@ -599,7 +599,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10_000)
     ap.add_argument("--warmup", type=int, default=200)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--g", choices=["fix64", "fix32", "f32"], default="fix32",
+    ap.add_argument("--g", choices=["fix64", "fix32", "f32"], default="f32",
                     help="conductance representation: int64 2^-32 (rule F1), int32 "
                          "2^-F (rule F2) or fp32 (rule T3 parity)")
     ap.add_argument("--f32", action="store_true", help="alias of --g f32")

@@ -291,6 +291,7 @@ def run_network(model: str, params, state: dict, proj_e: Projection,
         col_end = n_total
     fix32 = state["g_e"].dtype == np.int32
     fixed = state["g_e"].dtype == np.int64
+    f32 = not (fix32 or fixed)
     kind = OUT_FIX32 if fix32 else (OUT_FIX if fixed else OUT_F32)
     raster = np.zeros((n_steps, col_end - col_begin), np.uint8) if record else None
     counts = np.zeros(n_steps, np.int64)
@@ -298,6 +299,25 @@ def run_network(model: str, params, state: dict, proj_e: Projection,
         spikes = state["spikes"]
         for proj, g in ((proj_e, state["g_e"]), (proj_i, state["g_i"])):
             ev = spikes[proj.row0:proj.row0 + proj.n_rows]
+            homo_f32 = f32 and (proj.jit is not None and proj.jit.law == LAW_HOMO
+                                or proj.jit is None and proj.csr[2] is None)
+            if homo_f32:
+                # rule N1-f32: a homogeneous projection delivers `count`
+                # identical weights to a neuron in a step; the increment is
+                # fl32(count * w) (one rounding of the exact sum)
+                cnt = np.zeros(g.shape[0], np.float64)
+                if proj.jit is not None:
+                    spec1 = JitSpec(proj.jit.seed, proj.jit.K, proj.jit.L, LAW_HOMO, 1.0)
+                    jit_event_mv(spec1, proj.n_rows, n_total, ev, col_begin, col_end,
+                                 OUT_F64, out=cnt)
+                    w = np.float32(proj.jit.w0)
+                else:
+                    ip, ix, _ = proj.csr
+                    event_csrmv(ip, ix, None, 1.0, proj.n_rows, col_end - col_begin, ev,
+                                OUT_F64, out=cnt)
+                    w = np.float32(proj.w_homo)
+                g[:] = g + cnt.astype(np.float32) * w
+                continue
             # rule F2: the step's increments are summed exactly, then added
             # to the int32 conductance with saturation
             acc = np.zeros(g.shape[0], np.int64) if fix32 else g
