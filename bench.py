@@ -41,6 +41,25 @@ def step_bytes(n_local, events_per_step, fixed):
     return per_neuron * n_local + 4 * events_per_step
 
 
+def _ncu_traffic(kernel_prefix):
+    """dram__bytes_read + dram__bytes_write per launch of `kernel_prefix` from
+    the committed ncu --set full capture of this round (profiles/r01), or None."""
+    path = os.path.join(ROOT, "profiles", "r01", "ncu_full_f32_default.json")
+    try:
+        with open(path) as f:
+            rows = json.load(f)
+    except (OSError, ValueError):
+        return None
+    for r in rows:
+        if r.get("Kernel Name", "").startswith(kernel_prefix):
+            rd = float(r["dram__bytes_read.sum"].split()[0])
+            wr = float(r["dram__bytes_write.sum"].split()[0])
+            unit = r["dram__bytes_read.sum"].split()[1] if " " in r["dram__bytes_read.sum"] else "byte"
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+            return (rd + wr) * scale
+    return None
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -387,9 +406,16 @@ def run_ours(args):
         kname = ("k_small_net<%s,%s> (whole time loop in one CTA, state in shared memory)"
                  if small else "k_step<%s,%s> (fused: bucket counts -> Expon+COBA+neuron -> "
                  "spike bits + active list)") % (spec["model"].upper(), args.g)
+        traffic = (_ncu_traffic("void k_step<0, 0>")
+                   if (wl == "coba_lif_jit" and args.g == "f32" and world == 1) else None)
         roofline = {"kernel": kname, "bound": "hbm", "achieved": achieved,
                     "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-                    "traffic": None, "peak_source": peak_kind,
+                    "traffic": traffic,
+                    "traffic_source": ("profiles/r01/ncu_full_f32_default.json (ncu --set full, "
+                                       "--cache-control none): DRAM bytes per launch; below the "
+                                       "algorithmic bytes because the snake tile order re-uses "
+                                       "L2-resident state") if traffic else None,
+                    "peak_source": peak_kind,
                     "algorithmic_bytes_per_launch": bytes_per_launch,
                     "avg_launch_us": upd_s * 1e6,
                     "share_of_step": up_ms / (sc_ms + up_ms) if (sc_ms + up_ms) else None,
