@@ -320,10 +320,16 @@ def run_ours(args):
     world = args.gpus
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # one GPU per rank; --dist-backend gloo lets several ranks share a GPU for
+    # a functional check of the N > 1 path (host-mediated exchange)
+    device_index = local_rank % torch.cuda.device_count()
+    torch.cuda.set_device(device_index)
+    dev = torch.device("cuda", device_index)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     n_total = network_size(wl, world)
     fixed = {"fix64": True, "fix32": "fix32", "f32": False}[args.g]
 
@@ -370,10 +376,11 @@ def run_ours(args):
     events_local = ev1 - ev0
     spikes_seen = sp1 - sp0
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        rdev = dev if args.dist_backend == "nccl" else "cpu"
+        t = torch.tensor([ms], dtype=torch.float64, device=rdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-        e = torch.tensor([events_local], dtype=torch.float64, device=dev)
+        e = torch.tensor([events_local], dtype=torch.float64, device=rdev)
         dist.all_reduce(e, op=dist.ReduceOp.SUM)
         events_total = float(e.item())
     else:
@@ -637,6 +644,9 @@ def main():
     ap.add_argument("--density", type=float, default=0.1, help="microbench spike density")
     ap.add_argument("--law", choices=["homo", "uniform", "normal"], default="uniform")
     ap.add_argument("--fix", action="store_true", help="microbench int64 fixed-point output")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="spike exchange backend for --gpus > 1 (gloo: functional check "
+                         "with several ranks on one GPU)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -14,7 +14,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbp.so")
+# BP_LIB overrides the library path (A/B experiments with alternative builds)
+LIB_PATH = os.environ.get("BP_LIB") or os.path.join(_HERE, "libbp.so")
 
 OUT_F32, OUT_FIX64, OUT_FIX32 = 0, 1, 2
 ACCUMULATE = 1

@@ -624,9 +624,12 @@ bp::ConnArgs make_conn(const bp_network *net) {
     // expected events of one row in one segment: L * 2 / (K + 1)
     const double fe = net->jr_e.L * 2.0 / (net->jr_e.K + 1.0);
     const double fi = net->jr_i.L * 2.0 / (net->jr_i.K + 1.0);
-    // one lane per row only on request: measured slower at 186 rows per SM
-    // (too few warps to hide the Philox chain latency), see DESIGN.md
-    c.lane_rows = (fe <= 512.0 && fi <= 512.0 && std::getenv("BP_BIN_LANE_ROWS")) ? 1 : 0;
+    // One lane per row when a row has few events in this rank's segment
+    // (multi-GPU partitions: ~80/G per row): measured 3x faster at G = 8
+    // (220 k rows, 10 events per row-segment: 34 vs 99 us) but slower at
+    // G = 1 (80 events per row: 44 vs 34 us; tools/probes/probe_bin.cu).
+    const char *lr = std::getenv("BP_BIN_LANE_ROWS");
+    c.lane_rows = lr ? std::atoi(lr) : ((fe <= 48.0 && fi <= 48.0) ? 1 : 0);
   } else {
     c.ce.indptr = d.exc_indptr; c.ce.indices = d.exc_indices; c.ce.data = d.exc_data;
     c.ci.indptr = d.inh_indptr; c.ci.indices = d.inh_indices; c.ci.data = d.inh_data;

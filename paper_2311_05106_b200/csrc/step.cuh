@@ -45,9 +45,15 @@ __device__ __forceinline__ void pdl_trigger() {
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-constexpr int kTileShift = 12;
+#ifndef BP_TILE_SHIFT
+#define BP_TILE_SHIFT 12
+#endif
+constexpr int kTileShift = BP_TILE_SHIFT;
 constexpr int kTile = 1 << kTileShift;   // postsynaptic neurons per tile/block
-constexpr int kStepThreads = 256;        // 16 neurons per thread
+#ifndef BP_STEP_THREADS
+#define BP_STEP_THREADS 256
+#endif
+constexpr int kStepThreads = BP_STEP_THREADS;   // LIF block size (4 neurons per thread per pass)
 constexpr uint32_t kProjBit = 0x80000000u;
 
 // Per-tile bucket counters sit on their own 256-byte line: the 2M
@@ -507,7 +513,7 @@ __device__ __forceinline__ void pass_emit(const StepArgs &a, uint32_t nib, int64
 // LIF (memory-bound): 256 threads, 4 passes, register double buffering.
 // HH (FP32-latency-bound): 512 threads, 2 passes (more warps, 128 registers).
 template <int MODEL, int KIND>
-__global__ void __launch_bounds__(MODEL == 0 ? kStepThreads : 512, MODEL == 0 ? 4 : 1)
+__global__ void __launch_bounds__(MODEL == 0 ? kStepThreads : 512, MODEL == 0 ? 1024 / kStepThreads : 1)
 k_step(StepArgs a) {
   __shared__ int32_t cnt_e[kTile];
   __shared__ int32_t cnt_i[kTile];
