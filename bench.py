@@ -541,7 +541,9 @@ def run_micro(args):
     pats = [inputs.spike_pattern(n, d, 7000 + k) for k in range(n_pat)]
     spikes = [torch.from_numpy(inputs.pack_bits(e).view(np.int32)).to(dev) for e in pats]
     out = torch.zeros(n, dtype=torch.int64 if fixed else torch.float32, device=dev)
-    ws = bp.workspace(n, dev)
+    ws_bytes = (bp.lib().bp_csrmv_workspace_bytes(n, n, 1 if fixed else 0) if kind == "csrmv"
+                else bp.workspace_bytes(n))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     seed = 0xBE7C4
     spec = bp.jitconn_spec(seed, p)
     w0, w1 = {"homo": (0.6, 0.0), "uniform": (-0.1, 0.1),

@@ -86,6 +86,14 @@ uint32_t bp_conn_len(double prob);
  * input of n_rows presynaptic neurons (active-row list + counter).  Host. */
 size_t bp_workspace_bytes(int64_t n_rows);
 
+/* Workspace for bp_event_csrmv on an n_rows x n_cols matrix with output
+ * kind out_kind: the active list plus, when the output fits a few
+ * shared-memory column tiles, the per-CTA partial tiles that make the
+ * accumulation atomic-free (>= bp_workspace_bytes(n_rows); with only
+ * bp_workspace_bytes(n_rows) bytes the partial tiles are flushed with
+ * atomics instead).  Host function (queries the current device). */
+size_t bp_csrmv_workspace_bytes(int64_t n_rows, int64_t n_cols, int out_kind);
+
 /* a1: active = { r < n : bit r of spikes set }, written to active[0..count)
  * in unspecified order (a set); *count (device int32) receives its size.
  * active must hold n entries. */
@@ -96,7 +104,8 @@ bp_status bp_compact_spikes(const uint32_t *spikes, int64_t n, int32_t *active,
  * typo):  for r with bit r set, for k in [indptr[r], indptr[r+1]):
  *     out[indices[k]] += (data ? data[k] : w_homo)
  * out: n_cols float32 (BP_OUT_F32) or int64 (BP_OUT_FIX64), 16-byte aligned.
- * ws: >= bp_workspace_bytes(n_rows) bytes, 256-byte aligned. */
+ * ws: >= bp_workspace_bytes(n_rows) bytes (bp_csrmv_workspace_bytes for the
+ * atomic-free path), 256-byte aligned. */
 bp_status bp_event_csrmv(const int64_t *indptr, const int32_t *indices,
                          const float *data, float w_homo, int64_t n_rows,
                          int64_t n_cols, const uint32_t *spikes, void *out,

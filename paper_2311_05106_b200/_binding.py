@@ -25,7 +25,7 @@ CONN_JIT, CONN_CSR = 0, 1
 
 EXPORTED = [
     "bp_abi_version", "bp_status_string", "bp_last_error", "bp_conn_len",
-    "bp_workspace_bytes", "bp_compact_spikes", "bp_event_csrmv",
+    "bp_workspace_bytes", "bp_csrmv_workspace_bytes", "bp_compact_spikes", "bp_event_csrmv",
     "bp_jitconn_event_mv_homo", "bp_jitconn_event_mv_uniform",
     "bp_jitconn_event_mv_normal", "bp_jitconn_row_counts",
     "bp_jitconn_materialize", "bp_neuron_step", "bp_network_workspace_bytes",
@@ -98,6 +98,8 @@ def lib():
         L.bp_conn_len.restype = u32
         L.bp_workspace_bytes.argtypes = [i64]
         L.bp_workspace_bytes.restype = sz
+        L.bp_csrmv_workspace_bytes.argtypes = [i64, i64, i32]
+        L.bp_csrmv_workspace_bytes.restype = sz
         L.bp_compact_spikes.argtypes = [P, i64, P, P, P]
         L.bp_event_csrmv.argtypes = [P, P, P, f32, i64, i64, P, P, i32, u32, P, sz, P]
         jit_tail = [P, i64, i64, i64, i64, P, i32, u32, P, sz, P]
@@ -124,6 +126,7 @@ def lib():
         for name in EXPORTED:
             if name not in ("bp_network_destroy", "bp_status_string",
                             "bp_last_error", "bp_conn_len", "bp_workspace_bytes",
+                            "bp_csrmv_workspace_bytes",
                             "bp_network_workspace_bytes", "bp_abi_version"):
                 getattr(L, name).restype = ctypes.c_int
         _lib = L
@@ -194,7 +197,9 @@ def event_csrmv(indptr, indices, data, w_homo, n_rows, n_cols, spikes, out,
                 accumulate=False, ws=None, stream=None):
     """brainpy.math.event.csrmv (Listing S1) -> out[n_cols] (f32 or fix64)."""
     _cuda(indptr, indices, data, spikes, out)
-    ws = ws if ws is not None else workspace(n_rows, out.device)
+    if ws is None:
+        nbytes = int(lib().bp_csrmv_workspace_bytes(int(n_rows), int(n_cols), _out_kind(out)))
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=out.device)
     _check(lib().bp_event_csrmv(
         _ptr(indptr), _ptr(indices), _ptr(data), float(w_homo), int(n_rows),
         int(n_cols), _ptr(spikes), _ptr(out), _out_kind(out),

@@ -103,6 +103,8 @@ bp_status carve_ws(void *ws, size_t ws_bytes, int64_t n_rows, Ws *out) {
   return BP_OK;
 }
 
+bool n_tiles_ok(int64_t n_tiles) { return n_tiles >= 1 && n_tiles <= 4; }
+
 int grid_for_items(int64_t items_upper, int sms) {
   // one warp per item; at most 8 resident 256-thread blocks per SM
   const int64_t warps_per_block = bp::kScatterThreads / 32;
@@ -126,6 +128,30 @@ void launch_compact(const uint32_t *spikes, int64_t n, int32_t *active,
   const int64_t words = (n + 31) / 32;
   bp::k_compact<<<grid_for_words(words, sms), 256, 0, st>>>(spikes, n, active,
                                                             count, 0);
+}
+
+// ------------------------------------------------------------- CSR plan
+struct CsrPlan {
+  bool tiled;
+  int64_t n_tiles;
+  int32_t tile_cols, groups;
+  size_t acc;            // shared accumulator bytes per column
+  size_t partials_off;   // workspace offset of the partial tiles
+  size_t ws_bytes;       // workspace needed for the reduce path
+};
+
+CsrPlan csr_plan(int64_t n_rows, int64_t n_cols, int out_kind, int sms) {
+  CsrPlan p{};
+  p.acc = out_kind == BP_OUT_FIX64 ? 8 : 4;
+  const int64_t tile_cols = static_cast<int64_t>(200 * 1000 / p.acc);
+  p.n_tiles = (n_cols + tile_cols - 1) / tile_cols;
+  p.tiled = n_tiles_ok(p.n_tiles) && !std::getenv("BP_CSR_DIRECT");
+  p.tile_cols = static_cast<int32_t>(n_cols < tile_cols ? n_cols : tile_cols);
+  p.groups = static_cast<int32_t>(sms / p.n_tiles > 0 ? sms / p.n_tiles : 1);
+  p.partials_off = bp_workspace_bytes(n_rows);
+  p.ws_bytes = p.partials_off +
+               round_up(static_cast<size_t>(p.n_tiles) * p.groups * p.tile_cols * p.acc, 256);
+  return p;
 }
 
 // ------------------------------------------------------------- JIT helpers
@@ -294,6 +320,14 @@ size_t bp_workspace_bytes(int64_t n_rows) {
   return 256 + round_up(static_cast<size_t>(n_rows) * sizeof(int32_t), 256);
 }
 
+size_t bp_csrmv_workspace_bytes(int64_t n_rows, int64_t n_cols, int out_kind) {
+  int sms = 148;
+  if (device_ready(&sms) != BP_OK) sms = 148;
+  if (n_rows < 0 || n_cols < 1) return bp_workspace_bytes(n_rows);
+  const CsrPlan p = csr_plan(n_rows, n_cols, out_kind, sms);
+  return p.tiled ? p.ws_bytes : bp_workspace_bytes(n_rows);
+}
+
 bp_status bp_compact_spikes(const uint32_t *spikes, int64_t n, int32_t *active,
                             int32_t *count, bp_stream stream) {
   int sms = 0;
@@ -327,7 +361,11 @@ bp_status bp_event_csrmv(const int64_t *indptr, const int32_t *indices,
   if (s != BP_OK) return s;
   cudaStream_t st = as_stream(stream);
   const size_t elt = out_kind == BP_OUT_FIX64 ? 8 : 4;
-  if (!(flags & BP_ACCUMULATE)) BP_CUDA(cudaMemsetAsync(out, 0, elt * n_cols, st));
+  CsrPlan plan = csr_plan(n_rows, n_cols, out_kind, sms);
+  const bool reduce_path = plan.tiled && ws_bytes >= plan.ws_bytes && n_rows > 0 &&
+                           !std::getenv("BP_CSR_ATOMIC_FLUSH");
+  // the reduce kernel writes every output column: no memset needed there
+  if (!(flags & BP_ACCUMULATE) && !reduce_path) BP_CUDA(cudaMemsetAsync(out, 0, elt * n_cols, st));
   if (n_rows == 0) return launched();
   BP_CUDA(cudaMemsetAsync(w.count, 0, sizeof(int32_t), st));
   launch_compact(spikes, n_rows, w.active, w.count, sms, st);
@@ -343,17 +381,20 @@ bp_status bp_event_csrmv(const int64_t *indptr, const int32_t *indices,
   a.active = w.active;
   a.count = w.count;
   // Column-tiled shared-memory aggregation when the output fits <= 4 tiles
-  // of <= 200 KB (scatter.cuh, k_csr_tiled); else one RED per event.
-  const size_t acc = out_kind == BP_OUT_FIX64 ? 8 : 4;
-  const int64_t tile_cols = static_cast<int64_t>(200 * 1000 / acc);
-  const int64_t n_tiles = (n_cols + tile_cols - 1) / tile_cols;
-  if (n_tiles <= 4 && !std::getenv("BP_CSR_DIRECT")) {
+  // of <= 200 KB (scatter.cuh, k_csr_tiled); partial tiles reduced by
+  // k_csr_reduce when the workspace holds them, else flushed with REDs;
+  // outputs wider than 4 tiles: one RED per event (k_csr_scatter).
+  const size_t acc = plan.acc;
+  const int64_t n_tiles = plan.n_tiles;
+  if (plan.tiled) {
     bp::CsrTiledArgs t{};
     t.indptr = indptr; t.indices = indices; t.data = data; t.w = w_homo;
     t.q = a.e.q; t.out = out; t.n_cols = n_cols;
-    t.tile_cols = static_cast<int32_t>(n_cols < tile_cols ? n_cols : tile_cols);
-    t.groups = static_cast<int32_t>(sms / n_tiles > 0 ? sms / n_tiles : 1);
+    t.tile_cols = plan.tile_cols;
+    t.groups = plan.groups;
     t.active = w.active; t.count = w.count;
+    t.partials = reduce_path ? static_cast<char *>(ws) + plan.partials_off : nullptr;
+    t.accumulate = (flags & BP_ACCUMULATE) ? 1 : 0;
     const size_t smem = static_cast<size_t>(t.tile_cols) * acc;
     static bool attr_set[2] = {false, false};
     if (!attr_set[out_kind]) {
@@ -368,6 +409,11 @@ bp_status bp_event_csrmv(const int64_t *indptr, const int32_t *indices,
     const int grid = static_cast<int>(n_tiles * t.groups);
     if (out_kind == BP_OUT_FIX64) bp::k_csr_tiled<1><<<grid, bp::kTiledThreads, smem, st>>>(t);
     else bp::k_csr_tiled<0><<<grid, bp::kTiledThreads, smem, st>>>(t);
+    if (reduce_path) {
+      const int rgrid = static_cast<int>((n_cols + 255) / 256);
+      if (out_kind == BP_OUT_FIX64) bp::k_csr_reduce<1><<<rgrid, 256, 0, st>>>(t, data == nullptr);
+      else bp::k_csr_reduce<0><<<rgrid, 256, 0, st>>>(t, data == nullptr);
+    }
     return launched();
   }
   launch_csr(a, out_kind, grid_for_items(n_rows, sms), st);

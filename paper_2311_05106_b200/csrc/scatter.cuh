@@ -213,12 +213,14 @@ struct CsrTiledArgs {
   int32_t groups;             // CTAs per tile
   const int32_t *active;
   const int32_t *count;
+  void *partials;             // nullable: [tile][group][tile_cols] partial sums
+  int accumulate;             // reduce: out += sum (else out = sum)
 };
 
 template <int KIND>
 __global__ void __launch_bounds__(kTiledThreads, 1)
 k_csr_tiled(CsrTiledArgs a) {
-  extern __shared__ unsigned char tile_raw[];
+  extern __shared__ __align__(16) unsigned char tile_raw[];
   const int tile = blockIdx.x / a.groups, group = blockIdx.x % a.groups;
   const int64_t c0 = static_cast<int64_t>(tile) * a.tile_cols;
   const int64_t c1 = min(c0 + a.tile_cols, a.n_cols);
@@ -253,35 +255,61 @@ k_csr_tiled(CsrTiledArgs a) {
     const int64_t span = hi - lo;
     hi = lo + span * (chunk + 1) / kChunks;
     lo = lo + span * chunk / kChunks;
-    int64_t j = lo + lane;
-    // 8 independent loads in flight per lane (latency-bound long rows)
-    for (; j + 224 < hi; j += 256) {
-      int32_t c[8];
-      float w[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        c[u] = __ldg(a.indices + j + 32 * u) - static_cast<int32_t>(c0);
-        w[u] = a.data ? __ldg(a.data + j + 32 * u) : a.w;
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (homo) atomicAdd(accc + c[u], 1u);          // native ATOMS.ADD
-        else if (KIND == 0) atomicAdd(accf + c[u], w[u]);
-        else atomicAdd(accq + c[u], static_cast<unsigned long long>(quantize(w[u])));
-      }
+    // entry j's contribution to the shared tile
+    auto add = [&](int32_t col, float w) {
+      if (homo) atomicAdd(accc + col, 1u);               // native ATOMS (POPC.INC)
+      else if (KIND == 0) atomicAdd(accf + col, w);
+      else atomicAdd(accq + col, static_cast<unsigned long long>(quantize(w)));
+    };
+    const int32_t c0i = static_cast<int32_t>(c0);
+    // head up to a 16-byte boundary, 128-bit body (4 int4 loads = 16
+    // entries in flight per lane), tail
+    const int64_t a0 = min(hi, (lo + 3) & ~int64_t{3});
+    const int64_t a1 = a0 + ((hi - a0) & ~int64_t{3});
+    if (lo + lane < a0) {
+      const int64_t jj = lo + lane;
+      add(__ldg(a.indices + jj) - c0i, a.data ? __ldg(a.data + jj) : a.w);
     }
-    for (; j < hi; j += 32) {
-      const int32_t c = __ldg(a.indices + j) - static_cast<int32_t>(c0);
-      if (homo) {
-        atomicAdd(accc + c, 1u);
-      } else {
-        const float w = __ldg(a.data + j);
-        if (KIND == 0) atomicAdd(accf + c, w);
-        else atomicAdd(accq + c, static_cast<unsigned long long>(quantize(w)));
+    if (a1 + lane < hi) {
+      const int64_t jj = a1 + lane;
+      add(__ldg(a.indices + jj) - c0i, a.data ? __ldg(a.data + jj) : a.w);
+    }
+    const int4 *iv = reinterpret_cast<const int4 *>(a.indices + a0);
+    const float4 *dv = a.data ? reinterpret_cast<const float4 *>(a.data + a0) : nullptr;
+    const int64_t nv = (a1 - a0) >> 2;                  // int4 vectors in the body
+    for (int64_t v = lane; v < nv; v += 128) {
+      int4 ci[4];
+      float4 wi[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t vv = v + 32 * u;
+        ci[u] = vv < nv ? __ldg(iv + vv) : make_int4(-1, -1, -1, -1);
+        wi[u] = (dv && vv < nv) ? __ldg(dv + vv) : make_float4(a.w, a.w, a.w, a.w);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (ci[u].x < 0) continue;
+        add(ci[u].x - c0i, wi[u].x);
+        add(ci[u].y - c0i, wi[u].y);
+        add(ci[u].z - c0i, wi[u].z);
+        add(ci[u].w - c0i, wi[u].w);
       }
     }
   }
   __syncthreads();
+  if (a.partials) {
+    // coalesced 16-byte stores of the whole tile; k_csr_reduce sums the
+    // groups in a fixed order (no global atomics, deterministic)
+    const size_t elt = (homo || KIND == 0) ? 4 : 8;
+    char *dst = static_cast<char *>(a.partials) +
+                (static_cast<size_t>(tile) * a.groups + group) * a.tile_cols * elt;
+    const int n16 = static_cast<int>(width * elt / 16);
+    const uint4 *src = reinterpret_cast<const uint4 *>(tile_raw);
+    for (int k = tid; k < n16; k += kTiledThreads) reinterpret_cast<uint4 *>(dst)[k] = src[k];
+    for (int b = n16 * 16 + tid; b < static_cast<int>(width * elt); b += kTiledThreads)
+      dst[b] = reinterpret_cast<const char *>(tile_raw)[b];
+    return;
+  }
   if (homo) {
     for (int c = tid; c < width; c += kTiledThreads) {
       const unsigned n = accc[c];
@@ -318,6 +346,45 @@ k_csr_tiled(CsrTiledArgs a) {
       const unsigned long long v = accq[c];
       if (v != 0ull) atomicAdd(static_cast<unsigned long long *>(a.out) + c0 + c, v);
     }
+  }
+}
+
+// Sum the per-CTA partial tiles of k_csr_tiled, groups in ascending order:
+// homogeneous weights -> fl32(count * w) or count * q; else the f32 / int64
+// partial sums.  One thread per output column.
+template <int KIND>
+__global__ void __launch_bounds__(256)
+k_csr_reduce(CsrTiledArgs a, int homo) {
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c >= a.n_cols) return;
+  const int64_t tile = c / a.tile_cols, cc = c - tile * a.tile_cols;
+  const size_t stride = static_cast<size_t>(a.tile_cols);
+  const size_t base = static_cast<size_t>(tile) * a.groups * stride + cc;
+  if (homo) {
+    const unsigned *p = static_cast<const unsigned *>(a.partials) + base;
+    unsigned long long n = 0;
+    for (int g = 0; g < a.groups; ++g) n += __ldcs(p + g * stride);
+    if (KIND == 0) {
+      const float v = __fmul_rn(__ull2float_rn(n), a.w);
+      float *o = static_cast<float *>(a.out) + c;
+      *o = a.accumulate ? __fadd_rn(*o, v) : v;
+    } else {
+      const long long v = static_cast<long long>(n) * a.q;
+      long long *o = static_cast<long long *>(a.out) + c;
+      *o = a.accumulate ? *o + v : v;
+    }
+  } else if (KIND == 0) {
+    const float *p = static_cast<const float *>(a.partials) + base;
+    float v = 0.f;
+    for (int g = 0; g < a.groups; ++g) v = __fadd_rn(v, __ldcs(p + g * stride));
+    float *o = static_cast<float *>(a.out) + c;
+    *o = a.accumulate ? __fadd_rn(*o, v) : v;
+  } else {
+    const long long *p = static_cast<const long long *>(a.partials) + base;
+    long long v = 0;
+    for (int g = 0; g < a.groups; ++g) v += __ldcs(p + g * stride);
+    long long *o = static_cast<long long *>(a.out) + c;
+    *o = a.accumulate ? *o + v : v;
   }
 }
 

@@ -68,12 +68,15 @@ CSR_CASES = [
 ]
 
 
-@pytest.mark.parametrize("direct", [False, True])
+@pytest.mark.parametrize("path", ["reduce", "atomic_flush", "direct"])
 @pytest.mark.parametrize("case", CSR_CASES)
-def test_event_csrmv(bp, orc, case, direct, monkeypatch):
-    """direct=False: column-tiled shared-memory kernel; True: one RED per event."""
-    if direct:
+def test_event_csrmv(bp, orc, case, path, monkeypatch):
+    """reduce: column tiles in shared memory + partial-tile reduction;
+    atomic_flush: tiles flushed with REDs; direct: one RED per event."""
+    if path == "direct":
         monkeypatch.setenv("BP_CSR_DIRECT", "1")
+    if path == "atomic_flush":
+        monkeypatch.setenv("BP_CSR_ATOMIC_FLUSH", "1")
     n_rows, n_cols, p, law, density = case
     ip, ix, dat = inputs.random_csr(n_rows, n_cols, p, seed=n_rows + n_cols,
                                     weights=law, w0=-0.5 if law != "homo" else 1.0,
