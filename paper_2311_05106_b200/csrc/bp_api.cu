@@ -14,6 +14,7 @@
 #include "../../include/bp.h"
 #include "neuron.cuh"
 #include "scatter.cuh"
+#include "csr_stream.cuh"
 #include "step.cuh"
 
 namespace {
@@ -146,12 +147,59 @@ CsrPlan csr_plan(int64_t n_rows, int64_t n_cols, int out_kind, int sms) {
   const int64_t tile_cols = static_cast<int64_t>(200 * 1000 / p.acc);
   p.n_tiles = (n_cols + tile_cols - 1) / tile_cols;
   p.tiled = n_tiles_ok(p.n_tiles) && !std::getenv("BP_CSR_DIRECT");
-  p.tile_cols = static_cast<int32_t>(n_cols < tile_cols ? n_cols : tile_cols);
+  // multiple of 4 columns: the partial tiles are stored with 16-byte stores
+  p.tile_cols = static_cast<int32_t>(
+      round_up(static_cast<size_t>(n_cols < tile_cols ? n_cols : tile_cols), 4));
   p.groups = static_cast<int32_t>(sms / p.n_tiles > 0 ? sms / p.n_tiles : 1);
   p.partials_off = bp_workspace_bytes(n_rows);
   p.ws_bytes = p.partials_off +
                round_up(static_cast<size_t>(p.n_tiles) * p.groups * p.tile_cols * p.acc, 256);
   return p;
+}
+
+// Streamed CSR plan (csr_stream.cuh): column tiles sized to the shared
+// memory left after the bulk-copy stages; one CTA per SM.
+constexpr size_t kSmemOptin = 232448;     // 227 KB dynamic shared memory per block
+constexpr int kStreamMaxTiles = 16;
+
+struct StreamPlan {
+  bool ok;
+  int32_t n_tiles, tile_cols, groups, stages;
+  size_t smem, bounds_off, partials_off, ws_bytes;
+};
+
+StreamPlan stream_plan(int64_t n_rows, int64_t n_cols, int out_kind, bool homo, int sms) {
+  StreamPlan p{};
+  const int acc = homo ? 4 : (out_kind == BP_OUT_FIX64 ? 8 : 4);
+  p.stages = homo ? 4 : 3;
+  const size_t fixed = bp::stream_smem(0, acc, p.stages, homo).total + 256;
+  if (n_rows < 1 || n_cols < 1 || fixed >= kSmemOptin) return p;
+  const int64_t max_cols = static_cast<int64_t>((kSmemOptin - fixed) / acc) & ~int64_t{3};
+  const int64_t nt = (n_cols + max_cols - 1) / max_cols;
+  if (nt > kStreamMaxTiles || nt > sms) return p;
+  p.n_tiles = static_cast<int32_t>(nt);
+  p.tile_cols = static_cast<int32_t>(round_up(static_cast<size_t>((n_cols + nt - 1) / nt), 4));
+  p.groups = sms / p.n_tiles;
+  p.smem = bp::stream_smem(p.tile_cols, acc, p.stages, homo).total;
+  const size_t bounds = static_cast<size_t>(n_rows) * (nt + 1) * sizeof(int64_t);
+  if (p.smem > kSmemOptin || bounds > (size_t{1} << 30)) return p;
+  p.bounds_off = bp_workspace_bytes(n_rows);
+  p.partials_off = p.bounds_off + round_up(bounds, 256);
+  p.ws_bytes = p.partials_off +
+               round_up(static_cast<size_t>(nt) * p.groups * p.tile_cols * acc, 256);
+  p.ok = true;
+  return p;
+}
+
+template <int KIND, bool HOMO>
+void launch_stream(const bp::CsrStreamArgs &a, const StreamPlan &p, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(bp::k_csr_stream<KIND, HOMO>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemOptin));
+    attr = true;
+  }
+  bp::k_csr_stream<KIND, HOMO><<<p.n_tiles * p.groups, bp::kStreamThreads, p.smem, st>>>(a);
 }
 
 // ------------------------------------------------------------- JIT helpers
@@ -325,7 +373,12 @@ size_t bp_csrmv_workspace_bytes(int64_t n_rows, int64_t n_cols, int out_kind) {
   if (device_ready(&sms) != BP_OK) sms = 148;
   if (n_rows < 0 || n_cols < 1) return bp_workspace_bytes(n_rows);
   const CsrPlan p = csr_plan(n_rows, n_cols, out_kind, sms);
-  return p.tiled ? p.ws_bytes : bp_workspace_bytes(n_rows);
+  size_t need = p.tiled ? p.ws_bytes : bp_workspace_bytes(n_rows);
+  for (int homo = 0; homo < 2; ++homo) {
+    const StreamPlan sp = stream_plan(n_rows, n_cols, out_kind, homo != 0, sms);
+    if (sp.ok && sp.ws_bytes > need) need = sp.ws_bytes;
+  }
+  return need;
 }
 
 bp_status bp_compact_spikes(const uint32_t *spikes, int64_t n, int32_t *active,
@@ -361,6 +414,45 @@ bp_status bp_event_csrmv(const int64_t *indptr, const int32_t *indices,
   if (s != BP_OK) return s;
   cudaStream_t st = as_stream(stream);
   const size_t elt = out_kind == BP_OUT_FIX64 ? 8 : 4;
+  const bool homo = data == nullptr;
+  const StreamPlan sp = stream_plan(n_rows, n_cols, out_kind, homo, sms);
+  if (sp.ok && ws_bytes >= sp.ws_bytes && aligned(indices, 16) && (homo || aligned(data, 16)) &&
+      !std::getenv("BP_CSR_TILED") && !std::getenv("BP_CSR_ATOMIC_FLUSH") &&
+      !std::getenv("BP_CSR_DIRECT")) {
+    // a1 -> split points -> bulk-copy streamed tiles -> ordered reduction
+    // (every output column written by k_csr_reduce: no memset)
+    BP_CUDA(cudaMemsetAsync(w.count, 0, sizeof(int32_t), st));
+    launch_compact(spikes, n_rows, w.active, w.count, sms, st);
+    int64_t *bounds = reinterpret_cast<int64_t *>(static_cast<char *>(ws) + sp.bounds_off);
+    void *partials = static_cast<char *>(ws) + sp.partials_off;
+    bp::CsrSplitArgs sa{indptr, indices, w.active, w.count, bounds, sp.n_tiles, sp.tile_cols,
+                        n_cols};
+    int64_t sblocks = (n_rows + 7) / 8;
+    if (sblocks > static_cast<int64_t>(sms) * 8) sblocks = static_cast<int64_t>(sms) * 8;
+    bp::k_csr_split<<<static_cast<int>(sblocks), 256, 0, st>>>(sa);
+    bp::CsrStreamArgs ca{indices, data, bounds, w.count, indptr + n_rows, partials,
+                         sp.tile_cols, sp.groups, sp.n_tiles, sp.stages, n_cols};
+    if (homo) {
+      if (out_kind == BP_OUT_FIX64) launch_stream<1, true>(ca, sp, st);
+      else launch_stream<0, true>(ca, sp, st);
+    } else {
+      if (out_kind == BP_OUT_FIX64) launch_stream<1, false>(ca, sp, st);
+      else launch_stream<0, false>(ca, sp, st);
+    }
+    bp::CsrTiledArgs t{};
+    t.w = w_homo;
+    t.q = llrint(static_cast<double>(w_homo) * 4294967296.0);
+    t.out = out;
+    t.n_cols = n_cols;
+    t.tile_cols = sp.tile_cols;
+    t.groups = sp.groups;
+    t.partials = partials;
+    t.accumulate = (flags & BP_ACCUMULATE) ? 1 : 0;
+    const int rgrid = static_cast<int>((n_cols + 255) / 256);
+    if (out_kind == BP_OUT_FIX64) bp::k_csr_reduce<1><<<rgrid, 256, 0, st>>>(t, homo);
+    else bp::k_csr_reduce<0><<<rgrid, 256, 0, st>>>(t, homo);
+    return launched();
+  }
   CsrPlan plan = csr_plan(n_rows, n_cols, out_kind, sms);
   const bool reduce_path = plan.tiled && ws_bytes >= plan.ws_bytes && n_rows > 0 &&
                            !std::getenv("BP_CSR_ATOMIC_FLUSH");
@@ -395,6 +487,7 @@ bp_status bp_event_csrmv(const int64_t *indptr, const int32_t *indices,
     t.active = w.active; t.count = w.count;
     t.partials = reduce_path ? static_cast<char *>(ws) + plan.partials_off : nullptr;
     t.accumulate = (flags & BP_ACCUMULATE) ? 1 : 0;
+    t.vec = aligned(indices, 16) && (data == nullptr || aligned(data, 16)) ? 1 : 0;
     const size_t smem = static_cast<size_t>(t.tile_cols) * acc;
     static bool attr_set[2] = {false, false};
     if (!attr_set[out_kind]) {

@@ -215,6 +215,7 @@ struct CsrTiledArgs {
   const int32_t *count;
   void *partials;             // nullable: [tile][group][tile_cols] partial sums
   int accumulate;             // reduce: out += sum (else out = sum)
+  int vec;                    // indices (and data) 16-byte aligned: 128-bit loads
 };
 
 template <int KIND>
@@ -257,11 +258,17 @@ k_csr_tiled(CsrTiledArgs a) {
     lo = lo + span * chunk / kChunks;
     // entry j's contribution to the shared tile
     auto add = [&](int32_t col, float w) {
+      if (static_cast<uint32_t>(col) >= static_cast<uint32_t>(width)) return;  // unsorted row
       if (homo) atomicAdd(accc + col, 1u);               // native ATOMS (POPC.INC)
       else if (KIND == 0) atomicAdd(accf + col, w);
       else atomicAdd(accq + col, static_cast<unsigned long long>(quantize(w)));
     };
     const int32_t c0i = static_cast<int32_t>(c0);
+    if (!a.vec) {                                       // arrays not 16-byte aligned
+      for (int64_t jj = lo + lane; jj < hi; jj += 32)
+        add(__ldg(a.indices + jj) - c0i, a.data ? __ldg(a.data + jj) : a.w);
+      continue;
+    }
     // head up to a 16-byte boundary, 128-bit body (4 int4 loads = 16
     // entries in flight per lane), tail
     const int64_t a0 = min(hi, (lo + 3) & ~int64_t{3});

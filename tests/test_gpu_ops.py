@@ -64,19 +64,26 @@ CSR_CASES = [
     (2000, 3000, 0.01, "normal", 0.01),
     (4000, 4000, 0.02, "homo", 0.002),
     (1000, 100_000, 0.05, "uniform", 0.05),   # fan-out 5000 (config 2 row shape)
-    (300, 500_000, 0.01, "uniform", 0.3),     # > 4 shared-memory tiles: direct path
+    (300, 500_000, 0.01, "uniform", 0.3),     # many column tiles
+    (500, 2_000_000, 0.001, "homo", 0.2),     # > 16 tiles: direct path
+    (20_000, 1000, 0.01, "uniform", 1.0),     # short rows: 16-piece stages
+    (64, 33_333, 0.5, "homo", 1.0),           # rows of ~16k: pieces span stages
 ]
 
 
-@pytest.mark.parametrize("path", ["reduce", "atomic_flush", "direct"])
+@pytest.mark.parametrize("path", ["stream", "tiled", "atomic_flush", "direct", "unaligned"])
 @pytest.mark.parametrize("case", CSR_CASES)
 def test_event_csrmv(bp, orc, case, path, monkeypatch):
-    """reduce: column tiles in shared memory + partial-tile reduction;
-    atomic_flush: tiles flushed with REDs; direct: one RED per event."""
+    """stream: bulk-copy streamed column tiles + ordered partial reduction
+    (default); tiled: register-staged tiles + reduction; atomic_flush: tiles
+    flushed with REDs; direct: one RED per event; unaligned: indices/data not
+    16-byte aligned (the bulk-copy path must step aside)."""
     if path == "direct":
         monkeypatch.setenv("BP_CSR_DIRECT", "1")
     if path == "atomic_flush":
         monkeypatch.setenv("BP_CSR_ATOMIC_FLUSH", "1")
+    if path == "tiled":
+        monkeypatch.setenv("BP_CSR_TILED", "1")
     n_rows, n_cols, p, law, density = case
     ip, ix, dat = inputs.random_csr(n_rows, n_cols, p, seed=n_rows + n_cols,
                                     weights=law, w0=-0.5 if law != "homo" else 1.0,
@@ -85,6 +92,9 @@ def test_event_csrmv(bp, orc, case, path, monkeypatch):
     ev = inputs.spike_pattern(n_rows, density, seed=3)
     spikes = _dev_spikes(ev)
     tip, tix, tdat = _t(ip), _t(ix), _t(dat)
+    if path == "unaligned":          # same values, views offset by one element
+        tix = torch.cat([tix.new_zeros(1), tix])[1:]
+        tdat = None if tdat is None else torch.cat([tdat.new_zeros(1), tdat])[1:]
     # fixed point: bit-exact
     out = torch.zeros(n_cols, dtype=torch.int64, device="cuda")
     bp.event_csrmv(tip, tix, tdat, w_homo, n_rows, n_cols, spikes, out)
