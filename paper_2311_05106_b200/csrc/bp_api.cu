@@ -164,15 +164,14 @@ constexpr int kStreamMaxTiles = 16;
 
 struct StreamPlan {
   bool ok;
-  int32_t n_tiles, tile_cols, groups, stages;
+  int32_t n_tiles, tile_cols, groups;
   size_t smem, bounds_off, partials_off, ws_bytes;
 };
 
 StreamPlan stream_plan(int64_t n_rows, int64_t n_cols, int out_kind, bool homo, int sms) {
   StreamPlan p{};
   const int acc = homo ? 4 : (out_kind == BP_OUT_FIX64 ? 8 : 4);
-  p.stages = homo ? 4 : 3;
-  const size_t fixed = bp::stream_smem(0, acc, p.stages, homo).total + 256;
+  const size_t fixed = bp::stream_smem(0, acc, homo).total + 256;
   if (n_rows < 1 || n_cols < 1 || fixed >= kSmemOptin) return p;
   const int64_t max_cols = static_cast<int64_t>((kSmemOptin - fixed) / acc) & ~int64_t{3};
   const int64_t nt = (n_cols + max_cols - 1) / max_cols;
@@ -180,7 +179,7 @@ StreamPlan stream_plan(int64_t n_rows, int64_t n_cols, int out_kind, bool homo, 
   p.n_tiles = static_cast<int32_t>(nt);
   p.tile_cols = static_cast<int32_t>(round_up(static_cast<size_t>((n_cols + nt - 1) / nt), 4));
   p.groups = sms / p.n_tiles;
-  p.smem = bp::stream_smem(p.tile_cols, acc, p.stages, homo).total;
+  p.smem = bp::stream_smem(p.tile_cols, acc, homo).total;
   const size_t bounds = static_cast<size_t>(n_rows) * (nt + 1) * sizeof(int64_t);
   if (p.smem > kSmemOptin || bounds > (size_t{1} << 30)) return p;
   p.bounds_off = bp_workspace_bytes(n_rows);
@@ -431,7 +430,7 @@ bp_status bp_event_csrmv(const int64_t *indptr, const int32_t *indices,
     if (sblocks > static_cast<int64_t>(sms) * 8) sblocks = static_cast<int64_t>(sms) * 8;
     bp::k_csr_split<<<static_cast<int>(sblocks), 256, 0, st>>>(sa);
     bp::CsrStreamArgs ca{indices, data, bounds, w.count, indptr + n_rows, partials,
-                         sp.tile_cols, sp.groups, sp.n_tiles, sp.stages, n_cols};
+                         sp.tile_cols, sp.groups, sp.n_tiles, 0, n_cols};
     if (homo) {
       if (out_kind == BP_OUT_FIX64) launch_stream<1, true>(ca, sp, st);
       else launch_stream<0, true>(ca, sp, st);

@@ -9,13 +9,11 @@
 //    column-tile boundary (warp-wide 128-entry window at the interpolated
 //    position: one dependent load for uniformly spread columns, a 32-way
 //    search otherwise) -> bounds[k][0..n_tiles];
-//  * k_csr_stream: CTA (tile t, group g) owns column tile t in shared memory
-//    and active rows k = g, g+G, ...  One producer warp issues
-//    cp.async.bulk copies of the rows' in-tile index (and weight) ranges into
-//    a ring of S stages of E entries (several rows per stage, mbarrier
-//    complete_tx), so S*E*4 bytes per SM are in flight without registers;
-//    15 consumer warps turn staged entries into shared-memory atomics and
-//    release the stage.  Only 32-bit integer shared atomics are native on
+//  * k_csr_stream: CTA (tile t, group g) owns column tile t in shared memory;
+//    each of its 32 warps streams its own active rows' in-tile index (and
+//    weight) ranges through a private ring of buffers filled by
+//    cp.async.bulk (mbarrier complete_tx), so ~96 KB per SM are in flight
+//    without registers, and turns them into shared-memory atomics.  Only 32-bit integer shared atomics are native on
 //    sm_100a (f32 and 64-bit adds compile to CAS loops): homogeneous weights
 //    count events (POPC.INC), fixed-point weights add int64 as two 32-bit
 //    words with a carry, fp32 weights use the CAS add.  The tile is stored
@@ -45,13 +43,15 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t *b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
+// try_wait with a suspend-time hint: a waiting warp sleeps in hardware instead
+// of spinning, so it does not take issue slots from the producer warp
 __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT;\n}" ::"r"(smem_u32(b)),
-      "r"(parity)
+      "r"(parity), "r"(0x989680u)
       : "memory");
 }
 // 1-D bulk copy global -> shared (16-byte aligned, size % 16 == 0), completion
@@ -66,33 +66,6 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 }
 
 // --------------------------------------------------------------- split
-// First j in [lo, hi) with idx[j] >= x, starting from a guess g: one 128-entry
-// window (4 per lane) around g, a 32-way search only if the answer is outside.
-__device__ __forceinline__ int64_t window_lower_bound(const int32_t *__restrict__ idx,
-                                                      int64_t lo, int64_t hi, int32_t x,
-                                                      int64_t g) {
-  if (hi - lo <= 128) {
-    const int lane = threadIdx.x & 31;
-    int n_lt = 0;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int64_t j = lo + 4 * lane + e;
-      n_lt += (j < hi && __ldg(idx + j) < x) ? 1 : 0;
-    }
-    return lo + __reduce_add_sync(0xffffffffu, static_cast<unsigned>(n_lt));
-  }
-  const int lane = threadIdx.x & 31;
-  int64_t w0 = g - 64;
-  w0 = w0 < lo ? lo : (w0 > hi - 128 ? hi - 128 : w0);
-  int n_lt = 0;
-#pragma unroll
-  for (int e = 0; e < 4; ++e) n_lt += __ldg(idx + w0 + 4 * lane + e) < x ? 1 : 0;
-  n_lt = static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<unsigned>(n_lt)));
-  if (n_lt == 0 && w0 > lo) return warp_lower_bound(idx, lo, w0, x);
-  if (n_lt == 128 && w0 + 128 < hi) return warp_lower_bound(idx, w0 + 128, hi, x);
-  return w0 + n_lt;
-}
-
 struct CsrSplitArgs {
   const int64_t *indptr;
   const int32_t *indices;
@@ -103,55 +76,108 @@ struct CsrSplitArgs {
   int64_t n_cols;
 };
 
-// One warp per active row: bounds[k][t] = first entry of row active[k] with
-// column >= t * tile_cols (t = 0 and n_tiles: the row's ends).
+// One warp per active row k: bounds[k][t] = first entry of row active[k]
+// with column >= t * tile_cols (t = 0 and n_tiles: the row's ends).  The
+// interior boundaries are searched 4 at a time, 8 lanes each: a 128-entry
+// window (16 loads per lane, all in flight) at the interpolated position --
+// columns of a random row are spread evenly -- so a row costs 3 dependent
+// loads (active, indptr, windows); a boundary outside its window falls back
+// to the warp-wide search.
 __global__ void __launch_bounds__(256) k_csr_split(CsrSplitArgs a) {
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, grp = lane >> 3, gl = lane & 7;
+  const int nt = a.n_tiles;
   const int64_t n_active = *a.count;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const int nt = a.n_tiles;
   for (int64_t k = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
        k < n_active; k += nw) {
     const int64_t r = a.active[k];
     const int64_t lo = __ldg(a.indptr + r), hi = __ldg(a.indptr + r + 1);
     int64_t *b = a.bounds + k * (nt + 1);
-    int64_t cur = lo;
-    for (int t = 1; t < nt; ++t) {
-      const int32_t x = t * a.tile_cols;
-      // columns of a random row are spread evenly: interpolate the position
-      int64_t g = lo + static_cast<int64_t>(static_cast<double>(hi - lo) * x /
-                                            static_cast<double>(a.n_cols));
-      g = g < cur ? cur : (g > hi ? hi : g);
-      const int64_t j = cur < hi ? window_lower_bound(a.indices, cur, hi, x, g) : hi;
-      if (lane == 0) b[t] = j;
-      cur = j;
-    }
     if (lane == 0) {
       b[0] = lo;
       b[nt] = hi;
+    }
+    for (int t0 = 1; t0 < nt; t0 += 4) {
+      const int t = t0 + grp;
+      const bool mine = t < nt;
+      const int32_t x = mine ? t * a.tile_cols : 0;
+      int64_t r0 = lo, r1 = lo;          // counted region of the window
+      int n_lt = 0;
+      if (mine && hi > lo) {
+        const int64_t g = lo + static_cast<int64_t>(static_cast<double>(hi - lo) * x /
+                                                    static_cast<double>(a.n_cols));
+        int64_t w0 = g - 64;
+        w0 = w0 > hi - 128 ? hi - 128 : w0;
+        w0 = (w0 < lo ? lo : w0) & ~int64_t{3};        // 16-byte aligned window start
+        r0 = w0 > lo ? w0 : lo;
+        r1 = w0 + 128 < hi ? w0 + 128 : hi;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int64_t j = w0 + 16 * gl + 4 * v;
+          int32_t e4[4];
+          if (j >= r0 && j + 4 <= r1) {
+            const int4 q = __ldg(reinterpret_cast<const int4 *>(a.indices + j));
+            e4[0] = q.x; e4[1] = q.y; e4[2] = q.z; e4[3] = q.w;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              e4[e] = (j + e >= r0 && j + e < r1) ? __ldg(a.indices + j + e) : INT32_MAX;
+          }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) n_lt += e4[e] < x ? 1 : 0;
+        }
+      }
+#pragma unroll
+      for (int o = 4; o >= 1; o >>= 1) n_lt += __shfl_xor_sync(0xffffffffu, n_lt, o);
+      // the window decides unless every counted entry is < x with more row
+      // beyond it, or none is < x with row before it
+      const bool below = mine && hi > lo && n_lt == 0 && r0 > lo;
+      const bool above = mine && hi > lo && r0 + n_lt == r1 && r1 < hi;
+      if (mine && gl == 0 && !below && !above) b[t] = hi > lo ? r0 + n_lt : lo;
+      const int64_t w0 = r0, w1 = r1;
+      unsigned fb = __ballot_sync(0xffffffffu, (below || above) && gl == 0);
+      while (fb) {                                  // rare: warp-wide search
+        const int src = __ffs(fb) - 1;
+        fb &= fb - 1;
+        const int ts = t0 + (src >> 3);
+        const bool bl = __shfl_sync(0xffffffffu, below, src);
+        const int64_t sw0 = __shfl_sync(0xffffffffu, w0, src);
+        const int64_t sw1 = __shfl_sync(0xffffffffu, w1, src);
+        const int32_t xs = ts * a.tile_cols;
+        const int64_t j = bl ? warp_lower_bound(a.indices, lo, sw0, xs)
+                             : warp_lower_bound(a.indices, sw1, hi, xs);
+        if (lane == 0) b[ts] = j;
+      }
     }
   }
 }
 
 // --------------------------------------------------------------- stream
-constexpr int kStreamThreads = 512;       // warp 0 produces, 15 warps consume
-constexpr int kStreamConsumers = kStreamThreads / 32 - 1;
-constexpr int kStreamSegs = 16;           // row pieces per stage
-constexpr int kStreamEnt = 4096;          // entries per stage
+// Every warp streams its own rows: a private ring of NB buffers of BE
+// entries, filled by cp.async.bulk issued from lane 0 (one mbarrier per
+// buffer, transaction-counted), so up to NB-1 chunks per warp are in flight
+// while the warp turns the current one into shared-memory atomics.  There is
+// no cross-warp synchronisation inside the loop (a single producer warp per
+// CTA could not keep up: one row costs ~100 issue slots).
+#ifndef BP_STREAM_BUFS
+#define BP_STREAM_BUFS 2
+#endif
+#ifndef BP_STREAM_BUF_BYTES
+#define BP_STREAM_BUF_BYTES 2048
+#endif
+constexpr int kStreamThreads = 1024;
+constexpr int kStreamWarps = kStreamThreads / 32;
+constexpr int kStreamBufs = BP_STREAM_BUFS;
+// entries per buffer: BP_STREAM_BUF_BYTES of indices (+ as many of weights)
+__host__ __device__ constexpr int stream_buf_ent(bool homo) {
+  return homo ? BP_STREAM_BUF_BYTES / 4 : BP_STREAM_BUF_BYTES / 8;
+}
 
-struct StreamSeg {
-  int32_t dst;     // first stage slot of the copy (multiple of 4)
-  int32_t len;     // slots of the copy (multiple of 4)
+struct StreamChunk {
   int32_t v0, v1;  // valid entries [v0, v1) relative to a0
   int32_t gl;      // entries >= gl were not copied (end of the array): read from global
-  int32_t pad;
-  int64_t a0;      // global index of slot dst (16-byte aligned)
-};
-struct StreamMeta {
-  int32_t nseg;    // < 0: no more stages
-  int32_t fill;
-  int32_t pad[2];
-  StreamSeg seg[kStreamSegs];
+  int32_t f1;      // min(v1, gl) rounded down to 4: whole quads [round4(v0), f1) valid and staged
+  int64_t a0;      // global index of buffer slot 0 (16-byte aligned)
 };
 
 struct CsrStreamArgs {
@@ -161,24 +187,23 @@ struct CsrStreamArgs {
   const int32_t *count;
   const int64_t *nnz;        // &indptr[n_rows]
   void *partials;            // [tile][group][tile_cols]
-  int32_t tile_cols, groups, n_tiles, stages;
+  int32_t tile_cols, groups, n_tiles, pad;
   int64_t n_cols;
 };
 
 // Shared-memory layout (host and device agree through this function).
 struct StreamSmem {
-  size_t acc, idx, dat, meta, bar, total;
+  size_t idx, dat, meta, bar, total;
 };
-__host__ __device__ inline StreamSmem stream_smem(int tile_cols, int acc_bytes, int stages,
-                                                  bool homo) {
+__host__ __device__ inline StreamSmem stream_smem(int tile_cols, int acc_bytes, bool homo) {
   auto up = [](size_t x) { return (x + 127) & ~size_t{127}; };
+  const size_t ring = static_cast<size_t>(kStreamWarps) * kStreamBufs * stream_buf_ent(homo) * 4;
   StreamSmem s{};
-  s.acc = 0;
-  s.idx = up(static_cast<size_t>(tile_cols) * acc_bytes);
-  s.dat = s.idx + static_cast<size_t>(stages) * kStreamEnt * 4;
-  s.meta = s.dat + (homo ? 0 : static_cast<size_t>(stages) * kStreamEnt * 4);
-  s.bar = up(s.meta + static_cast<size_t>(stages) * sizeof(StreamMeta));
-  s.total = s.bar + static_cast<size_t>(2 * stages) * 8;
+  s.idx = up(static_cast<size_t>(tile_cols + 4) * acc_bytes);   // + sink slot
+  s.dat = s.idx + ring;
+  s.meta = s.dat + (homo ? 0 : ring);
+  s.bar = up(s.meta + static_cast<size_t>(kStreamWarps) * kStreamBufs * sizeof(StreamChunk));
+  s.total = s.bar + static_cast<size_t>(kStreamWarps) * kStreamBufs * 8;
   return s;
 }
 
@@ -187,161 +212,163 @@ template <int KIND, bool HOMO>
 __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs a) {
   extern __shared__ __align__(128) unsigned char sm[];
   constexpr int acc_bytes = (HOMO || KIND == 0) ? 4 : 8;
-  const int S = a.stages;
-  const StreamSmem L = stream_smem(a.tile_cols, acc_bytes, S, HOMO);
-  int32_t *sidx = reinterpret_cast<int32_t *>(sm + L.idx);
-  float *sdat = reinterpret_cast<float *>(sm + L.dat);
-  StreamMeta *meta = reinterpret_cast<StreamMeta *>(sm + L.meta);
-  uint64_t *full = reinterpret_cast<uint64_t *>(sm + L.bar);
-  uint64_t *empty = full + S;
+  constexpr int BE = stream_buf_ent(HOMO);
+  constexpr int NB = kStreamBufs;
+  const StreamSmem L = stream_smem(a.tile_cols, acc_bytes, HOMO);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int32_t *bidx = reinterpret_cast<int32_t *>(sm + L.idx) + warp * NB * BE;
+  float *bdat = reinterpret_cast<float *>(sm + L.dat) + warp * NB * BE;
+  StreamChunk *meta = reinterpret_cast<StreamChunk *>(sm + L.meta) + warp * NB;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sm + L.bar) + warp * NB;
 
   const int tile = blockIdx.x / a.groups, group = blockIdx.x % a.groups;
   const int64_t c0 = static_cast<int64_t>(tile) * a.tile_cols;
   const int64_t c1 = min(c0 + a.tile_cols, a.n_cols);
   const int width = static_cast<int>(c1 - c0);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int32_t c0i = static_cast<int32_t>(c0);
 
-  for (int c = tid; c < width; c += kStreamThreads) {
+  for (int c = tid; c <= width; c += kStreamThreads) {      // tile + sink slot
     if (acc_bytes == 4) reinterpret_cast<uint32_t *>(sm)[c] = 0u;
     else reinterpret_cast<unsigned long long *>(sm)[c] = 0ull;
   }
-  if (tid == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, kStreamConsumers);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" ::
-                     : "memory");
-  }
+  if (lane < NB) mbar_init(bar + lane, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" ::
+                   : "memory");
   __syncthreads();
-  const int64_t n_active = *a.count;
-  const int nt = a.n_tiles, G = a.groups;
 
-  if (warp == 0) {
-    // ---- producer: pack the rows' in-tile ranges into stages
-    const int64_t nnz4 = __ldg(a.nnz) & ~int64_t{3};
-    int s = 0, nseg = 0, fill = 0;
-    uint32_t ph = 0;
-    mbar_wait(empty + s, ph ^ 1u);
-    auto commit = [&]() {
-      if (lane == 0) {
-        meta[s].nseg = nseg;
-        meta[s].fill = fill;
-        mbar_arrive(full + s);
-      }
-      if (++s == S) { s = 0; ph ^= 1u; }
-      nseg = 0;
-      fill = 0;
-      mbar_wait(empty + s, ph ^ 1u);
-    };
-    for (int64_t kb = group; kb < n_active; kb += 32LL * G) {
-      const int64_t k = kb + static_cast<int64_t>(lane) * G;
-      int64_t lo_l = 0, hi_l = 0;
-      if (k < n_active) {
-        lo_l = __ldg(a.bounds + k * (nt + 1) + tile);
-        hi_l = __ldg(a.bounds + k * (nt + 1) + tile + 1);
-      }
-      for (int j = 0; j < 32; ++j) {
-        int64_t lo = __shfl_sync(0xffffffffu, lo_l, j);
-        const int64_t hi = __shfl_sync(0xffffffffu, hi_l, j);
-        while (lo < hi) {
-          const int room = kStreamEnt - fill;
-          if (room < 4 || nseg == kStreamSegs) {
-            commit();
-            continue;
-          }
-          const int64_t a0 = lo & ~int64_t{3};
-          const int64_t a1 = min((hi + 3) & ~int64_t{3}, a0 + room);
-          const int64_t piece_hi = min(hi, a1);
-          const int64_t ac = min(a1, max(nnz4, a0));     // copyable end
-          const uint32_t bytes = static_cast<uint32_t>(ac - a0) * 4u;
-          if (lane == 0) {
-            StreamSeg &sg = meta[s].seg[nseg];
-            sg.dst = fill;
-            sg.len = static_cast<int32_t>(a1 - a0);
-            sg.v0 = static_cast<int32_t>(lo - a0);
-            sg.v1 = static_cast<int32_t>(piece_hi - a0);
-            sg.gl = static_cast<int32_t>(ac - a0);
-            sg.a0 = a0;
-            if (bytes) {
-              mbar_expect_tx(full + s, HOMO ? bytes : 2u * bytes);
-              bulk_g2s(sidx + static_cast<size_t>(s) * kStreamEnt + fill, a.indices + a0,
-                       bytes, full + s);
-              if (!HOMO)
-                bulk_g2s(sdat + static_cast<size_t>(s) * kStreamEnt + fill, a.data + a0,
-                         bytes, full + s);
-            }
-          }
-          fill += static_cast<int>(a1 - a0);
-          ++nseg;
-          lo = piece_hi;
-        }
-      }
+  const int64_t n_active = *a.count;
+  const int nt = a.n_tiles;
+  const int64_t nnz4 = __ldg(a.nnz) & ~int64_t{3};
+  // this warp's rows: k = w, w + NW, ... (w = global warp index within the tile)
+  const int64_t NW = static_cast<int64_t>(a.groups) * kStreamWarps;
+  const int64_t w = static_cast<int64_t>(group) * kStreamWarps + warp;
+  // lane j holds the tile range of the warp's row 32 b + j; next batch prefetched
+  auto load_range = [&](int64_t kb, int64_t &lo_r, int64_t &hi_r) {
+    const int64_t k = w + (kb + lane) * NW;
+    lo_r = 0;
+    hi_r = 0;
+    if (k < n_active) {
+      lo_r = __ldg(a.bounds + k * (nt + 1) + tile);
+      hi_r = __ldg(a.bounds + k * (nt + 1) + tile + 1);
     }
-    if (nseg) commit();
+  };
+  const int64_t my_rows = n_active > w ? (n_active - w + NW - 1) / NW : 0;
+  int64_t blo, bhi, nlo, nhi;             // current / next batch (per lane)
+  load_range(0, blo, bhi);
+  load_range(32, nlo, nhi);
+  // issue cursor (warp-uniform): row index ir, position pos in [pos, hi)
+  int64_t ir = 0, pos = 0, hi = 0;
+  auto row_at = [&](int64_t r) {          // broadcast row r's range (r in current batch)
+    const int j = static_cast<int>(r & 31);
+    pos = __shfl_sync(0xffffffffu, blo, j);
+    hi = __shfl_sync(0xffffffffu, bhi, j);
+  };
+  if (my_rows > 0) row_at(0);
+  // next chunk into buffer b; false when the rows are exhausted
+  auto issue = [&](int b) -> bool {
+    while (ir < my_rows && pos >= hi) {   // advance to the next non-empty row
+      ++ir;
+      if (ir >= my_rows) break;
+      if ((ir & 31) == 0) {
+        blo = nlo;
+        bhi = nhi;
+        load_range(ir + 32, nlo, nhi);
+      }
+      row_at(ir);
+    }
+    if (ir >= my_rows) return false;
+    const int64_t a0 = pos & ~int64_t{3};
+    const int64_t a1 = min((hi + 3) & ~int64_t{3}, a0 + BE);
+    const int64_t piece_hi = min(hi, a1);
+    const int64_t ac = min(a1, max(nnz4, a0));           // copyable end
+    const uint32_t bytes = static_cast<uint32_t>(ac - a0) * 4u;
     if (lane == 0) {
-      meta[s].nseg = -1;
-      mbar_arrive(full + s);
-    }
-  } else {
-    // ---- consumers: staged entries -> shared-memory atomics
-    const int c = tid - 32;
-    constexpr int NC = kStreamThreads - 32;
-    const int32_t c0i = static_cast<int32_t>(c0);
-    int s = 0;
-    uint32_t ph = 0;
-    for (;;) {
-      mbar_wait(full + s, ph);
-      const StreamMeta &m = meta[s];
-      const int nseg = m.nseg;
-      if (nseg < 0) break;
-      const int fill = m.fill;
-      const int32_t *si = sidx + static_cast<size_t>(s) * kStreamEnt;
-      const float *sd = sdat + static_cast<size_t>(s) * kStreamEnt;
-      int i = 0;
-      int seg_end = m.seg[0].len;      // seg[0].dst == 0
-      for (int q = 4 * c; q < fill; q += 4 * NC) {
-        while (q >= seg_end) {
-          ++i;
-          seg_end = m.seg[i].dst + m.seg[i].len;
-        }
-        const StreamSeg &sg = m.seg[i];
-        const int off = q - sg.dst;
-        const int4 ci = *reinterpret_cast<const int4 *>(si + q);
-        float4 wi = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (!HOMO) wi = *reinterpret_cast<const float4 *>(sd + q);
-        const int32_t cv[4] = {ci.x, ci.y, ci.z, ci.w};
-        const float wv[4] = {wi.x, wi.y, wi.z, wi.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int o = off + e;
-          if (o < sg.v0 || o >= sg.v1) continue;
-          int32_t col = cv[e];
-          float w = wv[e];
-          if (o >= sg.gl) {                    // tail past the last 16-byte boundary
-            col = __ldg(a.indices + sg.a0 + o);
-            if (!HOMO) w = __ldg(a.data + sg.a0 + o);
-          }
-          const uint32_t lc = static_cast<uint32_t>(col - c0i);
-          if (lc >= static_cast<uint32_t>(width)) continue;   // unsorted row: skip
-          if (HOMO) atomicAdd(reinterpret_cast<uint32_t *>(sm) + lc, 1u);
-          else if (KIND == 0) atomicAdd(reinterpret_cast<float *>(sm) + lc, w);
-          else {
-            // int64 add as two native 32-bit ATOMS (a 64-bit shared add is
-            // a CAS loop on sm_100a): low word with return, carry into the
-            // high word -- exact modulo 2^64, like an int64 add
-            unsigned *p = reinterpret_cast<unsigned *>(sm) + 2 * lc;
-            const unsigned long long qq = static_cast<unsigned long long>(quantize(w));
-            const unsigned lo = static_cast<unsigned>(qq);
-            const unsigned old = atomicAdd(p, lo);
-            atomicAdd(p + 1, static_cast<unsigned>(qq >> 32) + (old + lo < old ? 1u : 0u));
-          }
-        }
+      StreamChunk &m = meta[b];
+      m.v0 = static_cast<int32_t>(pos - a0);
+      m.v1 = static_cast<int32_t>(piece_hi - a0);
+      m.gl = static_cast<int32_t>(ac - a0);
+      m.f1 = min(m.v1, m.gl) & ~3;
+      m.a0 = a0;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                       smem_u32(bar + b)),
+                   "r"(HOMO ? bytes : 2u * bytes)
+                   : "memory");
+      if (bytes) {
+        bulk_g2s(bidx + b * BE, a.indices + a0, bytes, bar + b);
+        if (!HOMO) bulk_g2s(bdat + b * BE, a.data + a0, bytes, bar + b);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty + s);
-      if (++s == S) { s = 0; ph ^= 1u; }
     }
+    pos = piece_hi;
+    return true;
+  };
+
+  // lc = col - c0 clamped to the sink slot `width` (entries of an unsorted
+  // row that fall outside the tile land there and are never flushed):
+  // branch-free, one clamp per entry
+  auto add = [&](int32_t col, float wgt) {
+    const uint32_t lc = min(static_cast<uint32_t>(col - c0i), static_cast<uint32_t>(width));
+    if (HOMO) atomicAdd(reinterpret_cast<uint32_t *>(sm) + lc, 1u);
+    else if (KIND == 0) atomicAdd(reinterpret_cast<float *>(sm) + lc, wgt);
+    else {
+      // int64 add as two native 32-bit ATOMS (a 64-bit shared add is a CAS
+      // loop on sm_100a): low word with return, carry into the high word --
+      // exact modulo 2^64, like an int64 add
+      unsigned *p = reinterpret_cast<unsigned *>(sm) + 2 * lc;
+      const unsigned long long qq = static_cast<unsigned long long>(quantize(wgt));
+      const unsigned lo = static_cast<unsigned>(qq);
+      const unsigned old = atomicAdd(p, lo);
+      atomicAdd(p + 1, static_cast<unsigned>(qq >> 32) + (old + lo < old ? 1u : 0u));
+    }
+  };
+  auto add4 = [&](const int4 &ci, const float4 &wi) {
+    add(ci.x, wi.x);
+    add(ci.y, wi.y);
+    add(ci.z, wi.z);
+    add(ci.w, wi.w);
+  };
+
+  int64_t issued = 0;
+  for (int b = 0; b < NB; ++b) issued += issue(b) ? 1 : 0;
+  for (int64_t used = 0; used < issued; ++used) {
+    const int b = static_cast<int>(used % NB);
+    mbar_wait(bar + b, static_cast<uint32_t>((used / NB) & 1));
+    const StreamChunk m = meta[b];
+    const int32_t *si = bidx + b * BE;
+    const float *sd = bdat + b * BE;
+    // body: whole quads [qa, qb), two per lane per iteration, no checks
+    const int qa = (m.v0 + 3) & ~3, qb = m.f1;
+    for (int q = qa + 4 * lane; q < qb; q += 256) {
+      const bool two = q + 128 < qb;
+      const int4 c1 = *reinterpret_cast<const int4 *>(si + q);
+      const int4 c2 = two ? *reinterpret_cast<const int4 *>(si + q + 128) : c1;
+      float4 w1 = make_float4(0.f, 0.f, 0.f, 0.f), w2 = w1;
+      if (!HOMO) {
+        w1 = *reinterpret_cast<const float4 *>(sd + q);
+        if (two) w2 = *reinterpret_cast<const float4 *>(sd + q + 128);
+      }
+      add4(c1, w1);
+      if (two) add4(c2, w2);
+    }
+    // edges: head [v0, min(qa, v1)) on lanes 0-3, tail [max(qa, qb), v1) on
+    // lanes 4-11 (<= 3 rounding entries + <= 3 not copied at the array end)
+    {
+      const int o = lane < 4 ? m.v0 + lane : max(qa, qb) + lane - 4;
+      const int end = lane < 4 ? min(qa, m.v1) : m.v1;
+      if (lane < 12 && o < end) {
+        int32_t col;
+        float wgt = 0.f;
+        if (o < m.gl) {
+          col = si[o];
+          if (!HOMO) wgt = sd[o];
+        } else {                                  // tail past the last 16-byte boundary
+          col = __ldg(a.indices + m.a0 + o);
+          if (!HOMO) wgt = __ldg(a.data + m.a0 + o);
+        }
+        add(col, wgt);
+      }
+    }
+    __syncwarp();                                 // buffer b consumed by every lane
+    issued += issue(b) ? 1 : 0;
   }
   __syncthreads();
   // partial tile -> [tile][group][tile_cols], 16-byte stores
