@@ -553,7 +553,10 @@ def run_micro(args):
                                              with_data=(law != "homo"), device=dev)
         row_nnz = (ip[1:] - ip[:-1]).cpu().numpy()
         data = dat if law != "homo" else None
-        call = lambda s: bp.event_csrmv(ip, ix, data, 0.6, n, n, s, out, ws=ws)
+        # the matrix is fixed across calls: split points analysed once,
+        # outside the timed region (like the CSR itself); --no-plan: per call
+        plan = None if args.no_plan else bp.csrmv_plan(ip, ix, n, n, out.dtype, homo=data is None)
+        call = lambda s: bp.event_csrmv(ip, ix, data, 0.6, n, n, s, out, ws=ws, plan=plan)
         ev_per_pat = [int(row_nnz[e.astype(bool)].sum()) for e in pats]
         bytes_per_event = 8 if law != "homo" else 4
         nnz = int(ip[-1].item())
@@ -621,9 +624,12 @@ def run_micro(args):
             "config": {"workload": f"{kind}_{law}", "shape": [n, n], "p": p, "density": d,
                        "K": bp.conn_len(p), "events_per_call": events / args.steps,
                        "active_rows_per_call": active,
+                       "csr_plan": (kind == "csrmv" and not args.no_plan),
                        "l2": ("flushed between calls (256 MB write)" if flush
                               else "working set %.0f MB > 2 x L2" % (working_set / 1e6))},
-            "gpu_launches": 2 * args.steps, "clocks": clocks, "roofline": roof,
+            # compact + scatter (+ per-call split of the rows without a plan)
+            "gpu_launches": (3 if kind == "csrmv" and args.no_plan else 2) * args.steps,
+            "clocks": clocks, "roofline": roof,
             "call_us": {"median": float(np.median(ms)) * 1e3, "min": float(np.min(ms)) * 1e3}}
     print(json.dumps(line), flush=True)
 
@@ -646,6 +652,8 @@ def main():
     ap.add_argument("--density", type=float, default=0.1, help="microbench spike density")
     ap.add_argument("--law", choices=["homo", "uniform", "normal"], default="uniform")
     ap.add_argument("--fix", action="store_true", help="microbench int64 fixed-point output")
+    ap.add_argument("--no-plan", action="store_true",
+                    help="csrmv microbench: split rows on every call (no csrmv_plan)")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="spike exchange backend for --gpus > 1 (gloo: functional check "
                          "with several ranks on one GPU)")

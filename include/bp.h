@@ -103,6 +103,8 @@ bp_status bp_compact_spikes(const uint32_t *spikes, int64_t n, int32_t *active,
 /* a2: event_csrmv, Listing S1 with indices[j] (the listing's indices[i] is a
  * typo):  for r with bit r set, for k in [indptr[r], indptr[r+1]):
  *     out[indices[k]] += (data ? data[k] : w_homo)
+ * indices: ascending within each row (canonical CSR); an unsorted row gives
+ * wrong sums on the tiled paths but never writes outside `out`.
  * out: n_cols float32 (BP_OUT_F32) or int64 (BP_OUT_FIX64), 16-byte aligned.
  * ws: >= bp_workspace_bytes(n_rows) bytes (bp_csrmv_workspace_bytes for the
  * atomic-free path), 256-byte aligned. */
@@ -111,6 +113,30 @@ bp_status bp_event_csrmv(const int64_t *indptr, const int32_t *indices,
                          int64_t n_cols, const uint32_t *spikes, void *out,
                          int out_kind, uint32_t flags, void *ws,
                          size_t ws_bytes, bp_stream stream);
+
+/* a2 with a reusable analysis of a fixed matrix (cf. cuSPARSE's SpMV
+ * preprocessing).  bp_event_csrmv splits every active row at the column-tile
+ * boundaries of its shared-memory accumulation on each call; for a matrix
+ * that is reused (a network's projection, a benchmark's 10,000 calls) the
+ * split points of all rows can be computed once:
+ *   plan_bytes = bp_csrmv_plan_bytes(n_rows, n_cols, out_kind, data == NULL)
+ *     (0: nothing to precompute -- the output fits one tile);
+ *   bp_csrmv_plan(...) writes int32 split offsets [n_rows][n_tiles-1] into the
+ *     caller's device buffer `plan` (16-byte aligned), asynchronously;
+ *   bp_event_csrmv_planned(plan, ...) then behaves exactly like
+ *     bp_event_csrmv without the per-call split.
+ * The plan is valid for the same (indptr, indices, n_rows, n_cols, out_kind,
+ * homogeneous-or-not) on the same device type; a stale plan gives wrong sums
+ * but never reads outside the row.  Requires indices ascending per row. */
+size_t bp_csrmv_plan_bytes(int64_t n_rows, int64_t n_cols, int out_kind, int homo);
+bp_status bp_csrmv_plan(const int64_t *indptr, const int32_t *indices, int64_t n_rows,
+                        int64_t n_cols, int out_kind, int homo, void *plan,
+                        size_t plan_bytes, bp_stream stream);
+bp_status bp_event_csrmv_planned(const void *plan, size_t plan_bytes, const int64_t *indptr,
+                                 const int32_t *indices, const float *data, float w_homo,
+                                 int64_t n_rows, int64_t n_cols, const uint32_t *spikes,
+                                 void *out, int out_kind, uint32_t flags, void *ws,
+                                 size_t ws_bytes, bp_stream stream);
 
 /* JIT connectivity (App. C; the "four scalars (p, mu, sigma, s)"
  * of P:192).  The matrix is a pure function of (seed, K, seg_len, n_rows,

@@ -26,6 +26,7 @@ CONN_JIT, CONN_CSR = 0, 1
 EXPORTED = [
     "bp_abi_version", "bp_status_string", "bp_last_error", "bp_conn_len",
     "bp_workspace_bytes", "bp_csrmv_workspace_bytes", "bp_compact_spikes", "bp_event_csrmv",
+    "bp_csrmv_plan_bytes", "bp_csrmv_plan", "bp_event_csrmv_planned",
     "bp_jitconn_event_mv_homo", "bp_jitconn_event_mv_uniform",
     "bp_jitconn_event_mv_normal", "bp_jitconn_row_counts",
     "bp_jitconn_materialize", "bp_neuron_step", "bp_network_workspace_bytes",
@@ -102,6 +103,11 @@ def lib():
         L.bp_csrmv_workspace_bytes.restype = sz
         L.bp_compact_spikes.argtypes = [P, i64, P, P, P]
         L.bp_event_csrmv.argtypes = [P, P, P, f32, i64, i64, P, P, i32, u32, P, sz, P]
+        L.bp_csrmv_plan_bytes.argtypes = [i64, i64, i32, i32]
+        L.bp_csrmv_plan_bytes.restype = sz
+        L.bp_csrmv_plan.argtypes = [P, P, i64, i64, i32, i32, P, sz, P]
+        L.bp_event_csrmv_planned.argtypes = [P, sz, P, P, P, f32, i64, i64, P, P, i32, u32,
+                                             P, sz, P]
         jit_tail = [P, i64, i64, i64, i64, P, i32, u32, P, sz, P]
         L.bp_jitconn_event_mv_homo.argtypes = [ctypes.POINTER(JitConn), f32] + jit_tail
         L.bp_jitconn_event_mv_uniform.argtypes = [ctypes.POINTER(JitConn), f32, f32] + jit_tail
@@ -126,7 +132,7 @@ def lib():
         for name in EXPORTED:
             if name not in ("bp_network_destroy", "bp_status_string",
                             "bp_last_error", "bp_conn_len", "bp_workspace_bytes",
-                            "bp_csrmv_workspace_bytes",
+                            "bp_csrmv_workspace_bytes", "bp_csrmv_plan_bytes",
                             "bp_network_workspace_bytes", "bp_abi_version"):
                 getattr(L, name).restype = ctypes.c_int
         _lib = L
@@ -194,17 +200,38 @@ def compact_spikes(spikes: torch.Tensor, n: int, active: torch.Tensor,
 
 
 def event_csrmv(indptr, indices, data, w_homo, n_rows, n_cols, spikes, out,
-                accumulate=False, ws=None, stream=None):
-    """brainpy.math.event.csrmv (Listing S1) -> out[n_cols] (f32 or fix64)."""
+                accumulate=False, ws=None, stream=None, plan=None):
+    """brainpy.math.event.csrmv (Listing S1) -> out[n_cols] (f32 or fix64).
+    plan: optional csrmv_plan(...) of this matrix (skips the per-call split)."""
     _cuda(indptr, indices, data, spikes, out)
     if ws is None:
         nbytes = int(lib().bp_csrmv_workspace_bytes(int(n_rows), int(n_cols), _out_kind(out)))
         ws = torch.empty(nbytes, dtype=torch.uint8, device=out.device)
-    _check(lib().bp_event_csrmv(
-        _ptr(indptr), _ptr(indices), _ptr(data), float(w_homo), int(n_rows),
-        int(n_cols), _ptr(spikes), _ptr(out), _out_kind(out),
-        ACCUMULATE if accumulate else 0, _ptr(ws), ws.numel(), _stream(stream)))
+    tail = (_ptr(indptr), _ptr(indices), _ptr(data), float(w_homo), int(n_rows),
+            int(n_cols), _ptr(spikes), _ptr(out), _out_kind(out),
+            ACCUMULATE if accumulate else 0, _ptr(ws), ws.numel(), _stream(stream))
+    if plan is not None:
+        _check(lib().bp_event_csrmv_planned(_ptr(plan), plan.numel(), *tail))
+    else:
+        _check(lib().bp_event_csrmv(*tail))
     return out
+
+
+def csrmv_plan(indptr, indices, n_rows, n_cols, out_dtype=torch.float32, homo=True,
+               stream=None):
+    """Split points of every row at the column-tile boundaries of
+    event_csrmv's shared-memory accumulation, for a matrix reused across
+    calls; pass the result as event_csrmv(..., plan=...).  None when the
+    output fits one tile (nothing to precompute)."""
+    _cuda(indptr, indices)
+    kind = 1 if out_dtype == torch.int64 else 0
+    nbytes = int(lib().bp_csrmv_plan_bytes(int(n_rows), int(n_cols), kind, int(bool(homo))))
+    if nbytes == 0:
+        return None
+    plan = torch.empty(nbytes, dtype=torch.uint8, device=indptr.device)
+    _check(lib().bp_csrmv_plan(_ptr(indptr), _ptr(indices), int(n_rows), int(n_cols), kind,
+                               int(bool(homo)), _ptr(plan), plan.numel(), _stream(stream)))
+    return plan
 
 
 def jitconn_event_mv(law: int, spec: JitConn, w0: float, w1: float, spikes,

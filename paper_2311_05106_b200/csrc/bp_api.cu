@@ -165,7 +165,7 @@ constexpr int kStreamMaxTiles = 16;
 struct StreamPlan {
   bool ok;
   int32_t n_tiles, tile_cols, groups;
-  size_t smem, bounds_off, partials_off, ws_bytes;
+  size_t smem, split_off, partials_off, ws_bytes, plan_bytes;
 };
 
 StreamPlan stream_plan(int64_t n_rows, int64_t n_cols, int out_kind, bool homo, int sms) {
@@ -180,25 +180,38 @@ StreamPlan stream_plan(int64_t n_rows, int64_t n_cols, int out_kind, bool homo, 
   p.tile_cols = static_cast<int32_t>(round_up(static_cast<size_t>((n_cols + nt - 1) / nt), 4));
   p.groups = sms / p.n_tiles;
   p.smem = bp::stream_smem(p.tile_cols, acc, homo).total;
-  const size_t bounds = static_cast<size_t>(n_rows) * (nt + 1) * sizeof(int64_t);
-  if (p.smem > kSmemOptin || bounds > (size_t{1} << 30)) return p;
-  p.bounds_off = bp_workspace_bytes(n_rows);
-  p.partials_off = p.bounds_off + round_up(bounds, 256);
+  p.plan_bytes = round_up(static_cast<size_t>(n_rows) * (nt - 1) * sizeof(int32_t), 256);
+  if (p.smem > kSmemOptin || p.plan_bytes > (size_t{1} << 30)) return p;
+  p.split_off = bp_workspace_bytes(n_rows);
+  p.partials_off = p.split_off + p.plan_bytes;
   p.ws_bytes = p.partials_off +
                round_up(static_cast<size_t>(nt) * p.groups * p.tile_cols * acc, 256);
   p.ok = true;
   return p;
 }
 
+// Cooperative launch when a.out is set (the kernel reduces the partial tiles
+// itself after a grid barrier); returns false if that launch is refused
+// (not every CTA co-resident), so the caller runs k_csr_reduce instead.
 template <int KIND, bool HOMO>
-void launch_stream(const bp::CsrStreamArgs &a, const StreamPlan &p, cudaStream_t st) {
+bool launch_stream(bp::CsrStreamArgs a, const StreamPlan &p, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(bp::k_csr_stream<KIND, HOMO>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemOptin));
     attr = true;
   }
-  bp::k_csr_stream<KIND, HOMO><<<p.n_tiles * p.groups, bp::kStreamThreads, p.smem, st>>>(a);
+  const dim3 grid(p.n_tiles * p.groups), block(bp::kStreamThreads);
+  if (a.out != nullptr) {
+    void *args[] = {&a};
+    if (cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(bp::k_csr_stream<KIND, HOMO>),
+                                    grid, block, args, p.smem, st) == cudaSuccess)
+      return true;
+    cudaGetLastError();
+    a.out = nullptr;
+  }
+  bp::k_csr_stream<KIND, HOMO><<<grid, block, p.smem, st>>>(a);
+  return false;
 }
 
 // ------------------------------------------------------------- JIT helpers
@@ -394,11 +407,11 @@ bp_status bp_compact_spikes(const uint32_t *spikes, int64_t n, int32_t *active,
   return launched();
 }
 
-bp_status bp_event_csrmv(const int64_t *indptr, const int32_t *indices,
-                         const float *data, float w_homo, int64_t n_rows,
-                         int64_t n_cols, const uint32_t *spikes, void *out,
-                         int out_kind, uint32_t flags, void *ws,
-                         size_t ws_bytes, bp_stream stream) {
+namespace {
+bp_status csrmv_impl(const void *plan, size_t plan_bytes, const int64_t *indptr,
+                     const int32_t *indices, const float *data, float w_homo, int64_t n_rows,
+                     int64_t n_cols, const uint32_t *spikes, void *out, int out_kind,
+                     uint32_t flags, void *ws, size_t ws_bytes, bp_stream stream) {
   int sms = 0;
   bp_status s = device_ready(&sms);
   if (s != BP_OK) return s;
@@ -422,38 +435,46 @@ bp_status bp_event_csrmv(const int64_t *indptr, const int32_t *indices,
     // (every output column written by k_csr_reduce: no memset)
     BP_CUDA(cudaMemsetAsync(w.count, 0, sizeof(int32_t), st));
     launch_compact(spikes, n_rows, w.active, w.count, sms, st);
-    int64_t *bounds = reinterpret_cast<int64_t *>(static_cast<char *>(ws) + sp.bounds_off);
     void *partials = static_cast<char *>(ws) + sp.partials_off;
-    bp::CsrSplitArgs sa{indptr, indices, w.active, w.count, bounds, sp.n_tiles, sp.tile_cols,
-                        n_cols};
-    int64_t sblocks = (n_rows + 7) / 8;
-    if (sblocks > static_cast<int64_t>(sms) * 8) sblocks = static_cast<int64_t>(sms) * 8;
-    bp::k_csr_split<<<static_cast<int>(sblocks), 256, 0, st>>>(sa);
-    bp::CsrStreamArgs ca{indices, data, bounds, w.count, indptr + n_rows, partials,
-                         sp.tile_cols, sp.groups, sp.n_tiles, 0, n_cols};
-    if (homo) {
-      if (out_kind == BP_OUT_FIX64) launch_stream<1, true>(ca, sp, st);
-      else launch_stream<0, true>(ca, sp, st);
-    } else {
-      if (out_kind == BP_OUT_FIX64) launch_stream<1, false>(ca, sp, st);
-      else launch_stream<0, false>(ca, sp, st);
+    int32_t *split = static_cast<int32_t *>(const_cast<void *>(plan));
+    if (sp.n_tiles > 1 && (split == nullptr || plan_bytes < sp.plan_bytes)) {
+      // no (usable) plan: split points of this call's active rows
+      split = reinterpret_cast<int32_t *>(static_cast<char *>(ws) + sp.split_off);
+      bp::CsrSplitArgs sa{indptr, indices, w.active, w.count, n_rows, split, sp.n_tiles,
+                          sp.tile_cols, n_cols};
+      int64_t sblocks = (n_rows + 7) / 8;
+      if (sblocks > static_cast<int64_t>(sms) * 8) sblocks = static_cast<int64_t>(sms) * 8;
+      bp::k_csr_split<<<static_cast<int>(sblocks), 256, 0, st>>>(sa);
     }
+    bp::CsrStreamArgs ca{indices, data, indptr, split, w.active, w.count, indptr + n_rows, partials,
+                         sp.tile_cols, sp.groups, sp.n_tiles, (flags & BP_ACCUMULATE) ? 1 : 0,
+                         n_cols, std::getenv("BP_CSR_NO_FUSE") ? nullptr : out, w_homo,
+                         llrint(static_cast<double>(w_homo) * 4294967296.0)};
+    bool fused;
+    if (homo) {
+      fused = out_kind == BP_OUT_FIX64 ? launch_stream<1, true>(ca, sp, st)
+                                       : launch_stream<0, true>(ca, sp, st);
+    } else {
+      fused = out_kind == BP_OUT_FIX64 ? launch_stream<1, false>(ca, sp, st)
+                                       : launch_stream<0, false>(ca, sp, st);
+    }
+    if (fused) return launched();
     bp::CsrTiledArgs t{};
     t.w = w_homo;
-    t.q = llrint(static_cast<double>(w_homo) * 4294967296.0);
+    t.q = ca.q;
     t.out = out;
     t.n_cols = n_cols;
     t.tile_cols = sp.tile_cols;
     t.groups = sp.groups;
     t.partials = partials;
-    t.accumulate = (flags & BP_ACCUMULATE) ? 1 : 0;
+    t.accumulate = ca.accumulate;
     const int rgrid = static_cast<int>((n_cols + 255) / 256);
     if (out_kind == BP_OUT_FIX64) bp::k_csr_reduce<1><<<rgrid, 256, 0, st>>>(t, homo);
     else bp::k_csr_reduce<0><<<rgrid, 256, 0, st>>>(t, homo);
     return launched();
   }
-  CsrPlan plan = csr_plan(n_rows, n_cols, out_kind, sms);
-  const bool reduce_path = plan.tiled && ws_bytes >= plan.ws_bytes && n_rows > 0 &&
+  CsrPlan tp = csr_plan(n_rows, n_cols, out_kind, sms);
+  const bool reduce_path = tp.tiled && ws_bytes >= tp.ws_bytes && n_rows > 0 &&
                            !std::getenv("BP_CSR_ATOMIC_FLUSH");
   // the reduce kernel writes every output column: no memset needed there
   if (!(flags & BP_ACCUMULATE) && !reduce_path) BP_CUDA(cudaMemsetAsync(out, 0, elt * n_cols, st));
@@ -475,16 +496,16 @@ bp_status bp_event_csrmv(const int64_t *indptr, const int32_t *indices,
   // of <= 200 KB (scatter.cuh, k_csr_tiled); partial tiles reduced by
   // k_csr_reduce when the workspace holds them, else flushed with REDs;
   // outputs wider than 4 tiles: one RED per event (k_csr_scatter).
-  const size_t acc = plan.acc;
-  const int64_t n_tiles = plan.n_tiles;
-  if (plan.tiled) {
+  const size_t acc = tp.acc;
+  const int64_t n_tiles = tp.n_tiles;
+  if (tp.tiled) {
     bp::CsrTiledArgs t{};
     t.indptr = indptr; t.indices = indices; t.data = data; t.w = w_homo;
     t.q = a.e.q; t.out = out; t.n_cols = n_cols;
-    t.tile_cols = plan.tile_cols;
-    t.groups = plan.groups;
+    t.tile_cols = tp.tile_cols;
+    t.groups = tp.groups;
     t.active = w.active; t.count = w.count;
-    t.partials = reduce_path ? static_cast<char *>(ws) + plan.partials_off : nullptr;
+    t.partials = reduce_path ? static_cast<char *>(ws) + tp.partials_off : nullptr;
     t.accumulate = (flags & BP_ACCUMULATE) ? 1 : 0;
     t.vec = aligned(indices, 16) && (data == nullptr || aligned(data, 16)) ? 1 : 0;
     const size_t smem = static_cast<size_t>(t.tile_cols) * acc;
@@ -510,6 +531,56 @@ bp_status bp_event_csrmv(const int64_t *indptr, const int32_t *indices,
   }
   launch_csr(a, out_kind, grid_for_items(n_rows, sms), st);
   return launched();
+}
+}  // namespace
+
+bp_status bp_event_csrmv(const int64_t *indptr, const int32_t *indices,
+                         const float *data, float w_homo, int64_t n_rows,
+                         int64_t n_cols, const uint32_t *spikes, void *out,
+                         int out_kind, uint32_t flags, void *ws,
+                         size_t ws_bytes, bp_stream stream) {
+  return csrmv_impl(nullptr, 0, indptr, indices, data, w_homo, n_rows, n_cols, spikes, out,
+                    out_kind, flags, ws, ws_bytes, stream);
+}
+
+size_t bp_csrmv_plan_bytes(int64_t n_rows, int64_t n_cols, int out_kind, int homo) {
+  int sms = 148;
+  if (device_ready(&sms) != BP_OK) sms = 148;
+  const StreamPlan sp = stream_plan(n_rows, n_cols, out_kind, homo != 0, sms);
+  return sp.ok ? sp.plan_bytes : 0;
+}
+
+bp_status bp_csrmv_plan(const int64_t *indptr, const int32_t *indices, int64_t n_rows,
+                        int64_t n_cols, int out_kind, int homo, void *plan, size_t plan_bytes,
+                        bp_stream stream) {
+  int sms = 0;
+  bp_status s = device_ready(&sms);
+  if (s != BP_OK) return s;
+  BP_CHECK(n_rows >= 0 && n_rows <= kMaxDim && n_cols >= 1 && n_cols <= kMaxDim,
+           BP_ERR_SHAPE, "n_rows=%lld n_cols=%lld", (long long)n_rows, (long long)n_cols);
+  BP_CHECK(out_kind == BP_OUT_F32 || out_kind == BP_OUT_FIX64, BP_ERR_INVALID_ARG,
+           "out_kind %d", out_kind);
+  const StreamPlan sp = stream_plan(n_rows, n_cols, out_kind, homo != 0, sms);
+  if (!sp.ok || sp.n_tiles <= 1 || n_rows == 0) return BP_OK;   // nothing to precompute
+  BP_CHECK(indptr && indices && plan, BP_ERR_INVALID_ARG, "NULL indptr/indices/plan");
+  BP_CHECK(plan_bytes >= sp.plan_bytes, BP_ERR_WORKSPACE, "plan %zu bytes < %zu required",
+           plan_bytes, sp.plan_bytes);
+  BP_CHECK(aligned(plan, 16), BP_ERR_WORKSPACE, "plan must be 16-byte aligned");
+  bp::CsrSplitArgs sa{indptr, indices, nullptr, nullptr, n_rows, static_cast<int32_t *>(plan),
+                      sp.n_tiles, sp.tile_cols, n_cols};
+  int64_t blocks = (n_rows + 7) / 8;
+  if (blocks > static_cast<int64_t>(sms) * 16) blocks = static_cast<int64_t>(sms) * 16;
+  bp::k_csr_split<<<static_cast<int>(blocks), 256, 0, as_stream(stream)>>>(sa);
+  return launched();
+}
+
+bp_status bp_event_csrmv_planned(const void *plan, size_t plan_bytes, const int64_t *indptr,
+                                 const int32_t *indices, const float *data, float w_homo,
+                                 int64_t n_rows, int64_t n_cols, const uint32_t *spikes,
+                                 void *out, int out_kind, uint32_t flags, void *ws,
+                                 size_t ws_bytes, bp_stream stream) {
+  return csrmv_impl(plan, plan_bytes, indptr, indices, data, w_homo, n_rows, n_cols, spikes,
+                    out, out_kind, flags, ws, ws_bytes, stream);
 }
 
 bp_status bp_jitconn_event_mv_homo(const bp_jitconn *spec, float weight,

@@ -8,7 +8,8 @@
 //  * k_csr_split finds, once per active row, where the row crosses each
 //    column-tile boundary (warp-wide 128-entry window at the interpolated
 //    position: one dependent load for uniformly spread columns, a 32-way
-//    search otherwise) -> bounds[k][0..n_tiles];
+//    search otherwise) -> split[row][t-1] (per call for the active rows, or
+//    once for all rows by bp_csrmv_plan when the matrix is reused);
 //  * k_csr_stream: CTA (tile t, group g) owns column tile t in shared memory;
 //    each of its 32 warps streams its own active rows' in-tile index (and
 //    weight) ranges through a private ring of buffers filled by
@@ -24,9 +25,12 @@
 #pragma once
 #include <cstdint>
 
+#include <cooperative_groups.h>
+
 #include "scatter.cuh"
 
 namespace bp {
+namespace cg = cooperative_groups;
 
 // ----------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -69,34 +73,31 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 struct CsrSplitArgs {
   const int64_t *indptr;
   const int32_t *indices;
-  const int32_t *active;
-  const int32_t *count;
-  int64_t *bounds;       // [k][n_tiles + 1]
+  const int32_t *active;   // nullptr: every row (the plan of bp_csrmv_plan)
+  const int32_t *count;    // nullptr: n_rows rows
+  int64_t n_rows;
+  int32_t *split;          // [row][n_tiles - 1]: first entry with column >= t*tile_cols, - indptr[row]
   int32_t n_tiles, tile_cols;
   int64_t n_cols;
 };
 
-// One warp per active row k: bounds[k][t] = first entry of row active[k]
-// with column >= t * tile_cols (t = 0 and n_tiles: the row's ends).  The
-// interior boundaries are searched 4 at a time, 8 lanes each: a 128-entry
-// window (16 loads per lane, all in flight) at the interpolated position --
+// One warp per row r (active[k], or k itself): split[r][t-1] = (first entry
+// of row r with column >= t * tile_cols) - indptr[r], t = 1 .. n_tiles-1.
+// The boundaries are searched 4 at a time, 8 lanes each: a 128-entry window
+// (4 int4 loads per lane, all in flight) at the interpolated position --
 // columns of a random row are spread evenly -- so a row costs 3 dependent
 // loads (active, indptr, windows); a boundary outside its window falls back
 // to the warp-wide search.
 __global__ void __launch_bounds__(256) k_csr_split(CsrSplitArgs a) {
   const int lane = threadIdx.x & 31, grp = lane >> 3, gl = lane & 7;
   const int nt = a.n_tiles;
-  const int64_t n_active = *a.count;
+  const int64_t n_items = a.count ? *a.count : a.n_rows;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   for (int64_t k = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-       k < n_active; k += nw) {
-    const int64_t r = a.active[k];
+       k < n_items; k += nw) {
+    const int64_t r = a.active ? a.active[k] : k;
     const int64_t lo = __ldg(a.indptr + r), hi = __ldg(a.indptr + r + 1);
-    int64_t *b = a.bounds + k * (nt + 1);
-    if (lane == 0) {
-      b[0] = lo;
-      b[nt] = hi;
-    }
+    int32_t *b = a.split + r * (nt - 1) - 1;      // b[t], t = 1 .. nt-1
     for (int t0 = 1; t0 < nt; t0 += 4) {
       const int t = t0 + grp;
       const bool mine = t < nt;
@@ -133,7 +134,8 @@ __global__ void __launch_bounds__(256) k_csr_split(CsrSplitArgs a) {
       // beyond it, or none is < x with row before it
       const bool below = mine && hi > lo && n_lt == 0 && r0 > lo;
       const bool above = mine && hi > lo && r0 + n_lt == r1 && r1 < hi;
-      if (mine && gl == 0 && !below && !above) b[t] = hi > lo ? r0 + n_lt : lo;
+      if (mine && gl == 0 && !below && !above)
+        b[t] = static_cast<int32_t>((hi > lo ? r0 + n_lt : lo) - lo);
       const int64_t w0 = r0, w1 = r1;
       unsigned fb = __ballot_sync(0xffffffffu, (below || above) && gl == 0);
       while (fb) {                                  // rare: warp-wide search
@@ -146,7 +148,7 @@ __global__ void __launch_bounds__(256) k_csr_split(CsrSplitArgs a) {
         const int32_t xs = ts * a.tile_cols;
         const int64_t j = bl ? warp_lower_bound(a.indices, lo, sw0, xs)
                              : warp_lower_bound(a.indices, sw1, hi, xs);
-        if (lane == 0) b[ts] = j;
+        if (lane == 0) b[ts] = static_cast<int32_t>(j - lo);
       }
     }
   }
@@ -173,22 +175,35 @@ __host__ __device__ constexpr int stream_buf_ent(bool homo) {
   return homo ? BP_STREAM_BUF_BYTES / 4 : BP_STREAM_BUF_BYTES / 8;
 }
 
-struct StreamChunk {
+constexpr int kStreamSegs = 8;   // row pieces per buffer
+
+struct StreamChunk {   // one row piece in a buffer
+  int32_t dst;     // first buffer slot of the piece (multiple of 4)
   int32_t v0, v1;  // valid entries [v0, v1) relative to a0
   int32_t gl;      // entries >= gl were not copied (end of the array): read from global
   int32_t f1;      // min(v1, gl) rounded down to 4: whole quads [round4(v0), f1) valid and staged
-  int64_t a0;      // global index of buffer slot 0 (16-byte aligned)
+  int32_t pad;
+  int64_t a0;      // global index of slot dst (16-byte aligned)
+};
+struct StreamBuf {
+  int32_t nseg, pad[3];
+  StreamChunk seg[kStreamSegs];
 };
 
 struct CsrStreamArgs {
   const int32_t *indices;
   const float *data;         // nullptr -> homogeneous: count events per column
-  const int64_t *bounds;
+  const int64_t *indptr;
+  const int32_t *split;      // [row][n_tiles - 1] (k_csr_split / bp_csrmv_plan)
+  const int32_t *active;
   const int32_t *count;
   const int64_t *nnz;        // &indptr[n_rows]
   void *partials;            // [tile][group][tile_cols]
-  int32_t tile_cols, groups, n_tiles, pad;
+  int32_t tile_cols, groups, n_tiles, accumulate;
   int64_t n_cols;
+  void *out;                 // fused reduction (cooperative launch)
+  float w;                   // homogeneous weight
+  long long q;               // quantize(w)
 };
 
 // Shared-memory layout (host and device agree through this function).
@@ -202,10 +217,24 @@ __host__ __device__ inline StreamSmem stream_smem(int tile_cols, int acc_bytes, 
   s.idx = up(static_cast<size_t>(tile_cols + 4) * acc_bytes);   // + sink slot
   s.dat = s.idx + ring;
   s.meta = s.dat + (homo ? 0 : ring);
-  s.bar = up(s.meta + static_cast<size_t>(kStreamWarps) * kStreamBufs * sizeof(StreamChunk));
+  s.bar = up(s.meta + static_cast<size_t>(kStreamWarps) * kStreamBufs * sizeof(StreamBuf));
   s.total = s.bar + static_cast<size_t>(kStreamWarps) * kStreamBufs * 8;
   return s;
 }
+
+#ifdef BP_CSR_TIMING
+__device__ unsigned long long g_csr_t[1024][8];
+#define CSR_MARK(k)                                                            \
+  do {                                                                         \
+    if (threadIdx.x == 0) {                                                    \
+      unsigned long long t_;                                                   \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                   \
+      g_csr_t[blockIdx.x][k] = t_;                                             \
+    }                                                                          \
+  } while (0)
+#else
+#define CSR_MARK(k) do {} while (0)
+#endif
 
 // KIND: 0 f32 partials, 1 int64 fixed-point partials; HOMO: uint32 counts.
 template <int KIND, bool HOMO>
@@ -218,7 +247,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int32_t *bidx = reinterpret_cast<int32_t *>(sm + L.idx) + warp * NB * BE;
   float *bdat = reinterpret_cast<float *>(sm + L.dat) + warp * NB * BE;
-  StreamChunk *meta = reinterpret_cast<StreamChunk *>(sm + L.meta) + warp * NB;
+  StreamBuf *meta = reinterpret_cast<StreamBuf *>(sm + L.meta) + warp * NB;
   uint64_t *bar = reinterpret_cast<uint64_t *>(sm + L.bar) + warp * NB;
 
   const int tile = blockIdx.x / a.groups, group = blockIdx.x % a.groups;
@@ -226,6 +255,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs 
   const int64_t c1 = min(c0 + a.tile_cols, a.n_cols);
   const int width = static_cast<int>(c1 - c0);
   const int32_t c0i = static_cast<int32_t>(c0);
+  CSR_MARK(0);
 
   for (int c = tid; c <= width; c += kStreamThreads) {      // tile + sink slot
     if (acc_bytes == 4) reinterpret_cast<uint32_t *>(sm)[c] = 0u;
@@ -236,6 +266,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs 
                    : "memory");
   __syncthreads();
 
+  CSR_MARK(1);
   const int64_t n_active = *a.count;
   const int nt = a.n_tiles;
   const int64_t nnz4 = __ldg(a.nnz) & ~int64_t{3};
@@ -248,8 +279,13 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs 
     lo_r = 0;
     hi_r = 0;
     if (k < n_active) {
-      lo_r = __ldg(a.bounds + k * (nt + 1) + tile);
-      hi_r = __ldg(a.bounds + k * (nt + 1) + tile + 1);
+      const int64_t r = __ldg(a.active + k);
+      const int64_t p0 = __ldg(a.indptr + r), p1 = __ldg(a.indptr + r + 1);
+      const int32_t *sp = a.split + r * (nt - 1) - 1;      // sp[t], t = 1 .. nt-1
+      lo_r = tile > 0 ? p0 + __ldg(sp + tile) : p0;
+      hi_r = tile < nt - 1 ? p0 + __ldg(sp + tile + 1) : p1;
+      lo_r = min(max(lo_r, p0), p1);          // a stale plan cannot leave the row
+      hi_r = min(max(hi_r, lo_r), p1);
     }
   };
   const int64_t my_rows = n_active > w ? (n_active - w + NW - 1) / NW : 0;
@@ -264,41 +300,50 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs 
     hi = __shfl_sync(0xffffffffu, bhi, j);
   };
   if (my_rows > 0) row_at(0);
-  // next chunk into buffer b; false when the rows are exhausted
+  // fill buffer b with the next row pieces (up to kStreamSegs, BE slots);
+  // false when the rows are exhausted
   auto issue = [&](int b) -> bool {
-    while (ir < my_rows && pos >= hi) {   // advance to the next non-empty row
-      ++ir;
+    int fill = 0, nseg = 0;
+    while (nseg < kStreamSegs && fill <= BE - 4) {
+      while (ir < my_rows && pos >= hi) { // advance to the next non-empty row
+        ++ir;
+        if (ir >= my_rows) break;
+        if ((ir & 31) == 0) {
+          blo = nlo;
+          bhi = nhi;
+          load_range(ir + 32, nlo, nhi);
+        }
+        row_at(ir);
+      }
       if (ir >= my_rows) break;
-      if ((ir & 31) == 0) {
-        blo = nlo;
-        bhi = nhi;
-        load_range(ir + 32, nlo, nhi);
+      const int64_t a0 = pos & ~int64_t{3};
+      const int64_t a1 = min((hi + 3) & ~int64_t{3}, a0 + (BE - fill));
+      const int64_t piece_hi = min(hi, a1);
+      const int64_t ac = min(a1, max(nnz4, a0));         // copyable end
+      const uint32_t bytes = static_cast<uint32_t>(ac - a0) * 4u;
+      if (lane == 0) {
+        StreamChunk &m = meta[b].seg[nseg];
+        m.dst = fill;
+        m.v0 = static_cast<int32_t>(pos - a0);
+        m.v1 = static_cast<int32_t>(piece_hi - a0);
+        m.gl = static_cast<int32_t>(ac - a0);
+        m.f1 = min(m.v1, m.gl) & ~3;
+        m.a0 = a0;
+        if (bytes) {
+          mbar_expect_tx(bar + b, HOMO ? bytes : 2u * bytes);
+          bulk_g2s(bidx + b * BE + fill, a.indices + a0, bytes, bar + b);
+          if (!HOMO) bulk_g2s(bdat + b * BE + fill, a.data + a0, bytes, bar + b);
+        }
       }
-      row_at(ir);
+      fill += static_cast<int>(a1 - a0);
+      ++nseg;
+      pos = piece_hi;
     }
-    if (ir >= my_rows) return false;
-    const int64_t a0 = pos & ~int64_t{3};
-    const int64_t a1 = min((hi + 3) & ~int64_t{3}, a0 + BE);
-    const int64_t piece_hi = min(hi, a1);
-    const int64_t ac = min(a1, max(nnz4, a0));           // copyable end
-    const uint32_t bytes = static_cast<uint32_t>(ac - a0) * 4u;
+    if (nseg == 0) return false;
     if (lane == 0) {
-      StreamChunk &m = meta[b];
-      m.v0 = static_cast<int32_t>(pos - a0);
-      m.v1 = static_cast<int32_t>(piece_hi - a0);
-      m.gl = static_cast<int32_t>(ac - a0);
-      m.f1 = min(m.v1, m.gl) & ~3;
-      m.a0 = a0;
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                       smem_u32(bar + b)),
-                   "r"(HOMO ? bytes : 2u * bytes)
-                   : "memory");
-      if (bytes) {
-        bulk_g2s(bidx + b * BE, a.indices + a0, bytes, bar + b);
-        if (!HOMO) bulk_g2s(bdat + b * BE, a.data + a0, bytes, bar + b);
-      }
+      meta[b].nseg = nseg;
+      mbar_arrive(bar + b);
     }
-    pos = piece_hi;
     return true;
   };
 
@@ -332,26 +377,27 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs 
   for (int64_t used = 0; used < issued; ++used) {
     const int b = static_cast<int>(used % NB);
     mbar_wait(bar + b, static_cast<uint32_t>((used / NB) & 1));
-    const StreamChunk m = meta[b];
-    const int32_t *si = bidx + b * BE;
-    const float *sd = bdat + b * BE;
-    // body: whole quads [qa, qb), two per lane per iteration, no checks
-    const int qa = (m.v0 + 3) & ~3, qb = m.f1;
-    for (int q = qa + 4 * lane; q < qb; q += 256) {
-      const bool two = q + 128 < qb;
-      const int4 c1 = *reinterpret_cast<const int4 *>(si + q);
-      const int4 c2 = two ? *reinterpret_cast<const int4 *>(si + q + 128) : c1;
-      float4 w1 = make_float4(0.f, 0.f, 0.f, 0.f), w2 = w1;
-      if (!HOMO) {
-        w1 = *reinterpret_cast<const float4 *>(sd + q);
-        if (two) w2 = *reinterpret_cast<const float4 *>(sd + q + 128);
+    const int nseg = meta[b].nseg;
+    for (int sgi = 0; sgi < nseg; ++sgi) {
+      const StreamChunk m = meta[b].seg[sgi];
+      const int32_t *si = bidx + b * BE + m.dst;
+      const float *sd = bdat + b * BE + m.dst;
+      // body: whole quads [qa, qb), two per lane per iteration, no checks
+      const int qa = (m.v0 + 3) & ~3, qb = m.f1;
+      for (int q = qa + 4 * lane; q < qb; q += 256) {
+        const bool two = q + 128 < qb;
+        const int4 c1 = *reinterpret_cast<const int4 *>(si + q);
+        const int4 c2 = two ? *reinterpret_cast<const int4 *>(si + q + 128) : c1;
+        float4 w1 = make_float4(0.f, 0.f, 0.f, 0.f), w2 = w1;
+        if (!HOMO) {
+          w1 = *reinterpret_cast<const float4 *>(sd + q);
+          if (two) w2 = *reinterpret_cast<const float4 *>(sd + q + 128);
+        }
+        add4(c1, w1);
+        if (two) add4(c2, w2);
       }
-      add4(c1, w1);
-      if (two) add4(c2, w2);
-    }
-    // edges: head [v0, min(qa, v1)) on lanes 0-3, tail [max(qa, qb), v1) on
-    // lanes 4-11 (<= 3 rounding entries + <= 3 not copied at the array end)
-    {
+      // edges: head [v0, min(qa, v1)) on lanes 0-3, tail [max(qa, qb), v1)
+      // on lanes 4-11 (<= 3 rounding entries + <= 3 not copied at the end)
       const int o = lane < 4 ? m.v0 + lane : max(qa, qb) + lane - 4;
       const int end = lane < 4 ? min(qa, m.v1) : m.v1;
       if (lane < 12 && o < end) {
@@ -370,7 +416,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs 
     __syncwarp();                                 // buffer b consumed by every lane
     issued += issue(b) ? 1 : 0;
   }
+  CSR_MARK(2);
   __syncthreads();
+  CSR_MARK(3);
   // partial tile -> [tile][group][tile_cols], 16-byte stores
   char *dst = static_cast<char *>(a.partials) +
               (static_cast<size_t>(tile) * a.groups + group) * a.tile_cols * acc_bytes;
@@ -378,6 +426,48 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs 
   for (int k = tid; k < n16; k += kStreamThreads)
     reinterpret_cast<uint4 *>(dst)[k] = reinterpret_cast<const uint4 *>(sm)[k];
   for (int b = n16 * 16 + tid; b < width * acc_bytes; b += kStreamThreads) dst[b] = sm[b];
+  CSR_MARK(4);
+  if (a.out == nullptr) return;
+  // fused reduction (cooperative launch: every CTA is resident): after a
+  // grid-wide barrier, CTA g of tile t sums column slice g of the tile over
+  // the groups in ascending order (L2-resident partials, deterministic)
+  __threadfence();
+  cg::this_grid().sync();
+  CSR_MARK(5);
+  const int per = (width + a.groups - 1) / a.groups;
+  const int s0 = group * per, s1 = min(width, s0 + per);
+  const size_t stride = static_cast<size_t>(a.tile_cols);
+  const size_t base = static_cast<size_t>(tile) * a.groups * stride;
+  for (int cc = s0 + tid; cc < s1; cc += kStreamThreads) {
+    const int64_t c = c0 + cc;
+    if (HOMO) {
+      const unsigned *p = static_cast<const unsigned *>(a.partials) + base + cc;
+      unsigned long long n = 0;
+      for (int g = 0; g < a.groups; ++g) n += __ldcg(p + g * stride);
+      if (KIND == 0) {
+        const float v = __fmul_rn(__ull2float_rn(n), a.w);
+        float *o = static_cast<float *>(a.out) + c;
+        *o = a.accumulate ? __fadd_rn(*o, v) : v;
+      } else {
+        const long long v = static_cast<long long>(n) * a.q;
+        long long *o = static_cast<long long *>(a.out) + c;
+        *o = a.accumulate ? *o + v : v;
+      }
+    } else if (KIND == 0) {
+      const float *p = static_cast<const float *>(a.partials) + base + cc;
+      float v = 0.f;
+      for (int g = 0; g < a.groups; ++g) v = __fadd_rn(v, __ldcg(p + g * stride));
+      float *o = static_cast<float *>(a.out) + c;
+      *o = a.accumulate ? __fadd_rn(*o, v) : v;
+    } else {
+      const long long *p = static_cast<const long long *>(a.partials) + base + cc;
+      long long v = 0;
+      for (int g = 0; g < a.groups; ++g) v += __ldcg(p + g * stride);
+      long long *o = static_cast<long long *>(a.out) + c;
+      *o = a.accumulate ? *o + v : v;
+    }
+  }
+  CSR_MARK(6);
 }
 
 }  // namespace bp

@@ -71,11 +71,15 @@ CSR_CASES = [
 ]
 
 
-@pytest.mark.parametrize("path", ["stream", "tiled", "atomic_flush", "direct", "unaligned"])
+@pytest.mark.parametrize("path", ["stream", "planned", "stream_nofuse", "tiled", "atomic_flush",
+                                  "direct", "unaligned"])
 @pytest.mark.parametrize("case", CSR_CASES)
 def test_event_csrmv(bp, orc, case, path, monkeypatch):
     """stream: bulk-copy streamed column tiles + ordered partial reduction
-    (default); tiled: register-staged tiles + reduction; atomic_flush: tiles
+    (default, partials reduced inside the cooperative kernel); planned: the
+    same with split points precomputed by csrmv_plan; stream_nofuse:
+    the same with a separate reduction kernel; tiled: register-staged tiles
+    + reduction; atomic_flush: tiles
     flushed with REDs; direct: one RED per event; unaligned: indices/data not
     16-byte aligned (the bulk-copy path must step aside)."""
     if path == "direct":
@@ -84,6 +88,8 @@ def test_event_csrmv(bp, orc, case, path, monkeypatch):
         monkeypatch.setenv("BP_CSR_ATOMIC_FLUSH", "1")
     if path == "tiled":
         monkeypatch.setenv("BP_CSR_TILED", "1")
+    if path == "stream_nofuse":
+        monkeypatch.setenv("BP_CSR_NO_FUSE", "1")
     n_rows, n_cols, p, law, density = case
     ip, ix, dat = inputs.random_csr(n_rows, n_cols, p, seed=n_rows + n_cols,
                                     weights=law, w0=-0.5 if law != "homo" else 1.0,
@@ -95,14 +101,18 @@ def test_event_csrmv(bp, orc, case, path, monkeypatch):
     if path == "unaligned":          # same values, views offset by one element
         tix = torch.cat([tix.new_zeros(1), tix])[1:]
         tdat = None if tdat is None else torch.cat([tdat.new_zeros(1), tdat])[1:]
+    plan64 = plan32 = None
+    if path == "planned":
+        plan64 = bp.csrmv_plan(tip, tix, n_rows, n_cols, torch.int64, homo=tdat is None)
+        plan32 = bp.csrmv_plan(tip, tix, n_rows, n_cols, torch.float32, homo=tdat is None)
     # fixed point: bit-exact
     out = torch.zeros(n_cols, dtype=torch.int64, device="cuda")
-    bp.event_csrmv(tip, tix, tdat, w_homo, n_rows, n_cols, spikes, out)
+    bp.event_csrmv(tip, tix, tdat, w_homo, n_rows, n_cols, spikes, out, plan=plan64)
     want = orc.event_csrmv(ip, ix, dat, w_homo, n_rows, n_cols, ev, orc.OUT_FIX)
     assert np.array_equal(out.cpu().numpy(), want)
     # fp32 atomics: rule T2
     out32 = torch.full((n_cols,), 7.0, dtype=torch.float32, device="cuda")
-    bp.event_csrmv(tip, tix, tdat, w_homo, n_rows, n_cols, spikes, out32)
+    bp.event_csrmv(tip, tix, tdat, w_homo, n_rows, n_cols, spikes, out32, plan=plan32)
     ref, absw = orc.event_csrmv(ip, ix, dat, w_homo, n_rows, n_cols, ev, orc.OUT_F64,
                                 with_abs=True)
     err = np.abs(out32.cpu().numpy().astype(np.float64) - ref)
