@@ -171,7 +171,7 @@ struct StreamPlan {
 StreamPlan stream_plan(int64_t n_rows, int64_t n_cols, int out_kind, bool homo, int sms) {
   StreamPlan p{};
   const int acc = homo ? 4 : (out_kind == BP_OUT_FIX64 ? 8 : 4);
-  const size_t fixed = bp::stream_smem(0, acc, homo).total + 256;
+  const size_t fixed = bp::stream_smem(0, acc, homo).total + bp::kStreamStaticSmem + 256;
   if (n_rows < 1 || n_cols < 1 || fixed >= kSmemOptin) return p;
   const int64_t max_cols = static_cast<int64_t>((kSmemOptin - fixed) / acc) & ~int64_t{3};
   const int64_t nt = (n_cols + max_cols - 1) / max_cols;
@@ -181,7 +181,7 @@ StreamPlan stream_plan(int64_t n_rows, int64_t n_cols, int out_kind, bool homo, 
   p.groups = sms / p.n_tiles;
   p.smem = bp::stream_smem(p.tile_cols, acc, homo).total;
   p.plan_bytes = round_up(static_cast<size_t>(n_rows) * (nt - 1) * sizeof(int32_t), 256);
-  if (p.smem > kSmemOptin || p.plan_bytes > (size_t{1} << 30)) return p;
+  if (p.smem + bp::kStreamStaticSmem > kSmemOptin || p.plan_bytes > (size_t{1} << 30)) return p;
   p.split_off = bp_workspace_bytes(n_rows);
   p.partials_off = p.split_off + p.plan_bytes;
   p.ws_bytes = p.partials_off +
@@ -190,27 +190,40 @@ StreamPlan stream_plan(int64_t n_rows, int64_t n_cols, int out_kind, bool homo, 
   return p;
 }
 
-// Cooperative launch when a.out is set (the kernel reduces the partial tiles
-// itself after a grid barrier); returns false if that launch is refused
-// (not every CTA co-resident), so the caller runs k_csr_reduce instead.
 template <int KIND, bool HOMO>
-bool launch_stream(bp::CsrStreamArgs a, const StreamPlan &p, cudaStream_t st) {
+void stream_attr() {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(bp::k_csr_stream<KIND, HOMO>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemOptin));
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kSmemOptin - bp::kStreamStaticSmem));
     attr = true;
   }
-  const dim3 grid(p.n_tiles * p.groups), block(bp::kStreamThreads);
-  if (a.out != nullptr) {
-    void *args[] = {&a};
-    if (cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(bp::k_csr_stream<KIND, HOMO>),
-                                    grid, block, args, p.smem, st) == cudaSuccess)
-      return true;
-    cudaGetLastError();
-    a.out = nullptr;
-  }
-  bp::k_csr_stream<KIND, HOMO><<<grid, block, p.smem, st>>>(a);
+}
+
+// Cooperative launch (every CTA resident: grid barriers allowed); false if
+// the launch is refused.
+template <int KIND, bool HOMO>
+bool stream_coop(bp::CsrStreamArgs a, const StreamPlan &p, cudaStream_t st) {
+  stream_attr<KIND, HOMO>();
+  void *args[] = {&a};
+  if (cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(bp::k_csr_stream<KIND, HOMO>),
+                                  dim3(p.n_tiles * p.groups), dim3(bp::kStreamThreads), args,
+                                  p.smem, st) == cudaSuccess)
+    return true;
+  cudaGetLastError();
+  return false;
+}
+
+// With a.out set, try the cooperative launch (the kernel reduces the
+// partial tiles itself after a grid barrier); returns false when it ran
+// without the reduction, so the caller runs k_csr_reduce.
+template <int KIND, bool HOMO>
+bool launch_stream(bp::CsrStreamArgs a, const StreamPlan &p, cudaStream_t st) {
+  stream_attr<KIND, HOMO>();
+  if (a.out != nullptr && stream_coop<KIND, HOMO>(a, p, st)) return true;
+  a.out = nullptr;
+  bp::k_csr_stream<KIND, HOMO><<<p.n_tiles * p.groups, bp::kStreamThreads, p.smem, st>>>(a);
   return false;
 }
 
@@ -432,32 +445,33 @@ bp_status csrmv_impl(const void *plan, size_t plan_bytes, const int64_t *indptr,
       !std::getenv("BP_CSR_TILED") && !std::getenv("BP_CSR_ATOMIC_FLUSH") &&
       !std::getenv("BP_CSR_DIRECT")) {
     // a1 -> split points -> bulk-copy streamed tiles -> ordered reduction
-    // (every output column written by k_csr_reduce: no memset)
-    BP_CUDA(cudaMemsetAsync(w.count, 0, sizeof(int32_t), st));
-    launch_compact(spikes, n_rows, w.active, w.count, sms, st);
+    // (every output column written by the reduction: no memset)
     void *partials = static_cast<char *>(ws) + sp.partials_off;
     int32_t *split = static_cast<int32_t *>(const_cast<void *>(plan));
-    if (sp.n_tiles > 1 && (split == nullptr || plan_bytes < sp.plan_bytes)) {
-      // no (usable) plan: split points of this call's active rows
-      split = reinterpret_cast<int32_t *>(static_cast<char *>(ws) + sp.split_off);
+    const bool need_split = sp.n_tiles > 1 && (split == nullptr || plan_bytes < sp.plan_bytes);
+    const bool coop = !std::getenv("BP_CSR_NO_FUSE");
+    if (need_split) split = reinterpret_cast<int32_t *>(static_cast<char *>(ws) + sp.split_off);
+    bp::CsrStreamArgs ca{indices, data, indptr, split, w.active, w.count, indptr + n_rows,
+                         partials, sp.tile_cols, sp.groups, sp.n_tiles,
+                         (flags & BP_ACCUMULATE) ? 1 : 0, n_cols, coop ? out : nullptr, w_homo,
+                         llrint(static_cast<double>(w_homo) * 4294967296.0)};
+    auto stream_kernel = [&](const bp::CsrStreamArgs &c) {
+      if (homo)
+        return out_kind == BP_OUT_FIX64 ? launch_stream<1, true>(c, sp, st)
+                                        : launch_stream<0, true>(c, sp, st);
+      return out_kind == BP_OUT_FIX64 ? launch_stream<1, false>(c, sp, st)
+                                      : launch_stream<0, false>(c, sp, st);
+    };
+    BP_CUDA(cudaMemsetAsync(w.count, 0, sizeof(int32_t), st));
+    launch_compact(spikes, n_rows, w.active, w.count, sms, st);
+    if (need_split) {
       bp::CsrSplitArgs sa{indptr, indices, w.active, w.count, n_rows, split, sp.n_tiles,
                           sp.tile_cols, n_cols};
       int64_t sblocks = (n_rows + 7) / 8;
       if (sblocks > static_cast<int64_t>(sms) * 8) sblocks = static_cast<int64_t>(sms) * 8;
       bp::k_csr_split<<<static_cast<int>(sblocks), 256, 0, st>>>(sa);
     }
-    bp::CsrStreamArgs ca{indices, data, indptr, split, w.active, w.count, indptr + n_rows, partials,
-                         sp.tile_cols, sp.groups, sp.n_tiles, (flags & BP_ACCUMULATE) ? 1 : 0,
-                         n_cols, std::getenv("BP_CSR_NO_FUSE") ? nullptr : out, w_homo,
-                         llrint(static_cast<double>(w_homo) * 4294967296.0)};
-    bool fused;
-    if (homo) {
-      fused = out_kind == BP_OUT_FIX64 ? launch_stream<1, true>(ca, sp, st)
-                                       : launch_stream<0, true>(ca, sp, st);
-    } else {
-      fused = out_kind == BP_OUT_FIX64 ? launch_stream<1, false>(ca, sp, st)
-                                       : launch_stream<0, false>(ca, sp, st);
-    }
+    const bool fused = stream_kernel(ca);
     if (fused) return launched();
     bp::CsrTiledArgs t{};
     t.w = w_homo;

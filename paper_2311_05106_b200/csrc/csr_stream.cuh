@@ -168,6 +168,8 @@ __global__ void __launch_bounds__(256) k_csr_split(CsrSplitArgs a) {
 #define BP_STREAM_BUF_BYTES 2048
 #endif
 constexpr int kStreamThreads = 1024;
+// static shared memory of k_csr_stream
+constexpr size_t kStreamStaticSmem = 0;
 constexpr int kStreamWarps = kStreamThreads / 32;
 constexpr int kStreamBufs = BP_STREAM_BUFS;
 // entries per buffer: BP_STREAM_BUF_BYTES of indices (+ as many of weights)
@@ -179,14 +181,14 @@ constexpr int kStreamSegs = 8;   // row pieces per buffer
 
 struct StreamChunk {   // one row piece in a buffer
   int32_t dst;     // first buffer slot of the piece (multiple of 4)
+  int32_t len;     // slots of the piece (multiple of 4)
   int32_t v0, v1;  // valid entries [v0, v1) relative to a0
   int32_t gl;      // entries >= gl were not copied (end of the array): read from global
-  int32_t f1;      // min(v1, gl) rounded down to 4: whole quads [round4(v0), f1) valid and staged
   int32_t pad;
   int64_t a0;      // global index of slot dst (16-byte aligned)
 };
 struct StreamBuf {
-  int32_t nseg, pad[3];
+  int32_t nseg, fill, pad[2];
   StreamChunk seg[kStreamSegs];
 };
 
@@ -267,125 +269,144 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs 
   __syncthreads();
 
   CSR_MARK(1);
-  const int64_t n_active = *a.count;
   const int nt = a.n_tiles;
   const int64_t nnz4 = __ldg(a.nnz) & ~int64_t{3};
-  // this warp's rows: k = w, w + NW, ... (w = global warp index within the tile)
-  const int64_t NW = static_cast<int64_t>(a.groups) * kStreamWarps;
-  const int64_t w = static_cast<int64_t>(group) * kStreamWarps + warp;
-  // lane j holds the tile range of the warp's row 32 b + j; next batch prefetched
-  auto load_range = [&](int64_t kb, int64_t &lo_r, int64_t &hi_r) {
-    const int64_t k = w + (kb + lane) * NW;
-    lo_r = 0;
-    hi_r = 0;
-    if (k < n_active) {
-      const int64_t r = __ldg(a.active + k);
-      const int64_t p0 = __ldg(a.indptr + r), p1 = __ldg(a.indptr + r + 1);
-      const int32_t *sp = a.split + r * (nt - 1) - 1;      // sp[t], t = 1 .. nt-1
-      lo_r = tile > 0 ? p0 + __ldg(sp + tile) : p0;
-      hi_r = tile < nt - 1 ? p0 + __ldg(sp + tile + 1) : p1;
-      lo_r = min(max(lo_r, p0), p1);          // a stale plan cannot leave the row
-      hi_r = min(max(hi_r, lo_r), p1);
-    }
-  };
-  const int64_t my_rows = n_active > w ? (n_active - w + NW - 1) / NW : 0;
-  int64_t blo, bhi, nlo, nhi;             // current / next batch (per lane)
-  load_range(0, blo, bhi);
-  load_range(32, nlo, nhi);
-  // issue cursor (warp-uniform): row index ir, position pos in [pos, hi)
-  int64_t ir = 0, pos = 0, hi = 0;
-  auto row_at = [&](int64_t r) {          // broadcast row r's range (r in current batch)
-    const int j = static_cast<int>(r & 31);
-    pos = __shfl_sync(0xffffffffu, blo, j);
-    hi = __shfl_sync(0xffffffffu, bhi, j);
-  };
-  if (my_rows > 0) row_at(0);
-  // fill buffer b with the next row pieces (up to kStreamSegs, BE slots);
-  // false when the rows are exhausted
-  auto issue = [&](int b) -> bool {
-    int fill = 0, nseg = 0;
-    while (nseg < kStreamSegs && fill <= BE - 4) {
-      while (ir < my_rows && pos >= hi) { // advance to the next non-empty row
-        ++ir;
+  int64_t issued_total = 0, used_total = 0;
+  // Stream the rows list[w], list[w + NW], ... (n_active entries) of this
+  // warp through its ring into the tile.
+  auto stream_rows = [&](const int32_t *list, bool list_smem, int64_t n_active, int64_t w,
+                         int64_t NW) {
+    // lane j holds the tile range of the warp's row 32 b + j; next batch prefetched
+    auto load_range = [&](int64_t kb, int64_t &lo_r, int64_t &hi_r) {
+      const int64_t k = w + (kb + lane) * NW;
+      lo_r = 0;
+      hi_r = 0;
+      if (k < n_active) {
+        const int64_t r = list_smem ? list[k] : __ldg(list + k);
+        const int64_t p0 = __ldg(a.indptr + r), p1 = __ldg(a.indptr + r + 1);
+        const int32_t *sp = a.split + r * (nt - 1) - 1;      // sp[t], t = 1 .. nt-1
+        lo_r = tile > 0 ? p0 + __ldg(sp + tile) : p0;
+        hi_r = tile < nt - 1 ? p0 + __ldg(sp + tile + 1) : p1;
+        lo_r = min(max(lo_r, p0), p1);          // a stale plan cannot leave the row
+        hi_r = min(max(hi_r, lo_r), p1);
+      }
+    };
+    const int64_t my_rows = n_active > w ? (n_active - w + NW - 1) / NW : 0;
+    int64_t blo, bhi, nlo, nhi;             // current / next batch (per lane)
+    load_range(0, blo, bhi);
+    load_range(32, nlo, nhi);
+    // issue cursor (warp-uniform): row index ir, position pos in [pos, hi)
+    int64_t ir = 0, pos = 0, hi = 0;
+    auto row_at = [&](int64_t r) {          // broadcast row r's range (r in current batch)
+      const int j = static_cast<int>(r & 31);
+      pos = __shfl_sync(0xffffffffu, blo, j);
+      hi = __shfl_sync(0xffffffffu, bhi, j);
+    };
+    if (my_rows > 0) row_at(0);
+    // fill buffer b with the next row pieces (up to kStreamSegs, BE slots);
+    // false when the rows are exhausted
+    auto issue = [&](int b) -> bool {
+      int fill = 0, nseg = 0;
+      // the buffer's sentinel slots were written through the generic proxy:
+      // order them before the bulk copies (async proxy) overwrite the buffer
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      while (nseg < kStreamSegs && fill <= BE - 4) {
+        while (ir < my_rows && pos >= hi) { // advance to the next non-empty row
+          ++ir;
+          if (ir >= my_rows) break;
+          if ((ir & 31) == 0) {
+            blo = nlo;
+            bhi = nhi;
+            load_range(ir + 32, nlo, nhi);
+          }
+          row_at(ir);
+        }
         if (ir >= my_rows) break;
-        if ((ir & 31) == 0) {
-          blo = nlo;
-          bhi = nhi;
-          load_range(ir + 32, nlo, nhi);
+        const int64_t a0 = pos & ~int64_t{3};
+        const int64_t a1 = min((hi + 3) & ~int64_t{3}, a0 + (BE - fill));
+        const int64_t piece_hi = min(hi, a1);
+        const int64_t ac = min(a1, max(nnz4, a0));         // copyable end
+        const uint32_t bytes = static_cast<uint32_t>(ac - a0) * 4u;
+        if (lane == 0) {
+          StreamChunk &m = meta[b].seg[nseg];
+          m.dst = fill;
+          m.len = static_cast<int32_t>(a1 - a0);
+          m.v0 = static_cast<int32_t>(pos - a0);
+          m.v1 = static_cast<int32_t>(piece_hi - a0);
+          m.gl = static_cast<int32_t>(ac - a0);
+          m.a0 = a0;
+          if (bytes) {
+            mbar_expect_tx(bar + b, HOMO ? bytes : 2u * bytes);
+            bulk_g2s(bidx + b * BE + fill, a.indices + a0, bytes, bar + b);
+            if (!HOMO) bulk_g2s(bdat + b * BE + fill, a.data + a0, bytes, bar + b);
+          }
         }
-        row_at(ir);
+        fill += static_cast<int>(a1 - a0);
+        ++nseg;
+        pos = piece_hi;
       }
-      if (ir >= my_rows) break;
-      const int64_t a0 = pos & ~int64_t{3};
-      const int64_t a1 = min((hi + 3) & ~int64_t{3}, a0 + (BE - fill));
-      const int64_t piece_hi = min(hi, a1);
-      const int64_t ac = min(a1, max(nnz4, a0));         // copyable end
-      const uint32_t bytes = static_cast<uint32_t>(ac - a0) * 4u;
+      if (nseg == 0) return false;
       if (lane == 0) {
-        StreamChunk &m = meta[b].seg[nseg];
-        m.dst = fill;
-        m.v0 = static_cast<int32_t>(pos - a0);
-        m.v1 = static_cast<int32_t>(piece_hi - a0);
-        m.gl = static_cast<int32_t>(ac - a0);
-        m.f1 = min(m.v1, m.gl) & ~3;
-        m.a0 = a0;
-        if (bytes) {
-          mbar_expect_tx(bar + b, HOMO ? bytes : 2u * bytes);
-          bulk_g2s(bidx + b * BE + fill, a.indices + a0, bytes, bar + b);
-          if (!HOMO) bulk_g2s(bdat + b * BE + fill, a.data + a0, bytes, bar + b);
+        meta[b].nseg = nseg;
+        meta[b].fill = fill;
+        mbar_arrive(bar + b);
+      }
+      return true;
+    };
+
+    // lc = col - c0 clamped to the sink slot `width` (entries of an unsorted
+    // row that fall outside the tile land there and are never flushed):
+    // branch-free, one clamp per entry
+    auto add = [&](int32_t col, float wgt) {
+      const uint32_t lc = min(static_cast<uint32_t>(col - c0i), static_cast<uint32_t>(width));
+      if (HOMO) atomicAdd(reinterpret_cast<uint32_t *>(sm) + lc, 1u);
+      else if (KIND == 0) atomicAdd(reinterpret_cast<float *>(sm) + lc, wgt);
+      else {
+        // int64 add as two native 32-bit ATOMS (a 64-bit shared add is a CAS
+        // loop on sm_100a): low word with return, carry into the high word --
+        // exact modulo 2^64, like an int64 add
+        unsigned *p = reinterpret_cast<unsigned *>(sm) + 2 * lc;
+        const unsigned long long qq = static_cast<unsigned long long>(quantize(wgt));
+        const unsigned lo = static_cast<unsigned>(qq);
+        const unsigned old = atomicAdd(p, lo);
+        atomicAdd(p + 1, static_cast<unsigned>(qq >> 32) + (old + lo < old ? 1u : 0u));
+      }
+    };
+    auto add4 = [&](const int4 &ci, const float4 &wi) {
+      add(ci.x, wi.x);
+      add(ci.y, wi.y);
+      add(ci.z, wi.z);
+      add(ci.w, wi.w);
+    };
+
+    // buffer of the i-th chunk: i % NB, its mbarrier phase (i / NB) & 1;
+    // the counts run on across calls of this lambda
+    const int64_t used0 = used_total;
+    for (int j = 0; j < NB; ++j)
+      if (issue(static_cast<int>(issued_total % NB))) ++issued_total;
+    for (int64_t used = used0; used < issued_total; ++used) {
+      const int b = static_cast<int>(used % NB);
+      mbar_wait(bar + b, static_cast<uint32_t>((used / NB) & 1));
+      // lane i sanitises piece i: slots outside [v0, v1) (16-byte alignment
+      // padding, <= 3 each side) get a column that clamps into the sink slot,
+      // entries past the last copied 16 bytes of the array (<= 3) are loaded
+      int32_t *si = bidx + b * BE;
+      float *sd = bdat + b * BE;
+      if (lane < meta[b].nseg) {
+        const StreamChunk m = meta[b].seg[lane];
+        int32_t *pi = si + m.dst;
+        for (int o = 0; o < m.v0; ++o) pi[o] = INT32_MIN;
+        for (int o = m.v1; o < m.len; ++o) pi[o] = INT32_MIN;
+        for (int o = m.gl; o < m.v1; ++o) {
+          pi[o] = __ldg(a.indices + m.a0 + o);
+          if (!HOMO) sd[m.dst + o] = __ldg(a.data + m.a0 + o);
         }
       }
-      fill += static_cast<int>(a1 - a0);
-      ++nseg;
-      pos = piece_hi;
-    }
-    if (nseg == 0) return false;
-    if (lane == 0) {
-      meta[b].nseg = nseg;
-      mbar_arrive(bar + b);
-    }
-    return true;
-  };
-
-  // lc = col - c0 clamped to the sink slot `width` (entries of an unsorted
-  // row that fall outside the tile land there and are never flushed):
-  // branch-free, one clamp per entry
-  auto add = [&](int32_t col, float wgt) {
-    const uint32_t lc = min(static_cast<uint32_t>(col - c0i), static_cast<uint32_t>(width));
-    if (HOMO) atomicAdd(reinterpret_cast<uint32_t *>(sm) + lc, 1u);
-    else if (KIND == 0) atomicAdd(reinterpret_cast<float *>(sm) + lc, wgt);
-    else {
-      // int64 add as two native 32-bit ATOMS (a 64-bit shared add is a CAS
-      // loop on sm_100a): low word with return, carry into the high word --
-      // exact modulo 2^64, like an int64 add
-      unsigned *p = reinterpret_cast<unsigned *>(sm) + 2 * lc;
-      const unsigned long long qq = static_cast<unsigned long long>(quantize(wgt));
-      const unsigned lo = static_cast<unsigned>(qq);
-      const unsigned old = atomicAdd(p, lo);
-      atomicAdd(p + 1, static_cast<unsigned>(qq >> 32) + (old + lo < old ? 1u : 0u));
-    }
-  };
-  auto add4 = [&](const int4 &ci, const float4 &wi) {
-    add(ci.x, wi.x);
-    add(ci.y, wi.y);
-    add(ci.z, wi.z);
-    add(ci.w, wi.w);
-  };
-
-  int64_t issued = 0;
-  for (int b = 0; b < NB; ++b) issued += issue(b) ? 1 : 0;
-  for (int64_t used = 0; used < issued; ++used) {
-    const int b = static_cast<int>(used % NB);
-    mbar_wait(bar + b, static_cast<uint32_t>((used / NB) & 1));
-    const int nseg = meta[b].nseg;
-    for (int sgi = 0; sgi < nseg; ++sgi) {
-      const StreamChunk m = meta[b].seg[sgi];
-      const int32_t *si = bidx + b * BE + m.dst;
-      const float *sd = bdat + b * BE + m.dst;
-      // body: whole quads [qa, qb), two per lane per iteration, no checks
-      const int qa = (m.v0 + 3) & ~3, qb = m.f1;
-      for (int q = qa + 4 * lane; q < qb; q += 256) {
-        const bool two = q + 128 < qb;
+      __syncwarp();
+      // every slot of the buffer: two quads per lane per iteration, no checks
+      const int fill = meta[b].fill;
+      for (int q = 4 * lane; q < fill; q += 256) {
+        const bool two = q + 128 < fill;
         const int4 c1 = *reinterpret_cast<const int4 *>(si + q);
         const int4 c2 = two ? *reinterpret_cast<const int4 *>(si + q + 128) : c1;
         float4 w1 = make_float4(0.f, 0.f, 0.f, 0.f), w2 = w1;
@@ -396,26 +417,17 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs 
         add4(c1, w1);
         if (two) add4(c2, w2);
       }
-      // edges: head [v0, min(qa, v1)) on lanes 0-3, tail [max(qa, qb), v1)
-      // on lanes 4-11 (<= 3 rounding entries + <= 3 not copied at the end)
-      const int o = lane < 4 ? m.v0 + lane : max(qa, qb) + lane - 4;
-      const int end = lane < 4 ? min(qa, m.v1) : m.v1;
-      if (lane < 12 && o < end) {
-        int32_t col;
-        float wgt = 0.f;
-        if (o < m.gl) {
-          col = si[o];
-          if (!HOMO) wgt = sd[o];
-        } else {                                  // tail past the last 16-byte boundary
-          col = __ldg(a.indices + m.a0 + o);
-          if (!HOMO) wgt = __ldg(a.data + m.a0 + o);
-        }
-        add(col, wgt);
-      }
+      __syncwarp();                                 // buffer b consumed by every lane
+      if (issue(b)) ++issued_total;
     }
-    __syncwarp();                                 // buffer b consumed by every lane
-    issued += issue(b) ? 1 : 0;
-  }
+    used_total = issued_total;
+  };
+
+  // rows from the active list: warp w of the tile takes k = w, w + NW, ... --
+  // dealt evenly over the tile's CTAs (a per-CTA compaction of its slice of
+  // the spike words avoids the compaction launch but leaves ~12 % imbalance)
+  stream_rows(a.active, false, *a.count, static_cast<int64_t>(group) * kStreamWarps + warp,
+              static_cast<int64_t>(a.groups) * kStreamWarps);
   CSR_MARK(2);
   __syncthreads();
   CSR_MARK(3);

@@ -43,14 +43,14 @@ __device__ __forceinline__ void count_events(unsigned long long *counter,
 }
 
 // ---------------------------------------------------------------- a1
-__global__ void __launch_bounds__(256)
-k_compact(const uint32_t *__restrict__ spikes, int64_t n,
-          int32_t *__restrict__ active, int32_t *__restrict__ count,
-          int32_t id_base) {
+// Warps warp0, warp0 + n_warps, ... each take 32 spike words: warp scan of
+// the popcounts, one atomicAdd per warp claims a slice of the active list.
+__device__ __forceinline__ void compact_words(const uint32_t *__restrict__ spikes, int64_t n,
+                                              int32_t *__restrict__ active,
+                                              int32_t *__restrict__ count, int32_t id_base,
+                                              int64_t warp0, int64_t n_warps) {
   const int lane = threadIdx.x & 31;
   const int64_t n_words = (n + 31) >> 5;
-  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
   for (int64_t base = warp0 * 32; base < n_words; base += n_warps * 32) {
     const int64_t wi = base + lane;
     uint32_t word = 0;
@@ -77,6 +77,15 @@ k_compact(const uint32_t *__restrict__ spikes, int64_t n,
       word &= word - 1u;
     }
   }
+}
+
+__global__ void __launch_bounds__(256)
+k_compact(const uint32_t *__restrict__ spikes, int64_t n,
+          int32_t *__restrict__ active, int32_t *__restrict__ count,
+          int32_t id_base) {
+  compact_words(spikes, n, active, count, id_base,
+                (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5,
+                (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5);
 }
 
 // ---------------------------------------------------------------- a2

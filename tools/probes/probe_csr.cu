@@ -1,6 +1,7 @@
 // Phase timing of the streamed CSR scatter (k_csr_split + k_csr_stream) on a
 // synthetic 100k x 100k matrix with rows of exactly p*n sorted columns.
-// usage: probe_csr <p> <density> <homo 0|1> <fused 0|1>
+// usage: probe_csr <p> <density> <homo 0|1> <fused 0|1>  (fused: cooperative, in-kernel
+// compaction and reduction; else separate compaction, partials only)
 #define BP_CSR_TIMING 1
 #include <cstdio>
 #include <cstdlib>
@@ -55,27 +56,34 @@ int main(int argc, char **argv) {
   k_compact<<<(n / 32 + 255) / 256, 256>>>(sp, n, act, cnt);
   int na; cudaMemcpy(&na, cnt, 4, cudaMemcpyDeviceToHost);
   const int acc = 4;
-  const size_t fixed = bp::stream_smem(0, acc, homo).total + 256;
+  const size_t fixed = bp::stream_smem(0, acc, homo).total + bp::kStreamStaticSmem + 256;
   const int64_t max_cols = ((232448 - fixed) / acc) & ~3LL;
   const int nt = (int)((n + max_cols - 1) / max_cols);
   const int tile_cols = (int)(((n + nt - 1) / nt + 3) & ~3LL);
   const int G = 148 / nt;
-  cudaMalloc(&bounds, (size_t)n * (nt + 1) * 8);
+  int32_t *split;
+  cudaMalloc(&split, (size_t)n * (nt + 1) * 4);
   void *partials, *out;
   cudaMalloc(&partials, (size_t)nt * G * tile_cols * 4);
   cudaMalloc(&out, n * 4);
-  bp::CsrSplitArgs sa{indptr, idx, act, cnt, bounds, nt, tile_cols, n};
-  bp::CsrStreamArgs ca{idx, dat, bounds, cnt, indptr + n, partials, tile_cols, G, nt, 0, n,
-                       fused ? out : nullptr, 0.6f, 0};
+  bp::CsrSplitArgs sa{indptr, idx, nullptr, nullptr, n, split, nt, tile_cols, n};   // plan
+  bp::k_csr_split<<<148 * 16, 256>>>(sa);
+  bp::CsrStreamArgs ca{idx, dat, indptr, split, act, cnt, indptr + n, partials, tile_cols, G, nt,
+                       0, n, fused ? out : nullptr, 0.6f, 0};
   const size_t smem = bp::stream_smem(tile_cols, acc, homo).total;
   auto kern = homo ? bp::k_csr_stream<0, true> : bp::k_csr_stream<0, false>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(232448 - bp::kStreamStaticSmem));
   cudaEvent_t e0, e1, e2; cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2);
+  if (getenv("CARVEOUT")) {   // keep the SM's shared-memory carveout at max across kernels
+    cudaFuncSetAttribute(k_compact, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  }
   printf("p=%g d=%g homo=%d fused=%d active=%d tiles=%d groups=%d tile_cols=%d smem=%zu\n",
          p, d, homo, fused, na, nt, G, tile_cols, smem);
   for (int rep = 0; rep < 5; ++rep) {
     cudaEventRecord(e0);
-    bp::k_csr_split<<<(n + 7) / 8 < 148 * 8 ? (n + 7) / 8 : 148 * 8, 256>>>(sa);
+    cudaMemsetAsync(cnt, 0, 4);
+    k_compact<<<(n / 32 + 255) / 256, 256>>>(sp, n, act, cnt);
     cudaEventRecord(e1);
     void *args[] = {&ca};
     if (fused) cudaLaunchCooperativeKernel((const void *)kern, dim3(nt * G), dim3(1024), args, smem, 0);
@@ -88,10 +96,10 @@ int main(int argc, char **argv) {
     cudaMemcpyFromSymbol(T, bp::g_csr_t, sizeof(T));
     unsigned long long t0 = ~0ull;
     for (int b = 0; b < nt * G; ++b) t0 = std::min(t0, T[b][0]);
-    double ph[7] = {0}, mx[7] = {0};
+    double ph[8] = {0}, mx[8] = {0};
     for (int b = 0; b < nt * G; ++b)
-      for (int k = 0; k < 7; ++k) { double v = (T[b][k] - t0) / 1e3; ph[k] += v / (nt * G); mx[k] = std::max(mx[k], v); }
-    printf("split %.1f us  stream %.1f us | mean/max since first CTA start (us):", t1 * 1e3, t2 * 1e3);
+      for (int k = 0; k < 8; ++k) { double v = (T[b][k] - t0) / 1e3; ph[k] += v / (nt * G); mx[k] = std::max(mx[k], v); }
+    printf("compact %.1f us  stream %.1f us | mean/max since first CTA start (us):", t1 * 1e3, t2 * 1e3);
     const char *nm[7] = {"start", "init", "w0loop", "allloop", "flush", "gsync", "end"};
     for (int k = 0; k < (fused ? 7 : 5); ++k) printf(" %s %.1f/%.1f", nm[k], ph[k], mx[k]);
     printf("\n");
