@@ -1,5 +1,5 @@
 # config 2 microbenchmark cells (100k x 100k)
-for w in csrmv jitmv; do for law in homo uniform normal; do for p in 0.001 0.01 0.05; do for d in 0.001 0.01 0.1; do
+for w in ${WORKLOADS:-csrmv jitmv}; do for law in homo uniform normal; do for p in 0.001 0.01 0.05; do for d in 0.001 0.01 0.1; do
   if [ $w = csrmv ] && [ $law = normal ]; then continue; fi
   python bench.py --workload $w --law $law --p $p --density $d --steps ${STEPS:-100} --warmup 10 > gpurun_out/m.log 2>&1 || { tail -3 gpurun_out/m.log; continue; }
   python - $w $law $p $d <<'PY'
