@@ -16,7 +16,6 @@
 #include "scatter.cuh"
 #include "csr_stream.cuh"
 #include "step.cuh"
-#include "persist.cuh"
 
 namespace {
 
@@ -789,11 +788,6 @@ struct bp_network {
   int32_t *small_steps = nullptr;    // per-step spike counts scratch
   int64_t small_steps_cap = 0;
   int64_t prof_steps = 0;
-  // one device, LIF: the whole time loop in one cooperative kernel
-  // (persist.cuh) -- ready-tile queue and control words
-  bool persist = false;
-  unsigned long long *pqueue = nullptr;
-  uint32_t *pctl = nullptr;
 };
 
 namespace {
@@ -1203,28 +1197,6 @@ bp_status bp_network_create(const bp_network_desc *desc, bp_stream stream,
     launch_compact(desc->spikes, desc->n, net->small_active, net->small_count, sms, st);
     s = launched();
   }
-  // opt-in (BP_PERSIST): one device, whole network, LIF, larger than one CTA:
-  // the persistent cooperative kernel (update and binning overlapped,
-  // persist.cuh).  Measured slower than the two kernels per step: the
-  // update needs every warp of the SM for memory parallelism.
-  if (s == BP_OK && !net->small && desc->col_begin == 0 && desc->col_end == desc->n &&
-      desc->model == BP_MODEL_LIF && net->n_tiles <= static_cast<uint32_t>(bp::kPerMaxTiles) &&
-      std::getenv("BP_PERSIST")) {
-    int coop = 0, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
-    if (coop && bp::persist_smem(net->n_tiles) + 1024 <= kSmemOptin) {
-      const size_t qb = 2 * static_cast<size_t>(net->n_tiles) * sizeof(unsigned long long);
-      const size_t cb = bp::kCtlWords * bp::kCtlStride * sizeof(uint32_t);
-      if (cudaMalloc(&net->pqueue, qb) == cudaSuccess &&
-          cudaMalloc(&net->pctl, cb) == cudaSuccess &&
-          cudaMemsetAsync(net->pqueue, 0, qb, st) == cudaSuccess &&
-          cudaMemsetAsync(net->pctl, 0, cb, st) == cudaSuccess)
-        net->persist = true;
-      else
-        cudaGetLastError();
-    }
-  }
   if (s != BP_OK) {
     bp_network_destroy(net);
     return s;
@@ -1233,65 +1205,7 @@ bp_status bp_network_create(const bp_network_desc *desc, bp_stream stream,
   return BP_OK;
 }
 
-}  // extern "C"
 
-namespace {
-
-template <int KIND>
-bool launch_persist(bp::PersistArgs a, uint32_t n_tiles, int sms, cudaStream_t st) {
-  const size_t smem = bp::persist_smem(n_tiles);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(bp::k_net_persist<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem > 48 * 1024 ? kSmemOptin - 1024 : smem));
-    attr = true;
-  }
-  void *args[] = {&a};
-  if (cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(bp::k_net_persist<KIND>),
-                                  dim3(sms), dim3(bp::kPerThreads), args, smem, st) == cudaSuccess)
-    return true;
-  cudaGetLastError();
-  return false;
-}
-
-// n_steps of the whole network in one launch; false if the cooperative
-// launch is refused (the caller falls back to two kernels per step).
-bool persist_steps(bp_network *net, int64_t n_steps, uint32_t *raster, int32_t *counts_out,
-                   cudaStream_t st) {
-  const bp_network_desc &d = net->d;
-  bp::PersistArgs a{};
-  for (int b = 0; b < 2; ++b) {
-    // steps reading buckets b: step0 + k with (bpar0 ^ k) & 1 == b
-    const int par = (b ^ net->bpar ^ static_cast<int>(net->steps_done & 1)) & 1;
-    bp::StepArgs &sa = a.st[b];
-    sa = step_args(net);
-    sa.in = net->bk[b];
-    sa.out = bin_target(net, b ^ 1);
-    sa.reverse = par;
-    sa.step_spikes = reinterpret_cast<int32_t *>(net->pctl + (bp::kCtlSpk + par) * bp::kCtlStride);
-  }
-  a.bpar0 = net->bpar;
-  a.step0 = static_cast<uint32_t>(net->steps_done);
-  a.n_steps = n_steps;
-  a.raster = raster;
-  a.spikes = net->neuron.spikes;
-  a.n_words = net->local_words;
-  a.counts_out = counts_out;
-  a.queue = net->pqueue;
-  a.ctl = net->pctl;
-  bool ok;
-  if (d.g_kind == BP_OUT_FIX64) ok = launch_persist<1>(a, net->n_tiles, net->sms, st);
-  else if (d.g_kind == BP_OUT_FIX32) ok = launch_persist<2>(a, net->n_tiles, net->sms, st);
-  else ok = launch_persist<0>(a, net->n_tiles, net->sms, st);
-  if (!ok) return false;
-  if (n_steps & 1) net->bpar ^= 1;
-  net->steps_done += n_steps;
-  return true;
-}
-
-}  // namespace
-
-extern "C" {
 
 bp_status bp_network_step(bp_network *net, int64_t n_steps, uint32_t *raster_out,
                           int32_t *counts_out, bp_stream stream) {
@@ -1300,26 +1214,6 @@ bp_status bp_network_step(bp_network *net, int64_t n_steps, uint32_t *raster_out
   BP_CHECK(net != nullptr && n_steps >= 0, BP_ERR_INVALID_ARG, "bad net/n_steps");
   cudaStream_t st = as_stream(stream);
   if (net->small && n_steps > 0) return small_step(net, n_steps, raster_out, counts_out, st);
-  if (net->persist && n_steps > 0) {
-    cudaEvent_t *ev = nullptr;
-    if (net->prof_ev && net->prof_used < net->prof_cap) {
-      ev = net->prof_ev + 3 * net->prof_used++;
-      net->prof_steps += n_steps;
-    }
-    if (ev) BP_CUDA(cudaEventRecord(ev[0], st));
-    if (persist_steps(net, n_steps, raster_out, counts_out, st)) {
-      if (ev) {                            // one fused kernel: all "update", no separate binning
-        BP_CUDA(cudaEventRecord(ev[1], st));
-        BP_CUDA(cudaEventRecord(ev[2], st));
-      }
-      return launched();
-    }
-    net->persist = false;                  // refused: two kernels per step from now on
-    if (ev) {
-      net->prof_used -= 1;
-      net->prof_steps -= n_steps;
-    }
-  }
   for (int64_t k = 0; k < n_steps; ++k) {
     cudaEvent_t *ev = nullptr;
     if (net->prof_ev && net->prof_used < net->prof_cap) {
@@ -1408,19 +1302,12 @@ bp_status bp_network_counters(bp_network *net, uint64_t *host_out, bp_stream str
   cudaStream_t st = as_stream(stream);
   BP_CUDA(cudaMemcpyAsync(host_out, net->counters, 3 * sizeof(uint64_t),
                           cudaMemcpyDeviceToHost, st));
-  uint32_t err = 0;
-  if (net->pctl)
-    BP_CUDA(cudaMemcpyAsync(&err, net->pctl + bp::kCtlErr * bp::kCtlStride, sizeof(uint32_t),
-                            cudaMemcpyDeviceToHost, st));
   BP_CUDA(cudaStreamSynchronize(st));
-  BP_CHECK(err == 0, BP_ERR_CUDA, "persistent network kernel: ready-tile queue timed out");
   return BP_OK;
 }
 
 void bp_network_destroy(bp_network *net) {
   if (net && net->bk_mem) cudaFree(net->bk_mem);
-  if (net && net->pqueue) cudaFree(net->pqueue);
-  if (net && net->pctl) cudaFree(net->pctl);
   if (net && net->small_steps) cudaFree(net->small_steps);
   if (net && net->prof_ev) {
     for (int64_t i = 0; i < 3 * net->prof_cap; ++i) cudaEventDestroy(net->prof_ev[i]);
@@ -1430,12 +1317,3 @@ void bp_network_destroy(bp_network *net) {
 }
 
 }  // extern "C"
-
-#ifdef BP_PERSIST_TIMING
-// debug builds only (tools/probes/probe_persist.py): the persistent kernel's
-// per-block, per-step phase marks
-extern "C" int bp_debug_persist_timing(unsigned long long *host, size_t n) {
-  return static_cast<int>(cudaMemcpyFromSymbol(host, bp::g_per_t,
-                                               n * sizeof(unsigned long long)));
-}
-#endif

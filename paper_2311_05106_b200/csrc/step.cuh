@@ -197,7 +197,7 @@ struct GVec<0> {
   __device__ __forceinline__ void load(const void *g, int64_t i, uint64_t pol) {
     const float *p = static_cast<const float *>(g) + i;
     float4 x;
-    asm volatile("ld.global.cg.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+    asm volatile("ld.global.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
                  : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "l"(p), "l"(pol));
     v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
   }
@@ -212,9 +212,9 @@ struct GVec<1> {
   long long v[4];
   __device__ __forceinline__ void load(const void *g, int64_t i, uint64_t pol) {
     const long long *p = static_cast<const long long *>(g) + i;
-    asm volatile("ld.global.cg.L2::cache_hint.v2.s64 {%0,%1}, [%2], %3;"
+    asm volatile("ld.global.L2::cache_hint.v2.s64 {%0,%1}, [%2], %3;"
                  : "=l"(v[0]), "=l"(v[1]) : "l"(p), "l"(pol));
-    asm volatile("ld.global.cg.L2::cache_hint.v2.s64 {%0,%1}, [%2], %3;"
+    asm volatile("ld.global.L2::cache_hint.v2.s64 {%0,%1}, [%2], %3;"
                  : "=l"(v[2]), "=l"(v[3]) : "l"(p + 2), "l"(pol));
   }
   __device__ __forceinline__ void store(void *g, int64_t i, uint64_t pol) const {
@@ -231,7 +231,7 @@ struct GVec<2> {
   int32_t v[4];
   __device__ __forceinline__ void load(const void *g, int64_t i, uint64_t pol) {
     const int32_t *p = static_cast<const int32_t *>(g) + i;
-    asm volatile("ld.global.cg.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+    asm volatile("ld.global.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "l"(p), "l"(pol));
   }
   __device__ __forceinline__ void store(void *g, int64_t i, uint64_t pol) const {
@@ -319,7 +319,7 @@ __device__ __forceinline__ bool hh_one(const NeuronArgs &a, float &V, float &M, 
 
 __device__ __forceinline__ float4 ld4(const float *p, uint64_t pol) {
   float4 x;
-  asm volatile("ld.global.cg.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+  asm volatile("ld.global.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
                : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "l"(p), "l"(pol));
   return x;
 }
@@ -348,7 +348,7 @@ __device__ __forceinline__ void pass_load(Pass<MODEL, KIND> &p, const NeuronArgs
   p.gi.load(nr.g_i, i0, pol.keep);
   p.V = ld4(nr.v + i0, pol.stream);
   if constexpr (MODEL == 0) {
-    asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;"
+    asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;"
                  : "=r"(p.R) : "l"(nr.ref + i0), "l"(pol.stream));
   } else {
     p.M = ld4(nr.m + i0, pol.stream);
@@ -423,7 +423,7 @@ __device__ __forceinline__ uint32_t pass_update(Pass<MODEL, KIND> &p, const Step
     if constexpr (KIND == 2) {
       int32_t *pe = static_cast<int32_t *>(nr.g_e) + i;
       int32_t *pi = static_cast<int32_t *>(nr.g_i) + i;
-      int32_t ge = __ldcg(pe), gi = __ldcg(pi);
+      int32_t ge = *pe, gi = *pi;
       gEf = g_fold32(ge, cnt_e[j0 + q], a.q_e, nr.inv_scale32, sat);
       gIf = g_fold32(gi, cnt_i[j0 + q], a.q_i, nr.inv_scale32, sat);
       g_after32(ge, nr.a_e_q);
@@ -433,7 +433,7 @@ __device__ __forceinline__ uint32_t pass_update(Pass<MODEL, KIND> &p, const Step
     } else if constexpr (KIND == 1) {
       long long *pe = static_cast<long long *>(nr.g_e) + i;
       long long *pi = static_cast<long long *>(nr.g_i) + i;
-      long long ge = __ldcg(pe), gi = __ldcg(pi);
+      long long ge = *pe, gi = *pi;
       gEf = g_fold(ge, cnt_e[j0 + q], a.q_e);
       gIf = g_fold(gi, cnt_i[j0 + q], a.q_i);
       g_after(ge, nr.alpha_e, 0.f);
@@ -443,7 +443,7 @@ __device__ __forceinline__ uint32_t pass_update(Pass<MODEL, KIND> &p, const Step
     } else {
       float *pe = static_cast<float *>(nr.g_e) + i;
       float *pi = static_cast<float *>(nr.g_i) + i;
-      float ge = __ldcg(pe), gi = __ldcg(pi);
+      float ge = *pe, gi = *pi;
       gEf = g_fold(ge, cnt_e[j0 + q], a.w_e);
       gIf = g_fold(gi, cnt_i[j0 + q], a.w_i);
       g_after(ge, 0.0, nr.alpha_e32);
@@ -451,13 +451,13 @@ __device__ __forceinline__ uint32_t pass_update(Pass<MODEL, KIND> &p, const Step
       *pe = ge;
       *pi = gi;
     }
-    float V = __ldcg(nr.v + i);
+    float V = nr.v[i];
     if constexpr (MODEL == 0) {
-      uint32_t r = __ldcg(nr.ref + i);
+      uint32_t r = nr.ref[i];
       if (lif_one(nr, V, r, gEf, gIf)) nib |= 1u << q;
       nr.ref[i] = static_cast<uint8_t>(r);
     } else {
-      float M = __ldcg(nr.m + i), H = __ldcg(nr.h + i), Nk = __ldcg(nr.nk + i);
+      float M = nr.m[i], H = nr.h[i], Nk = nr.nk[i];
       if (hh_one(nr, V, M, H, Nk, gEf, gIf)) nib |= 1u << q;
       nr.m[i] = M;
       nr.h[i] = H;
@@ -471,23 +471,22 @@ __device__ __forceinline__ uint32_t pass_update(Pass<MODEL, KIND> &p, const Step
 // Spike words of one pass (lanes 8w..8w+7 hold the 32 neurons of word w)
 // and the active-list append (one atomic per warp with spikes).
 __device__ __forceinline__ void pass_emit(const StepArgs &a, uint32_t nib, int64_t base,
-                                          int pass_off, uint32_t &my_sp, int gtid,
-                                          uint32_t *spk_words, uint32_t *raster_words) {
+                                          int pass_off, uint32_t &my_sp) {
   const NeuronArgs &nr = a.nrn;
-  const uint32_t lane = threadIdx.x & 31u, warp = static_cast<uint32_t>(gtid) >> 5;
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   uint32_t word = nib << (4u * (lane & 7u));
   word |= __shfl_xor_sync(0xffffffffu, word, 1);
   word |= __shfl_xor_sync(0xffffffffu, word, 2);
   word |= __shfl_xor_sync(0xffffffffu, word, 4);
   const int64_t wi = (base + pass_off + warp * 128) / 32 + (lane >> 3);
   if ((lane & 7u) == 0 && wi * 32 < nr.n) {
-    spk_words[wi] = word;
-    if (raster_words) raster_words[wi] = word;
+    nr.spikes[wi] = word;
+    if (nr.raster) nr.raster[wi] = word;
   }
   const uint32_t c = __popc(nib);
   my_sp += c;
   const uint32_t warp_sp = __reduce_add_sync(0xffffffffu, c);
-  if (warp_sp && a.active) {
+  if (warp_sp) {
     uint32_t incl = c;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -497,7 +496,7 @@ __device__ __forceinline__ void pass_emit(const StepArgs &a, uint32_t nib, int64
     int slot = 0;
     if (lane == 0) slot = atomicAdd(a.active_count, static_cast<int>(warp_sp));
     slot = __shfl_sync(0xffffffffu, slot, 0) + static_cast<int>(incl - c);
-    const int64_t i0 = base + pass_off + 4 * static_cast<int64_t>(gtid);
+    const int64_t i0 = base + pass_off + 4 * static_cast<int64_t>(threadIdx.x);
     uint32_t bits = nib;
     while (bits) {
       const int q = __ffs(bits) - 1;
@@ -508,76 +507,6 @@ __device__ __forceinline__ void pass_emit(const StepArgs &a, uint32_t nib, int64
 }
 
 // ---------------------------------------------------------------- kernel
-// One tile of the step (NT threads, group-local index tid, `sync` a barrier
-// over those NT threads): count the tile's incoming event records, fold them
-// into g while streaming the state once, emit spike words (+ active list).
-template <int MODEL, int KIND, int NT, typename Sync>
-__device__ __forceinline__ void step_tile(const StepArgs &a, uint32_t tile, int tid,
-                                          int32_t *cnt_e, int32_t *cnt_i,
-                                          unsigned long long *block_sp, bool zero_count,
-                                          uint32_t *spk_words, uint32_t *raster_words,
-                                          Sync sync) {
-  constexpr int passes = kTile / (4 * NT);
-  constexpr int pstride = 4 * NT;   // neurons per pass
-  const uint32_t lane = threadIdx.x & 31u;
-  const int64_t base = static_cast<int64_t>(tile) << kTileShift;
-  const NeuronArgs &nr = a.nrn;
-  const Policies pol = make_policies(nr.keep_frac);
-  Pass<MODEL, KIND> pa, pb;
-  pass_load(pa, nr, base + 4 * tid, pol);
-  pass_load(pb, nr, base + pstride + 4 * tid, pol);
-
-  // 1. count this tile's incoming events (bucket + rare spill); L2-only
-  //    loads: the buckets are rewritten every other step
-  for (int j = tid; j < kTile; j += NT) { cnt_e[j] = 0; cnt_i[j] = 0; }
-  if (tid == 0) *block_sp = 0;
-  sync();
-  const int32_t n_in = min(static_cast<uint32_t>(__ldcg(a.in.cnt + tile * kCntStride)), a.out.cap);
-  const uint32_t *buf = a.in.buf + static_cast<size_t>(tile) * a.out.cap;
-  for (int k = tid; k < n_in; k += NT) {
-    const uint32_t e = __ldcg(buf + k);
-    atomicAdd((e & kProjBit) ? &cnt_i[e & (kTile - 1)] : &cnt_e[e & (kTile - 1)], 1);
-  }
-  if (__ldcg(a.in.flag + tile)) {              // overflow spill (exact, rare)
-    for (int j = tid; j < kTile && base + j < nr.n; j += NT) {
-      int32_t *se = a.in.spill + base + j;
-      int32_t *si = a.in.spill + a.out.n_local + base + j;
-      atomicAdd(&cnt_e[j], __ldcg(se));
-      atomicAdd(&cnt_i[j], __ldcg(si));
-      *se = 0;
-      *si = 0;
-    }
-  }
-  sync();
-  if (tid == 0) {
-    a.in.cnt[tile * kCntStride] = 0;
-    a.in.flag[tile] = 0;
-    if (zero_count && a.zero_count) *a.zero_count = 0;
-  }
-
-  // 2. update the tile: passes of 4*NT neurons, 4 consecutive per thread
-  uint32_t my_sp = 0, sat = 0;
-#pragma unroll
-  for (int p = 0; p < passes; ++p) {
-    Pass<MODEL, KIND> &cur = (p & 1) ? pb : pa;
-    const int off = p * pstride;
-    const uint32_t nib = pass_update(cur, a, cnt_e, cnt_i, off + 4 * tid, base + off + 4 * tid, pol,
-                                     sat);
-    if (p + 2 < passes) pass_load(cur, nr, base + off + 2 * pstride + 4 * tid, pol);
-    pass_emit(a, nib, base, off, my_sp, tid, spk_words, raster_words);
-  }
-
-  // 3. counters
-  if (KIND == 2 && sat) atomicAdd(a.saturated, static_cast<unsigned long long>(sat));
-  my_sp = __reduce_add_sync(0xffffffffu, my_sp);
-  if (lane == 0 && my_sp) atomicAdd(block_sp, static_cast<unsigned long long>(my_sp));
-  sync();
-  if (tid == 0 && *block_sp) {
-    atomicAdd(a.spikes, *block_sp);
-    if (a.step_spikes) atomicAdd(a.step_spikes, static_cast<int32_t>(*block_sp));
-  }
-}
-
 // The first two passes' state loads are issued before the bucket-counting
 // phase so their DRAM latency overlaps it; passes 2 and 3 are loaded while
 // 0 and 1 compute (register double buffering).
@@ -589,13 +518,70 @@ k_step(StepArgs a) {
   __shared__ int32_t cnt_e[kTile];
   __shared__ int32_t cnt_i[kTile];
   __shared__ unsigned long long block_sp;
+  const int tid = threadIdx.x;
   constexpr int nthreads = MODEL == 0 ? kStepThreads : 512;
+  constexpr int passes = kTile / (4 * nthreads);
+  constexpr int pstride = 4 * nthreads;   // neurons per pass
+  const uint32_t lane = tid & 31u;
   const uint32_t tile = a.reverse ? a.n_tiles - 1u - blockIdx.x : blockIdx.x;
+  const int64_t base = static_cast<int64_t>(tile) << kTileShift;
+  const NeuronArgs &nr = a.nrn;
+  const Policies pol = make_policies(nr.keep_frac);
+
   pdl_trigger();
   pdl_wait();               // state and buckets of the previous kernels are final
-  step_tile<MODEL, KIND, nthreads>(a, tile, threadIdx.x, cnt_e, cnt_i, &block_sp,
-                                   blockIdx.x == 0, a.nrn.spikes, a.nrn.raster,
-                                   [] { __syncthreads(); });
+  Pass<MODEL, KIND> pa, pb;
+  pass_load(pa, nr, base + 4 * tid, pol);
+  pass_load(pb, nr, base + pstride + 4 * tid, pol);
+
+  // 1. count this tile's incoming events (bucket + rare spill)
+  for (int j = tid; j < kTile; j += nthreads) { cnt_e[j] = 0; cnt_i[j] = 0; }
+  if (tid == 0) block_sp = 0;
+  __syncthreads();
+  const int32_t n_in = min(static_cast<uint32_t>(a.in.cnt[tile * kCntStride]), a.out.cap);
+  const uint32_t *buf = a.in.buf + static_cast<size_t>(tile) * a.out.cap;
+  for (int k = tid; k < n_in; k += nthreads) {
+    const uint32_t e = __ldcs(buf + k);
+    atomicAdd((e & kProjBit) ? &cnt_i[e & (kTile - 1)] : &cnt_e[e & (kTile - 1)], 1);
+  }
+  if (a.in.flag[tile]) {                       // overflow spill (exact, rare)
+    for (int j = tid; j < kTile && base + j < nr.n; j += nthreads) {
+      int32_t *se = a.in.spill + base + j;
+      int32_t *si = a.in.spill + a.out.n_local + base + j;
+      atomicAdd(&cnt_e[j], *se);
+      atomicAdd(&cnt_i[j], *si);
+      *se = 0;
+      *si = 0;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    a.in.cnt[tile * kCntStride] = 0;
+    a.in.flag[tile] = 0;
+    if (blockIdx.x == 0) *a.zero_count = 0;
+  }
+
+  // 2. update the tile: 4 passes of 1024 neurons, 4 consecutive per thread
+  uint32_t my_sp = 0, sat = 0;
+#pragma unroll
+  for (int p = 0; p < passes; ++p) {
+    Pass<MODEL, KIND> &cur = (p & 1) ? pb : pa;
+    const int off = p * pstride;
+    const uint32_t nib = pass_update(cur, a, cnt_e, cnt_i, off + 4 * tid, base + off + 4 * tid, pol,
+                                     sat);
+    if (p + 2 < passes) pass_load(cur, nr, base + off + 2 * pstride + 4 * tid, pol);
+    pass_emit(a, nib, base, off, my_sp);
+  }
+
+  // 3. counters
+  if (KIND == 2 && sat) atomicAdd(a.saturated, static_cast<unsigned long long>(sat));
+  my_sp = __reduce_add_sync(0xffffffffu, my_sp);
+  if (lane == 0 && my_sp) atomicAdd(&block_sp, static_cast<unsigned long long>(my_sp));
+  __syncthreads();
+  if (tid == 0 && block_sp) {
+    atomicAdd(a.spikes, block_sp);
+    if (a.step_spikes) atomicAdd(a.step_spikes, static_cast<int32_t>(block_sp));
+  }
 }
 
 // Remote (or initial) spikes: bin the events of every active row in
@@ -641,7 +627,6 @@ __device__ __forceinline__ uint32_t stage_record(uint32_t proj, uint32_t loc) {
 
 // Generate the local targets of row r into the block's staging area (or the
 // global per-event path when it is full).  Whole warp, warp-uniform r.
-template <int CAP = kBinStage>
 __device__ __forceinline__ uint32_t stage_row(const ConnArgs &c, const BinTarget &b, int64_t r,
                                               uint32_t *staged, int32_t *n_staged,
                                               int32_t *hist) {
@@ -670,7 +655,7 @@ __device__ __forceinline__ uint32_t stage_row(const ConnArgs &c, const BinTarget
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       if (!valid[k]) continue;
-      if (slot < CAP) {
+      if (slot < kBinStage) {
         staged[slot] = stage_record(proj, loc[k]);
         atomicAdd(hist + (loc[k] >> kTileShift), 1);
       } else {
@@ -740,15 +725,14 @@ __device__ __forceinline__ uint32_t stage_row(const ConnArgs &c, const BinTarget
 // Philox block of 4 gaps per lane per chunk of 128 gaps.  Positions grow
 // with (lane, k), so the valid events are a prefix of that order and their
 // staging slots follow from four ballots -- no second scan.
-template <int STRIDE = 32, int CAP = kBinStage>
 __device__ __forceinline__ uint32_t stage_rows_jit(const ConnArgs &c, const BinTarget &b,
                                                    const int32_t *active, int k0, int k_end,
                                                    uint32_t *staged, int32_t *n_staged,
                                                    int32_t *hist) {
   const uint32_t lane = threadIdx.x & 31u;
-  // rows k0, k0 + STRIDE, k0 + 2 STRIDE, ... (STRIDE = warps staging rows)
-  const int nrows = min(32, (k_end - k0 + STRIDE - 1) / STRIDE);
-  const int64_t r_l = lane < static_cast<uint32_t>(nrows) ? active[k0 + STRIDE * lane] : 0;
+  // rows k0, k0 + 32, k0 + 64, ... (stride = warps per block)
+  const int nrows = min(32, (k_end - k0 + 31) / 32);
+  const int64_t r_l = lane < static_cast<uint32_t>(nrows) ? active[k0 + 32 * lane] : 0;
   const bool inh_l = r_l >= c.split;
   const uint32_t row_l = static_cast<uint32_t>(inh_l ? r_l - c.split : r_l);
   const uint32_t n_seg_max = max(c.je.n_seg, c.ji.n_seg);
@@ -794,7 +778,7 @@ __device__ __forceinline__ uint32_t stage_rows_jit(const ConnArgs &c, const BinT
         if (lane == 0) base = atomicAdd(n_staged, static_cast<int>(n_valid));
         base = __shfl_sync(0xffffffffu, base, 0) + static_cast<int>(4 * lane);
         const uint32_t pbit = proj ? kProjBit : 0u;
-        if (base - static_cast<int>(4 * lane) + static_cast<int>(n_valid) <= CAP) {
+        if (base - static_cast<int>(4 * lane) + static_cast<int>(n_valid) <= kBinStage) {
           // common case, warp-uniform: predicated stores + histogram atomics
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
@@ -809,7 +793,7 @@ __device__ __forceinline__ uint32_t stage_rows_jit(const ConnArgs &c, const BinT
           for (int k = 0; k < 4; ++k) {
             if (!v[k]) continue;
             const uint32_t loc = pos[k] - b.col_begin;
-            if (base + k < CAP) {
+            if (base + k < kBinStage) {
               staged[base + k] = pbit | loc;
               atomicAdd(hist + (loc >> kTileShift), 1);
             } else {
@@ -830,7 +814,6 @@ __device__ __forceinline__ uint32_t stage_rows_jit(const ConnArgs &c, const BinT
 // per row.  The lane walks its row's gap chain itself, two Philox blocks
 // (8 gaps) per iteration; the blocks do not depend on the running position,
 // so their 10-round chains overlap (ILP) and no cross-lane scan is needed.
-template <int CAP = kBinStage>
 __device__ __forceinline__ uint32_t stage_row_lane(const ConnArgs &c, const BinTarget &b,
                                                    int64_t r, uint32_t *staged,
                                                    int32_t *n_staged, int32_t *hist) {
@@ -864,7 +847,7 @@ __device__ __forceinline__ uint32_t stage_row_lane(const ConnArgs &c, const BinT
       for (int k = 0; k < 8; ++k) {
         if (e[k] >= seg_end) break;
         const uint32_t loc = e[k] - b.col_begin;
-        if (slot < CAP) {
+        if (slot < kBinStage) {
           staged[slot] = stage_record(proj, loc);
           atomicAdd(hist + (loc >> kTileShift), 1);
         } else {
