@@ -605,7 +605,10 @@ k_bin_rows(ConnArgs conn, BinTarget out, const int32_t *active, const int32_t *c
 // atomics and sectors than one atomic + one 4-byte store per event.
 // Events that do not fit the shared staging area take the per-event path.
 constexpr int kBinThreads = 1024;
-constexpr int kBinStage = 12288;          // staged records per block
+#ifndef BP_BIN_STAGE
+#define BP_BIN_STAGE 16384
+#endif
+constexpr int kBinStage = BP_BIN_STAGE;   // staged records per block
 
 #ifdef BP_BIN_TIMING
 __device__ unsigned long long g_bin_t[1024][6];
