@@ -542,7 +542,7 @@ def run_micro(args):
     spikes = [torch.from_numpy(inputs.pack_bits(e).view(np.int32)).to(dev) for e in pats]
     out = torch.zeros(n, dtype=torch.int64 if fixed else torch.float32, device=dev)
     ws_bytes = (bp.lib().bp_csrmv_workspace_bytes(n, n, 1 if fixed else 0) if kind == "csrmv"
-                else bp.workspace_bytes(n))
+                else bp.lib().bp_jitconn_workspace_bytes(n, 0, n, 1 if fixed else 0))
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     seed = 0xBE7C4
     spec = bp.jitconn_spec(seed, p)

@@ -151,6 +151,15 @@ typedef struct {
   uint32_t seg_len;  /* L; 0 => n_cols (one segment per row)                */
 } bp_jitconn;
 
+/* Workspace for bp_jitconn_event_mv_* over output columns [col_begin,
+ * col_end): the active list plus, when the partition fits <= 16 shared-memory
+ * column tiles, the per-CTA partial tiles of the tiled path (k_jit_tiled:
+ * events accumulate in shared memory instead of one global atomic each).
+ * With only bp_workspace_bytes(n_rows) bytes the per-event path runs.  Host
+ * function (queries the current device). */
+size_t bp_jitconn_workspace_bytes(int64_t n_rows, int64_t col_begin, int64_t col_end,
+                                  int out_kind);
+
 /* a3+a4: out[c - col_begin] += sum over active rows r of w_e(r) for every
  * generated edge (r, c) with c in [col_begin, col_end).  col_begin must be a
  * multiple of seg_len and col_end a multiple of seg_len or equal to n_cols

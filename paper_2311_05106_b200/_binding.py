@@ -27,6 +27,7 @@ EXPORTED = [
     "bp_abi_version", "bp_status_string", "bp_last_error", "bp_conn_len",
     "bp_workspace_bytes", "bp_csrmv_workspace_bytes", "bp_compact_spikes", "bp_event_csrmv",
     "bp_csrmv_plan_bytes", "bp_csrmv_plan", "bp_event_csrmv_planned",
+    "bp_jitconn_workspace_bytes",
     "bp_jitconn_event_mv_homo", "bp_jitconn_event_mv_uniform",
     "bp_jitconn_event_mv_normal", "bp_jitconn_row_counts",
     "bp_jitconn_materialize", "bp_neuron_step", "bp_network_workspace_bytes",
@@ -103,6 +104,8 @@ def lib():
         L.bp_csrmv_workspace_bytes.restype = sz
         L.bp_compact_spikes.argtypes = [P, i64, P, P, P]
         L.bp_event_csrmv.argtypes = [P, P, P, f32, i64, i64, P, P, i32, u32, P, sz, P]
+        L.bp_jitconn_workspace_bytes.argtypes = [i64, i64, i64, i32]
+        L.bp_jitconn_workspace_bytes.restype = sz
         L.bp_csrmv_plan_bytes.argtypes = [i64, i64, i32, i32]
         L.bp_csrmv_plan_bytes.restype = sz
         L.bp_csrmv_plan.argtypes = [P, P, i64, i64, i32, i32, P, sz, P]
@@ -133,6 +136,7 @@ def lib():
             if name not in ("bp_network_destroy", "bp_status_string",
                             "bp_last_error", "bp_conn_len", "bp_workspace_bytes",
                             "bp_csrmv_workspace_bytes", "bp_csrmv_plan_bytes",
+                            "bp_jitconn_workspace_bytes",
                             "bp_network_workspace_bytes", "bp_abi_version"):
                 getattr(L, name).restype = ctypes.c_int
         _lib = L
@@ -240,7 +244,10 @@ def jitconn_event_mv(law: int, spec: JitConn, w0: float, w1: float, spikes,
     """brainpy.math.jitconn.event_mv_prob_{homo,uniform,normal} (Listing S2)."""
     _cuda(spikes, out)
     col_end = n_cols if col_end is None else col_end
-    ws = ws if ws is not None else workspace(n_rows, out.device)
+    if ws is None:
+        nbytes = int(lib().bp_jitconn_workspace_bytes(int(n_rows), int(col_begin), int(col_end),
+                                                      _out_kind(out)))
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=out.device)
     flags = ACCUMULATE if accumulate else 0
     tail = (_ptr(spikes), int(n_rows), int(n_cols), int(col_begin), int(col_end),
             _ptr(out), _out_kind(out), flags, _ptr(ws), ws.numel(), _stream(stream))

@@ -238,6 +238,50 @@ __device__ unsigned long long g_csr_t[1024][8];
 #define CSR_MARK(k) do {} while (0)
 #endif
 
+// Sum a tile's partials (CTA-major: partial of CTA b of the tile at
+// (first + b) * tile_cols) over its `groups` CTAs in ascending order; CTA
+// `group` handles column slice `group` and writes out[c0 + column]
+// (accumulate: +=).  Homogeneous partials are event counts: fl32(n * w) or
+// n * q.  Deterministic for counts and fixed point.
+template <int KIND, bool HOMO, int NT>
+__device__ __forceinline__ void tile_reduce(const void *partials, size_t first, int group,
+                                            int groups, int tile_cols, int width, int64_t c0,
+                                            void *out, int accumulate, float w, long long q) {
+  const int per = (width + groups - 1) / groups;
+  const int s0 = group * per, s1 = min(width, s0 + per);
+  const size_t stride = static_cast<size_t>(tile_cols);
+  const size_t base = first * stride;
+  for (int cc = s0 + static_cast<int>(threadIdx.x); cc < s1; cc += NT) {
+    const int64_t c = c0 + cc;
+    if (HOMO) {
+      const unsigned *p = static_cast<const unsigned *>(partials) + base + cc;
+      unsigned long long n = 0;
+      for (int g = 0; g < groups; ++g) n += __ldcg(p + g * stride);
+      if (KIND == 0) {
+        const float v = __fmul_rn(__ull2float_rn(n), w);
+        float *o = static_cast<float *>(out) + c;
+        *o = accumulate ? __fadd_rn(*o, v) : v;
+      } else {
+        const long long v = static_cast<long long>(n) * q;
+        long long *o = static_cast<long long *>(out) + c;
+        *o = accumulate ? *o + v : v;
+      }
+    } else if (KIND == 0) {
+      const float *p = static_cast<const float *>(partials) + base + cc;
+      float v = 0.f;
+      for (int g = 0; g < groups; ++g) v = __fadd_rn(v, __ldcg(p + g * stride));
+      float *o = static_cast<float *>(out) + c;
+      *o = accumulate ? __fadd_rn(*o, v) : v;
+    } else {
+      const long long *p = static_cast<const long long *>(partials) + base + cc;
+      long long v = 0;
+      for (int g = 0; g < groups; ++g) v += __ldcg(p + g * stride);
+      long long *o = static_cast<long long *>(out) + c;
+      *o = accumulate ? *o + v : v;
+    }
+  }
+}
+
 // KIND: 0 f32 partials, 1 int64 fixed-point partials; HOMO: uint32 counts.
 template <int KIND, bool HOMO>
 __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs a) {
@@ -446,39 +490,9 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs 
   __threadfence();
   cg::this_grid().sync();
   CSR_MARK(5);
-  const int per = (width + a.groups - 1) / a.groups;
-  const int s0 = group * per, s1 = min(width, s0 + per);
-  const size_t stride = static_cast<size_t>(a.tile_cols);
-  const size_t base = static_cast<size_t>(tile) * a.groups * stride;
-  for (int cc = s0 + tid; cc < s1; cc += kStreamThreads) {
-    const int64_t c = c0 + cc;
-    if (HOMO) {
-      const unsigned *p = static_cast<const unsigned *>(a.partials) + base + cc;
-      unsigned long long n = 0;
-      for (int g = 0; g < a.groups; ++g) n += __ldcg(p + g * stride);
-      if (KIND == 0) {
-        const float v = __fmul_rn(__ull2float_rn(n), a.w);
-        float *o = static_cast<float *>(a.out) + c;
-        *o = a.accumulate ? __fadd_rn(*o, v) : v;
-      } else {
-        const long long v = static_cast<long long>(n) * a.q;
-        long long *o = static_cast<long long *>(a.out) + c;
-        *o = a.accumulate ? *o + v : v;
-      }
-    } else if (KIND == 0) {
-      const float *p = static_cast<const float *>(a.partials) + base + cc;
-      float v = 0.f;
-      for (int g = 0; g < a.groups; ++g) v = __fadd_rn(v, __ldcg(p + g * stride));
-      float *o = static_cast<float *>(a.out) + c;
-      *o = a.accumulate ? __fadd_rn(*o, v) : v;
-    } else {
-      const long long *p = static_cast<const long long *>(a.partials) + base + cc;
-      long long v = 0;
-      for (int g = 0; g < a.groups; ++g) v += __ldcg(p + g * stride);
-      long long *o = static_cast<long long *>(a.out) + c;
-      *o = a.accumulate ? *o + v : v;
-    }
-  }
+  tile_reduce<KIND, HOMO, kStreamThreads>(a.partials, static_cast<size_t>(tile) * a.groups,
+                                         group, a.groups, a.tile_cols, width, c0, a.out,
+                                         a.accumulate, a.w, a.q);
   CSR_MARK(6);
 }
 

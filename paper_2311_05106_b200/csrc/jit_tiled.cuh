@@ -1,0 +1,151 @@
+// jit_tiled.cuh -- JIT-connectivity event scatter (a3 + a4, Listing S2) with
+// shared-memory column tiles instead of one global RED per event.
+//
+// The stateless bp_jitconn_event_mv_* spends its time in random global REDs
+// (~0.11-0.19 T/s on B200, k_jit_scatter).  Regeneration reads no memory, so
+// the whole shared memory of an SM can hold accumulators: columns are cut
+// into tiles of up to ~57 k f32 / int32 counts (28 k int64), CTA (tile t,
+// group g) regenerates its share of the active (row, segment) items, keeps
+// the events inside its tile in shared memory (native int32 counts for
+// homogeneous weights, two int32 words for fixed point, f32 CAS otherwise),
+// and stops each gap chain at the tile's end.  A row segment that spans
+// several tiles is regenerated from its start by every tile it reaches, so
+// later tiles do more work: they get proportionally more CTAs.  The partial
+// tiles are reduced in the same cooperative kernel (tile_reduce).  (Adding
+// the non-zero columns of sparse CTAs with atomics instead, to spare small
+// calls the 148 dense partials, measured slower at every size.)
+#pragma once
+#include <cstdint>
+
+#include "csr_stream.cuh"
+
+namespace bp {
+
+constexpr int kJitTiledThreads = 1024;
+constexpr int kJitMaxTiles = 16;
+
+struct JitTiledArgs {
+  JitSide s;                   // the projection (one per call)
+  uint32_t n_cols, col_begin, col_end;
+  const int32_t *active;
+  const int32_t *count;
+  void *partials;              // [CTA][tile_cols]
+  void *out;                   // indexed c - col_begin
+  int accumulate;
+  int32_t tile_cols, n_tiles;
+  int32_t cta0[kJitMaxTiles + 1];   // first CTA of each tile (CTA-major partials)
+  unsigned long long *events;       // nullable
+};
+
+template <int LAW, int KIND>
+__global__ void __launch_bounds__(kJitTiledThreads, 1) k_jit_tiled(JitTiledArgs a) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  constexpr bool HOMO = LAW == 0;
+  constexpr int acc_bytes = (HOMO || KIND == 0) ? 4 : 8;
+  int tile = 0;
+  while (tile + 1 < a.n_tiles && static_cast<int>(blockIdx.x) >= a.cta0[tile + 1]) ++tile;
+  const int group = blockIdx.x - a.cta0[tile];
+  const int groups = a.cta0[tile + 1] - a.cta0[tile];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t W = a.col_end - a.col_begin;
+  const uint32_t t0 = static_cast<uint32_t>(tile) * a.tile_cols;
+  const uint32_t g0 = a.col_begin + t0;                        // global tile range
+  const uint32_t g1 = a.col_begin + min(W, t0 + a.tile_cols);
+  const int width = static_cast<int>(g1 - g0);
+  for (int c = tid; c <= width; c += kJitTiledThreads) {        // tile + sink slot
+    if (acc_bytes == 4) reinterpret_cast<uint32_t *>(sm)[c] = 0u;
+    else reinterpret_cast<unsigned long long *>(sm)[c] = 0ull;
+  }
+  __syncthreads();
+  const JitSide &s = a.s;
+  auto add = [&](uint32_t pos, float w) {
+    const uint32_t lc = min(pos - g0, static_cast<uint32_t>(width));
+    if (HOMO) atomicAdd(reinterpret_cast<uint32_t *>(sm) + lc, 1u);
+    else if (KIND == 0) atomicAdd(reinterpret_cast<float *>(sm) + lc, w);
+    else {
+      unsigned *p = reinterpret_cast<unsigned *>(sm) + 2 * lc;   // int64 as 2 x int32 + carry
+      const unsigned long long qq = static_cast<unsigned long long>(quantize(w));
+      const unsigned lo = static_cast<unsigned>(qq);
+      const unsigned old = atomicAdd(p, lo);
+      atomicAdd(p + 1, static_cast<unsigned>(qq >> 32) + (old + lo < old ? 1u : 0u));
+    }
+  };
+
+  const int64_t n_items = static_cast<int64_t>(*a.count) * s.n_seg;
+  const int64_t NW = static_cast<int64_t>(groups) * (kJitTiledThreads / 32);
+  uint32_t ev = 0;
+  for (int64_t item = static_cast<int64_t>(group) * (kJitTiledThreads / 32) + warp;
+       item < n_items; item += NW) {
+    const uint32_t row = static_cast<uint32_t>(a.active[item / s.n_seg]);
+    const uint32_t seg = s.seg_first + static_cast<uint32_t>(item % s.n_seg);
+    const uint32_t seg_begin = seg * s.L;
+    const uint32_t seg_end = min(seg_begin + s.L, a.n_cols);
+    const uint32_t stop = min(seg_end, g1);
+    if (seg_begin >= g1 || seg_end <= g0) continue;             // warp-uniform
+    u32x4 g = philox_block(s.seed, kTagGap, row, seg, lane);
+    uint32_t start = seg_begin + first_offset(s.seed, s.K, row, seg);
+    uint32_t chunk = 0;
+    while (start < stop) {                                      // warp-uniform
+      const uint32_t blk = chunk * 32u + lane;
+      const uint32_t q0 = bounded(1u, s.K, g.x), q1 = bounded(1u, s.K, g.y);
+      const uint32_t q2 = bounded(1u, s.K, g.z), q3 = bounded(1u, s.K, g.w);
+      const uint32_t p1 = q0, p2 = q0 + q1, p3 = p2 + q2, t = p3 + q3;
+      uint32_t incl = t;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += v;
+      }
+      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      const uint32_t pos0 = start + (incl - t);
+      const uint32_t pos[4] = {pos0, pos0 + p1, pos0 + p2, pos0 + p3};
+      // this lane's events inside the tile (positions ascend along the chain)
+      const bool any = pos0 < stop && pos[3] >= g0;
+      if (any) {
+        float w[4] = {s.w0, s.w0, s.w0, s.w0};
+        if (LAW == 1) {
+          const u32x4 x = philox_block(s.seed, kTagWeight, row, seg, blk);
+          w[0] = uniform_weight(x.x, s.w0, s.w1); w[1] = uniform_weight(x.y, s.w0, s.w1);
+          w[2] = uniform_weight(x.z, s.w0, s.w1); w[3] = uniform_weight(x.w, s.w0, s.w1);
+        } else if (LAW == 2) {
+          const u32x4 x = philox_block(s.seed, kTagWeight, row, seg, 2u * blk);
+          if (pos[0] >= g0) w[0] = normal_weight(x.x, x.y, s.w0, s.w1);
+          if (pos[1] >= g0 && pos[1] < stop) w[1] = normal_weight(x.z, x.w, s.w0, s.w1);
+          if (pos[2] < stop && pos[3] >= g0) {
+            const u32x4 y = philox_block(s.seed, kTagWeight, row, seg, 2u * blk + 1u);
+            if (pos[2] >= g0) w[2] = normal_weight(y.x, y.y, s.w0, s.w1);
+            if (pos[3] < stop) w[3] = normal_weight(y.z, y.w, s.w0, s.w1);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (pos[k] >= g0 && pos[k] < stop) {
+            add(pos[k], w[k]);
+            ++ev;
+          }
+        }
+      }
+      start += total;
+      ++chunk;
+      if (start < stop) g = philox_block(s.seed, kTagGap, row, seg, chunk * 32u + lane);
+    }
+  }
+  __syncthreads();
+  char *dst = static_cast<char *>(a.partials) +
+              static_cast<size_t>(blockIdx.x) * a.tile_cols * acc_bytes;
+  const int n16 = width * acc_bytes / 16;
+  for (int k = tid; k < n16; k += kJitTiledThreads)
+    reinterpret_cast<uint4 *>(dst)[k] = reinterpret_cast<const uint4 *>(sm)[k];
+  for (int b = n16 * 16 + tid; b < width * acc_bytes; b += kJitTiledThreads) dst[b] = sm[b];
+  if (a.events) {
+    ev = __reduce_add_sync(0xffffffffu, ev);
+    if (lane == 0 && ev) atomicAdd(a.events, static_cast<unsigned long long>(ev));
+  }
+  __threadfence();
+  cg::this_grid().sync();
+  tile_reduce<KIND, HOMO, kJitTiledThreads>(a.partials, static_cast<size_t>(a.cta0[tile]), group,
+                                            groups, a.tile_cols, width, t0, a.out, a.accumulate,
+                                            s.w0, s.q);
+}
+
+}  // namespace bp

@@ -157,13 +157,22 @@ JIT_CASES = [
     (300, 10_000, 0.1, 1000, 0.2),     # 10 segments
     (1000, 100_000, 0.05, 0, 0.01),    # fan-out 5000 (config 2 row shape)
     (4000, 4000, 0.02, 0, 0.01),       # COBA-4000 projection shape
-    (3, 2**20, 80 / 2**20, 0, 1.0),    # huge K = 26213
+    (3, 2**20, 80 / 2**20, 0, 1.0),    # huge K = 26213; > 16 column tiles: per-event path
+    (200, 300_000, 0.005, 0, 0.1),     # 6-11 column tiles, rows spanning all of them
+    (150, 240_000, 0.01, 40_000, 0.2), # segments shorter than a tile
 ]
 
 
+@pytest.mark.parametrize("path", ["tiled", "direct"])
 @pytest.mark.parametrize("case", JIT_CASES)
 @pytest.mark.parametrize("law", ["homo", "uniform", "normal"])
-def test_jitconn_event_mv(bp, orc, case, law):
+def test_jitconn_event_mv(bp, orc, case, law, path, monkeypatch):
+    """tiled: shared-memory column tiles + in-kernel reduction (default when
+    the workspace holds the partial tiles); direct: one global RED per event."""
+    if path == "direct":
+        monkeypatch.setenv("BP_JIT_DIRECT", "1")
+    else:
+        monkeypatch.setenv("BP_JIT_TILED", "1")     # normal weights too
     n_rows, n_cols, p, seg_len, density = case
     w0, w1 = {"homo": (0.6, 0.0), "uniform": (-0.1, 0.1), "normal": (0.0, 0.3)}[law]
     seed = 0xC0FFEE + n_rows
@@ -195,8 +204,11 @@ def test_jitconn_event_mv(bp, orc, case, law):
     assert np.all(err <= 1e-5 * absw + 1e-6 * (law == "normal") * absw + 1e-30)
 
 
+@pytest.mark.parametrize("path", ["tiled", "direct"])
 @pytest.mark.parametrize("bounds", [(0, 1000), (1000, 5000), (9000, 10_000), (2000, 2000)])
-def test_jitconn_partition(bp, orc, bounds):
+def test_jitconn_partition(bp, orc, bounds, path, monkeypatch):
+    if path == "direct":
+        monkeypatch.setenv("BP_JIT_DIRECT", "1")
     n_rows, n_cols, L = 400, 10_000, 1000
     cb, ce = bounds
     spec = bp.jitconn_spec(77, 0.02, 0, L)
@@ -207,6 +219,24 @@ def test_jitconn_partition(bp, orc, bounds):
                                 col_begin=cb, col_end=ce)
     want = orc.jit_event_mv(ospec, n_rows, n_cols, ev, cb, ce, orc.OUT_FIX)
     assert np.array_equal(out.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("law", ["homo", "uniform"])
+def test_jitconn_tiled_accumulate_and_wide_partition(bp, orc, law):
+    """Tiled path: accumulate into a non-zero output; a partition of 130 k
+    columns (3 tiles) out of 260 k."""
+    n_rows, n_cols, L = 300, 260_000, 130_000
+    cb, ce = 130_000, 260_000
+    w0, w1 = (0.6, 0.0) if law == "homo" else (-0.2, 0.3)
+    spec = bp.jitconn_spec(4242, 0.004, 0, L)
+    ospec = orc.JitSpec(4242, orc.conn_len(0.004), L, orc.LAWS[law], w0, w1)
+    ev = inputs.spike_pattern(n_rows, 0.25, seed=12)
+    out = torch.full((ce - cb,), 3 * 2 ** 32, dtype=torch.int64, device="cuda")
+    fn = bp.jitconn_event_mv_homo if law == "homo" else bp.jitconn_event_mv_uniform
+    args = (spec, w0) if law == "homo" else (spec, w0, w1)
+    fn(*args, _dev_spikes(ev), n_rows, n_cols, out, col_begin=cb, col_end=ce, accumulate=True)
+    want = orc.jit_event_mv(ospec, n_rows, n_cols, ev, cb, ce, orc.OUT_FIX)
+    assert np.array_equal(out.cpu().numpy(), want + 3 * 2 ** 32)
 
 
 def test_jitconn_rejects_unaligned_partition(bp):
