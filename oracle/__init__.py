@@ -88,6 +88,8 @@ def lib():
         _lib.or_event_csrmv.argtypes = [P, P, P, f32, i64, P, i32, P, P]
         _lib.or_jit_event_mv.argtypes = [u64, u32, u32, i32, f32, f32, i64,
                                          i64, i64, i64, P, i32, P, P]
+        _lib.or_jit_mv.argtypes = [u64, u32, u32, i32, f32, f32, i64, i64, i64, i64,
+                                   P, i32, P, P]
         _lib.or_lif_step.argtypes = [ctypes.POINTER(LifParams), i64, P, P, P,
                                      i32, P, P]
         _lib.or_hh_step.argtypes = [ctypes.POINTER(HHParams), i64, P, P, P, P,
@@ -217,6 +219,21 @@ def jit_event_mv(spec: JitSpec, n_rows, n_cols, events, col_begin=0,
     lib().or_jit_event_mv(spec.seed, spec.K, spec.L, spec.law, spec.w0,
                           spec.w1, n_rows, n_cols, col_begin, col_end,
                           _p(ev), out_kind, _p(out), _p(absd))
+    return (out, absd) if with_abs else out
+
+
+def jit_mv(spec: JitSpec, n_rows, n_cols, v, col_begin=0, col_end=None,
+           out_kind=OUT_F64, out=None, with_abs=False):
+    """Non-event mv_prob_* (reading MV1): out[c] += sum_r v[r] w_e."""
+    if col_end is None:
+        col_end = n_cols
+    vv = np.ascontiguousarray(v, np.float32)
+    assert vv.shape[0] == n_rows
+    if out is None:
+        out = _out_buf(col_end - col_begin, out_kind)
+    absd = np.zeros(col_end - col_begin, np.float64) if with_abs else None
+    lib().or_jit_mv(spec.seed, spec.K, spec.L, spec.law, spec.w0, spec.w1, n_rows, n_cols,
+                    col_begin, col_end, _p(vv), out_kind, _p(out), _p(absd))
     return (out, absd) if with_abs else out
 
 

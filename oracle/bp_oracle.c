@@ -257,6 +257,55 @@ void or_jit_event_mv(uint64_t seed, uint32_t K, uint32_t L, int law, float w0,
 }
 
 /* ------------------------------------------------------------------------
+ * Non-event JIT matrix-vector product, mv_prob_{homo,uniform,normal} (P:94,
+ * P:192), reading MV1:
+ *   out[c] (+)= sum_r v[r] * w_e(r) over the edges (r, e) with pos_e(r) = c,
+ * the same connectivity and weights as rules J1-J9 (orientation as
+ * Listing S2: rows = vector index, columns = output).  The product of two
+ * fp32 numbers is exact in fp64, so
+ *   OR_OUT_F64: (double)v * (double)w   (the reference),
+ *   OR_OUT_FIX: llrint(2^32 * (double)v * (double)w)  (one rounding, rule F1),
+ *   OR_OUT_F32: fl32(v * w) added in fp32.
+ * Rows with v[r] == 0 contribute nothing and are skipped.
+ * Pinned by: v in {0, 1} equals or_jit_event_mv bit for bit (fixed point),
+ * the dense fp64 D^T v of the materialised matrix, linearity in v
+ * (test_oracle_jit.py).
+ * ---------------------------------------------------------------------- */
+void or_jit_mv(uint64_t seed, uint32_t K, uint32_t L, int law, float w0, float w1,
+               int64_t n_rows, int64_t n_cols, int64_t col_begin, int64_t col_end,
+               const float *v, int out_kind, void *out, double *abs_out) {
+  if (col_end <= col_begin) return;
+  int64_t seg_first = col_begin / (int64_t)L;
+  int64_t seg_last = (col_end - 1) / (int64_t)L;
+  for (int64_t r = 0; r < n_rows; ++r) {
+    if (v[r] == 0.0f) continue;
+    for (int64_t s = seg_first; s <= seg_last; ++s) {
+      int64_t seg_begin = s * (int64_t)L;
+      int64_t seg_end = seg_begin + (int64_t)L;
+      if (seg_end > n_cols) seg_end = n_cols;
+      uint32_t a = uniform_int(0u, K - 1u, or_word(seed, 2u, (uint32_t)r, (uint32_t)s, 0u));
+      uint32_t b = uniform_int(0u, K, or_word(seed, 2u, (uint32_t)r, (uint32_t)s, 1u));
+      if (b <= a) a = K - 1u - a;
+      int64_t pos = seg_begin + (int64_t)a;
+      uint32_t e = 0;
+      while (pos < seg_end) {
+        if (pos >= col_begin && pos < col_end) {
+          float w = edge_weight(seed, law, w0, w1, (uint32_t)r, (uint32_t)s, e);
+          double prod = (double)v[r] * (double)w;         /* exact */
+          int64_t c = pos - col_begin;
+          if (out_kind == OR_OUT_F64) ((double *)out)[c] += prod;
+          else if (out_kind == OR_OUT_FIX) ((int64_t *)out)[c] += llrint(ldexp(prod, 32));
+          else ((float *)out)[c] += v[r] * w;
+          if (abs_out) abs_out[c] += fabs(prod);
+        }
+        pos += (int64_t)uniform_int(1u, K, or_word(seed, 0u, (uint32_t)r, (uint32_t)s, e));
+        ++e;
+      }
+    }
+  }
+}
+
+/* ------------------------------------------------------------------------
  * Rule F2: a step's increments (summed exactly in int64, OR_OUT_FIX32) are
  * added to the int32 conductance with saturation at the int32 range.
  * Returns the number of saturated entries (a diagnostic; 0 in any sane run).

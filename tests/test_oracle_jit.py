@@ -200,3 +200,54 @@ def test_empty_and_degenerate(orc):
     out = orc.jit_event_mv(spec, 5, 10, np.ones(5, np.uint8), 4, 4,
                            out_kind=orc.OUT_FIX)
     assert out.size == 0
+
+
+# ---------------------------------------------------------------- MV1
+# Non-event mv_prob_* (SURVEY 8(f) NEXT 1): out = sum_r v[r] w_e.
+
+@pytest.mark.parametrize("law", ["homo", "uniform", "normal"])
+def test_mv_with_binary_vector_is_event_mv(orc, law):
+    """v in {0, 1}: 1.0 * w is exact, so the non-event product equals the
+    event scatter bit for bit in fixed point and in fp64."""
+    n_rows, n_cols = 300, 2000
+    spec = _spec(orc, 0.05, seed=21, n_cols=n_cols, law=law, w0=-0.2, w1=0.3)
+    ev = inputs.spike_pattern(n_rows, 0.3, 5)
+    v = ev.astype(np.float32)
+    for kind in (orc.OUT_FIX, orc.OUT_F64):
+        assert np.array_equal(orc.jit_mv(spec, n_rows, n_cols, v, out_kind=kind),
+                              orc.jit_event_mv(spec, n_rows, n_cols, ev, out_kind=kind))
+
+
+@pytest.mark.parametrize("law", ["homo", "uniform"])
+def test_mv_equals_dense_product(orc, law):
+    """Against D^T v with D densified row by row (fp64, products exact)."""
+    n_rows, n_cols = 120, 700
+    spec = _spec(orc, 0.1, seed=5, n_cols=n_cols, L=350, law=law, w0=-0.5, w1=0.5)
+    D = np.zeros((n_rows, n_cols))
+    for r in range(n_rows):
+        pos, w = orc.jit_row(spec, n_cols, r)
+        D[r, pos] = w.astype(np.float64)
+    rng = np.random.default_rng(8)
+    v = rng.normal(size=n_rows).astype(np.float32)
+    v[rng.random(n_rows) < 0.2] = 0.0
+    want = D.T @ v.astype(np.float64)
+    got, absw = orc.jit_mv(spec, n_rows, n_cols, v, out_kind=orc.OUT_F64, with_abs=True)
+    assert np.all(np.abs(got - want) <= 1e-13 * absw + 1e-300)
+    # fixed point: each exact product rounded once to 2^-32
+    fix = orc.jit_mv(spec, n_rows, n_cols, v, out_kind=orc.OUT_FIX)
+    nnz = (D != 0).T.astype(np.int64) @ (v != 0).astype(np.int64)
+    assert np.all(np.abs(fix / 2.0 ** 32 - want) <= 0.5 * nnz * 2.0 ** -32 + 1e-12 * absw)
+
+
+def test_mv_is_linear(orc):
+    n_rows, n_cols = 200, 1500
+    spec = _spec(orc, 0.05, seed=9, n_cols=n_cols, law="uniform", w0=-1.0, w1=1.0)
+    rng = np.random.default_rng(2)
+    v1 = rng.integers(-3, 4, n_rows).astype(np.float32)
+    v2 = rng.integers(-3, 4, n_rows).astype(np.float32)
+    y1 = orc.jit_mv(spec, n_rows, n_cols, v1, out_kind=orc.OUT_F64)
+    y2 = orc.jit_mv(spec, n_rows, n_cols, v2, out_kind=orc.OUT_F64)
+    y12 = orc.jit_mv(spec, n_rows, n_cols, (2 * v1 - v2).astype(np.float32),
+                     out_kind=orc.OUT_F64)
+    # integer v times fp32 weights: every product and partial sum is exact
+    assert np.array_equal(y12, 2 * y1 - y2)
