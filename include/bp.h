@@ -190,6 +190,30 @@ bp_status bp_jitconn_event_mv_normal(const bp_jitconn *spec, float w_mu,
                                      void *ws, size_t ws_bytes,
                                      bp_stream stream);
 
+/* Non-event products with the same JIT matrices (brainpy.math.jitconn
+ * mv_prob_{homo,uniform,normal}(vector, ...); SURVEY
+ * 8(f) NEXT 1), reading MV1:
+ *     out[c] (+)= sum_r v[r] * w_e(r)   over the edges (r, e) with pos_e(r) = c,
+ * v: n_rows float32 (device); rows with v[r] == 0 are skipped (they add
+ * nothing).  Contribution per edge: fl32(v[r] * w) in BP_OUT_F32 (float
+ * atomics, order-dependent, rule T2); in BP_OUT_FIX64 the exact fp64 product
+ * rounded once to 2^-32 (bit-reproducible).  Connectivity, weights,
+ * partition, workspace (bp_jitconn_workspace_bytes) and errors as the event
+ * variants.  With v in {0, 1} the result equals the event variant bit for
+ * bit in fixed point. */
+bp_status bp_jitconn_mv_homo(const bp_jitconn *spec, float weight, const float *v,
+                             int64_t n_rows, int64_t n_cols, int64_t col_begin,
+                             int64_t col_end, void *out, int out_kind, uint32_t flags,
+                             void *ws, size_t ws_bytes, bp_stream stream);
+bp_status bp_jitconn_mv_uniform(const bp_jitconn *spec, float w_low, float w_high,
+                                const float *v, int64_t n_rows, int64_t n_cols,
+                                int64_t col_begin, int64_t col_end, void *out, int out_kind,
+                                uint32_t flags, void *ws, size_t ws_bytes, bp_stream stream);
+bp_status bp_jitconn_mv_normal(const bp_jitconn *spec, float w_mu, float w_sigma,
+                               const float *v, int64_t n_rows, int64_t n_cols,
+                               int64_t col_begin, int64_t col_end, void *out, int out_kind,
+                               uint32_t flags, void *ws, size_t ws_bytes, bp_stream stream);
+
 /* Debug/inspection: materialise the implied matrix with the KERNEL's own
  * generator.  row_counts: counts[r] = number of edges of row r (int64[n_rows]).
  * materialize: given indptr (exclusive prefix sum of the counts, int64

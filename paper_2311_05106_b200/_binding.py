@@ -27,7 +27,8 @@ EXPORTED = [
     "bp_abi_version", "bp_status_string", "bp_last_error", "bp_conn_len",
     "bp_workspace_bytes", "bp_csrmv_workspace_bytes", "bp_compact_spikes", "bp_event_csrmv",
     "bp_csrmv_plan_bytes", "bp_csrmv_plan", "bp_event_csrmv_planned",
-    "bp_jitconn_workspace_bytes",
+    "bp_jitconn_workspace_bytes", "bp_jitconn_mv_homo", "bp_jitconn_mv_uniform",
+    "bp_jitconn_mv_normal",
     "bp_jitconn_event_mv_homo", "bp_jitconn_event_mv_uniform",
     "bp_jitconn_event_mv_normal", "bp_jitconn_row_counts",
     "bp_jitconn_materialize", "bp_neuron_step", "bp_network_workspace_bytes",
@@ -115,6 +116,9 @@ def lib():
         L.bp_jitconn_event_mv_homo.argtypes = [ctypes.POINTER(JitConn), f32] + jit_tail
         L.bp_jitconn_event_mv_uniform.argtypes = [ctypes.POINTER(JitConn), f32, f32] + jit_tail
         L.bp_jitconn_event_mv_normal.argtypes = [ctypes.POINTER(JitConn), f32, f32] + jit_tail
+        L.bp_jitconn_mv_homo.argtypes = [ctypes.POINTER(JitConn), f32, P] + jit_tail[1:]
+        L.bp_jitconn_mv_uniform.argtypes = [ctypes.POINTER(JitConn), f32, f32, P] + jit_tail[1:]
+        L.bp_jitconn_mv_normal.argtypes = [ctypes.POINTER(JitConn), f32, f32, P] + jit_tail[1:]
         L.bp_jitconn_row_counts.argtypes = [ctypes.POINTER(JitConn), i64, i64, P, P]
         L.bp_jitconn_materialize.argtypes = [ctypes.POINTER(JitConn), i32, f32, f32,
                                              i64, i64, P, P, P, P]
@@ -261,6 +265,29 @@ def jitconn_event_mv(law: int, spec: JitConn, w0: float, w1: float, spikes,
     else:
         raise BpError(f"unknown law {law}")
     _check(st)
+    return out
+
+
+def jitconn_mv(law: int, spec: JitConn, w0: float, w1: float, v, n_rows, n_cols, out,
+               col_begin=0, col_end=None, accumulate=False, ws=None, stream=None):
+    """brainpy.math.jitconn.mv_prob_{homo,uniform,normal}(vector, ...): the
+    non-event product out[c] (+)= sum_r v[r] w_e (reading MV1)."""
+    _cuda(v, out)
+    col_end = n_cols if col_end is None else col_end
+    if ws is None:
+        nbytes = int(lib().bp_jitconn_workspace_bytes(int(n_rows), int(col_begin), int(col_end),
+                                                      _out_kind(out)))
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=out.device)
+    tail = (_ptr(v), int(n_rows), int(n_cols), int(col_begin), int(col_end), _ptr(out),
+            _out_kind(out), ACCUMULATE if accumulate else 0, _ptr(ws), ws.numel(),
+            _stream(stream))
+    L = lib()
+    if law == LAW_HOMO:
+        _check(L.bp_jitconn_mv_homo(ctypes.byref(spec), float(w0), *tail))
+    elif law == LAW_UNIFORM:
+        _check(L.bp_jitconn_mv_uniform(ctypes.byref(spec), float(w0), float(w1), *tail))
+    else:
+        _check(L.bp_jitconn_mv_normal(ctypes.byref(spec), float(w0), float(w1), *tail))
     return out
 
 

@@ -317,10 +317,10 @@ struct JitTilePlan {
 };
 
 JitTilePlan jit_tile_plan(int64_t n_rows, int64_t width, int out_kind, int law, uint32_t L,
-                          int sms) {
+                          int sms, bool vec = false) {
   JitTilePlan p{};
   if (width < 1 || n_rows < 1) return p;
-  const int acc = (law == BP_LAW_HOMO || out_kind == BP_OUT_F32) ? 4 : 8;
+  const int acc = ((law == BP_LAW_HOMO && !vec) || out_kind == BP_OUT_F32) ? 4 : 8;
   const int64_t max_cols =
       ((static_cast<int64_t>(kSmemOptin) - kJitStaticSmem) / acc - 4) & ~int64_t{3};
   const int64_t nt = (width + max_cols - 1) / max_cols;
@@ -355,16 +355,17 @@ JitTilePlan jit_tile_plan(int64_t n_rows, int64_t width, int out_kind, int law, 
   return p;
 }
 
-template <int LAW, int KIND>
+template <int LAW, int KIND, bool VEC>
 bool jit_tiled_coop(bp::JitTiledArgs a, const JitTilePlan &p, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(bp::k_jit_tiled<LAW, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(bp::k_jit_tiled<LAW, KIND, VEC>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kSmemOptin - kJitStaticSmem));
     attr = true;
   }
   void *args[] = {&a};
-  if (cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(bp::k_jit_tiled<LAW, KIND>),
+  if (cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(bp::k_jit_tiled<LAW, KIND, VEC>),
                                   dim3(p.grid), dim3(bp::kJitTiledThreads), args, p.smem,
                                   st) == cudaSuccess)
     return true;
@@ -372,19 +373,31 @@ bool jit_tiled_coop(bp::JitTiledArgs a, const JitTilePlan &p, cudaStream_t st) {
   return false;
 }
 
-bool launch_jit_tiled(const bp::JitTiledArgs &a, int law, int out_kind, const JitTilePlan &p,
-                      cudaStream_t st) {
-  const bool fix = out_kind == BP_OUT_FIX64;
-  if (law == BP_LAW_HOMO) return fix ? jit_tiled_coop<0, 1>(a, p, st) : jit_tiled_coop<0, 0>(a, p, st);
-  if (law == BP_LAW_UNIFORM) return fix ? jit_tiled_coop<1, 1>(a, p, st) : jit_tiled_coop<1, 0>(a, p, st);
-  return fix ? jit_tiled_coop<2, 1>(a, p, st) : jit_tiled_coop<2, 0>(a, p, st);
+template <bool VEC>
+bool launch_jit_tiled_v(const bp::JitTiledArgs &a, int law, bool fix, const JitTilePlan &p,
+                        cudaStream_t st) {
+  if (law == BP_LAW_HOMO)
+    return fix ? jit_tiled_coop<0, 1, VEC>(a, p, st) : jit_tiled_coop<0, 0, VEC>(a, p, st);
+  if (law == BP_LAW_UNIFORM)
+    return fix ? jit_tiled_coop<1, 1, VEC>(a, p, st) : jit_tiled_coop<1, 0, VEC>(a, p, st);
+  return fix ? jit_tiled_coop<2, 1, VEC>(a, p, st) : jit_tiled_coop<2, 0, VEC>(a, p, st);
 }
 
+bool launch_jit_tiled(const bp::JitTiledArgs &a, int law, int out_kind, bool vec,
+                      const JitTilePlan &p, cudaStream_t st) {
+  const bool fix = out_kind == BP_OUT_FIX64;
+  return vec ? launch_jit_tiled_v<true>(a, law, fix, p, st)
+             : launch_jit_tiled_v<false>(a, law, fix, p, st);
+}
+
+// Event scatter (spikes) or non-event product (v, reading MV1); exactly one
+// of spikes / v is used.
 bp_status jit_event_mv(int law, const bp_jitconn *spec, float w0, float w1,
                        const uint32_t *spikes, int64_t n_rows, int64_t n_cols,
                        int64_t col_begin, int64_t col_end, void *out,
                        int out_kind, uint32_t flags, void *ws, size_t ws_bytes,
-                       bp_stream stream) {
+                       bp_stream stream, const float *v = nullptr) {
+  const bool vec = v != nullptr;
   int sms = 0;
   bp_status s = device_ready(&sms);
   if (s != BP_OK) return s;
@@ -393,7 +406,7 @@ bp_status jit_event_mv(int law, const bp_jitconn *spec, float w0, float w1,
   BP_CHECK(col_begin >= 0 && col_begin <= col_end && col_end <= n_cols, BP_ERR_SHAPE,
            "partition [%lld, %lld) outside [0, %lld)", (long long)col_begin,
            (long long)col_end, (long long)n_cols);
-  BP_CHECK(n_rows == 0 || spikes != nullptr, BP_ERR_INVALID_ARG, "spikes is NULL");
+  BP_CHECK(n_rows == 0 || vec || spikes != nullptr, BP_ERR_INVALID_ARG, "spikes is NULL");
   if (col_end > col_begin) {
     s = check_out(out, out_kind);
     if (s != BP_OK) return s;
@@ -414,7 +427,8 @@ bp_status jit_event_mv(int law, const bp_jitconn *spec, float w0, float w1,
   if (s != BP_OK) return s;
   cudaStream_t st = as_stream(stream);
   const size_t elt = out_kind == BP_OUT_FIX64 ? 8 : 4;
-  const JitTilePlan tp = jit_tile_plan(n_rows, col_end - col_begin, out_kind, law, jr.L, sms);
+  const JitTilePlan tp =
+      jit_tile_plan(n_rows, col_end - col_begin, out_kind, law, jr.L, sms, vec);
   // normal weights: the fp64 Box-Muller of every event dominates and is the
   // same on both paths; the per-event path skips the partial tiles (measured
   // 510 vs 551 us on the 100 k x 100 k, p = 0.05, 10 % cell)
@@ -428,9 +442,13 @@ bp_status jit_event_mv(int law, const bp_jitconn *spec, float w0, float w1,
   if (tiled) {
     // shared-memory column tiles + in-kernel reduction (every output
     // column of the partition is written: no memset)
-    BP_CUDA(cudaMemsetAsync(w.count, 0, sizeof(int32_t), st));
-    launch_compact(spikes, n_rows, w.active, w.count, sms, st);
+    if (!vec) {
+      BP_CUDA(cudaMemsetAsync(w.count, 0, sizeof(int32_t), st));
+      launch_compact(spikes, n_rows, w.active, w.count, sms, st);
+    }
     bp::JitTiledArgs t{};
+    t.v = v;
+    t.n_rows = n_rows;
     t.s = jit_side(spec, jr, law, w0, w1, col_begin, col_end, out);
     t.n_cols = static_cast<uint32_t>(n_cols);
     t.col_begin = static_cast<uint32_t>(col_begin);
@@ -443,14 +461,18 @@ bp_status jit_event_mv(int law, const bp_jitconn *spec, float w0, float w1,
     t.tile_cols = tp.tile_cols;
     t.n_tiles = tp.n_tiles;
     for (int k = 0; k <= tp.n_tiles; ++k) t.cta0[k] = tp.cta0[k];
-    if (launch_jit_tiled(t, law, out_kind, tp, st)) return launched();
+    if (launch_jit_tiled(t, law, out_kind, vec, tp, st)) return launched();
   }
   if (!(flags & BP_ACCUMULATE) && col_end > col_begin)
     BP_CUDA(cudaMemsetAsync(out, 0, elt * (col_end - col_begin), st));
   if (n_rows == 0 || col_end == col_begin) return launched();
-  BP_CUDA(cudaMemsetAsync(w.count, 0, sizeof(int32_t), st));
-  launch_compact(spikes, n_rows, w.active, w.count, sms, st);
+  if (!vec) {
+    BP_CUDA(cudaMemsetAsync(w.count, 0, sizeof(int32_t), st));
+    launch_compact(spikes, n_rows, w.active, w.count, sms, st);
+  }
   bp::JitScatterArgs a{};
+  a.v = v;
+  a.n_rows = n_rows;
   a.e = jit_side(spec, jr, law, w0, w1, col_begin, col_end, out);
   a.i = a.e;
   a.split = n_rows;
@@ -754,6 +776,36 @@ bp_status bp_jitconn_event_mv_normal(const bp_jitconn *spec, float w_mu,
   return jit_event_mv(BP_LAW_NORMAL, spec, w_mu, w_sigma, spikes, n_rows,
                       n_cols, col_begin, col_end, out, out_kind, flags, ws,
                       ws_bytes, stream);
+}
+
+bp_status bp_jitconn_mv_homo(const bp_jitconn *spec, float weight, const float *v,
+                             int64_t n_rows, int64_t n_cols, int64_t col_begin,
+                             int64_t col_end, void *out, int out_kind, uint32_t flags,
+                             void *ws, size_t ws_bytes, bp_stream stream) {
+  if (n_rows > 0 && v == nullptr) return fail(BP_ERR_INVALID_ARG, "v is NULL");
+  return jit_event_mv(BP_LAW_HOMO, spec, weight, 0.0f, nullptr, n_rows, n_cols, col_begin,
+                      col_end, out, out_kind, flags, ws, ws_bytes, stream,
+                      v ? v : reinterpret_cast<const float *>(&weight));
+}
+
+bp_status bp_jitconn_mv_uniform(const bp_jitconn *spec, float w_low, float w_high,
+                                const float *v, int64_t n_rows, int64_t n_cols,
+                                int64_t col_begin, int64_t col_end, void *out, int out_kind,
+                                uint32_t flags, void *ws, size_t ws_bytes, bp_stream stream) {
+  if (n_rows > 0 && v == nullptr) return fail(BP_ERR_INVALID_ARG, "v is NULL");
+  return jit_event_mv(BP_LAW_UNIFORM, spec, w_low, w_high, nullptr, n_rows, n_cols, col_begin,
+                      col_end, out, out_kind, flags, ws, ws_bytes, stream,
+                      v ? v : reinterpret_cast<const float *>(&w_low));
+}
+
+bp_status bp_jitconn_mv_normal(const bp_jitconn *spec, float w_mu, float w_sigma,
+                               const float *v, int64_t n_rows, int64_t n_cols,
+                               int64_t col_begin, int64_t col_end, void *out, int out_kind,
+                               uint32_t flags, void *ws, size_t ws_bytes, bp_stream stream) {
+  if (n_rows > 0 && v == nullptr) return fail(BP_ERR_INVALID_ARG, "v is NULL");
+  return jit_event_mv(BP_LAW_NORMAL, spec, w_mu, w_sigma, nullptr, n_rows, n_cols, col_begin,
+                      col_end, out, out_kind, flags, ws, ws_bytes, stream,
+                      v ? v : reinterpret_cast<const float *>(&w_mu));
 }
 
 bp_status bp_jitconn_row_counts(const bp_jitconn *spec, int64_t n_rows,

@@ -27,8 +27,10 @@ constexpr int kJitMaxTiles = 16;
 struct JitTiledArgs {
   JitSide s;                   // the projection (one per call)
   uint32_t n_cols, col_begin, col_end;
-  const int32_t *active;
+  const int32_t *active;       // event mode: the spiking rows
   const int32_t *count;
+  const float *v;              // vector mode (mv_prob_*, reading MV1): every row r, v[r] * w
+  int64_t n_rows;
   void *partials;              // [CTA][tile_cols]
   void *out;                   // indexed c - col_begin
   int accumulate;
@@ -37,10 +39,12 @@ struct JitTiledArgs {
   unsigned long long *events;       // nullable
 };
 
-template <int LAW, int KIND>
+// VEC: non-event product with a float vector (every row, contribution v[r] w:
+// fl32 product in f32 mode, the exact fp64 product rounded once in fixed point)
+template <int LAW, int KIND, bool VEC>
 __global__ void __launch_bounds__(kJitTiledThreads, 1) k_jit_tiled(JitTiledArgs a) {
   extern __shared__ __align__(128) unsigned char sm[];
-  constexpr bool HOMO = LAW == 0;
+  constexpr bool HOMO = LAW == 0 && !VEC;     // count events, scale once
   constexpr int acc_bytes = (HOMO || KIND == 0) ? 4 : 8;
   int tile = 0;
   while (tile + 1 < a.n_tiles && static_cast<int>(blockIdx.x) >= a.cta0[tile + 1]) ++tile;
@@ -58,25 +62,33 @@ __global__ void __launch_bounds__(kJitTiledThreads, 1) k_jit_tiled(JitTiledArgs 
   }
   __syncthreads();
   const JitSide &s = a.s;
-  auto add = [&](uint32_t pos, float w) {
+  auto add = [&](uint32_t pos, float w, float vr) {
     const uint32_t lc = min(pos - g0, static_cast<uint32_t>(width));
     if (HOMO) atomicAdd(reinterpret_cast<uint32_t *>(sm) + lc, 1u);
-    else if (KIND == 0) atomicAdd(reinterpret_cast<float *>(sm) + lc, w);
+    else if (KIND == 0) atomicAdd(reinterpret_cast<float *>(sm) + lc, VEC ? __fmul_rn(vr, w) : w);
     else {
       unsigned *p = reinterpret_cast<unsigned *>(sm) + 2 * lc;   // int64 as 2 x int32 + carry
-      const unsigned long long qq = static_cast<unsigned long long>(quantize(w));
+      const unsigned long long qq = static_cast<unsigned long long>(
+          VEC ? __double2ll_rn(__dmul_rn(static_cast<double>(vr), static_cast<double>(w)) *
+                               4294967296.0)
+              : quantize(w));
       const unsigned lo = static_cast<unsigned>(qq);
       const unsigned old = atomicAdd(p, lo);
       atomicAdd(p + 1, static_cast<unsigned>(qq >> 32) + (old + lo < old ? 1u : 0u));
     }
   };
 
-  const int64_t n_items = static_cast<int64_t>(*a.count) * s.n_seg;
+  const int64_t n_items = (VEC ? a.n_rows : static_cast<int64_t>(*a.count)) * s.n_seg;
   const int64_t NW = static_cast<int64_t>(groups) * (kJitTiledThreads / 32);
   uint32_t ev = 0;
   for (int64_t item = static_cast<int64_t>(group) * (kJitTiledThreads / 32) + warp;
        item < n_items; item += NW) {
-    const uint32_t row = static_cast<uint32_t>(a.active[item / s.n_seg]);
+    const uint32_t row = static_cast<uint32_t>(VEC ? item / s.n_seg : a.active[item / s.n_seg]);
+    float vr = 1.f;
+    if (VEC) {
+      vr = __ldg(a.v + row);
+      if (vr == 0.f) continue;                                  // contributes nothing
+    }
     const uint32_t seg = s.seg_first + static_cast<uint32_t>(item % s.n_seg);
     const uint32_t seg_begin = seg * s.L;
     const uint32_t seg_end = min(seg_begin + s.L, a.n_cols);
@@ -120,7 +132,7 @@ __global__ void __launch_bounds__(kJitTiledThreads, 1) k_jit_tiled(JitTiledArgs 
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           if (pos[k] >= g0 && pos[k] < stop) {
-            add(pos[k], w[k]);
+            add(pos[k], w[k], vr);
             ++ev;
           }
         }

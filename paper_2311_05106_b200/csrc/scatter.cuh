@@ -416,6 +416,8 @@ struct JitSide {
 
 struct JitScatterArgs {
   JitSide e, i;
+  const float *v;              // nullable: non-event product, every row, v[r] * w (MV1)
+  int64_t n_rows;
   int64_t split;
   uint32_t n_seg_max;
   uint32_t n_cols, col_begin, col_end;
@@ -444,8 +446,18 @@ __device__ __forceinline__ JitSide pick(bool second, const JitSide &x,
 
 template <int LAW, int KIND>
 __device__ __forceinline__ void jit_emit(const JitSide &s, uint32_t pos,
-                                         uint32_t col_begin, float w, uint64_t pol) {
+                                         uint32_t col_begin, float w, uint64_t pol,
+                                         const float *v, float vr) {
   const int64_t c = static_cast<int64_t>(pos) - col_begin;
+  if (v) {                     // MV1: fl32(v w), or the exact product rounded once
+    if (KIND == 0) add_f32(s.out, c, __fmul_rn(vr, w), pol);
+    else
+      add_fix(s.out, c,
+              __double2ll_rn(__dmul_rn(static_cast<double>(vr), static_cast<double>(w)) *
+                             4294967296.0),
+              pol);
+    return;
+  }
   if (KIND == 0) add_f32(s.out, c, w, pol);
   else add_fix(s.out, c, LAW == 0 ? s.q : quantize(w), pol);
 }
@@ -453,7 +465,7 @@ __device__ __forceinline__ void jit_emit(const JitSide &s, uint32_t pos,
 template <int LAW, int KIND>
 __global__ void __launch_bounds__(kScatterThreads)
 k_jit_scatter(JitScatterArgs a) {
-  const int n_active = *a.count;
+  const int n_active = a.v ? 0 : *a.count;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (a.zero_count) *a.zero_count = 0;
     if (a.spikes) atomicAdd(a.spikes, static_cast<unsigned long long>(n_active));
@@ -461,11 +473,13 @@ k_jit_scatter(JitScatterArgs a) {
   const uint32_t lane = threadIdx.x & 31;
   const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const int64_t n_items = static_cast<int64_t>(n_active) * a.n_seg_max;
+  const int64_t n_items = (a.v ? a.n_rows : static_cast<int64_t>(n_active)) * a.n_seg_max;
   const uint64_t pol = make_policies(a.keep_frac).keep;
   unsigned long long ev = 0;
   for (int64_t item = warp0; item < n_items; item += n_warps) {
-    const int64_t r = a.active[item / a.n_seg_max];
+    const int64_t r = a.v ? item / a.n_seg_max : a.active[item / a.n_seg_max];
+    const float vr = a.v ? __ldg(a.v + r) : 1.f;
+    if (a.v && vr == 0.f) continue;                // contributes nothing
     const uint32_t sidx = static_cast<uint32_t>(item % a.n_seg_max);
     const bool inh = r >= a.split;
     const JitSide s = pick(inh, a.e, a.i);
@@ -512,7 +526,7 @@ k_jit_scatter(JitScatterArgs a) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           if (pos[k] < seg_end && pos[k] >= a.col_begin && pos[k] < a.col_end) {
-            jit_emit<LAW, KIND>(s, pos[k], a.col_begin, w[k], pol);
+            jit_emit<LAW, KIND>(s, pos[k], a.col_begin, w[k], pol, a.v, vr);
             ++ev;
           }
         }

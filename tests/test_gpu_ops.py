@@ -340,3 +340,61 @@ def test_hh_step_bit_exact(bp, orc, n, fixed):
         for k in ("v", "m", "h", "n"):
             assert np.array_equal(dev[k].cpu().numpy().view(np.uint32), st[k].view(np.uint32)), k
         assert np.array_equal(inputs.unpack_bits(spikes.cpu().numpy().view(np.uint32), n), ev)
+
+
+# ------------------------------------------------------ NEXT 1: non-event mv
+MV_CASES = [
+    # n_rows, n_cols, p, seg_len
+    (500, 3000, 0.05, 0),
+    (300, 100_000, 0.05, 0),          # config-2 row shape, 2 column tiles
+    (200, 300_000, 0.005, 0),         # many tiles, rows spanning them
+    (150, 240_000, 0.01, 40_000),     # segments shorter than a tile
+    (64, 37, 1.0, 0),                 # K = 1: dense
+]
+
+
+@pytest.mark.parametrize("path", ["tiled", "direct"])
+@pytest.mark.parametrize("case", MV_CASES)
+@pytest.mark.parametrize("law", ["homo", "uniform", "normal"])
+def test_jitconn_mv(bp, orc, case, law, path, monkeypatch):
+    """mv_prob_* (reading MV1) against the oracle: fixed point bit-exact
+    (normal weights: libm-level differences allowed), fp32 within rule T2."""
+    monkeypatch.setenv("BP_JIT_DIRECT" if path == "direct" else "BP_JIT_TILED", "1")
+    n_rows, n_cols, p, seg_len = case
+    w0, w1 = {"homo": (0.6, 0.0), "uniform": (-0.1, 0.2), "normal": (0.0, 0.3)}[law]
+    seed = 0xABC + n_rows
+    L = seg_len or n_cols
+    ospec = orc.JitSpec(seed, orc.conn_len(p), L, orc.LAWS[law], w0, w1)
+    spec = bp.jitconn_spec(seed, p, 0, seg_len)
+    rng = np.random.default_rng(n_rows)
+    v = rng.normal(0.0, 2.0, n_rows).astype(np.float32)
+    v[rng.random(n_rows) < 0.3] = 0.0                 # skipped rows
+    tv = _t(v)
+    out = torch.zeros(n_cols, dtype=torch.int64, device="cuda")
+    code = {"homo": bp.LAW_HOMO, "uniform": bp.LAW_UNIFORM, "normal": bp.LAW_NORMAL}[law]
+    bp.jitconn_mv(code, spec, w0, w1, tv, n_rows, n_cols, out)
+    want = orc.jit_mv(ospec, n_rows, n_cols, v, out_kind=orc.OUT_FIX)
+    got = out.cpu().numpy()
+    if law == "normal":
+        diff = np.abs(got - want)
+        assert np.mean(diff != 0) < 1e-3
+        assert np.all(diff <= 2 ** 32 * 2.0 ** -22 * (abs(w1) * 6 + 1) * np.abs(v).max())
+    else:
+        assert np.array_equal(got, want)
+    out32 = torch.zeros(n_cols, dtype=torch.float32, device="cuda")
+    bp.jitconn_mv(code, spec, w0, w1, tv, n_rows, n_cols, out32)
+    ref, absw = orc.jit_mv(ospec, n_rows, n_cols, v, out_kind=orc.OUT_F64, with_abs=True)
+    err = np.abs(out32.cpu().numpy().astype(np.float64) - ref)
+    assert np.all(err <= 1e-5 * absw + 1e-6 * (law == "normal") * absw + 1e-30)
+
+
+def test_jitconn_mv_binary_vector_equals_event_mv(bp):
+    """v in {0, 1}: the non-event product is the event scatter, bit for bit."""
+    n_rows, n_cols = 400, 100_000
+    spec = bp.jitconn_spec(99, 0.05)
+    ev = inputs.spike_pattern(n_rows, 0.2, seed=3)
+    a = torch.zeros(n_cols, dtype=torch.int64, device="cuda")
+    b = torch.zeros(n_cols, dtype=torch.int64, device="cuda")
+    bp.jitconn_event_mv_uniform(spec, -0.3, 0.3, _dev_spikes(ev), n_rows, n_cols, a)
+    bp.jitconn_mv(bp.LAW_UNIFORM, spec, -0.3, 0.3, _t(ev.astype(np.float32)), n_rows, n_cols, b)
+    assert torch.equal(a, b)
