@@ -564,7 +564,15 @@ def run_micro(args):
     else:
         fn = {"homo": bp.jitconn_event_mv_homo, "uniform": bp.jitconn_event_mv_uniform,
               "normal": bp.jitconn_event_mv_normal}[law]
-        if law == "homo":
+        if kind == "jitmv_vec":
+            # non-event mv_prob_* (NEXT 1): a float vector whose non-zeros sit
+            # on the same Bernoulli patterns (density = fraction of non-zeros)
+            code = {"homo": bp.LAW_HOMO, "uniform": bp.LAW_UNIFORM, "normal": bp.LAW_NORMAL}[law]
+            rng = np.random.default_rng(11)
+            spikes = [torch.from_numpy((e * rng.normal(0.0, 1.0, n)).astype(np.float32)).to(dev)
+                      for e in pats]
+            call = lambda vv: bp.jitconn_mv(code, spec, w0, w1, vv, n, n, out, ws=ws)
+        elif law == "homo":
             call = lambda s: fn(spec, w0, s, n, n, out, ws=ws)
         else:
             call = lambda s: fn(spec, w0, w1, s, n, n, out, ws=ws)
@@ -603,7 +611,8 @@ def run_micro(args):
         per_call = (events / args.steps) * bytes_per_event + 16 * active + n / 8 + \
             n * out.element_size()
         achieved = per_call / (total_ms / args.steps / 1e3) / 1e9
-        roof = {"kernel": "k_compact + k_csr_scatter", "bound": "hbm", "achieved": achieved,
+        roof = {"kernel": "k_compact + k_csr_stream (split plan precomputed)" if not args.no_plan
+                else "k_compact + k_csr_split + k_csr_stream", "bound": "hbm", "achieved": achieved,
                 "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                 "traffic": None, "peak_source": peak_kind,
                 "algorithmic_bytes_per_launch": per_call}
@@ -611,7 +620,8 @@ def run_micro(args):
         sm_mhz = clocks.get("sm_mhz") or 1965.0
         peak_ops = 148 * 4 * 32 * sm_mhz * 1e6
         ops = JIT_OPS_PER_EVENT[law] * events / (total_ms / 1e3)
-        roof = {"kernel": "k_compact + k_jit_scatter<%s>" % law, "bound": "alu",
+        roof = {"kernel": "%sk_jit_tiled<%s> (k_jit_scatter for rows < 1000 events, normal law)"
+                % ("" if kind == "jitmv_vec" else "k_compact + ", law), "bound": "alu",
                 "achieved": ops / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s (int32 lane ops)",
                 "frac": ops / peak_ops, "traffic": None,
                 "peak_source": "derived: 148 SMs x 4 schedulers x 32 lanes x sampled SM clock",
@@ -646,7 +656,7 @@ def main():
     ap.add_argument("--f32", action="store_true", help="alias of --g f32")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
-    ap.add_argument("--workload", choices=list(NETWORKS) + ["csrmv", "jitmv"],
+    ap.add_argument("--workload", choices=list(NETWORKS) + ["csrmv", "jitmv", "jitmv_vec"],
                     default="coba_lif_jit")
     ap.add_argument("--p", type=float, default=0.05, help="microbench connection probability")
     ap.add_argument("--density", type=float, default=0.1, help="microbench spike density")
@@ -664,7 +674,7 @@ def main():
         args.g = "f32"
     if args.impl == "reference":
         run_reference(args)
-    elif args.workload in ("csrmv", "jitmv"):
+    elif args.workload in ("csrmv", "jitmv", "jitmv_vec"):
         run_micro(args)
     else:
         run_ours(args)
