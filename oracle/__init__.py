@@ -292,17 +292,24 @@ class Projection:
 
 def run_network(model: str, params, state: dict, proj_e: Projection,
                 proj_i: Projection, n_steps: int, col_begin: int = 0,
-                col_end: int | None = None, record=True):
+                col_end: int | None = None, record=True, delay: int = 1):
     """Rule S1, for n = 0 .. n_steps-1:
-        1. read spikes_{n-1} (state['spikes'], all false at n = 0)
+        1. read spikes_{n-D} (D = delay steps, reading D1; D = 1 is the
+           paper's one-step VarDelay, P:971/P:988/P:991)
         2. E rows add into g_E and I rows into g_I (a2/a4)
         3. neuron rule N1 (LIF) or H1 (HH) -> spikes_n
         4. store spikes_n
     `state` holds numpy arrays (v, g_e, g_i, ref | m, h, n) over the
-    postsynaptic columns [col_begin, col_end) and 'spikes' (uint8, all N).
+    postsynaptic columns [col_begin, col_end) and 'spikes' (uint8, all N):
+    spikes_{-1} on entry (spikes_{-2}, ..., spikes_{-D} are empty unless
+    state['history'] holds them, oldest first), spikes_{n_steps-1} on exit.
     g dtype int64 selects fixed point (rule F1), float32 selects fp32.
     Returns the raster (n_steps x N uint8) when record, else spike counts.
     """
+    assert delay >= 1
+    hist = state.get("history")
+    if delay == 1 or hist is None or len(hist) != delay:
+        hist = [np.zeros_like(state["spikes"]) for _ in range(delay - 1)] + [state["spikes"]]
     n_total = state["spikes"].shape[0]
     if col_end is None:
         col_end = n_total
@@ -313,7 +320,7 @@ def run_network(model: str, params, state: dict, proj_e: Projection,
     raster = np.zeros((n_steps, col_end - col_begin), np.uint8) if record else None
     counts = np.zeros(n_steps, np.int64)
     for step in range(n_steps):
-        spikes = state["spikes"]
+        spikes = hist[0]
         for proj, g in ((proj_e, state["g_e"]), (proj_i, state["g_i"])):
             ev = spikes[proj.row0:proj.row0 + proj.n_rows]
             homo_f32 = f32 and (proj.jit is not None and proj.jit.law == LAW_HOMO
@@ -356,7 +363,9 @@ def run_network(model: str, params, state: dict, proj_e: Projection,
         new = np.zeros(n_total, np.uint8)
         new[col_begin:col_end] = local
         state["spikes"] = new
+        hist = hist[1:] + [new]
         counts[step] = int(local.sum())
         if record:
             raster[step] = local
+    state["history"] = hist
     return raster if record else counts

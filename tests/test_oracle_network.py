@@ -170,3 +170,51 @@ def test_hh_network_runs_finite(orc, fixed):
     raster = orc.run_network("hh", orc.hh_params(), state, pe, pi, 300)
     assert np.all(np.isfinite(state["v"]))
     assert raster.sum() > 0
+
+
+# ---------------------------------------------------------------- reading D1
+@pytest.mark.parametrize("delay", [1, 3, 8])
+def test_delay_single_spike_arrives_after_d_steps(orc, delay):
+    """One presynaptic spike in spikes_{-1}, a network that stays silent on
+    its own: the spike's targets receive w at step D-1 (0-based) and decay
+    afterwards; nothing arrives before.  Fixed point (F1) makes it exact."""
+    n, T = 400, 12
+    state, pe, pi = _coba(orc, n=n)
+    state["v"][:] = -60.0                    # rest: first own spike after 139 steps
+    state["spikes"][:] = 0
+    state["spikes"][5] = 1                   # excitatory row 5
+    targets = orc.jit_row(pe.jit, n, 5)[0]
+    for t_end in (delay - 1, delay, T):      # before / just after / well after delivery
+        st = {k: (v.copy() if hasattr(v, "copy") else v) for k, v in state.items()}
+        raster = orc.run_network("lif", orc.lif_params(), st, pe, pi, t_end, delay=delay)
+        assert raster.sum() == 0
+        g = st["g_e"]
+        if t_end < delay:
+            assert not g.any()
+            continue
+        # delivered at step delay-1, then decayed (t_end - delay + 1) times
+        # by rule F1: g <- llrint(g * alpha_E) in fp64
+        alpha = math.exp(-0.1 / 5.0)
+        want = int(orc.quantize(np.float32(0.6)))
+        for _ in range(t_end - delay + 1):
+            want = int(np.rint(np.float64(want) * alpha))
+        assert np.all(g[targets] == want), (t_end, g[targets][:3], want)
+        others = np.setdiff1d(np.arange(n), targets)
+        assert not g[others].any()
+
+
+def test_delay_one_equals_default_and_history_continues(orc):
+    """delay = 1 is rule S1; a delayed run split in two calls equals one call."""
+    n, T = 2000, 120
+    s1, pe, pi = _coba(orc, n=n)
+    r1 = orc.run_network("lif", orc.lif_params(), s1, pe, pi, T)
+    s2, _, _ = _coba(orc, n=n)
+    r2 = orc.run_network("lif", orc.lif_params(), s2, pe, pi, T, delay=1)
+    assert np.array_equal(r1, r2)
+    s3, _, _ = _coba(orc, n=n)
+    ra = orc.run_network("lif", orc.lif_params(), s3, pe, pi, 50, delay=4)
+    rb = orc.run_network("lif", orc.lif_params(), s3, pe, pi, T - 50, delay=4)
+    s4, _, _ = _coba(orc, n=n)
+    rc = orc.run_network("lif", orc.lif_params(), s4, pe, pi, T, delay=4)
+    assert np.array_equal(np.vstack([ra, rb]), rc)
+    assert not np.array_equal(rc, r1)        # the delay changes the dynamics
