@@ -278,7 +278,10 @@ typedef struct {
   int32_t model;  /* bp_model */
   int32_t conn;   /* bp_conn  */
   int32_t g_kind; /* bp_out_kind of state.g_exc / g_inh */
-  int32_t reserved;
+  int32_t delay_steps; /* synaptic delay D in steps (0 => 1, the paper's one-step
+                          VarDelay); spikes of step n are delivered at
+                          step n + D (reading D1); <= 16.
+                          D > 1 keeps D + 1 bucket slots. */
   int64_t n, n_exc;
   int64_t col_begin, col_end;
   bp_jitconn jit_exc, jit_inh; /* conn == BP_CONN_JIT                       */

@@ -69,7 +69,7 @@ class NeuronState(ctypes.Structure):
 
 class NetworkDesc(ctypes.Structure):
     _fields_ = [("model", ctypes.c_int32), ("conn", ctypes.c_int32),
-                ("g_kind", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("g_kind", ctypes.c_int32), ("delay_steps", ctypes.c_int32),
                 ("n", ctypes.c_int64), ("n_exc", ctypes.c_int64),
                 ("col_begin", ctypes.c_int64), ("col_end", ctypes.c_int64),
                 ("jit_exc", JitConn), ("jit_inh", JitConn),
@@ -380,10 +380,11 @@ class Network:
 
     def __init__(self, *, model, conn, n, n_exc, state: dict, spikes, params,
                  col_begin=0, col_end=None, jit_exc=None, jit_inh=None,
-                 w_exc=0.6, w_inh=6.7, csr_exc=None, csr_inh=None, stream=None):
+                 w_exc=0.6, w_inh=6.7, csr_exc=None, csr_inh=None, stream=None, delay=1):
         col_end = n if col_end is None else col_end
         d = NetworkDesc()
         d.model, d.conn = model, conn
+        d.delay_steps = int(delay)
         d.g_kind = _out_kind(state["g_e"])
         d.n, d.n_exc, d.col_begin, d.col_end = n, n_exc, col_begin, col_end
         if jit_exc is not None:

@@ -161,6 +161,8 @@ CsrPlan csr_plan(int64_t n_rows, int64_t n_cols, int out_kind, int sms) {
 // Streamed CSR plan (csr_stream.cuh): column tiles sized to the shared
 // memory left after the bulk-copy stages; one CTA per SM.
 constexpr size_t kSmemOptin = 232448;     // 227 KB dynamic shared memory per block
+constexpr int kMaxDelay = 16;             // synaptic delay steps (reading D1)
+constexpr int kMaxSlots = kMaxDelay + 1;
 constexpr int kStreamMaxTiles = 16;
 
 struct StreamPlan {
@@ -952,9 +954,11 @@ struct bp_network {
   float keep_frac = 0.f;          // L2 evict_last fraction of g (cache.cuh)
   // fused-step event buckets (step.cuh), two parities, owned by the network
   uint32_t n_tiles = 0, cap = 0;
-  bp::Buckets bk[2] = {};
+  bp::Buckets bk[kMaxSlots] = {};  // ring of delay + 1 slots (reading D1)
   void *bk_mem = nullptr;
-  int bpar = 0;                   // bucket parity holding the next step's input
+  int delay = 1;                  // synaptic delay in steps (desc.delay_steps)
+  int slots = 2;                  // bucket ring: step n reads slot n % slots and its
+                                  // spikes are binned into slot (n + delay) % slots
   int64_t steps_done = 0;
   bp::ConnArgs conn{};
   // small networks (step.cuh k_small_net): whole time loop in one CTA
@@ -991,6 +995,8 @@ bp_status validate_network(const bp_network_desc *d) {
   BP_CHECK(d->spikes != nullptr && aligned(d->spikes, 4), BP_ERR_INVALID_ARG,
            "spikes NULL/misaligned");
   BP_CHECK(d->params.model == d->model, BP_ERR_INVALID_ARG, "params.model != model");
+  BP_CHECK(d->delay_steps >= 0 && d->delay_steps <= kMaxDelay, BP_ERR_INVALID_ARG,
+           "delay_steps %d not in [0, %d]", d->delay_steps, kMaxDelay);
   BP_CHECK(d->state.g_kind == d->g_kind, BP_ERR_INVALID_ARG, "state.g_kind != g_kind");
   if (d->conn == BP_CONN_CSR) {
     BP_CHECK(d->n_exc == 0 || (d->exc_indptr && d->exc_indices), BP_ERR_INVALID_ARG,
@@ -1076,12 +1082,13 @@ bp_status alloc_buckets(bp_network *net, cudaStream_t st) {
   const size_t spill_b = round_up(2 * static_cast<size_t>(net->n_local) * sizeof(int32_t), 256);
   const size_t per = 2 * cnt_b + buf_b + spill_b;     // cnt, flag, buf, spill
   const size_t small_b = round_up((static_cast<size_t>(net->n_local) + 64) * sizeof(int32_t), 256);
-  BP_CUDA(cudaMalloc(&net->bk_mem, 2 * per + small_b));
-  net->small_count = reinterpret_cast<int32_t *>(static_cast<char *>(net->bk_mem) + 2 * per);
+  const size_t R = static_cast<size_t>(net->slots);
+  BP_CUDA(cudaMalloc(&net->bk_mem, R * per + small_b));
+  net->small_count = reinterpret_cast<int32_t *>(static_cast<char *>(net->bk_mem) + R * per);
   net->small_active = net->small_count + 64;
   BP_CUDA(cudaMemsetAsync(net->small_count, 0, sizeof(int32_t), st));
   char *m = static_cast<char *>(net->bk_mem);
-  for (int p = 0; p < 2; ++p) {
+  for (int p = 0; p < net->slots; ++p) {
     char *b = m + p * per;
     net->bk[p].cnt = reinterpret_cast<int32_t *>(b);
     net->bk[p].flag = reinterpret_cast<int32_t *>(b + cnt_b);
@@ -1183,11 +1190,13 @@ bp_status launch_step(bp_network *net, uint32_t *raster, cudaStream_t st,
   const bp_network_desc &d = net->d;
   bp::StepArgs a = step_args(net);
   a.nrn.raster = raster;
-  a.in = net->bk[net->bpar];
-  a.out = bin_target(net, net->bpar ^ 1);
+  const int in_slot = static_cast<int>(net->steps_done % net->slots);
+  const int out_slot = static_cast<int>((net->steps_done + net->delay) % net->slots);
+  a.in = net->bk[in_slot];
+  a.out = bin_target(net, out_slot);
   a.reverse = static_cast<int>(net->steps_done & 1);
   a.step_spikes = step_spikes;
-  const int out_par = net->bpar ^ 1;
+  const int out_par = out_slot;
   // ping-pong list counters: this step appends at count[2 + p] and zeroes
   // count[2 + (p ^ 1)] for the next step (its reader finished last step)
   const int cp = static_cast<int>(net->steps_done & 1);
@@ -1209,7 +1218,6 @@ bp_status launch_step(bp_network *net, uint32_t *raster, cudaStream_t st,
   if (mid) BP_CUDA(cudaEventRecord(mid, st));
   s = launch_bin(net, net->active[1], net->count + 2 + cp, out_par, net->n_local, st);
   if (s != BP_OK) return s;
-  net->bpar = out_par;
   net->steps_done += 1;
   return BP_OK;
 }
@@ -1305,6 +1313,8 @@ bp_status bp_network_create(const bp_network_desc *desc, bp_stream stream,
   BP_CHECK(net != nullptr, BP_ERR_INVALID_ARG, "out of host memory");
   net->d = *desc;
   net->sms = sms;
+  net->delay = desc->delay_steps > 0 ? desc->delay_steps : 1;
+  net->slots = net->delay + 1;
   net->n_local = desc->col_end - desc->col_begin;
   net->local_words = (net->n_local + 31) / 32;
   net->global_words = (desc->n + 31) / 32;
@@ -1364,11 +1374,12 @@ bp_status bp_network_create(const bp_network_desc *desc, bp_stream stream,
   // the local part of the initial spike vector (spikes_{-1}) is delivered
   // into the first step; remote parts arrive through bp_network_scatter
   if (s == BP_OK)
-    s = bin_spike_range(net, desc->col_begin / 32, (desc->col_end + 31) / 32, net->bpar, st);
+    s = bin_spike_range(net, desc->col_begin / 32, (desc->col_end + 31) / 32,
+                        (net->delay - 1) % net->slots, st);
   // one device, whole network, state fits one CTA's shared memory: the
   // single-CTA time loop (k_small_net) drives bp_network_step
   net->small = s == BP_OK && desc->col_begin == 0 && desc->col_end == desc->n &&
-               desc->n <= bp::kSmallMax && !std::getenv("BP_NO_SMALL_NET");
+               desc->n <= bp::kSmallMax && net->delay == 1 && !std::getenv("BP_NO_SMALL_NET");
   if (net->small) {
     launch_compact(desc->spikes, desc->n, net->small_active, net->small_count, sms, st);
     s = launched();
@@ -1459,9 +1470,12 @@ bp_status bp_network_scatter(bp_network *net, bp_stream stream) {
   // spikes were binned by the update that produced them.
   const int64_t lw0 = net->d.col_begin / 32;
   const int64_t lw1 = (net->d.col_end + 31) / 32;
-  s = bin_spike_range(net, 0, lw0, net->bpar, st);
+  // the exchanged spikes are those of step steps_done - 1: delivered at
+  // step steps_done - 1 + delay
+  const int slot = static_cast<int>((net->steps_done + net->delay - 1) % net->slots);
+  s = bin_spike_range(net, 0, lw0, slot, st);
   if (s != BP_OK) return s;
-  return bin_spike_range(net, lw1, net->global_words, net->bpar, st);
+  return bin_spike_range(net, lw1, net->global_words, slot, st);
 }
 
 bp_status bp_network_update(bp_network *net, uint32_t *raster_row, bp_stream stream) {

@@ -93,7 +93,7 @@ class CobaNetwork:
                  w_exc: float | None = None, w_inh: float | None = None,
                  seed_e: int = SEED_E, seed_i: int = SEED_I, v0=None,
                  init_seed: int = inputs.V0_SEED, spikes: torch.Tensor | None = None,
-                 frac_bits: int | None = None):
+                 frac_bits: int | None = None, delay: int = 1):
         device = torch.device(device or "cuda")
         self.n = n
         self.n_exc = n * 4 // 5
@@ -153,7 +153,8 @@ class CobaNetwork:
                              conn=B.CONN_JIT if conn == "jit" else B.CONN_CSR,
                              n=n, n_exc=self.n_exc, state=st, spikes=self.spikes,
                              params=params, col_begin=lo, col_end=hi,
-                             w_exc=w_exc, w_inh=w_inh, **kw)
+                             w_exc=w_exc, w_inh=w_inh, delay=delay, **kw)
+        self.delay = delay
         self._send = None
 
     # single device: the whole loop runs in the library

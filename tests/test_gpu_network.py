@@ -192,3 +192,40 @@ def test_step_counts_out(orc):
     torch.cuda.synchronize()
     got = _raster(raster, n).sum(axis=1)
     assert np.array_equal(counts.numpy(), got)
+
+
+# ---------------------------------------------------- NEXT 2: synaptic delays
+@pytest.mark.parametrize("mode", ["fix64", "f32"])
+@pytest.mark.parametrize("delay", [2, 5, 16])
+@pytest.mark.parametrize("n,steps", [(4000, 600), (20_000, 300)])
+def test_coba_lif_delay_bit_exact(orc, n, steps, delay, mode):
+    """Reading D1: spikes of step n arrive at step n + D (D + 1 bucket slots)."""
+    net = CobaNetwork(n, conn="jit", fixed={"fix64": True, "f32": False}[mode], delay=delay)
+    raster = torch.zeros((steps, (n + 31) // 32), dtype=torch.int32, device="cuda")
+    net.run(steps // 3, raster[:steps // 3])               # two calls: the ring carries over
+    net.run(steps - steps // 3, raster[steps // 3:])
+    st, pe, pi = _oracle_lif(orc, n, {"fix64": True, "f32": False}[mode])
+    want = orc.run_network("lif", orc.lif_params(), st, pe, pi, steps, delay=delay)
+    assert want.sum() > 0
+    assert np.array_equal(_raster(raster, n), want)
+    assert np.array_equal(net.state["v"].cpu().numpy().view(np.uint32), st["v"].view(np.uint32))
+    assert np.array_equal(net.state["g_e"].cpu().numpy().view(np.uint32 if mode == "f32" else np.int64),
+                          st["g_e"].view(np.uint32 if mode == "f32" else np.int64))
+
+
+def test_delay_partitions_emulated_equal_whole(orc):
+    """Delayed network over 4 postsynaptic partitions (exchange emulated by a
+    shared spike vector) equals the single partition bit for bit."""
+    n, steps, world, delay = 4096, 200, 4, 3
+    whole = CobaNetwork(n, conn="jit", fixed=True, seg_len=1024, delay=delay)
+    whole.run(steps)
+    shared = torch.zeros(n // 32, dtype=torch.int32, device="cuda")
+    parts = [CobaNetwork(n, conn="jit", fixed=True, seg_len=1024, rank=r, world=world,
+                         spikes=shared, delay=delay) for r in range(world)]
+    for _ in range(steps):
+        for q in parts:
+            q.net.scatter()
+        for q in parts:
+            q.net.update()
+    v = np.concatenate([q.state["v"].cpu().numpy() for q in parts])
+    assert np.array_equal(v.view(np.uint32), whole.state["v"].cpu().numpy().view(np.uint32))
