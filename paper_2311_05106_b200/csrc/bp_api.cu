@@ -968,6 +968,9 @@ struct bp_network {
   int32_t *small_steps = nullptr;    // per-step spike counts scratch
   int64_t small_steps_cap = 0;
   int64_t prof_steps = 0;
+  // dense delivery: events as per-neuron atomic counts (cap 0), small
+  // blocks (k_step_dense) -- compute-bound networks that fill few tiles
+  bool dense = false;
 };
 
 namespace {
@@ -1075,6 +1078,7 @@ bp_status alloc_buckets(bp_network *net, cudaStream_t st) {
   uint32_t cap = static_cast<uint32_t>(round_up(static_cast<size_t>(expect) + 1024, 1024));
   if (const char *env = std::getenv("BP_BUCKET_CAP")) cap = static_cast<uint32_t>(std::atoi(env));
   if (cap < 1) cap = 1;
+  if (net->dense) cap = 0;               // every event straight into the dense counts
   net->cap = cap;
   const size_t cnt_b = round_up(static_cast<size_t>(net->n_tiles) * bp::kCntStride *
                                     sizeof(int32_t), 256);
@@ -1124,7 +1128,8 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, size_t sme
 bp_status launch_bin(bp_network *net, const int32_t *active, const int32_t *count, int par,
                      int64_t max_rows, cudaStream_t st) {
   const size_t smem = (2 * static_cast<size_t>(bp::kBinStage) + 2 * net->n_tiles) * 4;
-  if (net->n_tiles <= 8192 && smem <= 200 * 1024 && !std::getenv("BP_BIN_PER_EVENT")) {
+  if (!net->dense && net->n_tiles <= 8192 && smem <= 200 * 1024 &&
+      !std::getenv("BP_BIN_PER_EVENT")) {
     static bool attr_set = false;
     if (!attr_set) {
       BP_CUDA(cudaFuncSetAttribute(bp::k_bin_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1204,7 +1209,19 @@ bp_status launch_step(bp_network *net, uint32_t *raster, cudaStream_t st,
   a.active_count = net->count + 2 + cp;
   a.zero_count = net->count + 2 + (cp ^ 1);
   const int grid = static_cast<int>(net->n_tiles);
-  if (d.model == BP_MODEL_LIF) {
+  if (net->dense) {
+    const int dgrid = static_cast<int>((net->n_local + 4 * bp::kDenseThreads - 1) /
+                                       (4 * bp::kDenseThreads));
+    if (d.model == BP_MODEL_LIF) {
+      if (d.g_kind == BP_OUT_FIX64) BP_CUDA(launch_pdl(bp::k_step_dense<0, 1>, dgrid, bp::kDenseThreads, 0, st, a));
+      else if (d.g_kind == BP_OUT_FIX32) BP_CUDA(launch_pdl(bp::k_step_dense<0, 2>, dgrid, bp::kDenseThreads, 0, st, a));
+      else BP_CUDA(launch_pdl(bp::k_step_dense<0, 0>, dgrid, bp::kDenseThreads, 0, st, a));
+    } else {
+      if (d.g_kind == BP_OUT_FIX64) BP_CUDA(launch_pdl(bp::k_step_dense<1, 1>, dgrid, bp::kDenseThreads, 0, st, a));
+      else if (d.g_kind == BP_OUT_FIX32) BP_CUDA(launch_pdl(bp::k_step_dense<1, 2>, dgrid, bp::kDenseThreads, 0, st, a));
+      else BP_CUDA(launch_pdl(bp::k_step_dense<1, 0>, dgrid, bp::kDenseThreads, 0, st, a));
+    }
+  } else if (d.model == BP_MODEL_LIF) {
     if (d.g_kind == BP_OUT_FIX64) BP_CUDA(launch_pdl(bp::k_step<0, 1>, grid, bp::kStepThreads, 0, st, a));
     else if (d.g_kind == BP_OUT_FIX32) BP_CUDA(launch_pdl(bp::k_step<0, 2>, grid, bp::kStepThreads, 0, st, a));
     else BP_CUDA(launch_pdl(bp::k_step<0, 0>, grid, bp::kStepThreads, 0, st, a));
@@ -1315,6 +1332,14 @@ bp_status bp_network_create(const bp_network_desc *desc, bp_stream stream,
   net->sms = sms;
   net->delay = desc->delay_steps > 0 ? desc->delay_steps : 1;
   net->slots = net->delay + 1;
+  // dense delivery for the compute-bound HH model up to 2 M local neurons
+  // (counts stay L2-resident; 4096-neuron tiles would leave SMs idle);
+  // BP_DENSE=0/1 overrides
+  {
+    const char *env = std::getenv("BP_DENSE");
+    net->dense = env ? std::atoi(env) != 0
+                     : (desc->model == BP_MODEL_HH && net->n_local <= (int64_t{2} << 20));
+  }
   net->n_local = desc->col_end - desc->col_begin;
   net->local_words = (net->n_local + 31) / 32;
   net->global_words = (desc->n + 31) / 32;

@@ -91,8 +91,13 @@ __device__ __forceinline__ void bin_store(const BinTarget &b, uint32_t proj,
 }
 
 // Append one event (projection proj, local postsynaptic index loc).
+// Dense delivery (b.cap == 0): one atomic on the neuron's count.
 __device__ __forceinline__ void bin_event(const BinTarget &b, uint32_t proj,
                                           uint32_t loc) {
+  if (b.cap == 0) {
+    atomicAdd(b.out.spill + static_cast<size_t>(proj) * b.n_local + loc, 1);
+    return;
+  }
   const int slot = atomicAdd(b.out.cnt + (loc >> kTileShift) * kCntStride, 1);
   bin_store(b, proj, loc, slot);
 }
@@ -574,6 +579,61 @@ k_step(StepArgs a) {
   }
 
   // 3. counters
+  if (KIND == 2 && sat) atomicAdd(a.saturated, static_cast<unsigned long long>(sat));
+  my_sp = __reduce_add_sync(0xffffffffu, my_sp);
+  if (lane == 0 && my_sp) atomicAdd(&block_sp, static_cast<unsigned long long>(my_sp));
+  __syncthreads();
+  if (tid == 0 && block_sp) {
+    atomicAdd(a.spikes, block_sp);
+    if (a.step_spikes) atomicAdd(a.step_spikes, static_cast<int32_t>(block_sp));
+  }
+}
+
+// Dense delivery (small, compute-bound networks -- config 4's 400 k HH
+// neurons fill only 98 tiles of 4096): events arrive as per-neuron counts
+// (one global atomic each, bin_event with cap 0) and every block updates
+// DENSE_NT * 4 neurons in one pass, so the grid covers every SM.  The block
+// moves its neurons' counts into shared memory (and clears them) and then
+// runs the same pass code as k_step.
+constexpr int kDenseThreads = 128;
+
+template <int MODEL, int KIND>
+__global__ void __launch_bounds__(kDenseThreads, MODEL == 0 ? 8 : 4)
+k_step_dense(StepArgs a) {
+  __shared__ int32_t cnt_e[4 * kDenseThreads];
+  __shared__ int32_t cnt_i[4 * kDenseThreads];
+  __shared__ unsigned long long block_sp;
+  const int tid = threadIdx.x;
+  const uint32_t lane = tid & 31u;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * (4 * kDenseThreads);
+  const NeuronArgs &nr = a.nrn;
+  const Policies pol = make_policies(nr.keep_frac);
+  pdl_trigger();
+  pdl_wait();               // counts of the previous binning are final
+  Pass<MODEL, KIND> pa;
+  pass_load(pa, nr, base + 4 * tid, pol);
+  if (tid == 0) {
+    block_sp = 0;
+    if (blockIdx.x == 0 && a.zero_count) *a.zero_count = 0;
+  }
+  for (int j = tid; j < 4 * kDenseThreads; j += kDenseThreads) {
+    const int64_t i = base + j;
+    int32_t ce = 0, ci = 0;
+    if (i < nr.n) {
+      int32_t *se = a.in.spill + i;
+      int32_t *si = a.in.spill + a.out.n_local + i;
+      ce = *se;
+      ci = *si;
+      if (ce) *se = 0;
+      if (ci) *si = 0;
+    }
+    cnt_e[j] = ce;
+    cnt_i[j] = ci;
+  }
+  __syncthreads();
+  uint32_t my_sp = 0, sat = 0;
+  const uint32_t nib = pass_update(pa, a, cnt_e, cnt_i, 4 * tid, base + 4 * tid, pol, sat);
+  pass_emit(a, nib, base, 0, my_sp);
   if (KIND == 2 && sat) atomicAdd(a.saturated, static_cast<unsigned long long>(sat));
   my_sp = __reduce_add_sync(0xffffffffu, my_sp);
   if (lane == 0 && my_sp) atomicAdd(&block_sp, static_cast<unsigned long long>(my_sp));

@@ -107,11 +107,16 @@ def test_coba_lif_f32_bit_exact(orc, n, steps):
     assert np.array_equal(net.state["v"].cpu().numpy().view(np.uint32), st["v"].view(np.uint32))
 
 
-@pytest.mark.parametrize("small", [True, False])
+@pytest.mark.parametrize("path", ["small", "dense", "tiles"])
 @pytest.mark.parametrize("fixed", ["fix64", "fix32", "f32"])
-def test_coba_hh_csr(orc, fixed, small, monkeypatch):
-    if not small:
+def test_coba_hh_csr(orc, fixed, path, monkeypatch):
+    """small: single-CTA loop; dense: per-neuron event counts + 512-neuron
+    blocks (the HH default beyond one CTA); tiles: 4096-neuron tiles with
+    event buckets."""
+    if path != "small":
         monkeypatch.setenv("BP_NO_SMALL_NET", "1")
+    if path == "tiles":
+        monkeypatch.setenv("BP_DENSE", "0")
     n, steps = 4000, 400
     orc.set_fix32_bits(16)
     n_exc = 3200
@@ -229,3 +234,18 @@ def test_delay_partitions_emulated_equal_whole(orc):
             q.net.update()
     v = np.concatenate([q.state["v"].cpu().numpy() for q in parts])
     assert np.array_equal(v.view(np.uint32), whole.state["v"].cpu().numpy().view(np.uint32))
+
+
+@pytest.mark.parametrize("mode", ["fix64", "f32"])
+def test_coba_lif_dense_delivery_bit_exact(orc, mode, monkeypatch):
+    """Dense delivery forced for the LIF network (ragged last block)."""
+    monkeypatch.setenv("BP_DENSE", "1")
+    n, steps = 20_001 - 20_001 % 32 + 32, 300
+    net = CobaNetwork(n, conn="jit", fixed={"fix64": True, "f32": False}[mode])
+    raster = torch.zeros((steps, (n + 31) // 32), dtype=torch.int32, device="cuda")
+    net.run(steps, raster)
+    st, pe, pi = _oracle_lif(orc, n, {"fix64": True, "f32": False}[mode])
+    want = orc.run_network("lif", orc.lif_params(), st, pe, pi, steps)
+    assert want.sum() > 0
+    assert np.array_equal(_raster(raster, n), want)
+    assert np.array_equal(net.state["v"].cpu().numpy().view(np.uint32), st["v"].view(np.uint32))
