@@ -1216,10 +1216,12 @@ bp_status launch_step(bp_network *net, uint32_t *raster, cudaStream_t st,
       if (d.g_kind == BP_OUT_FIX64) BP_CUDA(launch_pdl(bp::k_step_dense<0, 1>, dgrid, bp::kDenseThreads, 0, st, a));
       else if (d.g_kind == BP_OUT_FIX32) BP_CUDA(launch_pdl(bp::k_step_dense<0, 2>, dgrid, bp::kDenseThreads, 0, st, a));
       else BP_CUDA(launch_pdl(bp::k_step_dense<0, 0>, dgrid, bp::kDenseThreads, 0, st, a));
-    } else {
-      if (d.g_kind == BP_OUT_FIX64) BP_CUDA(launch_pdl(bp::k_step_dense<1, 1>, dgrid, bp::kDenseThreads, 0, st, a));
-      else if (d.g_kind == BP_OUT_FIX32) BP_CUDA(launch_pdl(bp::k_step_dense<1, 2>, dgrid, bp::kDenseThreads, 0, st, a));
-      else BP_CUDA(launch_pdl(bp::k_step_dense<1, 0>, dgrid, bp::kDenseThreads, 0, st, a));
+    } else {   // HH: one neuron per thread
+      const int64_t per_block = static_cast<int64_t>(bp::kHHThreads) * bp::kHHPerThread;
+      const int hgrid = static_cast<int>((net->n_local + per_block - 1) / per_block);
+      if (d.g_kind == BP_OUT_FIX64) BP_CUDA(launch_pdl(bp::k_hh_dense1<1>, hgrid, bp::kHHThreads, 0, st, a));
+      else if (d.g_kind == BP_OUT_FIX32) BP_CUDA(launch_pdl(bp::k_hh_dense1<2>, hgrid, bp::kHHThreads, 0, st, a));
+      else BP_CUDA(launch_pdl(bp::k_hh_dense1<0>, hgrid, bp::kHHThreads, 0, st, a));
     }
   } else if (d.model == BP_MODEL_LIF) {
     if (d.g_kind == BP_OUT_FIX64) BP_CUDA(launch_pdl(bp::k_step<0, 1>, grid, bp::kStepThreads, 0, st, a));

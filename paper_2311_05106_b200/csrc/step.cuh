@@ -644,6 +644,111 @@ k_step_dense(StepArgs a) {
   }
 }
 
+// HH with dense delivery: few neurons per thread.  The HH update is a long
+// dependent fp32 chain (~490 instructions per neuron); at 400 k neurons four
+// neurons per thread leave ~21 warps per SM and the per-warp chain sets the
+// time, so here a thread takes kHHPerThread neurons (the same rule H1 code and
+// count folding as the 4-wide pass, hence bit-identical results).
+constexpr int kHHThreads = 256;
+
+template <int KIND>
+__device__ __forceinline__ bool hh_dense_one(const StepArgs &a, int64_t i, uint32_t &sat) {
+  const NeuronArgs &nr = a.nrn;
+  int32_t *se = a.in.spill + i;
+  int32_t *si = a.in.spill + a.out.n_local + i;
+  const int32_t ce = *se, ci = *si;
+  if (ce) *se = 0;
+  if (ci) *si = 0;
+  float gEf, gIf;
+  if constexpr (KIND == 2) {
+    int32_t *pe = static_cast<int32_t *>(nr.g_e) + i;
+    int32_t *pi = static_cast<int32_t *>(nr.g_i) + i;
+    int32_t ge = *pe, gi = *pi;
+    gEf = g_fold32(ge, ce, a.q_e, nr.inv_scale32, sat);
+    gIf = g_fold32(gi, ci, a.q_i, nr.inv_scale32, sat);
+    g_after32(ge, nr.a_e_q);
+    g_after32(gi, nr.a_i_q);
+    *pe = ge;
+    *pi = gi;
+  } else if constexpr (KIND == 1) {
+    long long *pe = static_cast<long long *>(nr.g_e) + i;
+    long long *pi = static_cast<long long *>(nr.g_i) + i;
+    long long ge = *pe, gi = *pi;
+    gEf = g_fold(ge, ce, a.q_e);
+    gIf = g_fold(gi, ci, a.q_i);
+    g_after(ge, nr.alpha_e, 0.f);
+    g_after(gi, nr.alpha_i, 0.f);
+    *pe = ge;
+    *pi = gi;
+  } else {
+    float *pe = static_cast<float *>(nr.g_e) + i;
+    float *pi = static_cast<float *>(nr.g_i) + i;
+    float ge = *pe, gi = *pi;
+    gEf = g_fold(ge, ce, a.w_e);
+    gIf = g_fold(gi, ci, a.w_i);
+    g_after(ge, 0.0, nr.alpha_e32);
+    g_after(gi, 0.0, nr.alpha_i32);
+    *pe = ge;
+    *pi = gi;
+  }
+  float V = nr.v[i], M = nr.m[i], H = nr.h[i], Nk = nr.nk[i];
+  const bool spike = hh_one(nr, V, M, H, Nk, gEf, gIf);
+  nr.v[i] = V;
+  nr.m[i] = M;
+  nr.h[i] = H;
+  nr.nk[i] = Nk;
+  return spike;
+}
+
+// kHHPerThread neurons per thread, kHHThreads apart (measured at 400 k
+// neurons: 1 -> 14.7 us per step, 2 -> 16.4 us).
+constexpr int kHHPerThread = 1;
+
+template <int KIND>
+__global__ void __launch_bounds__(kHHThreads, 8) k_hh_dense1(StepArgs a) {
+  const NeuronArgs &nr = a.nrn;
+  const int64_t base = static_cast<int64_t>(blockIdx.x) * kHHThreads * kHHPerThread;
+  const uint32_t lane = threadIdx.x & 31u;
+  pdl_trigger();
+  pdl_wait();               // counts of the previous binning are final
+  if (blockIdx.x == 0 && threadIdx.x == 0 && a.zero_count) *a.zero_count = 0;
+  bool spike[kHHPerThread];
+  uint32_t sat = 0;
+#pragma unroll
+  for (int k = 0; k < kHHPerThread; ++k) {
+    const int64_t i = base + k * kHHThreads + threadIdx.x;
+    spike[k] = i < nr.n ? hh_dense_one<KIND>(a, i, sat) : false;
+  }
+#pragma unroll
+  for (int k = 0; k < kHHPerThread; ++k) {
+    // spike word of the warp's 32 neurons, active-list append, counters
+    const int64_t i = base + k * kHHThreads + threadIdx.x;
+    const uint32_t ballot = __ballot_sync(0xffffffffu, spike[k]);
+    const int64_t w0 = i - lane;
+    if (lane == 0 && w0 < nr.n) {
+      nr.spikes[w0 >> 5] = ballot;
+      if (nr.raster) nr.raster[w0 >> 5] = ballot;
+    }
+    if (ballot) {
+      const int c = __popc(ballot);
+      int slot = 0;
+      if (lane == 0) {
+        if (a.active) slot = atomicAdd(a.active_count, c);
+        atomicAdd(a.spikes, static_cast<unsigned long long>(c));
+        if (a.step_spikes) atomicAdd(a.step_spikes, c);
+      }
+      slot = __shfl_sync(0xffffffffu, slot, 0);
+      if (spike[k] && a.active)
+        a.active[slot + __popc(ballot & ((1u << lane) - 1u))] =
+            nr.active_base + static_cast<int32_t>(i);
+    }
+  }
+  if (KIND == 2) {
+    sat = __reduce_add_sync(0xffffffffu, sat);
+    if (lane == 0 && sat) atomicAdd(a.saturated, static_cast<unsigned long long>(sat));
+  }
+}
+
 // Remote (or initial) spikes: bin the events of every active row in
 // `active[0..*count)` whose targets fall in this partition.
 __global__ void __launch_bounds__(kScatterThreads)
