@@ -167,7 +167,10 @@ __global__ void __launch_bounds__(256) k_csr_split(CsrSplitArgs a) {
 #ifndef BP_STREAM_BUF_BYTES
 #define BP_STREAM_BUF_BYTES 2048
 #endif
-constexpr int kStreamThreads = 1024;
+#ifndef BP_STREAM_THREADS
+#define BP_STREAM_THREADS 1024
+#endif
+constexpr int kStreamThreads = BP_STREAM_THREADS;
 // static shared memory of k_csr_stream
 constexpr size_t kStreamStaticSmem = 0;
 constexpr int kStreamWarps = kStreamThreads / 32;
