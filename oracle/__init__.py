@@ -88,6 +88,8 @@ def lib():
         _lib.or_event_csrmv.argtypes = [P, P, P, f32, i64, P, i32, P, P]
         _lib.or_jit_event_mv.argtypes = [u64, u32, u32, i32, f32, f32, i64,
                                          i64, i64, i64, P, i32, P, P]
+        _lib.or_csrmv_gather.argtypes = [P, P, P, f32, i64, P, i32, P, P]
+        _lib.or_csrmv_grad.argtypes = [P, P, P, f32, i64, P, P, P, P, P]
         _lib.or_jit_mv.argtypes = [u64, u32, u32, i32, f32, f32, i64, i64, i64, i64,
                                    P, i32, P, P]
         _lib.or_lif_step.argtypes = [ctypes.POINTER(LifParams), i64, P, P, P,
@@ -204,6 +206,39 @@ def event_csrmv(indptr, indices, data, w_homo, n_rows, n_cols, events,
     lib().or_event_csrmv(_p(indptr), _p(indices), _p(data), float(w_homo),
                          n_rows, _p(ev), out_kind, _p(out), _p(absd))
     return (out, absd) if with_abs else out
+
+
+def csrmv_gather(indptr, indices, data, w_homo, n_rows, n_cols, events,
+                 out_kind=OUT_F64, out=None, with_abs=False):
+    """Gather orientation (transpose=False, reading G1): out[r] = sum over
+    row r of w_k [events[indices[k]]]; events has n_cols entries."""
+    indptr = np.ascontiguousarray(indptr, np.int64)
+    indices = np.ascontiguousarray(indices, np.int32)
+    data = None if data is None else np.ascontiguousarray(data, np.float32)
+    ev = np.ascontiguousarray(events, np.uint8)
+    assert ev.shape[0] == n_cols
+    if out is None:
+        out = _out_buf(n_rows, out_kind)
+    absd = np.zeros(n_rows, np.float64) if with_abs else None
+    lib().or_csrmv_gather(_p(indptr), _p(indices), _p(data), float(w_homo), n_rows, _p(ev),
+                          out_kind, _p(out), _p(absd))
+    return (out, absd) if with_abs else out
+
+
+def csrmv_grad(indptr, indices, data, w_homo, n_rows, events, gy):
+    """Reverse mode of the event scatter y = M^T s (reading G1): returns
+    (grad_data f32[nnz], grad_events f64[n_rows], grad_w f64)."""
+    indptr = np.ascontiguousarray(indptr, np.int64)
+    indices = np.ascontiguousarray(indices, np.int32)
+    data = None if data is None else np.ascontiguousarray(data, np.float32)
+    ev = np.ascontiguousarray(events, np.uint8)
+    gy = np.ascontiguousarray(gy, np.float32)
+    gd = np.zeros(indices.shape[0], np.float32)
+    ge = np.zeros(n_rows, np.float64)
+    gw = np.zeros(1, np.float64)
+    lib().or_csrmv_grad(_p(indptr), _p(indices), _p(data), float(w_homo), n_rows, _p(ev),
+                        _p(gy), _p(gd), _p(ge), _p(gw))
+    return gd, ge, float(gw[0])
 
 
 def jit_event_mv(spec: JitSpec, n_rows, n_cols, events, col_begin=0,

@@ -257,6 +257,50 @@ void or_jit_event_mv(uint64_t seed, uint32_t K, uint32_t L, int law, float w0,
 }
 
 /* ------------------------------------------------------------------------
+ * Gather-orientation event csrmv (BrainPy csrmv(..., transpose=False);
+ * SURVEY 8(f) NEXT 3, reading G1): the CSR rows are the OUTPUTS and the
+ * column indices the event (spike) index:
+ *   out[r] (+)= sum_{k in row r} [events[indices[k]]] * w_k.
+ * Pinned by: equals the scatter (Listing S1) of the transposed matrix, bit
+ * for bit in fixed point (test_oracle_csr.py).
+ * ---------------------------------------------------------------------- */
+void or_csrmv_gather(const int64_t *indptr, const int32_t *indices, const float *data,
+                     float w_homo, int64_t n_rows, const uint8_t *events, int out_kind,
+                     void *out, double *abs_out) {
+  for (int64_t r = 0; r < n_rows; ++r)
+    for (int64_t k = indptr[r]; k < indptr[r + 1]; ++k)
+      if (events[indices[k]]) accumulate(out_kind, out, abs_out, r, data ? data[k] : w_homo);
+}
+
+/* ------------------------------------------------------------------------
+ * Reverse mode of the event scatter y = M^T s (Listing S1; SURVEY 8(f)
+ * NEXT 3, "differentiability", reading G1): with upstream gradient gy
+ * (n_cols) of L,
+ *   dL/ddata[k] = s[r(k)] * gy[indices[k]]            (grad_data, nnz)
+ *   dL/ds[r]    = sum_{k in row r} w_k * gy[indices[k]] (grad_events, n_rows,
+ *                 the events read as real numbers: a gather product)
+ *   dL/dw       = sum_{r: s[r]} sum_{k in row r} gy[indices[k]]  (homogeneous w)
+ * in fp64 (grad_data is exact in fp32).  Any output may be NULL.
+ * Pinned by: torch autograd of the dense fp64 product (test_oracle_csr.py).
+ * ---------------------------------------------------------------------- */
+void or_csrmv_grad(const int64_t *indptr, const int32_t *indices, const float *data,
+                   float w_homo, int64_t n_rows, const uint8_t *events, const float *gy,
+                   float *grad_data, double *grad_events, double *grad_w) {
+  double gw = 0.0;
+  for (int64_t r = 0; r < n_rows; ++r) {
+    double ge = 0.0;
+    for (int64_t k = indptr[r]; k < indptr[r + 1]; ++k) {
+      const double g = (double)gy[indices[k]];
+      if (grad_data) grad_data[k] = events[r] ? gy[indices[k]] : 0.0f;
+      ge += (data ? (double)data[k] : (double)w_homo) * g;
+      if (events[r]) gw += g;
+    }
+    if (grad_events) grad_events[r] = ge;
+  }
+  if (grad_w) *grad_w = gw;
+}
+
+/* ------------------------------------------------------------------------
  * Non-event JIT matrix-vector product, mv_prob_{homo,uniform,normal} (P:94,
  * P:192), reading MV1:
  *   out[c] (+)= sum_r v[r] * w_e(r) over the edges (r, e) with pos_e(r) = c,

@@ -95,3 +95,55 @@ def test_degenerate_shapes(orc, n_rows, n_cols):
     assert out.shape == (n_cols,)
     d = _dense(ip, ix, dat, 1.0, n_rows, n_cols)
     assert np.array_equal(out, d.sum(axis=0))
+
+
+# ---------------------------------------------------------------- reading G1
+@pytest.mark.parametrize("homo", [True, False])
+def test_gather_equals_scatter_of_transpose(orc, homo):
+    """Gather orientation on M equals the Listing-S1 scatter on M^T."""
+    n_rows, n_cols = 60, 45
+    ip, ix, dat = inputs.random_csr(n_rows, n_cols, 0.2, seed=3, integer_weights=not homo)
+    w = 0.75
+    d = _dense(ip, ix, dat, w, n_rows, n_cols)             # M[r, c]
+    # transpose as CSR (rows = columns of M)
+    rows_t, cols_t = np.nonzero(d.T)
+    ipt = np.zeros(n_cols + 1, np.int64)
+    np.add.at(ipt, rows_t + 1, 1)
+    ipt = np.cumsum(ipt)
+    datt = d.T[rows_t, cols_t].astype(np.float32)
+    ev = inputs.spike_pattern(n_cols, 0.4, 8)
+    got = orc.csrmv_gather(ip, ix, dat, w, n_rows, n_cols, ev, out_kind=orc.OUT_FIX)
+    want = orc.event_csrmv(ipt, cols_t.astype(np.int32), datt, 0.0, n_cols, n_rows, ev,
+                           orc.OUT_FIX)
+    assert np.array_equal(got, want)
+    assert np.allclose(orc.csrmv_gather(ip, ix, dat, w, n_rows, n_cols, ev), d @ ev)
+
+
+@pytest.mark.parametrize("homo", [True, False])
+def test_grad_matches_torch_autograd(orc, homo):
+    """dL/ddata, dL/ds and dL/dw of L = gy . (M^T s) against torch autograd
+    of the dense fp64 product (an independent computation)."""
+    import torch
+    n_rows, n_cols = 50, 70
+    ip, ix, dat = inputs.random_csr(n_rows, n_cols, 0.15, seed=5,
+                                    weights="homo" if homo else "uniform", w0=-1.0, w1=1.0)
+    w = float(np.float32(0.6))                  # the oracle's weights are fp32
+    ev = inputs.spike_pattern(n_rows, 0.5, 2)
+    rng = np.random.default_rng(4)
+    gy = rng.normal(size=n_cols).astype(np.float32)
+    rows = np.repeat(np.arange(n_rows), np.diff(ip))
+    vals = torch.tensor(np.full(ix.shape[0], w) if homo else dat.astype(np.float64),
+                        requires_grad=True)
+    wt = torch.tensor(w, dtype=torch.float64, requires_grad=True)
+    s = torch.tensor(ev.astype(np.float64), requires_grad=True)
+    dense = torch.zeros(n_rows, n_cols, dtype=torch.float64)
+    dense = dense.index_put((torch.tensor(rows), torch.tensor(ix.astype(np.int64))),
+                            vals * (wt / w if homo else 1.0), accumulate=True)
+    y = dense.T @ s
+    (y @ torch.tensor(gy.astype(np.float64))).backward()
+    gd, ge, gw = orc.csrmv_grad(ip, ix, None if homo else dat, w, n_rows, ev, gy)
+    assert np.allclose(ge, s.grad.numpy(), rtol=1e-12, atol=1e-12)
+    if homo:
+        assert abs(gw - wt.grad.item()) <= 1e-9 * max(1.0, abs(gw))
+    else:
+        assert np.allclose(gd.astype(np.float64), vals.grad.numpy(), rtol=0, atol=0)
