@@ -114,6 +114,31 @@ bp_status bp_event_csrmv(const int64_t *indptr, const int32_t *indices,
                          int out_kind, uint32_t flags, void *ws,
                          size_t ws_bytes, bp_stream stream);
 
+/* Gather orientation (BrainPy csrmv(..., transpose=False); SURVEY 8(f)
+ * NEXT 3, reading G1): the CSR rows are the OUTPUTS, the column indices the
+ * event index:  out[r] (+)= sum_{k in row r} w_k [bit indices[k] of spikes].
+ * spikes: ceil(n_cols/32) words; out: n_rows float32 / int64 fixed point.
+ * One warp per output row: no atomics, deterministic (fp32: fixed warp-tree
+ * order, rule T2 against the sequential sum; homogeneous: fl32(count * w);
+ * fixed point exact).  Indices need not be sorted. */
+bp_status bp_csrmv_gather(const int64_t *indptr, const int32_t *indices, const float *data,
+                          float w_homo, int64_t n_rows, int64_t n_cols, const uint32_t *spikes,
+                          void *out, int out_kind, uint32_t flags, bp_stream stream);
+
+/* Reverse mode of the event scatter y = M^T s (bp_event_csrmv; SURVEY 8(f)
+ * NEXT 3, reading G1; the paper's differentiability claim) for an
+ * upstream gradient gy (n_cols float32):
+ *   grad_data[k]   = s[r(k)] * gy[indices[k]]          (nnz, exact)
+ *   grad_events[r] = sum_{k in row r} w_k gy[indices[k]] (n_rows; the events
+ *                    as real inputs; fp32, fixed warp-tree order)
+ *   grad_w         = sum_{r: s[r]} sum_k gy[indices[k]] (fp64 scalar, only
+ *                    for homogeneous weights, data == NULL; overwritten)
+ * spikes: ceil(n_rows/32) words.  Any output may be NULL. */
+bp_status bp_event_csrmv_grad(const int64_t *indptr, const int32_t *indices, const float *data,
+                              float w_homo, int64_t n_rows, int64_t n_cols,
+                              const uint32_t *spikes, const float *gy, float *grad_data,
+                              float *grad_events, double *grad_w, bp_stream stream);
+
 /* a2 with a reusable analysis of a fixed matrix (cf. cuSPARSE's SpMV
  * preprocessing).  bp_event_csrmv splits every active row at the column-tile
  * boundaries of its shared-memory accumulation on each call; for a matrix

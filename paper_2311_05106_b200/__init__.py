@@ -8,7 +8,7 @@ raises; there is no CPU fallback.
 from ._binding import (ACCUMULATE, CONN_CSR, CONN_JIT, LAW_HOMO, LAW_NORMAL,  # noqa: F401
                        LAW_UNIFORM, MODEL_HH, MODEL_LIF, OUT_F32, OUT_FIX64,
                        BpError, JitConn, Network, NeuronParams, compact_spikes,
-                       conn_len, csrmv_plan, event_csrmv, hh_params, jitconn_event_mv, jitconn_mv,
+                       conn_len, csrmv_gather, csrmv_plan, event_csrmv, event_csrmv_grad, hh_params, jitconn_event_mv, jitconn_mv,
                        jitconn_event_mv_homo, jitconn_event_mv_normal,
                        jitconn_event_mv_uniform, jitconn_materialize,
                        jitconn_spec, lib, lif_params, neuron_step, workspace,

@@ -28,7 +28,7 @@ EXPORTED = [
     "bp_workspace_bytes", "bp_csrmv_workspace_bytes", "bp_compact_spikes", "bp_event_csrmv",
     "bp_csrmv_plan_bytes", "bp_csrmv_plan", "bp_event_csrmv_planned",
     "bp_jitconn_workspace_bytes", "bp_jitconn_mv_homo", "bp_jitconn_mv_uniform",
-    "bp_jitconn_mv_normal",
+    "bp_jitconn_mv_normal", "bp_csrmv_gather", "bp_event_csrmv_grad",
     "bp_jitconn_event_mv_homo", "bp_jitconn_event_mv_uniform",
     "bp_jitconn_event_mv_normal", "bp_jitconn_row_counts",
     "bp_jitconn_materialize", "bp_neuron_step", "bp_network_workspace_bytes",
@@ -107,6 +107,8 @@ def lib():
         L.bp_event_csrmv.argtypes = [P, P, P, f32, i64, i64, P, P, i32, u32, P, sz, P]
         L.bp_jitconn_workspace_bytes.argtypes = [i64, i64, i64, i32]
         L.bp_jitconn_workspace_bytes.restype = sz
+        L.bp_csrmv_gather.argtypes = [P, P, P, f32, i64, i64, P, P, i32, u32, P]
+        L.bp_event_csrmv_grad.argtypes = [P, P, P, f32, i64, i64, P, P, P, P, P, P]
         L.bp_csrmv_plan_bytes.argtypes = [i64, i64, i32, i32]
         L.bp_csrmv_plan_bytes.restype = sz
         L.bp_csrmv_plan.argtypes = [P, P, i64, i64, i32, i32, P, sz, P]
@@ -223,6 +225,30 @@ def event_csrmv(indptr, indices, data, w_homo, n_rows, n_cols, spikes, out,
     else:
         _check(lib().bp_event_csrmv(*tail))
     return out
+
+
+def csrmv_gather(indptr, indices, data, w_homo, n_rows, n_cols, spikes, out,
+                 accumulate=False, stream=None):
+    """Gather orientation (csrmv transpose=False, reading G1): out[r] (+)=
+    sum over row r of w_k [spike indices[k]] -> out[n_rows] (f32 or fix64)."""
+    _cuda(indptr, indices, data, spikes, out)
+    _check(lib().bp_csrmv_gather(_ptr(indptr), _ptr(indices), _ptr(data), float(w_homo),
+                                 int(n_rows), int(n_cols), _ptr(spikes), _ptr(out),
+                                 _out_kind(out), ACCUMULATE if accumulate else 0,
+                                 _stream(stream)))
+    return out
+
+
+def event_csrmv_grad(indptr, indices, data, w_homo, n_rows, n_cols, spikes, gy,
+                     grad_data=None, grad_events=None, grad_w=None, stream=None):
+    """Reverse mode of the event scatter y = M^T s (reading G1): fills the
+    given outputs (grad_data[nnz] f32, grad_events[n_rows] f32, grad_w f64[1])."""
+    _cuda(indptr, indices, data, spikes, gy, grad_data, grad_events, grad_w)
+    _check(lib().bp_event_csrmv_grad(_ptr(indptr), _ptr(indices), _ptr(data), float(w_homo),
+                                     int(n_rows), int(n_cols), _ptr(spikes), _ptr(gy),
+                                     _ptr(grad_data), _ptr(grad_events), _ptr(grad_w),
+                                     _stream(stream)))
+    return grad_data, grad_events, grad_w
 
 
 def csrmv_plan(indptr, indices, n_rows, n_cols, out_dtype=torch.float32, homo=True,

@@ -16,6 +16,7 @@
 #include "scatter.cuh"
 #include "csr_stream.cuh"
 #include "jit_tiled.cuh"
+#include "csr_grad.cuh"
 #include "step.cuh"
 
 namespace {
@@ -703,6 +704,56 @@ bp_status bp_event_csrmv(const int64_t *indptr, const int32_t *indices,
                          size_t ws_bytes, bp_stream stream) {
   return csrmv_impl(nullptr, 0, indptr, indices, data, w_homo, n_rows, n_cols, spikes, out,
                     out_kind, flags, ws, ws_bytes, stream);
+}
+
+bp_status bp_csrmv_gather(const int64_t *indptr, const int32_t *indices, const float *data,
+                          float w_homo, int64_t n_rows, int64_t n_cols, const uint32_t *spikes,
+                          void *out, int out_kind, uint32_t flags, bp_stream stream) {
+  int sms = 0;
+  bp_status s = device_ready(&sms);
+  if (s != BP_OK) return s;
+  BP_CHECK(n_rows >= 0 && n_rows <= kMaxDim && n_cols >= 1 && n_cols <= kMaxDim,
+           BP_ERR_SHAPE, "n_rows=%lld n_cols=%lld", (long long)n_rows, (long long)n_cols);
+  BP_CHECK(n_rows == 0 || (indptr && indices && spikes), BP_ERR_INVALID_ARG,
+           "NULL indptr/indices/spikes");
+  s = check_out(out, out_kind);
+  if (s != BP_OK) return s;
+  if (n_rows == 0) return BP_OK;
+  bp::CsrGatherArgs a{indptr, indices, data, w_homo,
+                      llrint(static_cast<double>(w_homo) * 4294967296.0), n_rows, spikes, out,
+                      (flags & BP_ACCUMULATE) ? 1 : 0};
+  int64_t blocks = (n_rows + 7) / 8;
+  if (blocks > static_cast<int64_t>(sms) * 16) blocks = static_cast<int64_t>(sms) * 16;
+  cudaStream_t st = as_stream(stream);
+  if (out_kind == BP_OUT_FIX64)
+    bp::k_csr_gather<1><<<static_cast<int>(blocks), bp::kGatherThreads, 0, st>>>(a);
+  else
+    bp::k_csr_gather<0><<<static_cast<int>(blocks), bp::kGatherThreads, 0, st>>>(a);
+  return launched();
+}
+
+bp_status bp_event_csrmv_grad(const int64_t *indptr, const int32_t *indices, const float *data,
+                              float w_homo, int64_t n_rows, int64_t n_cols,
+                              const uint32_t *spikes, const float *gy, float *grad_data,
+                              float *grad_events, double *grad_w, bp_stream stream) {
+  int sms = 0;
+  bp_status s = device_ready(&sms);
+  if (s != BP_OK) return s;
+  BP_CHECK(n_rows >= 0 && n_rows <= kMaxDim && n_cols >= 1 && n_cols <= kMaxDim,
+           BP_ERR_SHAPE, "n_rows=%lld n_cols=%lld", (long long)n_rows, (long long)n_cols);
+  BP_CHECK(n_rows == 0 || (indptr && indices && spikes && gy), BP_ERR_INVALID_ARG,
+           "NULL indptr/indices/spikes/gy");
+  BP_CHECK(grad_w == nullptr || data == nullptr, BP_ERR_INVALID_ARG,
+           "grad_w is the gradient of the homogeneous weight (data must be NULL)");
+  cudaStream_t st = as_stream(stream);
+  if (grad_w) BP_CUDA(cudaMemsetAsync(grad_w, 0, sizeof(double), st));
+  if (n_rows == 0) return launched();
+  bp::CsrGradArgs a{indptr, indices, data, w_homo, n_rows, spikes, gy,
+                    grad_data, grad_events, grad_w};
+  int64_t blocks = (n_rows + 7) / 8;
+  if (blocks > static_cast<int64_t>(sms) * 16) blocks = static_cast<int64_t>(sms) * 16;
+  bp::k_csr_grad<<<static_cast<int>(blocks), bp::kGatherThreads, 0, st>>>(a);
+  return launched();
 }
 
 size_t bp_csrmv_plan_bytes(int64_t n_rows, int64_t n_cols, int out_kind, int homo) {

@@ -398,3 +398,60 @@ def test_jitconn_mv_binary_vector_equals_event_mv(bp):
     bp.jitconn_event_mv_uniform(spec, -0.3, 0.3, _dev_spikes(ev), n_rows, n_cols, a)
     bp.jitconn_mv(bp.LAW_UNIFORM, spec, -0.3, 0.3, _t(ev.astype(np.float32)), n_rows, n_cols, b)
     assert torch.equal(a, b)
+
+
+# ------------------------------------------ NEXT 3: gather orientation + grad
+GATHER_CASES = [
+    # n_rows (outputs), n_cols (event vector), p, weights, density
+    (1, 1, 1.0, "homo", 1.0),
+    (300, 5000, 0.05, "uniform", 0.1),
+    (2000, 3000, 0.01, "homo", 0.3),
+    (500, 100_000, 0.02, "uniform", 0.05),
+    (10_000, 64, 0.5, "normal", 0.5),        # short rows
+]
+
+
+@pytest.mark.parametrize("case", GATHER_CASES)
+def test_csrmv_gather(bp, orc, case):
+    n_rows, n_cols, p, law, density = case
+    ip, ix, dat = inputs.random_csr(n_rows, n_cols, p, seed=n_rows + 7 * n_cols,
+                                    weights=law, w0=-0.5 if law != "homo" else 1.0,
+                                    w1=0.5 if law != "homo" else 0.0)
+    w = 0.6
+    ev = inputs.spike_pattern(n_cols, density, seed=5)
+    spikes = _dev_spikes(ev)
+    tip, tix, tdat = _t(ip), _t(ix), _t(dat)
+    out = torch.full((n_rows,), 3, dtype=torch.int64, device="cuda")
+    bp.csrmv_gather(tip, tix, tdat, w, n_rows, n_cols, spikes, out, accumulate=True)
+    want = orc.csrmv_gather(ip, ix, dat, w, n_rows, n_cols, ev, orc.OUT_FIX)
+    assert np.array_equal(out.cpu().numpy(), want + 3)
+    out32 = torch.zeros(n_rows, dtype=torch.float32, device="cuda")
+    bp.csrmv_gather(tip, tix, tdat, w, n_rows, n_cols, spikes, out32)
+    ref, absw = orc.csrmv_gather(ip, ix, dat, w, n_rows, n_cols, ev, orc.OUT_F64, with_abs=True)
+    assert np.all(np.abs(out32.cpu().numpy() - ref) <= 1e-5 * absw + 1e-30)
+
+
+@pytest.mark.parametrize("homo", [True, False])
+def test_event_csrmv_grad(bp, orc, homo):
+    n_rows, n_cols = 3000, 20_000
+    ip, ix, dat = inputs.random_csr(n_rows, n_cols, 0.01, seed=31,
+                                    weights="homo" if homo else "uniform", w0=-1.0, w1=1.0)
+    data = None if homo else dat
+    w = 0.6
+    ev = inputs.spike_pattern(n_rows, 0.2, seed=6)
+    rng = np.random.default_rng(3)
+    gy = rng.normal(size=n_cols).astype(np.float32)
+    gd = torch.full((ix.shape[0],), 9.0, device="cuda")
+    ge = torch.zeros(n_rows, device="cuda")
+    gw = torch.full((1,), 5.0, dtype=torch.float64, device="cuda") if homo else None
+    bp.event_csrmv_grad(_t(ip), _t(ix), _t(data), w, n_rows, n_cols, _dev_spikes(ev), _t(gy),
+                        gd, ge, gw)
+    want_gd, want_ge, want_gw = orc.csrmv_grad(ip, ix, data, w, n_rows, ev, gy)
+    assert np.array_equal(gd.cpu().numpy(), want_gd)            # exact
+    absg = np.zeros(n_rows)
+    np.add.at(absg, np.repeat(np.arange(n_rows), np.diff(ip)),
+              np.abs((np.float32(w) if homo else dat).astype(np.float64) * gy[ix]))
+    assert np.all(np.abs(ge.cpu().numpy() - want_ge) <= 1e-5 * absg + 1e-30)
+    if homo:
+        tot = np.abs(gy[ix][np.repeat(ev, np.diff(ip)).astype(bool)]).sum()
+        assert abs(gw.item() - want_gw) <= 1e-12 * tot + 1e-12
