@@ -99,6 +99,13 @@ def lib():
         _lib.or_expf.argtypes = [f32]
         _lib.or_expf.restype = f32
         _lib.or_set_fix32_bits.argtypes = [i32]
+        _lib.or_set_gap_sampler.argtypes = [f32]
+        _lib.or_geo_c.argtypes = [f64]
+        _lib.or_geo_c.restype = f32
+        _lib.or_logf_j10.argtypes = [f32]
+        _lib.or_logf_j10.restype = f32
+        _lib.or_geo_gap.argtypes = [f32, u32, u32]
+        _lib.or_geo_gap.restype = u32
         _lib.or_fix32_add.argtypes = [P, P, i64]
         _lib.or_fix32_add.restype = i64
     return _lib
@@ -145,6 +152,37 @@ class JitSpec:
     law: int = LAW_HOMO
     w0: float = 1.0
     w1: float = 0.0
+    # rule J10: 0 -> uniform gaps U[1, K] (J3); else c = fl32(log1p(-p)) and
+    # gaps are Geo(p) by inversion (geometric sampler)
+    geo_c: float = 0.0
+
+
+def geo_c(p: float) -> float:
+    """Rule J10 constant c = fl32(log1p(-p))."""
+    return float(lib().or_geo_c(p))
+
+
+def logf_j10(u: float) -> float:
+    """Rule J10's specified fp32 natural log."""
+    return float(lib().or_logf_j10(u))
+
+
+def geo_gap(c: float, cap: int, x: int) -> int:
+    """Rule J10 gap from one 32-bit word x."""
+    return int(lib().or_geo_gap(c, cap, x))
+
+
+class _Sampler:
+    """Selects the gap sampler of one oracle call (rule J3 or J10)."""
+
+    def __init__(self, spec):
+        self.c = spec.geo_c
+
+    def __enter__(self):
+        lib().or_set_gap_sampler(self.c)
+
+    def __exit__(self, *exc):
+        lib().or_set_gap_sampler(0.0)
 
 
 def jit_row(spec: JitSpec, n_cols: int, row: int, seg_first: int = 0,
@@ -156,9 +194,10 @@ def jit_row(spec: JitSpec, n_cols: int, row: int, seg_first: int = 0,
     while True:
         pos = np.empty(cap, np.int32)
         w = np.empty(cap, np.float32)
-        n = lib().or_jit_row(spec.seed, spec.K, spec.L, n_cols, spec.law,
-                             spec.w0, spec.w1, row, seg_first, seg_last,
-                             _p(pos), _p(w), cap)
+        with _Sampler(spec):
+            n = lib().or_jit_row(spec.seed, spec.K, spec.L, n_cols, spec.law,
+                                 spec.w0, spec.w1, row, seg_first, seg_last,
+                                 _p(pos), _p(w), cap)
         if n <= cap:
             return pos[:n].copy(), w[:n].copy()
         cap = int(n)
@@ -251,9 +290,10 @@ def jit_event_mv(spec: JitSpec, n_rows, n_cols, events, col_begin=0,
     if out is None:
         out = _out_buf(col_end - col_begin, out_kind)
     absd = np.zeros(col_end - col_begin, np.float64) if with_abs else None
-    lib().or_jit_event_mv(spec.seed, spec.K, spec.L, spec.law, spec.w0,
-                          spec.w1, n_rows, n_cols, col_begin, col_end,
-                          _p(ev), out_kind, _p(out), _p(absd))
+    with _Sampler(spec):
+        lib().or_jit_event_mv(spec.seed, spec.K, spec.L, spec.law, spec.w0,
+                              spec.w1, n_rows, n_cols, col_begin, col_end,
+                              _p(ev), out_kind, _p(out), _p(absd))
     return (out, absd) if with_abs else out
 
 
@@ -267,8 +307,9 @@ def jit_mv(spec: JitSpec, n_rows, n_cols, v, col_begin=0, col_end=None,
     if out is None:
         out = _out_buf(col_end - col_begin, out_kind)
     absd = np.zeros(col_end - col_begin, np.float64) if with_abs else None
-    lib().or_jit_mv(spec.seed, spec.K, spec.L, spec.law, spec.w0, spec.w1, n_rows, n_cols,
-                    col_begin, col_end, _p(vv), out_kind, _p(out), _p(absd))
+    with _Sampler(spec):
+        lib().or_jit_mv(spec.seed, spec.K, spec.L, spec.law, spec.w0, spec.w1, n_rows,
+                        n_cols, col_begin, col_end, _p(vv), out_kind, _p(out), _p(absd))
     return (out, absd) if with_abs else out
 
 
@@ -366,7 +407,8 @@ def run_network(model: str, params, state: dict, proj_e: Projection,
                 # fl32(count * w) (one rounding of the exact sum)
                 cnt = np.zeros(g.shape[0], np.float64)
                 if proj.jit is not None:
-                    spec1 = JitSpec(proj.jit.seed, proj.jit.K, proj.jit.L, LAW_HOMO, 1.0)
+                    spec1 = JitSpec(proj.jit.seed, proj.jit.K, proj.jit.L, LAW_HOMO, 1.0,
+                                    geo_c=proj.jit.geo_c)
                     jit_event_mv(spec1, proj.n_rows, n_total, ev, col_begin, col_end,
                                  OUT_F64, out=cnt)
                     w = np.float32(proj.jit.w0)

@@ -104,6 +104,89 @@ uint32_t or_conn_len(double p) {
   return (uint32_t)k;
 }
 
+/* ------------------------------------------------------------------------
+ * Rule J10: the geometric-gap sampler the paper
+ * compares against (App. C: "sampled in constant time by inverting
+ * the cumulative density function ... log(U[0,1]) / log(1 - P)", after
+ * Knight & Nowotny 2020).  Gaps G ~ Geo(p) on {1, 2, ...}:
+ *   u = ((x >> 8) + 1) 2^-24 in (0, 1]           (24-bit, exact in fp32)
+ *   t = logf_j10(u) / c,   c = fl32(log1p(-p))    (IEEE fp32 division)
+ *   G = 1 if ceil(t) < 1;  cap if t >= (float)cap;  else (uint32) ceil(t)
+ * P(G >= k) = P(u < (1-p)^(k-1)) = (1-p)^(k-1): the exact geometric law
+ * (up to the 24-bit u and fp32 rounding).  Being memoryless, the first
+ * target of a segment is seg_begin + G_0 - 1 (G_0 from the tag-2 word 0):
+ * every column is connected independently with probability p -- unlike
+ * the uniform-gap rule, whose density is 2/(K+1) (reading R4).
+ * cap = L + 1 (L = seg_len): any gap that long leaves the segment, so the
+ * cap changes no position and keeps positions within 32 bits.
+ * logf_j10 is an op-for-op specified fp32 log (the product kernels run the
+ * same operations, so both sides draw identical gaps):
+ *   u = m 2^e, m in [1, 2); if m > fl32(sqrt 2): m /= 2, e += 1
+ *   f = m - 1 (exact), s = f / (2 + f), z = s s,
+ *   r = Horner(z; 1/11, 1/9, 1/7, 1/5, 1/3) with fmaf (fl32 coefficients),
+ *   log m = fmaf(2s, z r, 2s)   (2 atanh(s) = 2s (1 + z/3 + z^2/5 + ...))
+ *   log u = fmaf(e, LN2_HI, fmaf(e, LN2_LO, log m)), LN2_HI = 0.693145751953125
+ * Pinned by: <= 2 ulp vs libm logf on (0, 1]; the SPEC example p = 0.5,
+ * u = 0.25 -> 2 and u -> 1 -> 1; mean gap 1/p within 1 %;
+ * P(first = j) = (1-p)^j p; per-column density p within 4 sigma; row
+ * fan-out variance L p (1-p) (Bernoulli process), test_oracle_jit.py.
+ * ---------------------------------------------------------------------- */
+static float g_geo_c = 0.0f;          /* 0: uniform gaps (rule J3)         */
+void or_set_gap_sampler(float c) { g_geo_c = c; }
+float or_geo_c(double p) { return (float)log1p(-p); }
+
+float or_logf_j10(float u) {
+  uint32_t b;
+  memcpy(&b, &u, 4);
+  int e = (int)(b >> 23) - 127;
+  uint32_t mb = (b & 0x7FFFFFu) | 0x3F800000u;
+  float m;
+  memcpy(&m, &mb, 4);
+  if (m > 1.41421353816986083984375f) { m = m * 0.5f; e += 1; }
+  float f = m - 1.0f;
+  float s = f / (2.0f + f);
+  float z = s * s;
+  float r = fmaf(z, 1.0f / 11.0f, 1.0f / 9.0f);
+  r = fmaf(z, r, 1.0f / 7.0f);
+  r = fmaf(z, r, 1.0f / 5.0f);
+  r = fmaf(z, r, 1.0f / 3.0f);
+  float zr = z * r;
+  float s2 = s + s;
+  float lm = fmaf(s2, zr, s2);
+  float ef = (float)e;
+  return fmaf(ef, 0.693145751953125f, fmaf(ef, 1.428606765330187e-6f, lm));
+}
+
+uint32_t or_geo_gap(float c, uint32_t cap, uint32_t x) {
+  float u = (float)((x >> 8) + 1u) * 0x1p-24f;
+  float t = or_logf_j10(u) / c;
+  if (!(t < (float)cap)) return cap;
+  float ct = ceilf(t);
+  if (ct < 1.0f) return 1u;
+  uint32_t g = (uint32_t)ct;
+  return g > cap ? cap : g;
+}
+
+/* Offset of the first target of (row, seg) from the segment start: rule J5
+ * (uniform gaps) or G_0 - 1 (rule J10). */
+static uint32_t first_offset_of(uint64_t seed, uint32_t K, uint32_t L,
+                                uint32_t row, uint32_t s) {
+  if (g_geo_c != 0.0f)
+    return or_geo_gap(g_geo_c, L + 1u, or_word(seed, 2u, row, s, 0u)) - 1u;
+  uint32_t a = uniform_int(0u, K - 1u, or_word(seed, 2u, row, s, 0u));
+  uint32_t b = uniform_int(0u, K, or_word(seed, 2u, row, s, 1u));
+  if (b <= a) a = K - 1u - a;
+  return a;
+}
+
+/* Gap e of (row, seg): U[1, K] (rule J3/J6) or Geo(p) (rule J10). */
+static uint32_t gap_of(uint64_t seed, uint32_t K, uint32_t L, uint32_t row,
+                       uint32_t s, uint32_t e) {
+  uint32_t x = or_word(seed, 0u, row, s, e);
+  if (g_geo_c != 0.0f) return or_geo_gap(g_geo_c, L + 1u, x);
+  return uniform_int(1u, K, x);
+}
+
 /* Rule F1: fixed-point quantisation q(w) = llrint(w * 2^32) (half-even). */
 int64_t or_quantize(float w) {
   return llrint((double)w * 4294967296.0);
@@ -158,10 +241,7 @@ int64_t or_jit_row(uint64_t seed, uint32_t K, uint32_t L, int64_t n_cols,
     int64_t seg_begin = s * (int64_t)L;
     int64_t seg_end = seg_begin + (int64_t)L;
     if (seg_end > n_cols) seg_end = n_cols;
-    uint32_t a = uniform_int(0u, K - 1u, or_word(seed, 2u, row, (uint32_t)s, 0u));
-    uint32_t b = uniform_int(0u, K, or_word(seed, 2u, row, (uint32_t)s, 1u));
-    if (b <= a) a = K - 1u - a;
-    int64_t pos = seg_begin + (int64_t)a;
+    int64_t pos = seg_begin + (int64_t)first_offset_of(seed, K, L, row, (uint32_t)s);
     uint32_t e = 0;
     while (pos < seg_end) {
       if (count < cap) {
@@ -169,7 +249,7 @@ int64_t or_jit_row(uint64_t seed, uint32_t K, uint32_t L, int64_t n_cols,
         if (w_out) w_out[count] = edge_weight(seed, law, w0, w1, row, (uint32_t)s, e);
       }
       ++count;
-      pos += (int64_t)uniform_int(1u, K, or_word(seed, 0u, row, (uint32_t)s, e));
+      pos += (int64_t)gap_of(seed, K, L, row, (uint32_t)s, e);
       ++e;
     }
   }
@@ -239,17 +319,15 @@ void or_jit_event_mv(uint64_t seed, uint32_t K, uint32_t L, int law, float w0,
       int64_t seg_begin = s * (int64_t)L;
       int64_t seg_end = seg_begin + (int64_t)L;
       if (seg_end > n_cols) seg_end = n_cols;
-      uint32_t a = uniform_int(0u, K - 1u, or_word(seed, 2u, (uint32_t)r, (uint32_t)s, 0u));
-      uint32_t b = uniform_int(0u, K, or_word(seed, 2u, (uint32_t)r, (uint32_t)s, 1u));
-      if (b <= a) a = K - 1u - a;
-      int64_t pos = seg_begin + (int64_t)a;
+      int64_t pos = seg_begin +
+                    (int64_t)first_offset_of(seed, K, L, (uint32_t)r, (uint32_t)s);
       uint32_t e = 0;
       while (pos < seg_end) {
         if (pos >= col_begin && pos < col_end) {
           float w = edge_weight(seed, law, w0, w1, (uint32_t)r, (uint32_t)s, e);
           accumulate(out_kind, out, abs_out, pos - col_begin, w);
         }
-        pos += (int64_t)uniform_int(1u, K, or_word(seed, 0u, (uint32_t)r, (uint32_t)s, e));
+        pos += (int64_t)gap_of(seed, K, L, (uint32_t)r, (uint32_t)s, e);
         ++e;
       }
     }
@@ -327,10 +405,8 @@ void or_jit_mv(uint64_t seed, uint32_t K, uint32_t L, int law, float w0, float w
       int64_t seg_begin = s * (int64_t)L;
       int64_t seg_end = seg_begin + (int64_t)L;
       if (seg_end > n_cols) seg_end = n_cols;
-      uint32_t a = uniform_int(0u, K - 1u, or_word(seed, 2u, (uint32_t)r, (uint32_t)s, 0u));
-      uint32_t b = uniform_int(0u, K, or_word(seed, 2u, (uint32_t)r, (uint32_t)s, 1u));
-      if (b <= a) a = K - 1u - a;
-      int64_t pos = seg_begin + (int64_t)a;
+      int64_t pos = seg_begin +
+                    (int64_t)first_offset_of(seed, K, L, (uint32_t)r, (uint32_t)s);
       uint32_t e = 0;
       while (pos < seg_end) {
         if (pos >= col_begin && pos < col_end) {
@@ -342,7 +418,7 @@ void or_jit_mv(uint64_t seed, uint32_t K, uint32_t L, int law, float w0, float w
           else ((float *)out)[c] += v[r] * w;
           if (abs_out) abs_out[c] += fabs(prod);
         }
-        pos += (int64_t)uniform_int(1u, K, or_word(seed, 0u, (uint32_t)r, (uint32_t)s, e));
+        pos += (int64_t)gap_of(seed, K, L, (uint32_t)r, (uint32_t)s, e);
         ++e;
       }
     }

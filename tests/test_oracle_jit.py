@@ -251,3 +251,153 @@ def test_mv_is_linear(orc):
                      out_kind=orc.OUT_F64)
     # integer v times fp32 weights: every product and partial sum is exact
     assert np.array_equal(y12, 2 * y1 - y2)
+
+
+# ---------------------------------------------------------------- J10
+# Geometric-gap sampler (App. C).  Gap law
+# Geo(p) by inversion with the specified fp32 log of rule J10; the targets
+# of a row form a Bernoulli(p) process.
+
+def _word_for_u(u: float) -> int:
+    """A 32-bit word whose rule-J10 u = ((x >> 8) + 1) 2^-24 is the multiple
+    of 2^-24 nearest to u in (0, 1] (exact for the dyadic golden values)."""
+    k = int(round(u * 2 ** 24)) - 1
+    assert 0 <= k < 2 ** 24
+    return k << 8
+
+
+def test_logf_j10_within_2ulp(orc):
+    """Rule J10's log on (0, 1] vs the fp64 log, in fp32 ulps."""
+    rng = np.random.default_rng(4)
+    ks = np.unique(np.concatenate([rng.integers(0, 2 ** 24, 200_000),
+                                   np.arange(0, 4096), 2 ** 24 - 1 - np.arange(4096),
+                                   (2 ** np.arange(24)) - 1]))
+    us = ((ks + 1) * 2.0 ** -24).astype(np.float32)
+    got = np.array([orc.logf_j10(float(u)) for u in us], np.float32)
+    want = np.log(us.astype(np.float64))
+    ulp = np.spacing(np.abs(want).astype(np.float32)).astype(np.float64)
+    ulp[want == 0] = np.spacing(np.float32(0))
+    err = np.abs(got.astype(np.float64) - want) / ulp
+    assert err.max() <= 2.0, (us[err.argmax()], err.max())
+    assert orc.logf_j10(1.0) == 0.0
+    for e in range(1, 25):            # exact powers of two: e * ln 2 to 1 ulp
+        assert abs(orc.logf_j10(2.0 ** -e) + e * math.log(2)) <= \
+            np.spacing(np.float32(e * math.log(2)))
+
+
+def test_geo_gap_golden(orc):
+    """tests/golden/geo_gap.txt: analytic values of ceil(log u / log(1-p))."""
+    path = __file__.replace("test_oracle_jit.py", "golden/geo_gap.txt")
+    rows = [ln.split() for ln in open(path) if ln.strip() and not ln.startswith("#")]
+    assert len(rows) >= 8
+    for p, u, g in rows:
+        c = orc.geo_c(float(p))
+        assert orc.geo_gap(c, 1 << 20, _word_for_u(float(u))) == int(g), (p, u, g)
+
+
+@pytest.mark.parametrize("p", [0.5, 0.05, 0.002])
+def test_geo_gap_law(orc, p):
+    """Gaps are Geo(p) on {1, 2, ...}: mean 1/p within 1 %, and
+    P(G = k) = (1-p)^(k-1) p per bin within 4 sigma."""
+    rng = np.random.default_rng(17)
+    n = 400_000
+    c = orc.geo_c(p)
+    xs = rng.integers(0, 2 ** 32, n, dtype=np.uint64)
+    g = np.array([orc.geo_gap(c, 1 << 30, int(x)) for x in xs], np.int64)
+    assert g.min() >= 1
+    assert abs(g.mean() - 1 / p) < 0.01 / p
+    for k in range(1, 6):
+        pk = (1 - p) ** (k - 1) * p
+        sd = math.sqrt(n * pk * (1 - pk))
+        assert abs(np.sum(g == k) - n * pk) <= 4 * sd + 1, k
+
+
+def test_geo_gap_cap(orc):
+    """The cap L + 1 binds only beyond the segment (any such gap exits)."""
+    c = orc.geo_c(1e-6)
+    x_small_u = 0                     # u = 2^-24 -> t = 16.6 / 1e-6
+    assert orc.geo_gap(c, 1001, x_small_u) == 1001
+    assert orc.geo_gap(c, 1 << 30, x_small_u) > 1001
+    assert orc.geo_gap(orc.geo_c(1.0), 10, x_small_u) == 1   # p = 1: dense
+
+
+def _geo_spec(orc, p, seed=7, L=None, n_cols=None, law="homo", w0=0.6, w1=0.0):
+    return orc.JitSpec(seed=seed, K=orc.conn_len(p), L=L or n_cols, law=orc.LAWS[law],
+                       w0=w0, w1=w1, geo_c=orc.geo_c(p))
+
+
+def test_geo_first_offset_is_geometric(orc):
+    """Memoryless start: P(first = j) = (1-p)^j p (every column, incl. 0)."""
+    p, n_rows = 0.2, 30_000
+    spec = _geo_spec(orc, p, seed=3, L=64, n_cols=64)
+    counts = np.zeros(65, np.int64)
+    for r in range(n_rows):
+        pos, _ = orc.jit_row(spec, 64, r, 0, 0)
+        counts[pos[0] if pos.size else 64] += 1
+    for j in range(8):
+        pj = (1 - p) ** j * p
+        sd = math.sqrt(n_rows * pj * (1 - pj))
+        assert abs(counts[j] - n_rows * pj) <= 4 * sd + 1, (j, counts[:8])
+    # an empty row of 64 columns has probability (1-p)^64
+    p0 = (1 - p) ** 64
+    assert abs(counts[64] - n_rows * p0) <= 4 * math.sqrt(n_rows * p0) + 2
+
+
+@pytest.mark.parametrize("p", [0.01, 0.05, 0.1])
+def test_geo_density_2000x2000(orc, p):
+    """Density p itself (not 2/(K+1)): the Bernoulli process is exact."""
+    spec = _geo_spec(orc, p, n_cols=2000)
+    ip, _, _ = orc.jit_materialize(spec, 2000, 2000)
+    cells = 2000 * 2000
+    sd = math.sqrt(cells * p * (1 - p))
+    assert abs(ip[-1] - cells * p) < 4 * sd
+
+
+def test_geo_fan_out_is_binomial(orc):
+    """Row fan-out ~ Binomial(L, p): variance L p (1-p) = 95 at L = 2000,
+    p = 0.05 (the uniform-gap renewal process gives ~32 instead)."""
+    p, L, n_rows = 0.05, 2000, 3000
+    spec = _geo_spec(orc, p, seed=12, n_cols=L)
+    ip, _, _ = orc.jit_materialize(spec, n_rows, L)
+    fan = np.diff(ip).astype(np.float64)
+    var = L * p * (1 - p)
+    assert abs(fan.mean() - L * p) < 4 * math.sqrt(var / n_rows)
+    assert abs(fan.var() - var) < 4 * var * math.sqrt(2.0 / (n_rows - 1))
+    uni = orc.JitSpec(seed=12, K=orc.conn_len(p), L=L)
+    ipu, _, _ = orc.jit_materialize(uni, n_rows, L)
+    assert np.diff(ipu).var() < 0.5 * var
+
+
+def test_geo_columns_independent(orc):
+    """Bernoulli process: connections at columns j and j + 1 of a row are
+    independent: P(both) = p^2 (with U[1, K] gaps P(both) = p_eff / K
+    instead)."""
+    p, L, n_rows = 0.3, 40, 20_000
+    spec = _geo_spec(orc, p, seed=5, n_cols=L)
+    both = 0
+    for r in range(n_rows):
+        pos, _ = orc.jit_row(spec, L, r)
+        s = set(pos.tolist())
+        both += (10 in s) and (11 in s)
+    pb = p * p
+    assert abs(both - n_rows * pb) <= 4 * math.sqrt(n_rows * pb * (1 - pb))
+
+
+@pytest.mark.parametrize("law", ["homo", "uniform", "normal"])
+@pytest.mark.parametrize("L", [None, 64])
+def test_geo_materialised_csr_equals_direct(orc, law, L):
+    """Two independent oracle paths agree with geometric gaps too, and the
+    connectivity does not depend on the events or the weight law."""
+    n_rows, n_cols = 300, 500
+    w0, w1 = {"homo": (0.6, 0.0), "uniform": (-0.1, 0.1), "normal": (0.0, 0.5)}[law]
+    spec = _geo_spec(orc, 0.05, seed=99, n_cols=n_cols, L=L, law=law, w0=w0, w1=w1)
+    ip, ix, dat = orc.jit_materialize(spec, n_rows, n_cols)
+    homo = _geo_spec(orc, 0.05, seed=99, n_cols=n_cols, L=L)
+    assert np.array_equal(ix, orc.jit_materialize(homo, n_rows, n_cols)[1])
+    for density in (0.01, 0.3):
+        ev = inputs.spike_pattern(n_rows, density, 5)
+        a = orc.event_csrmv(ip, ix, dat, 0.0, n_rows, n_cols, ev, orc.OUT_FIX)
+        b = orc.jit_event_mv(spec, n_rows, n_cols, ev, out_kind=orc.OUT_FIX)
+        assert np.array_equal(a, b)
+        v = ev.astype(np.float32)
+        assert np.array_equal(orc.jit_mv(spec, n_rows, n_cols, v, out_kind=orc.OUT_FIX), b)
