@@ -520,6 +520,12 @@ def run_e2e(args, wl, fixed, dev):
 # log/cos/sqrt, counted as 40).  Issue peak: 148 SMs x 4 schedulers x 32
 # lanes x 1 warp-instruction per cycle at the sampled SM clock.
 JIT_OPS_PER_EVENT = {"homo": 21.5, "uniform": 38.5, "normal": 91.5}
+# Per gap draw: uniform (rule J3) = Philox share 15 + multiply-shift 2 +
+# running sum 1 + scan share 2.5 = 20.5; geometric (rule J10) replaces the
+# multiply-shift by u, the specified log (incl. one IEEE division ~ 10),
+# the division by c (~ 10), ceil and clamps: + ~40 (instruction counts of
+# the SASS).
+JIT_OPS_PER_GAP = {"uniform": 20.5, "geometric": 60.5}
 
 
 def run_micro(args):
@@ -545,7 +551,8 @@ def run_micro(args):
                 else bp.lib().bp_jitconn_workspace_bytes(n, 0, n, 1 if fixed else 0))
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
     seed = 0xBE7C4
-    spec = bp.jitconn_spec(seed, p)
+    geo = args.gap == "geometric"
+    spec = bp.jitconn_spec(seed, p, gap_law=bp.GAP_GEOMETRIC if geo else bp.GAP_UNIFORM)
     w0, w1 = {"homo": (0.6, 0.0), "uniform": (-0.1, 0.1),
               "normal": (0.0, 1.0 / np.sqrt(n * p))}[law]     # Table S1 scales
     if kind == "csrmv":
@@ -561,6 +568,20 @@ def run_micro(args):
         bytes_per_event = 8 if law != "homo" else 4
         nnz = int(ip[-1].item())
         working_set = nnz * bytes_per_event + ip.numel() * 8
+    elif kind == "jitrows":
+        # gap-sampler cost (App. C; NEXT 4): regenerate every row
+        # of the matrix (bp_jitconn_row_counts: gap chains only, no weights,
+        # no scatter) -- one call = n_rows x fan-out gap draws
+        counts = torch.empty(n, dtype=torch.int64, device=dev)
+        c_spec = bp._binding.ctypes.byref(spec)
+
+        def call(_s):
+            bp._binding._check(bp.lib().bp_jitconn_row_counts(
+                c_spec, n, n, bp._binding._ptr(counts), bp._binding._stream()))
+        call(None)
+        torch.cuda.synchronize()
+        ev_per_pat = [int(counts.sum().item())] * n_pat
+        working_set = n * 8
     else:
         fn = {"homo": bp.jitconn_event_mv_homo, "uniform": bp.jitconn_event_mv_uniform,
               "normal": bp.jitconn_event_mv_normal}[law]
@@ -619,26 +640,33 @@ def run_micro(args):
     else:
         sm_mhz = clocks.get("sm_mhz") or 1965.0
         peak_ops = 148 * 4 * 32 * sm_mhz * 1e6
-        ops = JIT_OPS_PER_EVENT[law] * events / (total_ms / 1e3)
-        roof = {"kernel": "%sk_jit_tiled<%s> (k_jit_scatter for rows < 1000 events, normal law)"
-                % ("" if kind == "jitmv_vec" else "k_compact + ", law), "bound": "alu",
+        ops_ev = (JIT_OPS_PER_GAP[args.gap] if kind == "jitrows"
+                  else JIT_OPS_PER_EVENT[law] + (JIT_OPS_PER_GAP["geometric"] -
+                                                 JIT_OPS_PER_GAP["uniform"]) * geo)
+        ops = ops_ev * events / (total_ms / 1e3)
+        kern = ("k_jit_rows (row counts: gap chains only)" if kind == "jitrows" else
+                "%sk_jit_tiled<%s> (k_jit_scatter for rows < 1000 events, normal law)"
+                % ("" if kind == "jitmv_vec" else "k_compact + ", law))
+        roof = {"kernel": kern, "bound": "alu",
                 "achieved": ops / 1e12, "peak": peak_ops / 1e12, "unit": "Tops/s (int32 lane ops)",
                 "frac": ops / peak_ops, "traffic": None,
                 "peak_source": "derived: 148 SMs x 4 schedulers x 32 lanes x sampled SM clock",
-                "ops_per_event": JIT_OPS_PER_EVENT[law]}
+                "ops_per_event": ops_ev}
     line = {"metric": "synaptic events/sec (event_mv microbenchmark, config 2)",
             "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "none", "vs_baseline": None,
             "dtype": "i64fix" if fixed else "f32", "data": "synthetic",
-            "config": {"workload": f"{kind}_{law}", "shape": [n, n], "p": p, "density": d,
+            "config": {"workload": f"{kind}_{law}" + ("_geo" if geo else ""), "shape": [n, n],
+                       "p": p, "density": d, "gap_sampler": args.gap,
                        "K": bp.conn_len(p), "events_per_call": events / args.steps,
                        "active_rows_per_call": active,
                        "csr_plan": (kind == "csrmv" and not args.no_plan),
                        "l2": ("flushed between calls (256 MB write)" if flush
                               else "working set %.0f MB > 2 x L2" % (working_set / 1e6))},
             # compact + scatter (+ per-call split of the rows without a plan)
-            "gpu_launches": (3 if kind == "csrmv" and args.no_plan else 2) * args.steps,
+            "gpu_launches": {"csrmv": 3 if args.no_plan else 2, "jitmv": 2, "jitmv_vec": 1,
+                             "jitrows": 1}[kind] * args.steps,
             "clocks": clocks, "roofline": roof,
             "call_us": {"median": float(np.median(ms)) * 1e3, "min": float(np.min(ms)) * 1e3}}
     print(json.dumps(line), flush=True)
@@ -656,12 +684,16 @@ def main():
     ap.add_argument("--f32", action="store_true", help="alias of --g f32")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
-    ap.add_argument("--workload", choices=list(NETWORKS) + ["csrmv", "jitmv", "jitmv_vec"],
+    ap.add_argument("--workload",
+                    choices=list(NETWORKS) + ["csrmv", "jitmv", "jitmv_vec", "jitrows"],
                     default="coba_lif_jit")
     ap.add_argument("--p", type=float, default=0.05, help="microbench connection probability")
     ap.add_argument("--density", type=float, default=0.1, help="microbench spike density")
     ap.add_argument("--law", choices=["homo", "uniform", "normal"], default="uniform")
     ap.add_argument("--fix", action="store_true", help="microbench int64 fixed-point output")
+    ap.add_argument("--gap", choices=["uniform", "geometric"], default="uniform",
+                    help="JIT gap sampler: the paper's U[1, K] (rule J3) or Geo(p) "
+                         "by inversion (rule J10, P:340)")
     ap.add_argument("--no-plan", action="store_true",
                     help="csrmv microbench: split rows on every call (no csrmv_plan)")
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
@@ -674,7 +706,7 @@ def main():
         args.g = "f32"
     if args.impl == "reference":
         run_reference(args)
-    elif args.workload in ("csrmv", "jitmv", "jitmv_vec"):
+    elif args.workload in ("csrmv", "jitmv", "jitmv_vec", "jitrows"):
         run_micro(args)
     else:
         run_ours(args)

@@ -174,7 +174,23 @@ typedef struct {
   double prob;       /* connection probability p in (0, 1]                  */
   uint32_t conn_len; /* K; 0 => bp_conn_len(prob)                           */
   uint32_t seg_len;  /* L; 0 => n_cols (one segment per row)                */
+  int32_t gap_law;   /* bp_gap_law; 0 = the paper's uniform gaps            */
+  int32_t reserved;  /* must be 0                                           */
 } bp_jitconn;
+
+/* Gap sampler of a JIT matrix.
+ * BP_GAP_UNIFORM (the paper's proposal): gaps U[1, K], stationary
+ *   first offset (rules J1-J6); connection density 2/(K+1).
+ * BP_GAP_GEOMETRIC (the baseline the paper compares against, after
+ *   Knight & Nowotny 2020): gaps Geo(p) by CDF
+ *   inversion, G = ceil(logf_j10(u) / fl32(log1p(-p))) with u = ((x >> 8) +
+ *   1) 2^-24 and the op-for-op specified fp32 log of rule J10,
+ *   clamped to [1, L + 1]; first target = segment start + G_0 - 1.  The
+ *   targets form a Bernoulli(p) process (density p exactly).  conn_len is
+ *   ignored; requires n_cols + 128 (L + 1) < 2^32.  Stateless operators only
+ *   (event_mv, mv, row_counts, materialize); networks return
+ *   BP_ERR_UNSUPPORTED. */
+typedef enum { BP_GAP_UNIFORM = 0, BP_GAP_GEOMETRIC = 1 } bp_gap_law;
 
 /* Workspace for bp_jitconn_event_mv_* over output columns [col_begin,
  * col_end): the active list plus, when the partition fits <= 16 shared-memory

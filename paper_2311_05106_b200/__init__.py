@@ -5,7 +5,8 @@ binding in _binding.py (argument marshalling only), plus the network/host
 logic in network.py.  libbp.so is loaded lazily on first use and its absence
 raises; there is no CPU fallback.
 """
-from ._binding import (ACCUMULATE, CONN_CSR, CONN_JIT, LAW_HOMO, LAW_NORMAL,  # noqa: F401
+from ._binding import (ACCUMULATE, CONN_CSR, CONN_JIT, GAP_GEOMETRIC, GAP_UNIFORM,  # noqa: F401
+                       LAW_HOMO, LAW_NORMAL,
                        LAW_UNIFORM, MODEL_HH, MODEL_LIF, OUT_F32, OUT_FIX64,
                        BpError, JitConn, Network, NeuronParams, compact_spikes,
                        conn_len, csrmv_gather, csrmv_plan, event_csrmv, event_csrmv_grad, hh_params, jitconn_event_mv, jitconn_mv,

@@ -44,7 +44,11 @@ class BpError(RuntimeError):
 
 class JitConn(ctypes.Structure):
     _fields_ = [("seed", ctypes.c_uint64), ("prob", ctypes.c_double),
-                ("conn_len", ctypes.c_uint32), ("seg_len", ctypes.c_uint32)]
+                ("conn_len", ctypes.c_uint32), ("seg_len", ctypes.c_uint32),
+                ("gap_law", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+GAP_UNIFORM, GAP_GEOMETRIC = 0, 1   # bp_gap_law (include/bp.h)
 
 
 _F = ctypes.c_float
@@ -196,8 +200,11 @@ def workspace(n_rows: int, device=None) -> torch.Tensor:
                        device=device or torch.cuda.current_device())
 
 
-def jitconn_spec(seed: int, prob: float, conn_len: int = 0, seg_len: int = 0) -> JitConn:
-    return JitConn(int(seed) & (2 ** 64 - 1), float(prob), int(conn_len), int(seg_len))
+def jitconn_spec(seed: int, prob: float, conn_len: int = 0, seg_len: int = 0,
+                 gap_law: int = GAP_UNIFORM) -> JitConn:
+    """bp_jitconn; gap_law GAP_GEOMETRIC selects rule J10 (Geo(p) gaps)."""
+    return JitConn(int(seed) & (2 ** 64 - 1), float(prob), int(conn_len), int(seg_len),
+                   int(gap_law), 0)
 
 
 # ------------------------------------------------------------- operators

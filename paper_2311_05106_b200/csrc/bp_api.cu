@@ -234,6 +234,9 @@ bool launch_stream(bp::CsrStreamArgs a, const StreamPlan &p, cudaStream_t st) {
 // ------------------------------------------------------------- JIT helpers
 struct JitResolved {
   uint32_t K, L;
+  float geo_c;        // rule J10: fl32(log1p(-p)); 0 for uniform gaps
+  uint32_t geo_cap;   // L + 1
+  double density;     // expected connection probability: 2/(K+1) or p
 };
 
 bp_status resolve_jit(const bp_jitconn *spec, int64_t n_cols, JitResolved *r) {
@@ -251,8 +254,29 @@ bp_status resolve_jit(const bp_jitconn *spec, int64_t n_cols, JitResolved *r) {
            static_cast<unsigned long long>(reach));
   uint32_t L = spec->seg_len ? spec->seg_len : static_cast<uint32_t>(n_cols);
   BP_CHECK(L >= 1, BP_ERR_INVALID_ARG, "seg_len 0 with n_cols 0");
+  BP_CHECK(spec->reserved == 0, BP_ERR_INVALID_ARG, "bp_jitconn.reserved must be 0");
   r->K = K;
   r->L = L;
+  r->geo_c = 0.f;
+  r->geo_cap = 0;
+  r->density = 2.0 / (K + 1.0);
+  if (spec->gap_law == BP_GAP_GEOMETRIC) {
+    // rule J10: gaps Geo(p) by inversion, c = fl32(log1p(-p)) (-inf at p = 1)
+    BP_CHECK(spec->prob > 0.0 && spec->prob <= 1.0, BP_ERR_INVALID_ARG,
+             "geometric gaps need prob in (0, 1], got %g", spec->prob);
+    const uint64_t greach = static_cast<uint64_t>(n_cols) + 128ull * (L + 1ull);
+    BP_CHECK(greach < (1ull << 32), BP_ERR_UNSUPPORTED,
+             "n_cols + 128*(seg_len+1) = %llu exceeds 32-bit positions",
+             static_cast<unsigned long long>(greach));
+    r->geo_c = static_cast<float>(std::log1p(-spec->prob));
+    BP_CHECK(r->geo_c != 0.f, BP_ERR_UNSUPPORTED, "prob %g too small for fp32 log1p",
+             spec->prob);
+    r->geo_cap = L + 1u;
+    r->density = spec->prob;
+  } else {
+    BP_CHECK(spec->gap_law == BP_GAP_UNIFORM, BP_ERR_INVALID_ARG, "gap_law %d",
+             spec->gap_law);
+  }
   return BP_OK;
 }
 
@@ -270,23 +294,33 @@ bp::JitSide jit_side(const bp_jitconn *spec, const JitResolved &jr, int law,
   s.w1 = (law == BP_LAW_UNIFORM) ? (w1 - w0) : w1;   // uniform: fp32 span
   s.q = llrint(static_cast<double>(w0) * 4294967296.0);
   s.out = out;
+  s.geo_c = jr.geo_c;
+  s.geo_cap = jr.geo_cap;
   return s;
 }
 
-template <int LAW>
+template <int LAW, bool GEO>
 void launch_jit_law(const bp::JitScatterArgs &a, int kind, int grid,
                     cudaStream_t st) {
   if (kind == BP_OUT_FIX64)
-    bp::k_jit_scatter<LAW, 1><<<grid, bp::kScatterThreads, 0, st>>>(a);
+    bp::k_jit_scatter<LAW, 1, GEO><<<grid, bp::kScatterThreads, 0, st>>>(a);
   else
-    bp::k_jit_scatter<LAW, 0><<<grid, bp::kScatterThreads, 0, st>>>(a);
+    bp::k_jit_scatter<LAW, 0, GEO><<<grid, bp::kScatterThreads, 0, st>>>(a);
 }
 
+template <bool GEO>
+void launch_jit_g(const bp::JitScatterArgs &a, int law, int kind, int grid,
+                  cudaStream_t st) {
+  if (law == BP_LAW_HOMO) launch_jit_law<0, GEO>(a, kind, grid, st);
+  else if (law == BP_LAW_UNIFORM) launch_jit_law<1, GEO>(a, kind, grid, st);
+  else launch_jit_law<2, GEO>(a, kind, grid, st);
+}
+
+// geometric gaps (rule J10) when the projection's geo_c is set
 void launch_jit(const bp::JitScatterArgs &a, int law, int kind, int grid,
                 cudaStream_t st) {
-  if (law == BP_LAW_HOMO) launch_jit_law<0>(a, kind, grid, st);
-  else if (law == BP_LAW_UNIFORM) launch_jit_law<1>(a, kind, grid, st);
-  else launch_jit_law<2>(a, kind, grid, st);
+  if (a.e.geo_c != 0.f) launch_jit_g<true>(a, law, kind, grid, st);
+  else launch_jit_g<false>(a, law, kind, grid, st);
 }
 
 void launch_csr(const bp::CsrScatterArgs &a, int kind, int grid, cudaStream_t st) {
@@ -358,17 +392,17 @@ JitTilePlan jit_tile_plan(int64_t n_rows, int64_t width, int out_kind, int law, 
   return p;
 }
 
-template <int LAW, int KIND, bool VEC>
+template <int LAW, int KIND, bool VEC, bool GEO>
 bool jit_tiled_coop(bp::JitTiledArgs a, const JitTilePlan &p, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(bp::k_jit_tiled<LAW, KIND, VEC>,
+    cudaFuncSetAttribute(bp::k_jit_tiled<LAW, KIND, VEC, GEO>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kSmemOptin - kJitStaticSmem));
     attr = true;
   }
   void *args[] = {&a};
-  if (cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(bp::k_jit_tiled<LAW, KIND, VEC>),
+  if (cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(bp::k_jit_tiled<LAW, KIND, VEC, GEO>),
                                   dim3(p.grid), dim3(bp::kJitTiledThreads), args, p.smem,
                                   st) == cudaSuccess)
     return true;
@@ -376,21 +410,27 @@ bool jit_tiled_coop(bp::JitTiledArgs a, const JitTilePlan &p, cudaStream_t st) {
   return false;
 }
 
-template <bool VEC>
+template <bool VEC, bool GEO>
 bool launch_jit_tiled_v(const bp::JitTiledArgs &a, int law, bool fix, const JitTilePlan &p,
                         cudaStream_t st) {
   if (law == BP_LAW_HOMO)
-    return fix ? jit_tiled_coop<0, 1, VEC>(a, p, st) : jit_tiled_coop<0, 0, VEC>(a, p, st);
+    return fix ? jit_tiled_coop<0, 1, VEC, GEO>(a, p, st)
+               : jit_tiled_coop<0, 0, VEC, GEO>(a, p, st);
   if (law == BP_LAW_UNIFORM)
-    return fix ? jit_tiled_coop<1, 1, VEC>(a, p, st) : jit_tiled_coop<1, 0, VEC>(a, p, st);
-  return fix ? jit_tiled_coop<2, 1, VEC>(a, p, st) : jit_tiled_coop<2, 0, VEC>(a, p, st);
+    return fix ? jit_tiled_coop<1, 1, VEC, GEO>(a, p, st)
+               : jit_tiled_coop<1, 0, VEC, GEO>(a, p, st);
+  return fix ? jit_tiled_coop<2, 1, VEC, GEO>(a, p, st)
+             : jit_tiled_coop<2, 0, VEC, GEO>(a, p, st);
 }
 
 bool launch_jit_tiled(const bp::JitTiledArgs &a, int law, int out_kind, bool vec,
                       const JitTilePlan &p, cudaStream_t st) {
   const bool fix = out_kind == BP_OUT_FIX64;
-  return vec ? launch_jit_tiled_v<true>(a, law, fix, p, st)
-             : launch_jit_tiled_v<false>(a, law, fix, p, st);
+  if (a.s.geo_c != 0.f)
+    return vec ? launch_jit_tiled_v<true, true>(a, law, fix, p, st)
+               : launch_jit_tiled_v<false, true>(a, law, fix, p, st);
+  return vec ? launch_jit_tiled_v<true, false>(a, law, fix, p, st)
+             : launch_jit_tiled_v<false, false>(a, law, fix, p, st);
 }
 
 // Event scatter (spikes) or non-event product (v, reading MV1); exactly one
@@ -437,7 +477,7 @@ bp_status jit_event_mv(int law, const bp_jitconn *spec, float w0, float w1,
   // 510 vs 551 us on the 100 k x 100 k, p = 0.05, 10 % cell)
   // short rows (< ~1000 events per active row in the partition): the
   // partial tiles cost more than the atomics they save
-  const double row_events = 2.0 / (jr.K + 1.0) * static_cast<double>(col_end - col_begin);
+  const double row_events = jr.density * static_cast<double>(col_end - col_begin);
   const bool tiled = tp.ok && n_rows > 0 && ws_bytes >= tp.ws_bytes &&
                      !std::getenv("BP_JIT_DIRECT") &&
                      ((law != BP_LAW_NORMAL && row_events >= 1000.0) ||
@@ -875,9 +915,10 @@ bp_status bp_jitconn_row_counts(const bp_jitconn *spec, int64_t n_rows,
   if (s != BP_OK) return s;
   if (n_rows == 0) return BP_OK;
   bp::JitSide side = jit_side(spec, jr, BP_LAW_HOMO, 0.f, 0.f, 0, n_cols, nullptr);
-  bp::k_jit_rows<<<grid_for_items(n_rows, sms), bp::kScatterThreads, 0,
-                   as_stream(stream)>>>(side, n_rows, static_cast<uint32_t>(n_cols),
-                                        BP_LAW_HOMO, nullptr, counts, nullptr, nullptr);
+  auto rows = side.geo_c != 0.f ? bp::k_jit_rows<true> : bp::k_jit_rows<false>;
+  rows<<<grid_for_items(n_rows, sms), bp::kScatterThreads, 0, as_stream(stream)>>>(
+      side, n_rows, static_cast<uint32_t>(n_cols), BP_LAW_HOMO, nullptr, counts, nullptr,
+      nullptr);
   return launched();
 }
 
@@ -897,9 +938,9 @@ bp_status bp_jitconn_materialize(const bp_jitconn *spec, int law, float w0,
   if (s != BP_OK) return s;
   if (n_rows == 0) return BP_OK;
   bp::JitSide side = jit_side(spec, jr, law, w0, w1, 0, n_cols, nullptr);
-  bp::k_jit_rows<<<grid_for_items(n_rows, sms), bp::kScatterThreads, 0,
-                   as_stream(stream)>>>(side, n_rows, static_cast<uint32_t>(n_cols),
-                                        law, indptr, nullptr, indices, data);
+  auto rows = side.geo_c != 0.f ? bp::k_jit_rows<true> : bp::k_jit_rows<false>;
+  rows<<<grid_for_items(n_rows, sms), bp::kScatterThreads, 0, as_stream(stream)>>>(
+      side, n_rows, static_cast<uint32_t>(n_cols), law, indptr, nullptr, indices, data);
   return launched();
 }
 
@@ -1399,6 +1440,10 @@ bp_status bp_network_create(const bp_network_desc *desc, bp_stream stream,
   if (desc->conn == BP_CONN_JIT) {
     s = resolve_jit(&desc->jit_exc, desc->n, &net->jr_e);
     if (s == BP_OK) s = resolve_jit(&desc->jit_inh, desc->n, &net->jr_i);
+    if (s == BP_OK && (net->jr_e.geo_c != 0.f || net->jr_i.geo_c != 0.f)) {
+      s = fail(BP_ERR_UNSUPPORTED,
+               "networks use the uniform gap sampler (rule J3); gap_law must be 0");
+    }
     if (s == BP_OK &&
         (desc->col_begin % net->jr_e.L || desc->col_begin % net->jr_i.L ||
          (desc->col_end != desc->n &&

@@ -41,7 +41,7 @@ struct JitTiledArgs {
 
 // VEC: non-event product with a float vector (every row, contribution v[r] w:
 // fl32 product in f32 mode, the exact fp64 product rounded once in fixed point)
-template <int LAW, int KIND, bool VEC>
+template <int LAW, int KIND, bool VEC, bool GEO>
 __global__ void __launch_bounds__(kJitTiledThreads, 1) k_jit_tiled(JitTiledArgs a) {
   extern __shared__ __align__(128) unsigned char sm[];
   constexpr bool HOMO = LAW == 0 && !VEC;     // count events, scale once
@@ -95,12 +95,12 @@ __global__ void __launch_bounds__(kJitTiledThreads, 1) k_jit_tiled(JitTiledArgs 
     const uint32_t stop = min(seg_end, g1);
     if (seg_begin >= g1 || seg_end <= g0) continue;             // warp-uniform
     u32x4 g = philox_block(s.seed, kTagGap, row, seg, lane);
-    uint32_t start = seg_begin + first_offset(s.seed, s.K, row, seg);
+    uint32_t start = seg_begin + jit_first<GEO>(s, row, seg);
     uint32_t chunk = 0;
     while (start < stop) {                                      // warp-uniform
       const uint32_t blk = chunk * 32u + lane;
-      const uint32_t q0 = bounded(1u, s.K, g.x), q1 = bounded(1u, s.K, g.y);
-      const uint32_t q2 = bounded(1u, s.K, g.z), q3 = bounded(1u, s.K, g.w);
+      const uint32_t q0 = jit_gap<GEO>(s, g.x), q1 = jit_gap<GEO>(s, g.y);
+      const uint32_t q2 = jit_gap<GEO>(s, g.z), q3 = jit_gap<GEO>(s, g.w);
       const uint32_t p1 = q0, p2 = q0 + q1, p3 = p2 + q2, t = p3 + q3;
       uint32_t incl = t;
 #pragma unroll

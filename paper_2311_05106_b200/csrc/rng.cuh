@@ -87,6 +87,45 @@ __device__ __forceinline__ float normal_weight(uint32_t x1, uint32_t x2,
   return __fmaf_rn(sigma, __double2float_rn(z), mu);
 }
 
+// Rule J10 (geometric-gap sampler; NEXT 4): op-for-op specified fp32
+// natural log on (0, 1] -- the oracle runs the same operations, so both
+// sides draw identical gaps.  u = m 2^e; m in [sqrt(1/2), sqrt 2];
+// log m = 2 atanh(s), s = (m-1)/(m+1), as 2s + 2s z r(z), z = s^2.
+__device__ __forceinline__ float logf_j10(float u) {
+  const uint32_t b = __float_as_uint(u);
+  int e = static_cast<int>(b >> 23) - 127;
+  float m = __uint_as_float((b & 0x7FFFFFu) | 0x3F800000u);
+  if (m > 1.41421353816986083984375f) {
+    m = __fmul_rn(m, 0.5f);
+    e += 1;
+  }
+  const float f = __fsub_rn(m, 1.0f);
+  const float s = __fdiv_rn(f, __fadd_rn(2.0f, f));
+  const float z = __fmul_rn(s, s);
+  float r = __fmaf_rn(z, 1.0f / 11.0f, 1.0f / 9.0f);
+  r = __fmaf_rn(z, r, 1.0f / 7.0f);
+  r = __fmaf_rn(z, r, 1.0f / 5.0f);
+  r = __fmaf_rn(z, r, 1.0f / 3.0f);
+  const float zr = __fmul_rn(z, r);
+  const float s2 = __fadd_rn(s, s);
+  const float lm = __fmaf_rn(s2, zr, s2);
+  const float ef = static_cast<float>(e);
+  return __fmaf_rn(ef, 0.693145751953125f, __fmaf_rn(ef, 1.428606765330187e-6f, lm));
+}
+
+// Rule J10 gap G ~ Geo(p) from one word: u = ((x >> 8) + 1) 2^-24 in (0, 1],
+// t = log(u) / c with c = fl32(log1p(-p)) (IEEE division), G = ceil(t)
+// clamped to [1, cap], cap = L + 1 (a gap that long leaves the segment).
+__device__ __forceinline__ uint32_t geo_gap(uint32_t x, float c, uint32_t cap) {
+  const float u = __fmul_rn(__uint2float_rn((x >> 8) + 1u), 0x1p-24f);
+  const float t = __fdiv_rn(logf_j10(u), c);
+  if (!(t < __uint2float_rn(cap))) return cap;
+  const float ct = ceilf(t);
+  if (ct < 1.0f) return 1u;
+  const uint32_t g = __float2uint_rz(ct);
+  return g > cap ? cap : g;
+}
+
 // Rule F1: q(w) = round-half-even(w * 2^32) as int64.
 __device__ __forceinline__ long long quantize(float w) {
   return __double2ll_rn(__dmul_rn(static_cast<double>(w), 4294967296.0));

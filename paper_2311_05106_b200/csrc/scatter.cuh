@@ -412,7 +412,26 @@ struct JitSide {
   float w0, w1;                // homo: (w, -); uniform: (lo, hi-lo); normal: (mu, sigma)
   long long q;                 // quantize(w0) for homo
   void *out;                   // indexed c - col_begin
+  float geo_c;                 // 0: uniform gaps (J3); else fl32(log1p(-p)) (rule J10)
+  uint32_t geo_cap;            // L + 1
 };
+
+// Gap e of a JIT row from its word x: U[1, K] (rules J3, J6) or Geo(p)
+// (rule J10).  A template parameter of the hot kernels, so the paper's
+// uniform sampler pays nothing for the other one.  The network kernels
+// (step.cuh) use the uniform rule only.
+template <bool GEO>
+__device__ __forceinline__ uint32_t jit_gap(const JitSide &s, uint32_t x) {
+  if (GEO) return geo_gap(x, s.geo_c, s.geo_cap);
+  return bounded(1u, s.K, x);
+}
+// Offset of the first target from the segment start: rule J5 or G_0 - 1 (J10).
+template <bool GEO>
+__device__ __forceinline__ uint32_t jit_first(const JitSide &s, uint32_t row, uint32_t seg) {
+  if (GEO)
+    return geo_gap(philox_block(s.seed, kTagFirst, row, seg, 0).x, s.geo_c, s.geo_cap) - 1u;
+  return first_offset(s.seed, s.K, row, seg);
+}
 
 struct JitScatterArgs {
   JitSide e, i;
@@ -441,6 +460,8 @@ __device__ __forceinline__ JitSide pick(bool second, const JitSide &x,
   s.w1 = second ? y.w1 : x.w1;
   s.q = second ? y.q : x.q;
   s.out = second ? y.out : x.out;
+  s.geo_c = second ? y.geo_c : x.geo_c;
+  s.geo_cap = second ? y.geo_cap : x.geo_cap;
   return s;
 }
 
@@ -462,7 +483,7 @@ __device__ __forceinline__ void jit_emit(const JitSide &s, uint32_t pos,
   else add_fix(s.out, c, LAW == 0 ? s.q : quantize(w), pol);
 }
 
-template <int LAW, int KIND>
+template <int LAW, int KIND, bool GEO>
 __global__ void __launch_bounds__(kScatterThreads)
 k_jit_scatter(JitScatterArgs a) {
   const int n_active = a.v ? 0 : *a.count;
@@ -491,12 +512,12 @@ k_jit_scatter(JitScatterArgs a) {
     // The first gap block does not depend on the first offset: issue both
     // Philox evaluations back to back so their 10-round chains overlap.
     u32x4 g = philox_block(s.seed, kTagGap, row, seg, lane);
-    uint32_t start = seg_begin + first_offset(s.seed, s.K, row, seg);
+    uint32_t start = seg_begin + jit_first<GEO>(s, row, seg);
     uint32_t chunk = 0;
     while (start < seg_end) {                      // warp-uniform
       const uint32_t blk = chunk * 32u + lane;
-      const uint32_t g0 = bounded(1u, s.K, g.x), g1 = bounded(1u, s.K, g.y);
-      const uint32_t g2 = bounded(1u, s.K, g.z), g3 = bounded(1u, s.K, g.w);
+      const uint32_t g0 = jit_gap<GEO>(s, g.x), g1 = jit_gap<GEO>(s, g.y);
+      const uint32_t g2 = jit_gap<GEO>(s, g.z), g3 = jit_gap<GEO>(s, g.w);
       const uint32_t p1 = g0, p2 = g0 + g1, p3 = p2 + g2, t = p3 + g3;
       uint32_t incl = t;
 #pragma unroll
@@ -539,7 +560,9 @@ k_jit_scatter(JitScatterArgs a) {
   count_events(a.events, ev);
 }
 
-// Row counts / materialisation with the kernel's own generator (debug).
+// Row counts / materialisation with the kernel's own generator (debug;
+// also the gap-sampler cost benchmark: row counts are gap chains only).
+template <bool GEO>
 __global__ void __launch_bounds__(kScatterThreads)
 k_jit_rows(JitSide s, int64_t n_rows, uint32_t n_cols, int law,
            const int64_t *__restrict__ indptr, int64_t *__restrict__ counts,
@@ -553,13 +576,13 @@ k_jit_rows(JitSide s, int64_t n_rows, uint32_t n_cols, int law,
     for (uint32_t seg = 0; seg < s.n_seg; ++seg) {
       const uint32_t seg_begin = seg * s.L;
       const uint32_t seg_end = min(seg_begin + s.L, n_cols);
-      uint32_t start = seg_begin + first_offset(s.seed, s.K, row, seg);
+      uint32_t start = seg_begin + jit_first<GEO>(s, row, seg);
       uint32_t chunk = 0;
       while (start < seg_end) {
         const uint32_t blk = chunk * 32u + lane;
         const u32x4 g = philox_block(s.seed, kTagGap, row, seg, blk);
-        const uint32_t g0 = bounded(1u, s.K, g.x), g1 = bounded(1u, s.K, g.y);
-        const uint32_t g2 = bounded(1u, s.K, g.z), g3 = bounded(1u, s.K, g.w);
+        const uint32_t g0 = jit_gap<GEO>(s, g.x), g1 = jit_gap<GEO>(s, g.y);
+        const uint32_t g2 = jit_gap<GEO>(s, g.z), g3 = jit_gap<GEO>(s, g.w);
         const uint32_t p1 = g0, p2 = g0 + g1, p3 = p2 + g2, t = p3 + g3;
         uint32_t incl = t;
 #pragma unroll
