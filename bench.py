@@ -124,7 +124,8 @@ class ClockSampler:
 # CPU oracle leg (cpu_baseline and --impl reference): the oracle as it stands
 # ---------------------------------------------------------------------------
 
-def oracle_sample_steps(n_total: int, n_steps: int, fraction: float, seed: int = 7):
+def oracle_sample_steps(n_total: int, n_steps: int, fraction: float, seed: int = 7,
+                        wl: str = "coba_lif_jit"):
     """Time the oracle on a bounded sample of the same workload: each step
     delivers the spikes of `fraction` of the presynaptic rows (all of their
     events, E and I projections, Bernoulli(22 Hz * dt) activity -- the
@@ -137,9 +138,10 @@ def oracle_sample_steps(n_total: int, n_steps: int, fraction: float, seed: int =
     from paper_2311_05106_b200.network import SEED_E, SEED_I
     oracle.build()
     n_exc = n_total * 4 // 5
-    K = oracle.conn_len(80.0 / n_total)
-    je = oracle.JitSpec(SEED_E, K, n_total, oracle.LAW_HOMO, 0.6)
-    ji = oracle.JitSpec(SEED_I, K, n_total, oracle.LAW_HOMO, 6.7)
+    p, w_e, w_i = net_params(wl, n_total)
+    K = oracle.conn_len(p)
+    je = oracle.JitSpec(SEED_E, K, n_total, oracle.LAW_HOMO, w_e)
+    ji = oracle.JitSpec(SEED_I, K, n_total, oracle.LAW_HOMO, w_i)
     n_rows_e = max(1, int(n_exc * fraction))
     n_rows_i = max(1, int((n_total - n_exc) * fraction))
     n_upd = max(32, int(n_total * fraction))
@@ -182,8 +184,9 @@ def oracle_full_network(wl, n_total, csr, n_steps):
     spec = NETWORKS[wl]
     n = n_total
     n_exc = n * 4 // 5
-    K = oracle.conn_len(80.0 / n)
-    w = (0.6, 6.7) if spec["model"] == "lif" else (6.0, 67.0)
+    p, w_e, w_i = net_params(wl, n)
+    K = oracle.conn_len(p)
+    w = (w_e, w_i)
     if csr is None:
         pe = oracle.Projection(0, n_exc, jit=oracle.JitSpec(SEED_E, K, n, oracle.LAW_HOMO, w[0]))
         pi = oracle.Projection(n_exc, n - n_exc, jit=oracle.JitSpec(SEED_I, K, n, oracle.LAW_HOMO, w[1]))
@@ -215,10 +218,10 @@ def oracle_full_network(wl, n_total, csr, n_steps):
 def cpu_baseline(wl, n_total, csr, budget_s: float = 15.0):
     if n_total > 1_000_000:
         fraction = 1.0 / 32
-        secs, events, _ = oracle_sample_steps(n_total, 2, fraction)   # calibrate
+        secs, events, _ = oracle_sample_steps(n_total, 2, fraction, wl=wl)   # calibrate
         per_step = max(secs / 2, 1e-3)
         steps = max(2, min(5000, int(budget_s / per_step)))
-        secs, events, upd = oracle_sample_steps(n_total, steps, fraction)
+        secs, events, upd = oracle_sample_steps(n_total, steps, fraction, wl=wl)
         return {"value": events / secs, "unit": UNIT, "cores": 1, "kind": "oracle",
                 "sample": (f"{steps} steps of the {n_total:,}-neuron network with 1/32 of "
                            f"presynaptic rows active-eligible (Bernoulli 22 Hz x dt) and 1/32 "
@@ -275,7 +278,29 @@ NETWORKS = {
                          cfg="config 1: COBA-LIF 4000 neurons (3200E/800I), p=0.02, CSR"),
     "hh400k_csr": dict(model="hh", conn="csr", n=400_000, scaling="strong",
                        cfg="config 4: COBA-HH 400k neurons, fan-in 80, CSR"),
+    # Fig S3B / S3C regimes at the config-3 size
+    "coba4m_k1000": dict(model="lif", conn="jit", n=4_000_000, scaling="strong", fan_in=1000,
+                         cfg="Fig S3B: COBA-LIF JIT 4M neurons, 1000 synapses per neuron, "
+                             "weights x 80/1000"),
+    "coba4m_p001": dict(model="lif", conn="jit", n=4_000_000, scaling="strong", p=0.001,
+                        cfg="Fig S3C: COBA-LIF JIT 4M neurons, fixed p = 0.001 (fan-in 4000), "
+                            "weights x 80/4000"),
 }
+
+
+def net_params(wl, n):
+    """(p, w_exc, w_inh) of a workload: fan-in 80 unless the workload
+    sets `fan_in` (Fig S3B) or a fixed `p` (Fig S3C); then the weights are
+    rescaled by 80 / fan-in (reading R29: the mean synaptic drive K w of
+    P:974-981 is kept)."""
+    spec = NETWORKS[wl]
+    w = (0.6, 6.7) if spec["model"] == "lif" else (6.0, 67.0)
+    if "p" in spec:
+        p = spec["p"]
+    else:
+        p = spec.get("fan_in", 80) / n
+    scale = 80.0 / (p * n) if ("p" in spec or "fan_in" in spec) else 1.0
+    return p, w[0] * scale, w[1] * scale
 
 
 def network_size(wl, world):
@@ -293,14 +318,15 @@ def build_network(wl, world, rank, fixed, dev):
     csr = None
     if spec["conn"] == "csr":
         n_exc = n * 4 // 5
-        p = 80.0 / n
+        p = net_params(wl, n)[0]
         ipe, ixe, _ = bp.jitconn_materialize(bp.jitconn_spec(SEED_E, p), n_exc, n,
                                              with_data=False, device=dev)
         ipi, ixi, _ = bp.jitconn_materialize(bp.jitconn_spec(SEED_I, p), n - n_exc, n,
                                              with_data=False, device=dev)
         csr = ((ipe, ixe), (ipi, ixi))
+    p, w_e, w_i = net_params(wl, n)
     return CobaNetwork(n, model=spec["model"], conn=spec["conn"], fixed=fixed, rank=rank,
-                       world=world, device=dev, csr=csr), csr
+                       world=world, device=dev, csr=csr, p=p, w_exc=w_e, w_inh=w_i), csr
 
 
 def state_bytes_per_neuron(model, fixed):
@@ -442,7 +468,9 @@ def run_ours(args):
         "data": "synthetic",
         "config": {"workload": wl, "description": spec["cfg"], "n_total": n_total,
                    "n_per_gpu": n_local, "model": spec["model"], "connectivity": spec["conn"],
-                   "fan_in": 80, "p": 80.0 / n_total, "dt_ms": DT_MS,
+                   "fan_in": round(net_params(wl, n_total)[0] * n_total, 3),
+                   "p": net_params(wl, n_total)[0],
+                   "w_exc_inh": list(net_params(wl, n_total)[1:]), "dt_ms": DT_MS,
                    "g": {"fix64": "int64 fixed point 2^-32 (rule F1)",
                          "fix32": "int32 fixed point 2^-%d (rule F2), saturations: %d" % (
                              20 if spec["model"] == "lif" else 16, sat1),

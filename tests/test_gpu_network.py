@@ -28,12 +28,12 @@ def _g_dtype(fixed):
             "f32": np.float32}[fixed]
 
 
-def _oracle_lif(orc, n, fixed, csr=None):
+def _oracle_lif(orc, n, fixed, csr=None, p=None, w=(0.6, 6.7)):
     n_exc = n * 4 // 5
-    K = orc.conn_len(80.0 / n)
+    K = orc.conn_len(80.0 / n if p is None else p)
     if csr is None:
-        pe = orc.Projection(0, n_exc, jit=orc.JitSpec(SEED_E, K, n, orc.LAW_HOMO, 0.6))
-        pi = orc.Projection(n_exc, n - n_exc, jit=orc.JitSpec(SEED_I, K, n, orc.LAW_HOMO, 6.7))
+        pe = orc.Projection(0, n_exc, jit=orc.JitSpec(SEED_E, K, n, orc.LAW_HOMO, w[0]))
+        pi = orc.Projection(n_exc, n - n_exc, jit=orc.JitSpec(SEED_I, K, n, orc.LAW_HOMO, w[1]))
     else:
         (ipe, ixe), (ipi, ixi) = csr
         pe = orc.Projection(0, n_exc, csr=(ipe, ixe, None), w_homo=0.6)
@@ -249,3 +249,26 @@ def test_coba_lif_dense_delivery_bit_exact(orc, mode, monkeypatch):
     assert want.sum() > 0
     assert np.array_equal(_raster(raster, n), want)
     assert np.array_equal(net.state["v"].cpu().numpy().view(np.uint32), st["v"].view(np.uint32))
+
+
+# Fig S3B / S3C regimes (NEXT 4): 1000 synapses per neuron, and a
+# fixed p = 0.001, weights rescaled by 80 / fan-in (reading R29).
+@pytest.mark.parametrize("mode", ["fix64", "f32"])
+@pytest.mark.parametrize("n,p,steps", [(20_000, 0.05, 400),      # fan-in 1000 (S3B)
+                                       (100_000, 0.001, 200),    # p = 0.001 (S3C)
+                                       (50_000, 0.02, 200)])     # fan-in 1000 again, 2 tiles+
+def test_fig_s3_regimes_bit_exact(orc, n, p, steps, mode):
+    scale = 80.0 / (p * n)
+    w = (0.6 * scale, 6.7 * scale)
+    net = CobaNetwork(n, conn="jit", fixed=mode, p=p, w_exc=w[0], w_inh=w[1])
+    raster = torch.zeros((steps, (n + 31) // 32), dtype=torch.int32, device="cuda")
+    net.run(steps, raster)
+    st, pe, pi = _oracle_lif(orc, n, mode, p=p, w=w)
+    want = orc.run_network("lif", orc.lif_params(), st, pe, pi, steps)
+    got = _raster(raster, n)
+    assert want.sum() > 0
+    assert np.array_equal(got, want)
+    assert np.array_equal(net.state["v"].cpu().numpy().view(np.uint32), st["v"].view(np.uint32))
+    g = net.state["g_e"].cpu().numpy()
+    assert np.array_equal(g.view(np.uint32) if mode == "f32" else g,
+                          st["g_e"].view(np.uint32) if mode == "f32" else st["g_e"])
