@@ -361,6 +361,13 @@ bp_status bp_network_step(bp_network *net, int64_t n_steps,
 bp_status bp_network_scatter(bp_network *net, bp_stream stream);
 bp_status bp_network_update(bp_network *net, uint32_t *raster_row,
                             bp_stream stream);
+/* bp_network_update, and make `exchange_stream` wait (cudaStreamWaitEvent)
+ * only for this step's spike words -- before the local binning kernel -- so
+ * the caller's all-gather on exchange_stream overlaps the binning (SURVEY
+ * 8(e) overlap option (i)).  The caller must order its next
+ * bp_network_scatter on `stream` after the exchange. */
+bp_status bp_network_update_overlap(bp_network *net, uint32_t *raster_row,
+                                    bp_stream stream, bp_stream exchange_stream);
 /* Device counters since create: [0] = local spikes, [1] = synaptic events
  * delivered into local neurons, [2] = saturated BP_OUT_FIX32 conductance
  * updates (0 in a well-scaled run).  Copies into host uint64[3];

@@ -33,7 +33,7 @@ EXPORTED = [
     "bp_jitconn_event_mv_normal", "bp_jitconn_row_counts",
     "bp_jitconn_materialize", "bp_neuron_step", "bp_network_workspace_bytes",
     "bp_network_create", "bp_network_step", "bp_network_scatter",
-    "bp_network_update", "bp_network_counters", "bp_network_profile_begin",
+    "bp_network_update", "bp_network_update_overlap", "bp_network_counters", "bp_network_profile_begin",
     "bp_network_profile_end", "bp_network_destroy",
 ]
 
@@ -139,6 +139,7 @@ def lib():
         L.bp_network_profile_end.argtypes = [P, P, P, P]
         L.bp_network_scatter.argtypes = [P, P]
         L.bp_network_update.argtypes = [P, P, P]
+        L.bp_network_update_overlap.argtypes = [P, P, P, P]
         L.bp_network_counters.argtypes = [P, P, P]
         L.bp_network_destroy.argtypes = [P]
         L.bp_network_destroy.restype = None
@@ -468,6 +469,13 @@ class Network:
 
     def update(self, raster_row=None, stream=None):
         _check(lib().bp_network_update(self._h, _ptr(raster_row), _stream(stream)))
+
+    def update_overlap(self, exchange_stream, raster_row=None, stream=None):
+        """update(); `exchange_stream` (torch.cuda.Stream) waits for this
+        step's spike words only, so an all-gather there overlaps the local
+        binning kernel."""
+        _check(lib().bp_network_update_overlap(self._h, _ptr(raster_row), _stream(stream),
+                                               _stream(exchange_stream)))
 
     def counters(self, stream=None):
         """-> (local spikes, synaptic events delivered, saturated FIX32 updates)."""

@@ -1042,6 +1042,7 @@ struct bp_network {
   bp::NeuronArgs neuron;
   // profiling: 3 events per step (before scatter, between, after update)
   cudaEvent_t *prof_ev = nullptr;
+  cudaEvent_t xev = nullptr;      // bp_network_update_overlap: spike words final
   int64_t prof_cap = 0, prof_used = 0;
   float keep_frac = 0.f;          // L2 evict_last fraction of g (cache.cuh)
   // fused-step event buckets (step.cuh), two parities, owned by the network
@@ -1608,6 +1609,20 @@ bp_status bp_network_update(bp_network *net, uint32_t *raster_row, bp_stream str
   return launch_step(net, raster_row, as_stream(stream));
 }
 
+bp_status bp_network_update_overlap(bp_network *net, uint32_t *raster_row, bp_stream stream,
+                                    bp_stream exchange_stream) {
+  bp_status s = device_ready(nullptr);
+  if (s != BP_OK) return s;
+  BP_CHECK(net != nullptr, BP_ERR_INVALID_ARG, "net is NULL");
+  if (net->xev == nullptr) BP_CUDA(cudaEventCreateWithFlags(&net->xev, cudaEventDisableTiming));
+  // k_step (spike words of this step) -> record xev -> local binning; the
+  // exchange stream waits for xev only, so the all-gather overlaps k_bin
+  s = launch_step(net, raster_row, as_stream(stream), nullptr, net->xev);
+  if (s != BP_OK) return s;
+  BP_CUDA(cudaStreamWaitEvent(as_stream(exchange_stream), net->xev, 0));
+  return BP_OK;
+}
+
 bp_status bp_network_counters(bp_network *net, uint64_t *host_out, bp_stream stream) {
   bp_status s = device_ready(nullptr);
   if (s != BP_OK) return s;
@@ -1620,6 +1635,7 @@ bp_status bp_network_counters(bp_network *net, uint64_t *host_out, bp_stream str
 }
 
 void bp_network_destroy(bp_network *net) {
+  if (net && net->xev) cudaEventDestroy(net->xev);
   if (net && net->bk_mem) cudaFree(net->bk_mem);
   if (net && net->small_steps) cudaFree(net->small_steps);
   if (net && net->prof_ev) {

@@ -161,14 +161,25 @@ class CobaNetwork:
     def run(self, n_steps: int, raster: torch.Tensor | None = None, counts=None):
         self.net.step(n_steps, raster, counts)
 
-    # several devices: scatter -> update -> all-gather, per step
-    def step_distributed(self, group=None, raster_row=None):
-        self.net.scatter()
-        self.net.update(raster_row)
+    # several devices: scatter -> update -> all-gather, per step.  The
+    # all-gather runs on a side stream that waits only for the update kernel's
+    # spike words, so it overlaps the local binning kernel (SURVEY 8(e)
+    # option (i)); the next scatter waits for it.  overlap=False: one stream.
+    def step_distributed(self, group=None, raster_row=None, overlap: bool = True):
         if self._send is None:
             self._send = torch.empty(self.part.local_words, dtype=torch.int32,
                                      device=self.spikes.device)
-        exchange_spikes(self.spikes, self.part, group, self._send)
+            self._comm = torch.cuda.Stream(device=self.spikes.device)
+        self.net.scatter()
+        if not overlap:
+            self.net.update(raster_row)
+            exchange_spikes(self.spikes, self.part, group, self._send)
+            return
+        compute = torch.cuda.current_stream(self.spikes.device)
+        self.net.update_overlap(self._comm, raster_row)
+        with torch.cuda.stream(self._comm):
+            exchange_spikes(self.spikes, self.part, group, self._send)
+        compute.wait_stream(self._comm)
 
     def counters(self):
         return self.net.counters()

@@ -27,7 +27,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _rank(rank, world, port, out_dir, mode):
+def _rank(rank, world, port, out_dir, mode, overlap):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -37,7 +37,7 @@ def _rank(rank, world, port, out_dir, mode):
     net = CobaNetwork(N, conn="jit", fixed=mode, rank=rank, world=world, device="cuda:0")
     rows = []
     for _ in range(STEPS):
-        net.step_distributed()
+        net.step_distributed(overlap=overlap)
         rows.append(net.spikes.cpu().numpy().view(np.uint32).copy())
     np.save(os.path.join(out_dir, f"r{rank}.npy"), np.stack(rows))
     np.save(os.path.join(out_dir, f"v{rank}.npy"), net.state["v"].cpu().numpy())
@@ -46,10 +46,13 @@ def _rank(rank, world, port, out_dir, mode):
 
 
 @pytest.mark.timeout(900)
-@pytest.mark.parametrize("mode", ["fix32", "f32"])
-def test_two_ranks_on_one_gpu_gloo(orc, tmp_path, mode):
+@pytest.mark.parametrize("mode,overlap", [("fix32", True), ("f32", True), ("f32", False)])
+def test_two_ranks_on_one_gpu_gloo(orc, tmp_path, mode, overlap):
+    """overlap: the all-gather runs on a side stream that waits only for the
+    update kernel (bp_network_update_overlap), concurrent with the binning."""
     world = 2
-    mp.start_processes(_rank, args=(world, _free_port(), str(tmp_path), mode), nprocs=world,
+    mp.start_processes(_rank, args=(world, _free_port(), str(tmp_path), mode, overlap),
+                       nprocs=world,
                        join=True, start_method="spawn")
     r0, r1 = np.load(tmp_path / "r0.npy"), np.load(tmp_path / "r1.npy")
     assert np.array_equal(r0, r1)
