@@ -548,12 +548,11 @@ def run_e2e(args, wl, fixed, dev):
 # log/cos/sqrt, counted as 40).  Issue peak: 148 SMs x 4 schedulers x 32
 # lanes x 1 warp-instruction per cycle at the sampled SM clock.
 JIT_OPS_PER_EVENT = {"homo": 21.5, "uniform": 38.5, "normal": 91.5}
-# Per gap draw: uniform (rule J3) = Philox share 15 + multiply-shift 2 +
-# running sum 1 + scan share 2.5 = 20.5; geometric (rule J10) replaces the
-# multiply-shift by u, the specified log (incl. one IEEE division ~ 10),
-# the division by c (~ 10), ceil and clamps: + ~40 (instruction counts of
-# the SASS).
-JIT_OPS_PER_GAP = {"uniform": 20.5, "geometric": 60.5}
+# Per gap draw, MEASURED: ncu smsp__inst_executed x 32 lanes / gaps of one
+# k_jit_rows call (100 k x 100 k, p = 0.05; profiles/r01/ncu_gap_samplers.json):
+# the paper's U[1, K] gaps (rule J3) 27.4 lane instructions, Geo(p) by
+# inversion with the specified log (rule J10) 86.8.
+JIT_OPS_PER_GAP = {"uniform": 27.4, "geometric": 86.8}
 
 
 def run_micro(args):
