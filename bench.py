@@ -364,12 +364,18 @@ def run_ours(args):
     small = world == 1 and n_total <= 4096
     stream = torch.cuda.current_stream()
 
+    graph = {"g": None, "period": 1, "note": None}
+
     def steps(k):
         if world == 1:
             net.run(k)
-        else:
-            for _ in range(k):
-                net.step_distributed()
+            return
+        if graph["g"] is not None:
+            for _ in range(k // graph["period"]):
+                graph["g"].replay()
+            k %= graph["period"]
+        for _ in range(k):
+            net.step_distributed()
 
     def barrier():
         if world > 1:
@@ -379,6 +385,16 @@ def run_ours(args):
     # warm-up (untimed)
     steps(args.warmup)
     barrier()
+    if world > 1 and args.dist_backend == "nccl" and not args.no_graph:
+        # one CUDA graph per step period (network.py capture): the per-step
+        # host calls cost about as much as the GPU step
+        try:
+            graph["g"], graph["period"] = net.capture()
+            graph["note"] = "CUDA graph of %d steps (exchange included), replayed" % graph["period"]
+            steps(2 * graph["period"])                       # warm replays
+        except Exception as exc:                           # eager fallback
+            graph["g"], graph["note"] = None, "eager (graph capture failed: %s)" % exc
+        barrier()
     sp0, ev0, _ = net.counters()
 
     # timed region: exactly K steps, CUDA events on the launching stream
@@ -476,6 +492,8 @@ def run_ours(args):
                              20 if spec["model"] == "lif" else 16, sat1),
                          "f32": "fp32, increments fl32(count*w) (rule N1-f32), bit-exact vs oracle"}[args.g],
                    "parallelism": f"postsynaptic partition x{world}",
+                   "host_loop": ("library time loop (bp_network_step)" if world == 1
+                                 else graph["note"] or "eager per-step calls"),
                    "l2": (f"state {state_mb:.0f} MB/GPU > 2 x 126 MB L2: no flush needed"
                           if state_mb > 252 else
                           f"state {state_mb:.1f} MB is L2/SM-resident by design (the workload is that small)"),
@@ -711,6 +729,8 @@ def main():
     ap.add_argument("--f32", action="store_true", help="alias of --g f32")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="N > 1: eager per-step calls instead of the captured CUDA graph")
     ap.add_argument("--workload",
                     choices=list(NETWORKS) + ["csrmv", "jitmv", "jitmv_vec", "jitrows"],
                     default="coba_lif_jit")

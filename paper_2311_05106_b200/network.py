@@ -181,6 +181,20 @@ class CobaNetwork:
             exchange_spikes(self.spikes, self.part, group, self._send)
         compute.wait_stream(self._comm)
 
+    def capture(self, group=None, overlap: bool = True):
+        """CUDA graph of one period of step_distributed -- lcm(2, delay + 1)
+        steps, after which the host-side step parity and bucket slot repeat
+        -- so a replay costs one launch instead of ~10 host calls per step
+        (their enqueue cost is close to the GPU step time).  The exchange is
+        captured with it (NCCL; gloo cannot be captured).  Call after at least
+        one eager step_distributed.  Returns (graph, steps per replay)."""
+        period = math.lcm(2, self.delay + 1)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for _ in range(period):
+                self.step_distributed(group, overlap=overlap)
+        return graph, period
+
     def counters(self):
         return self.net.counters()
 
