@@ -348,22 +348,23 @@ constexpr size_t kJitStaticSmem = 1024;
 
 struct JitTilePlan {
   bool ok;
+  bool c16;            // homogeneous counts in 16 bits
   int32_t n_tiles, tile_cols, grid;
   int32_t cta0[bp::kJitMaxTiles + 1];
   size_t partials_off, ws_bytes, smem;
 };
 
-JitTilePlan jit_tile_plan(int64_t n_rows, int64_t width, int out_kind, int law, uint32_t L,
-                          int sms, bool vec = false) {
+JitTilePlan jit_tile_plan_acc(int64_t n_rows, int64_t width, int acc, int law, uint32_t L,
+                              int sms) {
   JitTilePlan p{};
-  if (width < 1 || n_rows < 1) return p;
-  const int acc = ((law == BP_LAW_HOMO && !vec) || out_kind == BP_OUT_F32) ? 4 : 8;
   const int64_t max_cols =
-      ((static_cast<int64_t>(kSmemOptin) - kJitStaticSmem) / acc - 4) & ~int64_t{3};
+      ((static_cast<int64_t>(kSmemOptin) - kJitStaticSmem) / acc - 4) & ~int64_t{7};
   const int64_t nt = (width + max_cols - 1) / max_cols;
   if (nt > bp::kJitMaxTiles || nt > sms) return p;
   p.n_tiles = static_cast<int32_t>(nt);
-  p.tile_cols = static_cast<int32_t>(round_up(static_cast<size_t>((width + nt - 1) / nt), 4));
+  // tile rows of the partials stay 16-byte aligned (uint4 flush): 8 columns for 2-byte counts
+  p.tile_cols = static_cast<int32_t>(
+      round_up(static_cast<size_t>((width + nt - 1) / nt), acc == 2 ? 8 : 4));
   // cost of tile t per row: gap chain up to the tile's end ((t + 1) / nt of
   // a row spanning all tiles) + weights of the tile's own events (1 / nt);
   // in units of one row's gap chain: uniform weights ~1 (one Philox word per
@@ -392,17 +393,41 @@ JitTilePlan jit_tile_plan(int64_t n_rows, int64_t width, int out_kind, int law, 
   return p;
 }
 
-template <int LAW, int KIND, bool VEC, bool GEO>
+// n_seg: segments of a row inside the partition
+JitTilePlan jit_tile_plan(int64_t n_rows, int64_t width, int out_kind, int law, uint32_t L,
+                          int sms, bool vec = false, int64_t n_seg = 1) {
+  if (width < 1 || n_rows < 1) return JitTilePlan{};
+  if (law == BP_LAW_HOMO && !vec && !std::getenv("BP_JIT_C32")) {
+    // homogeneous counts in 16 bits (k_jit_tiled C16) while no CTA can count
+    // 2^16 events in one column: a CTA of a tile with G CTAs takes at most
+    // 32 ceil(items / (32 G)) (row, segment) items, each adding <= 1
+    JitTilePlan p = jit_tile_plan_acc(n_rows, width, 2, law, L, sms);
+    const int64_t items = n_rows * n_seg;
+    bool fits = p.ok;
+    for (int t = 0; fits && t < p.n_tiles; ++t) {
+      const int64_t g = p.cta0[t + 1] - p.cta0[t];
+      fits = 32 * ((items + 32 * g - 1) / (32 * g)) < 65535;
+    }
+    if (fits) {
+      p.c16 = true;
+      return p;
+    }
+  }
+  const int acc = ((law == BP_LAW_HOMO && !vec) || out_kind == BP_OUT_F32) ? 4 : 8;
+  return jit_tile_plan_acc(n_rows, width, acc, law, L, sms);
+}
+
+template <int LAW, int KIND, bool VEC, bool GEO, bool C16 = false>
 bool jit_tiled_coop(bp::JitTiledArgs a, const JitTilePlan &p, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(bp::k_jit_tiled<LAW, KIND, VEC, GEO>,
+    cudaFuncSetAttribute(bp::k_jit_tiled<LAW, KIND, VEC, GEO, C16>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kSmemOptin - kJitStaticSmem));
     attr = true;
   }
   void *args[] = {&a};
-  if (cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(bp::k_jit_tiled<LAW, KIND, VEC, GEO>),
+  if (cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(bp::k_jit_tiled<LAW, KIND, VEC, GEO, C16>),
                                   dim3(p.grid), dim3(bp::kJitTiledThreads), args, p.smem,
                                   st) == cudaSuccess)
     return true;
@@ -413,9 +438,13 @@ bool jit_tiled_coop(bp::JitTiledArgs a, const JitTilePlan &p, cudaStream_t st) {
 template <bool VEC, bool GEO>
 bool launch_jit_tiled_v(const bp::JitTiledArgs &a, int law, bool fix, const JitTilePlan &p,
                         cudaStream_t st) {
-  if (law == BP_LAW_HOMO)
+  if (law == BP_LAW_HOMO) {
+    if (!VEC && p.c16)
+      return fix ? jit_tiled_coop<0, 1, false, GEO, true>(a, p, st)
+                 : jit_tiled_coop<0, 0, false, GEO, true>(a, p, st);
     return fix ? jit_tiled_coop<0, 1, VEC, GEO>(a, p, st)
                : jit_tiled_coop<0, 0, VEC, GEO>(a, p, st);
+  }
   if (law == BP_LAW_UNIFORM)
     return fix ? jit_tiled_coop<1, 1, VEC, GEO>(a, p, st)
                : jit_tiled_coop<1, 0, VEC, GEO>(a, p, st);
@@ -470,8 +499,10 @@ bp_status jit_event_mv(int law, const bp_jitconn *spec, float w0, float w1,
   if (s != BP_OK) return s;
   cudaStream_t st = as_stream(stream);
   const size_t elt = out_kind == BP_OUT_FIX64 ? 8 : 4;
+  const int64_t n_seg_part = col_end > col_begin
+                                 ? (col_end - 1) / jr.L - col_begin / jr.L + 1 : 0;
   const JitTilePlan tp =
-      jit_tile_plan(n_rows, col_end - col_begin, out_kind, law, jr.L, sms, vec);
+      jit_tile_plan(n_rows, col_end - col_begin, out_kind, law, jr.L, sms, vec, n_seg_part);
   // normal weights: the fp64 Box-Muller of every event dominates and is the
   // same on both paths; the per-event path skips the partial tiles (measured
   // 510 vs 551 us on the 100 k x 100 k, p = 0.05, 10 % cell)

@@ -246,7 +246,8 @@ __device__ unsigned long long g_csr_t[1024][8];
 // `group` handles column slice `group` and writes out[c0 + column]
 // (accumulate: +=).  Homogeneous partials are event counts: fl32(n * w) or
 // n * q.  Deterministic for counts and fixed point.
-template <int KIND, bool HOMO, int NT>
+// C16: homogeneous partials are 16-bit counts (k_jit_tiled's packed tiles).
+template <int KIND, bool HOMO, int NT, bool C16 = false>
 __device__ __forceinline__ void tile_reduce(const void *partials, size_t first, int group,
                                             int groups, int tile_cols, int width, int64_t c0,
                                             void *out, int accumulate, float w, long long q) {
@@ -257,9 +258,14 @@ __device__ __forceinline__ void tile_reduce(const void *partials, size_t first, 
   for (int cc = s0 + static_cast<int>(threadIdx.x); cc < s1; cc += NT) {
     const int64_t c = c0 + cc;
     if (HOMO) {
-      const unsigned *p = static_cast<const unsigned *>(partials) + base + cc;
       unsigned long long n = 0;
-      for (int g = 0; g < groups; ++g) n += __ldcg(p + g * stride);
+      if (C16) {
+        const unsigned short *p = static_cast<const unsigned short *>(partials) + base + cc;
+        for (int g = 0; g < groups; ++g) n += __ldcg(p + g * stride);
+      } else {
+        const unsigned *p = static_cast<const unsigned *>(partials) + base + cc;
+        for (int g = 0; g < groups; ++g) n += __ldcg(p + g * stride);
+      }
       if (KIND == 0) {
         const float v = __fmul_rn(__ull2float_rn(n), w);
         float *o = static_cast<float *>(out) + c;

@@ -41,11 +41,17 @@ struct JitTiledArgs {
 
 // VEC: non-event product with a float vector (every row, contribution v[r] w:
 // fl32 product in f32 mode, the exact fp64 product rounded once in fixed point)
-template <int LAW, int KIND, bool VEC, bool GEO>
+// C16 (homogeneous only): 16-bit counts, two per 32-bit word, added with a
+// native 32-bit ATOMS of 1 << 16 (c & 1) -- exact while a CTA's count of a
+// column stays below 2^16 (the host checks: a (row, segment) adds at most
+// one event per column).  Twice the columns per tile: 100 k columns fit one
+// tile, so no gap chain is regenerated twice.
+template <int LAW, int KIND, bool VEC, bool GEO, bool C16 = false>
 __global__ void __launch_bounds__(kJitTiledThreads, 1) k_jit_tiled(JitTiledArgs a) {
   extern __shared__ __align__(128) unsigned char sm[];
   constexpr bool HOMO = LAW == 0 && !VEC;     // count events, scale once
-  constexpr int acc_bytes = (HOMO || KIND == 0) ? 4 : 8;
+  static_assert(!C16 || HOMO, "16-bit counts for homogeneous weights only");
+  constexpr int acc_bytes = C16 ? 2 : ((HOMO || KIND == 0) ? 4 : 8);
   int tile = 0;
   while (tile + 1 < a.n_tiles && static_cast<int>(blockIdx.x) >= a.cta0[tile + 1]) ++tile;
   const int group = blockIdx.x - a.cta0[tile];
@@ -56,15 +62,14 @@ __global__ void __launch_bounds__(kJitTiledThreads, 1) k_jit_tiled(JitTiledArgs 
   const uint32_t g0 = a.col_begin + t0;                        // global tile range
   const uint32_t g1 = a.col_begin + min(W, t0 + a.tile_cols);
   const int width = static_cast<int>(g1 - g0);
-  for (int c = tid; c <= width; c += kJitTiledThreads) {        // tile + sink slot
-    if (acc_bytes == 4) reinterpret_cast<uint32_t *>(sm)[c] = 0u;
-    else reinterpret_cast<unsigned long long *>(sm)[c] = 0ull;
-  }
+  const int n_zero32 = ((width + 1) * acc_bytes + 3) / 4;        // tile + sink slot
+  for (int c = tid; c < n_zero32; c += kJitTiledThreads) reinterpret_cast<uint32_t *>(sm)[c] = 0u;
   __syncthreads();
   const JitSide &s = a.s;
   auto add = [&](uint32_t pos, float w, float vr) {
     const uint32_t lc = min(pos - g0, static_cast<uint32_t>(width));
-    if (HOMO) atomicAdd(reinterpret_cast<uint32_t *>(sm) + lc, 1u);
+    if (C16) atomicAdd(reinterpret_cast<uint32_t *>(sm) + (lc >> 1), 1u << ((lc & 1u) * 16u));
+    else if (HOMO) atomicAdd(reinterpret_cast<uint32_t *>(sm) + lc, 1u);
     else if (KIND == 0) atomicAdd(reinterpret_cast<float *>(sm) + lc, VEC ? __fmul_rn(vr, w) : w);
     else {
       unsigned *p = reinterpret_cast<unsigned *>(sm) + 2 * lc;   // int64 as 2 x int32 + carry
@@ -155,7 +160,7 @@ __global__ void __launch_bounds__(kJitTiledThreads, 1) k_jit_tiled(JitTiledArgs 
   }
   __threadfence();
   cg::this_grid().sync();
-  tile_reduce<KIND, HOMO, kJitTiledThreads>(a.partials, static_cast<size_t>(a.cta0[tile]), group,
+  tile_reduce<KIND, HOMO, kJitTiledThreads, C16>(a.partials, static_cast<size_t>(a.cta0[tile]), group,
                                             groups, a.tile_cols, width, t0, a.out, a.accumulate,
                                             s.w0, s.q);
 }

@@ -455,3 +455,21 @@ def test_event_csrmv_grad(bp, orc, homo):
     if homo:
         tot = np.abs(gy[ix][np.repeat(ev, np.diff(ip)).astype(bool)]).sum()
         assert abs(gw.item() - want_gw) <= 1e-12 * tot + 1e-12
+
+
+@pytest.mark.parametrize("n_rows", [70_000, 10_000_000])
+def test_jitconn_homo_counts_16_bit_boundary(bp, n_rows, monkeypatch):
+    """Homogeneous tiles count events in 16 bits while no CTA can reach 2^16
+    in one column (k_jit_tiled C16) and fall back to 32 bits beyond (10 M
+    dense rows: ~68 k rows per CTA).  Dense rows (p = 1): every column gets
+    exactly n_active events, so out = n_active * q(w) in fixed point."""
+    monkeypatch.setenv("BP_JIT_TILED", "1")
+    n_cols = 40
+    spec = bp.jitconn_spec(5, 1.0)
+    ev = np.ones(n_rows, np.uint8)
+    out = torch.zeros(n_cols, dtype=torch.int64, device="cuda")
+    bp.jitconn_event_mv_homo(spec, 0.25, _dev_spikes(ev), n_rows, n_cols, out)
+    assert torch.all(out == n_rows * (2 ** 30)).item()      # q(0.25) = 2^30
+    out32 = torch.zeros(n_cols, dtype=torch.float32, device="cuda")
+    bp.jitconn_event_mv_homo(spec, 0.25, _dev_spikes(ev), n_rows, n_cols, out32)
+    assert torch.all(out32 == np.float32(np.float32(n_rows) * np.float32(0.25))).item()
