@@ -291,11 +291,15 @@ __device__ __forceinline__ void tile_reduce(const void *partials, size_t first, 
   }
 }
 
-// KIND: 0 f32 partials, 1 int64 fixed-point partials; HOMO: uint32 counts.
-template <int KIND, bool HOMO>
+// KIND: 0 f32 partials, 1 int64 fixed-point partials; HOMO: uint32 counts,
+// or (C16) 16-bit counts packed two per word -- exact while a CTA streams
+// fewer than 2^16 rows (the host's check; canonical rows hold a column at
+// most once), and half the shared memory per column, so fewer column tiles.
+template <int KIND, bool HOMO, bool C16 = false>
 __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs a) {
   extern __shared__ __align__(128) unsigned char sm[];
-  constexpr int acc_bytes = (HOMO || KIND == 0) ? 4 : 8;
+  static_assert(!C16 || HOMO, "16-bit counts for homogeneous weights only");
+  constexpr int acc_bytes = C16 ? 2 : ((HOMO || KIND == 0) ? 4 : 8);
   constexpr int BE = stream_buf_ent(HOMO);
   constexpr int NB = kStreamBufs;
   const StreamSmem L = stream_smem(a.tile_cols, acc_bytes, HOMO);
@@ -312,10 +316,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs 
   const int32_t c0i = static_cast<int32_t>(c0);
   CSR_MARK(0);
 
-  for (int c = tid; c <= width; c += kStreamThreads) {      // tile + sink slot
-    if (acc_bytes == 4) reinterpret_cast<uint32_t *>(sm)[c] = 0u;
-    else reinterpret_cast<unsigned long long *>(sm)[c] = 0ull;
-  }
+  const int n_zero32 = ((width + 1) * acc_bytes + 3) / 4;      // tile + sink slot
+  for (int c = tid; c < n_zero32; c += kStreamThreads) reinterpret_cast<uint32_t *>(sm)[c] = 0u;
   if (lane < NB) mbar_init(bar + lane, 1);
   asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" ::
                    : "memory");
@@ -412,7 +414,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs 
     // branch-free, one clamp per entry
     auto add = [&](int32_t col, float wgt) {
       const uint32_t lc = min(static_cast<uint32_t>(col - c0i), static_cast<uint32_t>(width));
-      if (HOMO) atomicAdd(reinterpret_cast<uint32_t *>(sm) + lc, 1u);
+      if (C16) atomicAdd(reinterpret_cast<uint32_t *>(sm) + (lc >> 1), 1u << ((lc & 1u) * 16u));
+      else if (HOMO) atomicAdd(reinterpret_cast<uint32_t *>(sm) + lc, 1u);
       else if (KIND == 0) atomicAdd(reinterpret_cast<float *>(sm) + lc, wgt);
       else {
         // int64 add as two native 32-bit ATOMS (a 64-bit shared add is a CAS
@@ -499,7 +502,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs 
   __threadfence();
   cg::this_grid().sync();
   CSR_MARK(5);
-  tile_reduce<KIND, HOMO, kStreamThreads>(a.partials, static_cast<size_t>(tile) * a.groups,
+  tile_reduce<KIND, HOMO, kStreamThreads, C16>(a.partials, static_cast<size_t>(tile) * a.groups,
                                          group, a.groups, a.tile_cols, width, c0, a.out,
                                          a.accumulate, a.w, a.q);
   CSR_MARK(6);

@@ -370,16 +370,21 @@ k_csr_tiled(CsrTiledArgs a) {
 // partial sums.  One thread per output column.
 template <int KIND>
 __global__ void __launch_bounds__(256)
-k_csr_reduce(CsrTiledArgs a, int homo) {
+k_csr_reduce(CsrTiledArgs a, int homo, int c16 = 0) {
   const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (c >= a.n_cols) return;
   const int64_t tile = c / a.tile_cols, cc = c - tile * a.tile_cols;
   const size_t stride = static_cast<size_t>(a.tile_cols);
   const size_t base = static_cast<size_t>(tile) * a.groups * stride + cc;
   if (homo) {
-    const unsigned *p = static_cast<const unsigned *>(a.partials) + base;
     unsigned long long n = 0;
-    for (int g = 0; g < a.groups; ++g) n += __ldcs(p + g * stride);
+    if (c16) {       // 16-bit counts (k_csr_stream C16)
+      const unsigned short *p = static_cast<const unsigned short *>(a.partials) + base;
+      for (int g = 0; g < a.groups; ++g) n += __ldcs(p + g * stride);
+    } else {
+      const unsigned *p = static_cast<const unsigned *>(a.partials) + base;
+      for (int g = 0; g < a.groups; ++g) n += __ldcs(p + g * stride);
+    }
     if (KIND == 0) {
       const float v = __fmul_rn(__ull2float_rn(n), a.w);
       float *o = static_cast<float *>(a.out) + c;

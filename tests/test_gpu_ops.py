@@ -473,3 +473,24 @@ def test_jitconn_homo_counts_16_bit_boundary(bp, n_rows, monkeypatch):
     out32 = torch.zeros(n_cols, dtype=torch.float32, device="cuda")
     bp.jitconn_event_mv_homo(spec, 0.25, _dev_spikes(ev), n_rows, n_cols, out32)
     assert torch.all(out32 == np.float32(np.float32(n_rows) * np.float32(0.25))).item()
+
+
+@pytest.mark.parametrize("c16", [0, 1])
+@pytest.mark.parametrize("n_rows", [100_000, 12_000_000])
+def test_event_csrmv_homo_counts_16_bit_boundary(bp, n_rows, c16, monkeypatch):
+    """The streamed CSR tiles count homogeneous events in 16 bits while a CTA
+    streams < 2^16 rows (k_csr_stream C16), 32 bits beyond (12 M dense rows
+    of 40 columns).  out = n_active * q(w) exactly.  16-bit counts are
+    opt-in (BP_CSR_C16=1); both modes are tested."""
+    monkeypatch.setenv("BP_CSR_C16", str(c16))
+    n_cols = 40
+    indptr = torch.arange(0, n_cols * (n_rows + 1), n_cols, dtype=torch.int64, device="cuda")
+    indices = torch.arange(n_cols, dtype=torch.int32, device="cuda").repeat(n_rows)
+    ev = np.ones(n_rows, np.uint8)
+    for plan in (False, True):
+        pl = bp.csrmv_plan(indptr, indices, n_rows, n_cols, torch.int64, homo=True) if plan else None
+        out = torch.zeros(n_cols, dtype=torch.int64, device="cuda")
+        bp.event_csrmv(indptr, indices, None, 0.25, n_rows, n_cols, _dev_spikes(ev), out, plan=pl)
+        assert torch.all(out == n_rows * (2 ** 30)).item()
+    del indices
+    torch.cuda.empty_cache()
