@@ -180,7 +180,10 @@ __host__ __device__ constexpr int stream_buf_ent(bool homo) {
   return homo ? BP_STREAM_BUF_BYTES / 4 : BP_STREAM_BUF_BYTES / 8;
 }
 
-constexpr int kStreamSegs = 8;   // row pieces per buffer
+#ifndef BP_STREAM_SEGS
+#define BP_STREAM_SEGS 8
+#endif
+constexpr int kStreamSegs = BP_STREAM_SEGS;   // row pieces per buffer
 
 struct StreamChunk {   // one row piece in a buffer
   int32_t dst;     // first buffer slot of the piece (multiple of 4)
