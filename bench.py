@@ -278,6 +278,8 @@ NETWORKS = {
                          cfg="config 1: COBA-LIF 4000 neurons (3200E/800I), p=0.02, CSR"),
     "hh400k_csr": dict(model="hh", conn="csr", n=400_000, scaling="strong",
                        cfg="config 4: COBA-HH 400k neurons, fan-in 80, CSR"),
+    "coba100m_jit": dict(model="lif", conn="jit", n=100_000_000, scaling="strong",
+                         cfg="config 5 total size on ONE GPU: COBA-LIF JIT 1e8 neurons, fan-in 80"),
     # Fig S3B / S3C regimes at the config-3 size
     "coba4m_k1000": dict(model="lif", conn="jit", n=4_000_000, scaling="strong", fan_in=1000,
                          cfg="Fig S3B: COBA-LIF JIT 4M neurons, 1000 synapses per neuron, "

@@ -47,6 +47,35 @@ def test_config5_network_first_steps(orc, mode):
     assert np.array_equal(net.state["g_i"].cpu().numpy(), st["g_i"])
 
 
+@pytest.mark.timeout(900)
+def test_1e8_neurons_on_one_gpu_first_steps(orc):
+    """The north_star's >= 1e8-neuron COBA-LIF JIT network (config 5's total
+    size) fits one B200: its first steps (step 0 spikes ~0.6 % = ~600 k
+    neurons, so step 1 delivers ~48 M synaptic events) bit for bit."""
+    n, steps = 100_000_000, 2
+    net = CobaNetwork(n, conn="jit", fixed=False)
+    raster = torch.zeros((steps, n // 32), dtype=torch.int32, device="cuda")
+    net.run(steps, raster)
+    got = raster.cpu().numpy().view(np.uint32)
+    v_gpu = net.state["v"].cpu().numpy()
+    ge_gpu = net.state["g_e"].cpu().numpy()
+    del net
+    torch.cuda.empty_cache()
+    n_exc = n * 4 // 5
+    K = orc.conn_len(80.0 / n)
+    assert K == n // 40 - 1
+    pe = orc.Projection(0, n_exc, jit=orc.JitSpec(SEED_E, K, n, orc.LAW_HOMO, 0.6))
+    pi = orc.Projection(n_exc, n - n_exc, jit=orc.JitSpec(SEED_I, K, n, orc.LAW_HOMO, 6.7))
+    st = dict(v=inputs.lif_v0(n), g_e=np.zeros(n, np.float32), g_i=np.zeros(n, np.float32),
+              ref=np.zeros(n, np.uint8), spikes=np.zeros(n, np.uint8))
+    want = orc.run_network("lif", orc.lif_params(), st, pe, pi, steps)
+    assert want[0].sum() > 400_000
+    for k in range(steps):
+        assert np.array_equal(got[k], inputs.pack_bits(want[k])), k
+    assert np.array_equal(v_gpu.view(np.uint32), st["v"].view(np.uint32))
+    assert np.array_equal(ge_gpu.view(np.uint32), st["g_e"].view(np.uint32))
+
+
 def test_config2_csr_full_size(bp, orc):
     n, p, d = 100_000, 0.01, 0.1
     ip, ix, _ = inputs.fixed_fanin_csr_fast(n, n, p, seed=17)
