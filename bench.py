@@ -607,6 +607,65 @@ def run_e2e_dist(args, wl, net, steps, barrier, dev):
                     "ms=%.3f" % ms}
 
 
+def run_emulated_rank(args):
+    """One rank of a G-GPU weak-scaling run, on one GPU: rank 0's partition
+    (12.5 M neurons) of the G x 12.5 M network steps with scatter (remote
+    rows regenerated restricted to the local segment) + update (fold, LIF,
+    local binning), and the all-gather is replaced by one device copy that
+    replicates rank 0's own spike words into every remote slot (the bytes
+    NCCL would write; the remote ranks then fire like rank 0, which keeps
+    the E/I feedback of the network -- fixed synthetic remote rates do not:
+    they let rank 0's excitatory neurons run away).  Not a multi-GPU number:
+    the per-rank compute of one (no NVLink in it)."""
+    import torch
+
+    import __graft_entry__ as ge
+    ge.build_lib()
+    from paper_2311_05106_b200.network import CobaNetwork
+    torch.cuda.set_device(0)
+    G = args.emulate_world
+    n = N_PER_GPU * G
+    net = CobaNetwork(n, conn="jit", fixed={"fix64": True, "fix32": "fix32", "f32": False}[args.g],
+                      rank=0, world=G, device="cuda:0")
+    lw = net.part.local_words
+    words = net.spikes.numel()
+    assert words == G * lw
+    local = net.spikes[:lw]
+    remote = net.spikes[lw:].view(G - 1, lw)
+
+    def step(k):
+        net.net.scatter()
+        net.net.update()
+        remote.copy_(local.expand(G - 1, lw))
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize()
+    sp0, ev0, _ = net.counters()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        a.record()
+        for k in range(args.steps):
+            step(k)
+        b.record()
+        torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    sp1, ev1, _ = net.counters()
+    line = {"metric": METRIC + " (emulated single rank)", "value": (ev1 - ev0) / (ms / 1e3),
+            "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": args.g, "data": "synthetic",
+            "config": {"workload": "coba_lif_jit rank 0 of %d" % G, "n_total": n,
+                       "n_per_gpu": N_PER_GPU, "emulated_world": G,
+                       "exchange": "replaced by one device copy of rank 0's spike words "
+                                   "into the %d remote slots (%.1f MB/step)" % (
+                                       G - 1, (words - lw) * 4 / 1e6),
+                       "local_spikes_per_step": (sp1 - sp0) / args.steps,
+                       "events_per_step": (ev1 - ev0) / args.steps},
+            "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
 # ---------------------------------------------------------------------------
 # config 2: event_csrmv / jitconn event_mv microbenchmark, 100k x 100k
 # ---------------------------------------------------------------------------
@@ -780,6 +839,9 @@ def main():
     ap.add_argument("--f32", action="store_true", help="alias of --g f32")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
+    ap.add_argument("--emulate-world", type=int, default=0,
+                    help="one GPU: time rank 0 of a G-GPU weak-scaling run (exchange "
+                         "replaced by a device copy; not a multi-GPU number)")
     ap.add_argument("--no-graph", action="store_true",
                     help="N > 1: eager per-step calls instead of the captured CUDA graph")
     ap.add_argument("--workload",
@@ -804,6 +866,8 @@ def main():
         args.g = "f32"
     if args.impl == "reference":
         run_reference(args)
+    elif args.emulate_world > 1:
+        run_emulated_rank(args)
     elif args.workload in ("csrmv", "jitmv", "jitmv_vec", "jitrows"):
         run_micro(args)
     else:

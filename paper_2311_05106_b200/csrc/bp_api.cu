@@ -119,7 +119,7 @@ int grid_for_items(int64_t items_upper, int sms) {
 }
 
 int grid_for_words(int64_t n_words, int sms) {
-  int64_t blocks = (n_words + 255) / 256;
+  int64_t blocks = (n_words + bp::kCompactWords - 1) / bp::kCompactWords;
   const int64_t cap = static_cast<int64_t>(sms) * 8;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
