@@ -118,19 +118,32 @@ int grid_for_items(int64_t items_upper, int sms) {
   return static_cast<int>(blocks);
 }
 
-int grid_for_words(int64_t n_words, int sms) {
-  int64_t blocks = (n_words + bp::kCompactWords - 1) / bp::kCompactWords;
+// a1: warp-level claims for short vectors (k_compact_warp, no barriers);
+// block-aggregated claims (k_compact) from 64 k words on, 4 words per thread
+// once the vector fills every SM with 8 blocks of 1024-word iterations
+void launch_compact(const uint32_t *spikes, int64_t n, int32_t *active, int32_t *count,
+                    int sms, cudaStream_t st, int32_t id_base = 0) {
+  const int64_t words = (n + 31) / 32;
   const int64_t cap = static_cast<int64_t>(sms) * 8;
+  if (words < (int64_t{1} << 16)) {
+    int64_t blocks = (words + 255) / 256;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    bp::k_compact_warp<<<static_cast<int>(blocks), 256, 0, st>>>(spikes, n, active, count,
+                                                                 id_base);
+    return;
+  }
+  const bool wide = words >= cap * 4 * bp::kCompactThreads;
+  const int64_t per = (wide ? 4 : 1) * bp::kCompactThreads;
+  int64_t blocks = (words + per - 1) / per;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  return static_cast<int>(blocks);
-}
-
-void launch_compact(const uint32_t *spikes, int64_t n, int32_t *active,
-                    int32_t *count, int sms, cudaStream_t st) {
-  const int64_t words = (n + 31) / 32;
-  bp::k_compact<<<grid_for_words(words, sms), 256, 0, st>>>(spikes, n, active,
-                                                            count, 0);
+  if (wide)
+    bp::k_compact<4><<<static_cast<int>(blocks), bp::kCompactThreads, 0, st>>>(
+        spikes, n, active, count, id_base);
+  else
+    bp::k_compact<1><<<static_cast<int>(blocks), bp::kCompactThreads, 0, st>>>(
+        spikes, n, active, count, id_base);
 }
 
 // ------------------------------------------------------------- CSR plan
@@ -1303,8 +1316,8 @@ bp_status bin_spike_range(bp_network *net, int64_t w_begin, int64_t w_end, int p
   int32_t *active = net->active[0];
   int32_t *count = net->count;
   BP_CUDA(cudaMemsetAsync(count, 0, sizeof(int32_t), st));
-  bp::k_compact<<<grid_for_words(w_end - w_begin, net->sms), 256, 0, st>>>(
-      net->d.spikes + w_begin, last - first, active, count, static_cast<int32_t>(first));
+  launch_compact(net->d.spikes + w_begin, last - first, active, count, net->sms, st,
+                 static_cast<int32_t>(first));
   bp_status s = launched();
   if (s != BP_OK) return s;
   return launch_bin(net, active, count, par, last - first, st);

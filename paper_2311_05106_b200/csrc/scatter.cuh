@@ -43,15 +43,64 @@ __device__ __forceinline__ void count_events(unsigned long long *counter,
 }
 
 // ---------------------------------------------------------------- a1
-// a1: block-aggregated compaction.  Each block takes 1024 consecutive spike
+// Short vectors (config-2 calls): warps warp0, warp0 + n_warps, ... each
+// take 32 spike words: warp scan of the popcounts, one atomicAdd per warp
+// claims a slice of the active list (no block barriers).
+__device__ __forceinline__ void compact_words(const uint32_t *__restrict__ spikes, int64_t n,
+                                              int32_t *__restrict__ active,
+                                              int32_t *__restrict__ count, int32_t id_base,
+                                              int64_t warp0, int64_t n_warps) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n_words = (n + 31) >> 5;
+  for (int64_t base = warp0 * 32; base < n_words; base += n_warps * 32) {
+    const int64_t wi = base + lane;
+    uint32_t word = 0;
+    if (wi < n_words) {
+      word = __ldg(spikes + wi);
+      const int64_t valid = n - (wi << 5);
+      if (valid < 32) word &= (1u << valid) - 1u;
+    }
+    const int c = __popc(word);
+    int incl = c;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += t;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) continue;
+    int slot = 0;
+    if (lane == 31) slot = atomicAdd(count, total);
+    slot = __shfl_sync(0xffffffffu, slot, 31) + incl - c;
+    while (word) {
+      const int b = __ffs(word) - 1;
+      active[slot++] = id_base + static_cast<int32_t>((wi << 5) + b);
+      word &= word - 1u;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256)
+k_compact_warp(const uint32_t *__restrict__ spikes, int64_t n,
+          int32_t *__restrict__ active, int32_t *__restrict__ count,
+          int32_t id_base) {
+  compact_words(spikes, n, active, count, id_base,
+                (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5,
+                (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5);
+}
+
+// Long vectors (the remote words of a partitioned network): block-aggregated
+// compaction.  Each block takes 1024 consecutive spike
 // words per iteration (4 per thread), ranks their set bits with a block
 // scan of the popcounts and claims its slice of the active list with ONE
 // atomic per non-empty iteration.  (A claim per warp of 32 words put ~10^5
 // returning atomics on the single counter for a 10^8-neuron vector --
 // 55 us at 0.22 % density, serialised on one L2 address.)
+// WPT words per thread: 4 for long vectors (fewer claims), 1 for short ones
+// (more blocks in flight).
 constexpr int kCompactThreads = 256;
-constexpr int kCompactWords = 4 * kCompactThreads;
 
+template <int WPT>
 __global__ void __launch_bounds__(kCompactThreads)
 k_compact(const uint32_t *__restrict__ spikes, int64_t n,
           int32_t *__restrict__ active, int32_t *__restrict__ count,
@@ -60,13 +109,14 @@ k_compact(const uint32_t *__restrict__ spikes, int64_t n,
   __shared__ int32_t block_base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t n_words = (n + 31) >> 5;
-  for (int64_t w0 = static_cast<int64_t>(blockIdx.x) * kCompactWords; w0 < n_words;
-       w0 += static_cast<int64_t>(gridDim.x) * kCompactWords) {
-    uint32_t wd[4];
+  constexpr int BW = WPT * kCompactThreads;     // words per block iteration
+  for (int64_t w0 = static_cast<int64_t>(blockIdx.x) * BW; w0 < n_words;
+       w0 += static_cast<int64_t>(gridDim.x) * BW) {
+    uint32_t wd[WPT];
     int c = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int64_t wi = w0 + 4 * tid + k;
+    for (int k = 0; k < WPT; ++k) {
+      const int64_t wi = w0 + WPT * tid + k;
       uint32_t word = 0;
       if (wi < n_words) {
         word = __ldg(spikes + wi);
@@ -96,12 +146,12 @@ k_compact(const uint32_t *__restrict__ spikes, int64_t n,
     if (total == 0) continue;        // block-uniform
     int slot = block_base + before + incl - c;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < WPT; ++k) {
       uint32_t word = wd[k];
       while (word) {
         const int b = __ffs(word) - 1;
         word &= word - 1u;
-        active[slot++] = id_base + static_cast<int32_t>(((w0 + 4 * tid + k) << 5) + b);
+        active[slot++] = id_base + static_cast<int32_t>(((w0 + WPT * tid + k) << 5) + b);
       }
     }
   }
