@@ -17,6 +17,7 @@ Prints ONE JSON line on rank 0.
 from __future__ import annotations
 
 import argparse
+import math
 import json
 import os
 import statistics
@@ -621,12 +622,12 @@ def run_emulated_rank(args):
 
     import __graft_entry__ as ge
     ge.build_lib()
-    from paper_2311_05106_b200.network import CobaNetwork
     torch.cuda.set_device(0)
     G = args.emulate_world
-    n = N_PER_GPU * G
-    net = CobaNetwork(n, conn="jit", fixed={"fix64": True, "fix32": "fix32", "f32": False}[args.g],
-                      rank=0, world=G, device="cuda:0")
+    wl = args.workload
+    n = network_size(wl, G)
+    net, _ = build_network(wl, G, 0, {"fix64": True, "fix32": "fix32", "f32": False}[args.g],
+                           torch.device("cuda", 0))
     lw = net.part.local_words
     words = net.spikes.numel()
     assert words == G * lw
@@ -641,12 +642,28 @@ def run_emulated_rank(args):
     for k in range(args.warmup):
         step(k)
     torch.cuda.synchronize()
+    # one period of steps in a CUDA graph, as the N > 1 bench replays it
+    period = math.lcm(2, net.delay + 1)
+    graph = None
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for k in range(period):
+                step(k)
+        graph.replay()
+        torch.cuda.synchronize()
     sp0, ev0, _ = net.counters()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(0) as clk:
         a.record()
-        for k in range(args.steps):
-            step(k)
+        if graph is not None:
+            for _ in range(args.steps // period):
+                graph.replay()
+            for k in range(args.steps % period):
+                step(k)
+        else:
+            for k in range(args.steps):
+                step(k)
         b.record()
         torch.cuda.synchronize()
     ms = a.elapsed_time(b)
@@ -655,11 +672,13 @@ def run_emulated_rank(args):
             "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": args.g, "data": "synthetic",
-            "config": {"workload": "coba_lif_jit rank 0 of %d" % G, "n_total": n,
-                       "n_per_gpu": N_PER_GPU, "emulated_world": G,
+            "config": {"workload": "%s rank 0 of %d" % (wl, G), "n_total": n,
+                       "n_per_gpu": net.part.col_end - net.part.col_begin, "emulated_world": G,
                        "exchange": "replaced by one device copy of rank 0's spike words "
                                    "into the %d remote slots (%.1f MB/step)" % (
                                        G - 1, (words - lw) * 4 / 1e6),
+                       "host_loop": "CUDA graph of %d steps" % period if graph is not None
+                                    else "eager",
                        "local_spikes_per_step": (sp1 - sp0) / args.steps,
                        "events_per_step": (ev1 - ev0) / args.steps},
             "clocks": clk.summary()}
