@@ -104,6 +104,8 @@ def lib():
         _lib.or_geo_c.restype = f32
         _lib.or_logf_j10.argtypes = [f32]
         _lib.or_logf_j10.restype = f32
+        _lib.or_cos2pi_j7.argtypes = [f32]
+        _lib.or_cos2pi_j7.restype = f32
         _lib.or_geo_gap.argtypes = [f32, u32, u32]
         _lib.or_geo_gap.restype = u32
         _lib.or_fix32_add.argtypes = [P, P, i64]
@@ -165,6 +167,11 @@ def geo_c(p: float) -> float:
 def logf_j10(u: float) -> float:
     """Rule J10's specified fp32 natural log."""
     return float(lib().or_logf_j10(u))
+
+
+def cos2pi_j7(u: float) -> float:
+    """Reading J7n's specified fp32 cos(2 pi u)."""
+    return float(lib().or_cos2pi_j7(u))
 
 
 def geo_gap(c: float, cap: int, x: int) -> int:

@@ -157,6 +157,41 @@ float or_logf_j10(float u) {
   return fmaf(ef, 0.693145751953125f, fmaf(ef, 1.428606765330187e-6f, lm));
 }
 
+/* ------------------------------------------------------------------------
+ * Reading J7n: cos(2 pi u) for u in [0, 1) (24-bit u), op-for-op specified
+ * in fp32 (the kernels run the same operations):
+ *   v = u - rint(u) in [-1/2, 1/2] (exact);  a = |v|;
+ *   a > 1/4:  cos(2 pi a) = -cos(2 pi (1/2 - a));  b = min(a, 1/2 - a) (exact)
+ *   b <= 1/8: cos(theta), theta = fl(2 pi b), Taylor to theta^10 (Horner, fmaf)
+ *   b >  1/8: sin(theta'), theta' = fl(2 pi (1/4 - b)), Taylor to theta'^9
+ * Pinned by: <= 4 ulp vs libm cos on a dense grid of [0, 1) (absolute
+ * 2^-24 near the zeros), symmetry and the exact values at u = 0, 1/4, 1/2.
+ * ---------------------------------------------------------------------- */
+float or_cos2pi_j7(float u) {
+  float v = u - rintf(u);
+  float a = fabsf(v);
+  float sgn = 1.0f;
+  if (a > 0.25f) { a = 0.5f - a; sgn = -1.0f; }
+  float r;
+  if (a <= 0.125f) {
+    float t = 6.28318548202514648438f * a;            /* fl32(2 pi) */
+    float t2 = t * t;
+    float p = fmaf(t2, -2.7557319e-7f, 2.4801587e-5f);   /* -1/10!, 1/8! */
+    p = fmaf(t2, p, -1.3888889e-3f);                     /* -1/6! */
+    p = fmaf(t2, p, 4.1666668e-2f);                      /* 1/4! */
+    p = fmaf(t2, p, -0.5f);
+    r = fmaf(t2, p, 1.0f);
+  } else {
+    float t = 6.28318548202514648438f * (0.25f - a);
+    float t2 = t * t;
+    float p = fmaf(t2, 2.7557319e-6f, -1.9841270e-4f);  /* 1/9!, -1/7! */
+    p = fmaf(t2, p, 8.3333338e-3f);                      /* 1/5! */
+    p = fmaf(t2, p, -0.16666667f);                       /* -1/3! */
+    r = fmaf(t * t2, p, t);
+  }
+  return sgn * r;
+}
+
 uint32_t or_geo_gap(float c, uint32_t cap, uint32_t x) {
   float u = (float)((x >> 8) + 1u) * 0x1p-24f;
   float t = or_logf_j10(u) / c;
@@ -207,14 +242,15 @@ static float edge_weight(uint64_t seed, int law, float w0, float w1,
     float span = w1 - w0;                              /* fp32 rounding */
     return fmaf(u, span, w0);
   }
-  /* normal */
+  /* normal: Box-Muller in fp32 with the specified log (rule J10) and
+   * cos(2 pi u) (or_cos2pi_j7) -- reading J7n */
   uint32_t x1 = or_word(seed, 1u, row, seg, 2u * e);
   uint32_t x2 = or_word(seed, 1u, row, seg, 2u * e + 1u);
   float u1 = (float)((x1 >> 8) + 1u) * 0x1p-24f;       /* (0, 1], exact */
   float u2 = (float)(x2 >> 8) * 0x1p-24f;              /* [0, 1), exact */
-  double radius = sqrt(-2.0 * log((double)u1));
-  double z = radius * cos(6.283185307179586 * (double)u2);
-  return fmaf(w1, (float)z, w0);
+  float radius = sqrtf(-2.0f * or_logf_j10(u1));       /* IEEE sqrt */
+  float z = radius * or_cos2pi_j7(u2);
+  return fmaf(w1, z, w0);
 }
 
 /* ------------------------------------------------------------------------

@@ -401,3 +401,26 @@ def test_geo_materialised_csr_equals_direct(orc, law, L):
         assert np.array_equal(a, b)
         v = ev.astype(np.float32)
         assert np.array_equal(orc.jit_mv(spec, n_rows, n_cols, v, out_kind=orc.OUT_FIX), b)
+
+
+# ---------------------------------------------------------------- J7n
+def test_cos2pi_j7_accuracy_and_special_values(orc):
+    """Reading J7n's fp32 cos(2 pi u) on the 24-bit grid of u in [0, 1):
+    within 4 ulp of the fp64 cosine (2^-24 absolute near its zeros);
+    exact at u = 0, 1/4, 1/2, 3/4 and even about u = 1/2."""
+    rng = np.random.default_rng(9)
+    ks = np.unique(np.concatenate([rng.integers(0, 2 ** 24, 150_000), np.arange(0, 2048),
+                                   2 ** 22 + np.arange(-1024, 1024),
+                                   2 ** 23 + np.arange(-1024, 1024),
+                                   3 * 2 ** 22 + np.arange(-1024, 1024)]))
+    ks = ks[(ks >= 0) & (ks < 2 ** 24)]
+    us = (ks * 2.0 ** -24).astype(np.float32)
+    got = np.array([orc.cos2pi_j7(float(u)) for u in us], np.float64)
+    want = np.cos(2 * np.pi * us.astype(np.float64))
+    tol = 4 * np.spacing(np.abs(want).astype(np.float32)).astype(np.float64) + 2.0 ** -24
+    assert np.all(np.abs(got - want) <= tol), us[np.argmax(np.abs(got - want) - tol)]
+    assert orc.cos2pi_j7(0.0) == 1.0 and orc.cos2pi_j7(0.5) == -1.0
+    assert orc.cos2pi_j7(0.25) == 0.0 and orc.cos2pi_j7(0.75) == 0.0
+    for u in us[:2000]:
+        if u < 0.5:
+            assert orc.cos2pi_j7(float(u)) == orc.cos2pi_j7(float(np.float32(1.0) - u))
