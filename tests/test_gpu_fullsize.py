@@ -112,12 +112,7 @@ def test_config2_jitconn_full_size(bp, orc, law):
     ospec = orc.JitSpec(seed, orc.conn_len(p), n, orc.LAWS[law], w0, w1)
     want = orc.jit_event_mv(ospec, n, n, ev, out_kind=orc.OUT_FIX)
     got = out.cpu().numpy()
-    if law == "normal":
-        diff = np.abs(got - want)
-        assert np.mean(diff != 0) < 1e-3
-        assert np.all(diff <= 2 ** 32 * 2.0 ** -20)
-    else:
-        assert np.array_equal(got, want)
+    assert np.array_equal(got, want)              # every law bit-exact (J7n)
 
 
 @pytest.fixture(scope="module")

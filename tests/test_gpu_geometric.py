@@ -3,8 +3,7 @@ NEXT 4) against the CPU oracle.
 
 Positions and every BP_OUT_FIX64 output are bit-exact (both sides draw the
 same gaps through the op-for-op specified fp32 log of rule J10); BP_OUT_F32
-outputs satisfy rule T2.  Normal-law weights may differ by 1 ulp (fp64
-libm vs CUDA log/cos), as in test_gpu_ops.py.
+outputs satisfy rule T2.  Normal-law weights are bit-identical too (J7n).
 """
 import numpy as np
 import pytest
@@ -47,10 +46,7 @@ def test_geo_materialize_bit_exact(bp, orc, law, shape):
     assert np.array_equal(ip.cpu().numpy(), oip)
     assert np.array_equal(ix.cpu().numpy(), oix)
     dat = dat.cpu().numpy()
-    if law == "normal":
-        assert np.all(np.abs(dat - odat) <= np.spacing(np.abs(odat).astype(np.float32)))
-    else:
-        assert np.array_equal(dat.view(np.uint32), odat.view(np.uint32))
+    assert np.array_equal(dat.view(np.uint32), odat.view(np.uint32))   # J7n: every law
 
 
 def test_geo_differs_from_uniform_and_has_density_p(bp, orc):
@@ -96,18 +92,13 @@ def test_geo_event_mv(bp, orc, case, law, path, monkeypatch):
     fn(out)
     want = orc.jit_event_mv(ospec, n_rows, n_cols, ev, out_kind=orc.OUT_FIX)
     got = out.cpu().numpy()
-    if law == "normal":
-        diff = np.abs(got - want)
-        assert np.mean(diff != 0) < 1e-3
-        assert np.all(diff <= 2 ** 32 * 2.0 ** -22 * (abs(w1) * 6 + 1))
-    else:
-        assert np.array_equal(got, want)
+    assert np.array_equal(got, want)              # every law bit-exact (J7n)
     out32 = torch.zeros(n_cols, dtype=torch.float32, device="cuda")
     fn(out32)
     ref, absw = orc.jit_event_mv(ospec, n_rows, n_cols, ev, out_kind=orc.OUT_F64,
                                  with_abs=True)
     err = np.abs(out32.cpu().numpy().astype(np.float64) - ref)
-    assert np.all(err <= 1e-5 * absw + 1e-6 * (law == "normal") * absw + 1e-30)
+    assert np.all(err <= 1e-5 * absw + 1e-30)
 
 
 @pytest.mark.parametrize("bounds", [(0, 1000), (1000, 5000), (9000, 10_000)])

@@ -3,9 +3,8 @@
 Bars: index sets, positions and every BP_OUT_FIX64
 output are bit-exact; BP_OUT_F32 outputs satisfy rule T2,
 |y_gpu - y_f64| <= 1e-5 * sum|w| + 1e-30 per output (order-free bound for
-fp32 atomics); normal-law weights (fp64 log/cos on both sides, rounded to
-fp32) may differ by 1 ulp from the oracle's in a vanishing fraction of
-edges, so their fixed-point sums are compared within that allowance.
+fp32 atomics).  Weights of every law (normal: the fp32 Box-Muller of
+reading J7n) are bit-identical on both sides.
 """
 import numpy as np
 import pytest
@@ -189,19 +188,13 @@ def test_jitconn_event_mv(bp, orc, case, law, path, monkeypatch):
     fn(out)
     want = orc.jit_event_mv(ospec, n_rows, n_cols, ev, out_kind=orc.OUT_FIX)
     got = out.cpu().numpy()
-    if law == "normal":
-        # a 1-ulp weight difference moves a fixed-point sum by <= ulp(w) * 2^32
-        diff = np.abs(got - want)
-        assert np.mean(diff != 0) < 1e-3
-        assert np.all(diff <= 2 ** 32 * 2.0 ** -22 * (abs(w1) * 6 + 1))
-    else:
-        assert np.array_equal(got, want)
+    assert np.array_equal(got, want)              # every law bit-exact (J7n)
     out32 = torch.zeros(n_cols, dtype=torch.float32, device="cuda")
     fn(out32)
     ref, absw = orc.jit_event_mv(ospec, n_rows, n_cols, ev, out_kind=orc.OUT_F64,
                                  with_abs=True)
     err = np.abs(out32.cpu().numpy().astype(np.float64) - ref)
-    assert np.all(err <= 1e-5 * absw + 1e-6 * (law == "normal") * absw + 1e-30)
+    assert np.all(err <= 1e-5 * absw + 1e-30)
 
 
 @pytest.mark.parametrize("path", ["tiled", "direct"])
@@ -266,12 +259,7 @@ def test_materialize_positions_bit_exact(bp, orc, law, shape):
     oip, oix, odat = orc.jit_materialize(ospec, n_rows, n_cols)
     assert np.array_equal(ip, oip)
     assert np.array_equal(ix, oix)
-    if law == "normal":
-        ulp = np.spacing(np.abs(odat).astype(np.float32))
-        assert np.all(np.abs(dat - odat) <= ulp)
-        assert np.mean(dat != odat) < 1e-3
-    else:
-        assert np.array_equal(dat.view(np.uint32), odat.view(np.uint32))
+    assert np.array_equal(dat.view(np.uint32), odat.view(np.uint32))   # J7n: every law
 
 
 # ------------------------------------------------------------------ a5 + a6
@@ -358,7 +346,7 @@ MV_CASES = [
 @pytest.mark.parametrize("law", ["homo", "uniform", "normal"])
 def test_jitconn_mv(bp, orc, case, law, path, monkeypatch):
     """mv_prob_* (reading MV1) against the oracle: fixed point bit-exact
-    (normal weights: libm-level differences allowed), fp32 within rule T2."""
+    (every law), fp32 within rule T2."""
     monkeypatch.setenv("BP_JIT_DIRECT" if path == "direct" else "BP_JIT_TILED", "1")
     n_rows, n_cols, p, seg_len = case
     w0, w1 = {"homo": (0.6, 0.0), "uniform": (-0.1, 0.2), "normal": (0.0, 0.3)}[law]
@@ -375,17 +363,12 @@ def test_jitconn_mv(bp, orc, case, law, path, monkeypatch):
     bp.jitconn_mv(code, spec, w0, w1, tv, n_rows, n_cols, out)
     want = orc.jit_mv(ospec, n_rows, n_cols, v, out_kind=orc.OUT_FIX)
     got = out.cpu().numpy()
-    if law == "normal":
-        diff = np.abs(got - want)
-        assert np.mean(diff != 0) < 1e-3
-        assert np.all(diff <= 2 ** 32 * 2.0 ** -22 * (abs(w1) * 6 + 1) * np.abs(v).max())
-    else:
-        assert np.array_equal(got, want)
+    assert np.array_equal(got, want)              # every law bit-exact (J7n)
     out32 = torch.zeros(n_cols, dtype=torch.float32, device="cuda")
     bp.jitconn_mv(code, spec, w0, w1, tv, n_rows, n_cols, out32)
     ref, absw = orc.jit_mv(ospec, n_rows, n_cols, v, out_kind=orc.OUT_F64, with_abs=True)
     err = np.abs(out32.cpu().numpy().astype(np.float64) - ref)
-    assert np.all(err <= 1e-5 * absw + 1e-6 * (law == "normal") * absw + 1e-30)
+    assert np.all(err <= 1e-5 * absw + 1e-30)
 
 
 def test_jitconn_mv_binary_vector_equals_event_mv(bp):
