@@ -403,7 +403,7 @@ JitTilePlan jit_tile_plan_acc(int64_t n_rows, int64_t width, int acc, int law, u
   // a row spanning all tiles) + weights of the tile's own events (1 / nt);
   // in units of one row's gap chain: uniform weights ~1 (one Philox word per
   // event), normal ~6 (two words + fp64 log/sqrt/cos per event)
-  const double wcost = law == BP_LAW_HOMO ? 0.0 : (law == BP_LAW_UNIFORM ? 1.0 : 6.0);  // normal: BP_JIT_TILED
+  const double wcost = law == BP_LAW_HOMO ? 0.0 : (law == BP_LAW_UNIFORM ? 1.0 : 3.0);
   const bool spans = L >= static_cast<uint64_t>(p.tile_cols) * 2;
   double wsum = 0.0, wt[bp::kJitMaxTiles];
   for (int t = 0; t < nt; ++t) {
@@ -537,15 +537,14 @@ bp_status jit_event_mv(int law, const bp_jitconn *spec, float w0, float w1,
                                  ? (col_end - 1) / jr.L - col_begin / jr.L + 1 : 0;
   const JitTilePlan tp =
       jit_tile_plan(n_rows, col_end - col_begin, out_kind, law, jr.L, sms, vec, n_seg_part);
-  // normal weights: the fp64 Box-Muller of every event dominates and is the
-  // same on both paths; the per-event path skips the partial tiles (measured
-  // 510 vs 551 us on the 100 k x 100 k, p = 0.05, 10 % cell)
-  // short rows (< ~1000 events per active row in the partition): the
-  // partial tiles cost more than the atomics they save
+  // short rows (< ~1000 events per active row in the partition; < ~2500 for
+  // normal weights, whose Box-Muller is the same on both paths): the partial
+  // tiles cost more than the atomics they save (normal, 100 k x 100 k, 10 %:
+  // tiled 366 vs 398 us at p = 0.05, 105 vs 92 us at p = 0.01)
   const double row_events = jr.density * static_cast<double>(col_end - col_begin);
   const bool tiled = tp.ok && n_rows > 0 && ws_bytes >= tp.ws_bytes &&
                      !std::getenv("BP_JIT_DIRECT") &&
-                     ((law != BP_LAW_NORMAL && row_events >= 1000.0) ||
+                     ((row_events >= (law == BP_LAW_NORMAL ? 2500.0 : 1000.0)) ||
                       std::getenv("BP_JIT_TILED"));
   if (tiled) {
     // shared-memory column tiles + in-kernel reduction (every output

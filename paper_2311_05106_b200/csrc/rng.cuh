@@ -75,18 +75,6 @@ __device__ __forceinline__ float uniform_weight(uint32_t x, float lo,
   return __fmaf_rn(u, span, lo);
 }
 
-// normal: u1 = ((x1 >> 8) + 1) 2^-24 in (0,1], u2 = (x2 >> 8) 2^-24;
-// z = sqrt(-2 ln u1) cos(2 pi u2) evaluated in fp64, w = fmaf(sigma, (float)z, mu).
-__device__ __forceinline__ float normal_weight(uint32_t x1, uint32_t x2,
-                                               float mu, float sigma) {
-  const float u1 = __uint2float_rn((x1 >> 8) + 1u) * 0x1p-24f;
-  const float u2 = __uint2float_rn(x2 >> 8) * 0x1p-24f;
-  const double radius = sqrt(__dmul_rn(-2.0, log(static_cast<double>(u1))));
-  const double z =
-      __dmul_rn(radius, cos(__dmul_rn(6.283185307179586, static_cast<double>(u2))));
-  return __fmaf_rn(sigma, __double2float_rn(z), mu);
-}
-
 // Rule J10 (geometric-gap sampler; NEXT 4): op-for-op specified fp32
 // natural log on (0, 1] -- the oracle runs the same operations, so both
 // sides draw identical gaps.  u = m 2^e; m in [sqrt(1/2), sqrt 2];
@@ -124,6 +112,49 @@ __device__ __forceinline__ uint32_t geo_gap(uint32_t x, float c, uint32_t cap) {
   if (ct < 1.0f) return 1u;
   const uint32_t g = __float2uint_rz(ct);
   return g > cap ? cap : g;
+}
+
+// Reading J7n: cos(2 pi u) for u in [0, 1), op-for-op specified in fp32 (the
+// oracle runs the same operations): reduce by symmetry to b in [0, 1/4],
+// Taylor cos (to theta^10) for b <= 1/8, else sin of 2 pi (1/4 - b) (to
+// theta^9), Horner with fmaf.
+__device__ __forceinline__ float cos2pi_j7(float u) {
+  const float v = __fsub_rn(u, rintf(u));
+  float a = fabsf(v);
+  float sgn = 1.0f;
+  if (a > 0.25f) {
+    a = __fsub_rn(0.5f, a);
+    sgn = -1.0f;
+  }
+  float r;
+  if (a <= 0.125f) {
+    const float t = __fmul_rn(6.28318548202514648438f, a);
+    const float t2 = __fmul_rn(t, t);
+    float p = __fmaf_rn(t2, -2.7557319e-7f, 2.4801587e-5f);
+    p = __fmaf_rn(t2, p, -1.3888889e-3f);
+    p = __fmaf_rn(t2, p, 4.1666668e-2f);
+    p = __fmaf_rn(t2, p, -0.5f);
+    r = __fmaf_rn(t2, p, 1.0f);
+  } else {
+    const float t = __fmul_rn(6.28318548202514648438f, __fsub_rn(0.25f, a));
+    const float t2 = __fmul_rn(t, t);
+    float p = __fmaf_rn(t2, 2.7557319e-6f, -1.9841270e-4f);
+    p = __fmaf_rn(t2, p, 8.3333338e-3f);
+    p = __fmaf_rn(t2, p, -0.16666667f);
+    r = __fmaf_rn(__fmul_rn(t, t2), p, t);
+  }
+  return __fmul_rn(sgn, r);
+}
+
+// Rule J7 / reading J7n, normal weights: Box-Muller in fp32, u1 = ((x1 >> 8)
+// + 1) 2^-24 in (0,1], u2 = (x2 >> 8) 2^-24, z = sqrt(-2 logf_j10(u1)) *
+// cos2pi_j7(u2) (IEEE sqrt), w = fmaf(sigma, z, mu).
+__device__ __forceinline__ float normal_weight(uint32_t x1, uint32_t x2, float mu,
+                                               float sigma) {
+  const float u1 = __fmul_rn(__uint2float_rn((x1 >> 8) + 1u), 0x1p-24f);
+  const float u2 = __fmul_rn(__uint2float_rn(x2 >> 8), 0x1p-24f);
+  const float radius = __fsqrt_rn(__fmul_rn(-2.0f, logf_j10(u1)));
+  return __fmaf_rn(sigma, __fmul_rn(radius, cos2pi_j7(u2)), mu);
 }
 
 // Rule F1: q(w) = round-half-even(w * 2^32) as int64.
