@@ -250,10 +250,14 @@ __device__ unsigned long long g_csr_t[1024][8];
 // (accumulate: +=).  Homogeneous partials are event counts: fl32(n * w) or
 // n * q.  Deterministic for counts and fixed point.
 // C16: homogeneous partials are 16-bit counts (k_jit_tiled's packed tiles).
+// Only the first `used` CTAs of a tile received work (rows / items are
+// dealt 32 per CTA in order), so only their partials are summed -- a call
+// with few active rows does not read 148 empty partial tiles.
 template <int KIND, bool HOMO, int NT, bool C16 = false>
 __device__ __forceinline__ void tile_reduce(const void *partials, size_t first, int group,
-                                            int groups, int tile_cols, int width, int64_t c0,
-                                            void *out, int accumulate, float w, long long q) {
+                                            int groups, int used, int tile_cols, int width,
+                                            int64_t c0, void *out, int accumulate, float w,
+                                            long long q) {
   const int per = (width + groups - 1) / groups;
   const int s0 = group * per, s1 = min(width, s0 + per);
   const size_t stride = static_cast<size_t>(tile_cols);
@@ -264,10 +268,10 @@ __device__ __forceinline__ void tile_reduce(const void *partials, size_t first, 
       unsigned long long n = 0;
       if (C16) {
         const unsigned short *p = static_cast<const unsigned short *>(partials) + base + cc;
-        for (int g = 0; g < groups; ++g) n += __ldcg(p + g * stride);
+        for (int g = 0; g < used; ++g) n += __ldcg(p + g * stride);
       } else {
         const unsigned *p = static_cast<const unsigned *>(partials) + base + cc;
-        for (int g = 0; g < groups; ++g) n += __ldcg(p + g * stride);
+        for (int g = 0; g < used; ++g) n += __ldcg(p + g * stride);
       }
       if (KIND == 0) {
         const float v = __fmul_rn(__ull2float_rn(n), w);
@@ -281,13 +285,13 @@ __device__ __forceinline__ void tile_reduce(const void *partials, size_t first, 
     } else if (KIND == 0) {
       const float *p = static_cast<const float *>(partials) + base + cc;
       float v = 0.f;
-      for (int g = 0; g < groups; ++g) v = __fadd_rn(v, __ldcg(p + g * stride));
+      for (int g = 0; g < used; ++g) v = __fadd_rn(v, __ldcg(p + g * stride));
       float *o = static_cast<float *>(out) + c;
       *o = accumulate ? __fadd_rn(*o, v) : v;
     } else {
       const long long *p = static_cast<const long long *>(partials) + base + cc;
       long long v = 0;
-      for (int g = 0; g < groups; ++g) v += __ldcg(p + g * stride);
+      for (int g = 0; g < used; ++g) v += __ldcg(p + g * stride);
       long long *o = static_cast<long long *>(out) + c;
       *o = accumulate ? *o + v : v;
     }
@@ -485,18 +489,26 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs 
   // rows from the active list: warp w of the tile takes k = w, w + NW, ... --
   // dealt evenly over the tile's CTAs (a per-CTA compaction of its slice of
   // the spike words avoids the compaction launch but leaves ~12 % imbalance)
-  stream_rows(a.active, false, *a.count, static_cast<int64_t>(group) * kStreamWarps + warp,
+  const int64_t n_active_rows = *a.count;
+  stream_rows(a.active, false, n_active_rows, static_cast<int64_t>(group) * kStreamWarps + warp,
               static_cast<int64_t>(a.groups) * kStreamWarps);
   CSR_MARK(2);
   __syncthreads();
   CSR_MARK(3);
-  // partial tile -> [tile][group][tile_cols], 16-byte stores
-  char *dst = static_cast<char *>(a.partials) +
-              (static_cast<size_t>(tile) * a.groups + group) * a.tile_cols * acc_bytes;
-  const int n16 = width * acc_bytes / 16;
-  for (int k = tid; k < n16; k += kStreamThreads)
-    reinterpret_cast<uint4 *>(dst)[k] = reinterpret_cast<const uint4 *>(sm)[k];
-  for (int b = n16 * 16 + tid; b < width * acc_bytes; b += kStreamThreads) dst[b] = sm[b];
+  // partial tile -> [tile][group][tile_cols], 16-byte stores.  Rows are
+  // dealt 32 per CTA in order, so only the first `used` CTAs of a tile got
+  // any; with the fused reduction the others skip the flush (it reads only
+  // the first `used` partials), k_csr_reduce reads them all.
+  const int64_t cta_rows = (n_active_rows + 31) / 32;
+  const int used = cta_rows < a.groups ? static_cast<int>(cta_rows) : a.groups;
+  if (a.out == nullptr || group < used) {
+    char *dst = static_cast<char *>(a.partials) +
+                (static_cast<size_t>(tile) * a.groups + group) * a.tile_cols * acc_bytes;
+    const int n16 = width * acc_bytes / 16;
+    for (int k = tid; k < n16; k += kStreamThreads)
+      reinterpret_cast<uint4 *>(dst)[k] = reinterpret_cast<const uint4 *>(sm)[k];
+    for (int b = n16 * 16 + tid; b < width * acc_bytes; b += kStreamThreads) dst[b] = sm[b];
+  }
   CSR_MARK(4);
   if (a.out == nullptr) return;
   // fused reduction (cooperative launch: every CTA is resident): after a
@@ -506,8 +518,8 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs 
   cg::this_grid().sync();
   CSR_MARK(5);
   tile_reduce<KIND, HOMO, kStreamThreads, C16>(a.partials, static_cast<size_t>(tile) * a.groups,
-                                         group, a.groups, a.tile_cols, width, c0, a.out,
-                                         a.accumulate, a.w, a.q);
+                                               group, a.groups, used, a.tile_cols, width, c0,
+                                               a.out, a.accumulate, a.w, a.q);
   CSR_MARK(6);
 }
 

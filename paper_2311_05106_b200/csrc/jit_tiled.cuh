@@ -148,21 +148,27 @@ __global__ void __launch_bounds__(kJitTiledThreads, 1) k_jit_tiled(JitTiledArgs 
     }
   }
   __syncthreads();
-  char *dst = static_cast<char *>(a.partials) +
-              static_cast<size_t>(blockIdx.x) * a.tile_cols * acc_bytes;
-  const int n16 = width * acc_bytes / 16;
-  for (int k = tid; k < n16; k += kJitTiledThreads)
-    reinterpret_cast<uint4 *>(dst)[k] = reinterpret_cast<const uint4 *>(sm)[k];
-  for (int b = n16 * 16 + tid; b < width * acc_bytes; b += kJitTiledThreads) dst[b] = sm[b];
+  // items are dealt 32 per CTA in order: only the first `used` CTAs of the
+  // tile got any, and only their partials are written and reduced
+  const int64_t cta_items = (n_items + 31) / 32;
+  const int used = cta_items < groups ? static_cast<int>(cta_items) : groups;
+  if (group < used) {
+    char *dst = static_cast<char *>(a.partials) +
+                static_cast<size_t>(blockIdx.x) * a.tile_cols * acc_bytes;
+    const int n16 = width * acc_bytes / 16;
+    for (int k = tid; k < n16; k += kJitTiledThreads)
+      reinterpret_cast<uint4 *>(dst)[k] = reinterpret_cast<const uint4 *>(sm)[k];
+    for (int b = n16 * 16 + tid; b < width * acc_bytes; b += kJitTiledThreads) dst[b] = sm[b];
+  }
   if (a.events) {
     ev = __reduce_add_sync(0xffffffffu, ev);
     if (lane == 0 && ev) atomicAdd(a.events, static_cast<unsigned long long>(ev));
   }
   __threadfence();
   cg::this_grid().sync();
-  tile_reduce<KIND, HOMO, kJitTiledThreads, C16>(a.partials, static_cast<size_t>(a.cta0[tile]), group,
-                                            groups, a.tile_cols, width, t0, a.out, a.accumulate,
-                                            s.w0, s.q);
+  tile_reduce<KIND, HOMO, kJitTiledThreads, C16>(a.partials, static_cast<size_t>(a.cta0[tile]),
+                                                 group, groups, used, a.tile_cols, width, t0,
+                                                 a.out, a.accumulate, s.w0, s.q);
 }
 
 }  // namespace bp
