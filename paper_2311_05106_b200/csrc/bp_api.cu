@@ -568,6 +568,11 @@ bp_status jit_event_mv(int law, const bp_jitconn *spec, float w0, float w1,
     t.tile_cols = tp.tile_cols;
     t.n_tiles = tp.n_tiles;
     for (int k = 0; k <= tp.n_tiles; ++k) t.cta0[k] = tp.cta0[k];
+    // CTA-parallel chains advance 32 chunks (4096 gaps) per round
+    const uint64_t max_gap = jr.geo_c != 0.f ? jr.geo_cap : jr.K;
+    t.cta_ok = (static_cast<uint64_t>(n_cols) + 4096ull * max_gap < (1ull << 32)) &&
+               !std::getenv("BP_JIT_NO_CTA_CHAINS");
+    t.row_chunks = static_cast<int>(row_events / 128.0) + 1;
     if (launch_jit_tiled(t, law, out_kind, vec, tp, st)) return launched();
   }
   if (!(flags & BP_ACCUMULATE) && col_end > col_begin)

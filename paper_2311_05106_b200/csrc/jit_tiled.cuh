@@ -37,6 +37,8 @@ struct JitTiledArgs {
   int32_t tile_cols, n_tiles;
   int32_t cta0[kJitMaxTiles + 1];   // first CTA of each tile (CTA-major partials)
   unsigned long long *events;       // nullable
+  int cta_ok;                       // n_cols + 4096 max_gap < 2^32: CTA-parallel chains allowed
+  int row_chunks;                   // expected 128-gap chunks of a row in the partition
 };
 
 // VEC: non-event product with a float vector (every row, contribution v[r] w:
@@ -86,71 +88,132 @@ __global__ void __launch_bounds__(kJitTiledThreads, 1) k_jit_tiled(JitTiledArgs 
   const int64_t n_items = (VEC ? a.n_rows : static_cast<int64_t>(*a.count)) * s.n_seg;
   const int64_t NW = static_cast<int64_t>(groups) * (kJitTiledThreads / 32);
   uint32_t ev = 0;
-  for (int64_t item = static_cast<int64_t>(group) * (kJitTiledThreads / 32) + warp;
-       item < n_items; item += NW) {
-    const uint32_t row = static_cast<uint32_t>(VEC ? item / s.n_seg : a.active[item / s.n_seg]);
-    float vr = 1.f;
-    if (VEC) {
-      vr = __ldg(a.v + row);
-      if (vr == 0.f) continue;                                  // contributes nothing
+  // one chunk of 128 gaps of (row, seg): lane holds gaps g (one Philox
+  // block), its inclusive warp prefix incl and the chunk start; emits the
+  // lane's events inside [g0, stop)
+  auto emit = [&](uint32_t row, uint32_t seg, uint32_t blk, uint32_t q0, uint32_t q1,
+                  uint32_t q2, uint32_t t, uint32_t incl, uint32_t start, uint32_t stop,
+                  float vr) {
+    const uint32_t pos0 = start + (incl - t);
+    const uint32_t pos[4] = {pos0, pos0 + q0, pos0 + q0 + q1, pos0 + q0 + q1 + q2};
+    // this lane's events inside the tile (positions ascend along the chain)
+    if (!(pos0 < stop && pos[3] >= g0)) return;
+    float w[4] = {s.w0, s.w0, s.w0, s.w0};
+    if (LAW == 1) {
+      const u32x4 x = philox_block(s.seed, kTagWeight, row, seg, blk);
+      w[0] = uniform_weight(x.x, s.w0, s.w1); w[1] = uniform_weight(x.y, s.w0, s.w1);
+      w[2] = uniform_weight(x.z, s.w0, s.w1); w[3] = uniform_weight(x.w, s.w0, s.w1);
+    } else if (LAW == 2) {
+      const u32x4 x = philox_block(s.seed, kTagWeight, row, seg, 2u * blk);
+      if (pos[0] >= g0) w[0] = normal_weight(x.x, x.y, s.w0, s.w1);
+      if (pos[1] >= g0 && pos[1] < stop) w[1] = normal_weight(x.z, x.w, s.w0, s.w1);
+      if (pos[2] < stop && pos[3] >= g0) {
+        const u32x4 y = philox_block(s.seed, kTagWeight, row, seg, 2u * blk + 1u);
+        if (pos[2] >= g0) w[2] = normal_weight(y.x, y.y, s.w0, s.w1);
+        if (pos[3] < stop) w[3] = normal_weight(y.z, y.w, s.w0, s.w1);
+      }
     }
-    const uint32_t seg = s.seg_first + static_cast<uint32_t>(item % s.n_seg);
-    const uint32_t seg_begin = seg * s.L;
-    const uint32_t seg_end = min(seg_begin + s.L, a.n_cols);
-    const uint32_t stop = min(seg_end, g1);
-    if (seg_begin >= g1 || seg_end <= g0) continue;             // warp-uniform
-    u32x4 g = philox_block(s.seed, kTagGap, row, seg, lane);
-    uint32_t start = seg_begin + jit_first<GEO>(s, row, seg);
-    uint32_t chunk = 0;
-    while (start < stop) {                                      // warp-uniform
-      const uint32_t blk = chunk * 32u + lane;
-      const uint32_t q0 = jit_gap<GEO>(s, g.x), q1 = jit_gap<GEO>(s, g.y);
-      const uint32_t q2 = jit_gap<GEO>(s, g.z), q3 = jit_gap<GEO>(s, g.w);
-      const uint32_t p1 = q0, p2 = q0 + q1, p3 = p2 + q2, t = p3 + q3;
-      uint32_t incl = t;
 #pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= off) incl += v;
+    for (int k = 0; k < 4; ++k) {
+      if (pos[k] >= g0 && pos[k] < stop) {
+        add(pos[k], w[k], vr);
+        ++ev;
       }
-      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-      const uint32_t pos0 = start + (incl - t);
-      const uint32_t pos[4] = {pos0, pos0 + p1, pos0 + p2, pos0 + p3};
-      // this lane's events inside the tile (positions ascend along the chain)
-      const bool any = pos0 < stop && pos[3] >= g0;
-      if (any) {
-        float w[4] = {s.w0, s.w0, s.w0, s.w0};
-        if (LAW == 1) {
-          const u32x4 x = philox_block(s.seed, kTagWeight, row, seg, blk);
-          w[0] = uniform_weight(x.x, s.w0, s.w1); w[1] = uniform_weight(x.y, s.w0, s.w1);
-          w[2] = uniform_weight(x.z, s.w0, s.w1); w[3] = uniform_weight(x.w, s.w0, s.w1);
-        } else if (LAW == 2) {
-          const u32x4 x = philox_block(s.seed, kTagWeight, row, seg, 2u * blk);
-          if (pos[0] >= g0) w[0] = normal_weight(x.x, x.y, s.w0, s.w1);
-          if (pos[1] >= g0 && pos[1] < stop) w[1] = normal_weight(x.z, x.w, s.w0, s.w1);
-          if (pos[2] < stop && pos[3] >= g0) {
-            const u32x4 y = philox_block(s.seed, kTagWeight, row, seg, 2u * blk + 1u);
-            if (pos[2] >= g0) w[2] = normal_weight(y.x, y.y, s.w0, s.w1);
-            if (pos[3] < stop) w[3] = normal_weight(y.z, y.w, s.w0, s.w1);
-          }
-        }
+    }
+  };
+  auto warp_scan = [&](uint32_t t) {
+    uint32_t incl = t;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          if (pos[k] >= g0 && pos[k] < stop) {
-            add(pos[k], w[k], vr);
-            ++ev;
-          }
-        }
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += v;
+    }
+    return incl;
+  };
+
+  // CTA-parallel chains for long rows (>= 32 chunks of 128 gaps) when a
+  // CTA's share of items, each ~4 chunk-times per round of 32 chunks
+  // (barriers, and every used CTA flushes and reduces a partial tile), beats
+  // a warp taking a whole row (measured on the config-2 cells: 100 rows of
+  // 5,000 events 53 -> 31 us; 1,000 such rows are faster per warp)
+  const int64_t ipc = (n_items + groups - 1) / groups;
+  const int rounds = (a.row_chunks + 31) / 32;
+  const bool cta_mode = a.cta_ok && a.row_chunks >= 32 &&
+                        4 * ipc * rounds <= static_cast<int64_t>(a.row_chunks);
+  if (cta_mode) {
+    // few items (long rows, low density): the chain of one item is
+    // regenerated by the whole CTA, 32 chunks per round -- warp w takes
+    // chunk 32 r + w, the chunk starts follow from a block prefix of the 32
+    // chunk totals (Philox blocks do not depend on the running position)
+    __shared__ uint32_t chunk_tot[32];
+    for (int64_t item = group; item < n_items; item += groups) {   // block-uniform
+      const uint32_t row = static_cast<uint32_t>(VEC ? item / s.n_seg : a.active[item / s.n_seg]);
+      float vr = 1.f;
+      if (VEC) {
+        vr = __ldg(a.v + row);
+        if (vr == 0.f) continue;
       }
-      start += total;
-      ++chunk;
-      if (start < stop) g = philox_block(s.seed, kTagGap, row, seg, chunk * 32u + lane);
+      const uint32_t seg = s.seg_first + static_cast<uint32_t>(item % s.n_seg);
+      const uint32_t seg_begin = seg * s.L;
+      const uint32_t seg_end = min(seg_begin + s.L, a.n_cols);
+      const uint32_t stop = min(seg_end, g1);
+      if (seg_begin >= g1 || seg_end <= g0) continue;
+      uint32_t round_start = seg_begin + jit_first<GEO>(s, row, seg);
+      for (uint32_t r = 0; round_start < stop; ++r) {              // block-uniform
+        const uint32_t chunk = 32u * r + static_cast<uint32_t>(warp);
+        const u32x4 g = philox_block(s.seed, kTagGap, row, seg, chunk * 32u + lane);
+        const uint32_t q0 = jit_gap<GEO>(s, g.x), q1 = jit_gap<GEO>(s, g.y);
+        const uint32_t q2 = jit_gap<GEO>(s, g.z), q3 = jit_gap<GEO>(s, g.w);
+        const uint32_t t = q0 + q1 + q2 + q3;
+        const uint32_t incl = warp_scan(t);
+        if (lane == 31) chunk_tot[warp] = incl;
+        __syncthreads();
+        uint32_t before = 0, round_total = 0;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const uint32_t v = chunk_tot[k];
+          before += k < warp ? v : 0u;
+          round_total += v;
+        }
+        emit(row, seg, chunk * 32u + lane, q0, q1, q2, t, incl, round_start + before, stop, vr);
+        round_start += round_total;
+        __syncthreads();                                           // chunk_tot reused
+      }
+    }
+  } else {
+    for (int64_t item = static_cast<int64_t>(group) * (kJitTiledThreads / 32) + warp;
+         item < n_items; item += NW) {
+      const uint32_t row = static_cast<uint32_t>(VEC ? item / s.n_seg : a.active[item / s.n_seg]);
+      float vr = 1.f;
+      if (VEC) {
+        vr = __ldg(a.v + row);
+        if (vr == 0.f) continue;                                  // contributes nothing
+      }
+      const uint32_t seg = s.seg_first + static_cast<uint32_t>(item % s.n_seg);
+      const uint32_t seg_begin = seg * s.L;
+      const uint32_t seg_end = min(seg_begin + s.L, a.n_cols);
+      const uint32_t stop = min(seg_end, g1);
+      if (seg_begin >= g1 || seg_end <= g0) continue;             // warp-uniform
+      u32x4 g = philox_block(s.seed, kTagGap, row, seg, lane);
+      uint32_t start = seg_begin + jit_first<GEO>(s, row, seg);
+      uint32_t chunk = 0;
+      while (start < stop) {                                      // warp-uniform
+        const uint32_t q0 = jit_gap<GEO>(s, g.x), q1 = jit_gap<GEO>(s, g.y);
+        const uint32_t q2 = jit_gap<GEO>(s, g.z), q3 = jit_gap<GEO>(s, g.w);
+        const uint32_t t = q0 + q1 + q2 + q3;
+        const uint32_t incl = warp_scan(t);
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        emit(row, seg, chunk * 32u + lane, q0, q1, q2, t, incl, start, stop, vr);
+        start += total;
+        ++chunk;
+        if (start < stop) g = philox_block(s.seed, kTagGap, row, seg, chunk * 32u + lane);
+      }
     }
   }
   __syncthreads();
   // items are dealt 32 per CTA in order: only the first `used` CTAs of the
   // tile got any, and only their partials are written and reduced
-  const int64_t cta_items = (n_items + 31) / 32;
+  const int64_t cta_items = cta_mode ? n_items : (n_items + 31) / 32;
   const int used = cta_items < groups ? static_cast<int>(cta_items) : groups;
   if (group < used) {
     char *dst = static_cast<char *>(a.partials) +
