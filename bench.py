@@ -626,18 +626,21 @@ def run_emulated_rank(args):
     G = args.emulate_world
     wl = args.workload
     n = network_size(wl, G)
-    net, _ = build_network(wl, G, 0, {"fix64": True, "fix32": "fix32", "f32": False}[args.g],
+    R = args.emulate_rank
+    net, _ = build_network(wl, G, R, {"fix64": True, "fix32": "fix32", "f32": False}[args.g],
                            torch.device("cuda", 0))
     lw = net.part.local_words
     words = net.spikes.numel()
     assert words == G * lw
-    local = net.spikes[:lw]
-    remote = net.spikes[lw:].view(G - 1, lw)
+    slots = net.spikes.view(G, lw)
+    local = slots[R].clone()
 
     def step(k):
         net.net.scatter()
         net.net.update()
-        remote.copy_(local.expand(G - 1, lw))
+        # every slot <- this rank's words (its own slot: the same values)
+        local.copy_(slots[R])
+        slots.copy_(local.expand(G, lw))
 
     for k in range(args.warmup):
         step(k)
@@ -672,9 +675,9 @@ def run_emulated_rank(args):
             "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": args.g, "data": "synthetic",
-            "config": {"workload": "%s rank 0 of %d" % (wl, G), "n_total": n,
+            "config": {"workload": "%s rank %d of %d" % (wl, R, G), "n_total": n,
                        "n_per_gpu": net.part.col_end - net.part.col_begin, "emulated_world": G,
-                       "exchange": "replaced by one device copy of rank 0's spike words "
+                       "exchange": "replaced by a device copy of this rank's spike words "
                                    "into the %d remote slots (%.1f MB/step)" % (
                                        G - 1, (words - lw) * 4 / 1e6),
                        "host_loop": "CUDA graph of %d steps" % period if graph is not None
@@ -861,6 +864,8 @@ def main():
     ap.add_argument("--emulate-world", type=int, default=0,
                     help="one GPU: time rank 0 of a G-GPU weak-scaling run (exchange "
                          "replaced by a device copy; not a multi-GPU number)")
+    ap.add_argument("--emulate-rank", type=int, default=0,
+                    help="--emulate-world: which rank's partition to time")
     ap.add_argument("--no-graph", action="store_true",
                     help="N > 1: eager per-step calls instead of the captured CUDA graph")
     ap.add_argument("--workload",

@@ -122,7 +122,8 @@ int grid_for_items(int64_t items_upper, int sms) {
 // block-aggregated claims (k_compact) from 64 k words on, 4 words per thread
 // once the vector fills every SM with 8 blocks of 1024-word iterations
 void launch_compact(const uint32_t *spikes, int64_t n, int32_t *active, int32_t *count,
-                    int sms, cudaStream_t st, int32_t id_base = 0) {
+                    int sms, cudaStream_t st, int32_t id_base = 0, int64_t skip_b = 0,
+                    int64_t skip_e = 0) {
   const int64_t words = (n + 31) / 32;
   const int64_t cap = static_cast<int64_t>(sms) * 8;
   if (words < (int64_t{1} << 16)) {
@@ -130,7 +131,7 @@ void launch_compact(const uint32_t *spikes, int64_t n, int32_t *active, int32_t 
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     bp::k_compact_warp<<<static_cast<int>(blocks), 256, 0, st>>>(spikes, n, active, count,
-                                                                 id_base);
+                                                                 id_base, skip_b, skip_e);
     return;
   }
   const bool wide = words >= cap * 4 * bp::kCompactThreads;
@@ -140,10 +141,10 @@ void launch_compact(const uint32_t *spikes, int64_t n, int32_t *active, int32_t 
   if (blocks < 1) blocks = 1;
   if (wide)
     bp::k_compact<4><<<static_cast<int>(blocks), bp::kCompactThreads, 0, st>>>(
-        spikes, n, active, count, id_base);
+        spikes, n, active, count, id_base, skip_b, skip_e);
   else
     bp::k_compact<1><<<static_cast<int>(blocks), bp::kCompactThreads, 0, st>>>(
-        spikes, n, active, count, id_base);
+        spikes, n, active, count, id_base, skip_b, skip_e);
 }
 
 // ------------------------------------------------------------- CSR plan
@@ -1311,8 +1312,10 @@ bp_status launch_bin(bp_network *net, const int32_t *active, const int32_t *coun
 
 // Bin the events of the spikes in words [w_begin, w_end) of the global
 // vector (neurons [32 w_begin, min(32 w_end, n))) into bucket parity `par`.
+// words [skip_b, skip_e) (absolute) are skipped: one pass over the remote
+// words on both sides of a partition's own range
 bp_status bin_spike_range(bp_network *net, int64_t w_begin, int64_t w_end, int par,
-                          cudaStream_t st) {
+                          cudaStream_t st, int64_t skip_b = 0, int64_t skip_e = 0) {
   if (w_end <= w_begin) return BP_OK;
   const int64_t first = w_begin * 32;
   const int64_t last = w_end * 32 < net->d.n ? w_end * 32 : net->d.n;
@@ -1321,7 +1324,7 @@ bp_status bin_spike_range(bp_network *net, int64_t w_begin, int64_t w_end, int p
   int32_t *count = net->count;
   BP_CUDA(cudaMemsetAsync(count, 0, sizeof(int32_t), st));
   launch_compact(net->d.spikes + w_begin, last - first, active, count, net->sms, st,
-                 static_cast<int32_t>(first));
+                 static_cast<int32_t>(first), skip_b - w_begin, skip_e - w_begin);
   bp_status s = launched();
   if (s != BP_OK) return s;
   return launch_bin(net, active, count, par, last - first, st);
@@ -1668,9 +1671,8 @@ bp_status bp_network_scatter(bp_network *net, bp_stream stream) {
   // the exchanged spikes are those of step steps_done - 1: delivered at
   // step steps_done - 1 + delay
   const int slot = static_cast<int>((net->steps_done + net->delay - 1) % net->slots);
-  s = bin_spike_range(net, 0, lw0, slot, st);
-  if (s != BP_OK) return s;
-  return bin_spike_range(net, lw1, net->global_words, slot, st);
+  // one compaction + one binning launch for the words on both sides
+  return bin_spike_range(net, 0, net->global_words, slot, st, lw0, lw1);
 }
 
 bp_status bp_network_update(bp_network *net, uint32_t *raster_row, bp_stream stream) {

@@ -43,19 +43,21 @@ __device__ __forceinline__ void count_events(unsigned long long *counter,
 }
 
 // ---------------------------------------------------------------- a1
-// Short vectors (config-2 calls): warps warp0, warp0 + n_warps, ... each
+// Words [skip_b, skip_e) count as empty (a partition's own words in
+// bp_network_scatter).  Short vectors (config-2 calls): warps warp0, warp0 + n_warps, ... each
 // take 32 spike words: warp scan of the popcounts, one atomicAdd per warp
 // claims a slice of the active list (no block barriers).
 __device__ __forceinline__ void compact_words(const uint32_t *__restrict__ spikes, int64_t n,
                                               int32_t *__restrict__ active,
                                               int32_t *__restrict__ count, int32_t id_base,
-                                              int64_t warp0, int64_t n_warps) {
+                                              int64_t warp0, int64_t n_warps,
+                                              int64_t skip_b, int64_t skip_e) {
   const int lane = threadIdx.x & 31;
   const int64_t n_words = (n + 31) >> 5;
   for (int64_t base = warp0 * 32; base < n_words; base += n_warps * 32) {
     const int64_t wi = base + lane;
     uint32_t word = 0;
-    if (wi < n_words) {
+    if (wi < n_words && (wi < skip_b || wi >= skip_e)) {
       word = __ldg(spikes + wi);
       const int64_t valid = n - (wi << 5);
       if (valid < 32) word &= (1u << valid) - 1u;
@@ -83,10 +85,10 @@ __device__ __forceinline__ void compact_words(const uint32_t *__restrict__ spike
 __global__ void __launch_bounds__(256)
 k_compact_warp(const uint32_t *__restrict__ spikes, int64_t n,
           int32_t *__restrict__ active, int32_t *__restrict__ count,
-          int32_t id_base) {
+          int32_t id_base, int64_t skip_b, int64_t skip_e) {
   compact_words(spikes, n, active, count, id_base,
                 (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5,
-                (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5);
+                (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5, skip_b, skip_e);
 }
 
 // Long vectors (the remote words of a partitioned network): block-aggregated
@@ -104,7 +106,7 @@ template <int WPT>
 __global__ void __launch_bounds__(kCompactThreads)
 k_compact(const uint32_t *__restrict__ spikes, int64_t n,
           int32_t *__restrict__ active, int32_t *__restrict__ count,
-          int32_t id_base) {
+          int32_t id_base, int64_t skip_b, int64_t skip_e) {
   __shared__ int32_t warp_tot[kCompactThreads / 32];
   __shared__ int32_t block_base;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -118,7 +120,7 @@ k_compact(const uint32_t *__restrict__ spikes, int64_t n,
     for (int k = 0; k < WPT; ++k) {
       const int64_t wi = w0 + WPT * tid + k;
       uint32_t word = 0;
-      if (wi < n_words) {
+      if (wi < n_words && (wi < skip_b || wi >= skip_e)) {
         word = __ldg(spikes + wi);
         const int64_t valid = n - (wi << 5);
         if (valid < 32) word &= (1u << valid) - 1u;
