@@ -508,7 +508,7 @@ def run_ours(args):
         # libbp kernels in the timed region: k_step + k_bin per step (world 1),
         # one k_small_net launch for small networks, and k_compact + k_bin +
         # k_step per step for world > 1 (NCCL kernels not counted)
-        "gpu_launches": (1 if small else (2 if world == 1 else 3) * args.steps),
+        "gpu_launches": (1 if small else (2 if world == 1 else 4) * args.steps),
         "clocks": clocks,
         "roofline": roofline,
         "cpu_baseline": cpu,
