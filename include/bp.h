@@ -14,8 +14,18 @@
  *   bp_neuron_step           -- Expon + COBA + LIF
  *                               or COBA-HH (rule H1, EXTERNAL)   [a5, a6]
  *   bp_network_*             -- Listing S3's update() loop: 1-step
- *                               delayed spikes -> scatter -> neuron update [a7]
- * Rule names (J1..J9, F1, N1, H1, S1, R-numbered readings) refer to DESIGN.md.
+ *                               delayed spikes -> scatter -> neuron update [a7];
+ *                               bp_network_scatter / _update(_overlap): the two
+ *                               halves of a partitioned step around the spike
+ *                               all-gather                     [a8]
+ *   bp_jitconn_mv_*          -- mv_prob_* with a float vector (NEXT 1, MV1)
+ *   bp_csrmv_gather,
+ *   bp_event_csrmv_grad      -- csrmv(transpose=False) and the reverse mode
+ *                               (NEXT 3, G1)
+ *   bp_jitconn.gap_law       -- BP_GAP_GEOMETRIC: the Geo(p) sampler the paper
+ *                               compares against (NEXT 4, J10)
+ * Rule names (J1..J10, J7n, F1, F2, N1, H1, S1, D1, G1, MV1, R-numbered
+ * readings) refer to DESIGN.md.
  *
  * Conventions (all entry points):
  *  - Every pointer argument is a DEVICE pointer owned by the caller unless
