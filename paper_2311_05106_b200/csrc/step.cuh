@@ -518,7 +518,10 @@ __device__ __forceinline__ void pass_emit(const StepArgs &a, uint32_t nib, int64
 // LIF (memory-bound): 256 threads, 4 passes, register double buffering.
 // HH (FP32-latency-bound): 512 threads, 2 passes (more warps, 128 registers).
 template <int MODEL, int KIND>
-__global__ void __launch_bounds__(MODEL == 0 ? kStepThreads : 512, MODEL == 0 ? 1024 / kStepThreads : 1)
+#ifndef BP_STEP_MINB
+#define BP_STEP_MINB (1024 / BP_STEP_THREADS)
+#endif
+__global__ void __launch_bounds__(MODEL == 0 ? kStepThreads : 512, MODEL == 0 ? BP_STEP_MINB : 1)
 k_step(StepArgs a) {
   __shared__ int32_t cnt_e[kTile];
   __shared__ int32_t cnt_i[kTile];
