@@ -106,6 +106,8 @@ def lib():
         _lib.or_logf_j10.restype = f32
         _lib.or_cos2pi_j7.argtypes = [f32]
         _lib.or_cos2pi_j7.restype = f32
+        _lib.or_gap_draws.argtypes = [i32, f64, u64, u64]
+        _lib.or_gap_draws.restype = u64
         _lib.or_geo_gap.argtypes = [f32, u32, u32]
         _lib.or_geo_gap.restype = u32
         _lib.or_fix32_add.argtypes = [P, P, i64]
@@ -172,6 +174,11 @@ def logf_j10(u: float) -> float:
 def cos2pi_j7(u: float) -> float:
     """Reading J7n's specified fp32 cos(2 pi u)."""
     return float(lib().or_cos2pi_j7(u))
+
+
+def gap_draws(geometric: bool, p: float, n: int, seed: int = 1) -> int:
+    """Sum of n gap draws (sampler-cost probe): U[1, K] or Geo(p)."""
+    return int(lib().or_gap_draws(1 if geometric else 0, p, n, seed))
 
 
 def geo_gap(c: float, cap: int, x: int) -> int:

@@ -202,6 +202,22 @@ uint32_t or_geo_gap(float c, uint32_t cap, uint32_t x) {
   return g > cap ? cap : g;
 }
 
+/* Sampler-cost probe (App. C: uniform gaps are "one order of
+ * magnitude faster than sampling from Geo[p]"; SPEC bench_gap_samplers):
+ * sum of n gaps drawn from counter-based words with U[1, K] (geometric == 0)
+ * or Geo(p) by inversion (geometric != 0, c = fl32(log1p(-p))).  Timed by
+ * tests/test_oracle_jit.py; the sums pin both means (K+1)/2 and ~1/p. */
+uint64_t or_gap_draws(int geometric, double p, uint64_t n, uint64_t seed) {
+  uint32_t K = or_conn_len(p);
+  float c = (float)log1p(-p);
+  uint64_t sum = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    uint32_t x = or_word(seed, 0u, (uint32_t)(i >> 20), 0u, (uint32_t)(i & 0xFFFFFu));
+    sum += geometric ? or_geo_gap(c, 0x7FFFFFFFu, x) : uniform_int(1u, K, x);
+  }
+  return sum;
+}
+
 /* Offset of the first target of (row, seg) from the segment start: rule J5
  * (uniform gaps) or G_0 - 1 (rule J10). */
 static uint32_t first_offset_of(uint64_t seed, uint32_t K, uint32_t L,

@@ -424,3 +424,26 @@ def test_cos2pi_j7_accuracy_and_special_values(orc):
     for u in us[:2000]:
         if u < 0.5:
             assert orc.cos2pi_j7(float(u)) == orc.cos2pi_j7(float(np.float32(1.0) - u))
+
+
+def test_uniform_gaps_cheaper_than_geometric_on_cpu(orc):
+    """App. C: sampling U[1, K] gaps is cheaper than Geo(p) by
+    inversion (the paper: an order of magnitude; SPEC S:168 relaxes the
+    desk-scale check to strictly faster).  Both draw from the same Philox
+    words here, which dominate on a CPU too, so only 'faster' is asserted;
+    the sums pin the means (K + 1)/2 and ~1/p within 1 %."""
+    import time
+    p, n = 0.05, 2_000_000
+    K = orc.conn_len(p)
+    best = {}
+    for geo in (False, True):
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            tot = orc.gap_draws(geo, p, n)
+            ts.append(time.perf_counter() - t0)
+        best[geo] = min(ts)
+        mean = tot / n
+        want = 1 / p if geo else (K + 1) / 2
+        assert abs(mean - want) < 0.01 * want, (geo, mean, want)
+    assert best[False] < best[True], best
