@@ -13,7 +13,10 @@ product's bit-packed words is done by the tests, not here.
 
 Parity status per function:
   philox / conn_len / jit_row / jit_event_mv / event_csrmv /
-  lif_step / hh_step / expf / run_network: pinned (tests/test_oracle_*.py).
+  lif_step / hh_step / expf / run_network: pinned (tests/test_oracle_*.py);
+  run_network's fp32 conductance branch (rule N1-f32, the bench's default
+  mode) by the exactly rounded increment (exact rational arithmetic) and the
+  fp64 recursion within its rounding bound (test_oracle_network.py).
   run_network firing *rates*: parity unpinned by the paper (reading R23) --
   the paper prints no COBA statistics; rasters are pinned only through the
   closed-form w = 0 network and the per-step primitives.

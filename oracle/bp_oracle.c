@@ -579,7 +579,7 @@ void or_lif_step(const or_lif_params *p, int64_t n, float *v, void *g_exc,
  *   r = fmaf(k, -ln2_hi, x); r = fmaf(k, -ln2_lo, r);
  *   p = degree-7 Taylor polynomial of e^r by Horner with fmaf;
  *   result = p * 2^k.
- * Pinned by: |or_expf(x) - exp(x)| <= 4 ulp on a dense grid of [-87, 88]
+ * Pinned by: |or_expf(x) - exp(x)| <= 2 ulp on a dense grid of [-87, 88]
  * against libm's double exp (test_oracle_neuron.py).
  * ---------------------------------------------------------------------- */
 float or_expf(float x) {

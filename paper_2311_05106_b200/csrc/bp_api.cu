@@ -2,6 +2,7 @@
 // and the per-step orchestration of the network (include/bp.h).
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <new>
@@ -89,6 +90,24 @@ inline bool aligned(const void *p, size_t a) {
 constexpr int64_t kMaxDim = (int64_t{1} << 31) - 1;
 
 size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// cudaFuncSetAttribute applies to the CURRENT device only: a kernel's opt-in
+// is remembered per device ordinal (bit d of `mask`), so a second GPU used
+// from the same process gets its own call.  Returns true the first time on
+// this device.
+bool first_on_device(std::atomic<uint64_t> &mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = uint64_t{1} << (dev & 63);
+  return (mask.fetch_or(bit) & bit) == 0;
+}
+
+// Dense event delivery (per-neuron atomic counts, one neuron per thread) for
+// the compute-bound HH model up to 2 M local neurons: the counts stay
+// L2-resident and 4096-neuron tiles would leave SMs idle.
+bool dense_delivery(int model, int64_t n_local) {
+  return model == BP_MODEL_HH && n_local <= (int64_t{2} << 20);
+}
 
 // Workspace of the stateless scatter calls: [count int32 | pad to 256]
 // [active int32[n_rows]].
@@ -218,9 +237,11 @@ StreamPlan stream_plan(int64_t n_rows, int64_t n_cols, int out_kind, bool homo, 
   const char *c16_env = std::getenv("BP_CSR_C16");
   if (homo && c16_env != nullptr && std::atoi(c16_env) != 0) {
     // 16-bit counts while a CTA streams < 2^16 rows: CTA g of a tile takes the
-    // active ranks k with (k / 32) % groups == g, at most 32 ceil(n / (32 G))
+    // active ranks k with (k / W) % groups == g (W = bp::kStreamWarps), at
+    // most W ceil(n / (W G))
+    constexpr int64_t W = bp::kStreamWarps;
     StreamPlan p = stream_plan_acc(n_rows, n_cols, 2, homo, sms);
-    if (p.ok && 32 * ((n_rows + 32 * p.groups - 1) / (32 * p.groups)) < 65535) {
+    if (p.ok && W * ((n_rows + W * p.groups - 1) / (W * p.groups)) < 65535) {
       p.c16 = true;
       return p;
     }
@@ -231,13 +252,11 @@ StreamPlan stream_plan(int64_t n_rows, int64_t n_cols, int out_kind, bool homo, 
 
 template <int KIND, bool HOMO, bool C16 = false>
 void stream_attr() {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr))
     cudaFuncSetAttribute(bp::k_csr_stream<KIND, HOMO, C16>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kSmemOptin - bp::kStreamStaticSmem));
-    attr = true;
-  }
 }
 
 // Cooperative launch (every CTA resident: grid barriers allowed); false if
@@ -454,13 +473,11 @@ JitTilePlan jit_tile_plan(int64_t n_rows, int64_t width, int out_kind, int law, 
 
 template <int LAW, int KIND, bool VEC, bool GEO, bool C16 = false>
 bool jit_tiled_coop(bp::JitTiledArgs a, const JitTilePlan &p, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr))
     cudaFuncSetAttribute(bp::k_jit_tiled<LAW, KIND, VEC, GEO, C16>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kSmemOptin - kJitStaticSmem));
-    attr = true;
-  }
   void *args[] = {&a};
   if (cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(bp::k_jit_tiled<LAW, KIND, VEC, GEO, C16>),
                                   dim3(p.grid), dim3(bp::kJitTiledThreads), args, p.smem,
@@ -784,15 +801,14 @@ bp_status csrmv_impl(const void *plan, size_t plan_bytes, const int64_t *indptr,
     t.accumulate = (flags & BP_ACCUMULATE) ? 1 : 0;
     t.vec = aligned(indices, 16) && (data == nullptr || aligned(data, 16)) ? 1 : 0;
     const size_t smem = static_cast<size_t>(t.tile_cols) * acc;
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[out_kind]) {
+    static std::atomic<uint64_t> attr_set[2] = {{0}, {0}};
+    if (first_on_device(attr_set[out_kind])) {
       if (out_kind == BP_OUT_FIX64)
         BP_CUDA(cudaFuncSetAttribute(bp::k_csr_tiled<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      200 * 1000 + 1024));
       else
         BP_CUDA(cudaFuncSetAttribute(bp::k_csr_tiled<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      200 * 1000 + 1024));
-      attr_set[out_kind] = true;
     }
     const int grid = static_cast<int>(n_tiles * t.groups);
     if (out_kind == BP_OUT_FIX64) bp::k_csr_tiled<1><<<grid, bp::kTiledThreads, smem, st>>>(t);
@@ -1295,12 +1311,10 @@ bp_status launch_bin(bp_network *net, const int32_t *active, const int32_t *coun
   const size_t smem = (2 * static_cast<size_t>(bp::kBinStage) + 2 * net->n_tiles) * 4;
   if (!net->dense && net->n_tiles <= 8192 && smem <= 200 * 1024 &&
       !std::getenv("BP_BIN_PER_EVENT")) {
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::atomic<uint64_t> attr_set{0};
+    if (first_on_device(attr_set))
       BP_CUDA(cudaFuncSetAttribute(bp::k_bin_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    200 * 1024));
-      attr_set = true;
-    }
     BP_CUDA(launch_pdl(bp::k_bin_sorted, net->sms, bp::kBinThreads, smem, st, net->conn,
                        bin_target(net, par), active, count, net->counters + 1, net->n_tiles));
   } else {
@@ -1415,13 +1429,11 @@ namespace {
 template <int MODEL, int KIND>
 bp_status launch_small(const bp::SmallArgs &a, cudaStream_t st) {
   const size_t smem = bp::small_net_smem(MODEL, KIND);
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr))
     BP_CUDA(cudaFuncSetAttribute(bp::k_small_net<MODEL, KIND>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
-    attr = true;
-  }
   bp::k_small_net<MODEL, KIND><<<1, bp::kSmallThreads, smem, st>>>(a);
   return launched();
 }
@@ -1501,17 +1513,16 @@ bp_status bp_network_create(const bp_network_desc *desc, bp_stream stream,
   net->sms = sms;
   net->delay = desc->delay_steps > 0 ? desc->delay_steps : 1;
   net->slots = net->delay + 1;
+  net->n_local = desc->col_end - desc->col_begin;
+  net->local_words = (net->n_local + 31) / 32;
+  net->global_words = (desc->n + 31) / 32;
   // dense delivery for the compute-bound HH model up to 2 M local neurons
   // (counts stay L2-resident; 4096-neuron tiles would leave SMs idle);
   // BP_DENSE=0/1 overrides
   {
     const char *env = std::getenv("BP_DENSE");
-    net->dense = env ? std::atoi(env) != 0
-                     : (desc->model == BP_MODEL_HH && net->n_local <= (int64_t{2} << 20));
+    net->dense = env ? std::atoi(env) != 0 : dense_delivery(desc->model, net->n_local);
   }
-  net->n_local = desc->col_end - desc->col_begin;
-  net->local_words = (net->n_local + 31) / 32;
-  net->global_words = (desc->n + 31) / 32;
   if (desc->conn == BP_CONN_JIT) {
     s = resolve_jit(&desc->jit_exc, desc->n, &net->jr_e);
     if (s == BP_OK) s = resolve_jit(&desc->jit_inh, desc->n, &net->jr_i);

@@ -251,7 +251,7 @@ __device__ unsigned long long g_csr_t[1024][8];
 // n * q.  Deterministic for counts and fixed point.
 // C16: homogeneous partials are 16-bit counts (k_jit_tiled's packed tiles).
 // Only the first `used` CTAs of a tile received work (rows / items are
-// dealt 32 per CTA in order), so only their partials are summed -- a call
+// dealt kStreamWarps per CTA in order), so only their partials are summed -- a call
 // with few active rows does not read 148 empty partial tiles.
 template <int KIND, bool HOMO, int NT, bool C16 = false>
 __device__ __forceinline__ void tile_reduce(const void *partials, size_t first, int group,
@@ -496,10 +496,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs 
   __syncthreads();
   CSR_MARK(3);
   // partial tile -> [tile][group][tile_cols], 16-byte stores.  Rows are
-  // dealt 32 per CTA in order, so only the first `used` CTAs of a tile got
+  // dealt kStreamWarps per CTA in order, so only the first `used` CTAs of a tile got
   // any; with the fused reduction the others skip the flush (it reads only
   // the first `used` partials), k_csr_reduce reads them all.
-  const int64_t cta_rows = (n_active_rows + 31) / 32;
+  const int64_t cta_rows = (n_active_rows + kStreamWarps - 1) / kStreamWarps;
   const int used = cta_rows < a.groups ? static_cast<int>(cta_rows) : a.groups;
   if (a.out == nullptr || group < used) {
     char *dst = static_cast<char *>(a.partials) +

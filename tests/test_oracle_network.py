@@ -218,3 +218,100 @@ def test_delay_one_equals_default_and_history_continues(orc):
     rc = orc.run_network("lif", orc.lif_params(), s4, pe, pi, T, delay=4)
     assert np.array_equal(np.vstack([ra, rb]), rc)
     assert not np.array_equal(rc, r1)        # the delay changes the dynamics
+
+
+# ---------------------------------------------------------------- rule N1-f32
+# The fp32 conductance mode (the bench's default): a homogeneous projection
+# delivers `count` identical weights to a neuron in one step and the
+# increment is fl32(count * w), the exactly rounded sum (N1-f32);
+# then g <- fl32(g + inc), the neuron reads g, and g <- fl32(g * fl32(alpha))
+# (Expon: decay, then add -- reading R12).
+
+def _round_f32_exact(q):
+    """Round the exact rational q to the nearest float32 (ties to even),
+    independently of any fp32 arithmetic: bracket q between the two float32
+    neighbours of float64(q) and pick the nearer one with Fractions."""
+    from fractions import Fraction
+    x = np.float32(float(q))
+    cands = [np.nextafter(x, np.float32(-np.inf)), x, np.nextafter(x, np.float32(np.inf))]
+    best = min(cands, key=lambda c: (abs(Fraction(float(c)) - q),
+                                     int(np.array(c, np.float32).view(np.uint32)) & 1))
+    return np.float32(best)
+
+
+def test_f32_increment_is_the_exactly_rounded_sum(orc):
+    """A neuron receiving k events of w = fl32(0.6) in one step gets exactly
+    round_f32(k * w) (exact rational arithmetic), which for some k differs
+    from summing the k weights one by one in fp32 -- so the oracle's rule is
+    the exactly rounded sum, not a sequential fp32 accumulation."""
+    from fractions import Fraction
+    w = np.float32(0.6)
+    differs = 0
+    for k in (1, 2, 3, 7, 10, 13, 37, 80, 129, 1000):
+        n = k + 32
+        ip = np.zeros(n + 1, np.int64)
+        ip[1:k + 1] = np.arange(1, k + 1)            # rows 0..k-1 -> column 0
+        ip[k + 1:] = k
+        ix = np.zeros(k, np.int32)
+        pe = orc.Projection(0, n, csr=(ip, ix, None), w_homo=float(w))
+        pi = orc.Projection(n, 0, csr=(np.zeros(1, np.int64), np.zeros(0, np.int32), None),
+                            w_homo=6.7)
+        spikes = np.zeros(n, np.uint8)
+        spikes[:k] = 1
+        st = dict(v=np.full(n, -60.0, np.float32), g_e=np.zeros(n, np.float32),
+                  g_i=np.zeros(n, np.float32), ref=np.zeros(n, np.uint8), spikes=spikes)
+        # tau_E = inf: alpha = 1, so the stored g is the increment itself
+        orc.run_network("lif", orc.lif_params(tau_e=float("inf")), st, pe, pi, 1)
+        want = _round_f32_exact(k * Fraction(float(w)))
+        assert st["g_e"][0].view(np.uint32) == want.view(np.uint32), k
+        assert np.all(st["g_e"][1:] == 0)
+        seq = np.float32(0)
+        for _ in range(k):
+            seq = np.float32(seq + w)
+        differs += int(seq != want)
+    assert differs > 0          # the pin distinguishes the two summation rules
+
+
+def test_f32_g_within_bound_of_fp64_recursion(orc):
+    """Rule N1-f32 over 300 steps of the 4000-neuron network: the fp32 g
+    equals the exact fp64 recursion a_n = alpha a_{n-1} + inc_n (recomputed
+    from the oracle's raster with an independent dense matrix) within the
+    rounding bound of the fp32 rule.  With u = 2^-24, per step
+      |err_n| <= alpha |err_{n-1}| + |alpha32 - alpha| |a_{n-1}|
+                 + u (|alpha a_{n-1}| + |inc_n| + |a_n|)      (+ 1 % slack),
+    the three roundings being the decay product, fl32(count w) and the add.
+    A dropped or misplaced term (add after the decay, w of the other
+    projection, alpha of the other synapse) moves g by far more."""
+    n, T = 4000, 300
+    state, pe, pi = _coba(orc, n=n, fixed=False)
+    raster = orc.run_network("lif", orc.lif_params(), state, pe, pi, T)
+    assert raster.sum() > 0
+    u = 2.0 ** -24
+    out = []
+    for proj, w, tau, rows in ((pe, 0.6, 5.0, slice(0, pe.n_rows)),
+                               (pi, 6.7, 10.0, slice(pe.n_rows, n))):
+        d = np.zeros((proj.n_rows, n))
+        for r in range(proj.n_rows):
+            d[r, orc.jit_row(proj.jit, n, r)[0]] = float(np.float32(w))
+        a = math.exp(-0.1 / tau)
+        a32 = float(np.float32(a))
+        g = np.zeros(n)
+        b = np.zeros(n)
+        prev = np.zeros(n)
+        for step in range(T):
+            inc = prev[rows] @ d
+            g_new = a * g + inc                        # decay, then add (R12)
+            b = a * b + abs(a32 - a) * g + u * (a * g + inc + g_new)
+            g = g_new
+            prev = raster[step].astype(np.float64)
+        # stored state: pre-decayed once more
+        b = a * b + abs(a32 - a) * g + u * a * g
+        g = a * g
+        out.append((g, b * 1.01 + 1e-30))
+    (ge, be), (gi, bi) = out
+    err_e = np.abs(state["g_e"].astype(np.float64) - ge)
+    err_i = np.abs(state["g_i"].astype(np.float64) - gi)
+    assert np.all(err_e <= be), float(np.max(err_e - be))
+    assert np.all(err_i <= bi), float(np.max(err_i - bi))
+    # the bound is tight enough to matter: well below one event's weight
+    assert be.max() < 1e-3 * 0.6 and bi.max() < 1e-3 * 6.7
