@@ -70,55 +70,91 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clocks + throttle reasons sampled in-process through NVML (a
+    background thread, every 5 ms) from before the warm-up to after the
+    timed region, so even a millisecond-long timed region has samples on
+    both sides of it; mark() brackets the timed region (host clock) and the
+    summary reports the samples inside it and around it.  Falls back to a
+    `nvidia-smi -lms 100` subprocess when NVML is unavailable."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+               "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4,
+               "hw_power_brake_slowdown": 0x80}
 
-    def __init__(self, index: int):
-        self.index = index
-        self.proc = None
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.index, self.period = index, period_s
+        self.samples = []               # (t, sm_mhz, reasons bitmask)
+        self.max_mhz = None
+        self.t0 = self.t1 = None
+        self._stop = None
+        self._thread = None
+        self.source = None
+
+    def _handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            import torch
+            pr = torch.cuda.get_device_properties(self.index)
+            bus = "%08x:%02x:%02x.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
 
     def __enter__(self):
+        import threading
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.proc = None
+            nv, h = self._handle()
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self.source = "nvml"
+        except Exception:
+            nv = h = None
+            self.source = "none"
+        self._stop = threading.Event()
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                    rs = int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+                    self.samples.append((time.perf_counter(), sm, rs))
+                except Exception:
+                    return
+                self._stop.wait(self.period)
+        if h is not None:
+            self._thread = threading.Thread(target=run, daemon=True)
+            self._thread.start()
         return self
 
+    def mark_start(self):
+        self.t0 = time.perf_counter()
+
+    def mark_stop(self):
+        self.t1 = time.perf_counter()
+
     def __exit__(self, *exc):
-        self.lines = []
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                out, _ = self.proc.communicate(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
-                out, _ = self.proc.communicate()
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        if self._thread is not None:
+            self._stop.set()
+            self._thread.join(timeout=2)
         return False
 
     def summary(self):
-        sm, mx, reasons = [], 0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in getattr(self, "lines", []):
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except ValueError:
-                continue
-            for nm, val in zip(names, parts[3:7]):
-                if val.lower() == "active":
+        t0 = self.t0 if self.t0 is not None else -1e30
+        t1 = self.t1 if self.t1 is not None else 1e30
+        inside = [s for s in self.samples if t0 <= s[0] <= t1]
+        # a short timed region: the samples of the 50 ms on each side of it
+        near = inside or [s for s in self.samples if t0 - 0.05 <= s[0] <= t1 + 0.05]
+        reasons = set()
+        for _, _, rs in near:
+            for nm, bit in self.REASONS.items():
+                if rs & bit:
                     reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": mx or None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        sm = [x[1] for x in near]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(near),
+                "samples_in_timed_region": len(inside), "samples_total": len(self.samples),
+                "source": self.source,
+                "window": ("inside the timed region" if inside else
+                           "within 50 ms of the timed region (region shorter than the period)")}
 
 
 # ---------------------------------------------------------------------------
@@ -337,6 +373,42 @@ def state_bytes_per_neuron(model, fixed):
     return (8 + 1 if model == "lif" else 32) + g + 0.125
 
 
+# Measured lane instructions per regenerated gap of the paper's U[1, K]
+# sampler (ncu smsp__inst_executed x 32 / gaps of a k_jit_rows call:
+# profiles/r01/ncu_gap_samplers.json) -- the algorithmic core of the network
+# binning kernel (regeneration); staging, sort and the bucket writes are on
+# top of it, so the k_bin "alu" fraction below is that core's share of the
+# issue roof.
+BIN_CORE_OPS_PER_EVENT = 27.4
+
+
+def _ncu_traffic_r02(wl, g, kernel_prefix):
+    """DRAM bytes (read + write) per launch of `kernel_prefix` from the
+    committed ncu --set full capture of THIS workload in the settled regime
+    (profiles/r02/ncu_settled_<wl>_<g>.json, written by
+    tools/ncu_settled.py from an ncu run that skips the settle steps), or
+    None when no such capture exists."""
+    path = os.path.join(ROOT, "profiles", "r02", f"ncu_settled_{wl}_{g}.json")
+    try:
+        with open(path) as f:
+            rec = json.load(f)
+    except (OSError, ValueError):
+        return None, None
+    k = rec.get("kernels", {}).get(kernel_prefix)
+    if not k:
+        return None, None
+    return float(k["dram_bytes"]), os.path.relpath(path, ROOT)
+
+
+def settle_default(wl):
+    """Untimed pre-roll: the network starts from V0 ~ N(-55, 2),
+    every neuron crosses threshold within the first ~30 steps and the
+    synchronous burst and its echoes (up to ~15 M events per step at 12.5 M
+    neurons, 7x the settled load) fade over the first few hundred steps; the
+    timed region starts in the settled asynchronous regime."""
+    return 0 if network_size(wl, 1) <= 4096 else 2000
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -361,6 +433,7 @@ def run_ours(args):
             dist.init_process_group("gloo")
     n_total = network_size(wl, world)
     fixed = {"fix64": True, "fix32": "fix32", "f32": False}[args.g]
+    settle = settle_default(wl) if args.settle is None else args.settle
 
     net, csr = build_network(wl, world, rank, fixed, dev)
     n_local = net.part.col_end - net.part.col_begin
@@ -385,39 +458,48 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # warm-up (untimed)
-    steps(args.warmup)
-    barrier()
-    if world > 1 and args.dist_backend == "nccl" and not args.no_graph:
-        # one CUDA graph per step period (network.py capture): the per-step
-        # host calls cost about as much as the GPU step
-        try:
-            graph["g"], graph["period"] = net.capture()
-            graph["note"] = "CUDA graph of %d steps (exchange included), replayed" % graph["period"]
-            steps(2 * graph["period"])                       # warm replays
-        except Exception as exc:                           # eager fallback
-            graph["g"], graph["note"] = None, "eager (graph capture failed: %s)" % exc
-        barrier()
-    sp0, ev0, _ = net.counters()
-
-    # timed region: exactly K steps, CUDA events on the launching stream
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(device_index) as clk:
+        # settle + warm-up (untimed)
+        steps(settle)
+        steps(args.warmup)
         barrier()
+        if world > 1 and args.dist_backend == "nccl" and not args.no_graph:
+            # one CUDA graph per step period (network.py capture): the per-step
+            # host calls cost about as much as the GPU step
+            try:
+                graph["g"], graph["period"] = net.capture()
+                graph["note"] = ("CUDA graph of %d steps (exchange included), replayed"
+                                 % graph["period"])
+                steps(2 * graph["period"])                       # warm replays
+            except Exception as exc:                           # eager fallback
+                graph["g"], graph["note"] = None, "eager (graph capture failed: %s)" % exc
+            barrier()
+        sp0, ev0, _ = net.counters()
+        # timed region: exactly K steps, CUDA events on the launching stream
+        barrier()
+        clk.mark_start()
         start.record(stream)
         steps(args.steps)
         stop.record(stream)
         barrier()
+        clk.mark_stop()
     ms = start.elapsed_time(stop)
     sp1, ev1, sat1 = net.counters()
-    # per-kernel durations: an instrumented window of K more steps right after
-    # (events recorded between the two kernels of a step; they also disable
-    # the programmatic-launch overlap, so this window is slightly slower)
+    # per-kernel durations: an instrumented window of the SAME (settled)
+    # regime right after the timed region, its bytes from its own event
+    # counter (events are recorded between the two kernels of a step, which
+    # also disables their programmatic-launch overlap: slightly slower)
     prof = None
     if world == 1:
-        net.net.profile_begin(args.steps)
-        steps(args.steps)
-        prof = net.net.profile_end()
+        k_prof = max(args.steps, 200)
+        pw0 = net.counters()
+        net.net.profile_begin(k_prof)
+        steps(k_prof)
+        sc_ms, up_ms, nrec = net.net.profile_end()
+        pw1 = net.counters()
+        prof = dict(scatter_ms=sc_ms, update_ms=up_ms, steps=nrec,
+                    events=pw1[1] - pw0[1], spikes=pw1[0] - pw0[0])
     events_local = ev1 - ev0
     spikes_seen = sp1 - sp0
     if world > 1:
@@ -434,12 +516,13 @@ def run_ours(args):
     value = events_total / secs
     sim_ratio = args.steps * DT_MS * 1e-3 / secs
 
-    # end-to-end through the public API with host buffers: initial state H2D
-    # from pinned memory inside the timed region, every step's spike count
-    # D2H into pinned memory (the step's population-rate result).
+    # end-to-end through the public API with host buffers (same network, same
+    # settled regime): the current state is snapshotted to pinned host memory
+    # (untimed); the timed region copies it back H2D, runs the K steps and
+    # reads every step's spike count D2H into pinned memory.
     e2e = None
     if world == 1 and not args.no_e2e:
-        e2e = run_e2e(args, wl, fixed, dev)
+        e2e = run_e2e(args, net)
     elif world > 1 and not args.no_e2e:
         e2e = run_e2e_dist(args, wl, net, steps, barrier, dev)
 
@@ -452,32 +535,48 @@ def run_ours(args):
     peaks, peak_kind = _peaks()
     roofline = None
     if prof is not None:
-        sc_ms, up_ms, nrec = prof
-        upd_s = up_ms / 1e3 / max(nrec, 1)
-        bytes_per_launch = (state_bytes_per_neuron(spec["model"], fixed) * n_local +
-                            4 * events_total / args.steps)
+        nrec = max(prof["steps"], 1)
+        upd_s = prof["update_ms"] / 1e3 / nrec
+        bin_s = prof["scatter_ms"] / 1e3 / nrec
+        ev_step = prof["events"] / nrec
+        bytes_per_launch = state_bytes_per_neuron(spec["model"], fixed) * n_local + 4 * ev_step
         achieved = bytes_per_launch / upd_s / 1e9
         kname = ("k_small_net<%s,%s> (whole time loop in one CTA, state in shared memory)"
                  if small else "k_step<%s,%s> (fused: bucket counts -> Expon+COBA+neuron -> "
                  "spike bits + active list)") % (spec["model"].upper(), args.g)
-        traffic = (_ncu_traffic("void k_step<0, 0>")
-                   if (wl == "coba_lif_jit" and args.g == "f32" and world == 1) else None)
+        traffic, tsrc = _ncu_traffic_r02(wl, args.g, "k_step")
         roofline = {"kernel": kname, "bound": "hbm", "achieved": achieved,
                     "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                     "traffic": traffic,
-                    "traffic_source": ("profiles/r01/ncu_full_f32_default.json (ncu --set full, "
-                                       "--cache-control none): DRAM bytes per launch; below the "
-                                       "algorithmic bytes because the snake tile order re-uses "
-                                       "L2-resident state") if traffic else None,
+                    "traffic_source": (tsrc + " (ncu --set full of this workload after the "
+                                       "settle steps; dram bytes read + write per launch)")
+                    if traffic else None,
                     "peak_source": peak_kind,
                     "algorithmic_bytes_per_launch": bytes_per_launch,
+                    "bytes_model": "%.3f B/neuron x %d neurons + 4 B x %.0f event records" % (
+                        state_bytes_per_neuron(spec["model"], fixed), n_local, ev_step),
                     "avg_launch_us": upd_s * 1e6,
-                    "share_of_step": up_ms / (sc_ms + up_ms) if (sc_ms + up_ms) else None,
-                    "bin_kernel_avg_us": sc_ms / 1e3 / max(nrec, 1) * 1e6,
-                    "window": "instrumented K steps right after the timed region (same run)"}
+                    "share_of_step": upd_s / (upd_s + bin_s) if (upd_s + bin_s) else None,
+                    "window": "instrumented %d steps right after the timed region (same settled "
+                              "regime); bytes from that window's own event counter (%.0f events "
+                              "per step)" % (nrec, ev_step)}
         if small:
             roofline["note"] = ("latency-bound: the whole state (%d neurons) lives in one SM's "
                                 "shared memory; HBM fraction is not the limiter" % n_local)
+        elif spec["conn"] == "jit":
+            sm_mhz = clk.summary().get("sm_mhz") or 1965.0
+            peak_ops = 148 * 4 * 32 * sm_mhz * 1e6
+            ops = BIN_CORE_OPS_PER_EVENT * ev_step / bin_s
+            roofline["bin_kernel"] = {
+                "kernel": "k_bin_sorted (regenerate JIT rows of spikes_n, stage, sort by "
+                          "tile, write bucket runs)",
+                "bound": "alu", "achieved": ops / 1e12, "peak": peak_ops / 1e12,
+                "unit": "T lane-instructions/s", "frac": ops / peak_ops,
+                "avg_launch_us": bin_s * 1e6, "events_per_launch": ev_step,
+                "ops_per_event": BIN_CORE_OPS_PER_EVENT,
+                "ops_source": "measured lane instructions per U[1,K] gap of k_jit_rows "
+                              "(profiles/r01/ncu_gap_samplers.json): the regeneration core",
+                "peak_source": "derived: 148 SMs x 4 schedulers x 32 lanes x sampled SM clock"}
     cpu = cpu_baseline(wl, n_total, csr) if (world == 1 and not args.no_cpu) else None
     state_mb = state_bytes_per_neuron(spec["model"], fixed) * n_local / 1e6
     clocks = clk.summary()
@@ -492,6 +591,7 @@ def run_ours(args):
                    "fan_in": round(net_params(wl, n_total)[0] * n_total, 3),
                    "p": net_params(wl, n_total)[0],
                    "w_exc_inh": list(net_params(wl, n_total)[1:]), "dt_ms": DT_MS,
+                   "settle_steps": settle,
                    "g": {"fix64": "int64 fixed point 2^-32 (rule F1)",
                          "fix32": "int32 fixed point 2^-%d (rule F2), saturations: %d" % (
                              20 if spec["model"] == "lif" else 16, sat1),
@@ -520,28 +620,18 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def run_e2e(args, wl, fixed, dev):
-    """Same metric through the public API with host buffers."""
+def run_e2e(args, net):
+    """Same metric through the public API with host buffers, on the same
+    (settled) network: its state is copied to pinned host memory outside the
+    timed region; inside it, the state goes back H2D, the K steps run through
+    bp_network_step and every step's spike count comes back D2H (pinned)."""
     import torch
 
-    from paper_2311_05106_b200 import inputs
-    net, _ = build_network(wl, 1, 0, fixed, dev)
-    n = net.n
-    host = {k: torch.empty_like(v, device="cpu").pin_memory() for k, v in net.state.items()
+    host = {k: v.to("cpu").pin_memory() for k, v in net.state.items()
             if isinstance(v, torch.Tensor)}
-    if NETWORKS[wl]["model"] == "lif":
-        host["v"].copy_(torch.from_numpy(inputs.lif_v0(n)))
-        for k in ("g_e", "g_i", "ref"):
-            host[k].zero_()
-    else:
-        for k, a in zip(("v", "m", "h", "n"), inputs.hh_init(n)):
-            host[k].copy_(torch.from_numpy(a))
-        for k in ("g_e", "g_i"):
-            host[k].zero_()
     counts = torch.zeros(args.steps, dtype=torch.int32).pin_memory()
     h2d = sum(t.numel() * t.element_size() for t in host.values())
     stream = torch.cuda.current_stream()
-    net.run(args.warmup)
     torch.cuda.synchronize()
     sp0, ev0, _ = net.counters()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -556,7 +646,7 @@ def run_e2e(args, wl, fixed, dev):
     sp1, ev1, sat1 = net.counters()
     return {"value": (ev1 - ev0) / (ms / 1e3), "unit": UNIT,
             "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": 4,
-            "note": "initial state H2D (pinned) amortised over the K steps; per-step "
+            "note": "settled state H2D (pinned) amortised over the K steps; per-step "
                     "spike count D2H into pinned memory; ms=%.3f" % ms,
             "spikes_total": int(counts.sum().item())}
 
@@ -658,6 +748,7 @@ def run_emulated_rank(args):
     sp0, ev0, _ = net.counters()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(0) as clk:
+        clk.mark_start()
         a.record()
         if graph is not None:
             for _ in range(args.steps // period):
@@ -669,6 +760,7 @@ def run_emulated_rank(args):
                 step(k)
         b.record()
         torch.cuda.synchronize()
+        clk.mark_stop()
     ms = a.elapsed_time(b)
     sp1, ev1, _ = net.counters()
     line = {"metric": METRIC + " (emulated single rank)", "value": (ev1 - ev0) / (ms / 1e3),
@@ -791,6 +883,7 @@ def run_micro(args):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     with ClockSampler(0) as clk:
+        clk.mark_start()
         for k in range(args.steps):
             if flush:
                 scratch.fill_(k & 0xFF)           # evict the working set from L2
@@ -798,6 +891,7 @@ def run_micro(args):
             call(spikes[k % n_pat])
             evs[k][1].record(stream)
         torch.cuda.synchronize()
+        clk.mark_stop()
     ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = sum(ms)
     events = sum(ev_per_pat[k % n_pat] for k in range(args.steps))
@@ -860,6 +954,9 @@ def main():
                          "2^-F (rule F2) or fp32 (rule T3 parity)")
     ap.add_argument("--f32", action="store_true", help="alias of --g f32")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--settle", type=int, default=None,
+                    help="untimed pre-roll steps before the warm-up (default: 2000 for "
+                         "networks > 4096 neurons, the initial synchronous burst)")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer e2e leg")
     ap.add_argument("--emulate-world", type=int, default=0,
                     help="one GPU: time rank 0 of a G-GPU weak-scaling run (exchange "

@@ -40,7 +40,7 @@ LAW_HOMO, LAW_UNIFORM, LAW_NORMAL = 0, 1, 2
 LAWS = {"homo": LAW_HOMO, "uniform": LAW_UNIFORM, "normal": LAW_NORMAL}
 
 BUILD_CMD = ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math",
-             "-fPIC", "-shared", "-o", _LIB_PATH, _SRC, "-lm"]
+             "-fopenmp", "-fPIC", "-shared", "-o", _LIB_PATH, _SRC, "-lm"]
 
 
 def build() -> str:
@@ -115,6 +115,8 @@ def lib():
         _lib.or_geo_gap.restype = u32
         _lib.or_fix32_add.argtypes = [P, P, i64]
         _lib.or_fix32_add.restype = i64
+        _lib.or_set_threads.argtypes = [i32]
+        _lib.or_get_threads.restype = i32
     return _lib
 
 
@@ -235,6 +237,17 @@ def jit_materialize(spec: JitSpec, n_rows: int, n_cols: int):
 def _out_buf(n: int, out_kind: int):
     return np.zeros(n, {OUT_F64: np.float64, OUT_FIX: np.int64,
                         OUT_F32: np.float32, OUT_FIX32: np.int64}[out_kind])
+
+
+def set_threads(n: int):
+    """Host threads for the order-free loops (per-neuron updates, integer
+    event scatters); results are bit-identical to 1 thread (see the C
+    header).  Test-time speed only."""
+    lib().or_set_threads(int(n))
+
+
+def get_threads() -> int:
+    return int(lib().or_get_threads())
 
 
 def set_fix32_bits(bits: int):

@@ -31,6 +31,20 @@
 #define OR_OUT_F32 2   /* accumulate w in float, sequentially (network f32)  */
 #define OR_OUT_FIX32 3 /* accumulate llrint(w * 2^F) into int64 (rule F2)    */
 
+/* ------------------------------------------------------------------------
+ * Threads (test-time speed only; default 1).  The loops that may run on
+ * several host threads are the ones whose result does not depend on the
+ * order: per-neuron updates (or_lif_step, or_hh_step: independent
+ * neurons) and event scatters into INTEGER accumulators (fixed point, or
+ * fp64 sums of integer-valued weights, exact below 2^53), where every add
+ * is an atomic integer/exact add.  Every other call runs the plain
+ * sequential loop.  The parallel result is therefore bit-identical to the
+ * sequential one (pinned: test_oracle_network.py threaded == sequential).
+ * ---------------------------------------------------------------------- */
+static int g_threads = 1;
+void or_set_threads(int n) { g_threads = n < 1 ? 1 : n; }
+int or_get_threads(void) { return g_threads; }
+
 /* Rule F2 (32-bit fixed point): F fractional bits, set per run. */
 static int g_fix32_bits = 20;
 void or_set_fix32_bits(int bits) { g_fix32_bits = bits; }
@@ -308,6 +322,30 @@ int64_t or_jit_row(uint64_t seed, uint32_t K, uint32_t L, int64_t n_cols,
   return count;
 }
 
+/* The exact-accumulation kinds that may be summed by several threads. */
+static int order_free(int out_kind, const double *abs_out, int law, float w0,
+                      const float *data) {
+  if (g_threads <= 1 || abs_out) return 0;
+  if (out_kind == OR_OUT_FIX || out_kind == OR_OUT_FIX32) return 1;
+  return out_kind == OR_OUT_F64 && law == OR_LAW_HOMO && !data &&
+         w0 == rintf(w0) && fabsf(w0) < 1048576.0f;
+}
+
+/* Atomic variant of accumulate() for order_free() kinds. */
+static void accumulate_atomic(int out_kind, void *out, int64_t c, float w) {
+  if (out_kind == OR_OUT_F64) {
+    double *o = (double *)out + c;
+#pragma omp atomic
+    *o += (double)w;
+  } else {
+    int64_t q = out_kind == OR_OUT_FIX ? or_quantize(w)
+                                       : llrint(ldexp((double)w, g_fix32_bits));
+    int64_t *o = (int64_t *)out + c;
+#pragma omp atomic
+    *o += q;
+  }
+}
+
 static void accumulate(int out_kind, void *out, double *abs_out, int64_t c,
                        float w) {
   if (out_kind == OR_OUT_F64) {
@@ -339,6 +377,15 @@ void or_event_csrmv(const int64_t *indptr, const int32_t *indices,
                     const float *data, float w_homo, int64_t n_rows,
                     const uint8_t *events, int out_kind, void *out,
                     double *abs_out) {
+  if (order_free(out_kind, abs_out, OR_LAW_HOMO, w_homo, data)) {
+#pragma omp parallel for schedule(dynamic, 64) num_threads(g_threads)
+    for (int64_t i = 0; i < n_rows; ++i) {
+      if (!events[i]) continue;
+      for (int64_t j = indptr[i]; j < indptr[i + 1]; ++j)
+        accumulate_atomic(out_kind, out, (int64_t)indices[j], w_homo);
+    }
+    return;
+  }
   for (int64_t i = 0; i < n_rows; ++i) {
     if (!events[i]) continue;
     for (int64_t j = indptr[i]; j < indptr[i + 1]; ++j) {
@@ -365,6 +412,8 @@ void or_jit_event_mv(uint64_t seed, uint32_t K, uint32_t L, int law, float w0,
   if (col_end <= col_begin) return;
   int64_t seg_first = col_begin / (int64_t)L;
   int64_t seg_last = (col_end - 1) / (int64_t)L;
+  const int par = order_free(out_kind, abs_out, law, w0, NULL);
+#pragma omp parallel for schedule(dynamic, 64) num_threads(g_threads) if (par)
   for (int64_t r = 0; r < n_rows; ++r) {
     if (!events[r]) continue;
     for (int64_t s = seg_first; s <= seg_last; ++s) {
@@ -377,7 +426,8 @@ void or_jit_event_mv(uint64_t seed, uint32_t K, uint32_t L, int law, float w0,
       while (pos < seg_end) {
         if (pos >= col_begin && pos < col_end) {
           float w = edge_weight(seed, law, w0, w1, (uint32_t)r, (uint32_t)s, e);
-          accumulate(out_kind, out, abs_out, pos - col_begin, w);
+          if (par) accumulate_atomic(out_kind, out, pos - col_begin, w);
+          else accumulate(out_kind, out, abs_out, pos - col_begin, w);
         }
         pos += (int64_t)gap_of(seed, K, L, (uint32_t)r, (uint32_t)s, e);
         ++e;
@@ -549,6 +599,7 @@ static void g_decay(int g_kind, void *g, int64_t i, double alpha) {
 
 void or_lif_step(const or_lif_params *p, int64_t n, float *v, void *g_exc,
                  void *g_inh, int g_kind, uint8_t *ref, uint8_t *events) {
+  #pragma omp parallel for schedule(static) num_threads(g_threads) if (g_threads > 1)
   for (int64_t i = 0; i < n; ++i) {
     float V = v[i];
     float gE = g_read(g_kind, g_exc, i);
@@ -639,6 +690,7 @@ typedef struct {
 void or_hh_step(const or_hh_params *p, int64_t n, float *v, float *m, float *h,
                 float *nk, void *g_exc, void *g_inh, int g_kind,
                 uint8_t *events) {
+  #pragma omp parallel for schedule(static) num_threads(g_threads) if (g_threads > 1)
   for (int64_t i = 0; i < n; ++i) {
     float V = v[i], M = m[i], H = h[i], Nk = nk[i];
     float gE = g_read(g_kind, g_exc, i);

@@ -108,3 +108,40 @@ def fixed_fanin_csr_fast(n_rows: int, n_cols: int, p: float, seed: int):
     indptr = np.zeros(n_rows + 1, np.int64)
     np.cumsum(np.bincount(rows, minlength=n_rows), out=indptr[1:])
     return indptr, cols, None
+
+
+def bernoulli_csr(n_rows: int, n_cols: int, p: float, seed: int, weights: str = "homo",
+                  w0: float = 1.0, w1: float = 0.0, chunk: int = 2048):
+    """Large random CSR with every entry present independently with
+    probability p (per-row Binomial(n_cols, p) fan-out, no duplicates),
+    vectorised by rows of Geo(p) column gaps: row r's columns are the
+    partial sums of its gaps (minus one) below n_cols.  Sorted per row.
+    weights: 'homo' -> data None; 'uniform' -> U[w0, w1).
+    Returns (indptr int64, indices int32, data float32 | None)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    mean = n_cols * p
+    width = int(mean + 10.0 * np.sqrt(mean + 1.0) + 16)
+    idx_parts, counts = [], np.zeros(n_rows, np.int64)
+    for r0 in range(0, n_rows, chunk):
+        r1 = min(n_rows, r0 + chunk)
+        pos = np.cumsum(rng.geometric(p, size=(r1 - r0, width)), axis=1, dtype=np.int64) - 1
+        short = np.nonzero(pos[:, -1] < n_cols)[0]
+        while short.size:                       # extend the rare rows that need more gaps
+            ext = pos[short, -1:] + np.cumsum(rng.geometric(p, size=(short.size, width)),
+                                              axis=1, dtype=np.int64)
+            grown = np.full((pos.shape[0], pos.shape[1] + width), np.iinfo(np.int64).max,
+                            np.int64)
+            grown[:, :pos.shape[1]] = pos
+            grown[short, pos.shape[1]:] = ext
+            pos = grown
+            short = np.nonzero(pos[:, -1] < n_cols)[0]
+        keep = pos < n_cols
+        counts[r0:r1] = keep.sum(axis=1)
+        idx_parts.append(pos[keep].astype(np.int32))
+    indptr = np.zeros(n_rows + 1, np.int64)
+    np.cumsum(counts, out=indptr[1:])
+    indices = np.concatenate(idx_parts) if idx_parts else np.zeros(0, np.int32)
+    data = None
+    if weights == "uniform":
+        data = rng.uniform(w0, w1, indices.shape[0]).astype(np.float32)
+    return indptr, indices, data

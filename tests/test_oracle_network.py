@@ -315,3 +315,25 @@ def test_f32_g_within_bound_of_fp64_recursion(orc):
     assert np.all(err_i <= bi), float(np.max(err_i - bi))
     # the bound is tight enough to matter: well below one event's weight
     assert be.max() < 1e-3 * 0.6 and bi.max() < 1e-3 * 6.7
+
+
+@pytest.mark.parametrize("g_dtype", [np.int64, np.int32, np.float32])
+def test_threaded_oracle_equals_sequential(orc, g_dtype):
+    """The oracle's optional host threads (order-free loops only: per-neuron
+    updates and integer event scatters) give bit-identical networks."""
+    n, T = 4000, 150
+    runs = []
+    for threads in (1, 4):
+        orc.set_threads(threads)
+        try:
+            state, pe, pi = _coba(orc, n=n)
+            state["g_e"] = np.zeros(n, g_dtype)
+            state["g_i"] = np.zeros(n, g_dtype)
+            raster = orc.run_network("lif", orc.lif_params(), state, pe, pi, T)
+        finally:
+            orc.set_threads(1)
+        runs.append((raster, state))
+    (r1, s1), (r2, s2) = runs
+    assert r1.sum() > 0 and np.array_equal(r1, r2)
+    for k in ("v", "g_e", "g_i", "ref"):
+        assert np.array_equal(s1[k].view(np.uint8), s2[k].view(np.uint8)), k
