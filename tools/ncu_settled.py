@@ -72,7 +72,11 @@ def main():
                     v = float(r[i].replace(",", ""))
                 except ValueError:
                     continue
-                rec[short] = v * SCALE.get(units[i], 1.0)
+                if short == "duration":
+                    rec["duration_unit"] = units[i]
+                    rec[short] = v
+                else:
+                    rec[short] = v * SCALE.get(units[i], 1.0)
         if "dram_read" in rec and "dram_write" in rec:
             rec["dram_bytes"] = rec["dram_read"] + rec["dram_write"]
         out["kernels"][key] = rec
