@@ -309,19 +309,21 @@ def run_reference(args):
 NETWORKS = {
     "coba_lif_jit": dict(model="lif", conn="jit", per_gpu=N_PER_GPU, scaling="weak",
                          cfg="config 5: COBA-LIF JIT, 12.5M neurons per GPU, postsynaptic partition"),
-    "coba4m_jit": dict(model="lif", conn="jit", n=4_000_000, scaling="strong",
+    "coba4m_jit": dict(model="lif", conn="jit", n=4_000_000, scaling="strong", seg8=True,
                        cfg="config 3: COBA-LIF JIT 4M neurons, fan-in 80"),
     "coba4000_csr": dict(model="lif", conn="csr", n=4000, scaling="strong",
                          cfg="config 1: COBA-LIF 4000 neurons (3200E/800I), p=0.02, CSR"),
     "hh400k_csr": dict(model="hh", conn="csr", n=400_000, scaling="strong",
                        cfg="config 4: COBA-HH 400k neurons, fan-in 80, CSR"),
-    "coba100m_jit": dict(model="lif", conn="jit", n=100_000_000, scaling="strong",
+    "coba100m_jit": dict(model="lif", conn="jit", n=100_000_000, scaling="strong", seg8=True,
                          cfg="config 5 total size on ONE GPU: COBA-LIF JIT 1e8 neurons, fan-in 80"),
     # Fig S3B / S3C regimes at the config-3 size
     "coba4m_k1000": dict(model="lif", conn="jit", n=4_000_000, scaling="strong", fan_in=1000,
+                         seg8=True,
                          cfg="Fig S3B: COBA-LIF JIT 4M neurons, 1000 synapses per neuron, "
                              "weights x 80/1000"),
     "coba4m_p001": dict(model="lif", conn="jit", n=4_000_000, scaling="strong", p=0.001,
+                        seg8=True,
                         cfg="Fig S3C: COBA-LIF JIT 4M neurons, fixed p = 0.001 (fan-in 4000), "
                             "weights x 80/4000"),
 }
@@ -347,7 +349,18 @@ def network_size(wl, world):
     return spec["per_gpu"] * world if "per_gpu" in spec else spec["n"]
 
 
-def build_network(wl, world, rank, fixed, dev):
+def seg_len_of(wl, n):
+    """JIT segment length (rule J4).  Weak scaling (config 5): the 12.5 M
+    neurons of one GPU, so each rank regenerates only its own segment.
+    Strong-scaling JIT configs: n / 8 at EVERY GPU count (the 8-GPU
+    partition), so G = 1, 2, 4, 8 simulate the same connectivity."""
+    spec = NETWORKS[wl]
+    if spec.get("seg8"):
+        return -(-n // 8 // 32) * 32
+    return spec.get("per_gpu", n) if "per_gpu" in spec else n
+
+
+def build_network(wl, world, rank, fixed, dev, exchange="caller"):
     """The workload's network; CSR connectivity = materialise(JIT spec) with
     the library's own generator ('CSR = materialise(jit spec)')."""
     import paper_2311_05106_b200 as bp
@@ -364,8 +377,10 @@ def build_network(wl, world, rank, fixed, dev):
                                              with_data=False, device=dev)
         csr = ((ipe, ixe), (ipi, ixi))
     p, w_e, w_i = net_params(wl, n)
+    seg = seg_len_of(wl, n) if spec["conn"] == "jit" else None
     return CobaNetwork(n, model=spec["model"], conn=spec["conn"], fixed=fixed, rank=rank,
-                       world=world, device=dev, csr=csr, p=p, w_exc=w_e, w_inh=w_i), csr
+                       world=world, device=dev, csr=csr, p=p, w_exc=w_e, w_inh=w_i,
+                       seg_len=seg, exchange=exchange), csr
 
 
 def state_bytes_per_neuron(model, fixed):
@@ -435,21 +450,20 @@ def run_ours(args):
     fixed = {"fix64": True, "fix32": "fix32", "f32": False}[args.g]
     settle = settle_default(wl) if args.settle is None else args.settle
 
-    net, csr = build_network(wl, world, rank, fixed, dev)
+    # N > 1: the library's own NCCL exchange (bp_network_step runs the whole
+    # step, the bit-packed all-gather included); --dist-backend gloo: the
+    # caller-driven exchange through torch.distributed (functional check of
+    # several ranks sharing one GPU)
+    exchange = "nccl" if (world > 1 and args.dist_backend == "nccl") else "caller"
+    net, csr = build_network(wl, world, rank, fixed, dev, exchange=exchange)
     n_local = net.part.col_end - net.part.col_begin
     small = world == 1 and n_total <= 4096
     stream = torch.cuda.current_stream()
 
-    graph = {"g": None, "period": 1, "note": None}
-
     def steps(k):
-        if world == 1:
+        if world == 1 or exchange == "nccl":
             net.run(k)
             return
-        if graph["g"] is not None:
-            for _ in range(k // graph["period"]):
-                graph["g"].replay()
-            k %= graph["period"]
         for _ in range(k):
             net.step_distributed()
 
@@ -464,17 +478,6 @@ def run_ours(args):
         steps(settle)
         steps(args.warmup)
         barrier()
-        if world > 1 and args.dist_backend == "nccl" and not args.no_graph:
-            # one CUDA graph per step period (network.py capture): the per-step
-            # host calls cost about as much as the GPU step
-            try:
-                graph["g"], graph["period"] = net.capture()
-                graph["note"] = ("CUDA graph of %d steps (exchange included), replayed"
-                                 % graph["period"])
-                steps(2 * graph["period"])                       # warm replays
-            except Exception as exc:                           # eager fallback
-                graph["g"], graph["note"] = None, "eager (graph capture failed: %s)" % exc
-            barrier()
         sp0, ev0, _ = net.counters()
         # timed region: exactly K steps, CUDA events on the launching stream
         barrier()
@@ -488,10 +491,10 @@ def run_ours(args):
     sp1, ev1, sat1 = net.counters()
     # per-kernel durations: an instrumented window of the SAME (settled)
     # regime right after the timed region, its bytes from its own event
-    # counter (events are recorded between the two kernels of a step, which
+    # counter (events are recorded between the kernels of a step, which
     # also disables their programmatic-launch overlap: slightly slower)
     prof = None
-    if world == 1:
+    if world == 1 or exchange == "nccl":
         k_prof = max(args.steps, 200)
         pw0 = net.counters()
         net.net.profile_begin(k_prof)
@@ -521,11 +524,19 @@ def run_ours(args):
     # (untimed); the timed region copies it back H2D, runs the K steps and
     # reads every step's spike count D2H into pinned memory.
     e2e = None
-    if world == 1 and not args.no_e2e:
-        e2e = run_e2e(args, net)
-    elif world > 1 and not args.no_e2e:
-        e2e = run_e2e_dist(args, wl, net, steps, barrier, dev)
+    if not args.no_e2e and (world == 1 or exchange == "nccl"):
+        e2e = run_e2e(args, net, world, dev)
 
+    # per-rank kernel times (N > 1: every rank's window, gathered to rank 0)
+    mine = None
+    if prof is not None:
+        nr = max(prof["steps"], 1)
+        mine = {"rank": rank, "k_step_us": prof["update_ms"] * 1e3 / nr,
+                "k_bin_us": prof["scatter_ms"] * 1e3 / nr, "events_per_step": prof["events"] / nr}
+    per_rank = [mine]
+    if world > 1:
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, mine)
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -560,6 +571,13 @@ def run_ours(args):
                     "window": "instrumented %d steps right after the timed region (same settled "
                               "regime); bytes from that window's own event counter (%.0f events "
                               "per step)" % (nrec, ev_step)}
+        if world > 1:
+            sb = state_bytes_per_neuron(spec["model"], fixed) * n_local
+            roofline["per_rank"] = [
+                dict(r, frac=(sb + 4 * r["events_per_step"]) / (r["k_step_us"] * 1e-6) / 1e9 /
+                     peaks["hbm_gbs"]) for r in per_rank if r]
+            roofline["window"] += ("; k_step = the neuron-update kernel, k_bin = local binning "
+                                   "(+ the remote scatter of the previous step for delay >= 2)")
         if small:
             roofline["note"] = ("latency-bound: the whole state (%d neurons) lives in one SM's "
                                 "shared memory; HBM fraction is not the limiter" % n_local)
@@ -597,8 +615,16 @@ def run_ours(args):
                              20 if spec["model"] == "lif" else 16, sat1),
                          "f32": "fp32, increments fl32(count*w) (rule N1-f32), bit-exact vs oracle"}[args.g],
                    "parallelism": f"postsynaptic partition x{world}",
-                   "host_loop": ("library time loop (bp_network_step)" if world == 1
-                                 else graph["note"] or "eager per-step calls"),
+                   "host_loop": ("library time loop (bp_network_step)" if world == 1 else
+                                 "library time loop with its own NCCL spike all-gather "
+                                 "(bp_network_step, BP_EXCHANGE_NCCL)" if exchange == "nccl"
+                                 else "torch.distributed exchange, eager per-step calls"),
+                   "seg_len": seg_len_of(wl, n_total) if spec["conn"] == "jit" else None,
+                   "exchange": {"nccl": "ncclAllGather of the bit-packed local words "
+                                        "(%d B per rank per step), in place, on the "
+                                        "library's comm stream" % (net.part.local_words * 4),
+                                "caller": "none (one GPU)" if world == 1 else
+                                          "torch.distributed all_gather_into_tensor"}[exchange],
                    "l2": (f"state {state_mb:.0f} MB/GPU > 2 x 126 MB L2: no flush needed"
                           if state_mb > 252 else
                           f"state {state_mb:.1f} MB is L2/SM-resident by design (the workload is that small)"),
@@ -606,8 +632,9 @@ def run_ours(args):
         "sim_s_per_wall_s": sim_ratio,
         "events_per_step": events_total / args.steps,
         # libbp kernels in the timed region: k_step + k_bin per step (world 1),
-        # one k_small_net launch for small networks, and k_compact + k_bin +
-        # k_step per step for world > 1 (NCCL kernels not counted)
+        # one k_small_net launch for small networks, and k_step + k_bin +
+        # k_compact + k_bin (remote rows) per step for world > 1 (the memset
+        # and NCCL's all-gather kernel not counted)
         "gpu_launches": (1 if small else (2 if world == 1 else 4) * args.steps),
         "clocks": clocks,
         "roofline": roofline,
@@ -620,12 +647,15 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def run_e2e(args, net):
+def run_e2e(args, net, world, dev):
     """Same metric through the public API with host buffers, on the same
     (settled) network: its state is copied to pinned host memory outside the
     timed region; inside it, the state goes back H2D, the K steps run through
-    bp_network_step and every step's spike count comes back D2H (pinned)."""
+    bp_network_step (the NCCL exchange included for N > 1) and every step's
+    spike count comes back D2H (pinned).  N > 1: max time over ranks, events
+    summed."""
     import torch
+    import torch.distributed as dist
 
     host = {k: v.to("cpu").pin_memory() for k, v in net.state.items()
             if isinstance(v, torch.Tensor)}
@@ -635,6 +665,8 @@ def run_e2e(args, net):
     torch.cuda.synchronize()
     sp0, ev0, _ = net.counters()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
     torch.cuda.synchronize()
     start.record(stream)
     for k, t in host.items():
@@ -644,58 +676,19 @@ def run_e2e(args, net):
     stop.synchronize()
     ms = start.elapsed_time(stop)
     sp1, ev1, sat1 = net.counters()
-    return {"value": (ev1 - ev0) / (ms / 1e3), "unit": UNIT,
+    ev = float(ev1 - ev0)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e = torch.tensor([ev], dtype=torch.float64, device=dev)
+        dist.all_reduce(e, op=dist.ReduceOp.SUM)
+        ms, ev = float(t.item()), float(e.item())
+    return {"value": ev / (ms / 1e3), "unit": UNIT,
             "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": 4,
             "note": "settled state H2D (pinned) amortised over the K steps; per-step "
-                    "spike count D2H into pinned memory; ms=%.3f" % ms,
+                    "spike count D2H into pinned memory; %sms=%.3f" % (
+                        "per rank, max over ranks; " if world > 1 else "", ms),
             "spikes_total": int(counts.sum().item())}
-
-
-def run_e2e_dist(args, wl, net, steps, barrier, dev):
-    """N > 1: the same metric with this rank's initial state copied from
-    pinned host memory inside the timed region (then K steps through the
-    same loop, exchange included) and the device counters read back to the
-    host at the end; max time over ranks, events summed."""
-    import torch
-    import torch.distributed as dist
-
-    from paper_2311_05106_b200 import inputs
-    lo, hi = net.part.col_begin, net.part.col_end
-    host = {k: torch.empty_like(v, device="cpu").pin_memory() for k, v in net.state.items()
-            if isinstance(v, torch.Tensor)}
-    if NETWORKS[wl]["model"] == "lif":
-        host["v"].copy_(torch.from_numpy(inputs.lif_v0(net.n)[lo:hi]))
-        for k in ("g_e", "g_i", "ref"):
-            host[k].zero_()
-    else:
-        for k, a in zip(("v", "m", "h", "n"), inputs.hh_init(net.n)):
-            host[k].copy_(torch.from_numpy(a[lo:hi]))
-        for k in ("g_e", "g_i"):
-            host[k].zero_()
-    h2d = sum(t.numel() * t.element_size() for t in host.values())
-    stream = torch.cuda.current_stream()
-    sp0, ev0, _ = net.counters()
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    start.record(stream)
-    for k, t in host.items():
-        net.state[k].copy_(t, non_blocking=True)
-    steps(args.steps)
-    sp1, ev1, _ = net.counters()          # D2H of the counters (synchronises)
-    stop.record(stream)
-    stop.synchronize()
-    t = torch.tensor([start.elapsed_time(stop), float(ev1 - ev0)], dtype=torch.float64,
-                     device=dev if args.dist_backend == "nccl" else "cpu")
-    mx = t[:1].clone()
-    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-    ev = t[1:].clone()
-    dist.all_reduce(ev, op=dist.ReduceOp.SUM)
-    ms = float(mx.item())
-    return {"value": float(ev.item()) / (ms / 1e3), "unit": UNIT,
-            "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": 24 / args.steps,
-            "note": "per rank: initial local state H2D (pinned) amortised over the K steps; "
-                    "device counters (spikes, events) D2H once at the end; max over ranks; "
-                    "ms=%.3f" % ms}
 
 
 def run_emulated_rank(args):
@@ -943,6 +936,123 @@ def run_micro(args):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# Fig 3A/B: memory and speed of the JIT operator
+# y = J v against the same matrix materialised, as n grows at fixed p
+# ---------------------------------------------------------------------------
+def _time_calls(fn, reps, flush=None):
+    """Median device time of `reps` calls (CUDA events on the current stream;
+    the L2 scratch write between calls when `flush` is given)."""
+    import torch
+    st = torch.cuda.current_stream()
+    fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        if flush is not None:
+            flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        fn()
+        b.record(st)
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts) * 1e3
+
+
+def run_fig3ab(args):
+    """For n in a sweep (square n x n, connection probability p, normal
+    weights N(0, 1/(n p)), the Table S1 scale), one JSON line per n:
+      * device bytes the connectivity occupies: JIT = 0 (four scalars,
+        P:192), CSR = indptr + indices + weights, dense = 4 n^2;
+      * time per call of the non-event product y = J v (v dense, fp32) --
+        bp_jitconn_mv_normal (ours) vs the same matrix materialised by the
+        library's own generator and multiplied by cuSPARSE SpMV
+        (torch.sparse_csr) and, while 4 n^2 fits the budget, dense cuBLAS
+        (torch.mv) -- the comparison systems of Fig 3A/B as library calls;
+      * time per call of the event-driven product at 10 % spike density:
+        bp_jitconn_event_mv_normal vs bp_event_csrmv on the materialised
+        matrix (both ours).
+    Matrices over --fig3-budget-gb of device memory are skipped (reported)."""
+    import numpy as np
+    import torch
+
+    import __graft_entry__ as ge
+    ge.build_lib()
+    import paper_2311_05106_b200 as bp
+    from paper_2311_05106_b200 import inputs
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    p = args.p
+    budget = args.fig3_budget_gb * 1e9
+    flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
+    sizes = [int(x) for x in args.fig3_sizes.split(",")]
+    for n in sizes:
+        seed = 0xF163
+        spec = bp.jitconn_spec(seed, p)
+        mu, sigma = 0.0, 1.0 / math.sqrt(n * p)
+        rng = np.random.default_rng(5)
+        v = torch.from_numpy(rng.standard_normal(n).astype(np.float32)).to(dev)
+        ev = inputs.spike_pattern(n, 0.1, 9000 + n % 1000)
+        spikes = torch.from_numpy(inputs.pack_bits(ev).view(np.int32)).to(dev)
+        out = torch.zeros(n, dtype=torch.float32, device=dev)
+        ws = torch.empty(bp.lib().bp_jitconn_workspace_bytes(n, 0, n, 0), dtype=torch.uint8,
+                         device=dev)
+        reps = max(3, min(args.steps, int(2e10 / max(n * n * p, 1.0))))
+        rec = {"workload": "fig3ab", "n": n, "p": p, "K": bp.conn_len(p),
+               "weights": "normal(0, 1/(n p))", "expected_nnz": n * n * 2.0 / (bp.conn_len(p) + 1),
+               "reps": reps}
+        rec["jit_bytes"] = 0
+        rec["jit_mv_us"] = _time_calls(lambda: bp.jitconn_mv(bp.LAW_NORMAL, spec, mu, sigma, v, n,
+                                                             n, out, ws=ws), reps, flush)
+        rec["jit_event_mv_us"] = _time_calls(lambda: bp.jitconn_event_mv_normal(
+            spec, mu, sigma, spikes, n, n, out, ws=ws), reps, flush)
+        csr_bytes = 8 * (n + 1) + 8 * rec["expected_nnz"]
+        rec["csr_bytes"] = csr_bytes
+        if csr_bytes <= budget:
+            ip, ix, dat = bp.jitconn_materialize(spec, n, n, law=bp.LAW_NORMAL, w0=mu, w1=sigma,
+                                                 device=dev)
+            nnz = int(ix.numel())
+            rec["nnz"] = nnz
+            rec["csr_bytes"] = ip.numel() * 8 + nnz * 8
+            # the materialised matrix IS the JIT matrix: one call of each agrees
+            bp.jitconn_mv(bp.LAW_NORMAL, spec, mu, sigma, v, n, n, out, ws=ws)
+            y_jit = out.clone()
+            A = torch.sparse_csr_tensor(ip, ix, dat, size=(n, n))
+            # Listing S2 scatters rows into columns: y = J^T v with J rows = pre
+            At = A.t().to_sparse_csr()
+            y_sp = torch.mv(At, v)
+            err = (y_sp - y_jit).abs().max().item()
+            scale = torch.mv(At.abs() if hasattr(At, "abs") else At, v.abs()).max().item()
+            rec["jit_vs_cusparse_max_abs_diff"] = err
+            rec["jit_vs_cusparse_rel_to_sum_abs"] = err / max(scale, 1e-30)
+            rec["cusparse_spmv_us"] = _time_calls(lambda: torch.mv(At, v), reps, flush)
+            del A
+            cws = torch.empty(bp.lib().bp_csrmv_workspace_bytes(n, n, 0), dtype=torch.uint8,
+                              device=dev)
+            plan = bp.csrmv_plan(ip, ix, n, n, torch.float32, homo=False)
+            rec["csr_event_mv_us"] = _time_calls(lambda: bp.event_csrmv(
+                ip, ix, dat, 0.0, n, n, spikes, out, ws=cws, plan=plan), reps, flush)
+            del At, ip, ix, dat, plan, cws
+        else:
+            rec["csr_skipped"] = "CSR would need %.1f GB > budget" % (csr_bytes / 1e9)
+        dense_bytes = 4.0 * n * n
+        rec["dense_bytes"] = dense_bytes
+        if dense_bytes <= budget and n <= 150_000:
+            D = torch.zeros((n, n), dtype=torch.float32, device=dev)
+            ipd, ixd, datd = bp.jitconn_materialize(spec, n, n, law=bp.LAW_NORMAL, w0=mu,
+                                                    w1=sigma, device=dev)
+            rows = torch.repeat_interleave(torch.arange(n, device=dev), ipd[1:] - ipd[:-1])
+            D[ixd.long(), rows] = datd            # D = J^T (column r = row r of J)
+            del ipd, ixd, datd, rows
+            rec["dense_mv_us"] = _time_calls(lambda: torch.mv(D, v), reps, flush)
+            del D
+        else:
+            rec["dense_skipped"] = "dense would need %.1f GB" % (dense_bytes / 1e9)
+        torch.cuda.empty_cache()
+        print(json.dumps(rec), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -964,9 +1074,13 @@ def main():
     ap.add_argument("--emulate-rank", type=int, default=0,
                     help="--emulate-world: which rank's partition to time")
     ap.add_argument("--no-graph", action="store_true",
-                    help="N > 1: eager per-step calls instead of the captured CUDA graph")
+                    help="--emulate-world: eager per-step calls instead of a CUDA graph")
+    ap.add_argument("--fig3-sizes", default="10000,30000,100000,300000,1000000,3000000",
+                    help="--workload fig3ab: matrix sizes n")
+    ap.add_argument("--fig3-budget-gb", type=float, default=60.0,
+                    help="--workload fig3ab: largest materialised matrix")
     ap.add_argument("--workload",
-                    choices=list(NETWORKS) + ["csrmv", "jitmv", "jitmv_vec", "jitrows"],
+                    choices=list(NETWORKS) + ["csrmv", "jitmv", "jitmv_vec", "jitrows", "fig3ab"],
                     default="coba_lif_jit")
     ap.add_argument("--p", type=float, default=0.05, help="microbench connection probability")
     ap.add_argument("--density", type=float, default=0.1, help="microbench spike density")
@@ -985,10 +1099,24 @@ def main():
         args.warmup = 3
     if args.f32:
         args.g = "f32"
+    if args.gpus > 1 and "RANK" not in os.environ and args.impl == "ours" \
+            and args.emulate_world <= 1:
+        # `python bench.py --gpus N`: launch the N ranks ourselves (one per
+        # GPU), exactly as the driver's torchrun command does
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        os.execv(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                                  f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+                                  f"--master-port={port}", os.path.abspath(__file__),
+                                  *sys.argv[1:]])
     if args.impl == "reference":
         run_reference(args)
     elif args.emulate_world > 1:
         run_emulated_rank(args)
+    elif args.workload == "fig3ab":
+        run_fig3ab(args)
     elif args.workload in ("csrmv", "jitmv", "jitmv_vec", "jitrows"):
         run_micro(args)
     else:

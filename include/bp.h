@@ -15,9 +15,11 @@
  *                               or COBA-HH (rule H1, EXTERNAL)   [a5, a6]
  *   bp_network_*             -- Listing S3's update() loop: 1-step
  *                               delayed spikes -> scatter -> neuron update [a7];
- *                               bp_network_scatter / _update(_overlap): the two
- *                               halves of a partitioned step around the spike
- *                               all-gather                     [a8]
+ *                               several projections merged per receptor
+ *                               (AlignPost); multi-GPU: the library's
+ *                               own NCCL spike all-gather or the
+ *                               caller-driven halves bp_network_scatter /
+ *                               _update(_overlap)                          [a8]
  *   bp_jitconn_mv_*          -- mv_prob_* with a float vector (NEXT 1, MV1)
  *   bp_csrmv_gather,
  *   bp_event_csrmv_grad      -- csrmv(transpose=False) and the reverse mode
@@ -69,7 +71,8 @@ typedef enum {
   BP_ERR_SHAPE = 2,       /* sizes <= 0 or >= 2^31, partition not aligned      */
   BP_ERR_UNSUPPORTED = 3, /* not an sm_100 device, K too large for 32-bit pos  */
   BP_ERR_WORKSPACE = 4,   /* workspace NULL, misaligned or too small           */
-  BP_ERR_CUDA = 5         /* a CUDA runtime error (launch or sticky)           */
+  BP_ERR_CUDA = 5,        /* a CUDA runtime error (launch or sticky)           */
+  BP_ERR_NCCL = 6         /* NCCL missing or an NCCL call failed               */
 } bp_status;
 
 /* Output / state accumulator kinds.  BP_OUT_FIX32 is a STATE kind only
@@ -83,7 +86,7 @@ typedef enum { BP_LAW_HOMO = 0, BP_LAW_UNIFORM = 1, BP_LAW_NORMAL = 2 } bp_law;
 typedef enum { BP_MODEL_LIF = 0, BP_MODEL_HH = 1 } bp_model;
 typedef enum { BP_CONN_JIT = 0, BP_CONN_CSR = 1 } bp_conn;
 
-int bp_abi_version(void); /* 1 */
+int bp_abi_version(void); /* 2 */
 const char *bp_status_string(int status);
 const char *bp_last_error(void);
 
@@ -316,58 +319,115 @@ bp_status bp_neuron_step(const bp_neuron_params *params,
                          bp_stream stream);
 
 /* ---------------------------------------------------------------------
- * Network: Listing S3.  Neurons [0, n_exc) are excitatory
- * (projection E, rows 0..n_exc-1), [n_exc, n) inhibitory (projection I,
- * rows 0..n-n_exc-1); both project onto all n neurons.  This
- * process owns postsynaptic neurons [col_begin, col_end);
- * col_begin must be a multiple of 32 and of both seg_lens.
- * Per step (rule S1): scatter(spikes_{n-1}) into g, neuron update ->
- * spikes_n.  With several processes the caller all-gathers the bit-packed
- * spike vector between bp_network_update and the next bp_network_scatter.
+ * Network: Listing S3, generalised to up to BP_MAX_PROJ
+ * homogeneous projections (AlignPost): projection k
+ * takes the spikes of presynaptic neurons [pre_begin, pre_end) (its rows
+ * 0 .. pre_end - pre_begin - 1) and adds `weight` per event into the
+ * conductance of its receptor at every target among all n neurons
+ * (columns).  Projections of one receptor MERGE into that
+ * receptor's single conductance per neuron (one g_exc and one g_inh array
+ * however many projections: "all synaptic interactions with
+ * identical time constants can be converged into a single trace"); their
+ * increments of one step are summed exactly (fixed point: integer sum; fp32:
+ * the exactly rounded sum, rule N1-f32 -- which requires every fp32 weight
+ * of a receptor with several distinct weights to be a multiple of 2^-32,
+ * else BP_ERR_UNSUPPORTED).  At most 4 distinct (receptor, weight) pairs.
+ * Listing S3 itself is two projections: E rows [0, n_exc) -> g_exc with
+ * w_E, I rows [n_exc, n) -> g_inh with w_I.
+ *
+ * This process owns postsynaptic neurons [col_begin, col_end) (SURVEY
+ * 8(e)); col_begin must be a multiple of 32 and of every JIT seg_len.
+ * Per step (rule S1): scatter(spikes_{n-D}) into g, neuron update ->
+ * spikes_n.
+ *
+ * Several processes (one per GPU), two ways:
+ *  - exchange = BP_EXCHANGE_NCCL: the library owns an NCCL communicator
+ *    (created in bp_network_create from nccl_id / rank / world, a
+ *    collective call on every rank) and bp_network_step runs the whole
+ *    loop, the bit-packed spike all-gather included ("gather only
+ *    non-zero spikes", realised as bit packing).  The partition must be
+ *    rank-ordered with equal lengths: col_begin = rank * part_len, col_end =
+ *    min(n, (rank + 1) * part_len), part_len a multiple of 32; `spikes` holds
+ *    world * part_len / 32 words.  The all-gather of step n overlaps the
+ *    local binning of step n (delay 1) or the whole update of step n + 1
+ *    (delay >= 2; SURVEY 8(e) options (i) and (iii)).  world may be 1.
+ *  - exchange = BP_EXCHANGE_CALLER: the caller all-gathers the vector itself
+ *    between bp_network_update and the next bp_network_scatter.
+ *
+ * Memory: the network's event buckets (~5 % of the fan-in x local neurons
+ * x 4 B per delay slot, plus 4 B x classes x local neurons of overflow
+ * counters) and its projection table are DEVICE memory that
+ * bp_network_create allocates and bp_network_destroy frees
+ * (bp_network_device_bytes reports the amount); all state arrays, the spike
+ * vector and the workspace belong to the caller.
  * --------------------------------------------------------------------- */
+#define BP_MAX_PROJ 8
+typedef enum { BP_RECEPTOR_EXC = 0, BP_RECEPTOR_INH = 1 } bp_receptor;
+typedef enum { BP_EXCHANGE_CALLER = 0, BP_EXCHANGE_NCCL = 1 } bp_exchange;
+
+typedef struct {
+  int32_t conn;               /* bp_conn                                        */
+  int32_t receptor;           /* bp_receptor: the conductance it adds into      */
+  int64_t pre_begin, pre_end; /* presynaptic neurons (global ids)               */
+  float weight;               /* homogeneous weight per event                   */
+  int32_t reserved;           /* must be 0                                      */
+  bp_jitconn jit;             /* conn == BP_CONN_JIT: columns = all n neurons   */
+  /* conn == BP_CONN_CSR: column-sliced CSR of this process's columns, indices
+   * local to [col_begin, col_end), pre_end - pre_begin rows               */
+  const int64_t *indptr;
+  const int32_t *indices;
+} bp_projection;
+
 typedef struct {
   int32_t model;  /* bp_model */
-  int32_t conn;   /* bp_conn  */
   int32_t g_kind; /* bp_out_kind of state.g_exc / g_inh */
   int32_t delay_steps; /* synaptic delay D in steps (0 => 1, the paper's one-step
                           VarDelay); spikes of step n are delivered at
                           step n + D (reading D1); <= 16.
                           D > 1 keeps D + 1 bucket slots. */
-  int64_t n, n_exc;
+  int32_t n_proj; /* 1 .. BP_MAX_PROJ */
+  int64_t n;
   int64_t col_begin, col_end;
-  bp_jitconn jit_exc, jit_inh; /* conn == BP_CONN_JIT                       */
-  float w_exc, w_inh;          /* homogeneous weights (both conn kinds)     */
-  /* conn == BP_CONN_CSR: column-sliced CSR of each projection, indices local
-   * to [col_begin, col_end); data NULL => homogeneous w_exc / w_inh.       */
-  const int64_t *exc_indptr;
-  const int32_t *exc_indices;
-  const float *exc_data;
-  const int64_t *inh_indptr;
-  const int32_t *inh_indices;
-  const float *inh_data;
+  bp_projection proj[BP_MAX_PROJ];
   bp_neuron_params params;
   bp_neuron_state state; /* local neurons, col_end - col_begin entries     */
-  uint32_t *spikes;      /* global bit vector, >= ceil(n/32) words; holds
-                            spikes_{n-1} on entry to a step               */
+  uint32_t *spikes;      /* global bit vector, >= ceil(n/32) words (NCCL:
+                            world * part_len / 32); holds spikes_{n-1} on
+                            entry to a step                               */
   void *ws;              /* >= bp_network_workspace_bytes(desc), 256-aligned */
   size_t ws_bytes;
+  /* multi-process exchange */
+  int32_t exchange;      /* bp_exchange                                     */
+  int32_t rank, world;   /* BP_EXCHANGE_NCCL: this process / process count  */
+  int32_t reserved2;     /* must be 0                                       */
+  int64_t part_len;      /* BP_EXCHANGE_NCCL: partition length (see above)  */
+  uint8_t nccl_id[128];  /* BP_EXCHANGE_NCCL: ncclUniqueId, the same bytes on
+                            every rank (bp_nccl_unique_id on one of them)   */
 } bp_network_desc;
 
 typedef struct bp_network bp_network; /* opaque; not thread-safe */
 
+/* ncclUniqueId for BP_EXCHANGE_NCCL (128 bytes into out), to be sent to every
+ * rank by the caller's own means.  BP_ERR_NCCL when NCCL cannot be loaded
+ * (libbp resolves NCCL at run time: an already loaded libnccl.so.2, else
+ * the one the dynamic loader finds; BP_NCCL_LIB overrides the path). */
+bp_status bp_nccl_unique_id(uint8_t *out);
+
 size_t bp_network_workspace_bytes(const bp_network_desc *desc);
 /* Copies *desc (all buffers stay owned by the caller), initialises the
- * workspace on `stream` from desc->spikes. */
+ * workspace on `stream` from desc->spikes.  With BP_EXCHANGE_NCCL this is a
+ * collective: every rank must call it (ncclCommInitRank). */
 bp_status bp_network_create(const bp_network_desc *desc, bp_stream stream,
                             bp_network **out);
-/* n_steps full steps on one device (no exchange).  raster_out (nullable,
- * device): n_steps x ceil((col_end-col_begin)/32) words of local spikes.
- * counts_out (nullable; device or page-locked host memory): n_steps int32,
- * the number of local spikes emitted in each step (copied asynchronously). */
+/* n_steps full steps (with BP_EXCHANGE_NCCL the all-gather included).
+ * raster_out (nullable, device): n_steps x ceil((col_end-col_begin)/32)
+ * words of local spikes.  counts_out (nullable; device or page-locked host
+ * memory): n_steps int32, the number of local spikes emitted in each step
+ * (copied asynchronously). */
 bp_status bp_network_step(bp_network *net, int64_t n_steps,
                           uint32_t *raster_out, int32_t *counts_out,
                           bp_stream stream);
-/* The two halves of a step for multi-process runs. */
+/* The two halves of a step for BP_EXCHANGE_CALLER multi-process runs. */
 bp_status bp_network_scatter(bp_network *net, bp_stream stream);
 bp_status bp_network_update(bp_network *net, uint32_t *raster_row,
                             bp_stream stream);
@@ -384,6 +444,8 @@ bp_status bp_network_update_overlap(bp_network *net, uint32_t *raster_row,
  * synchronises `stream`. */
 bp_status bp_network_counters(bp_network *net, uint64_t *host_out,
                               bp_stream stream);
+/* Device memory the network allocated itself (buckets, projection table). */
+size_t bp_network_device_bytes(const bp_network *net);
 /* Per-kernel timing of the next bp_network_step calls (at most max_steps
  * steps): CUDA events are recorded on `stream` before the neuron-update
  * kernel, between it and the event-binning kernel, and after the latter.
@@ -393,6 +455,7 @@ bp_status bp_network_counters(bp_network *net, uint64_t *host_out,
 bp_status bp_network_profile_begin(bp_network *net, int64_t max_steps);
 bp_status bp_network_profile_end(bp_network *net, double *scatter_ms,
                                  double *update_ms, int64_t *steps);
+/* Frees the buckets and, with BP_EXCHANGE_NCCL, destroys the communicator. */
 void bp_network_destroy(bp_network *net);
 
 #ifdef __cplusplus

@@ -388,77 +388,131 @@ def hh_step(params: HHParams, v, m, h, nk, g_e, g_i):
 
 @dataclass
 class Projection:
-    """Rows = presynaptic neurons [row0, row0 + n_rows); cols = all N posts."""
+    """Rows = presynaptic neurons [row0, row0 + n_rows); cols = all N posts.
+    receptor: 'exc' (adds into g_e) or 'inh' (g_i); None = by position in
+    run_network's (proj_e, proj_i) pair."""
     row0: int
     n_rows: int
     jit: JitSpec | None = None
     csr: tuple | None = None        # (indptr, indices, data or None)
     w_homo: float = 0.0             # CSR homogeneous weight when data is None
+    receptor: str | None = None
+
+    @property
+    def weight(self) -> float:
+        return float(self.jit.w0) if self.jit is not None else float(self.w_homo)
+
+    @property
+    def homogeneous(self) -> bool:
+        return (self.jit is not None and self.jit.law == LAW_HOMO
+                or self.jit is None and self.csr[2] is None)
+
+
+def _counts(proj: Projection, ev, n_total, col_begin, col_end, out):
+    """Number of events of `proj` per postsynaptic column (Listing S1 / S2
+    with unit weights; exact integers in fp64), accumulated into out."""
+    if proj.jit is not None:
+        spec1 = JitSpec(proj.jit.seed, proj.jit.K, proj.jit.L, LAW_HOMO, 1.0,
+                        geo_c=proj.jit.geo_c)
+        jit_event_mv(spec1, proj.n_rows, n_total, ev, col_begin, col_end, OUT_F64, out=out)
+    else:
+        ip, ix, _ = proj.csr
+        event_csrmv(ip, ix, None, 1.0, proj.n_rows, col_end - col_begin, ev, OUT_F64, out=out)
+
+
+def _f32_increment(projs, spikes, n_total, col_begin, col_end, n_local):
+    """Rule N1-f32 for the homogeneous projections of one receptor: the
+    step's increment is the EXACTLY ROUNDED sum of its events' weights,
+    fl32(sum_p count_p w_p) (AlignPost merging: one conductance for
+    all of them).  Projections with equal weights are counted together; one
+    weight: fl32(count w) (count w is exact in fp64); several: the exact sum
+    in integer units of 2^-32 (every weight must be a multiple of 2^-32),
+    rounded once to fp32.  Returns (nonzero mask, fp32 increment)."""
+    groups = {}
+    for proj in projs:
+        w = np.float32(proj.weight)
+        cnt = groups.setdefault(w.tobytes(), (w, np.zeros(n_local, np.float64)))[1]
+        ev = spikes[proj.row0:proj.row0 + proj.n_rows]
+        _counts(proj, ev, n_total, col_begin, col_end, cnt)
+    if len(groups) == 1:
+        (w, cnt), = groups.values()
+        return cnt != 0, (cnt.astype(np.float32) * w).astype(np.float32)
+    S = np.zeros(n_local, np.int64)
+    for w, cnt in groups.values():
+        q = float(w) * 4294967296.0
+        assert q == math.floor(q), "merged fp32 weights must lie on the 2^-32 grid"
+        S += cnt.astype(np.int64) * np.int64(q)
+    return S != 0, (S.astype(np.float32) * np.float32(2.0 ** -32)).astype(np.float32)
 
 
 def run_network(model: str, params, state: dict, proj_e: Projection,
-                proj_i: Projection, n_steps: int, col_begin: int = 0,
+                proj_i: Projection | None, n_steps: int, col_begin: int = 0,
                 col_end: int | None = None, record=True, delay: int = 1):
     """Rule S1, for n = 0 .. n_steps-1:
         1. read spikes_{n-D} (D = delay steps, reading D1; D = 1 is the
            paper's one-step VarDelay, P:971/P:988/P:991)
-        2. E rows add into g_E and I rows into g_I (a2/a4)
+        2. every projection adds its events into the conductance of its
+           receptor (E rows -> g_E, I rows -> g_I in Listing S3; a2/a4);
+           projections of one receptor merge into its single g
         3. neuron rule N1 (LIF) or H1 (HH) -> spikes_n
         4. store spikes_n
+    proj_e, proj_i: Listing S3's two projections; or proj_e = a LIST of
+    projections (each with .receptor) and proj_i = None.
     `state` holds numpy arrays (v, g_e, g_i, ref | m, h, n) over the
     postsynaptic columns [col_begin, col_end) and 'spikes' (uint8, all N):
     spikes_{-1} on entry (spikes_{-2}, ..., spikes_{-D} are empty unless
     state['history'] holds them, oldest first), spikes_{n_steps-1} on exit.
-    g dtype int64 selects fixed point (rule F1), float32 selects fp32.
+    g dtype int64 selects fixed point (rule F1), int32 rule F2, float32 fp32.
     Returns the raster (n_steps x N uint8) when record, else spike counts.
     """
     assert delay >= 1
+    if isinstance(proj_e, (list, tuple)):
+        projs = list(proj_e)
+    else:
+        projs = [proj_e, proj_i]
+        for p, r in zip(projs, ("exc", "inh")):
+            if p.receptor is None:
+                p.receptor = r
+    by_rec = {"exc": [p for p in projs if p.receptor == "exc"],
+              "inh": [p for p in projs if p.receptor == "inh"]}
+    assert len(by_rec["exc"]) + len(by_rec["inh"]) == len(projs)
     hist = state.get("history")
     if delay == 1 or hist is None or len(hist) != delay:
         hist = [np.zeros_like(state["spikes"]) for _ in range(delay - 1)] + [state["spikes"]]
     n_total = state["spikes"].shape[0]
     if col_end is None:
         col_end = n_total
+    n_local = col_end - col_begin
     fix32 = state["g_e"].dtype == np.int32
     fixed = state["g_e"].dtype == np.int64
     f32 = not (fix32 or fixed)
     kind = OUT_FIX32 if fix32 else (OUT_FIX if fixed else OUT_F32)
-    raster = np.zeros((n_steps, col_end - col_begin), np.uint8) if record else None
+    raster = np.zeros((n_steps, n_local), np.uint8) if record else None
     counts = np.zeros(n_steps, np.int64)
     for step in range(n_steps):
         spikes = hist[0]
-        for proj, g in ((proj_e, state["g_e"]), (proj_i, state["g_i"])):
-            ev = spikes[proj.row0:proj.row0 + proj.n_rows]
-            homo_f32 = f32 and (proj.jit is not None and proj.jit.law == LAW_HOMO
-                                or proj.jit is None and proj.csr[2] is None)
-            if homo_f32:
-                # rule N1-f32: a homogeneous projection delivers `count`
-                # identical weights to a neuron in a step; the increment is
-                # fl32(count * w) (one rounding of the exact sum)
-                cnt = np.zeros(g.shape[0], np.float64)
-                if proj.jit is not None:
-                    spec1 = JitSpec(proj.jit.seed, proj.jit.K, proj.jit.L, LAW_HOMO, 1.0,
-                                    geo_c=proj.jit.geo_c)
-                    jit_event_mv(spec1, proj.n_rows, n_total, ev, col_begin, col_end,
-                                 OUT_F64, out=cnt)
-                    w = np.float32(proj.jit.w0)
-                else:
-                    ip, ix, _ = proj.csr
-                    event_csrmv(ip, ix, None, 1.0, proj.n_rows, col_end - col_begin, ev,
-                                OUT_F64, out=cnt)
-                    w = np.float32(proj.w_homo)
-                g[:] = g + cnt.astype(np.float32) * w
+        for rec, g in (("exc", state["g_e"]), ("inh", state["g_i"])):
+            group = by_rec[rec]
+            if not group:
                 continue
-            # rule F2: the step's increments are summed exactly, then added
-            # to the int32 conductance with saturation
-            acc = np.zeros(g.shape[0], np.int64) if fix32 else g
-            if proj.jit is not None:
-                jit_event_mv(proj.jit, proj.n_rows, n_total, ev, col_begin,
-                             col_end, kind, out=acc)
-            else:
-                ip, ix, dat = proj.csr
-                event_csrmv(ip, ix, dat, proj.w_homo, proj.n_rows,
-                            col_end - col_begin, ev, kind, out=acc)
+            if f32 and all(p.homogeneous for p in group):
+                nz, inc = _f32_increment(group, spikes, n_total, col_begin, col_end, n_local)
+                g[nz] = g[nz] + inc[nz]
+                continue
+            # fixed point: the increments of every projection of the receptor
+            # summed exactly (int64) -- rule F1 adds them straight into g,
+            # rule F2 adds the step's sum to the int32 g with saturation;
+            # fp32 with heterogeneous weights: sequential fp32 accumulation
+            acc = np.zeros(n_local, np.int64) if fix32 else g
+            for proj in group:
+                ev = spikes[proj.row0:proj.row0 + proj.n_rows]
+                if proj.jit is not None:
+                    jit_event_mv(proj.jit, proj.n_rows, n_total, ev, col_begin,
+                                 col_end, kind, out=acc)
+                else:
+                    ip, ix, dat = proj.csr
+                    event_csrmv(ip, ix, dat, proj.w_homo, proj.n_rows,
+                                n_local, ev, kind, out=acc)
             if fix32:
                 fix32_add(g, acc)
         if model == "lif":

@@ -34,7 +34,8 @@ EXPORTED = [
     "bp_jitconn_materialize", "bp_neuron_step", "bp_network_workspace_bytes",
     "bp_network_create", "bp_network_step", "bp_network_scatter",
     "bp_network_update", "bp_network_update_overlap", "bp_network_counters", "bp_network_profile_begin",
-    "bp_network_profile_end", "bp_network_destroy",
+    "bp_network_profile_end", "bp_network_destroy", "bp_network_device_bytes",
+    "bp_nccl_unique_id",
 ]
 
 
@@ -71,19 +72,30 @@ class NeuronState(ctypes.Structure):
                 ("n_gate", ctypes.c_void_p)]
 
 
+MAX_PROJ = 8                            # BP_MAX_PROJ
+RECEPTOR_EXC, RECEPTOR_INH = 0, 1
+EXCHANGE_CALLER, EXCHANGE_NCCL = 0, 1
+
+
+class Projection(ctypes.Structure):
+    _fields_ = [("conn", ctypes.c_int32), ("receptor", ctypes.c_int32),
+                ("pre_begin", ctypes.c_int64), ("pre_end", ctypes.c_int64),
+                ("weight", _F), ("reserved", ctypes.c_int32), ("jit", JitConn),
+                ("indptr", ctypes.c_void_p), ("indices", ctypes.c_void_p)]
+
+
 class NetworkDesc(ctypes.Structure):
-    _fields_ = [("model", ctypes.c_int32), ("conn", ctypes.c_int32),
-                ("g_kind", ctypes.c_int32), ("delay_steps", ctypes.c_int32),
-                ("n", ctypes.c_int64), ("n_exc", ctypes.c_int64),
+    _fields_ = [("model", ctypes.c_int32), ("g_kind", ctypes.c_int32),
+                ("delay_steps", ctypes.c_int32), ("n_proj", ctypes.c_int32),
+                ("n", ctypes.c_int64),
                 ("col_begin", ctypes.c_int64), ("col_end", ctypes.c_int64),
-                ("jit_exc", JitConn), ("jit_inh", JitConn),
-                ("w_exc", _F), ("w_inh", _F),
-                ("exc_indptr", ctypes.c_void_p), ("exc_indices", ctypes.c_void_p),
-                ("exc_data", ctypes.c_void_p), ("inh_indptr", ctypes.c_void_p),
-                ("inh_indices", ctypes.c_void_p), ("inh_data", ctypes.c_void_p),
+                ("proj", Projection * MAX_PROJ),
                 ("params", NeuronParams), ("state", NeuronState),
                 ("spikes", ctypes.c_void_p), ("ws", ctypes.c_void_p),
-                ("ws_bytes", ctypes.c_size_t)]
+                ("ws_bytes", ctypes.c_size_t),
+                ("exchange", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("world", ctypes.c_int32), ("reserved2", ctypes.c_int32),
+                ("part_len", ctypes.c_int64), ("nccl_id", ctypes.c_uint8 * 128)]
 
 
 _lib = None
@@ -143,12 +155,16 @@ def lib():
         L.bp_network_counters.argtypes = [P, P, P]
         L.bp_network_destroy.argtypes = [P]
         L.bp_network_destroy.restype = None
+        L.bp_network_device_bytes.argtypes = [P]
+        L.bp_network_device_bytes.restype = sz
+        L.bp_nccl_unique_id.argtypes = [P]
         for name in EXPORTED:
             if name not in ("bp_network_destroy", "bp_status_string",
                             "bp_last_error", "bp_conn_len", "bp_workspace_bytes",
                             "bp_csrmv_workspace_bytes", "bp_csrmv_plan_bytes",
                             "bp_jitconn_workspace_bytes",
-                            "bp_network_workspace_bytes", "bp_abi_version"):
+                            "bp_network_workspace_bytes", "bp_abi_version",
+                            "bp_network_device_bytes"):
                 getattr(L, name).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -406,41 +422,85 @@ def neuron_step(params: NeuronParams, state: dict, spikes_out: torch.Tensor,
                                 int(active_base), _stream(stream)))
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId for BP_EXCHANGE_NCCL networks (bp_nccl_unique_id)."""
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib().bp_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+    return bytes(buf)
+
+
+def projection(*, pre_begin, pre_end, weight, receptor=RECEPTOR_EXC, jit=None, csr=None):
+    """One bp_projection: rows = neurons [pre_begin, pre_end), `weight` per
+    event into the receptor's conductance; jit=JitConn or csr=(indptr,
+    indices) (column-sliced to this process's columns)."""
+    p = Projection()
+    p.receptor = int(receptor)
+    p.pre_begin, p.pre_end = int(pre_begin), int(pre_end)
+    p.weight = float(weight)
+    if jit is not None:
+        p.conn = CONN_JIT
+        p.jit = jit
+    else:
+        ip, ix = csr[0], csr[1]
+        _cuda(ip, ix)
+        if ip.dtype != torch.int64 or ix.dtype != torch.int32:
+            raise BpError("CSR projection: indptr int64, indices int32")
+        if ip.numel() != int(pre_end) - int(pre_begin) + 1:
+            raise BpError("CSR projection: indptr must have pre_end - pre_begin + 1 entries")
+        p.conn = CONN_CSR
+        p.indptr, p.indices = ip.data_ptr(), ix.data_ptr()
+    return p
+
+
+def _check_buf(t, numel, dtype, device, what, host_ok=False):
+    """A caller buffer the library writes: right dtype, contiguous, large
+    enough, and on the network's device (or pinned host memory when
+    host_ok)."""
+    if t is None:
+        return
+    if t.dtype != dtype or not t.is_contiguous() or t.numel() < numel:
+        raise BpError(f"{what}: need >= {numel} contiguous {dtype} elements")
+    if t.is_cuda:
+        if t.device != device:
+            raise BpError(f"{what}: on {t.device}, the network is on {device}")
+    elif not (host_ok and t.is_pinned()):
+        raise BpError(f"{what}: must be a CUDA tensor" + (" or pinned host memory"
+                                                          if host_ok else ""))
+
+
 class Network:
-    """Handle over bp_network_* (Listing S3's update loop, rule S1).
+    """Handle over bp_network_* (Listing S3's update loop, rule S1, with up to
+    MAX_PROJ projections merged per receptor).
 
     Keeps references to every tensor whose pointer it passed to the library.
     """
 
-    def __init__(self, *, model, conn, n, n_exc, state: dict, spikes, params,
-                 col_begin=0, col_end=None, jit_exc=None, jit_inh=None,
-                 w_exc=0.6, w_inh=6.7, csr_exc=None, csr_inh=None, stream=None, delay=1):
+    def __init__(self, *, model, n, state: dict, spikes, params, projections,
+                 col_begin=0, col_end=None, stream=None, delay=1, keep=(),
+                 exchange=EXCHANGE_CALLER, rank=0, world=1, part_len=0, nccl_id=None):
         col_end = n if col_end is None else col_end
+        if not 1 <= len(projections) <= MAX_PROJ:
+            raise BpError(f"1..{MAX_PROJ} projections, got {len(projections)}")
         d = NetworkDesc()
-        d.model, d.conn = model, conn
+        d.model = model
         d.delay_steps = int(delay)
         d.g_kind = _out_kind(state["g_e"])
-        d.n, d.n_exc, d.col_begin, d.col_end = n, n_exc, col_begin, col_end
-        if jit_exc is not None:
-            d.jit_exc = jit_exc
-        if jit_inh is not None:
-            d.jit_inh = jit_inh
-        d.w_exc, d.w_inh = w_exc, w_inh
-        self._keep = [state, spikes, csr_exc, csr_inh]
-        for side, csr in (("exc", csr_exc), ("inh", csr_inh)):
-            if csr is not None:
-                ip, ix, dat = csr
-                setattr(d, f"{side}_indptr", ip.data_ptr())
-                setattr(d, f"{side}_indices", ix.data_ptr())
-                if dat is not None:
-                    setattr(d, f"{side}_data", dat.data_ptr())
+        d.n, d.col_begin, d.col_end = n, col_begin, col_end
+        d.n_proj = len(projections)
+        for k, p in enumerate(projections):
+            d.proj[k] = p
+        self._keep = [state, spikes, *keep]
         d.params = params
         d.state = _state_struct(state)
         d.spikes = spikes.data_ptr()
+        d.exchange, d.rank, d.world, d.part_len = int(exchange), int(rank), int(world), int(part_len)
+        if nccl_id is not None:
+            ctypes.memmove(d.nccl_id, nccl_id, 128)
         nbytes = int(lib().bp_network_workspace_bytes(ctypes.byref(d)))
         self.ws = torch.zeros(nbytes, dtype=torch.uint8, device=spikes.device)
         d.ws, d.ws_bytes = self.ws.data_ptr(), nbytes
         self.desc = d
+        self.device = spikes.device
         self.state, self.spikes = state, spikes
         self.n_local = col_end - col_begin
         self.local_words = (self.n_local + 31) // 32
@@ -450,7 +510,10 @@ class Network:
         self._h = handle
 
     def step(self, n_steps: int, raster=None, counts=None, stream=None):
-        """counts: device tensor or pinned host tensor of n_steps int32."""
+        """raster: device int32 [n_steps, local_words] (nullable); counts:
+        device or pinned host int32 [n_steps] (nullable)."""
+        _check_buf(raster, int(n_steps) * self.local_words, torch.int32, self.device, "raster")
+        _check_buf(counts, int(n_steps), torch.int32, self.device, "counts", host_ok=True)
         _check(lib().bp_network_step(self._h, int(n_steps), _ptr(raster), _ptr(counts),
                                      _stream(stream)))
 
@@ -468,12 +531,14 @@ class Network:
         _check(lib().bp_network_scatter(self._h, _stream(stream)))
 
     def update(self, raster_row=None, stream=None):
+        _check_buf(raster_row, self.local_words, torch.int32, self.device, "raster_row")
         _check(lib().bp_network_update(self._h, _ptr(raster_row), _stream(stream)))
 
     def update_overlap(self, exchange_stream, raster_row=None, stream=None):
         """update(); `exchange_stream` (torch.cuda.Stream) waits for this
         step's spike words only, so an all-gather there overlaps the local
         binning kernel."""
+        _check_buf(raster_row, self.local_words, torch.int32, self.device, "raster_row")
         _check(lib().bp_network_update_overlap(self._h, _ptr(raster_row), _stream(stream),
                                                _stream(exchange_stream)))
 
@@ -483,6 +548,11 @@ class Network:
         _check(lib().bp_network_counters(self._h, ctypes.cast(out, ctypes.c_void_p),
                                          _stream(stream)))
         return int(out[0]), int(out[1]), int(out[2])
+
+    def device_bytes(self) -> int:
+        """Device memory the library allocated for this network (buckets,
+        projection table)."""
+        return int(lib().bp_network_device_bytes(self._h))
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:

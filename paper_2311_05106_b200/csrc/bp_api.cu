@@ -2,8 +2,14 @@
 // and the per-step orchestration of the network (include/bp.h).
 #include <cuda_runtime.h>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <mutex>
+#include <vector>
 #include <cstdarg>
 #include <new>
 #include <utility>
@@ -621,7 +627,7 @@ bp_status jit_event_mv(int law, const bp_jitconn *spec, float w0, float w1,
 // ====================================================================== ABI
 extern "C" {
 
-int bp_abi_version(void) { return 1; }
+int bp_abi_version(void) { return 2; }
 
 const char *bp_status_string(int status) {
   switch (status) {
@@ -631,6 +637,7 @@ const char *bp_status_string(int status) {
     case BP_ERR_UNSUPPORTED: return "BP_ERR_UNSUPPORTED";
     case BP_ERR_WORKSPACE: return "BP_ERR_WORKSPACE";
     case BP_ERR_CUDA: return "BP_ERR_CUDA";
+    case BP_ERR_NCCL: return "BP_ERR_NCCL";
     default: return "BP_ERR_UNKNOWN";
   }
 }
@@ -1117,26 +1124,95 @@ extern "C" bp_status bp_neuron_step(const bp_neuron_params *params,
   return launched();
 }
 
+// ================================================================ NCCL
+// NCCL is resolved at run time (dlopen), so libbp.so has no link-time NCCL
+// dependency and shares the process's already loaded libnccl.so.2 (torch's)
+// when there is one.
+namespace {
+
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*get_unique_id)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_gather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char *(*error_string)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+std::mutex g_nccl_mu;
+
+bp_status nccl_load() {
+  std::lock_guard<std::mutex> lock(g_nccl_mu);
+  if (!g_nccl.tried) {
+    g_nccl.tried = true;
+    void *h = nullptr;
+    if (const char *env = std::getenv("BP_NCCL_LIB")) h = dlopen(env, RTLD_NOW);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);   // already in the process
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW);
+    if (h) {
+      g_nccl.get_unique_id = reinterpret_cast<decltype(g_nccl.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+      g_nccl.comm_init_rank = reinterpret_cast<decltype(g_nccl.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+      g_nccl.all_gather = reinterpret_cast<decltype(g_nccl.all_gather)>(dlsym(h, "ncclAllGather"));
+      g_nccl.comm_destroy = reinterpret_cast<decltype(g_nccl.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+      g_nccl.error_string = reinterpret_cast<decltype(g_nccl.error_string)>(dlsym(h, "ncclGetErrorString"));
+      g_nccl.ok = g_nccl.get_unique_id && g_nccl.comm_init_rank && g_nccl.all_gather &&
+                  g_nccl.comm_destroy && g_nccl.error_string;
+    }
+  }
+  if (!g_nccl.ok) return fail(BP_ERR_NCCL, "NCCL not available (libnccl.so.2 not loadable)");
+  return BP_OK;
+}
+
+#define BP_NCCL(call)                                                       \
+  do {                                                                      \
+    ncclResult_t r_ = (call);                                               \
+    if (r_ != ncclSuccess)                                                  \
+      return fail(BP_ERR_NCCL, "%s: %s", #call, g_nccl.error_string(r_));   \
+  } while (0)
+
+}  // namespace
+
+extern "C" bp_status bp_nccl_unique_id(uint8_t *out) {
+  BP_CHECK(out != nullptr, BP_ERR_INVALID_ARG, "out is NULL");
+  bp_status s = nccl_load();
+  if (s != BP_OK) return s;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  ncclUniqueId id;
+  BP_NCCL(g_nccl.get_unique_id(&id));
+  std::memcpy(out, &id, sizeof id);
+  return BP_OK;
+}
+
 // ================================================================ network
 struct bp_network {
   bp_network_desc d;
   int sms;
   int64_t n_local, local_words, global_words;
-  JitResolved jr_e, jr_i;
   unsigned long long *counters;   // [0] spikes delivered, [1] events
   int32_t *count;                 // [2] ping-pong active counts
   int32_t *active[2];             // ping-pong active lists (n entries each)
-  int parity;                     // list holding spikes_{n-1}
   bp::NeuronArgs neuron;
+  // weight classes (step.cuh): projections with the same (receptor, weight)
+  // share one count array; ncls_kernel 2 = class 0 -> g_e, class 1 -> g_i
+  int n_cls = 2, ncls_kernel = 2;
+  float cls_w[bp::kMaxCls] = {};
+  int cls_rec[bp::kMaxCls] = {};
+  int proj_cls[BP_MAX_PROJ] = {};
+  JitResolved jr[BP_MAX_PROJ] = {};
+  bool all_jit = true;
+  bp::NetProj *proj_dev = nullptr;  // device projection table (in bk_mem)
   // profiling: 3 events per step (before scatter, between, after update)
   cudaEvent_t *prof_ev = nullptr;
   cudaEvent_t xev = nullptr;      // bp_network_update_overlap: spike words final
   int64_t prof_cap = 0, prof_used = 0;
   float keep_frac = 0.f;          // L2 evict_last fraction of g (cache.cuh)
-  // fused-step event buckets (step.cuh), two parities, owned by the network
+  // fused-step event buckets (step.cuh), owned by the network
   uint32_t n_tiles = 0, cap = 0;
   bp::Buckets bk[kMaxSlots] = {};  // ring of delay + 1 slots (reading D1)
   void *bk_mem = nullptr;
+  size_t dev_bytes = 0;
   int delay = 1;                  // synaptic delay in steps (desc.delay_steps)
   int slots = 2;                  // bucket ring: step n reads slot n % slots and its
                                   // spikes are binned into slot (n + delay) % slots
@@ -1152,41 +1228,85 @@ struct bp_network {
   // dense delivery: events as per-neuron atomic counts (cap 0), small
   // blocks (k_step_dense) -- compute-bound networks that fill few tiles
   bool dense = false;
+  // BP_EXCHANGE_NCCL: the library's own spike all-gather
+  bool nccl = false;
+  ncclComm_t comm = nullptr;
+  cudaStream_t comm_st = nullptr;
+  cudaEvent_t ev_spk = nullptr;     // this step's local spike words are final
+  cudaEvent_t ev_gath[2] = {};      // all-gather of step parity p done
+  uint32_t *spk[2] = {};            // global spike vectors (D >= 2: alternate per step)
+  int64_t part_words = 0;           // words per rank in the gathered vector
 };
 
 namespace {
 
-size_t network_ws_layout(const bp_network_desc *d, size_t *off_active0,
-                         size_t *off_active1) {
+struct NetWsLayout {
+  size_t active0, active1, spk1, total;
+};
+
+NetWsLayout network_ws_layout(const bp_network_desc *d) {
+  NetWsLayout l{};
   const size_t list = round_up(static_cast<size_t>(d->n) * sizeof(int32_t), 256);
-  *off_active0 = 256;
-  *off_active1 = 256 + list;
-  return 256 + 2 * list;
+  l.active0 = 256;
+  l.active1 = 256 + list;
+  l.spk1 = 256 + 2 * list;
+  l.total = l.spk1;
+  if (d->exchange == BP_EXCHANGE_NCCL && d->delay_steps > 1) {
+    // second gathered spike vector (the exchange of step n overlaps step n + 1)
+    const int64_t words = d->world > 0 && d->part_len > 0 ? d->world * (d->part_len / 32)
+                                                          : (d->n + 31) / 32;
+    l.total += round_up(static_cast<size_t>(words) * sizeof(uint32_t), 256);
+  }
+  return l;
 }
 
 bp_status validate_network(const bp_network_desc *d) {
   BP_CHECK(d != nullptr, BP_ERR_INVALID_ARG, "desc is NULL");
-  BP_CHECK(d->n >= 1 && d->n <= kMaxDim && d->n_exc >= 0 && d->n_exc <= d->n,
-           BP_ERR_SHAPE, "n=%lld n_exc=%lld", (long long)d->n, (long long)d->n_exc);
+  BP_CHECK(d->n >= 1 && d->n <= kMaxDim, BP_ERR_SHAPE, "n=%lld", (long long)d->n);
   BP_CHECK(d->col_begin >= 0 && d->col_begin < d->col_end && d->col_end <= d->n,
            BP_ERR_SHAPE, "partition [%lld, %lld)", (long long)d->col_begin,
            (long long)d->col_end);
+  BP_CHECK(d->col_end - d->col_begin < (int64_t{1} << 30), BP_ERR_SHAPE,
+           "a process owns at most 2^30 - 1 neurons");
   BP_CHECK(d->col_begin % 32 == 0, BP_ERR_SHAPE, "col_begin not a multiple of 32");
   BP_CHECK(d->col_end % 32 == 0 || d->col_end == d->n, BP_ERR_SHAPE,
            "col_end must be a multiple of 32 or n");
-  BP_CHECK(d->conn == BP_CONN_JIT || d->conn == BP_CONN_CSR, BP_ERR_INVALID_ARG,
-           "conn %d", d->conn);
+  BP_CHECK(d->n_proj >= 1 && d->n_proj <= BP_MAX_PROJ, BP_ERR_INVALID_ARG,
+           "n_proj %d not in [1, %d]", d->n_proj, BP_MAX_PROJ);
+  for (int p = 0; p < d->n_proj; ++p) {
+    const bp_projection &P = d->proj[p];
+    BP_CHECK(P.conn == BP_CONN_JIT || P.conn == BP_CONN_CSR, BP_ERR_INVALID_ARG,
+             "projection %d: conn %d", p, P.conn);
+    BP_CHECK(P.receptor == BP_RECEPTOR_EXC || P.receptor == BP_RECEPTOR_INH,
+             BP_ERR_INVALID_ARG, "projection %d: receptor %d", p, P.receptor);
+    BP_CHECK(P.pre_begin >= 0 && P.pre_begin <= P.pre_end && P.pre_end <= d->n,
+             BP_ERR_SHAPE, "projection %d: rows [%lld, %lld)", p, (long long)P.pre_begin,
+             (long long)P.pre_end);
+    BP_CHECK(std::isfinite(P.weight), BP_ERR_INVALID_ARG, "projection %d: weight", p);
+    BP_CHECK(P.reserved == 0, BP_ERR_INVALID_ARG, "projection %d: reserved must be 0", p);
+    if (P.conn == BP_CONN_CSR)
+      BP_CHECK(P.pre_end == P.pre_begin || (P.indptr && P.indices), BP_ERR_INVALID_ARG,
+               "projection %d: NULL CSR", p);
+  }
   BP_CHECK(d->spikes != nullptr && aligned(d->spikes, 4), BP_ERR_INVALID_ARG,
            "spikes NULL/misaligned");
   BP_CHECK(d->params.model == d->model, BP_ERR_INVALID_ARG, "params.model != model");
   BP_CHECK(d->delay_steps >= 0 && d->delay_steps <= kMaxDelay, BP_ERR_INVALID_ARG,
            "delay_steps %d not in [0, %d]", d->delay_steps, kMaxDelay);
   BP_CHECK(d->state.g_kind == d->g_kind, BP_ERR_INVALID_ARG, "state.g_kind != g_kind");
-  if (d->conn == BP_CONN_CSR) {
-    BP_CHECK(d->n_exc == 0 || (d->exc_indptr && d->exc_indices), BP_ERR_INVALID_ARG,
-             "NULL excitatory CSR");
-    BP_CHECK(d->n_exc == d->n || (d->inh_indptr && d->inh_indices), BP_ERR_INVALID_ARG,
-             "NULL inhibitory CSR");
+  BP_CHECK(d->exchange == BP_EXCHANGE_CALLER || d->exchange == BP_EXCHANGE_NCCL,
+           BP_ERR_INVALID_ARG, "exchange %d", d->exchange);
+  BP_CHECK(d->reserved2 == 0, BP_ERR_INVALID_ARG, "reserved2 must be 0");
+  if (d->exchange == BP_EXCHANGE_NCCL) {
+    BP_CHECK(d->world >= 1 && d->rank >= 0 && d->rank < d->world, BP_ERR_INVALID_ARG,
+             "rank %d of world %d", d->rank, d->world);
+    BP_CHECK(d->part_len > 0 && d->part_len % 32 == 0, BP_ERR_SHAPE,
+             "part_len %lld must be a positive multiple of 32", (long long)d->part_len);
+    BP_CHECK(d->part_len * d->world >= d->n, BP_ERR_SHAPE, "world * part_len < n");
+    const int64_t lo = d->rank * d->part_len;
+    const int64_t hi = std::min<int64_t>(d->n, lo + d->part_len);
+    BP_CHECK(d->col_begin == lo && d->col_end == hi, BP_ERR_SHAPE,
+             "rank %d must own [%lld, %lld)", d->rank, (long long)lo, (long long)hi);
   }
   BP_CHECK(d->ws != nullptr && aligned(d->ws, 256), BP_ERR_WORKSPACE,
            "workspace NULL or not 256-byte aligned");
@@ -1195,34 +1315,103 @@ bp_status validate_network(const bp_network_desc *d) {
   return BP_OK;
 }
 
-}  // namespace
+// Weight classes: projections with the same (receptor, weight) share one
+// count array.  The standard layout (at most one weight per receptor:
+// Listing S3) keeps class 0 = excitatory, class 1 = inhibitory and the
+// kernels' one-class-per-receptor fold; anything else uses the general merge
+// (up to 4 classes, exact integer sums; fp32 needs weights on the 2^-32 grid).
+bp_status assign_classes(bp_network *net) {
+  const bp_network_desc &d = net->d;
+  float w_rec[2] = {0.f, 0.f};
+  int n_w[2] = {0, 0};
+  for (int p = 0; p < d.n_proj; ++p) {
+    const int r = d.proj[p].receptor;
+    if (n_w[r] == 0 || std::memcmp(&w_rec[r], &d.proj[p].weight, sizeof(float)) != 0) {
+      if (n_w[r] == 0) w_rec[r] = d.proj[p].weight;
+      n_w[r] += (n_w[r] == 0 || std::memcmp(&w_rec[r], &d.proj[p].weight, sizeof(float)) != 0);
+    }
+  }
+  bool standard = n_w[0] <= 1 && n_w[1] <= 1;
+  if (const char *env = std::getenv("BP_MERGE_GENERAL")) standard = standard && !std::atoi(env);
+  if (standard) {
+    net->n_cls = 2;
+    net->ncls_kernel = 2;
+    net->cls_w[0] = w_rec[0];
+    net->cls_w[1] = w_rec[1];
+    net->cls_rec[0] = 0;
+    net->cls_rec[1] = 1;
+    for (int p = 0; p < d.n_proj; ++p) net->proj_cls[p] = d.proj[p].receptor;
+    return BP_OK;
+  }
+  net->n_cls = 0;
+  net->ncls_kernel = bp::kMaxCls;
+  for (int p = 0; p < d.n_proj; ++p) {
+    int c = 0;
+    for (; c < net->n_cls; ++c)
+      if (net->cls_rec[c] == d.proj[p].receptor &&
+          std::memcmp(&net->cls_w[c], &d.proj[p].weight, sizeof(float)) == 0)
+        break;
+    if (c == net->n_cls) {
+      BP_CHECK(net->n_cls < bp::kMaxCls, BP_ERR_UNSUPPORTED,
+               "more than %d distinct (receptor, weight) classes", bp::kMaxCls);
+      net->cls_w[c] = d.proj[p].weight;
+      net->cls_rec[c] = d.proj[p].receptor;
+      ++net->n_cls;
+    }
+    net->proj_cls[p] = c;
+  }
+  if (d.g_kind == BP_OUT_F32) {
+    for (int c = 0; c < net->n_cls; ++c) {
+      const double q = static_cast<double>(net->cls_w[c]) * 4294967296.0;
+      BP_CHECK(q == std::rint(q) && std::fabs(q) < 9.0e15, BP_ERR_UNSUPPORTED,
+               "fp32 merged conductances need weights on the 2^-32 grid (w = %g)",
+               static_cast<double>(net->cls_w[c]));
+    }
+  }
+  // the exact int64 sums of one step cannot overflow: rows x |q| summed
+  double bound = 0.0;
+  for (int p = 0; p < d.n_proj; ++p)
+    bound += static_cast<double>(d.proj[p].pre_end - d.proj[p].pre_begin) *
+             std::fabs(static_cast<double>(d.proj[p].weight)) * 4294967296.0;
+  BP_CHECK(bound < 4.0e18, BP_ERR_UNSUPPORTED, "merged increments may overflow int64");
+  return BP_OK;
+}
 
-namespace {
-
-bp::ConnArgs make_conn(const bp_network *net) {
+// Build the device projection table and the launch-wide connection args.
+bp::ConnArgs make_conn(bp_network *net, std::vector<bp::NetProj> *table) {
   const bp_network_desc &d = net->d;
   bp::ConnArgs c{};
-  c.conn = d.conn;
-  c.split = d.n_exc;
+  c.n_proj = d.n_proj;
   c.n_cols = static_cast<uint32_t>(d.n);
-  if (d.conn == BP_CONN_JIT) {
-    c.je = jit_side(&d.jit_exc, net->jr_e, BP_LAW_HOMO, d.w_exc, 0.f, d.col_begin,
-                    d.col_end, d.state.g_exc);
-    c.ji = jit_side(&d.jit_inh, net->jr_i, BP_LAW_HOMO, d.w_inh, 0.f, d.col_begin,
-                    d.col_end, d.state.g_inh);
-    // expected events of one row in one segment: L * 2 / (K + 1)
-    const double fe = net->jr_e.L * 2.0 / (net->jr_e.K + 1.0);
-    const double fi = net->jr_i.L * 2.0 / (net->jr_i.K + 1.0);
-    // One lane per row when a row has few events in this rank's segment
-    // (multi-GPU partitions: ~80/G per row): measured 3x faster at G = 8
-    // (220 k rows, 10 events per row-segment: 34 vs 99 us) but slower at
-    // G = 1 (80 events per row: 44 vs 34 us; tools/probes/probe_bin.cu).
-    const char *lr = std::getenv("BP_BIN_LANE_ROWS");
-    c.lane_rows = lr ? std::atoi(lr) : ((fe <= 48.0 && fi <= 48.0) ? 1 : 0);
-  } else {
-    c.ce.indptr = d.exc_indptr; c.ce.indices = d.exc_indices; c.ce.data = d.exc_data;
-    c.ci.indptr = d.inh_indptr; c.ci.indices = d.inh_indices; c.ci.data = d.inh_data;
+  bool lane = true;
+  net->all_jit = true;
+  table->assign(d.n_proj, bp::NetProj{});
+  for (int p = 0; p < d.n_proj; ++p) {
+    const bp_projection &P = d.proj[p];
+    bp::NetProj &t = (*table)[p];
+    t.pre_begin = static_cast<uint32_t>(P.pre_begin);
+    t.pre_end = static_cast<uint32_t>(P.pre_end);
+    t.conn = P.conn;
+    t.cls = static_cast<uint32_t>(net->proj_cls[p]);
+    if (P.conn == BP_CONN_JIT) {
+      t.j = jit_side(&P.jit, net->jr[p], BP_LAW_HOMO, P.weight, 0.f, d.col_begin, d.col_end,
+                     nullptr);
+      // expected events of one row in one segment: L * 2 / (K + 1)
+      lane = lane && net->jr[p].L * 2.0 / (net->jr[p].K + 1.0) <= 48.0;
+    } else {
+      t.c.indptr = P.indptr;
+      t.c.indices = P.indices;
+      t.c.w = P.weight;
+      net->all_jit = false;
+    }
   }
+  c.all_jit = net->all_jit ? 1 : 0;
+  // One lane per row when a row has few events in this rank's segment
+  // (multi-GPU partitions: ~80/G per row): measured 3x faster at G = 8
+  // (220 k rows, 10 events per row-segment: 34 vs 99 us) but slower at
+  // G = 1 (80 events per row: 44 vs 34 us; tools/probes/probe_bin.cu).
+  const char *lr = std::getenv("BP_BIN_LANE_ROWS");
+  c.lane_rows = net->all_jit ? (lr ? std::atoi(lr) : (lane ? 1 : 0)) : 0;
   return c;
 }
 
@@ -1238,22 +1427,28 @@ bp::BinTarget bin_target(const bp_network *net, int parity) {
 // Mean events per postsynaptic neuron per presynaptic spike wave: fan-in.
 double fan_in_estimate(const bp_network *net, cudaStream_t st) {
   const bp_network_desc &d = net->d;
-  if (d.conn == BP_CONN_JIT)
-    return static_cast<double>(d.n_exc) * 2.0 / (net->jr_e.K + 1.0) +
-           static_cast<double>(d.n - d.n_exc) * 2.0 / (net->jr_i.K + 1.0);
-  int64_t nnz_e = 0, nnz_i = 0;
-  if (d.n_exc > 0)
-    cudaMemcpyAsync(&nnz_e, d.exc_indptr + d.n_exc, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
-  if (d.n > d.n_exc)
-    cudaMemcpyAsync(&nnz_i, d.inh_indptr + (d.n - d.n_exc), sizeof(int64_t),
-                    cudaMemcpyDeviceToHost, st);
-  cudaStreamSynchronize(st);
-  return static_cast<double>(nnz_e + nnz_i) / static_cast<double>(net->n_local);
+  double f = 0.0;
+  for (int p = 0; p < d.n_proj; ++p) {
+    const bp_projection &P = d.proj[p];
+    const int64_t rows = P.pre_end - P.pre_begin;
+    if (rows == 0) continue;
+    if (P.conn == BP_CONN_JIT) {
+      f += static_cast<double>(rows) * net->jr[p].density;
+    } else {
+      int64_t nnz = 0;
+      cudaMemcpyAsync(&nnz, P.indptr + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      f += static_cast<double>(nnz) / static_cast<double>(net->n_local);
+    }
+  }
+  return f;
 }
 
 // Buckets sized for 5 % of the presynaptic neurons spiking in one step
-// (500 Hz at dt = 0.1 ms); more events spill exactly (step.cuh).
-bp_status alloc_buckets(bp_network *net, cudaStream_t st) {
+// (500 Hz at dt = 0.1 ms); more events spill exactly (step.cuh).  The
+// projection table shares the allocation.
+bp_status alloc_buckets(bp_network *net, const std::vector<bp::NetProj> &table,
+                        cudaStream_t st) {
   net->n_tiles = static_cast<uint32_t>((net->n_local + bp::kTile - 1) / bp::kTile);
   double expect = bp::kTile * fan_in_estimate(net, st) * 0.05;
   uint32_t cap = static_cast<uint32_t>(round_up(static_cast<size_t>(expect) + 1024, 1024));
@@ -1261,18 +1456,24 @@ bp_status alloc_buckets(bp_network *net, cudaStream_t st) {
   if (cap < 1) cap = 1;
   if (net->dense) cap = 0;               // every event straight into the dense counts
   net->cap = cap;
+  const size_t ncls = static_cast<size_t>(net->ncls_kernel);
   const size_t cnt_b = round_up(static_cast<size_t>(net->n_tiles) * bp::kCntStride *
                                     sizeof(int32_t), 256);
   const size_t buf_b = round_up(static_cast<size_t>(net->n_tiles) * cap * sizeof(uint32_t), 256);
-  const size_t spill_b = round_up(2 * static_cast<size_t>(net->n_local) * sizeof(int32_t), 256);
+  const size_t spill_b = round_up(ncls * static_cast<size_t>(net->n_local) * sizeof(int32_t), 256);
   const size_t per = 2 * cnt_b + buf_b + spill_b;     // cnt, flag, buf, spill
   const size_t small_b = round_up((static_cast<size_t>(net->n_local) + 64) * sizeof(int32_t), 256);
+  const size_t table_b = round_up(table.size() * sizeof(bp::NetProj), 256);
   const size_t R = static_cast<size_t>(net->slots);
-  BP_CUDA(cudaMalloc(&net->bk_mem, R * per + small_b));
-  net->small_count = reinterpret_cast<int32_t *>(static_cast<char *>(net->bk_mem) + R * per);
-  net->small_active = net->small_count + 64;
-  BP_CUDA(cudaMemsetAsync(net->small_count, 0, sizeof(int32_t), st));
+  net->dev_bytes = R * per + small_b + table_b;
+  BP_CUDA(cudaMalloc(&net->bk_mem, net->dev_bytes));
   char *m = static_cast<char *>(net->bk_mem);
+  net->small_count = reinterpret_cast<int32_t *>(m + R * per);
+  net->small_active = net->small_count + 64;
+  net->proj_dev = reinterpret_cast<bp::NetProj *>(m + R * per + small_b);
+  BP_CUDA(cudaMemcpyAsync(net->proj_dev, table.data(), table.size() * sizeof(bp::NetProj),
+                          cudaMemcpyHostToDevice, st));
+  BP_CUDA(cudaMemsetAsync(net->small_count, 0, sizeof(int32_t), st));
   for (int p = 0; p < net->slots; ++p) {
     char *b = m + p * per;
     net->bk[p].cnt = reinterpret_cast<int32_t *>(b);
@@ -1282,6 +1483,8 @@ bp_status alloc_buckets(bp_network *net, cudaStream_t st) {
     BP_CUDA(cudaMemsetAsync(b, 0, 2 * cnt_b, st));
     BP_CUDA(cudaMemsetAsync(net->bk[p].spill, 0, spill_b, st));
   }
+  // the table copy reads a host vector: finish it before that goes away
+  BP_CUDA(cudaStreamSynchronize(st));
   return BP_OK;
 }
 
@@ -1325,11 +1528,11 @@ bp_status launch_bin(bp_network *net, const int32_t *active, const int32_t *coun
 }
 
 // Bin the events of the spikes in words [w_begin, w_end) of the global
-// vector (neurons [32 w_begin, min(32 w_end, n))) into bucket parity `par`.
-// words [skip_b, skip_e) (absolute) are skipped: one pass over the remote
-// words on both sides of a partition's own range
-bp_status bin_spike_range(bp_network *net, int64_t w_begin, int64_t w_end, int par,
-                          cudaStream_t st, int64_t skip_b = 0, int64_t skip_e = 0) {
+// vector `vec` (neurons [32 w_begin, min(32 w_end, n))) into bucket parity
+// `par`.  Words [skip_b, skip_e) (absolute) are skipped: one pass over the
+// remote words on both sides of a partition's own range.
+bp_status bin_spike_range(bp_network *net, const uint32_t *vec, int64_t w_begin, int64_t w_end,
+                          int par, cudaStream_t st, int64_t skip_b = 0, int64_t skip_e = 0) {
   if (w_end <= w_begin) return BP_OK;
   const int64_t first = w_begin * 32;
   const int64_t last = w_end * 32 < net->d.n ? w_end * 32 : net->d.n;
@@ -1337,14 +1540,15 @@ bp_status bin_spike_range(bp_network *net, int64_t w_begin, int64_t w_end, int p
   int32_t *active = net->active[0];
   int32_t *count = net->count;
   BP_CUDA(cudaMemsetAsync(count, 0, sizeof(int32_t), st));
-  launch_compact(net->d.spikes + w_begin, last - first, active, count, net->sms, st,
+  launch_compact(vec + w_begin, last - first, active, count, net->sms, st,
                  static_cast<int32_t>(first), skip_b - w_begin, skip_e - w_begin);
   bp_status s = launched();
   if (s != BP_OK) return s;
   return launch_bin(net, active, count, par, last - first, st);
 }
 
-// Quantised homogeneous weight of the network's conductance kind.
+// Quantised class weight for the conductance kind (and the general fp32
+// merge, which sums at 2^-32).
 long long net_q(const bp_network *net, float w) {
   if (net->d.g_kind == BP_OUT_FIX32)
     return llrint(std::ldexp(static_cast<double>(w), net->neuron.frac_bits));
@@ -1353,17 +1557,18 @@ long long net_q(const bp_network *net, float w) {
 
 // The per-network fields of a step (buckets, order and lists set by callers).
 bp::StepArgs step_args(bp_network *net) {
-  const bp_network_desc &d = net->d;
   bp::StepArgs a{};
   a.nrn = net->neuron;
   a.nrn.raster = nullptr;
   a.nrn.active = nullptr;
-  a.model = d.model;
-  a.conn = net->conn;
-  a.w_e = d.w_exc;
-  a.w_i = d.w_inh;
-  a.q_e = net_q(net, d.w_exc);
-  a.q_i = net_q(net, d.w_inh);
+  a.model = net->d.model;
+  a.n_cls = net->n_cls;
+  for (int c = 0; c < bp::kMaxCls; ++c) {
+    const bool used = c < net->n_cls;
+    a.w[c] = used ? net->cls_w[c] : 0.f;
+    a.q[c] = used ? net_q(net, net->cls_w[c]) : 0;
+    a.rec[c] = used ? net->cls_rec[c] : 0;
+  }
   a.saturated = net->counters + 2;
   a.n_tiles = net->n_tiles;
   a.events = net->counters + 1;
@@ -1371,11 +1576,39 @@ bp::StepArgs step_args(bp_network *net) {
   return a;
 }
 
+// The gathered spike vector written by step n (NCCL, D >= 2: alternating).
+uint32_t *step_vector(const bp_network *net, int64_t step) {
+  return net->spk[net->spk[1] ? (step & 1) : 0];
+}
+
+template <int MODEL, int KIND, int NCLS>
+bp_status launch_k_step(const bp::StepArgs &a, int grid, cudaStream_t st) {
+  constexpr int threads = MODEL == 0 ? bp::kStepThreads : 512;
+  constexpr size_t smem = static_cast<size_t>(NCLS) * bp::kTile * sizeof(int32_t);
+  if (smem > 48 * 1024) {
+    static std::atomic<uint64_t> attr{0};
+    if (first_on_device(attr))
+      BP_CUDA(cudaFuncSetAttribute(bp::k_step<MODEL, KIND, NCLS>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+  }
+  BP_CUDA(launch_pdl(bp::k_step<MODEL, KIND, NCLS>, grid, threads, smem, st, a));
+  return BP_OK;
+}
+
+template <int MODEL, int KIND>
+bp_status launch_k_step_n(const bp::StepArgs &a, int ncls, int grid, cudaStream_t st) {
+  return ncls == 2 ? launch_k_step<MODEL, KIND, 2>(a, grid, st)
+                   : launch_k_step<MODEL, KIND, bp::kMaxCls>(a, grid, st);
+}
+
 bp_status launch_step(bp_network *net, uint32_t *raster, cudaStream_t st,
-                      int32_t *step_spikes = nullptr, cudaEvent_t mid = nullptr) {
+                      int32_t *step_spikes = nullptr, cudaEvent_t mid = nullptr,
+                      cudaEvent_t mid2 = nullptr) {
   const bp_network_desc &d = net->d;
   bp::StepArgs a = step_args(net);
   a.nrn.raster = raster;
+  a.nrn.spikes = step_vector(net, net->steps_done) + d.col_begin / 32;
   const int in_slot = static_cast<int>(net->steps_done % net->slots);
   const int out_slot = static_cast<int>((net->steps_done + net->delay) % net->slots);
   a.in = net->bk[in_slot];
@@ -1390,6 +1623,7 @@ bp_status launch_step(bp_network *net, uint32_t *raster, cudaStream_t st,
   a.active_count = net->count + 2 + cp;
   a.zero_count = net->count + 2 + (cp ^ 1);
   const int grid = static_cast<int>(net->n_tiles);
+  bp_status s = BP_OK;
   if (net->dense) {
     const int dgrid = static_cast<int>((net->n_local + 4 * bp::kDenseThreads - 1) /
                                        (4 * bp::kDenseThreads));
@@ -1405,17 +1639,19 @@ bp_status launch_step(bp_network *net, uint32_t *raster, cudaStream_t st,
       else BP_CUDA(launch_pdl(bp::k_hh_dense1<0>, hgrid, bp::kHHThreads, 0, st, a));
     }
   } else if (d.model == BP_MODEL_LIF) {
-    if (d.g_kind == BP_OUT_FIX64) BP_CUDA(launch_pdl(bp::k_step<0, 1>, grid, bp::kStepThreads, 0, st, a));
-    else if (d.g_kind == BP_OUT_FIX32) BP_CUDA(launch_pdl(bp::k_step<0, 2>, grid, bp::kStepThreads, 0, st, a));
-    else BP_CUDA(launch_pdl(bp::k_step<0, 0>, grid, bp::kStepThreads, 0, st, a));
+    if (d.g_kind == BP_OUT_FIX64) s = launch_k_step_n<0, 1>(a, net->ncls_kernel, grid, st);
+    else if (d.g_kind == BP_OUT_FIX32) s = launch_k_step_n<0, 2>(a, net->ncls_kernel, grid, st);
+    else s = launch_k_step_n<0, 0>(a, net->ncls_kernel, grid, st);
   } else {   // HH is compute-latency-bound: 512 threads per tile
-    if (d.g_kind == BP_OUT_FIX64) BP_CUDA(launch_pdl(bp::k_step<1, 1>, grid, 512, 0, st, a));
-    else if (d.g_kind == BP_OUT_FIX32) BP_CUDA(launch_pdl(bp::k_step<1, 2>, grid, 512, 0, st, a));
-    else BP_CUDA(launch_pdl(bp::k_step<1, 0>, grid, 512, 0, st, a));
+    if (d.g_kind == BP_OUT_FIX64) s = launch_k_step_n<1, 1>(a, net->ncls_kernel, grid, st);
+    else if (d.g_kind == BP_OUT_FIX32) s = launch_k_step_n<1, 2>(a, net->ncls_kernel, grid, st);
+    else s = launch_k_step_n<1, 0>(a, net->ncls_kernel, grid, st);
   }
-  bp_status s = launched();
+  if (s != BP_OK) return s;
+  s = launched();
   if (s != BP_OK) return s;
   if (mid) BP_CUDA(cudaEventRecord(mid, st));
+  if (mid2) BP_CUDA(cudaEventRecord(mid2, st));
   s = launch_bin(net, net->active[1], net->count + 2 + cp, out_par, net->n_local, st);
   if (s != BP_OK) return s;
   net->steps_done += 1;
@@ -1451,10 +1687,10 @@ bp_status small_step(bp_network *net, int64_t n_steps, uint32_t *raster, int32_t
   a.nrn = net->neuron;
   a.nrn.raster = raster;
   a.conn = net->conn;
-  a.w_e = d.w_exc;
-  a.w_i = d.w_inh;
-  a.q_e = net_q(net, d.w_exc);
-  a.q_i = net_q(net, d.w_inh);
+  a.w_e = net->cls_w[0];
+  a.w_i = net->cls_w[1];
+  a.q_e = net_q(net, net->cls_w[0]);
+  a.q_i = net_q(net, net->cls_w[1]);
   a.saturated = net->counters + 2;
   a.n_steps = n_steps;
   a.step_counts = counts_out ? net->small_steps : nullptr;
@@ -1489,15 +1725,79 @@ bp_status small_step(bp_network *net, int64_t n_steps, uint32_t *raster, int32_t
   return BP_OK;
 }
 
+// Remote spikes of step `step` (the words outside this rank's slice of the
+// gathered vector) into the slot they are delivered at, step + delay.
+bp_status remote_scatter(bp_network *net, int64_t step, cudaStream_t st) {
+  if (net->d.exchange == BP_EXCHANGE_NCCL && net->d.world == 1) return BP_OK;
+  const int64_t lw0 = net->d.col_begin / 32;
+  const int64_t lw1 = (net->d.col_end + 31) / 32;
+  const int slot = static_cast<int>((step + net->delay) % net->slots);
+  // one compaction + one binning launch for the words on both sides
+  return bin_spike_range(net, step_vector(net, step), 0, net->global_words, slot, st, lw0, lw1);
+}
+
+// One step of a BP_EXCHANGE_NCCL network:
+//   D = 1:  [wait gather(n-1); remote scatter(n-1)] -> k_step(n) -> local bin(n)
+//           with gather(n) on the comm stream after k_step (overlaps the bin);
+//   D >= 2: k_step(n) -> local bin(n) -> [wait gather(n-1); remote scatter(n-1)]
+//           -- gather(n) overlaps local bin(n), remote scatter(n-1) and the
+//           whole k_step(n + 1) (vectors alternate per step).
+bp_status nccl_step(bp_network *net, uint32_t *raster, int32_t *step_spikes, cudaEvent_t *prof,
+                    cudaStream_t st) {
+  const int64_t n = net->steps_done;
+  bp_status s = BP_OK;
+  if (net->delay == 1 && n > 0) {
+    BP_CUDA(cudaStreamWaitEvent(st, net->ev_gath[(n - 1) & 1], 0));
+    s = remote_scatter(net, n - 1, st);
+    if (s != BP_OK) return s;
+  }
+  // profiling: [0] before k_step, [1] after it, [2] after the local binning
+  if (prof) BP_CUDA(cudaEventRecord(prof[0], st));
+  s = launch_step(net, raster, st, step_spikes, net->ev_spk,
+                  prof ? prof[1] : nullptr);   // steps_done -> n + 1
+  if (s != BP_OK) return s;
+  if (prof) BP_CUDA(cudaEventRecord(prof[2], st));
+  // gather(n): every rank's words of step n into the vector of step n
+  uint32_t *vec = step_vector(net, n);
+  BP_CUDA(cudaStreamWaitEvent(net->comm_st, net->ev_spk, 0));
+  BP_NCCL(g_nccl.all_gather(vec + net->d.rank * net->part_words, vec,
+                            static_cast<size_t>(net->part_words), ncclUint32, net->comm,
+                            net->comm_st));
+  BP_CUDA(cudaEventRecord(net->ev_gath[n & 1], net->comm_st));
+  if (net->delay > 1 && n > 0) {
+    BP_CUDA(cudaStreamWaitEvent(st, net->ev_gath[(n - 1) & 1], 0));
+    s = remote_scatter(net, n - 1, st);
+    if (s != BP_OK) return s;
+  }
+  return BP_OK;
+}
+
+bp_status nccl_setup(bp_network *net, cudaStream_t st) {
+  bp_status s = nccl_load();
+  if (s != BP_OK) return s;
+  ncclUniqueId id;
+  std::memcpy(&id, net->d.nccl_id, sizeof id);
+  BP_CUDA(cudaStreamSynchronize(st));
+  BP_NCCL(g_nccl.comm_init_rank(&net->comm, net->d.world, id, net->d.rank));
+  BP_CUDA(cudaStreamCreateWithFlags(&net->comm_st, cudaStreamNonBlocking));
+  BP_CUDA(cudaEventCreateWithFlags(&net->ev_spk, cudaEventDisableTiming));
+  BP_CUDA(cudaEventCreateWithFlags(&net->ev_gath[0], cudaEventDisableTiming));
+  BP_CUDA(cudaEventCreateWithFlags(&net->ev_gath[1], cudaEventDisableTiming));
+  net->part_words = net->d.part_len / 32;
+  net->nccl = true;
+  return BP_OK;
+}
+
 }  // namespace
 
 extern "C" {
 
 size_t bp_network_workspace_bytes(const bp_network_desc *desc) {
   if (desc == nullptr || desc->n < 0) return 0;
-  size_t a0, a1;
-  return network_ws_layout(desc, &a0, &a1);
+  return network_ws_layout(desc).total;
 }
+
+size_t bp_network_device_bytes(const bp_network *net) { return net ? net->dev_bytes : 0; }
 
 bp_status bp_network_create(const bp_network_desc *desc, bp_stream stream,
                             bp_network **out) {
@@ -1515,44 +1815,42 @@ bp_status bp_network_create(const bp_network_desc *desc, bp_stream stream,
   net->slots = net->delay + 1;
   net->n_local = desc->col_end - desc->col_begin;
   net->local_words = (net->n_local + 31) / 32;
-  net->global_words = (desc->n + 31) / 32;
-  // dense delivery for the compute-bound HH model up to 2 M local neurons
-  // (counts stay L2-resident; 4096-neuron tiles would leave SMs idle);
-  // BP_DENSE=0/1 overrides
-  {
-    const char *env = std::getenv("BP_DENSE");
-    net->dense = env ? std::atoi(env) != 0 : dense_delivery(desc->model, net->n_local);
-  }
-  if (desc->conn == BP_CONN_JIT) {
-    s = resolve_jit(&desc->jit_exc, desc->n, &net->jr_e);
-    if (s == BP_OK) s = resolve_jit(&desc->jit_inh, desc->n, &net->jr_i);
-    if (s == BP_OK && (net->jr_e.geo_c != 0.f || net->jr_i.geo_c != 0.f)) {
+  net->global_words = desc->exchange == BP_EXCHANGE_NCCL
+                          ? desc->world * (desc->part_len / 32)
+                          : (desc->n + 31) / 32;
+  for (int p = 0; p < desc->n_proj && s == BP_OK; ++p) {
+    const bp_projection &P = desc->proj[p];
+    if (P.conn != BP_CONN_JIT) continue;
+    s = resolve_jit(&P.jit, desc->n, &net->jr[p]);
+    if (s == BP_OK && net->jr[p].geo_c != 0.f)
       s = fail(BP_ERR_UNSUPPORTED,
                "networks use the uniform gap sampler (rule J3); gap_law must be 0");
-    }
-    if (s == BP_OK &&
-        (desc->col_begin % net->jr_e.L || desc->col_begin % net->jr_i.L ||
-         (desc->col_end != desc->n &&
-          (desc->col_end % net->jr_e.L || desc->col_end % net->jr_i.L))))
-      s = fail(BP_ERR_SHAPE, "partition not aligned to seg_len");
-    if (s != BP_OK) {
-      delete net;
-      return s;
-    }
+    if (s == BP_OK && (desc->col_begin % net->jr[p].L ||
+                       (desc->col_end != desc->n && desc->col_end % net->jr[p].L)))
+      s = fail(BP_ERR_SHAPE, "partition not aligned to seg_len of projection %d", p);
   }
-  s = fill_neuron_args(&desc->params, &desc->state, net->n_local, &net->neuron);
+  if (s == BP_OK) s = fill_neuron_args(&desc->params, &desc->state, net->n_local, &net->neuron);
+  if (s == BP_OK) s = assign_classes(net);
   if (s != BP_OK) {
     delete net;
     return s;
   }
-  size_t a0, a1;
-  network_ws_layout(desc, &a0, &a1);
+  // dense delivery for the compute-bound HH model up to 2 M local neurons
+  // (counts stay L2-resident; 4096-neuron tiles would leave SMs idle);
+  // BP_DENSE=0/1 overrides.  Standard class layout only.
+  {
+    const char *env = std::getenv("BP_DENSE");
+    net->dense = (env ? std::atoi(env) != 0 : dense_delivery(desc->model, net->n_local)) &&
+                 net->ncls_kernel == 2;
+  }
+  const NetWsLayout wl = network_ws_layout(desc);
   char *ws = static_cast<char *>(desc->ws);
   net->counters = reinterpret_cast<unsigned long long *>(ws);
   net->count = reinterpret_cast<int32_t *>(ws + 64);
-  net->active[0] = reinterpret_cast<int32_t *>(ws + a0);
-  net->active[1] = reinterpret_cast<int32_t *>(ws + a1);
-  net->parity = 0;
+  net->active[0] = reinterpret_cast<int32_t *>(ws + wl.active0);
+  net->active[1] = reinterpret_cast<int32_t *>(ws + wl.active1);
+  net->spk[0] = desc->spikes;
+  if (wl.total > wl.spk1) net->spk[1] = reinterpret_cast<uint32_t *>(ws + wl.spk1);
   cudaStream_t st = as_stream(stream);
   cudaError_t e = cudaMemsetAsync(ws, 0, 256, st);
   if (e != cudaSuccess) {
@@ -1578,17 +1876,27 @@ bp_status bp_network_create(const bp_network_desc *desc, bp_stream stream,
   }
   net->neuron.spikes = desc->spikes + desc->col_begin / 32;
   net->neuron.active_base = static_cast<int32_t>(desc->col_begin);
-  net->conn = make_conn(net);
-  s = alloc_buckets(net, st);
-  // the local part of the initial spike vector (spikes_{-1}) is delivered
-  // into the first step; remote parts arrive through bp_network_scatter
+  std::vector<bp::NetProj> table;
+  net->conn = make_conn(net, &table);
+  s = alloc_buckets(net, table, st);
+  net->conn.proj = net->proj_dev;
+  if (s == BP_OK && desc->exchange == BP_EXCHANGE_NCCL) s = nccl_setup(net, st);
+  // spikes_{-1}: the local part is delivered into the first step; with the
+  // library's exchange the caller's initial vector is complete, so its
+  // remote part is binned here too; otherwise it arrives through
+  // bp_network_scatter
+  const int first_slot = (net->delay - 1) % net->slots;
   if (s == BP_OK)
-    s = bin_spike_range(net, desc->col_begin / 32, (desc->col_end + 31) / 32,
-                        (net->delay - 1) % net->slots, st);
+    s = bin_spike_range(net, desc->spikes, desc->col_begin / 32, (desc->col_end + 31) / 32,
+                        first_slot, st);
+  if (s == BP_OK && net->nccl && desc->world > 1)
+    s = bin_spike_range(net, desc->spikes, 0, net->global_words, first_slot, st,
+                        desc->col_begin / 32, (desc->col_end + 31) / 32);
   // one device, whole network, state fits one CTA's shared memory: the
   // single-CTA time loop (k_small_net) drives bp_network_step
   net->small = s == BP_OK && desc->col_begin == 0 && desc->col_end == desc->n &&
-               desc->n <= bp::kSmallMax && net->delay == 1 && !std::getenv("BP_NO_SMALL_NET");
+               desc->n <= bp::kSmallMax && net->delay == 1 && net->ncls_kernel == 2 &&
+               !net->nccl && !std::getenv("BP_NO_SMALL_NET");
   if (net->small) {
     launch_compact(desc->spikes, desc->n, net->small_active, net->small_count, sms, st);
     s = launched();
@@ -1600,8 +1908,6 @@ bp_status bp_network_create(const bp_network_desc *desc, bp_stream stream,
   *out = net;
   return BP_OK;
 }
-
-
 
 bp_status bp_network_step(bp_network *net, int64_t n_steps, uint32_t *raster_out,
                           int32_t *counts_out, bp_stream stream) {
@@ -1616,12 +1922,16 @@ bp_status bp_network_step(bp_network *net, int64_t n_steps, uint32_t *raster_out
       ev = net->prof_ev + 3 * net->prof_used++;
       net->prof_steps += 1;
     }
+    uint32_t *row = raster_out ? raster_out + k * net->local_words : nullptr;
     if (counts_out) BP_CUDA(cudaMemsetAsync(net->count + 1, 0, sizeof(int32_t), st));
-    if (ev) BP_CUDA(cudaEventRecord(ev[0], st));
-    s = launch_step(net, raster_out ? raster_out + k * net->local_words : nullptr, st,
-                    counts_out ? net->count + 1 : nullptr, ev ? ev[1] : nullptr);
+    if (net->nccl) {
+      s = nccl_step(net, row, counts_out ? net->count + 1 : nullptr, ev, st);
+    } else {
+      if (ev) BP_CUDA(cudaEventRecord(ev[0], st));
+      s = launch_step(net, row, st, counts_out ? net->count + 1 : nullptr, ev ? ev[1] : nullptr);
+      if (s == BP_OK && ev) BP_CUDA(cudaEventRecord(ev[2], st));
+    }
     if (s != BP_OK) return s;
-    if (ev) BP_CUDA(cudaEventRecord(ev[2], st));
     if (counts_out)
       BP_CUDA(cudaMemcpyAsync(counts_out + k, net->count + 1, sizeof(int32_t),
                               cudaMemcpyDefault, st));
@@ -1673,23 +1983,18 @@ bp_status bp_network_scatter(bp_network *net, bp_stream stream) {
   bp_status s = device_ready(nullptr);
   if (s != BP_OK) return s;
   BP_CHECK(net != nullptr, BP_ERR_INVALID_ARG, "net is NULL");
-  cudaStream_t st = as_stream(stream);
+  BP_CHECK(!net->nccl, BP_ERR_INVALID_ARG, "BP_EXCHANGE_NCCL networks run whole steps");
   // Deliver the spikes of the OTHER partitions (words outside this rank's
-  // slice) into the buckets the next bp_network_update consumes; local
-  // spikes were binned by the update that produced them.
-  const int64_t lw0 = net->d.col_begin / 32;
-  const int64_t lw1 = (net->d.col_end + 31) / 32;
-  // the exchanged spikes are those of step steps_done - 1: delivered at
-  // step steps_done - 1 + delay
-  const int slot = static_cast<int>((net->steps_done + net->delay - 1) % net->slots);
-  // one compaction + one binning launch for the words on both sides
-  return bin_spike_range(net, 0, net->global_words, slot, st, lw0, lw1);
+  // slice) of step steps_done - 1 into the buckets of their arrival step;
+  // local spikes were binned by the update that produced them.
+  return remote_scatter(net, net->steps_done - 1, as_stream(stream));
 }
 
 bp_status bp_network_update(bp_network *net, uint32_t *raster_row, bp_stream stream) {
   bp_status s = device_ready(nullptr);
   if (s != BP_OK) return s;
   BP_CHECK(net != nullptr, BP_ERR_INVALID_ARG, "net is NULL");
+  BP_CHECK(!net->nccl, BP_ERR_INVALID_ARG, "BP_EXCHANGE_NCCL networks run whole steps");
   return launch_step(net, raster_row, as_stream(stream));
 }
 
@@ -1698,6 +2003,7 @@ bp_status bp_network_update_overlap(bp_network *net, uint32_t *raster_row, bp_st
   bp_status s = device_ready(nullptr);
   if (s != BP_OK) return s;
   BP_CHECK(net != nullptr, BP_ERR_INVALID_ARG, "net is NULL");
+  BP_CHECK(!net->nccl, BP_ERR_INVALID_ARG, "BP_EXCHANGE_NCCL networks run whole steps");
   if (net->xev == nullptr) BP_CUDA(cudaEventCreateWithFlags(&net->xev, cudaEventDisableTiming));
   // k_step (spike words of this step) -> record xev -> local binning; the
   // exchange stream waits for xev only, so the all-gather overlaps k_bin
@@ -1712,6 +2018,9 @@ bp_status bp_network_counters(bp_network *net, uint64_t *host_out, bp_stream str
   if (s != BP_OK) return s;
   BP_CHECK(net != nullptr && host_out != nullptr, BP_ERR_INVALID_ARG, "NULL argument");
   cudaStream_t st = as_stream(stream);
+  if (net->nccl) {   // the comm stream's last gather is part of the state
+    BP_CUDA(cudaStreamWaitEvent(st, net->ev_gath[(net->steps_done + 1) & 1], 0));
+  }
   BP_CUDA(cudaMemcpyAsync(host_out, net->counters, 3 * sizeof(uint64_t),
                           cudaMemcpyDeviceToHost, st));
   BP_CUDA(cudaStreamSynchronize(st));
@@ -1719,10 +2028,17 @@ bp_status bp_network_counters(bp_network *net, uint64_t *host_out, bp_stream str
 }
 
 void bp_network_destroy(bp_network *net) {
-  if (net && net->xev) cudaEventDestroy(net->xev);
-  if (net && net->bk_mem) cudaFree(net->bk_mem);
-  if (net && net->small_steps) cudaFree(net->small_steps);
-  if (net && net->prof_ev) {
+  if (net == nullptr) return;
+  if (net->comm_st) cudaStreamSynchronize(net->comm_st);
+  if (net->comm) g_nccl.comm_destroy(net->comm);
+  if (net->comm_st) cudaStreamDestroy(net->comm_st);
+  if (net->ev_spk) cudaEventDestroy(net->ev_spk);
+  for (cudaEvent_t e : net->ev_gath)
+    if (e) cudaEventDestroy(e);
+  if (net->xev) cudaEventDestroy(net->xev);
+  if (net->bk_mem) cudaFree(net->bk_mem);
+  if (net->small_steps) cudaFree(net->small_steps);
+  if (net->prof_ev) {
     for (int64_t i = 0; i < 3 * net->prof_cap; ++i) cudaEventDestroy(net->prof_ev[i]);
     delete[] net->prof_ev;
   }

@@ -54,7 +54,15 @@ constexpr int kTile = 1 << kTileShift;   // postsynaptic neurons per tile/block
 #define BP_STEP_THREADS 256
 #endif
 constexpr int kStepThreads = BP_STEP_THREADS;   // LIF block size (4 neurons per thread per pass)
-constexpr uint32_t kProjBit = 0x80000000u;
+// Event records carry the WEIGHT CLASS of their projection in the top two
+// bits: projections that add the same homogeneous weight into the same
+// conductance share a class (one count array in k_step), projections with
+// other weights or receptors get their own.  At most kMaxCls classes.
+constexpr int kMaxProj = 8;        // projections per network (BP_MAX_PROJ)
+constexpr int kMaxCls = 4;         // weight classes
+constexpr int kClsShift = 30;
+constexpr uint32_t kClsMask = 3u << kClsShift;
+constexpr uint32_t kLocMask = (1u << kClsShift) - 1u;   // staged local index < 2^30
 
 // Per-tile bucket counters sit on their own 256-byte line: the 2M
 // slot-claiming atomics of a step then spread over all L2 slices instead of
@@ -64,7 +72,7 @@ constexpr int kCntStride = 64;
 struct Buckets {
   int32_t *cnt;      // [n_tiles * kCntStride], counter of tile t at t*kCntStride
   uint32_t *buf;     // [n_tiles][cap]
-  int32_t *spill;    // [2][n_local] dense event counts (E, I) on overflow
+  int32_t *spill;    // [n_cls][n_local] dense event counts per class on overflow
   int32_t *flag;     // [n_tiles] spill present
 };
 
@@ -75,100 +83,131 @@ struct BinTarget {
   uint32_t col_begin;
 };
 
-__device__ __forceinline__ uint32_t bin_record(uint32_t proj, uint32_t loc) {
-  return (proj ? kProjBit : 0u) | (loc & (kTile - 1));
+__device__ __forceinline__ uint32_t bin_record(uint32_t cls, uint32_t loc) {
+  return (cls << kClsShift) | (loc & (kTile - 1));
 }
 
-__device__ __forceinline__ void bin_store(const BinTarget &b, uint32_t proj,
+__device__ __forceinline__ void bin_store(const BinTarget &b, uint32_t cls,
                                           uint32_t loc, int slot) {
   const uint32_t tile = loc >> kTileShift;
   if (static_cast<uint32_t>(slot) < b.cap) {
-    b.out.buf[static_cast<size_t>(tile) * b.cap + slot] = bin_record(proj, loc);
+    b.out.buf[static_cast<size_t>(tile) * b.cap + slot] = bin_record(cls, loc);
   } else {
-    atomicAdd(b.out.spill + static_cast<size_t>(proj) * b.n_local + loc, 1);
+    atomicAdd(b.out.spill + static_cast<size_t>(cls) * b.n_local + loc, 1);
     b.out.flag[tile] = 1;
   }
 }
 
-// Append one event (projection proj, local postsynaptic index loc).
+// Append one event (weight class cls, local postsynaptic index loc).
 // Dense delivery (b.cap == 0): one atomic on the neuron's count.
-__device__ __forceinline__ void bin_event(const BinTarget &b, uint32_t proj,
+__device__ __forceinline__ void bin_event(const BinTarget &b, uint32_t cls,
                                           uint32_t loc) {
   if (b.cap == 0) {
-    atomicAdd(b.out.spill + static_cast<size_t>(proj) * b.n_local + loc, 1);
+    atomicAdd(b.out.spill + static_cast<size_t>(cls) * b.n_local + loc, 1);
     return;
   }
   const int slot = atomicAdd(b.out.cnt + (loc >> kTileShift) * kCntStride, 1);
-  bin_store(b, proj, loc, slot);
+  bin_store(b, cls, loc, slot);
 }
 
+// One projection of a network (include/bp.h bp_projection), device view.
+// The table lives in device memory (a runtime index into the kernel
+// parameters would copy them to local memory); a row's projection is
+// loaded once per row.
+struct NetProj {
+  uint32_t pre_begin, pre_end;  // presynaptic rows = global neurons [pre_begin, pre_end)
+  int32_t conn;                 // BP_CONN_JIT / BP_CONN_CSR
+  uint32_t cls;                 // weight class of its events
+  JitSide j;                    // JIT: seed, K, L, local segments
+  CsrSide c;                    // CSR: column-sliced rows, indices local
+};
+
 struct ConnArgs {
-  int conn;                 // BP_CONN_JIT / BP_CONN_CSR (uniform per launch)
-  JitSide je, ji;           // JIT: seed, K, L, local segments
-  CsrSide ce, ci;           // CSR: column-sliced rows, indices local
-  int64_t split;            // n_exc: rows >= split belong to projection I
-  uint32_t n_cols;          // all neurons (columns of both projections)
+  const NetProj *proj;      // device table [n_proj]
+  int n_proj;
+  int all_jit;              // every projection is JIT (the warp-batched path)
+  uint32_t n_cols;          // all neurons (columns of every projection)
   int lane_rows;            // JIT fan-out per segment small: one lane per row
 };
 
+__device__ __forceinline__ bool proj_has(const NetProj *P, int64_t r, uint32_t &row) {
+  const uint32_t lo = __ldg(&P->pre_begin), hi = __ldg(&P->pre_end);
+  row = static_cast<uint32_t>(r) - lo;
+  return static_cast<uint32_t>(r) >= lo && static_cast<uint32_t>(r) < hi;
+}
+
+__device__ __forceinline__ JitSide load_jit(const NetProj *P) {
+  JitSide s;
+  s.seed = __ldg(&P->j.seed);
+  s.K = __ldg(&P->j.K);
+  s.L = __ldg(&P->j.L);
+  s.seg_first = __ldg(&P->j.seg_first);
+  s.n_seg = __ldg(&P->j.n_seg);
+  return s;
+}
+
 // Regenerate (JIT) or read (CSR) the local targets of presynaptic neuron r
-// (global id) and bin them.  Called by a whole warp (warp-uniform r).
-// Returns the number of events this lane binned.
+// (global id) in every projection it belongs to and bin them.  Called by a
+// whole warp (warp-uniform r).  Returns the number of events this lane binned.
 __device__ __forceinline__ uint32_t deliver_row(const ConnArgs &c, const BinTarget &b,
                                                 int64_t r) {
   const uint32_t lane = threadIdx.x & 31u;
-  const bool inh = r >= c.split;
-  const uint32_t proj = inh ? 1u : 0u;
-  const int64_t row64 = inh ? r - c.split : r;
   uint32_t ev = 0;
-  if (c.conn == 1) {
-    const CsrSide s = pick(inh, c.ce, c.ci);
-    const int64_t begin = __ldg(s.indptr + row64), end = __ldg(s.indptr + row64 + 1);
-    for (int64_t j = begin + lane; j < end; j += 32) {
-      bin_event(b, proj, static_cast<uint32_t>(__ldg(s.indices + j)));
-      ++ev;
+  for (int p = 0; p < c.n_proj; ++p) {
+    const NetProj *P = c.proj + p;
+    uint32_t row;
+    if (!proj_has(P, r, row)) continue;
+    const uint32_t cls = __ldg(&P->cls);
+    if (__ldg(&P->conn) == 1) {
+      const int64_t *indptr = P->c.indptr;
+      const int32_t *indices = P->c.indices;
+      const int64_t begin = __ldg(indptr + row), end = __ldg(indptr + row + 1);
+      for (int64_t j = begin + lane; j < end; j += 32) {
+        bin_event(b, cls, static_cast<uint32_t>(__ldg(indices + j)));
+        ++ev;
+      }
+      continue;
     }
-    return ev;
-  }
-  const JitSide s = pick(inh, c.je, c.ji);
-  const uint32_t row = static_cast<uint32_t>(row64);
-  for (uint32_t sidx = 0; sidx < s.n_seg; ++sidx) {
-    const uint32_t seg = s.seg_first + sidx;
-    const uint32_t seg_begin = seg * s.L;
-    const uint32_t seg_end = min(seg_begin + s.L, c.n_cols);
-    u32x4 g = philox_block(s.seed, kTagGap, row, seg, lane);
-    uint32_t start = seg_begin + first_offset(s.seed, s.K, row, seg);
-    uint32_t chunk = 0;
-    while (start < seg_end) {                      // warp-uniform
-      const uint32_t g0 = bounded(1u, s.K, g.x), g1 = bounded(1u, s.K, g.y);
-      const uint32_t g2 = bounded(1u, s.K, g.z), g3 = bounded(1u, s.K, g.w);
-      const uint32_t p1 = g0, p2 = g0 + g1, p3 = p2 + g2, t = p3 + g3;
-      uint32_t incl = t;
+    const JitSide s = load_jit(P);
+    for (uint32_t sidx = 0; sidx < s.n_seg; ++sidx) {
+      const uint32_t seg = s.seg_first + sidx;
+      const uint32_t seg_begin = seg * s.L;
+      const uint32_t seg_end = min(seg_begin + s.L, c.n_cols);
+      u32x4 g = philox_block(s.seed, kTagGap, row, seg, lane);
+      uint32_t start = seg_begin + first_offset(s.seed, s.K, row, seg);
+      uint32_t chunk = 0;
+      while (start < seg_end) {                      // warp-uniform
+        const uint32_t g0 = bounded(1u, s.K, g.x), g1 = bounded(1u, s.K, g.y);
+        const uint32_t g2 = bounded(1u, s.K, g.z), g3 = bounded(1u, s.K, g.w);
+        const uint32_t p1 = g0, p2 = g0 + g1, p3 = p2 + g2, t = p3 + g3;
+        uint32_t incl = t;
 #pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= static_cast<uint32_t>(off)) incl += v;
-      }
-      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-      const uint32_t pos0 = start + (incl - t);
-      const uint32_t pos[4] = {pos0, pos0 + p1, pos0 + p2, pos0 + p3};
-      // claim all slots first so the four atomics are in flight together
-      int slot[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        slot[k] = pos[k] < seg_end
-                      ? atomicAdd(b.out.cnt + ((pos[k] - b.col_begin) >> kTileShift) * kCntStride, 1)
-                      : 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (pos[k] < seg_end) {
-          bin_store(b, proj, pos[k] - b.col_begin, slot[k]);
-          ++ev;
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= static_cast<uint32_t>(off)) incl += v;
         }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        const uint32_t pos0 = start + (incl - t);
+        const uint32_t pos[4] = {pos0, pos0 + p1, pos0 + p2, pos0 + p3};
+        // claim all slots first so the four atomics are in flight together
+        int slot[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          slot[k] = (pos[k] < seg_end && b.cap)
+                        ? atomicAdd(b.out.cnt + ((pos[k] - b.col_begin) >> kTileShift) * kCntStride, 1)
+                        : 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (pos[k] < seg_end) {
+            if (b.cap) bin_store(b, cls, pos[k] - b.col_begin, slot[k]);
+            else bin_event(b, cls, pos[k] - b.col_begin);
+            ++ev;
+          }
+        }
+        start += total;
+        ++chunk;
+        if (start < seg_end) g = philox_block(s.seed, kTagGap, row, seg, chunk * 32u + lane);
       }
-      start += total;
-      ++chunk;
-      if (start < seg_end) g = philox_block(s.seed, kTagGap, row, seg, chunk * 32u + lane);
     }
   }
   return ev;
@@ -177,9 +216,11 @@ __device__ __forceinline__ uint32_t deliver_row(const ConnArgs &c, const BinTarg
 struct StepArgs {
   NeuronArgs nrn;           // params, local state, n = n_local, spikes/raster words
   int model;                // BP_MODEL_LIF / BP_MODEL_HH
-  ConnArgs conn;
-  float w_e, w_i;           // homogeneous weights (fp32 mode)
-  long long q_e, q_i;       // quantised weights (fixed point: 2^32 or 2^F scale)
+  int n_cls;                // weight classes in use (<= NCLS of the kernel)
+  float w[kMaxCls];         // class weight (fp32 mode, one class per receptor)
+  long long q[kMaxCls];     // class weight quantised: 2^32 (fix64, multi-class fp32) or
+                            // 2^F (fix32); 0 for unused classes
+  int rec[kMaxCls];         // class receptor: 0 -> g_e, 1 -> g_i
   unsigned long long *saturated;   // rule F2 saturations
   Buckets in;               // events for this step (consumed, then cleared)
   BinTarget out;            // events for the next step
@@ -275,6 +316,74 @@ __device__ __forceinline__ void g_after(float &g, double, float a32) {
   g = __fmul_rn(g, a32);
 }
 
+// Several weight classes into one conductance (AlignPost merging):
+// the step's increment is the exact sum S = sum_c cnt_c q_c (int64).
+//   fixed point (F1): g += S;  F2: g += S with saturation;
+//   fp32 (rule N1-f32): g = fl32(g + fl32(S 2^-32)) -- the exactly rounded
+//   sum of the increments (the host requires every w = q 2^-32 exactly).
+__device__ __forceinline__ float g_add(long long &g, long long S) {
+  g += S;
+  return __double2float_rn(__dmul_rn(__ll2double_rn(g), 0x1p-32));
+}
+__device__ __forceinline__ float g_add32(int32_t &g, long long S, float inv_scale,
+                                         uint32_t &sat) {
+  const long long v = static_cast<long long>(g) + S;
+  const long long c = v > 2147483647ll ? 2147483647ll : (v < -2147483648ll ? -2147483648ll : v);
+  sat += c != v;
+  g = static_cast<int32_t>(c);
+  return fix32_read(g, inv_scale);
+}
+__device__ __forceinline__ float g_add(float &g, long long S) {
+  if (S) g = __fadd_rn(g, __fmul_rn(__ll2float_rn(S), 0x1p-32f));
+  return g;
+}
+
+// Fold the counts of neuron j (class c at cnt[c * stride + j]) into its two
+// conductances, return the values the neuron reads (gEf, gIf) and leave the
+// pre-decayed state in ge / gi.  NCLS == 2: class 0 -> g_e, class 1 -> g_i,
+// one class per receptor (Listing S3's network); else the general merge.
+template <int KIND, int NCLS, typename G>
+__device__ __forceinline__ void fold_pair(const StepArgs &a, G &ge, G &gi, const int32_t *cnt,
+                                          int stride, int j, uint32_t &sat, float &gEf,
+                                          float &gIf) {
+  const NeuronArgs &nr = a.nrn;
+  if constexpr (NCLS == 2) {
+    const int32_t ce = cnt[j], ci = cnt[stride + j];
+    if constexpr (KIND == 2) {
+      gEf = g_fold32(ge, ce, a.q[0], nr.inv_scale32, sat);
+      gIf = g_fold32(gi, ci, a.q[1], nr.inv_scale32, sat);
+    } else if constexpr (KIND == 1) {
+      gEf = g_fold(ge, ce, a.q[0]);
+      gIf = g_fold(gi, ci, a.q[1]);
+    } else {
+      gEf = g_fold(ge, ce, a.w[0]);
+      gIf = g_fold(gi, ci, a.w[1]);
+    }
+  } else {
+    long long se = 0, si = 0;
+#pragma unroll
+    for (int c = 0; c < NCLS; ++c) {
+      const long long t = static_cast<long long>(cnt[c * stride + j]) * a.q[c];
+      if (a.rec[c]) si += t;
+      else se += t;
+    }
+    if constexpr (KIND == 2) {
+      gEf = g_add32(ge, se, nr.inv_scale32, sat);
+      gIf = g_add32(gi, si, nr.inv_scale32, sat);
+    } else {
+      gEf = g_add(ge, se);
+      gIf = g_add(gi, si);
+    }
+  }
+  if constexpr (KIND == 2) {
+    g_after32(ge, nr.a_e_q);
+    g_after32(gi, nr.a_i_q);
+  } else {
+    g_after(ge, nr.alpha_e, nr.alpha_e32);
+    g_after(gi, nr.alpha_i, nr.alpha_i32);
+  }
+}
+
 // One LIF neuron (rule N1); returns spike.
 __device__ __forceinline__ bool lif_one(const NeuronArgs &a, float &V, uint32_t &ref,
                                         float gE, float gI) {
@@ -364,9 +473,9 @@ __device__ __forceinline__ void pass_load(Pass<MODEL, KIND> &p, const NeuronArgs
 
 // Update the 4 neurons of pass p (offset j0 in the tile, local index i0);
 // returns their spike nibble.
-template <int MODEL, int KIND>
+template <int MODEL, int KIND, int NCLS>
 __device__ __forceinline__ uint32_t pass_update(Pass<MODEL, KIND> &p, const StepArgs &a,
-                                                const int32_t *cnt_e, const int32_t *cnt_i,
+                                                const int32_t *cnt, int stride,
                                                 int j0, int64_t i0, const Policies &pol,
                                                 uint32_t &sat) {
   const NeuronArgs &nr = a.nrn;
@@ -375,25 +484,8 @@ __device__ __forceinline__ uint32_t pass_update(Pass<MODEL, KIND> &p, const Step
   if (p.full) {
     float gEf[4], gIf[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if constexpr (KIND == 2) {
-        gEf[q] = g_fold32(p.ge.v[q], cnt_e[j0 + q], a.q_e, nr.inv_scale32, sat);
-        gIf[q] = g_fold32(p.gi.v[q], cnt_i[j0 + q], a.q_i, nr.inv_scale32, sat);
-      } else if constexpr (KIND == 1) {
-        gEf[q] = g_fold(p.ge.v[q], cnt_e[j0 + q], a.q_e);
-        gIf[q] = g_fold(p.gi.v[q], cnt_i[j0 + q], a.q_i);
-      } else {
-        gEf[q] = g_fold(p.ge.v[q], cnt_e[j0 + q], a.w_e);
-        gIf[q] = g_fold(p.gi.v[q], cnt_i[j0 + q], a.w_i);
-      }
-      if constexpr (KIND == 2) {
-        g_after32(p.ge.v[q], nr.a_e_q);
-        g_after32(p.gi.v[q], nr.a_i_q);
-      } else {
-        g_after(p.ge.v[q], nr.alpha_e, nr.alpha_e32);
-        g_after(p.gi.v[q], nr.alpha_i, nr.alpha_i32);
-      }
-    }
+    for (int q = 0; q < 4; ++q)
+      fold_pair<KIND, NCLS>(a, p.ge.v[q], p.gi.v[q], cnt, stride, j0 + q, sat, gEf[q], gIf[q]);
     float V[4] = {p.V.x, p.V.y, p.V.z, p.V.w};
     if constexpr (MODEL == 0) {
       uint32_t Rn = 0;
@@ -425,37 +517,14 @@ __device__ __forceinline__ uint32_t pass_update(Pass<MODEL, KIND> &p, const Step
   for (int q = 0; q < 4 && i0 + q < nr.n; ++q) {
     const int64_t i = i0 + q;
     float gEf, gIf;
-    if constexpr (KIND == 2) {
-      int32_t *pe = static_cast<int32_t *>(nr.g_e) + i;
-      int32_t *pi = static_cast<int32_t *>(nr.g_i) + i;
-      int32_t ge = *pe, gi = *pi;
-      gEf = g_fold32(ge, cnt_e[j0 + q], a.q_e, nr.inv_scale32, sat);
-      gIf = g_fold32(gi, cnt_i[j0 + q], a.q_i, nr.inv_scale32, sat);
-      g_after32(ge, nr.a_e_q);
-      g_after32(gi, nr.a_i_q);
-      *pe = ge;
-      *pi = gi;
-    } else if constexpr (KIND == 1) {
-      long long *pe = static_cast<long long *>(nr.g_e) + i;
-      long long *pi = static_cast<long long *>(nr.g_i) + i;
-      long long ge = *pe, gi = *pi;
-      gEf = g_fold(ge, cnt_e[j0 + q], a.q_e);
-      gIf = g_fold(gi, cnt_i[j0 + q], a.q_i);
-      g_after(ge, nr.alpha_e, 0.f);
-      g_after(gi, nr.alpha_i, 0.f);
-      *pe = ge;
-      *pi = gi;
-    } else {
-      float *pe = static_cast<float *>(nr.g_e) + i;
-      float *pi = static_cast<float *>(nr.g_i) + i;
-      float ge = *pe, gi = *pi;
-      gEf = g_fold(ge, cnt_e[j0 + q], a.w_e);
-      gIf = g_fold(gi, cnt_i[j0 + q], a.w_i);
-      g_after(ge, 0.0, nr.alpha_e32);
-      g_after(gi, 0.0, nr.alpha_i32);
-      *pe = ge;
-      *pi = gi;
-    }
+    using G = typename std::conditional<KIND == 1, long long,
+                                        typename std::conditional<KIND == 2, int32_t, float>::type>::type;
+    G *pe = static_cast<G *>(nr.g_e) + i;
+    G *pi = static_cast<G *>(nr.g_i) + i;
+    G ge = *pe, gi = *pi;
+    fold_pair<KIND, NCLS>(a, ge, gi, cnt, stride, j0 + q, sat, gEf, gIf);
+    *pe = ge;
+    *pi = gi;
     float V = nr.v[i];
     if constexpr (MODEL == 0) {
       uint32_t r = nr.ref[i];
@@ -517,14 +586,15 @@ __device__ __forceinline__ void pass_emit(const StepArgs &a, uint32_t nib, int64
 // 0 and 1 compute (register double buffering).
 // LIF (memory-bound): 256 threads, 4 passes, register double buffering.
 // HH (FP32-latency-bound): 512 threads, 2 passes (more warps, 128 registers).
-template <int MODEL, int KIND>
+// NCLS count arrays of kTile int32 in dynamic shared memory (2: 32 KB,
+// Listing S3's E + I; 4: 64 KB, merged projections with several weights).
+template <int MODEL, int KIND, int NCLS>
 #ifndef BP_STEP_MINB
 #define BP_STEP_MINB (1024 / BP_STEP_THREADS)
 #endif
 __global__ void __launch_bounds__(MODEL == 0 ? kStepThreads : 512, MODEL == 0 ? BP_STEP_MINB : 1)
 k_step(StepArgs a) {
-  __shared__ int32_t cnt_e[kTile];
-  __shared__ int32_t cnt_i[kTile];
+  extern __shared__ int32_t cnt[];          // [NCLS][kTile]
   __shared__ unsigned long long block_sp;
   const int tid = threadIdx.x;
   constexpr int nthreads = MODEL == 0 ? kStepThreads : 512;
@@ -542,24 +612,24 @@ k_step(StepArgs a) {
   pass_load(pa, nr, base + 4 * tid, pol);
   pass_load(pb, nr, base + pstride + 4 * tid, pol);
 
-  // 1. count this tile's incoming events (bucket + rare spill)
-  for (int j = tid; j < kTile; j += nthreads) { cnt_e[j] = 0; cnt_i[j] = 0; }
+  // 1. count this tile's incoming events per weight class (bucket + rare spill)
+  for (int j = tid; j < NCLS * kTile; j += nthreads) cnt[j] = 0;
   if (tid == 0) block_sp = 0;
   __syncthreads();
   const int32_t n_in = min(static_cast<uint32_t>(a.in.cnt[tile * kCntStride]), a.out.cap);
   const uint32_t *buf = a.in.buf + static_cast<size_t>(tile) * a.out.cap;
   for (int k = tid; k < n_in; k += nthreads) {
     const uint32_t e = __ldcs(buf + k);
-    atomicAdd((e & kProjBit) ? &cnt_i[e & (kTile - 1)] : &cnt_e[e & (kTile - 1)], 1);
+    atomicAdd(&cnt[(e >> kClsShift) * kTile + (e & (kTile - 1))], 1);
   }
   if (a.in.flag[tile]) {                       // overflow spill (exact, rare)
     for (int j = tid; j < kTile && base + j < nr.n; j += nthreads) {
-      int32_t *se = a.in.spill + base + j;
-      int32_t *si = a.in.spill + a.out.n_local + base + j;
-      atomicAdd(&cnt_e[j], *se);
-      atomicAdd(&cnt_i[j], *si);
-      *se = 0;
-      *si = 0;
+#pragma unroll
+      for (int c = 0; c < NCLS; ++c) {
+        int32_t *sp = a.in.spill + static_cast<size_t>(c) * a.out.n_local + base + j;
+        atomicAdd(&cnt[c * kTile + j], *sp);
+        *sp = 0;
+      }
     }
   }
   __syncthreads();
@@ -575,8 +645,8 @@ k_step(StepArgs a) {
   for (int p = 0; p < passes; ++p) {
     Pass<MODEL, KIND> &cur = (p & 1) ? pb : pa;
     const int off = p * pstride;
-    const uint32_t nib = pass_update(cur, a, cnt_e, cnt_i, off + 4 * tid, base + off + 4 * tid, pol,
-                                     sat);
+    const uint32_t nib = pass_update<MODEL, KIND, NCLS>(cur, a, cnt, kTile, off + 4 * tid,
+                                                        base + off + 4 * tid, pol, sat);
     if (p + 2 < passes) pass_load(cur, nr, base + off + 2 * pstride + 4 * tid, pol);
     pass_emit(a, nib, base, off, my_sp);
   }
@@ -603,8 +673,7 @@ constexpr int kDenseThreads = 128;
 template <int MODEL, int KIND>
 __global__ void __launch_bounds__(kDenseThreads, MODEL == 0 ? 8 : 4)
 k_step_dense(StepArgs a) {
-  __shared__ int32_t cnt_e[4 * kDenseThreads];
-  __shared__ int32_t cnt_i[4 * kDenseThreads];
+  __shared__ int32_t cnt[2 * 4 * kDenseThreads];   // class 0 (E), class 1 (I)
   __shared__ unsigned long long block_sp;
   const int tid = threadIdx.x;
   const uint32_t lane = tid & 31u;
@@ -630,12 +699,13 @@ k_step_dense(StepArgs a) {
       if (ce) *se = 0;
       if (ci) *si = 0;
     }
-    cnt_e[j] = ce;
-    cnt_i[j] = ci;
+    cnt[j] = ce;
+    cnt[4 * kDenseThreads + j] = ci;
   }
   __syncthreads();
   uint32_t my_sp = 0, sat = 0;
-  const uint32_t nib = pass_update(pa, a, cnt_e, cnt_i, 4 * tid, base + 4 * tid, pol, sat);
+  const uint32_t nib = pass_update<MODEL, KIND, 2>(pa, a, cnt, 4 * kDenseThreads, 4 * tid,
+                                                   base + 4 * tid, pol, sat);
   pass_emit(a, nib, base, 0, my_sp);
   if (KIND == 2 && sat) atomicAdd(a.saturated, static_cast<unsigned long long>(sat));
   my_sp = __reduce_add_sync(0xffffffffu, my_sp);
@@ -663,37 +733,15 @@ __device__ __forceinline__ bool hh_dense_one(const StepArgs &a, int64_t i, uint3
   if (ce) *se = 0;
   if (ci) *si = 0;
   float gEf, gIf;
-  if constexpr (KIND == 2) {
-    int32_t *pe = static_cast<int32_t *>(nr.g_e) + i;
-    int32_t *pi = static_cast<int32_t *>(nr.g_i) + i;
-    int32_t ge = *pe, gi = *pi;
-    gEf = g_fold32(ge, ce, a.q_e, nr.inv_scale32, sat);
-    gIf = g_fold32(gi, ci, a.q_i, nr.inv_scale32, sat);
-    g_after32(ge, nr.a_e_q);
-    g_after32(gi, nr.a_i_q);
-    *pe = ge;
-    *pi = gi;
-  } else if constexpr (KIND == 1) {
-    long long *pe = static_cast<long long *>(nr.g_e) + i;
-    long long *pi = static_cast<long long *>(nr.g_i) + i;
-    long long ge = *pe, gi = *pi;
-    gEf = g_fold(ge, ce, a.q_e);
-    gIf = g_fold(gi, ci, a.q_i);
-    g_after(ge, nr.alpha_e, 0.f);
-    g_after(gi, nr.alpha_i, 0.f);
-    *pe = ge;
-    *pi = gi;
-  } else {
-    float *pe = static_cast<float *>(nr.g_e) + i;
-    float *pi = static_cast<float *>(nr.g_i) + i;
-    float ge = *pe, gi = *pi;
-    gEf = g_fold(ge, ce, a.w_e);
-    gIf = g_fold(gi, ci, a.w_i);
-    g_after(ge, 0.0, nr.alpha_e32);
-    g_after(gi, 0.0, nr.alpha_i32);
-    *pe = ge;
-    *pi = gi;
-  }
+  using G = typename std::conditional<KIND == 1, long long,
+                                      typename std::conditional<KIND == 2, int32_t, float>::type>::type;
+  G *pe = static_cast<G *>(nr.g_e) + i;
+  G *pi = static_cast<G *>(nr.g_i) + i;
+  G ge = *pe, gi = *pi;
+  const int32_t cnt2[2] = {ce, ci};
+  fold_pair<KIND, 2>(a, ge, gi, cnt2, 1, 0, sat, gEf, gIf);
+  *pe = ge;
+  *pi = gi;
   float V = nr.v[i], M = nr.m[i], H = nr.h[i], Nk = nr.nk[i];
   const bool spike = hh_one(nr, V, M, H, Nk, gEf, gIf);
   nr.v[i] = V;
@@ -792,140 +840,85 @@ __device__ unsigned long long g_bin_t[1024][6];
 #define BP_BIN_MARK(k) do {} while (0)
 #endif
 
-__device__ __forceinline__ uint32_t stage_record(uint32_t proj, uint32_t loc) {
-  return (proj ? kProjBit : 0u) | loc;    // loc < 2^31
+__device__ __forceinline__ uint32_t stage_record(uint32_t cls, uint32_t loc) {
+  return (cls << kClsShift) | loc;    // loc < 2^30
 }
 
-// Generate the local targets of row r into the block's staging area (or the
-// global per-event path when it is full).  Whole warp, warp-uniform r.
+// Stage up to 4 locs per lane (valid[k]) through one warp-wide slot claim;
+// events past the staging area take the per-event path.  Whole warp.
+__device__ __forceinline__ uint32_t stage_emit4(const BinTarget &b, uint32_t cls,
+                                                const uint32_t *loc, const bool *valid,
+                                                uint32_t *staged, int32_t *n_staged,
+                                                int32_t *hist) {
+  const uint32_t lane = threadIdx.x & 31u;
+  uint32_t mine = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) mine += valid[k];
+  uint32_t incl = mine;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= static_cast<uint32_t>(off)) incl += v;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  if (total == 0) return 0;
+  int base = 0;
+  if (lane == 31) base = atomicAdd(n_staged, static_cast<int>(total));
+  base = __shfl_sync(0xffffffffu, base, 31);
+  int slot = base + static_cast<int>(incl - mine);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (!valid[k]) continue;
+    if (slot < kBinStage) {
+      staged[slot] = stage_record(cls, loc[k]);
+      atomicAdd(hist + (loc[k] >> kTileShift), 1);
+    } else {
+      bin_event(b, cls, loc[k]);
+    }
+    ++slot;
+  }
+  return mine;
+}
+
+// Generate the local targets of row r (global id) in every projection it
+// belongs to into the block's staging area (or the global per-event path
+// when it is full).  Whole warp, warp-uniform r.  Any mix of CSR and JIT.
 __device__ __forceinline__ uint32_t stage_row(const ConnArgs &c, const BinTarget &b, int64_t r,
                                               uint32_t *staged, int32_t *n_staged,
                                               int32_t *hist) {
   const uint32_t lane = threadIdx.x & 31u;
-  const bool inh = r >= c.split;
-  const uint32_t proj = inh ? 1u : 0u;
-  const int64_t row64 = inh ? r - c.split : r;
   uint32_t ev = 0;
-  // emit up to 4 locs per lane (valid[k]) through one warp-wide slot claim
-  auto emit = [&](const uint32_t *loc, const bool *valid) {
-    uint32_t mine = 0;
+  for (int p = 0; p < c.n_proj; ++p) {
+    const NetProj *P = c.proj + p;
+    uint32_t row;
+    if (!proj_has(P, r, row)) continue;
+    const uint32_t cls = __ldg(&P->cls);
+    if (__ldg(&P->conn) == 1) {
+      const int64_t *indptr = P->c.indptr;
+      const int32_t *indices = P->c.indices;
+      const int64_t begin = __ldg(indptr + row), end = __ldg(indptr + row + 1);
+      for (int64_t j0 = begin; j0 < end; j0 += 128) {
+        uint32_t loc[4];
+        bool valid[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) mine += valid[k];
-    uint32_t incl = mine;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
-      if (lane >= static_cast<uint32_t>(off)) incl += v;
-    }
-    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-    if (total == 0) return;
-    int base = 0;
-    if (lane == 31) base = atomicAdd(n_staged, static_cast<int>(total));
-    base = __shfl_sync(0xffffffffu, base, 31);
-    int slot = base + static_cast<int>(incl - mine);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (!valid[k]) continue;
-      if (slot < kBinStage) {
-        staged[slot] = stage_record(proj, loc[k]);
-        atomicAdd(hist + (loc[k] >> kTileShift), 1);
-      } else {
-        bin_event(b, proj, loc[k]);
+        for (int k = 0; k < 4; ++k) {
+          const int64_t j = j0 + k * 32 + lane;
+          valid[k] = j < end;
+          loc[k] = valid[k] ? static_cast<uint32_t>(__ldg(indices + j)) : 0u;
+        }
+        ev += stage_emit4(b, cls, loc, valid, staged, n_staged, hist);
       }
-      ++slot;
-      ++ev;
+      continue;
     }
-  };
-  if (c.conn == 1) {
-    const CsrSide s = pick(inh, c.ce, c.ci);
-    const int64_t begin = __ldg(s.indptr + row64), end = __ldg(s.indptr + row64 + 1);
-    for (int64_t j0 = begin; j0 < end; j0 += 128) {
-      uint32_t loc[4];
-      bool valid[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int64_t j = j0 + k * 32 + lane;
-        valid[k] = j < end;
-        loc[k] = valid[k] ? static_cast<uint32_t>(__ldg(s.indices + j)) : 0u;
-      }
-      emit(loc, valid);
-    }
-    return ev;
-  }
-  const JitSide s = pick(inh, c.je, c.ji);
-  const uint32_t row = static_cast<uint32_t>(row64);
-  for (uint32_t sidx = 0; sidx < s.n_seg; ++sidx) {
-    const uint32_t seg = s.seg_first + sidx;
-    const uint32_t seg_begin = seg * s.L;
-    const uint32_t seg_end = min(seg_begin + s.L, c.n_cols);
-    u32x4 g = philox_block(s.seed, kTagGap, row, seg, lane);
-    uint32_t start = seg_begin + first_offset(s.seed, s.K, row, seg);
-    uint32_t chunk = 0;
-    while (start < seg_end) {                      // warp-uniform
-      const uint32_t g0 = bounded(1u, s.K, g.x), g1 = bounded(1u, s.K, g.y);
-      const uint32_t g2 = bounded(1u, s.K, g.z), g3 = bounded(1u, s.K, g.w);
-      const uint32_t p1 = g0, p2 = g0 + g1, p3 = p2 + g2, t = p3 + g3;
-      uint32_t incl = t;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= static_cast<uint32_t>(off)) incl += v;
-      }
-      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-      const uint32_t pos0 = start + (incl - t);
-      const uint32_t pos[4] = {pos0, pos0 + p1, pos0 + p2, pos0 + p3};
-      uint32_t loc[4];
-      bool valid[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        valid[k] = pos[k] < seg_end;
-        loc[k] = pos[k] - b.col_begin;
-      }
-      emit(loc, valid);
-      start += total;
-      ++chunk;
-      if (start < seg_end) g = philox_block(s.seed, kTagGap, row, seg, chunk * 32u + lane);
-    }
-  }
-  return ev;
-}
-
-// JIT rows active[k0 + 32 i] (i < 32, k0 + 32 i < k_end) for one warp.  Lane l first
-// computes the stationary first offset of row k0+l (one Philox per lane
-// instead of one per row), then the warp walks the rows one by one: one
-// Philox block of 4 gaps per lane per chunk of 128 gaps.  Positions grow
-// with (lane, k), so the valid events are a prefix of that order and their
-// staging slots follow from four ballots -- no second scan.
-__device__ __forceinline__ uint32_t stage_rows_jit(const ConnArgs &c, const BinTarget &b,
-                                                   const int32_t *active, int k0, int k_end,
-                                                   uint32_t *staged, int32_t *n_staged,
-                                                   int32_t *hist) {
-  const uint32_t lane = threadIdx.x & 31u;
-  // rows k0, k0 + 32, k0 + 64, ... (stride = warps per block)
-  const int nrows = min(32, (k_end - k0 + 31) / 32);
-  const int64_t r_l = lane < static_cast<uint32_t>(nrows) ? active[k0 + 32 * lane] : 0;
-  const bool inh_l = r_l >= c.split;
-  const uint32_t row_l = static_cast<uint32_t>(inh_l ? r_l - c.split : r_l);
-  const uint32_t n_seg_max = max(c.je.n_seg, c.ji.n_seg);
-  uint32_t ev = 0;
-  for (uint32_t sidx = 0; sidx < n_seg_max; ++sidx) {
-    // lane-parallel first offsets of the 32 rows in this segment
-    const JitSide sl = pick(inh_l, c.je, c.ji);
-    uint32_t first_l = 0;
-    if (lane < static_cast<uint32_t>(nrows) && sidx < sl.n_seg)
-      first_l = (sl.seg_first + sidx) * sl.L + first_offset(sl.seed, sl.K, row_l, sl.seg_first + sidx);
-    for (int j = 0; j < nrows; ++j) {
-      const bool inh = __shfl_sync(0xffffffffu, static_cast<int>(inh_l), j) != 0;
-      const JitSide s = pick(inh, c.je, c.ji);
-      if (sidx >= s.n_seg) continue;                       // warp-uniform
-      const uint32_t row = __shfl_sync(0xffffffffu, row_l, j);
-      const uint32_t proj = inh ? 1u : 0u;
+    const JitSide s = load_jit(P);
+    for (uint32_t sidx = 0; sidx < s.n_seg; ++sidx) {
       const uint32_t seg = s.seg_first + sidx;
-      const uint32_t seg_end = min(seg * s.L + s.L, c.n_cols);
-      uint32_t start = __shfl_sync(0xffffffffu, first_l, j);
+      const uint32_t seg_begin = seg * s.L;
+      const uint32_t seg_end = min(seg_begin + s.L, c.n_cols);
+      u32x4 g = philox_block(s.seed, kTagGap, row, seg, lane);
+      uint32_t start = seg_begin + first_offset(s.seed, s.K, row, seg);
       uint32_t chunk = 0;
-      while (start < seg_end) {                            // warp-uniform
-        const u32x4 g = philox_block(s.seed, kTagGap, row, seg, chunk * 32u + lane);
+      while (start < seg_end) {                      // warp-uniform
         const uint32_t g0 = bounded(1u, s.K, g.x), g1 = bounded(1u, s.K, g.y);
         const uint32_t g2 = bounded(1u, s.K, g.z), g3 = bounded(1u, s.K, g.w);
         const uint32_t p1 = g0, p2 = g0 + g1, p3 = p2 + g2, t = p3 + g3;
@@ -938,43 +931,111 @@ __device__ __forceinline__ uint32_t stage_rows_jit(const ConnArgs &c, const BinT
         const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
         const uint32_t pos0 = start + (incl - t);
         const uint32_t pos[4] = {pos0, pos0 + p1, pos0 + p2, pos0 + p3};
-        bool v[4];
-        uint32_t n_valid = 0;
+        uint32_t loc[4];
+        bool valid[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          v[k] = pos[k] < seg_end;
-          n_valid += __popc(__ballot_sync(0xffffffffu, v[k]));
+          valid[k] = pos[k] < seg_end;
+          loc[k] = pos[k] - b.col_begin;
         }
-        int base = 0;
-        if (lane == 0) base = atomicAdd(n_staged, static_cast<int>(n_valid));
-        base = __shfl_sync(0xffffffffu, base, 0) + static_cast<int>(4 * lane);
-        const uint32_t pbit = proj ? kProjBit : 0u;
-        if (base - static_cast<int>(4 * lane) + static_cast<int>(n_valid) <= kBinStage) {
-          // common case, warp-uniform: predicated stores + histogram atomics
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if (v[k]) {
-              const uint32_t loc = pos[k] - b.col_begin;
-              staged[base + k] = pbit | loc;
-              atomicAdd(hist + (loc >> kTileShift), 1);
-            }
-          }
-        } else {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            if (!v[k]) continue;
-            const uint32_t loc = pos[k] - b.col_begin;
-            if (base + k < kBinStage) {
-              staged[base + k] = pbit | loc;
-              atomicAdd(hist + (loc >> kTileShift), 1);
-            } else {
-              bin_event(b, proj, loc);
-            }
-          }
-        }
-        ev += static_cast<uint32_t>(v[0]) + v[1] + v[2] + v[3];
+        ev += stage_emit4(b, cls, loc, valid, staged, n_staged, hist);
         start += total;
         ++chunk;
+        if (start < seg_end) g = philox_block(s.seed, kTagGap, row, seg, chunk * 32u + lane);
+      }
+    }
+  }
+  return ev;
+}
+
+// JIT rows active[k0 + 32 i] (i < 32, k0 + 32 i < k_end) for one warp, every
+// projection JIT.  Per projection, the lanes whose row belongs to it first
+// compute the stationary first offset of that row (one Philox per lane
+// instead of one per row); then the warp walks those rows one by one: one
+// Philox block of 4 gaps per lane per chunk of 128 gaps.  Positions grow
+// with (lane, k), so the valid events are a prefix of that order and their
+// staging slots follow from four ballots -- no second scan.
+__device__ __forceinline__ uint32_t stage_rows_jit(const ConnArgs &c, const BinTarget &b,
+                                                   const int32_t *active, int k0, int k_end,
+                                                   uint32_t *staged, int32_t *n_staged,
+                                                   int32_t *hist) {
+  const uint32_t lane = threadIdx.x & 31u;
+  // rows k0, k0 + 32, k0 + 64, ... (stride = warps per block)
+  const int nrows = min(32, (k_end - k0 + 31) / 32);
+  const int64_t r_l = lane < static_cast<uint32_t>(nrows) ? active[k0 + 32 * lane] : -1;
+  uint32_t ev = 0;
+  for (int p = 0; p < c.n_proj; ++p) {
+    const NetProj *P = c.proj + p;
+    uint32_t row_l;
+    const bool mem = r_l >= 0 && proj_has(P, r_l, row_l);
+    const uint32_t members = __ballot_sync(0xffffffffu, mem);
+    if (!members) continue;
+    const JitSide s = load_jit(P);
+    const uint32_t pbit = __ldg(&P->cls) << kClsShift;
+    for (uint32_t sidx = 0; sidx < s.n_seg; ++sidx) {
+      const uint32_t seg = s.seg_first + sidx;
+      const uint32_t seg_end = min(seg * s.L + s.L, c.n_cols);
+      // lane-parallel first offsets of the member rows in this segment
+      uint32_t first_l = 0;
+      if (mem) first_l = seg * s.L + first_offset(s.seed, s.K, row_l, seg);
+      uint32_t todo = members;
+      while (todo) {
+        const int jl = __ffs(todo) - 1;
+        todo &= todo - 1u;
+        const uint32_t row = __shfl_sync(0xffffffffu, row_l, jl);
+        uint32_t start = __shfl_sync(0xffffffffu, first_l, jl);
+        uint32_t chunk = 0;
+        while (start < seg_end) {                            // warp-uniform
+          const u32x4 g = philox_block(s.seed, kTagGap, row, seg, chunk * 32u + lane);
+          const uint32_t g0 = bounded(1u, s.K, g.x), g1 = bounded(1u, s.K, g.y);
+          const uint32_t g2 = bounded(1u, s.K, g.z), g3 = bounded(1u, s.K, g.w);
+          const uint32_t p1 = g0, p2 = g0 + g1, p3 = p2 + g2, t = p3 + g3;
+          uint32_t incl = t;
+#pragma unroll
+          for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= static_cast<uint32_t>(off)) incl += v;
+          }
+          const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+          const uint32_t pos0 = start + (incl - t);
+          const uint32_t pos[4] = {pos0, pos0 + p1, pos0 + p2, pos0 + p3};
+          bool v[4];
+          uint32_t n_valid = 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            v[k] = pos[k] < seg_end;
+            n_valid += __popc(__ballot_sync(0xffffffffu, v[k]));
+          }
+          int base = 0;
+          if (lane == 0) base = atomicAdd(n_staged, static_cast<int>(n_valid));
+          base = __shfl_sync(0xffffffffu, base, 0) + static_cast<int>(4 * lane);
+          if (base - static_cast<int>(4 * lane) + static_cast<int>(n_valid) <= kBinStage) {
+            // common case, warp-uniform: predicated stores + histogram atomics
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              if (v[k]) {
+                const uint32_t loc = pos[k] - b.col_begin;
+                staged[base + k] = pbit | loc;
+                atomicAdd(hist + (loc >> kTileShift), 1);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              if (!v[k]) continue;
+              const uint32_t loc = pos[k] - b.col_begin;
+              if (base + k < kBinStage) {
+                staged[base + k] = pbit | loc;
+                atomicAdd(hist + (loc >> kTileShift), 1);
+              } else {
+                bin_event(b, pbit >> kClsShift, loc);
+              }
+            }
+          }
+          ev += static_cast<uint32_t>(v[0]) + v[1] + v[2] + v[3];
+          start += total;
+          ++chunk;
+        }
       }
     }
   }
@@ -988,44 +1049,47 @@ __device__ __forceinline__ uint32_t stage_rows_jit(const ConnArgs &c, const BinT
 __device__ __forceinline__ uint32_t stage_row_lane(const ConnArgs &c, const BinTarget &b,
                                                    int64_t r, uint32_t *staged,
                                                    int32_t *n_staged, int32_t *hist) {
-  const bool inh = r >= c.split;
-  const uint32_t proj = inh ? 1u : 0u;
-  const JitSide s = pick(inh, c.je, c.ji);
-  const uint32_t row = static_cast<uint32_t>(inh ? r - c.split : r);
   uint32_t ev = 0;
-  for (uint32_t sidx = 0; sidx < s.n_seg; ++sidx) {
-    const uint32_t seg = s.seg_first + sidx;
-    const uint32_t seg_end = min(seg * s.L + s.L, c.n_cols);
-    uint32_t pos = seg * s.L + first_offset(s.seed, s.K, row, seg);
-    for (uint32_t blk = 0; pos < seg_end; blk += 2) {
-      const u32x4 x = philox_block(s.seed, kTagGap, row, seg, blk);
-      const u32x4 y = philox_block(s.seed, kTagGap, row, seg, blk + 1);
-      uint32_t e[8];
-      e[0] = pos;
-      e[1] = e[0] + bounded(1u, s.K, x.x);
-      e[2] = e[1] + bounded(1u, s.K, x.y);
-      e[3] = e[2] + bounded(1u, s.K, x.z);
-      e[4] = e[3] + bounded(1u, s.K, x.w);
-      e[5] = e[4] + bounded(1u, s.K, y.x);
-      e[6] = e[5] + bounded(1u, s.K, y.y);
-      e[7] = e[6] + bounded(1u, s.K, y.z);
-      pos = e[7] + bounded(1u, s.K, y.w);
-      int nv = 0;
+  for (int p = 0; p < c.n_proj; ++p) {
+    const NetProj *P = c.proj + p;
+    uint32_t row;
+    if (!proj_has(P, r, row)) continue;
+    const uint32_t cls = __ldg(&P->cls);
+    const JitSide s = load_jit(P);
+    for (uint32_t sidx = 0; sidx < s.n_seg; ++sidx) {
+      const uint32_t seg = s.seg_first + sidx;
+      const uint32_t seg_end = min(seg * s.L + s.L, c.n_cols);
+      uint32_t pos = seg * s.L + first_offset(s.seed, s.K, row, seg);
+      for (uint32_t blk = 0; pos < seg_end; blk += 2) {
+        const u32x4 x = philox_block(s.seed, kTagGap, row, seg, blk);
+        const u32x4 y = philox_block(s.seed, kTagGap, row, seg, blk + 1);
+        uint32_t e[8];
+        e[0] = pos;
+        e[1] = e[0] + bounded(1u, s.K, x.x);
+        e[2] = e[1] + bounded(1u, s.K, x.y);
+        e[3] = e[2] + bounded(1u, s.K, x.z);
+        e[4] = e[3] + bounded(1u, s.K, x.w);
+        e[5] = e[4] + bounded(1u, s.K, y.x);
+        e[6] = e[5] + bounded(1u, s.K, y.y);
+        e[7] = e[6] + bounded(1u, s.K, y.z);
+        pos = e[7] + bounded(1u, s.K, y.w);
+        int nv = 0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) nv += e[k] < seg_end;
-      int slot = atomicAdd(n_staged, nv);
+        for (int k = 0; k < 8; ++k) nv += e[k] < seg_end;
+        int slot = atomicAdd(n_staged, nv);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        if (e[k] >= seg_end) break;
-        const uint32_t loc = e[k] - b.col_begin;
-        if (slot < kBinStage) {
-          staged[slot] = stage_record(proj, loc);
-          atomicAdd(hist + (loc >> kTileShift), 1);
-        } else {
-          bin_event(b, proj, loc);
+        for (int k = 0; k < 8; ++k) {
+          if (e[k] >= seg_end) break;
+          const uint32_t loc = e[k] - b.col_begin;
+          if (slot < kBinStage) {
+            staged[slot] = stage_record(cls, loc);
+            atomicAdd(hist + (loc >> kTileShift), 1);
+          } else {
+            bin_event(b, cls, loc);
+          }
+          ++slot;
+          ++ev;
         }
-        ++slot;
-        ++ev;
       }
     }
   }
@@ -1099,7 +1163,7 @@ k_bin_sorted(ConnArgs conn, BinTarget out, const int32_t *active, const int32_t 
 
   // A. regenerate this block's rows into shared memory + tile histogram
   uint32_t ev = 0;
-  if (conn.conn == 1) {
+  if (!conn.all_jit) {
     for (int k = r_lo + static_cast<int>(warp); k < r_hi; k += kBinThreads / 32)
       ev += stage_row(conn, out, active[k], staged, &n_staged, hist);
   } else if (conn.lane_rows) {
@@ -1140,7 +1204,7 @@ k_bin_sorted(ConnArgs conn, BinTarget out, const int32_t *active, const int32_t 
   // C. counting sort by tile (hist[] becomes the running cursor)
   for (int i = tid; i < ns; i += kBinThreads) {
     const uint32_t rec = staged[i];
-    const uint32_t t = (rec & ~kProjBit) >> kTileShift;
+    const uint32_t t = (rec & kLocMask) >> kTileShift;
     sorted[atomicAdd(hist + t, 1)] = rec;
   }
   __syncthreads();
@@ -1150,11 +1214,11 @@ k_bin_sorted(ConnArgs conn, BinTarget out, const int32_t *active, const int32_t 
   //    sorted[], so the run begins at hist[t-1] (tiles are in order).
   for (int i = tid; i < ns; i += kBinThreads) {
     const uint32_t rec = sorted[i];
-    const uint32_t loc = rec & ~kProjBit;
+    const uint32_t loc = rec & kLocMask;
     const uint32_t t = loc >> kTileShift;
     const int32_t run_begin = (t == 0) ? 0 : hist[t - 1];
     const int32_t slot = gbase[t] + (i - run_begin);
-    bin_store(out, (rec & kProjBit) ? 1u : 0u, loc, slot);
+    bin_store(out, rec >> kClsShift, loc, slot);
   }
   // events counter
   ev = __reduce_add_sync(0xffffffffu, ev);
@@ -1236,20 +1300,24 @@ k_small_net(SmallArgs a) {
     // (1) deliver spikes_{n-1}: count events per postsynaptic neuron
     for (int k = warp; k < n_act; k += kSmallThreads / 32) {
       const int64_t r = act[k];
-      const bool inh = r >= a.conn.split;
-      const int64_t row64 = inh ? r - a.conn.split : r;
-      int32_t *cnt = inh ? cI : cE;
-      if (a.conn.conn == 1) {
-        const CsrSide s = pick(inh, a.conn.ce, a.conn.ci);
-        const int64_t b = __ldg(s.indptr + row64), e = __ldg(s.indptr + row64 + 1);
-        for (int64_t j = b + lane; j < e; j += 32) {
-          atomicAdd(cnt + __ldg(s.indices + j), 1);
-          ++my_ev;
+      for (int pj = 0; pj < a.conn.n_proj; ++pj) {
+        const NetProj *P = a.conn.proj + pj;
+        uint32_t row;
+        if (!proj_has(P, r, row)) continue;
+        int32_t *cnt = __ldg(&P->cls) ? cI : cE;       // standard layout: class = receptor
+        if (__ldg(&P->conn) == 1) {
+          const int64_t *indptr = P->c.indptr;
+          const int32_t *indices = P->c.indices;
+          const int64_t b = __ldg(indptr + row), e = __ldg(indptr + row + 1);
+          for (int64_t j = b + lane; j < e; j += 32) {
+            atomicAdd(cnt + __ldg(indices + j), 1);
+            ++my_ev;
+          }
+          continue;
         }
-      } else {
-        const JitSide s = pick(inh, a.conn.je, a.conn.ji);
-        const uint32_t row = static_cast<uint32_t>(row64);
-        for (uint32_t seg = 0; seg < s.n_seg; ++seg) {
+        const JitSide s = load_jit(P);
+        for (uint32_t sidx = 0; sidx < s.n_seg; ++sidx) {
+          const uint32_t seg = s.seg_first + sidx;
           const uint32_t seg_end = min(seg * s.L + s.L, a.conn.n_cols);
           u32x4 g = philox_block(s.seed, kTagGap, row, seg, lane);
           uint32_t start = seg * s.L + first_offset(s.seed, s.K, row, seg);

@@ -77,14 +77,38 @@ def exchange_spikes(words: torch.Tensor, part: Partition, group=None,
     return words
 
 
+@dataclass(frozen=True)
+class ProjSpec:
+    """One projection of a network (bp_projection): the spikes of neurons
+    [pre_begin, pre_end) add `weight` per event into the conductance of
+    `receptor` ('exc' or 'inh') at their targets among all n neurons.
+    Connectivity: JIT (seed, p, seg_len; event_mv_prob_homo, P:949) or a
+    full CSR (indptr, indices) over the projection's rows (this rank keeps
+    the columns it owns)."""
+    pre_begin: int
+    pre_end: int
+    receptor: str
+    weight: float
+    seed: int | None = None
+    p: float | None = None
+    csr: tuple | None = None
+
+
 class CobaNetwork:
-    """One rank's share of the Listing S3 E/I network (COBA-LIF or COBA-HH).
+    """One rank's share of the Listing S3 E/I network (COBA-LIF or COBA-HH),
+    or of any network of up to 8 projections merged per receptor
+    (`projections`, AlignPost P:130).
 
     conn='jit': connectivity regenerated each step from (seed, p) -- the
     EventJitFPHomoLinear / event_mv_prob_homo projection of P:973-981.
     conn='csr': stored CSR (event_csrmv, Listing S1); `csr` gives the full
     (indptr, indices) of the E rows and the I rows (torch CPU or CUDA), and
     this rank keeps the columns it owns.
+    exchange='caller' (default): with world > 1 the spike all-gather runs in
+    step_distributed through torch.distributed (NCCL or gloo); 'nccl': the
+    library owns an NCCL communicator and run() executes whole steps,
+    the all-gather included (bp_network_step; needs torch.distributed
+    initialised when world > 1, only to broadcast the NCCL id).
     """
 
     def __init__(self, n: int, *, model: str = "lif", conn: str = "jit",
@@ -93,7 +117,9 @@ class CobaNetwork:
                  w_exc: float | None = None, w_inh: float | None = None,
                  seed_e: int = SEED_E, seed_i: int = SEED_I, v0=None,
                  init_seed: int = inputs.V0_SEED, spikes: torch.Tensor | None = None,
-                 frac_bits: int | None = None, delay: int = 1):
+                 frac_bits: int | None = None, delay: int = 1,
+                 projections: list[ProjSpec] | None = None, exchange: str = "caller",
+                 group=None):
         device = torch.device(device or "cuda")
         self.n = n
         self.n_exc = n * 4 // 5
@@ -103,7 +129,7 @@ class CobaNetwork:
             # one JIT segment per rank: the partition is the segment (8(e))
             seg_len = partition(n, world, rank).local if world > 1 else n
         self.seg_len = seg_len
-        self.part = partition(n, world, rank, align=seg_len if conn == "jit" and world > 1 else 32)
+        self.part = partition(n, world, rank, align=seg_len if world > 1 else 32)
         lo, hi = self.part.col_begin, self.part.col_end
         n_local = hi - lo
         if model == "lif":
@@ -140,32 +166,63 @@ class CobaNetwork:
         words = self.part.padded_words if world > 1 else (n + 31) // 32
         self.spikes = (torch.zeros(words, dtype=torch.int32, device=device)
                        if spikes is None else spikes)
+        if projections is None:
+            # Listing S3: E rows [0, n_exc) -> g_E with w_E, I rows -> g_I with w_I
+            if conn == "jit":
+                projections = [ProjSpec(0, self.n_exc, "exc", w_exc, seed=seed_e, p=self.p),
+                               ProjSpec(self.n_exc, n, "inh", w_inh, seed=seed_i, p=self.p)]
+            else:
+                (ip_e, ix_e), (ip_i, ix_i) = csr
+                projections = [ProjSpec(0, self.n_exc, "exc", w_exc, csr=(ip_e, ix_e)),
+                               ProjSpec(self.n_exc, n, "inh", w_inh, csr=(ip_i, ix_i))]
+        self.projections = projections
+        descs, keep = [], []
+        for ps in projections:
+            rec = B.RECEPTOR_EXC if ps.receptor == "exc" else B.RECEPTOR_INH
+            if ps.csr is None:
+                pp = self.p if ps.p is None else ps.p
+                jit = B.jitconn_spec(ps.seed, pp, B.conn_len(pp), seg_len)
+                descs.append(B.projection(pre_begin=ps.pre_begin, pre_end=ps.pre_end,
+                                          weight=ps.weight, receptor=rec, jit=jit))
+            else:
+                ip, ix, _ = _slice_csr(ps.csr[0], ps.csr[1], lo, hi, device)
+                keep += [ip, ix]
+                descs.append(B.projection(pre_begin=ps.pre_begin, pre_end=ps.pre_end,
+                                          weight=ps.weight, receptor=rec, csr=(ip, ix)))
+        self.exchange = exchange
         kw = {}
-        if conn == "jit":
-            K = B.conn_len(self.p)
-            kw["jit_exc"] = B.jitconn_spec(seed_e, self.p, K, seg_len)
-            kw["jit_inh"] = B.jitconn_spec(seed_i, self.p, K, seg_len)
-        else:
-            (ip_e, ix_e), (ip_i, ix_i) = csr
-            kw["csr_exc"] = _slice_csr(ip_e, ix_e, lo, hi, device)
-            kw["csr_inh"] = _slice_csr(ip_i, ix_i, lo, hi, device)
+        if exchange == "nccl":
+            nccl_id = B.nccl_unique_id() if rank == 0 else None
+            if world > 1:
+                import torch.distributed as dist
+                obj = [nccl_id]
+                dist.broadcast_object_list(obj, src=0, group=group)
+                nccl_id = obj[0]
+            kw = dict(exchange=B.EXCHANGE_NCCL, rank=rank, world=world,
+                      part_len=self.part.local, nccl_id=nccl_id)
+        elif exchange != "caller":
+            raise ValueError(f"exchange={exchange!r}")
         self.net = B.Network(model=B.MODEL_LIF if model == "lif" else B.MODEL_HH,
-                             conn=B.CONN_JIT if conn == "jit" else B.CONN_CSR,
-                             n=n, n_exc=self.n_exc, state=st, spikes=self.spikes,
-                             params=params, col_begin=lo, col_end=hi,
-                             w_exc=w_exc, w_inh=w_inh, delay=delay, **kw)
+                             n=n, state=st, spikes=self.spikes, params=params,
+                             projections=descs, col_begin=lo, col_end=hi, delay=delay,
+                             keep=keep, **kw)
         self.delay = delay
         self._send = None
 
-    # single device: the whole loop runs in the library
+    # single device, or the library's NCCL exchange: the whole loop runs in
+    # the library
     def run(self, n_steps: int, raster: torch.Tensor | None = None, counts=None):
         self.net.step(n_steps, raster, counts)
 
-    # several devices: scatter -> update -> all-gather, per step.  The
-    # all-gather runs on a side stream that waits only for the update kernel's
-    # spike words, so it overlaps the local binning kernel (SURVEY 8(e)
-    # option (i)); the next scatter waits for it.  overlap=False: one stream.
+    # several devices, caller exchange: scatter -> update -> all-gather, per
+    # step.  The all-gather runs on a side stream that waits only for the
+    # update kernel's spike words, so it overlaps the local binning kernel
+    # (SURVEY 8(e) option (i)); the next scatter waits for it.
+    # overlap=False: one stream.
     def step_distributed(self, group=None, raster_row=None, overlap: bool = True):
+        if self.exchange == "nccl":
+            self.net.step(1, None if raster_row is None else raster_row.view(1, -1))
+            return
         if self._send is None:
             self._send = torch.empty(self.part.local_words, dtype=torch.int32,
                                      device=self.spikes.device)
@@ -187,7 +244,9 @@ class CobaNetwork:
         -- so a replay costs one launch instead of ~10 host calls per step
         (their enqueue cost is close to the GPU step time).  The exchange is
         captured with it (NCCL; gloo cannot be captured).  Call after at least
-        one eager step_distributed.  Returns (graph, steps per replay)."""
+        one eager step_distributed; eager steps after the capture put the
+        device state out of phase with the graph unless they are a multiple
+        of the period.  Returns (graph, steps per replay)."""
         period = math.lcm(2, self.delay + 1)
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
@@ -197,6 +256,9 @@ class CobaNetwork:
 
     def counters(self):
         return self.net.counters()
+
+    def device_bytes(self) -> int:
+        return self.net.device_bytes()
 
 
 def _slice_csr(indptr, indices, lo, hi, device):

@@ -66,3 +66,39 @@ def test_device_calls_fail_loudly_without_gpu(libbp):
     rc = libbp.bp_compact_spikes(None, 0, None, ctypes.c_void_p(16), None)
     assert rc != 0
     assert libbp.bp_last_error()
+
+
+def test_struct_layouts_match_the_header(tmp_path):
+    """The ctypes mirrors of bp.h's structs have the C layout (size and the
+    offsets of the fields the binding sets), checked against gcc."""
+    from paper_2311_05106_b200 import _binding as B
+    fields = {"bp_network_desc": (B.NetworkDesc, ["n", "col_begin", "proj", "params", "state",
+                                                  "spikes", "ws_bytes", "exchange",
+                                                  "part_len", "nccl_id"]),
+              "bp_projection": (B.Projection, ["pre_begin", "weight", "jit", "indptr"]),
+              "bp_jitconn": (B.JitConn, ["prob", "seg_len", "gap_law"]),
+              "bp_neuron_params": (B.NeuronParams, ["alpha_e", "c_m", "v_spike"]),
+              "bp_neuron_state": (B.NeuronState, ["g_kind", "ref", "n_gate"])}
+    src = ['#include <stdio.h>', '#include <stddef.h>', '#include "bp.h"', "int main(void) {"]
+    for cname, (_, fs) in fields.items():
+        src.append(f'  printf("{cname} %zu\\n", sizeof({cname}));')
+        for f in fs:
+            src.append(f'  printf("{cname}.{f} %zu\\n", offsetof({cname}, {f}));')
+    src.append("  return 0; }")
+    c = tmp_path / "layout.c"
+    c.write_text("\n".join(src))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(c), "-o", str(exe)])
+    got = dict(line.split() for line in subprocess.check_output([str(exe)]).decode().splitlines())
+    for cname, (cls, fs) in fields.items():
+        assert int(got[cname]) == ctypes.sizeof(cls), cname
+        for f in fs:
+            assert int(got[f"{cname}.{f}"]) == getattr(cls, f).offset, (cname, f)
+
+
+def test_library_has_no_link_time_nccl_dependency(libbp):
+    """NCCL is resolved at run time (dlopen): loading libbp.so never pulls a
+    second libnccl into a process that already has torch's."""
+    from paper_2311_05106_b200 import _binding
+    out = subprocess.check_output(["readelf", "-d", _binding.LIB_PATH]).decode()
+    assert "nccl" not in out

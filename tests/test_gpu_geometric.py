@@ -146,6 +146,8 @@ def test_geo_errors(bp):
     net = CobaNetwork(4000, fixed=True, device="cuda")
     spec = bp.jitconn_spec(1, 0.02, 0, 0, gap_law=bp.GAP_GEOMETRIC)
     with pytest.raises(bp.BpError, match="UNSUPPORTED"):
-        bp.Network(model=bp.MODEL_LIF, conn=bp.CONN_JIT, n=4000, n_exc=3200,
-                   state=net.state, spikes=net.spikes, params=net.params, col_begin=0,
-                   col_end=4000, w_exc=0.6, w_inh=6.7, jit_exc=spec, jit_inh=spec)
+        bp.Network(model=bp.MODEL_LIF, n=4000, state=net.state, spikes=net.spikes,
+                   params=net.params, col_begin=0, col_end=4000,
+                   projections=[bp.projection(pre_begin=0, pre_end=3200, weight=0.6, jit=spec),
+                                bp.projection(pre_begin=3200, pre_end=4000, weight=6.7,
+                                              receptor=bp.RECEPTOR_INH, jit=spec)])

@@ -1,0 +1,124 @@
+"""GPU parity of networks with several projections merged per receptor
+(AlignPost) and of the library's
+own NCCL exchange (bp_network_create with BP_EXCHANGE_NCCL),
+bit for bit against the oracle's run_network.
+
+Layouts:
+* split    -- Listing S3 with the E population cut into two JIT projections
+              of the same weight (different seeds): one weight class per
+              receptor, the standard k_step fold;
+* general  -- two E weights and two I weights (4 weight classes, the
+              general merge: exact integer sums, fp32 rounded once);
+* mixed    -- a CSR projection and JIT projections into the same receptor,
+              3-step synaptic delay.
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_2311_05106_b200 import inputs
+from paper_2311_05106_b200.network import CobaNetwork, ProjSpec
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import __graft_entry__ as ge
+    ge.build_lib()
+    torch.cuda.set_device(0)
+
+
+def _layout(orc, name, n):
+    """(ProjSpecs for the library, oracle Projections, delay)."""
+    n_exc = n * 4 // 5
+    p = 80.0 / n
+    K = orc.conn_len(p)
+    c1 = n_exc // 3
+    if name == "split":
+        rows = [(0, c1, "exc", 0.6, 101), (c1, n_exc, "exc", 0.6, 102), (n_exc, n, "inh", 6.7, 103)]
+        delay, csr_rows = 1, None
+    elif name == "general":
+        c2 = n_exc + (n - n_exc) // 2
+        rows = [(0, c1, "exc", 0.6, 201), (c1, n_exc, "exc", 0.45, 202),
+                (n_exc, c2, "inh", 6.7, 203), (c2, n, "inh", 5.0, 204)]
+        delay, csr_rows = 1, None
+    else:   # mixed: projection 0 is stored CSR
+        rows = [(0, c1, "exc", 0.6, 301), (c1, n_exc, "exc", 0.5, 302), (n_exc, n, "inh", 6.7, 303)]
+        delay, csr_rows = 3, 0
+    specs, oproj = [], []
+    for k, (b, e, rec, w, seed) in enumerate(rows):
+        jit = orc.JitSpec(seed, K, n, orc.LAW_HOMO, w)
+        if k == csr_rows:
+            ip, ix, _ = orc.jit_materialize(jit, e - b, n)
+            specs.append(ProjSpec(b, e, rec, w, csr=(torch.from_numpy(ip), torch.from_numpy(ix))))
+            oproj.append(orc.Projection(b, e - b, csr=(ip, ix, None), w_homo=w, receptor=rec))
+        else:
+            specs.append(ProjSpec(b, e, rec, w, seed=seed, p=p))
+            oproj.append(orc.Projection(b, e - b, jit=jit, receptor=rec))
+    return specs, oproj, delay
+
+
+def _g(mode):
+    return {"fix64": np.int64, "fix32": np.int32, "f32": np.float32}[mode]
+
+
+@pytest.mark.parametrize("mode", ["fix64", "fix32", "f32"])
+@pytest.mark.parametrize("layout", ["split", "general", "mixed"])
+@pytest.mark.parametrize("n,steps", [(4000, 600), (20_000, 300)])
+def test_merged_network_bit_exact(orc, layout, mode, n, steps):
+    specs, oproj, delay = _layout(orc, layout, n)
+    net = CobaNetwork(n, conn="jit", fixed={"fix64": True, "fix32": "fix32", "f32": False}[mode],
+                      projections=specs, delay=delay)
+    raster = torch.zeros((steps, (n + 31) // 32), dtype=torch.int32, device="cuda")
+    net.run(steps, raster)
+    orc.set_fix32_bits(20)
+    st = dict(v=inputs.lif_v0(n), g_e=np.zeros(n, _g(mode)), g_i=np.zeros(n, _g(mode)),
+              ref=np.zeros(n, np.uint8), spikes=np.zeros(n, np.uint8))
+    want = orc.run_network("lif", orc.lif_params(), st, oproj, None, steps, delay=delay)
+    got = np.stack([inputs.unpack_bits(r, n) for r in raster.cpu().numpy().view(np.uint32)])
+    assert want.sum() > 0
+    assert np.array_equal(got, want)
+    for k in ("v", "g_e", "g_i", "ref"):
+        assert np.array_equal(net.state[k].cpu().numpy().view(np.uint8), st[k].view(np.uint8)), k
+
+
+def test_merged_conductance_memory(orc):
+    """The merged network holds ONE g_E and ONE g_I array whatever the number
+    of projections: the state bytes are those of Listing S3's
+    two-projection network, and the library's own allocation (buckets +
+    projection table) grows only by the table and the extra count classes."""
+    n = 100_000
+    specs, _, _ = _layout(orc, "general", n)
+    merged = CobaNetwork(n, conn="jit", fixed=False, projections=specs)
+    plain = CobaNetwork(n, conn="jit", fixed=False)
+    sb = lambda net: sum(t.numel() * t.element_size() for t in net.state.values()
+                         if isinstance(t, torch.Tensor))
+    assert sb(merged) == sb(plain)
+    assert merged.state["g_e"].numel() == n
+    # per-projection conductances would need 4 arrays of n fp32 instead of 2;
+    # the library's buckets grow by the two extra overflow-count classes only
+    slots = 2
+    assert merged.device_bytes() <= plain.device_bytes() + slots * 2 * 4 * n + 4096
+
+
+@pytest.mark.parametrize("delay", [1, 2, 4])
+@pytest.mark.parametrize("mode", ["fix64", "f32"])
+def test_nccl_exchange_world1_bit_exact(orc, delay, mode):
+    """The library-owned NCCL exchange (bp_network_create with
+    BP_EXCHANGE_NCCL, world 1: communicator, comm stream, all-gather of the
+    own words, the D >= 2 alternating vectors) gives the same network as
+    the plain loop and the oracle."""
+    n, steps = 20_000, 300
+    fixed = {"fix64": True, "f32": False}[mode]
+    a = CobaNetwork(n, conn="jit", fixed=fixed, delay=delay, exchange="nccl")
+    b = CobaNetwork(n, conn="jit", fixed=fixed, delay=delay)
+    ra = torch.zeros((steps, (n + 31) // 32), dtype=torch.int32, device="cuda")
+    rb = torch.zeros_like(ra)
+    a.run(steps // 2, ra[:steps // 2])
+    a.run(steps - steps // 2, ra[steps // 2:])
+    b.run(steps, rb)
+    assert torch.equal(ra, rb)
+    for k in ("v", "g_e", "g_i", "ref"):
+        assert torch.equal(a.state[k], b.state[k]), k
+    assert a.counters() == b.counters()

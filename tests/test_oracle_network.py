@@ -337,3 +337,100 @@ def test_threaded_oracle_equals_sequential(orc, g_dtype):
     assert r1.sum() > 0 and np.array_equal(r1, r2)
     for k in ("v", "g_e", "g_i", "ref"):
         assert np.array_equal(s1[k].view(np.uint8), s2[k].view(np.uint8)), k
+
+
+# ------------------------------------------------- AlignPost merging
+# Several projections into one receptor share its single conductance per
+# neuron; the step's increment is the exact sum of all their events
+# (fixed point) or its exactly rounded value (rule N1-f32).
+
+def _split_csr(ip, ix, cut):
+    """Rows [0, cut) and [cut, n_rows) of a CSR as two CSRs."""
+    a = (ip[:cut + 1].copy(), ix[:ip[cut]].copy(), None)
+    b = ((ip[cut:] - ip[cut]).copy(), ix[ip[cut]:].copy(), None)
+    return a, b
+
+
+@pytest.mark.parametrize("g_dtype", [np.int64, np.int32, np.float32])
+def test_merged_projections_equal_their_union(orc, g_dtype):
+    """Listing S3's E projection cut into two projections over rows
+    [0, 1000) and [1000, 3200) with the same weight, both adding into g_E,
+    is the same network: rasters and state bit for bit in every mode."""
+    n, T = 4000, 200
+    s1, pe, pi = _coba(orc, n=n, conn="csr")
+    s1["g_e"] = np.zeros(n, g_dtype)
+    s1["g_i"] = np.zeros(n, g_dtype)
+    r1 = orc.run_network("lif", orc.lif_params(), s1, pe, pi, T)
+    s2, _, _ = _coba(orc, n=n, conn="csr")
+    s2["g_e"] = np.zeros(n, g_dtype)
+    s2["g_i"] = np.zeros(n, g_dtype)
+    (a, b) = _split_csr(*pe.csr[:2], 1000)
+    projs = [orc.Projection(0, 1000, csr=a, w_homo=0.6, receptor="exc"),
+             orc.Projection(1000, pe.n_rows - 1000, csr=b, w_homo=0.6, receptor="exc"),
+             orc.Projection(pi.row0, pi.n_rows, csr=pi.csr, w_homo=6.7, receptor="inh")]
+    r2 = orc.run_network("lif", orc.lif_params(), s2, projs, None, T)
+    assert r1.sum() > 0 and np.array_equal(r1, r2)
+    for k in ("v", "g_e", "g_i", "ref"):
+        assert np.array_equal(s1[k].view(np.uint8), s2[k].view(np.uint8)), k
+
+
+def test_merged_distinct_weights_fixed_point_recursion(orc):
+    """Two excitatory projections with different weights (0.6 and 0.45,
+    different JIT seeds) and one inhibitory, merged: the fixed-point g_E
+    equals the fp64 recursion a_n = alpha a_{n-1} + sum_p w_p D_p^T s_{n-1}
+    from the raster and independent dense matrices, within the F1 bound."""
+    n, T, n1 = 3000, 250, 1200
+    n_exc = n * 4 // 5
+    K = orc.conn_len(80.0 / n)
+    j1 = orc.JitSpec(11, K, n, orc.LAW_HOMO, 0.6)
+    j2 = orc.JitSpec(12, K, n, orc.LAW_HOMO, 0.45)
+    ji = orc.JitSpec(13, K, n, orc.LAW_HOMO, 6.7)
+    projs = [orc.Projection(0, n1, jit=j1, receptor="exc"),
+             orc.Projection(n1, n_exc - n1, jit=j2, receptor="exc"),
+             orc.Projection(n_exc, n - n_exc, jit=ji, receptor="inh")]
+    st = dict(v=inputs.lif_v0(n), g_e=np.zeros(n, np.int64), g_i=np.zeros(n, np.int64),
+              ref=np.zeros(n, np.uint8), spikes=np.zeros(n, np.uint8))
+    raster = orc.run_network("lif", orc.lif_params(), st, projs, None, T)
+    assert raster.sum() > 0
+    dense = []
+    for p in projs[:2]:
+        d = np.zeros((p.n_rows, n))
+        for r in range(p.n_rows):
+            d[r, orc.jit_row(p.jit, n, r)[0]] = float(np.float32(p.jit.w0))
+        dense.append(d)
+    a = math.exp(-0.1 / 5.0)
+    g = np.zeros(n)
+    prev = np.zeros(n)
+    for step in range(T):
+        g = a * g + prev[:n1] @ dense[0] + prev[n1:n_exc] @ dense[1]
+        prev = raster[step].astype(np.float64)
+    g *= a
+    assert np.max(np.abs(st["g_e"] / 2.0 ** 32 - g)) < 2.0 ** -20 * max(1.0, g.max())
+
+
+def test_merged_f32_increment_is_the_exactly_rounded_sum(orc):
+    """One neuron receives k1 events of w1 = fl32(0.6) and k2 of w2 =
+    fl32(0.45) from two projections into g_E in one step: the increment is
+    round_f32(k1 w1 + k2 w2) in exact rationals -- which for some (k1, k2)
+    differs from adding the two per-projection roundings."""
+    from fractions import Fraction
+    w1, w2 = np.float32(0.6), np.float32(0.45)
+    differs = 0
+    for k1, k2 in ((1, 1), (1, 3), (2, 11), (5, 7), (10, 13), (37, 80), (129, 3), (1000, 999)):
+        n = k1 + k2 + 32
+        projs = []
+        for r0, k, w in ((0, k1, w1), (k1, k2, w2)):
+            ip = np.arange(k + 1, dtype=np.int64)       # every row -> column 0
+            projs.append(orc.Projection(r0, k, csr=(ip, np.zeros(k, np.int32), None),
+                                        w_homo=float(w), receptor="exc"))
+        spikes = np.zeros(n, np.uint8)
+        spikes[:k1 + k2] = 1
+        st = dict(v=np.full(n, -60.0, np.float32), g_e=np.zeros(n, np.float32),
+                  g_i=np.zeros(n, np.float32), ref=np.zeros(n, np.uint8), spikes=spikes)
+        orc.run_network("lif", orc.lif_params(tau_e=float("inf")), st, projs, None, 1)
+        want = _round_f32_exact(k1 * Fraction(float(w1)) + k2 * Fraction(float(w2)))
+        assert st["g_e"][0].view(np.uint32) == want.view(np.uint32), (k1, k2)
+        two = np.float32(_round_f32_exact(k1 * Fraction(float(w1))) +
+                         _round_f32_exact(k2 * Fraction(float(w2))))
+        differs += int(two != want)
+    assert differs > 0
