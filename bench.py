@@ -824,7 +824,7 @@ def run_micro(args):
         data = dat if law != "homo" else None
         # the matrix is fixed across calls: split points analysed once,
         # outside the timed region (like the CSR itself); --no-plan: per call
-        plan = None if args.no_plan else bp.csrmv_plan(ip, ix, n, n, out.dtype, homo=data is None)
+        plan = None if args.no_plan else bp.csrmv_plan(ip, ix, n, n, out.dtype, homo=data is None, data=data)
         call = lambda s: bp.event_csrmv(ip, ix, data, 0.6, n, n, s, out, ws=ws, plan=plan)
         ev_per_pat = [int(row_nnz[e.astype(bool)].sum()) for e in pats]
         bytes_per_event = 8 if law != "homo" else 4
@@ -1030,7 +1030,7 @@ def run_fig3ab(args):
             del A
             cws = torch.empty(bp.lib().bp_csrmv_workspace_bytes(n, n, 0), dtype=torch.uint8,
                               device=dev)
-            plan = bp.csrmv_plan(ip, ix, n, n, torch.float32, homo=False)
+            plan = bp.csrmv_plan(ip, ix, n, n, torch.float32, homo=False, data=dat)
             rec["csr_event_mv_us"] = _time_calls(lambda: bp.event_csrmv(
                 ip, ix, dat, 0.0, n, n, spikes, out, ws=cws, plan=plan), reps, flush)
             del At, ip, ix, dat, plan, cws

@@ -158,19 +158,36 @@ bp_status bp_event_csrmv_grad(const int64_t *indptr, const int32_t *indices, con
  * that is reused (a network's projection, a benchmark's 10,000 calls) the
  * split points of all rows can be computed once:
  *   plan_bytes = bp_csrmv_plan_bytes(n_rows, n_cols, out_kind, data == NULL)
- *     (0: nothing to precompute -- the output fits one tile);
- *   bp_csrmv_plan(...) writes int32 split offsets [n_rows][n_tiles-1] into the
- *     caller's device buffer `plan` (16-byte aligned), asynchronously;
- *   bp_event_csrmv_planned(plan, ...) then behaves exactly like
+ *     (0: nothing to precompute);
+ *   bp_csrmv_plan(...) writes the analysis into the caller's device buffer
+ *     `plan` (16-byte aligned) and a host summary into *info (nullable);
+ *   bp_event_csrmv_planned(plan, plan_bytes, info, ...) then behaves like
  *     bp_event_csrmv without the per-call split.
- * The plan is valid for the same (indptr, indices, n_rows, n_cols, out_kind,
- * homogeneous-or-not) on the same device type; a stale plan gives wrong sums
- * but never reads outside the row.  Requires indices ascending per row. */
+ * Heterogeneous weights with an fp32 output (rule T4): given a
+ * workspace (ws >= bp_csrmv_workspace_bytes), the analysis also bounds every
+ * column's sum of |w| over all rows (one pass of the kernel itself; this
+ * call then SYNCHRONISES `stream`) and picks info->f32_fixed_bits = F, so
+ * that each call accumulates q = rint(w 2^F) exactly in two independent
+ * 32-bit integer words per column (native shared-memory atomics instead of
+ * an fp32 compare-and-swap loop) and rounds each column's exact sum to fp32
+ * once -- within rule T2, and independent of the summation order.  -1: the
+ * fp32-atomic path (no workspace, n_rows >= 2^24, or unbounded sums).
+ * The plan is valid for the same (indptr, indices, data, n_rows, n_cols,
+ * out_kind, homogeneous-or-not) on the same device type; a stale plan gives
+ * wrong sums but never reads outside the row.  Requires indices ascending
+ * per row. */
+typedef struct {
+  int32_t n_tiles;          /* column tiles of the accumulation                */
+  int32_t f32_fixed_bits;   /* rule T4 scale F (fp32 output, heterogeneous), or -1 */
+  double max_col_abs_sum;   /* max over columns of sum |w| (when F >= 0)       */
+} bp_csrmv_plan_info;
 size_t bp_csrmv_plan_bytes(int64_t n_rows, int64_t n_cols, int out_kind, int homo);
-bp_status bp_csrmv_plan(const int64_t *indptr, const int32_t *indices, int64_t n_rows,
-                        int64_t n_cols, int out_kind, int homo, void *plan,
-                        size_t plan_bytes, bp_stream stream);
-bp_status bp_event_csrmv_planned(const void *plan, size_t plan_bytes, const int64_t *indptr,
+bp_status bp_csrmv_plan(const int64_t *indptr, const int32_t *indices, const float *data,
+                        int64_t n_rows, int64_t n_cols, int out_kind, int homo, void *plan,
+                        size_t plan_bytes, bp_csrmv_plan_info *info, void *ws,
+                        size_t ws_bytes, bp_stream stream);
+bp_status bp_event_csrmv_planned(const void *plan, size_t plan_bytes,
+                                 const bp_csrmv_plan_info *info, const int64_t *indptr,
                                  const int32_t *indices, const float *data, float w_homo,
                                  int64_t n_rows, int64_t n_cols, const uint32_t *spikes,
                                  void *out, int out_kind, uint32_t flags, void *ws,
@@ -440,7 +457,9 @@ bp_status bp_network_update_overlap(bp_network *net, uint32_t *raster_row,
                                     bp_stream stream, bp_stream exchange_stream);
 /* Device counters since create: [0] = local spikes, [1] = synaptic events
  * delivered into local neurons, [2] = saturated BP_OUT_FIX32 conductance
- * updates (0 in a well-scaled run).  Copies into host uint64[3];
+ * updates (0 in a well-scaled run), [3] = non-finite membrane potentials
+ * seen after a step (debug check, only with the environment variable
+ * BP_DEBUG_NAN=1 at create; else 0).  Copies into host uint64[4];
  * synchronises `stream`. */
 bp_status bp_network_counters(bp_network *net, uint64_t *host_out,
                               bp_stream stream);

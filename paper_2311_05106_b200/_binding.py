@@ -72,6 +72,11 @@ class NeuronState(ctypes.Structure):
                 ("n_gate", ctypes.c_void_p)]
 
 
+class CsrmvPlanInfo(ctypes.Structure):
+    _fields_ = [("n_tiles", ctypes.c_int32), ("f32_fixed_bits", ctypes.c_int32),
+                ("max_col_abs_sum", ctypes.c_double)]
+
+
 MAX_PROJ = 8                            # BP_MAX_PROJ
 RECEPTOR_EXC, RECEPTOR_INH = 0, 1
 EXCHANGE_CALLER, EXCHANGE_NCCL = 0, 1
@@ -127,9 +132,10 @@ def lib():
         L.bp_event_csrmv_grad.argtypes = [P, P, P, f32, i64, i64, P, P, P, P, P, P]
         L.bp_csrmv_plan_bytes.argtypes = [i64, i64, i32, i32]
         L.bp_csrmv_plan_bytes.restype = sz
-        L.bp_csrmv_plan.argtypes = [P, P, i64, i64, i32, i32, P, sz, P]
-        L.bp_event_csrmv_planned.argtypes = [P, sz, P, P, P, f32, i64, i64, P, P, i32, u32,
-                                             P, sz, P]
+        L.bp_csrmv_plan.argtypes = [P, P, P, i64, i64, i32, i32, P, sz,
+                                    ctypes.POINTER(CsrmvPlanInfo), P, sz, P]
+        L.bp_event_csrmv_planned.argtypes = [P, sz, ctypes.POINTER(CsrmvPlanInfo), P, P, P, f32,
+                                             i64, i64, P, P, i32, u32, P, sz, P]
         jit_tail = [P, i64, i64, i64, i64, P, i32, u32, P, sz, P]
         L.bp_jitconn_event_mv_homo.argtypes = [ctypes.POINTER(JitConn), f32] + jit_tail
         L.bp_jitconn_event_mv_uniform.argtypes = [ctypes.POINTER(JitConn), f32, f32] + jit_tail
@@ -245,7 +251,8 @@ def event_csrmv(indptr, indices, data, w_homo, n_rows, n_cols, spikes, out,
             int(n_cols), _ptr(spikes), _ptr(out), _out_kind(out),
             ACCUMULATE if accumulate else 0, _ptr(ws), ws.numel(), _stream(stream))
     if plan is not None:
-        _check(lib().bp_event_csrmv_planned(_ptr(plan), plan.numel(), *tail))
+        _check(lib().bp_event_csrmv_planned(_ptr(plan.buf), plan.buf.numel(),
+                                            ctypes.byref(plan.info), *tail))
     else:
         _check(lib().bp_event_csrmv(*tail))
     return out
@@ -275,21 +282,39 @@ def event_csrmv_grad(indptr, indices, data, w_homo, n_rows, n_cols, spikes, gy,
     return grad_data, grad_events, grad_w
 
 
+class CsrmvPlan:
+    """A bp_csrmv_plan analysis: the device buffer and its host summary."""
+
+    def __init__(self, buf, info):
+        self.buf, self.info = buf, info
+
+    @property
+    def f32_fixed_bits(self) -> int:
+        return int(self.info.f32_fixed_bits)
+
+
 def csrmv_plan(indptr, indices, n_rows, n_cols, out_dtype=torch.float32, homo=True,
-               stream=None):
-    """Split points of every row at the column-tile boundaries of
-    event_csrmv's shared-memory accumulation, for a matrix reused across
-    calls; pass the result as event_csrmv(..., plan=...).  None when the
-    output fits one tile (nothing to precompute)."""
-    _cuda(indptr, indices)
+               data=None, stream=None):
+    """Analysis of a matrix reused across calls (split points of every row at
+    the column tiles; for heterogeneous weights with an fp32 output also the
+    rule-T4 scale, which synchronises the stream once); pass the result as
+    event_csrmv(..., plan=...).  None when there is nothing to precompute."""
+    _cuda(indptr, indices, data)
     kind = 1 if out_dtype == torch.int64 else 0
-    nbytes = int(lib().bp_csrmv_plan_bytes(int(n_rows), int(n_cols), kind, int(bool(homo))))
+    homo = bool(homo) and data is None
+    nbytes = int(lib().bp_csrmv_plan_bytes(int(n_rows), int(n_cols), kind, int(homo)))
     if nbytes == 0:
         return None
-    plan = torch.empty(nbytes, dtype=torch.uint8, device=indptr.device)
-    _check(lib().bp_csrmv_plan(_ptr(indptr), _ptr(indices), int(n_rows), int(n_cols), kind,
-                               int(bool(homo)), _ptr(plan), plan.numel(), _stream(stream)))
-    return plan
+    buf = torch.empty(nbytes, dtype=torch.uint8, device=indptr.device)
+    ws = None
+    if not homo:
+        ws = torch.empty(int(lib().bp_csrmv_workspace_bytes(int(n_rows), int(n_cols), kind)),
+                         dtype=torch.uint8, device=indptr.device)
+    info = CsrmvPlanInfo()
+    _check(lib().bp_csrmv_plan(_ptr(indptr), _ptr(indices), _ptr(data), int(n_rows), int(n_cols),
+                               kind, int(homo), _ptr(buf), buf.numel(), ctypes.byref(info),
+                               _ptr(ws), 0 if ws is None else ws.numel(), _stream(stream)))
+    return CsrmvPlan(buf, info)
 
 
 def jitconn_event_mv(law: int, spec: JitConn, w0: float, w1: float, spikes,
@@ -477,7 +502,8 @@ class Network:
 
     def __init__(self, *, model, n, state: dict, spikes, params, projections,
                  col_begin=0, col_end=None, stream=None, delay=1, keep=(),
-                 exchange=EXCHANGE_CALLER, rank=0, world=1, part_len=0, nccl_id=None):
+                 exchange=EXCHANGE_CALLER, rank=0, world=1, part_len=0, nccl_id=None,
+                 ws=None):
         col_end = n if col_end is None else col_end
         if not 1 <= len(projections) <= MAX_PROJ:
             raise BpError(f"1..{MAX_PROJ} projections, got {len(projections)}")
@@ -497,8 +523,11 @@ class Network:
         if nccl_id is not None:
             ctypes.memmove(d.nccl_id, nccl_id, 128)
         nbytes = int(lib().bp_network_workspace_bytes(ctypes.byref(d)))
-        self.ws = torch.zeros(nbytes, dtype=torch.uint8, device=spikes.device)
-        d.ws, d.ws_bytes = self.ws.data_ptr(), nbytes
+        if ws is None:
+            ws = torch.zeros(nbytes, dtype=torch.uint8, device=spikes.device)
+        _check_buf(ws, nbytes, torch.uint8, spikes.device, "ws")
+        self.ws = ws
+        d.ws, d.ws_bytes = ws.data_ptr(), ws.numel()
         self.desc = d
         self.device = spikes.device
         self.state, self.spikes = state, spikes
@@ -544,10 +573,15 @@ class Network:
 
     def counters(self, stream=None):
         """-> (local spikes, synaptic events delivered, saturated FIX32 updates)."""
-        out = (ctypes.c_uint64 * 3)()
+        return self.counters_all(stream)[:3]
+
+    def counters_all(self, stream=None):
+        """-> (spikes, events, saturated FIX32 updates, non-finite V seen with
+        BP_DEBUG_NAN=1)."""
+        out = (ctypes.c_uint64 * 4)()
         _check(lib().bp_network_counters(self._h, ctypes.cast(out, ctypes.c_void_p),
                                          _stream(stream)))
-        return int(out[0]), int(out[1]), int(out[2])
+        return tuple(int(x) for x in out)
 
     def device_bytes(self) -> int:
         """Device memory the library allocated for this network (buckets,

@@ -239,7 +239,9 @@ StreamPlan stream_plan_acc(int64_t n_rows, int64_t n_cols, int acc, bool homo, i
 // Measured (100 k x 100 k, 10 %): p = 0.001 30.6 -> 26.6 us, p = 0.01 equal,
 // p = 0.05 61.8 -> 65.8 us (two columns per word: more same-word conflicts
 // among the lanes' atomics) -- so opt-in, not the default.
-StreamPlan stream_plan(int64_t n_rows, int64_t n_cols, int out_kind, bool homo, int sms) {
+StreamPlan stream_plan(int64_t n_rows, int64_t n_cols, int out_kind, bool homo, int sms,
+                       bool fix2 = false) {
+  if (fix2 && !homo) return stream_plan_acc(n_rows, n_cols, 8, false, sms);   // rule T4 pairs
   const char *c16_env = std::getenv("BP_CSR_C16");
   if (homo && c16_env != nullptr && std::atoi(c16_env) != 0) {
     // 16-bit counts while a CTA streams < 2^16 rows: CTA g of a tile takes the
@@ -669,8 +671,10 @@ size_t bp_csrmv_workspace_bytes(int64_t n_rows, int64_t n_cols, int out_kind) {
   const CsrPlan p = csr_plan(n_rows, n_cols, out_kind, sms);
   size_t need = p.tiled ? p.ws_bytes : bp_workspace_bytes(n_rows);
   for (int homo = 0; homo < 2; ++homo) {
-    const StreamPlan sp = stream_plan(n_rows, n_cols, out_kind, homo != 0, sms);
-    if (sp.ok && sp.ws_bytes > need) need = sp.ws_bytes;
+    for (int fix2 = 0; fix2 < 2; ++fix2) {
+      const StreamPlan sp = stream_plan(n_rows, n_cols, out_kind, homo != 0, sms, fix2 != 0);
+      if (sp.ok && sp.ws_bytes > need) need = sp.ws_bytes;
+    }
   }
   return need;
 }
@@ -707,7 +711,8 @@ namespace {
 bp_status csrmv_impl(const void *plan, size_t plan_bytes, const int64_t *indptr,
                      const int32_t *indices, const float *data, float w_homo, int64_t n_rows,
                      int64_t n_cols, const uint32_t *spikes, void *out, int out_kind,
-                     uint32_t flags, void *ws, size_t ws_bytes, bp_stream stream) {
+                     uint32_t flags, void *ws, size_t ws_bytes, bp_stream stream,
+                     int32_t fix_bits = -1) {
   int sms = 0;
   bp_status s = device_ready(&sms);
   if (s != BP_OK) return s;
@@ -723,7 +728,11 @@ bp_status csrmv_impl(const void *plan, size_t plan_bytes, const int64_t *indptr,
   cudaStream_t st = as_stream(stream);
   const size_t elt = out_kind == BP_OUT_FIX64 ? 8 : 4;
   const bool homo = data == nullptr;
-  const StreamPlan sp = stream_plan(n_rows, n_cols, out_kind, homo, sms);
+  // rule T4: heterogeneous fp32 output accumulated in scaled fixed point
+  // (the plan's analysis chose fix_bits; -1 = fp32 atomics)
+  const bool fix2 = !homo && out_kind == BP_OUT_F32 && fix_bits >= 0 &&
+                    !std::getenv("BP_CSR_NO_T4");
+  const StreamPlan sp = stream_plan(n_rows, n_cols, out_kind, homo, sms, fix2);
   if (sp.ok && ws_bytes >= sp.ws_bytes && aligned(indices, 16) && (homo || aligned(data, 16)) &&
       !std::getenv("BP_CSR_TILED") && !std::getenv("BP_CSR_ATOMIC_FLUSH") &&
       !std::getenv("BP_CSR_DIRECT")) {
@@ -737,8 +746,10 @@ bp_status csrmv_impl(const void *plan, size_t plan_bytes, const int64_t *indptr,
     bp::CsrStreamArgs ca{indices, data, indptr, split, w.active, w.count, indptr + n_rows,
                          partials, sp.tile_cols, sp.groups, sp.n_tiles,
                          (flags & BP_ACCUMULATE) ? 1 : 0, n_cols, coop ? out : nullptr, w_homo,
-                         llrint(static_cast<double>(w_homo) * 4294967296.0)};
+                         llrint(static_cast<double>(w_homo) * 4294967296.0),
+                         fix2 ? fix_bits : 0, 0, 0};
     auto stream_kernel = [&](const bp::CsrStreamArgs &c) {
+      if (fix2) return launch_stream<2, false>(c, sp, st);
       if (homo)
         return sp.c16 ? (out_kind == BP_OUT_FIX64 ? launch_stream<1, true, true>(c, sp, st)
                                                   : launch_stream<0, true, true>(c, sp, st))
@@ -767,8 +778,10 @@ bp_status csrmv_impl(const void *plan, size_t plan_bytes, const int64_t *indptr,
     t.groups = sp.groups;
     t.partials = partials;
     t.accumulate = ca.accumulate;
+    t.fix_bits = ca.fix_bits;
     const int rgrid = static_cast<int>((n_cols + 255) / 256);
-    if (out_kind == BP_OUT_FIX64) bp::k_csr_reduce<1><<<rgrid, 256, 0, st>>>(t, homo, sp.c16);
+    if (fix2) bp::k_csr_reduce<2><<<rgrid, 256, 0, st>>>(t, 0, 0);
+    else if (out_kind == BP_OUT_FIX64) bp::k_csr_reduce<1><<<rgrid, 256, 0, st>>>(t, homo, sp.c16);
     else bp::k_csr_reduce<0><<<rgrid, 256, 0, st>>>(t, homo, sp.c16);
     return launched();
   }
@@ -895,12 +908,50 @@ size_t bp_csrmv_plan_bytes(int64_t n_rows, int64_t n_cols, int out_kind, int hom
   int sms = 148;
   if (device_ready(&sms) != BP_OK) sms = 148;
   const StreamPlan sp = stream_plan(n_rows, n_cols, out_kind, homo != 0, sms);
-  return sp.ok ? sp.plan_bytes : 0;
+  size_t need = sp.ok && sp.n_tiles > 1 ? sp.plan_bytes : 0;
+  if (!homo && out_kind == BP_OUT_F32) {
+    // rule T4: the split points of the 8-byte-pair tiles, and the analysis's
+    // column sums of |w| behind them
+    const StreamPlan s2 = stream_plan(n_rows, n_cols, out_kind, false, sms, true);
+    if (s2.ok)
+      need = std::max(need, (s2.n_tiles > 1 ? s2.plan_bytes : 0) +
+                                round_up(static_cast<size_t>(n_cols + 64) * 4, 256));
+  }
+  return need;
 }
 
-bp_status bp_csrmv_plan(const int64_t *indptr, const int32_t *indices, int64_t n_rows,
-                        int64_t n_cols, int out_kind, int homo, void *plan, size_t plan_bytes,
-                        bp_stream stream) {
+namespace {
+// max of v[0..n) (non-negative floats) into *out: one block
+__global__ void __launch_bounds__(1024) k_max_f32(const float *v, int64_t n, float *out) {
+  __shared__ float red[32];
+  float m = 0.f;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) m = fmaxf(m, v[i]);
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = red[threadIdx.x];
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) *out = m;
+  }
+}
+
+bp_status write_split(const int64_t *indptr, const int32_t *indices, int64_t n_rows,
+                      int64_t n_cols, const StreamPlan &sp, int32_t *plan, int sms,
+                      cudaStream_t st) {
+  bp::CsrSplitArgs sa{indptr, indices, nullptr, nullptr, n_rows, plan, sp.n_tiles, sp.tile_cols,
+                      n_cols};
+  int64_t blocks = (n_rows + 7) / 8;
+  if (blocks > static_cast<int64_t>(sms) * 16) blocks = static_cast<int64_t>(sms) * 16;
+  bp::k_csr_split<<<static_cast<int>(blocks), 256, 0, st>>>(sa);
+  return launched();
+}
+}  // namespace
+
+bp_status bp_csrmv_plan(const int64_t *indptr, const int32_t *indices, const float *data,
+                        int64_t n_rows, int64_t n_cols, int out_kind, int homo, void *plan,
+                        size_t plan_bytes, bp_csrmv_plan_info *info, void *ws,
+                        size_t ws_bytes, bp_stream stream) {
   int sms = 0;
   bp_status s = device_ready(&sms);
   if (s != BP_OK) return s;
@@ -908,27 +959,85 @@ bp_status bp_csrmv_plan(const int64_t *indptr, const int32_t *indices, int64_t n
            BP_ERR_SHAPE, "n_rows=%lld n_cols=%lld", (long long)n_rows, (long long)n_cols);
   BP_CHECK(out_kind == BP_OUT_F32 || out_kind == BP_OUT_FIX64, BP_ERR_INVALID_ARG,
            "out_kind %d", out_kind);
+  BP_CHECK(homo || data != nullptr, BP_ERR_INVALID_ARG, "heterogeneous plan needs data");
+  cudaStream_t st = as_stream(stream);
+  bp_csrmv_plan_info inf{};
+  inf.f32_fixed_bits = -1;
   const StreamPlan sp = stream_plan(n_rows, n_cols, out_kind, homo != 0, sms);
-  if (!sp.ok || sp.n_tiles <= 1 || n_rows == 0) return BP_OK;   // nothing to precompute
-  BP_CHECK(indptr && indices && plan, BP_ERR_INVALID_ARG, "NULL indptr/indices/plan");
-  BP_CHECK(plan_bytes >= sp.plan_bytes, BP_ERR_WORKSPACE, "plan %zu bytes < %zu required",
-           plan_bytes, sp.plan_bytes);
-  BP_CHECK(aligned(plan, 16), BP_ERR_WORKSPACE, "plan must be 16-byte aligned");
-  bp::CsrSplitArgs sa{indptr, indices, nullptr, nullptr, n_rows, static_cast<int32_t *>(plan),
-                      sp.n_tiles, sp.tile_cols, n_cols};
-  int64_t blocks = (n_rows + 7) / 8;
-  if (blocks > static_cast<int64_t>(sms) * 16) blocks = static_cast<int64_t>(sms) * 16;
-  bp::k_csr_split<<<static_cast<int>(blocks), 256, 0, as_stream(stream)>>>(sa);
-  return launched();
+  inf.n_tiles = sp.ok ? sp.n_tiles : 0;
+  if (info) *info = inf;
+  if (!sp.ok || n_rows == 0) return BP_OK;                   // nothing to precompute
+  BP_CHECK(indptr && indices && (plan || plan_bytes == 0), BP_ERR_INVALID_ARG,
+           "NULL indptr/indices/plan");
+  const size_t need = bp_csrmv_plan_bytes(n_rows, n_cols, out_kind, homo);
+  BP_CHECK(plan_bytes >= need, BP_ERR_WORKSPACE, "plan %zu bytes < %zu required", plan_bytes,
+           need);
+  BP_CHECK(need == 0 || aligned(plan, 16), BP_ERR_WORKSPACE, "plan must be 16-byte aligned");
+  int32_t *split = static_cast<int32_t *>(plan);
+  if (sp.n_tiles > 1) {
+    s = write_split(indptr, indices, n_rows, n_cols, sp, split, sms, st);
+    if (s != BP_OK) return s;
+  }
+  const StreamPlan s2 = stream_plan(n_rows, n_cols, out_kind, false, sms, true);
+  if (homo || out_kind != BP_OUT_F32 || !s2.ok || n_rows >= (int64_t{1} << 24) || !ws ||
+      ws_bytes < std::max(sp.ws_bytes, s2.ws_bytes) || !aligned(indices, 16) ||
+      !aligned(data, 16) || std::getenv("BP_CSR_NO_T4"))
+    return BP_OK;
+  // Rule T4 analysis: column sums of |w| over ALL rows (an fp32 atomic pass of
+  // the stream kernel with every row active) bound every partial sum of any
+  // call; from B = max column sum choose the largest F with
+  // B 2^(F-8) + 2 n_rows < 2^31, so hi words never overflow, and lo words stay
+  // below n_rows 2^8 < 2^32.
+  Ws w;
+  s = carve_ws(ws, ws_bytes, n_rows, &w);
+  if (s != BP_OK) return s;
+  const size_t colsum_off = s2.n_tiles > 1 ? s2.plan_bytes : 0;
+  float *colsum = reinterpret_cast<float *>(static_cast<char *>(plan) + colsum_off);
+  float *colmax = colsum + n_cols;
+  bp::CsrStreamArgs ca{indices, data, indptr, split, nullptr, nullptr, indptr + n_rows,
+                       static_cast<char *>(ws) + sp.partials_off, sp.tile_cols, sp.groups,
+                       sp.n_tiles, 0, n_cols, colsum, 1.f, 0, 0, 1, n_rows};
+  if (!launch_stream<0, false>(ca, sp, st)) {
+    bp::CsrTiledArgs t{};
+    t.out = colsum;
+    t.n_cols = n_cols;
+    t.tile_cols = sp.tile_cols;
+    t.groups = sp.groups;
+    t.partials = ca.partials;
+    bp::k_csr_reduce<0><<<static_cast<int>((n_cols + 255) / 256), 256, 0, st>>>(t, 0, 0);
+  }
+  k_max_f32<<<1, 1024, 0, st>>>(colsum, n_cols, colmax);
+  float bmax = 0.f;
+  BP_CUDA(cudaMemcpyAsync(&bmax, colmax, sizeof(float), cudaMemcpyDeviceToHost, st));
+  BP_CUDA(cudaStreamSynchronize(st));
+  if (!std::isfinite(bmax)) return BP_OK;
+  // the fp32 column sums carry <= n_rows 2^-24 relative rounding: 1 % margin
+  const double B = std::max(static_cast<double>(bmax) * 1.01, 1e-30);
+  const double room = 2147483648.0 - 2.0 * static_cast<double>(n_rows) - 16.0;
+  int F = static_cast<int>(std::floor(std::log2(room / B))) + 8;
+  if (F > 100) F = 100;
+  if (F >= 8 && B * std::ldexp(1.0, F - 8) + 2.0 * n_rows < 2147483648.0) {
+    inf.f32_fixed_bits = F;
+    inf.n_tiles = s2.n_tiles;
+    inf.max_col_abs_sum = bmax;
+    if (s2.n_tiles > 1) {
+      s = write_split(indptr, indices, n_rows, n_cols, s2, split, sms, st);
+      if (s != BP_OK) return s;
+    }
+  }
+  if (info) *info = inf;
+  return BP_OK;
 }
 
-bp_status bp_event_csrmv_planned(const void *plan, size_t plan_bytes, const int64_t *indptr,
+bp_status bp_event_csrmv_planned(const void *plan, size_t plan_bytes,
+                                 const bp_csrmv_plan_info *info, const int64_t *indptr,
                                  const int32_t *indices, const float *data, float w_homo,
                                  int64_t n_rows, int64_t n_cols, const uint32_t *spikes,
                                  void *out, int out_kind, uint32_t flags, void *ws,
                                  size_t ws_bytes, bp_stream stream) {
   return csrmv_impl(plan, plan_bytes, indptr, indices, data, w_homo, n_rows, n_cols, spikes,
-                    out, out_kind, flags, ws, ws_bytes, stream);
+                    out, out_kind, flags, ws, ws_bytes, stream,
+                    info ? info->f32_fixed_bits : -1);
 }
 
 bp_status bp_jitconn_event_mv_homo(const bp_jitconn *spec, float weight,
@@ -1228,6 +1337,7 @@ struct bp_network {
   // dense delivery: events as per-neuron atomic counts (cap 0), small
   // blocks (k_step_dense) -- compute-bound networks that fill few tiles
   bool dense = false;
+  bool debug_nan = false;         // BP_DEBUG_NAN=1: count non-finite V after every step
   // BP_EXCHANGE_NCCL: the library's own spike all-gather
   bool nccl = false;
   ncclComm_t comm = nullptr;
@@ -1383,7 +1493,8 @@ bp::ConnArgs make_conn(bp_network *net, std::vector<bp::NetProj> *table) {
   bp::ConnArgs c{};
   c.n_proj = d.n_proj;
   c.n_cols = static_cast<uint32_t>(d.n);
-  bool lane = true;
+  double e_seg = 0.0;      // most expected events of a row in one segment
+  uint32_t n_seg_max = 0;
   net->all_jit = true;
   table->assign(d.n_proj, bp::NetProj{});
   for (int p = 0; p < d.n_proj; ++p) {
@@ -1397,7 +1508,8 @@ bp::ConnArgs make_conn(bp_network *net, std::vector<bp::NetProj> *table) {
       t.j = jit_side(&P.jit, net->jr[p], BP_LAW_HOMO, P.weight, 0.f, d.col_begin, d.col_end,
                      nullptr);
       // expected events of one row in one segment: L * 2 / (K + 1)
-      lane = lane && net->jr[p].L * 2.0 / (net->jr[p].K + 1.0) <= 48.0;
+      e_seg = std::max(e_seg, net->jr[p].L * 2.0 / (net->jr[p].K + 1.0));
+      n_seg_max = std::max(n_seg_max, t.j.n_seg);
     } else {
       t.c.indptr = P.indptr;
       t.c.indices = P.indices;
@@ -1406,12 +1518,16 @@ bp::ConnArgs make_conn(bp_network *net, std::vector<bp::NetProj> *table) {
     }
   }
   c.all_jit = net->all_jit ? 1 : 0;
-  // One lane per row when a row has few events in this rank's segment
-  // (multi-GPU partitions: ~80/G per row): measured 3x faster at G = 8
-  // (220 k rows, 10 events per row-segment: 34 vs 99 us) but slower at
-  // G = 1 (80 events per row: 44 vs 34 us; tools/probes/probe_bin.cu).
-  const char *lr = std::getenv("BP_BIN_LANE_ROWS");
-  c.lane_rows = net->all_jit ? (lr ? std::atoi(lr) : (lane ? 1 : 0)) : 0;
+  // Binning work split (k_bin_sorted): a whole warp per row and segment
+  // (one step regenerates 128 gaps) or 4 lanes per (row, segment) item (16
+  // gaps per step, 8 items per warp in flight).  Measured per binning launch
+  // (tools/bin_group_ab.sh, B200): ~80 events per item (config 5) 29.6 vs
+  // 32.5 us -> warp; ~10 (config 3 with seg_len n/8, an 8-GPU partition)
+  // 16.6 vs 37.4 us and 110 vs 143 us per step -> 4 lanes; ~125 (Fig S3B
+  // with seg_len n/8) 18.1 vs 21.6 us -> 4 lanes; rows of ~1000 events keep
+  // the warp (63 steps of 16 gaps would serialise).
+  c.group_lanes = ((e_seg >= 48.0 && e_seg <= 112.0) || e_seg >= 512.0) ? 32 : 4;
+  c.n_seg_max = n_seg_max;
   return c;
 }
 
@@ -1652,6 +1768,9 @@ bp_status launch_step(bp_network *net, uint32_t *raster, cudaStream_t st,
   if (s != BP_OK) return s;
   if (mid) BP_CUDA(cudaEventRecord(mid, st));
   if (mid2) BP_CUDA(cudaEventRecord(mid2, st));
+  if (net->debug_nan)
+    bp::k_count_nonfinite<<<net->sms * 4, 256, 0, st>>>(d.state.v, net->n_local,
+                                                         net->counters + 3);
   s = launch_bin(net, net->active[1], net->count + 2 + cp, out_par, net->n_local, st);
   if (s != BP_OK) return s;
   net->steps_done += 1;
@@ -1813,6 +1932,7 @@ bp_status bp_network_create(const bp_network_desc *desc, bp_stream stream,
   net->sms = sms;
   net->delay = desc->delay_steps > 0 ? desc->delay_steps : 1;
   net->slots = net->delay + 1;
+  net->debug_nan = std::getenv("BP_DEBUG_NAN") && std::atoi(std::getenv("BP_DEBUG_NAN"));
   net->n_local = desc->col_end - desc->col_begin;
   net->local_words = (net->n_local + 31) / 32;
   net->global_words = desc->exchange == BP_EXCHANGE_NCCL
@@ -2021,7 +2141,7 @@ bp_status bp_network_counters(bp_network *net, uint64_t *host_out, bp_stream str
   if (net->nccl) {   // the comm stream's last gather is part of the state
     BP_CUDA(cudaStreamWaitEvent(st, net->ev_gath[(net->steps_done + 1) & 1], 0));
   }
-  BP_CUDA(cudaMemcpyAsync(host_out, net->counters, 3 * sizeof(uint64_t),
+  BP_CUDA(cudaMemcpyAsync(host_out, net->counters, 4 * sizeof(uint64_t),
                           cudaMemcpyDeviceToHost, st));
   BP_CUDA(cudaStreamSynchronize(st));
   return BP_OK;

@@ -212,6 +212,9 @@ struct CsrStreamArgs {
   void *out;                 // fused reduction (cooperative launch)
   float w;                   // homogeneous weight
   long long q;               // quantize(w)
+  int32_t fix_bits;          // KIND 2 (rule T4): weights accumulated at 2^-fix_bits
+  int32_t absw;              // accumulate |w| (bp_csrmv_plan's column bound)
+  int64_t n_rows_all;        // active == nullptr: every row 0 .. n_rows_all - 1
 };
 
 // Shared-memory layout (host and device agree through this function).
@@ -257,7 +260,7 @@ template <int KIND, bool HOMO, int NT, bool C16 = false>
 __device__ __forceinline__ void tile_reduce(const void *partials, size_t first, int group,
                                             int groups, int used, int tile_cols, int width,
                                             int64_t c0, void *out, int accumulate, float w,
-                                            long long q) {
+                                            long long q, int fix_bits = 0) {
   const int per = (width + groups - 1) / groups;
   const int s0 = group * per, s1 = min(width, s0 + per);
   const size_t stride = static_cast<size_t>(tile_cols);
@@ -286,6 +289,18 @@ __device__ __forceinline__ void tile_reduce(const void *partials, size_t first, 
       const float *p = static_cast<const float *>(partials) + base + cc;
       float v = 0.f;
       for (int g = 0; g < used; ++g) v = __fadd_rn(v, __ldcg(p + g * stride));
+      float *o = static_cast<float *>(out) + c;
+      *o = accumulate ? __fadd_rn(*o, v) : v;
+    } else if (KIND == 2) {
+      const int2 *p = static_cast<const int2 *>(partials) + base + cc;
+      long long hi = 0;
+      unsigned long long lo = 0;
+      for (int g = 0; g < used; ++g) {
+        const int2 x = __ldcg(p + g * stride);
+        hi += x.x;
+        lo += static_cast<unsigned>(x.y);
+      }
+      const float v = fix2_value(hi, lo, fix_bits);
       float *o = static_cast<float *>(out) + c;
       *o = accumulate ? __fadd_rn(*o, v) : v;
     } else {
@@ -321,6 +336,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs 
   const int64_t c1 = min(c0 + a.tile_cols, a.n_cols);
   const int width = static_cast<int>(c1 - c0);
   const int32_t c0i = static_cast<int32_t>(c0);
+  const float fix_scale = __int_as_float((127 + (KIND == 2 ? a.fix_bits : 0)) << 23);  // 2^fix_bits
   CSR_MARK(0);
 
   const int n_zero32 = ((width + 1) * acc_bytes + 3) / 4;      // tile + sink slot
@@ -344,7 +360,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs 
       lo_r = 0;
       hi_r = 0;
       if (k < n_active) {
-        const int64_t r = list_smem ? list[k] : __ldg(list + k);
+        const int64_t r = list == nullptr ? k : (list_smem ? list[k] : __ldg(list + k));
         const int64_t p0 = __ldg(a.indptr + r), p1 = __ldg(a.indptr + r + 1);
         const int32_t *sp = a.split + r * (nt - 1) - 1;      // sp[t], t = 1 .. nt-1
         lo_r = tile > 0 ? p0 + __ldg(sp + tile) : p0;
@@ -423,8 +439,15 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs 
       const uint32_t lc = min(static_cast<uint32_t>(col - c0i), static_cast<uint32_t>(width));
       if (C16) atomicAdd(reinterpret_cast<uint32_t *>(sm) + (lc >> 1), 1u << ((lc & 1u) * 16u));
       else if (HOMO) atomicAdd(reinterpret_cast<uint32_t *>(sm) + lc, 1u);
-      else if (KIND == 0) atomicAdd(reinterpret_cast<float *>(sm) + lc, wgt);
-      else {
+      else if (KIND == 0) atomicAdd(reinterpret_cast<float *>(sm) + lc, a.absw ? fabsf(wgt) : wgt);
+      else if (KIND == 2) {
+        // rule T4: q = rint(w 2^fix_bits) as hi = q >> 8 and lo = q & 255,
+        // two independent native 32-bit ATOMS (no carry, no return value)
+        const long long qq = __float2ll_rn(__fmul_rn(wgt, fix_scale));
+        unsigned *p = reinterpret_cast<unsigned *>(sm) + 2 * lc;
+        atomicAdd(p, static_cast<unsigned>(static_cast<int>(qq >> 8)));
+        atomicAdd(p + 1, static_cast<unsigned>(qq & 255));
+      } else {
         // int64 add as two native 32-bit ATOMS (a 64-bit shared add is a CAS
         // loop on sm_100a): low word with return, carry into the high word --
         // exact modulo 2^64, like an int64 add
@@ -489,7 +512,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs 
   // rows from the active list: warp w of the tile takes k = w, w + NW, ... --
   // dealt evenly over the tile's CTAs (a per-CTA compaction of its slice of
   // the spike words avoids the compaction launch but leaves ~12 % imbalance)
-  const int64_t n_active_rows = *a.count;
+  const int64_t n_active_rows = a.active ? static_cast<int64_t>(*a.count) : a.n_rows_all;
   stream_rows(a.active, false, n_active_rows, static_cast<int64_t>(group) * kStreamWarps + warp,
               static_cast<int64_t>(a.groups) * kStreamWarps);
   CSR_MARK(2);
@@ -519,7 +542,7 @@ __global__ void __launch_bounds__(kStreamThreads, 1) k_csr_stream(CsrStreamArgs 
   CSR_MARK(5);
   tile_reduce<KIND, HOMO, kStreamThreads, C16>(a.partials, static_cast<size_t>(tile) * a.groups,
                                                group, a.groups, used, a.tile_cols, width, c0,
-                                               a.out, a.accumulate, a.w, a.q);
+                                               a.out, a.accumulate, a.w, a.q, a.fix_bits);
   CSR_MARK(6);
 }
 

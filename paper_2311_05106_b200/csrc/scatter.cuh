@@ -296,7 +296,18 @@ struct CsrTiledArgs {
   void *partials;             // nullable: [tile][group][tile_cols] partial sums
   int accumulate;             // reduce: out += sum (else out = sum)
   int vec;                    // indices (and data) 16-byte aligned: 128-bit loads
+  int32_t fix_bits;           // KIND 2 partials (k_csr_stream): fixed point 2^-fix_bits
 };
+
+// Rule T4 (heterogeneous fp32 output through scaled fixed point): a column's
+// partial is a (hi int32, lo uint32) pair with value hi 2^8 + lo in units
+// of 2^-fix_bits (each weight w adds q = rint(w 2^fix_bits) as hi = q >> 8,
+// lo = q & 255: two independent native 32-bit shared atomics, exact, and
+// order-free).  The sum of a column is rounded to fp32 once.
+__device__ __forceinline__ float fix2_value(long long hi, unsigned long long lo, int fix_bits) {
+  const long long t = hi * 256 + static_cast<long long>(lo);
+  return __fmul_rn(__ll2float_rn(t), __int_as_float((127 - fix_bits) << 23));
+}
 
 template <int KIND>
 __global__ void __launch_bounds__(kTiledThreads, 1)
@@ -469,6 +480,18 @@ k_csr_reduce(CsrTiledArgs a, int homo, int c16 = 0) {
     const float *p = static_cast<const float *>(a.partials) + base;
     float v = 0.f;
     for (int g = 0; g < a.groups; ++g) v = __fadd_rn(v, __ldcs(p + g * stride));
+    float *o = static_cast<float *>(a.out) + c;
+    *o = a.accumulate ? __fadd_rn(*o, v) : v;
+  } else if (KIND == 2) {
+    const int2 *p = static_cast<const int2 *>(a.partials) + base;
+    long long hi = 0;
+    unsigned long long lo = 0;
+    for (int g = 0; g < a.groups; ++g) {
+      const int2 x = __ldcs(p + g * stride);
+      hi += x.x;
+      lo += static_cast<unsigned>(x.y);
+    }
+    const float v = fix2_value(hi, lo, a.fix_bits);
     float *o = static_cast<float *>(a.out) + c;
     *o = a.accumulate ? __fadd_rn(*o, v) : v;
   } else {

@@ -127,7 +127,8 @@ struct ConnArgs {
   int n_proj;
   int all_jit;              // every projection is JIT (the warp-batched path)
   uint32_t n_cols;          // all neurons (columns of every projection)
-  int lane_rows;            // JIT fan-out per segment small: one lane per row
+  int group_lanes;          // JIT: lanes per (row, segment) item (4, 8 or 32)
+  uint32_t n_seg_max;       // JIT: most local segments of any projection
 };
 
 __device__ __forceinline__ bool proj_has(const NetProj *P, int64_t r, uint32_t &row) {
@@ -594,7 +595,7 @@ template <int MODEL, int KIND, int NCLS>
 #endif
 __global__ void __launch_bounds__(MODEL == 0 ? kStepThreads : 512, MODEL == 0 ? BP_STEP_MINB : 1)
 k_step(StepArgs a) {
-  extern __shared__ int32_t cnt[];          // [NCLS][kTile]
+  extern __shared__ __align__(16) int32_t cnt[];   // [NCLS][kTile]
   __shared__ unsigned long long block_sp;
   const int tid = threadIdx.x;
   constexpr int nthreads = MODEL == 0 ? kStepThreads : 512;
@@ -673,7 +674,7 @@ constexpr int kDenseThreads = 128;
 template <int MODEL, int KIND>
 __global__ void __launch_bounds__(kDenseThreads, MODEL == 0 ? 8 : 4)
 k_step_dense(StepArgs a) {
-  __shared__ int32_t cnt[2 * 4 * kDenseThreads];   // class 0 (E), class 1 (I)
+  __shared__ __align__(16) int32_t cnt[2 * 4 * kDenseThreads];   // class 0 (E), class 1 (I)
   __shared__ unsigned long long block_sp;
   const int tid = threadIdx.x;
   const uint32_t lane = tid & 31u;
@@ -798,6 +799,18 @@ __global__ void __launch_bounds__(kHHThreads, 8) k_hh_dense1(StepArgs a) {
     sat = __reduce_add_sync(0xffffffffu, sat);
     if (lane == 0 && sat) atomicAdd(a.saturated, static_cast<unsigned long long>(sat));
   }
+}
+
+// Debug check (BP_DEBUG_NAN=1, the SPEC's NaN abort turned into a counter):
+// counts the non-finite membrane potentials after a step.
+__global__ void __launch_bounds__(256) k_count_nonfinite(const float *v, int64_t n,
+                                                         unsigned long long *counter) {
+  uint32_t bad = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    bad += isfinite(v[i]) ? 0u : 1u;
+  bad = __reduce_add_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31u) == 0 && bad) atomicAdd(counter, static_cast<unsigned long long>(bad));
 }
 
 // Remote (or initial) spikes: bin the events of every active row in
@@ -1042,54 +1055,114 @@ __device__ __forceinline__ uint32_t stage_rows_jit(const ConnArgs &c, const BinT
   return ev;
 }
 
-// JIT rows with a small fan-out per segment (the network's ~80): ONE LANE
-// per row.  The lane walks its row's gap chain itself, two Philox blocks
-// (8 gaps) per iteration; the blocks do not depend on the running position,
-// so their 10-round chains overlap (ILP) and no cross-lane scan is needed.
-__device__ __forceinline__ uint32_t stage_row_lane(const ConnArgs &c, const BinTarget &b,
-                                                   int64_t r, uint32_t *staged,
-                                                   int32_t *n_staged, int32_t *hist) {
+// JIT items (active row k, segment sidx) of every projection the row
+// belongs to, S lanes per item (32 / S items per warp at a time) -- for
+// networks whose rows have few events per segment (the ~10 of a multi-GPU
+// partition or of a strong-scaling segment), where a whole warp per row
+// would regenerate 128 gaps for 10 events.  The first 32 / S lanes compute
+// the stationary first offsets of the warp's items (one Philox each); lane
+// q of an item then draws Philox block `chunk * S + q` (4 gaps) and a scan
+// over the S lanes turns the gaps into positions (4 S gaps per step).
+// Positions grow with (lane, k) within an item, so an item's valid events
+// are a prefix; the staging slots come from one warp-wide scan of the
+// per-lane counts and one shared atomic per warp and step.
+template <int S>
+__device__ __forceinline__ uint32_t stage_items(const ConnArgs &c, const BinTarget &b,
+                                                const int32_t *active, int r_lo, int r_hi,
+                                                uint32_t n_seg_max, uint32_t *staged,
+                                                int32_t *n_staged, int32_t *hist) {
+  constexpr int IPW = 32 / S;                 // items per warp
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t sub = lane & (S - 1);
+  const uint32_t gi = lane / S;               // item slot of this lane's group
+  const int64_t n_items = static_cast<int64_t>(r_hi - r_lo) * n_seg_max;
+  const int64_t stride = (kBinThreads / 32) * IPW;
   uint32_t ev = 0;
-  for (int p = 0; p < c.n_proj; ++p) {
-    const NetProj *P = c.proj + p;
-    uint32_t row;
-    if (!proj_has(P, r, row)) continue;
-    const uint32_t cls = __ldg(&P->cls);
-    const JitSide s = load_jit(P);
-    for (uint32_t sidx = 0; sidx < s.n_seg; ++sidx) {
-      const uint32_t seg = s.seg_first + sidx;
+  for (int64_t base = (threadIdx.x >> 5) * IPW; base < n_items; base += stride) {
+    // lane j < IPW decodes item base + j (first offsets); every lane its group's
+    const int64_t it_l = base + (lane < IPW ? lane : 0);
+    const bool have_l = lane < IPW && it_l < n_items;
+    const int64_t r_l = have_l ? active[r_lo + it_l / n_seg_max] : -1;
+    const uint32_t sidx_l = have_l ? static_cast<uint32_t>(it_l % n_seg_max) : 0u;
+    for (int p = 0; p < c.n_proj; ++p) {
+      const NetProj *P = c.proj + p;
+      uint32_t row_l = 0;
+      const JitSide s = load_jit(P);
+      const bool mem_l = have_l && proj_has(P, r_l, row_l) && sidx_l < s.n_seg;
+      if (!__ballot_sync(0xffffffffu, mem_l)) continue;
+      const uint32_t cbits = __ldg(&P->cls) << kClsShift;
+      uint32_t first_l = 0;
+      if (mem_l) {
+        const uint32_t seg = s.seg_first + sidx_l;
+        first_l = seg * s.L + first_offset(s.seed, s.K, row_l, seg);
+      }
+      // this lane's item (group gi)
+      const bool mine = __shfl_sync(0xffffffffu, static_cast<int>(mem_l), gi) != 0;
+      const uint32_t row = __shfl_sync(0xffffffffu, row_l, gi);
+      const uint32_t seg = s.seg_first + __shfl_sync(0xffffffffu, sidx_l, gi);
+      const uint32_t first = __shfl_sync(0xffffffffu, first_l, gi);
       const uint32_t seg_end = min(seg * s.L + s.L, c.n_cols);
-      uint32_t pos = seg * s.L + first_offset(s.seed, s.K, row, seg);
-      for (uint32_t blk = 0; pos < seg_end; blk += 2) {
-        const u32x4 x = philox_block(s.seed, kTagGap, row, seg, blk);
-        const u32x4 y = philox_block(s.seed, kTagGap, row, seg, blk + 1);
-        uint32_t e[8];
-        e[0] = pos;
-        e[1] = e[0] + bounded(1u, s.K, x.x);
-        e[2] = e[1] + bounded(1u, s.K, x.y);
-        e[3] = e[2] + bounded(1u, s.K, x.z);
-        e[4] = e[3] + bounded(1u, s.K, x.w);
-        e[5] = e[4] + bounded(1u, s.K, y.x);
-        e[6] = e[5] + bounded(1u, s.K, y.y);
-        e[7] = e[6] + bounded(1u, s.K, y.z);
-        pos = e[7] + bounded(1u, s.K, y.w);
-        int nv = 0;
+      uint32_t start = mine ? first : seg_end;
+      uint32_t chunk = 0;
+      while (__any_sync(0xffffffffu, start < seg_end)) {
+        // finished groups compute along (their results are masked off)
+        const bool go = start < seg_end;              // uniform within the group
+        const u32x4 g = philox_block(s.seed, kTagGap, row, seg, chunk * S + sub);
+        const uint32_t g0 = bounded(1u, s.K, g.x), g1 = bounded(1u, s.K, g.y);
+        const uint32_t g2 = bounded(1u, s.K, g.z), g3 = bounded(1u, s.K, g.w);
+        const uint32_t p1 = g0, p2 = g0 + g1, p3 = p2 + g2, t = p3 + g3;
+        uint32_t incl_g = t;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) nv += e[k] < seg_end;
-        int slot = atomicAdd(n_staged, nv);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          if (e[k] >= seg_end) break;
-          const uint32_t loc = e[k] - b.col_begin;
-          if (slot < kBinStage) {
-            staged[slot] = stage_record(cls, loc);
-            atomicAdd(hist + (loc >> kTileShift), 1);
-          } else {
-            bin_event(b, cls, loc);
-          }
-          ++slot;
-          ++ev;
+        for (int off = 1; off < S; off <<= 1) {
+          const uint32_t v = __shfl_up_sync(0xffffffffu, incl_g, off, S);
+          if (sub >= static_cast<uint32_t>(off)) incl_g += v;
         }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl_g, S - 1, S);
+        const uint32_t pos0 = start + (incl_g - t);
+        uint32_t pos[4] = {pos0, pos0 + p1, pos0 + p2, pos0 + p3};
+        if (!go) pos[0] = pos[1] = pos[2] = pos[3] = seg_end;
+        uint32_t nv = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) nv += pos[k] < seg_end;
+        // warp-wide exclusive scan of the per-lane counts -> staging slots
+        uint32_t incl = nv;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= static_cast<uint32_t>(off)) incl += v;
+        }
+        const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
+        int slot0 = 0;
+        if (lane == 31 && wtot) slot0 = atomicAdd(n_staged, static_cast<int>(wtot));
+        slot0 = __shfl_sync(0xffffffffu, slot0, 31);
+        int slot = slot0 + static_cast<int>(incl - nv);
+        if (slot0 + static_cast<int>(wtot) <= kBinStage) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (pos[k] < seg_end) {
+              const uint32_t loc = pos[k] - b.col_begin;
+              staged[slot++] = cbits | loc;
+              atomicAdd(hist + (loc >> kTileShift), 1);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (pos[k] < seg_end) {
+              const uint32_t loc = pos[k] - b.col_begin;
+              if (slot < kBinStage) {
+                staged[slot] = cbits | loc;
+                atomicAdd(hist + (loc >> kTileShift), 1);
+              } else {
+                bin_event(b, cbits >> kClsShift, loc);
+              }
+              ++slot;
+            }
+          }
+        }
+        ev += nv;
+        start += total;
+        ++chunk;
       }
     }
   }
@@ -1166,9 +1239,9 @@ k_bin_sorted(ConnArgs conn, BinTarget out, const int32_t *active, const int32_t 
   if (!conn.all_jit) {
     for (int k = r_lo + static_cast<int>(warp); k < r_hi; k += kBinThreads / 32)
       ev += stage_row(conn, out, active[k], staged, &n_staged, hist);
-  } else if (conn.lane_rows) {
-    for (int k = r_lo + tid; k < r_hi; k += kBinThreads)
-      ev += stage_row_lane(conn, out, active[k], staged, &n_staged, hist);
+  } else if (conn.group_lanes < 32) {
+    // few events per (row, segment): 4 lanes per item
+    ev = stage_items<4>(conn, out, active, r_lo, r_hi, conn.n_seg_max, staged, &n_staged, hist);
   } else {
     // warp w takes rows r_lo + w + 32 i (i = 0, 1, ...), 32 rows per batch
     for (int k0 = r_lo + static_cast<int>(warp); k0 < r_hi; k0 += kBinThreads)

@@ -77,6 +77,22 @@ def exchange_spikes(words: torch.Tensor, part: Partition, group=None,
     return words
 
 
+def share_nccl_id(rank: int, world: int, group=None, make_id=None) -> bytes:
+    """The 128-byte ncclUniqueId of a BP_EXCHANGE_NCCL network: rank 0 makes
+    it (bp_nccl_unique_id), every rank receives the same bytes over the
+    torch.distributed process group (any backend)."""
+    make_id = make_id or B.nccl_unique_id
+    nccl_id = make_id() if rank == 0 else None
+    if world > 1:
+        import torch.distributed as dist
+        obj = [nccl_id]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        nccl_id = obj[0]
+    if not isinstance(nccl_id, (bytes, bytearray)) or len(nccl_id) != 128:
+        raise ValueError("ncclUniqueId must be 128 bytes")
+    return bytes(nccl_id)
+
+
 @dataclass(frozen=True)
 class ProjSpec:
     """One projection of a network (bp_projection): the spikes of neurons
@@ -192,12 +208,7 @@ class CobaNetwork:
         self.exchange = exchange
         kw = {}
         if exchange == "nccl":
-            nccl_id = B.nccl_unique_id() if rank == 0 else None
-            if world > 1:
-                import torch.distributed as dist
-                obj = [nccl_id]
-                dist.broadcast_object_list(obj, src=0, group=group)
-                nccl_id = obj[0]
+            nccl_id = share_nccl_id(rank, world, group)
             kw = dict(exchange=B.EXCHANGE_NCCL, rank=rank, world=world,
                       part_len=self.part.local, nccl_id=nccl_id)
         elif exchange != "caller":

@@ -101,3 +101,28 @@ def test_two_rank_gloo_equals_single_process(orc, tmp_path):
     assert np.array_equal(raster[0], want)
     v = np.concatenate([np.load(tmp_path / f"v_{r}.npy") for r in range(world)])
     assert np.array_equal(v.view(np.uint32), st["v"].view(np.uint32))
+
+
+def _id_rank(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2311_05106_b200.network import share_nccl_id
+    # rank 0's id (a stand-in for bp_nccl_unique_id: no GPU here) reaches every rank
+    got = share_nccl_id(rank, world, make_id=lambda: bytes(range(128)))
+    with open(os.path.join(out_dir, f"id_{rank}.bin"), "wb") as f:
+        f.write(got)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_nccl_id_reaches_every_rank(tmp_path):
+    """BP_EXCHANGE_NCCL setup (network.share_nccl_id): rank 0 creates the
+    128-byte ncclUniqueId and the process group broadcasts it, so every
+    rank's bp_network_create gets the same bytes."""
+    world = 3
+    mp.start_processes(_id_rank, args=(world, _free_port(), str(tmp_path)), nprocs=world,
+                       join=True, start_method="spawn")
+    ids = [(tmp_path / f"id_{r}.bin").read_bytes() for r in range(world)]
+    assert all(i == bytes(range(128)) for i in ids)

@@ -227,7 +227,7 @@ def test_config2_csr_p005_hetero_full_size(bp, orc):
         out = torch.zeros(n, dtype=torch.int64, device="cuda")
         out32 = torch.zeros(n, dtype=torch.float32, device="cuda")
         for o in (out, out32):
-            plan = bp.csrmv_plan(tip, tix, n, n, o.dtype, homo=False) if planned else None
+            plan = bp.csrmv_plan(tip, tix, n, n, o.dtype, homo=False, data=tdat) if planned else None
             ws = torch.empty(bp.lib().bp_csrmv_workspace_bytes(n, n, 1 if o.dtype == torch.int64
                                                                else 0),
                              dtype=torch.uint8, device="cuda")

@@ -102,8 +102,8 @@ def test_event_csrmv(bp, orc, case, path, monkeypatch):
         tdat = None if tdat is None else torch.cat([tdat.new_zeros(1), tdat])[1:]
     plan64 = plan32 = None
     if path == "planned":
-        plan64 = bp.csrmv_plan(tip, tix, n_rows, n_cols, torch.int64, homo=tdat is None)
-        plan32 = bp.csrmv_plan(tip, tix, n_rows, n_cols, torch.float32, homo=tdat is None)
+        plan64 = bp.csrmv_plan(tip, tix, n_rows, n_cols, torch.int64, homo=tdat is None, data=tdat)
+        plan32 = bp.csrmv_plan(tip, tix, n_rows, n_cols, torch.float32, homo=tdat is None, data=tdat)
     # fixed point: bit-exact
     out = torch.zeros(n_cols, dtype=torch.int64, device="cuda")
     bp.event_csrmv(tip, tix, tdat, w_homo, n_rows, n_cols, spikes, out, plan=plan64)
@@ -477,3 +477,49 @@ def test_event_csrmv_homo_counts_16_bit_boundary(bp, n_rows, c16, monkeypatch):
         assert torch.all(out == n_rows * (2 ** 30)).item()
     del indices
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("scale", [1.0, 1e-4, 1e4])
+def test_csrmv_plan_t4_fixed_point_fp32(bp, orc, scale):
+    """Rule T4: a planned heterogeneous fp32 event_csrmv accumulates
+    rint(w 2^F) exactly in two 32-bit words per column (F from the plan's
+    column bound) and rounds once: within rule T2 of the fp64 definition,
+    bitwise identical from call to call (order-free), and ACCUMULATE adds."""
+    n_rows, n_cols = 3000, 50_000
+    ip, ix, dat = inputs.random_csr(n_rows, n_cols, 0.05, seed=11, weights="uniform",
+                                    w0=-scale, w1=scale)
+    tip, tix, tdat = _t(ip), _t(ix), _t(dat)
+    plan = bp.csrmv_plan(tip, tix, n_rows, n_cols, torch.float32, homo=False, data=tdat)
+    assert plan is not None and plan.f32_fixed_bits >= 8
+    assert plan.info.max_col_abs_sum > 0
+    ev = inputs.spike_pattern(n_rows, 0.3, 4)
+    spikes = _dev_spikes(ev)
+    a = torch.zeros(n_cols, dtype=torch.float32, device="cuda")
+    b = torch.zeros_like(a)
+    bp.event_csrmv(tip, tix, tdat, 0.0, n_rows, n_cols, spikes, a, plan=plan)
+    bp.event_csrmv(tip, tix, tdat, 0.0, n_rows, n_cols, spikes, b, plan=plan)
+    assert torch.equal(a.view(torch.int32), b.view(torch.int32))
+    ref, absw = orc.event_csrmv(ip, ix, dat, 0.0, n_rows, n_cols, ev, orc.OUT_F64, with_abs=True)
+    err = np.abs(a.cpu().numpy().astype(np.float64) - ref)
+    assert np.all(err <= 1e-5 * absw + 1e-30)
+    c = torch.full((n_cols,), 7.0 * scale, dtype=torch.float32, device="cuda")
+    bp.event_csrmv(tip, tix, tdat, 0.0, n_rows, n_cols, spikes, c, plan=plan, accumulate=True)
+    err = np.abs(c.cpu().numpy().astype(np.float64) - (ref + np.float32(7.0 * scale)))
+    assert np.all(err <= 1e-5 * (absw + 7.0 * scale))
+
+
+def test_csrmv_plan_t4_falls_back_for_unbounded_sums(bp, orc):
+    """Column sums too large for the 2^31 range of the high words (|w| ~ 1e30)
+    keep the fp32-atomic path (f32_fixed_bits = -1), still within T2."""
+    n_rows, n_cols = 2000, 40_000
+    ip, ix, dat = inputs.random_csr(n_rows, n_cols, 0.05, seed=12, weights="uniform",
+                                    w0=-1e30, w1=1e30)
+    tip, tix, tdat = _t(ip), _t(ix), _t(dat)
+    plan = bp.csrmv_plan(tip, tix, n_rows, n_cols, torch.float32, homo=False, data=tdat)
+    assert plan is not None and plan.f32_fixed_bits == -1
+    ev = inputs.spike_pattern(n_rows, 0.2, 5)
+    out = torch.zeros(n_cols, dtype=torch.float32, device="cuda")
+    bp.event_csrmv(tip, tix, tdat, 0.0, n_rows, n_cols, _dev_spikes(ev), out, plan=plan)
+    ref, absw = orc.event_csrmv(ip, ix, dat, 0.0, n_rows, n_cols, ev, orc.OUT_F64, with_abs=True)
+    err = np.abs(out.cpu().numpy().astype(np.float64) - ref)
+    assert np.all(err <= 1e-5 * absw + 1e-30)
