@@ -293,6 +293,11 @@ bp_status bp_jitconn_mv_normal(const bp_jitconn *spec, float w_mu, float w_sigma
 bp_status bp_jitconn_row_counts(const bp_jitconn *spec, int64_t n_rows,
                                 int64_t n_cols, int64_t *counts,
                                 bp_stream stream);
+/* indptr (int64[n_rows+1]) of the implied matrix: row counts and their
+ * exclusive prefix sum, on the device (the CSR row pointer that
+ * bp_jitconn_materialize takes). */
+bp_status bp_jitconn_indptr(const bp_jitconn *spec, int64_t n_rows, int64_t n_cols,
+                            int64_t *indptr, bp_stream stream);
 bp_status bp_jitconn_materialize(const bp_jitconn *spec, int law, float w0,
                                  float w1, int64_t n_rows, int64_t n_cols,
                                  const int64_t *indptr, int32_t *indices,

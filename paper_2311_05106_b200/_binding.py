@@ -30,7 +30,7 @@ EXPORTED = [
     "bp_jitconn_workspace_bytes", "bp_jitconn_mv_homo", "bp_jitconn_mv_uniform",
     "bp_jitconn_mv_normal", "bp_csrmv_gather", "bp_event_csrmv_grad",
     "bp_jitconn_event_mv_homo", "bp_jitconn_event_mv_uniform",
-    "bp_jitconn_event_mv_normal", "bp_jitconn_row_counts",
+    "bp_jitconn_event_mv_normal", "bp_jitconn_row_counts", "bp_jitconn_indptr",
     "bp_jitconn_materialize", "bp_neuron_step", "bp_network_workspace_bytes",
     "bp_network_create", "bp_network_step", "bp_network_scatter",
     "bp_network_update", "bp_network_update_overlap", "bp_network_counters", "bp_network_profile_begin",
@@ -144,6 +144,7 @@ def lib():
         L.bp_jitconn_mv_uniform.argtypes = [ctypes.POINTER(JitConn), f32, f32, P] + jit_tail[1:]
         L.bp_jitconn_mv_normal.argtypes = [ctypes.POINTER(JitConn), f32, f32, P] + jit_tail[1:]
         L.bp_jitconn_row_counts.argtypes = [ctypes.POINTER(JitConn), i64, i64, P, P]
+        L.bp_jitconn_indptr.argtypes = [ctypes.POINTER(JitConn), i64, i64, P, P]
         L.bp_jitconn_materialize.argtypes = [ctypes.POINTER(JitConn), i32, f32, f32,
                                              i64, i64, P, P, P, P]
         L.bp_neuron_step.argtypes = [ctypes.POINTER(NeuronParams),
@@ -382,11 +383,9 @@ def jitconn_materialize(spec: JitConn, n_rows: int, n_cols: int, law=LAW_HOMO,
                         w0=1.0, w1=0.0, with_data=True, device=None, stream=None):
     """CSR of the implied matrix, generated by the kernels' own generator."""
     device = device or torch.cuda.current_device()
-    counts = torch.empty(n_rows, dtype=torch.int64, device=device)
-    _check(lib().bp_jitconn_row_counts(ctypes.byref(spec), int(n_rows), int(n_cols),
-                                       _ptr(counts), _stream(stream)))
-    indptr = torch.zeros(n_rows + 1, dtype=torch.int64, device=device)
-    torch.cumsum(counts, 0, out=indptr[1:])
+    indptr = torch.empty(n_rows + 1, dtype=torch.int64, device=device)
+    _check(lib().bp_jitconn_indptr(ctypes.byref(spec), int(n_rows), int(n_cols),
+                                   _ptr(indptr), _stream(stream)))
     nnz = int(indptr[-1].item())
     indices = torch.empty(max(nnz, 1), dtype=torch.int32, device=device)
     data = torch.empty(max(nnz, 1), dtype=torch.float32, device=device) if with_data else None

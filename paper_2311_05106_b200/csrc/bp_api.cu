@@ -1126,6 +1126,48 @@ bp_status bp_jitconn_row_counts(const bp_jitconn *spec, int64_t n_rows,
   return launched();
 }
 
+}  // extern "C"
+
+namespace {
+// In-place inclusive scan of v[1..n] with v[0] = 0 (one block: the exclusive
+// prefix of the row counts, i.e. a CSR indptr).
+__global__ void __launch_bounds__(1024) k_indptr_scan(int64_t *v, int64_t n) {
+  __shared__ long long part[1024];
+  const int64_t per = (n + 1023) / 1024;
+  const int64_t lo = 1 + threadIdx.x * per, hi = min(n + 1, lo + per);
+  long long sum = 0;
+  for (int64_t i = lo; i < hi; ++i) sum += v[i];
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long run = 0;
+    for (int t = 0; t < 1024; ++t) {
+      const long long x = part[t];
+      part[t] = run;
+      run += x;
+    }
+    v[0] = 0;
+  }
+  __syncthreads();
+  long long run = part[threadIdx.x];
+  for (int64_t i = lo; i < hi; ++i) {
+    run += v[i];
+    v[i] = run;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+bp_status bp_jitconn_indptr(const bp_jitconn *spec, int64_t n_rows, int64_t n_cols,
+                            int64_t *indptr, bp_stream stream) {
+  BP_CHECK(indptr != nullptr, BP_ERR_INVALID_ARG, "indptr is NULL");
+  bp_status s = bp_jitconn_row_counts(spec, n_rows, n_cols, indptr + 1, stream);
+  if (s != BP_OK) return s;
+  k_indptr_scan<<<1, 1024, 0, as_stream(stream)>>>(indptr, n_rows);
+  return launched();
+}
+
 bp_status bp_jitconn_materialize(const bp_jitconn *spec, int law, float w0,
                                  float w1, int64_t n_rows, int64_t n_cols,
                                  const int64_t *indptr, int32_t *indices,
@@ -1712,8 +1754,43 @@ bp_status launch_k_step(const bp::StepArgs &a, int grid, cudaStream_t st) {
   return BP_OK;
 }
 
+// Persistent k_step (LIF): one resident wave of blocks taking tiles from
+// a per-step counter.  Measured (tools/persist_ab.sh, B200): f32 config 5
+// (3052 tiles, 5.2 waves) 63.8 -> 61.8 us; but config 3 (977 tiles) 23.5 ->
+// 24.9 us and the fixed-point kinds slower (fix32 71.9 -> 79.4, fix64
+// 95.9 -> 133.4: the int64 state spills) -- so only fp32 state with at
+// least 4 waves of tiles uses it (BP_STEP_PERSIST=0/1 overrides).
+template <int KIND, int NCLS>
+bp_status launch_k_step_persist(const bp::StepArgs &a, int sms, cudaStream_t st) {
+  constexpr size_t smem = static_cast<size_t>(NCLS) * bp::kTile * sizeof(int32_t);
+  static std::atomic<uint64_t> attr{0};
+  static int per_sm[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (first_on_device(attr)) {
+    if (smem > 48 * 1024)
+      BP_CUDA(cudaFuncSetAttribute(bp::k_step_persist<0, KIND, NCLS>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+    int b = 0;
+    BP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, bp::k_step_persist<0, KIND, NCLS>,
+                                                          bp::kStepThreads, smem));
+    per_sm[dev & 63] = b > 0 ? b : 1;
+  }
+  int grid = sms * per_sm[dev & 63];
+  if (grid > static_cast<int>(a.n_tiles)) grid = static_cast<int>(a.n_tiles);
+  BP_CUDA(launch_pdl(bp::k_step_persist<0, KIND, NCLS>, grid, bp::kStepThreads, smem, st, a));
+  return BP_OK;
+}
+
 template <int MODEL, int KIND>
-bp_status launch_k_step_n(const bp::StepArgs &a, int ncls, int grid, cudaStream_t st) {
+bp_status launch_k_step_n(const bp::StepArgs &a, int ncls, int grid, cudaStream_t st, int sms) {
+  const char *env = std::getenv("BP_STEP_PERSIST");
+  const bool persist = env ? std::atoi(env) != 0
+                           : (KIND == 0 && a.n_tiles >= static_cast<uint32_t>(4 * 4 * sms));
+  if (MODEL == 0 && persist)
+    return ncls == 2 ? launch_k_step_persist<KIND, 2>(a, sms, st)
+                     : launch_k_step_persist<KIND, bp::kMaxCls>(a, sms, st);
   return ncls == 2 ? launch_k_step<MODEL, KIND, 2>(a, grid, st)
                    : launch_k_step<MODEL, KIND, bp::kMaxCls>(a, grid, st);
 }
@@ -1738,6 +1815,8 @@ bp_status launch_step(bp_network *net, uint32_t *raster, cudaStream_t st,
   a.active = net->active[1];
   a.active_count = net->count + 2 + cp;
   a.zero_count = net->count + 2 + (cp ^ 1);
+  a.tile_counter = net->count + 4 + cp;           // k_step_persist's tile scheduler
+  a.zero_tile_counter = net->count + 4 + (cp ^ 1);
   const int grid = static_cast<int>(net->n_tiles);
   bp_status s = BP_OK;
   if (net->dense) {
@@ -1755,13 +1834,13 @@ bp_status launch_step(bp_network *net, uint32_t *raster, cudaStream_t st,
       else BP_CUDA(launch_pdl(bp::k_hh_dense1<0>, hgrid, bp::kHHThreads, 0, st, a));
     }
   } else if (d.model == BP_MODEL_LIF) {
-    if (d.g_kind == BP_OUT_FIX64) s = launch_k_step_n<0, 1>(a, net->ncls_kernel, grid, st);
-    else if (d.g_kind == BP_OUT_FIX32) s = launch_k_step_n<0, 2>(a, net->ncls_kernel, grid, st);
-    else s = launch_k_step_n<0, 0>(a, net->ncls_kernel, grid, st);
+    if (d.g_kind == BP_OUT_FIX64) s = launch_k_step_n<0, 1>(a, net->ncls_kernel, grid, st, net->sms);
+    else if (d.g_kind == BP_OUT_FIX32) s = launch_k_step_n<0, 2>(a, net->ncls_kernel, grid, st, net->sms);
+    else s = launch_k_step_n<0, 0>(a, net->ncls_kernel, grid, st, net->sms);
   } else {   // HH is compute-latency-bound: 512 threads per tile
-    if (d.g_kind == BP_OUT_FIX64) s = launch_k_step_n<1, 1>(a, net->ncls_kernel, grid, st);
-    else if (d.g_kind == BP_OUT_FIX32) s = launch_k_step_n<1, 2>(a, net->ncls_kernel, grid, st);
-    else s = launch_k_step_n<1, 0>(a, net->ncls_kernel, grid, st);
+    if (d.g_kind == BP_OUT_FIX64) s = launch_k_step_n<1, 1>(a, net->ncls_kernel, grid, st, net->sms);
+    else if (d.g_kind == BP_OUT_FIX32) s = launch_k_step_n<1, 2>(a, net->ncls_kernel, grid, st, net->sms);
+    else s = launch_k_step_n<1, 0>(a, net->ncls_kernel, grid, st, net->sms);
   }
   if (s != BP_OK) return s;
   s = launched();

@@ -233,6 +233,8 @@ struct StepArgs {
   int32_t *active;          // spikes_n as global ids, appended at *active_count
   int32_t *active_count;
   int32_t *zero_count;      // set to 0 (the other ping-pong list counter)
+  int32_t *tile_counter;    // k_step_persist: next tile index of this step
+  int32_t *zero_tile_counter;   // the next step's, set to 0
 };
 
 // ---------------------------------------------------------------- helpers
@@ -653,6 +655,103 @@ k_step(StepArgs a) {
   }
 
   // 3. counters
+  if (KIND == 2 && sat) atomicAdd(a.saturated, static_cast<unsigned long long>(sat));
+  my_sp = __reduce_add_sync(0xffffffffu, my_sp);
+  if (lane == 0 && my_sp) atomicAdd(&block_sp, static_cast<unsigned long long>(my_sp));
+  __syncthreads();
+  if (tid == 0 && block_sp) {
+    atomicAdd(a.spikes, block_sp);
+    if (a.step_spikes) atomicAdd(a.step_spikes, static_cast<int32_t>(block_sp));
+  }
+}
+
+// Persistent variant of k_step (LIF): the grid is the resident capacity
+// (4 blocks of 256 threads per SM) and every block takes tiles from a
+// per-step counter, so there is no partial last wave, and while it updates
+// passes 2 and 3 of its tile it already loads passes 0 and 1 of its NEXT
+// tile -- two passes of state in flight at every moment, also across tiles.
+// Same per-tile code (count -> fold + update -> emit) as k_step, hence
+// bit-identical results.
+template <int MODEL, int KIND, int NCLS>
+__global__ void __launch_bounds__(kStepThreads, BP_STEP_MINB)
+k_step_persist(StepArgs a) {
+  extern __shared__ __align__(16) int32_t cnt[];   // [NCLS][kTile]
+  __shared__ unsigned long long block_sp;
+  __shared__ int32_t next_s;
+  const int tid = threadIdx.x;
+  constexpr int nthreads = kStepThreads;
+  constexpr int passes = kTile / (4 * nthreads);
+  static_assert(passes >= 2, "two passes in flight");
+  constexpr int pstride = 4 * nthreads;
+  const uint32_t lane = tid & 31u;
+  const NeuronArgs &nr = a.nrn;
+  const Policies pol = make_policies(nr.keep_frac);
+  const int n_tiles = static_cast<int>(a.n_tiles);
+  auto tile_of = [&](int idx) -> uint32_t {
+    return a.reverse ? static_cast<uint32_t>(n_tiles - 1 - idx) : static_cast<uint32_t>(idx);
+  };
+
+  pdl_trigger();
+  pdl_wait();               // state and buckets of the previous kernels are final
+  if (tid == 0) {
+    block_sp = 0;
+    next_s = atomicAdd(a.tile_counter, 1);
+    if (blockIdx.x == 0) {
+      *a.zero_count = 0;
+      *a.zero_tile_counter = 0;
+    }
+  }
+  __syncthreads();
+  int idx = next_s;
+  uint32_t my_sp = 0, sat = 0;
+  Pass<MODEL, KIND> pa, pb;
+  if (idx < n_tiles) {
+    const int64_t base0 = static_cast<int64_t>(tile_of(idx)) << kTileShift;
+    pass_load(pa, nr, base0 + 4 * tid, pol);
+    pass_load(pb, nr, base0 + pstride + 4 * tid, pol);
+  }
+  while (idx < n_tiles) {
+    const uint32_t tile = tile_of(idx);
+    const int64_t base = static_cast<int64_t>(tile) << kTileShift;
+    __syncthreads();                          // the previous tile's counts are consumed
+    for (int j = tid; j < NCLS * kTile; j += nthreads) cnt[j] = 0;
+    __syncthreads();
+    const int32_t n_in = min(static_cast<uint32_t>(a.in.cnt[tile * kCntStride]), a.out.cap);
+    const uint32_t *buf = a.in.buf + static_cast<size_t>(tile) * a.out.cap;
+    for (int k = tid; k < n_in; k += nthreads) {
+      const uint32_t e = __ldcs(buf + k);
+      atomicAdd(&cnt[(e >> kClsShift) * kTile + (e & (kTile - 1))], 1);
+    }
+    if (a.in.flag[tile]) {                     // overflow spill (exact, rare)
+      for (int j = tid; j < kTile && base + j < nr.n; j += nthreads) {
+#pragma unroll
+        for (int c = 0; c < NCLS; ++c) {
+          int32_t *sp = a.in.spill + static_cast<size_t>(c) * a.out.n_local + base + j;
+          atomicAdd(&cnt[c * kTile + j], *sp);
+          *sp = 0;
+        }
+      }
+    }
+    if (tid == 0) next_s = atomicAdd(a.tile_counter, 1);
+    __syncthreads();
+    const int nxt = next_s;
+    if (tid == 0) {
+      a.in.cnt[tile * kCntStride] = 0;
+      a.in.flag[tile] = 0;
+    }
+    const int64_t nbase = nxt < n_tiles ? static_cast<int64_t>(tile_of(nxt)) << kTileShift : 0;
+#pragma unroll
+    for (int p = 0; p < passes; ++p) {
+      Pass<MODEL, KIND> &cur = (p & 1) ? pb : pa;
+      const int off = p * pstride;
+      const uint32_t nib = pass_update<MODEL, KIND, NCLS>(cur, a, cnt, kTile, off + 4 * tid,
+                                                          base + off + 4 * tid, pol, sat);
+      if (p + 2 < passes) pass_load(cur, nr, base + off + 2 * pstride + 4 * tid, pol);
+      else if (nxt < n_tiles) pass_load(cur, nr, nbase + (p + 2 - passes) * pstride + 4 * tid, pol);
+      pass_emit(a, nib, base, off, my_sp);
+    }
+    idx = nxt;
+  }
   if (KIND == 2 && sat) atomicAdd(a.saturated, static_cast<unsigned long long>(sat));
   my_sp = __reduce_add_sync(0xffffffffu, my_sp);
   if (lane == 0 && my_sp) atomicAdd(&block_sp, static_cast<unsigned long long>(my_sp));
