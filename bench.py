@@ -540,6 +540,8 @@ def run_ours(args):
     if rank != 0:
         if world > 1:
             dist.barrier()
+            net.net.close()            # NCCL communicator destroyed while every rank is alive
+            dist.barrier()
             dist.destroy_process_group()
         return
 
@@ -643,6 +645,8 @@ def run_ours(args):
     }
     print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()
+        net.net.close()
         dist.barrier()
         dist.destroy_process_group()
 

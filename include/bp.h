@@ -470,6 +470,11 @@ bp_status bp_network_counters(bp_network *net, uint64_t *host_out,
                               bp_stream stream);
 /* Device memory the network allocated itself (buckets, projection table). */
 size_t bp_network_device_bytes(const bp_network *net);
+/* The execution plan chosen at create, into out[0 .. n) (host int32, up to
+ * 8): [0] single-CTA time loop, [1] dense delivery, [2] tiles, [3] bucket
+ * capacity per tile, [4] weight-class fold (2 or 4), [5] binning lanes per
+ * (row, segment) item, [6] library NCCL exchange, [7] weight classes. */
+bp_status bp_network_describe(const bp_network *net, int32_t *out, int32_t n);
 /* Per-kernel timing of the next bp_network_step calls (at most max_steps
  * steps): CUDA events are recorded on `stream` before the neuron-update
  * kernel, between it and the event-binning kernel, and after the latter.

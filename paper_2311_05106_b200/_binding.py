@@ -35,7 +35,7 @@ EXPORTED = [
     "bp_network_create", "bp_network_step", "bp_network_scatter",
     "bp_network_update", "bp_network_update_overlap", "bp_network_counters", "bp_network_profile_begin",
     "bp_network_profile_end", "bp_network_destroy", "bp_network_device_bytes",
-    "bp_nccl_unique_id",
+    "bp_nccl_unique_id", "bp_network_describe",
 ]
 
 
@@ -162,6 +162,7 @@ def lib():
         L.bp_network_counters.argtypes = [P, P, P]
         L.bp_network_destroy.argtypes = [P]
         L.bp_network_destroy.restype = None
+        L.bp_network_describe.argtypes = [P, P, i32]
         L.bp_network_device_bytes.argtypes = [P]
         L.bp_network_device_bytes.restype = sz
         L.bp_nccl_unique_id.argtypes = [P]
@@ -586,6 +587,14 @@ class Network:
         """Device memory the library allocated for this network (buckets,
         projection table)."""
         return int(lib().bp_network_device_bytes(self._h))
+
+    def describe(self) -> dict:
+        """The execution plan chosen at create (bp_network_describe)."""
+        out = (ctypes.c_int32 * 8)()
+        _check(lib().bp_network_describe(self._h, ctypes.cast(out, ctypes.c_void_p), 8))
+        keys = ("small", "dense", "n_tiles", "cap", "fold_classes", "bin_lanes", "nccl",
+                "classes")
+        return dict(zip(keys, (int(x) for x in out)))
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:

@@ -2006,6 +2006,15 @@ size_t bp_network_workspace_bytes(const bp_network_desc *desc) {
 
 size_t bp_network_device_bytes(const bp_network *net) { return net ? net->dev_bytes : 0; }
 
+bp_status bp_network_describe(const bp_network *net, int32_t *out, int32_t n) {
+  BP_CHECK(net != nullptr && out != nullptr && n >= 0, BP_ERR_INVALID_ARG, "bad arguments");
+  const int32_t v[8] = {net->small ? 1 : 0, net->dense ? 1 : 0, static_cast<int32_t>(net->n_tiles),
+                        static_cast<int32_t>(net->cap), net->ncls_kernel, net->conn.group_lanes,
+                        net->nccl ? 1 : 0, net->n_cls};
+  for (int32_t i = 0; i < n && i < 8; ++i) out[i] = v[i];
+  return BP_OK;
+}
+
 bp_status bp_network_create(const bp_network_desc *desc, bp_stream stream,
                             bp_network **out) {
   int sms = 0;

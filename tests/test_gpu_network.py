@@ -272,3 +272,21 @@ def test_fig_s3_regimes_bit_exact(orc, n, p, steps, mode):
     g = net.state["g_e"].cpu().numpy()
     assert np.array_equal(g.view(np.uint32) if mode == "f32" else g,
                           st["g_e"].view(np.uint32) if mode == "f32" else st["g_e"])
+
+
+def test_execution_plan_choices():
+    """bp_network_describe: the single-CTA loop for <= 4096 neurons, dense
+    delivery for HH up to 2 M local neurons and tiles beyond (the
+    dense-before-n_local ordering bug of round 1 forced dense for every HH
+    network), 4 lanes per binning item for few events per segment."""
+    small = CobaNetwork(4000, conn="jit", fixed=True).net.describe()
+    assert small["small"] == 1
+    lif = CobaNetwork(50_000, conn="jit", fixed=False).net.describe()
+    assert lif["small"] == 0 and lif["dense"] == 0 and lif["n_tiles"] == 13
+    assert lif["bin_lanes"] == 32 and lif["fold_classes"] == 2
+    hh = CobaNetwork(100_000, model="hh", conn="jit", fixed=False).net.describe()
+    assert hh["dense"] == 1
+    big = CobaNetwork((2 << 20) + 64, model="hh", conn="jit", fixed=False, seg_len=None)
+    assert big.net.describe()["dense"] == 0
+    seg8 = CobaNetwork(400_000, conn="jit", fixed=False, seg_len=50_000).net.describe()
+    assert seg8["bin_lanes"] == 4
