@@ -98,6 +98,22 @@ __global__ void __launch_bounds__(kJitTiledThreads, 1) k_jit_tiled(JitTiledArgs 
     const uint32_t pos[4] = {pos0, pos0 + q0, pos0 + q0 + q1, pos0 + q0 + q1 + q2};
     // this lane's events inside the tile (positions ascend along the chain)
     if (!(pos0 < stop && pos[3] >= g0)) return;
+    if constexpr (HOMO) {
+      // counts only: branch-free, an event outside [g0, stop) (at most the
+      // boundary lane's) is counted into the sink slot `width`, never flushed
+      uint32_t nv = 0;
+      uint32_t *acc = reinterpret_cast<uint32_t *>(sm);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const bool ok = pos[k] >= g0 && pos[k] < stop;
+        nv += ok;
+        const uint32_t lc = ok ? pos[k] - g0 : static_cast<uint32_t>(width);
+        if (C16) atomicAdd(acc + (lc >> 1), 1u << ((lc & 1u) * 16u));
+        else atomicAdd(acc + lc, 1u);
+      }
+      ev += nv;
+      return;
+    }
     float w[4] = {s.w0, s.w0, s.w0, s.w0};
     if (LAW == 1) {
       const u32x4 x = philox_block(s.seed, kTagWeight, row, seg, blk);

@@ -122,3 +122,56 @@ def test_nccl_exchange_world1_bit_exact(orc, delay, mode):
     for k in ("v", "g_e", "g_i", "ref"):
         assert torch.equal(a.state[k], b.state[k]), k
     assert a.counters() == b.counters()
+
+
+@pytest.mark.parametrize("mode", ["fix64", "f32"])
+def test_eight_projections_overlapping_and_empty(orc, mode):
+    """The most projections a network takes (8), one of them empty, two whose
+    presynaptic ranges overlap (rows in both deliver twice), CSR and JIT
+    mixed, four weight classes: bit-exact against the oracle's merge."""
+    n, steps = 12_000, 250
+    p = 80.0 / n
+    K = orc.conn_len(p)
+    rows = [(0, 3000, "exc", 0.6, "jit"), (3000, 6000, "exc", 0.6, "jit"),
+            (6000, 9600, "exc", 0.45, "csr"), (2000, 2500, "exc", 0.45, "jit"),
+            (9600, 9600, "exc", 0.6, "jit"),                      # empty
+            (9600, 10800, "inh", 6.7, "jit"), (10800, n, "inh", 6.7, "csr"),
+            (9000, 11000, "inh", 5.0, "jit")]
+    specs, oproj = [], []
+    for k, (b, e, rec, w, kind) in enumerate(rows):
+        jit = orc.JitSpec(500 + k, K, n, orc.LAW_HOMO, w)
+        if kind == "csr":
+            ip, ix, _ = orc.jit_materialize(jit, e - b, n)
+            specs.append(ProjSpec(b, e, rec, w, csr=(torch.from_numpy(ip), torch.from_numpy(ix))))
+            oproj.append(orc.Projection(b, e - b, csr=(ip, ix, None), w_homo=w, receptor=rec))
+        else:
+            specs.append(ProjSpec(b, e, rec, w, seed=500 + k, p=p))
+            oproj.append(orc.Projection(b, e - b, jit=jit, receptor=rec))
+    net = CobaNetwork(n, conn="jit", fixed={"fix64": True, "f32": False}[mode],
+                      projections=specs)
+    assert net.net.describe()["classes"] == 4
+    raster = torch.zeros((steps, (n + 31) // 32), dtype=torch.int32, device="cuda")
+    net.run(steps, raster)
+    st = dict(v=inputs.lif_v0(n), g_e=np.zeros(n, _g(mode)), g_i=np.zeros(n, _g(mode)),
+              ref=np.zeros(n, np.uint8), spikes=np.zeros(n, np.uint8))
+    want = orc.run_network("lif", orc.lif_params(), st, oproj, None, steps)
+    got = np.stack([inputs.unpack_bits(r, n) for r in raster.cpu().numpy().view(np.uint32)])
+    assert want.sum() > 0
+    assert np.array_equal(got, want)
+    for k in ("v", "g_e", "g_i", "ref"):
+        assert np.array_equal(net.state[k].cpu().numpy().view(np.uint8), st[k].view(np.uint8)), k
+
+
+def test_merged_fp32_weights_off_the_fixed_grid_are_refused():
+    """Rule M1: merging fp32 conductances with several weights needs every
+    weight on the 2^-32 grid (the exact integer sum); a weight below it is
+    refused with BP_ERR_UNSUPPORTED instead of rounding silently."""
+    import paper_2311_05106_b200 as bp
+    n = 4000
+    p = 80.0 / n
+    specs = [ProjSpec(0, 2000, "exc", 0.6, seed=1, p=p),
+             ProjSpec(2000, 3200, "exc", 1e-12, seed=2, p=p),
+             ProjSpec(3200, n, "inh", 6.7, seed=3, p=p)]
+    with pytest.raises(bp.BpError, match="UNSUPPORTED"):
+        CobaNetwork(n, conn="jit", fixed=False, projections=specs)
+    CobaNetwork(n, conn="jit", fixed=True, projections=specs)      # fixed point: fine

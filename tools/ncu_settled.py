@@ -62,7 +62,7 @@ def main():
            "kernels": {}}
     for r in data:
         name = r[head.index("Kernel Name")]
-        key = "k_step" if name.startswith("void bp::k_step") or "k_step<" in name else (
+        key = "k_step" if "k_step" in name else (
             "k_bin_sorted" if "k_bin_sorted" in name else name)
         rec = {"name": name}
         for m, short in METRICS.items():
