@@ -1682,9 +1682,13 @@ bp_status launch_bin(bp_network *net, const int32_t *active, const int32_t *coun
   if (!net->dense && net->n_tiles <= 8192 && smem <= 200 * 1024 &&
       !std::getenv("BP_BIN_PER_EVENT")) {
     static std::atomic<uint64_t> attr_set{0};
-    if (first_on_device(attr_set))
+    if (first_on_device(attr_set)) {
       BP_CUDA(cudaFuncSetAttribute(bp::k_bin_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    200 * 1024));
+      if (const char *c = std::getenv("BP_CARVEOUT"); c && *c)
+        cudaFuncSetAttribute(bp::k_bin_sorted, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             std::atoi(c));
+    }
     BP_CUDA(launch_pdl(bp::k_bin_sorted, net->sms, bp::kBinThreads, smem, st, net->conn,
                        bin_target(net, par), active, count, net->counters + 1, net->n_tiles));
   } else {
@@ -1777,6 +1781,9 @@ bp_status launch_k_step_persist(const bp::StepArgs &a, int sms, cudaStream_t st)
   int dev = 0;
   cudaGetDevice(&dev);
   if (first_on_device(attr)) {
+    if (const char *c = std::getenv("BP_CARVEOUT"); c && *c)
+      cudaFuncSetAttribute(bp::k_step_persist<0, KIND, NCLS>,
+                           cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(c));
     if (smem > 48 * 1024)
       BP_CUDA(cudaFuncSetAttribute(bp::k_step_persist<0, KIND, NCLS>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -175,3 +175,50 @@ def test_merged_fp32_weights_off_the_fixed_grid_are_refused():
     with pytest.raises(bp.BpError, match="UNSUPPORTED"):
         CobaNetwork(n, conn="jit", fixed=False, projections=specs)
     CobaNetwork(n, conn="jit", fixed=True, projections=specs)      # fixed point: fine
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_random_networks_bit_exact(orc, case):
+    """Seeded random network shapes against the oracle: n not a multiple of
+    32 or of the tile, 1-4 projections with random row ranges, receptors,
+    weights (on the 2^-32 grid), JIT or CSR, delays 1-4, every conductance
+    mode, one or two calls of bp_network_step."""
+    rng = np.random.default_rng(9000 + case)
+    n = int(rng.integers(4097, 30_000))
+    mode = ["fix64", "fix32", "f32"][case % 3]
+    delay = int(rng.integers(1, 5))
+    p = float(rng.uniform(40, 120)) / n
+    K = orc.conn_len(p)
+    n_proj = int(rng.integers(1, 5))
+    specs, oproj = [], []
+    for k in range(n_proj):
+        b = int(rng.integers(0, n - 100))
+        e = int(rng.integers(b + 1, n + 1))
+        rec = "exc" if rng.random() < 0.6 else "inh"
+        w = float(np.float32(rng.choice([0.25, 0.5, 0.75, 1.0, 2.5, 5.0])))
+        jit = orc.JitSpec(1000 * case + k, K, n, orc.LAW_HOMO, w)
+        if rng.random() < 0.3:
+            ip, ix, _ = orc.jit_materialize(jit, e - b, n)
+            specs.append(ProjSpec(b, e, rec, w, csr=(torch.from_numpy(ip), torch.from_numpy(ix))))
+            oproj.append(orc.Projection(b, e - b, csr=(ip, ix, None), w_homo=w, receptor=rec))
+        else:
+            specs.append(ProjSpec(b, e, rec, w, seed=1000 * case + k, p=p))
+            oproj.append(orc.Projection(b, e - b, jit=jit, receptor=rec))
+    classes = {(s.receptor, s.weight) for s in specs}
+    if len(classes) > 4:
+        pytest.skip("more than 4 weight classes")
+    steps = 200
+    net = CobaNetwork(n, conn="jit", fixed={"fix64": True, "fix32": "fix32", "f32": False}[mode],
+                      projections=specs, delay=delay)
+    raster = torch.zeros((steps, (n + 31) // 32), dtype=torch.int32, device="cuda")
+    cut = int(rng.integers(1, steps))
+    net.run(cut, raster[:cut])
+    net.run(steps - cut, raster[cut:])
+    orc.set_fix32_bits(20)
+    st = dict(v=inputs.lif_v0(n), g_e=np.zeros(n, _g(mode)), g_i=np.zeros(n, _g(mode)),
+              ref=np.zeros(n, np.uint8), spikes=np.zeros(n, np.uint8))
+    want = orc.run_network("lif", orc.lif_params(), st, oproj, None, steps, delay=delay)
+    got = np.stack([inputs.unpack_bits(r, n) for r in raster.cpu().numpy().view(np.uint32)])
+    assert np.array_equal(got, want), (n, mode, delay, n_proj)
+    for k in ("v", "g_e", "g_i", "ref"):
+        assert np.array_equal(net.state[k].cpu().numpy().view(np.uint8), st[k].view(np.uint8)), k
