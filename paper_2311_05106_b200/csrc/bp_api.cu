@@ -1784,10 +1784,10 @@ bp_status launch_k_step_persist(const bp::StepArgs &a, int sms, cudaStream_t st)
     if (const char *c = std::getenv("BP_CARVEOUT"); c && *c)
       cudaFuncSetAttribute(bp::k_step_persist<0, KIND, NCLS>,
                            cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(c));
-    if (smem > 48 * 1024)
-      BP_CUDA(cudaFuncSetAttribute(bp::k_step_persist<0, KIND, NCLS>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
+    // (the opt-in also covers the kernel's static shared words beyond 48 KB)
+    BP_CUDA(cudaFuncSetAttribute(bp::k_step_persist<0, KIND, NCLS>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
     int b = 0;
     BP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, bp::k_step_persist<0, KIND, NCLS>,
                                                           bp::kStepThreads, smem));

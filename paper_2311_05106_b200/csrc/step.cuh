@@ -387,12 +387,23 @@ __device__ __forceinline__ void fold_pair(const StepArgs &a, G &ge, G &gi, const
   }
 }
 
-// One LIF neuron (rule N1); returns spike.
+// One LIF neuron (rule N1); returns spike.  SELECT: the three cases as
+// selects, no divergence (measured, same box: fp32 k_step 61.8 -> 59.8 us,
+// fix32 71.8 -> 69.8 us, fix64 unchanged; tools/lib_ab.sh).
+template <bool SELECT = true>
 __device__ __forceinline__ bool lif_one(const NeuronArgs &a, float &V, uint32_t &ref,
                                         float gE, float gI) {
   const float I = __fmaf_rn(gI, a.e_inh - V, __fmaf_rn(gE, a.e_exc - V, a.i_ext));
   const float Vinf = __fmaf_rn(a.r, I, a.v_rest);
   const float Vc = __fmaf_rn(V - Vinf, a.alpha_v, Vinf);
+  if constexpr (SELECT) {
+    // refractory -> hold V, count down; else Vc > V_th -> reset, spike; else V = Vc
+    const bool free = ref == 0u;
+    const bool spike = free && Vc > a.v_th;
+    V = free ? (spike ? a.v_reset : Vc) : V;
+    ref = free ? (spike ? static_cast<uint32_t>(a.ref_steps) : 0u) : ref - 1u;
+    return spike;
+  }
   if (ref > 0) {
     ref -= 1u;
     return false;
