@@ -164,12 +164,14 @@ void launch_compact(const uint32_t *spikes, int64_t n, int32_t *active, int32_t 
     return;
   }
   const bool wide = words >= cap * 4 * bp::kCompactThreads;
-  const int64_t per = (wide ? 4 : 1) * bp::kCompactThreads;
+  const int64_t per = (wide ? 8 : 1) * bp::kCompactThreads;
   int64_t blocks = (words + per - 1) / per;
-  if (blocks > cap) blocks = cap;
+  // long vectors: one 2048-word iteration per block (all loads in flight at
+  // once, 16-byte loads); the grid is not capped at the resident blocks
+  if (!wide && blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   if (wide)
-    bp::k_compact<4><<<static_cast<int>(blocks), bp::kCompactThreads, 0, st>>>(
+    bp::k_compact<8><<<static_cast<int>(blocks), bp::kCompactThreads, 0, st>>>(
         spikes, n, active, count, id_base, skip_b, skip_e);
   else
     bp::k_compact<1><<<static_cast<int>(blocks), bp::kCompactThreads, 0, st>>>(

@@ -116,18 +116,30 @@ k_compact(const uint32_t *__restrict__ spikes, int64_t n,
        w0 += static_cast<int64_t>(gridDim.x) * BW) {
     uint32_t wd[WPT];
     int c = 0;
+    const int64_t wt = w0 + WPT * tid;             // this thread's first word
+    if (WPT % 4 == 0 && wt + WPT <= n_words && (wt + WPT <= skip_b || wt >= skip_e) &&
+        (n & 31) == 0 && (reinterpret_cast<uintptr_t>(spikes) & 15) == 0) {
+      // whole 16-byte groups inside the vector and outside the skip range
 #pragma unroll
-    for (int k = 0; k < WPT; ++k) {
-      const int64_t wi = w0 + WPT * tid + k;
-      uint32_t word = 0;
-      if (wi < n_words && (wi < skip_b || wi >= skip_e)) {
-        word = __ldg(spikes + wi);
-        const int64_t valid = n - (wi << 5);
-        if (valid < 32) word &= (1u << valid) - 1u;
+      for (int k = 0; k < WPT; k += 4) {
+        const uint4 q = __ldg(reinterpret_cast<const uint4 *>(spikes + wt + k));
+        wd[k] = q.x; wd[k + 1] = q.y; wd[k + 2] = q.z; wd[k + 3] = q.w;
       }
-      wd[k] = word;
-      c += __popc(word);
+    } else {
+#pragma unroll
+      for (int k = 0; k < WPT; ++k) {
+        const int64_t wi = wt + k;
+        uint32_t word = 0;
+        if (wi < n_words && (wi < skip_b || wi >= skip_e)) {
+          word = __ldg(spikes + wi);
+          const int64_t valid = n - (wi << 5);
+          if (valid < 32) word &= (1u << valid) - 1u;
+        }
+        wd[k] = word;
+      }
     }
+#pragma unroll
+    for (int k = 0; k < WPT; ++k) c += __popc(wd[k]);
     int incl = c;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
