@@ -455,6 +455,15 @@ def run_ours(args):
     # caller-driven exchange through torch.distributed (functional check of
     # several ranks sharing one GPU)
     exchange = "nccl" if (world > 1 and args.dist_backend == "nccl") else "caller"
+    exchange_note = None
+    if exchange == "nccl":
+        # every rank must agree before the collective create: fall back to the
+        # torch.distributed exchange when any rank cannot load NCCL itself
+        import paper_2311_05106_b200 as bp
+        ok = torch.tensor([1 if bp.nccl_version() is not None else 0], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            exchange, exchange_note = "caller", "library NCCL unavailable on a rank"
     net, csr = build_network(wl, world, rank, fixed, dev, exchange=exchange)
     n_local = net.part.col_end - net.part.col_begin
     small = world == 1 and n_total <= 4096
@@ -626,7 +635,9 @@ def run_ours(args):
                                         "(%d B per rank per step), in place, on the "
                                         "library's comm stream" % (net.part.local_words * 4),
                                 "caller": "none (one GPU)" if world == 1 else
-                                          "torch.distributed all_gather_into_tensor"}[exchange],
+                                          "torch.distributed all_gather_into_tensor" + (
+                                              " (%s)" % exchange_note if exchange_note
+                                              else "")}[exchange],
                    "l2": (f"state {state_mb:.0f} MB/GPU > 2 x 126 MB L2: no flush needed"
                           if state_mb > 252 else
                           f"state {state_mb:.1f} MB is L2/SM-resident by design (the workload is that small)"),

@@ -434,6 +434,10 @@ typedef struct bp_network bp_network; /* opaque; not thread-safe */
  * (libbp resolves NCCL at run time: an already loaded libnccl.so.2, else
  * the one the dynamic loader finds; BP_NCCL_LIB overrides the path). */
 bp_status bp_nccl_unique_id(uint8_t *out);
+/* The NCCL the library resolved (ncclGetVersion code, e.g. 22809), or
+ * BP_ERR_NCCL when none can be loaded -- a cheap check every rank can make
+ * before the collective bp_network_create. */
+bp_status bp_nccl_version(int32_t *version);
 
 size_t bp_network_workspace_bytes(const bp_network_desc *desc);
 /* Copies *desc (all buffers stay owned by the caller), initialises the

@@ -13,5 +13,5 @@ from ._binding import (ACCUMULATE, CONN_CSR, CONN_JIT, EXCHANGE_CALLER,  # noqa:
                        conn_len, csrmv_gather, csrmv_plan, event_csrmv, event_csrmv_grad, hh_params, jitconn_event_mv, jitconn_mv,
                        jitconn_event_mv_homo, jitconn_event_mv_normal,
                        jitconn_event_mv_uniform, jitconn_materialize,
-                       jitconn_spec, lib, lif_params, nccl_unique_id, neuron_step,
+                       jitconn_spec, lib, lif_params, nccl_unique_id, nccl_version, neuron_step,
                        projection, workspace, workspace_bytes)

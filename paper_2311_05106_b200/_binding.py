@@ -35,7 +35,7 @@ EXPORTED = [
     "bp_network_create", "bp_network_step", "bp_network_scatter",
     "bp_network_update", "bp_network_update_overlap", "bp_network_counters", "bp_network_profile_begin",
     "bp_network_profile_end", "bp_network_destroy", "bp_network_device_bytes",
-    "bp_nccl_unique_id", "bp_network_describe",
+    "bp_nccl_unique_id", "bp_network_describe", "bp_nccl_version",
 ]
 
 
@@ -166,6 +166,7 @@ def lib():
         L.bp_network_device_bytes.argtypes = [P]
         L.bp_network_device_bytes.restype = sz
         L.bp_nccl_unique_id.argtypes = [P]
+        L.bp_nccl_version.argtypes = [P]
         for name in EXPORTED:
             if name not in ("bp_network_destroy", "bp_status_string",
                             "bp_last_error", "bp_conn_len", "bp_workspace_bytes",
@@ -452,6 +453,15 @@ def nccl_unique_id() -> bytes:
     buf = (ctypes.c_uint8 * 128)()
     _check(lib().bp_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
     return bytes(buf)
+
+
+def nccl_version() -> int | None:
+    """NCCL version code the library resolves, or None when NCCL cannot be
+    loaded (bp_nccl_version)."""
+    v = ctypes.c_int32()
+    if lib().bp_nccl_version(ctypes.byref(v)) != 0:
+        return None
+    return int(v.value)
 
 
 def projection(*, pre_begin, pre_end, weight, receptor=RECEPTOR_EXC, jit=None, csr=None):

@@ -1300,6 +1300,7 @@ struct NcclApi {
                              cudaStream_t) = nullptr;
   ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
   const char *(*error_string)(ncclResult_t) = nullptr;
+  ncclResult_t (*get_version)(int *) = nullptr;
 };
 NcclApi g_nccl;
 std::mutex g_nccl_mu;
@@ -1319,6 +1320,7 @@ bp_status nccl_load() {
       g_nccl.all_gather = reinterpret_cast<decltype(g_nccl.all_gather)>(dlsym(h, "ncclAllGather"));
       g_nccl.comm_destroy = reinterpret_cast<decltype(g_nccl.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
       g_nccl.error_string = reinterpret_cast<decltype(g_nccl.error_string)>(dlsym(h, "ncclGetErrorString"));
+      g_nccl.get_version = reinterpret_cast<decltype(g_nccl.get_version)>(dlsym(h, "ncclGetVersion"));
       g_nccl.ok = g_nccl.get_unique_id && g_nccl.comm_init_rank && g_nccl.all_gather &&
                   g_nccl.comm_destroy && g_nccl.error_string;
     }
@@ -1335,6 +1337,16 @@ bp_status nccl_load() {
   } while (0)
 
 }  // namespace
+
+extern "C" bp_status bp_nccl_version(int32_t *version) {
+  BP_CHECK(version != nullptr, BP_ERR_INVALID_ARG, "version is NULL");
+  bp_status s = nccl_load();
+  if (s != BP_OK) return s;
+  int v = 0;
+  if (g_nccl.get_version) BP_NCCL(g_nccl.get_version(&v));
+  *version = v;
+  return BP_OK;
+}
 
 extern "C" bp_status bp_nccl_unique_id(uint8_t *out) {
   BP_CHECK(out != nullptr, BP_ERR_INVALID_ARG, "out is NULL");

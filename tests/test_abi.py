@@ -102,3 +102,11 @@ def test_library_has_no_link_time_nccl_dependency(libbp):
     from paper_2311_05106_b200 import _binding
     out = subprocess.check_output(["readelf", "-d", _binding.LIB_PATH]).decode()
     assert "nccl" not in out
+
+
+def test_nccl_resolves_at_run_time(libbp):
+    """bp_nccl_version: the library finds an NCCL (torch's, already in the
+    process) without a link-time dependency; a version code >= 2.27."""
+    import paper_2311_05106_b200 as bp
+    v = bp.nccl_version()
+    assert v is not None and v >= 22700
