@@ -170,8 +170,11 @@ bp_status bp_event_csrmv_grad(const int64_t *indptr, const int32_t *indices, con
  * that each call accumulates q = rint(w 2^F) exactly in two independent
  * 32-bit integer words per column (native shared-memory atomics instead of
  * an fp32 compare-and-swap loop) and rounds each column's exact sum to fp32
- * once -- within rule T2, and independent of the summation order.  -1: the
- * fp32-atomic path (no workspace, n_rows >= 2^24, or unbounded sums).
+ * once -- independent of the summation order; the error per column is at
+ * most (terms) 2^-(F+1) + 1/2 ulp, within rule T2 unless a column's active
+ * terms average below 2^-(F+1) 1e5 in magnitude (T4).  -1: the
+ * fp32-atomic path (no workspace, n_rows >= 2^24, unbounded sums, or
+ * BP_CSR_NO_T4=1).
  * The plan is valid for the same (indptr, indices, data, n_rows, n_cols,
  * out_kind, homogeneous-or-not) on the same device type; a stale plan gives
  * wrong sums but never reads outside the row.  Requires indices ascending
