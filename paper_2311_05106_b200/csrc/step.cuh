@@ -1361,15 +1361,19 @@ k_bin_sorted(ConnArgs conn, BinTarget out, const int32_t *active, const int32_t 
   BP_BIN_MARK(1);
   const int ns = min(n_staged, kBinStage);
 
-  // B. tile offsets; one global slot claim per non-empty tile
+  // B. tile offsets; one global slot claim per non-empty tile.  The claims'
+  //    results are first needed in D, so (up to kClaimRegs tiles per thread)
+  //    they stay in flight across the sort (measured, B200, config 5: binning
+  //    B + C 7.1 -> 6.8 us; the ~150 same-address atomics per tile counter
+  //    are L2-throughput-bound, so most of their time remains).
   block_exclusive_scan(hist, static_cast<int>(n_tiles), warp_sums);
   BP_BIN_MARK(5);
-  // a thread's slot claims are independent: issue 4 before using any result
-  for (uint32_t t0 = tid; t0 < n_tiles; t0 += 4 * kBinThreads) {
-    int32_t base[4];
+  constexpr int kClaimRegs = 4;
+  if (n_tiles <= kClaimRegs * kBinThreads) {
+    int32_t base[kClaimRegs];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t t = t0 + u * kBinThreads;
+    for (int u = 0; u < kClaimRegs; ++u) {
+      const uint32_t t = tid + u * kBinThreads;
       base[u] = 0;
       if (t < n_tiles) {
         const int32_t begin = hist[t];
@@ -1377,18 +1381,43 @@ k_bin_sorted(ConnArgs conn, BinTarget out, const int32_t *active, const int32_t 
         if (end > begin) base[u] = atomicAdd(out.out.cnt + t * kCntStride, end - begin);
       }
     }
+    __syncthreads();          // every offset read before the sort moves them
+    BP_BIN_MARK(2);
+    // C. counting sort by tile (hist[] becomes the running cursor)
+    for (int i = tid; i < ns; i += kBinThreads) {
+      const uint32_t rec = staged[i];
+      const uint32_t t = (rec & kLocMask) >> kTileShift;
+      sorted[atomicAdd(hist + t, 1)] = rec;
+    }
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (t0 + u * kBinThreads < n_tiles) gbase[t0 + u * kBinThreads] = base[u];
-  }
-  __syncthreads();
-
-  BP_BIN_MARK(2);
-  // C. counting sort by tile (hist[] becomes the running cursor)
-  for (int i = tid; i < ns; i += kBinThreads) {
-    const uint32_t rec = staged[i];
-    const uint32_t t = (rec & kLocMask) >> kTileShift;
-    sorted[atomicAdd(hist + t, 1)] = rec;
+    for (int u = 0; u < kClaimRegs; ++u)
+      if (tid + u * kBinThreads < n_tiles) gbase[tid + u * kBinThreads] = base[u];
+  } else {
+    // a thread's slot claims are independent: issue 4 before using any result
+    for (uint32_t t0 = tid; t0 < n_tiles; t0 += 4 * kBinThreads) {
+      int32_t base[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t t = t0 + u * kBinThreads;
+        base[u] = 0;
+        if (t < n_tiles) {
+          const int32_t begin = hist[t];
+          const int32_t end = (t + 1 < n_tiles) ? hist[t + 1] : ns;
+          if (end > begin) base[u] = atomicAdd(out.out.cnt + t * kCntStride, end - begin);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (t0 + u * kBinThreads < n_tiles) gbase[t0 + u * kBinThreads] = base[u];
+    }
+    __syncthreads();
+    BP_BIN_MARK(2);
+    // C. counting sort by tile (hist[] becomes the running cursor)
+    for (int i = tid; i < ns; i += kBinThreads) {
+      const uint32_t rec = staged[i];
+      const uint32_t t = (rec & kLocMask) >> kTileShift;
+      sorted[atomicAdd(hist + t, 1)] = rec;
+    }
   }
   __syncthreads();
 
