@@ -1690,38 +1690,76 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, size_t sme
 
 // Bin the rows active[0..*count) into bucket parity `par`: block-aggregated
 // when the tile table fits in shared memory, else one atomic per event.
+bool bin_sorted_fits(const bp_network *net) {
+  const size_t smem = (2 * static_cast<size_t>(bp::kBinStage) + 2 * net->n_tiles) * 4;
+  return !net->dense && net->n_tiles <= 8192 && smem <= 200 * 1024 &&
+         !std::getenv("BP_BIN_PER_EVENT");
+}
+
+template <bool WORDS>
+bp_status launch_bin_sorted(bp_network *net, const int32_t *active, const int32_t *count,
+                            const bp::WordRange &wr, int par, cudaStream_t st) {
+  const size_t smem = (2 * static_cast<size_t>(bp::kBinStage) + 2 * net->n_tiles) * 4;
+  static std::atomic<uint64_t> attr_set{0};
+  if (first_on_device(attr_set)) {
+    BP_CUDA(cudaFuncSetAttribute(bp::k_bin_sorted<WORDS>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    if (const char *c = std::getenv("BP_CARVEOUT"); c && *c)
+      cudaFuncSetAttribute(bp::k_bin_sorted<WORDS>,
+                           cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(c));
+  }
+  BP_CUDA(launch_pdl(bp::k_bin_sorted<WORDS>, net->sms, bp::kBinThreads, smem, st, net->conn,
+                     bin_target(net, par), active, count, wr, net->counters + 1, net->n_tiles));
+  return launched();
+}
+
+// Bin the rows active[0..*count) into bucket parity `par`: block-aggregated
+// when the tile table fits in shared memory, else one atomic per event.
 bp_status launch_bin(bp_network *net, const int32_t *active, const int32_t *count, int par,
                      int64_t max_rows, cudaStream_t st) {
-  const size_t smem = (2 * static_cast<size_t>(bp::kBinStage) + 2 * net->n_tiles) * 4;
-  if (!net->dense && net->n_tiles <= 8192 && smem <= 200 * 1024 &&
-      !std::getenv("BP_BIN_PER_EVENT")) {
-    static std::atomic<uint64_t> attr_set{0};
-    if (first_on_device(attr_set)) {
-      BP_CUDA(cudaFuncSetAttribute(bp::k_bin_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   200 * 1024));
-      if (const char *c = std::getenv("BP_CARVEOUT"); c && *c)
-        cudaFuncSetAttribute(bp::k_bin_sorted, cudaFuncAttributePreferredSharedMemoryCarveout,
-                             std::atoi(c));
-    }
-    BP_CUDA(launch_pdl(bp::k_bin_sorted, net->sms, bp::kBinThreads, smem, st, net->conn,
-                       bin_target(net, par), active, count, net->counters + 1, net->n_tiles));
-  } else {
-    bp::k_bin_rows<<<grid_for_items(max_rows, net->sms), bp::kScatterThreads, 0, st>>>(
-        net->conn, bin_target(net, par), active, count, net->counters + 1);
-  }
+  if (bin_sorted_fits(net))
+    return launch_bin_sorted<false>(net, active, count, bp::WordRange{}, par, st);
+  bp::k_bin_rows<<<grid_for_items(max_rows, net->sms), bp::kScatterThreads, 0, st>>>(
+      net->conn, bin_target(net, par), active, count, net->counters + 1);
   return launched();
 }
 
 // Bin the events of the spikes in words [w_begin, w_end) of the global
 // vector `vec` (neurons [32 w_begin, min(32 w_end, n))) into bucket parity
 // `par`.  Words [skip_b, skip_e) (absolute) are skipped: one pass over the
-// remote words on both sides of a partition's own range.
+// remote words on both sides of a partition's own range.  When every
+// binning block's share is at most one word per thread, the block-aggregated
+// binning lists its rows itself (one launch, no count memset); longer
+// vectors go through the compaction launch, whose loads are all in flight
+// at once.  Measured (emulated ranks, B200, tools/words_ab.sh): config 3 with
+// the strong-scaling segments (420-740 words per block) 29.2 -> 27.2 us per
+// step at G = 8, 32.2 -> 30.7 at G = 2; the weak-scaling ranks with in-kernel
+// listing 99.8 -> 103.7 us (G = 2, 2.6 k words per block) and 109 -> 123 us
+// (G = 8, 18 k) -- kept on the compaction.  BP_BIN_COMPACT=0/1 overrides.
 bp_status bin_spike_range(bp_network *net, const uint32_t *vec, int64_t w_begin, int64_t w_end,
                           int par, cudaStream_t st, int64_t skip_b = 0, int64_t skip_e = 0) {
   if (w_end <= w_begin) return BP_OK;
   const int64_t first = w_begin * 32;
   const int64_t last = w_end * 32 < net->d.n ? w_end * 32 : net->d.n;
   if (last <= first) return BP_OK;
+  const int64_t sb = std::min(std::max(skip_b, w_begin), w_end);
+  const int64_t se = std::min(std::max(skip_e, sb), w_end);
+  const int64_t words = (sb - w_begin) + (w_end - se);
+  bool listing = words <= static_cast<int64_t>(net->sms) * bp::kBinThreads;
+  if (const char *e = std::getenv("BP_BIN_COMPACT"); e && *e) listing = std::atoi(e) == 0;
+  const bp::WordRange wr{vec, w_begin, w_end, skip_b, skip_e, net->d.n};
+  if (listing && bin_sorted_fits(net))
+    return launch_bin_sorted<true>(net, nullptr, nullptr, wr, par, st);
+  if (listing) {
+    // words per warp: spread the range over all resident warps (8 blocks of
+    // 8 warps per SM), up to 32
+    const int64_t resident = static_cast<int64_t>(net->sms) * 64;
+    const int wpw = static_cast<int>(std::min<int64_t>(32, std::max<int64_t>(1, (words + resident - 1) / resident)));
+    const int64_t warps = (words + wpw - 1) / wpw;
+    bp::k_bin_rows_words<<<grid_for_items(warps, net->sms), bp::kScatterThreads, 0, st>>>(
+        net->conn, bin_target(net, par), wr, wpw, net->counters + 1);
+    return launched();
+  }
   int32_t *active = net->active[0];
   int32_t *count = net->count;
   BP_CUDA(cudaMemsetAsync(count, 0, sizeof(int32_t), st));

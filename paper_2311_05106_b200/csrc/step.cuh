@@ -1318,9 +1318,118 @@ __device__ __forceinline__ int32_t block_exclusive_scan(int32_t *v, int n, int32
   return total;
 }
 
+// Phase A of the binning for the rows list[r_lo, r_hi): regenerate (JIT) or
+// read (CSR) them into the shared staging area + tile histogram.
+__device__ __forceinline__ uint32_t stage_list(const ConnArgs &conn, const BinTarget &out,
+                                               const int32_t *list, int r_lo, int r_hi,
+                                               uint32_t *staged, int32_t *n_staged,
+                                               int32_t *hist) {
+  const uint32_t warp = threadIdx.x >> 5;
+  uint32_t ev = 0;
+  if (!conn.all_jit) {
+    for (int k = r_lo + static_cast<int>(warp); k < r_hi; k += kBinThreads / 32)
+      ev += stage_row(conn, out, list[k], staged, n_staged, hist);
+  } else if (conn.group_lanes < 32) {
+    // few events per (row, segment): 4 lanes per item
+    ev = stage_items<4>(conn, out, list, r_lo, r_hi, conn.n_seg_max, staged, n_staged, hist);
+  } else {
+    // warp w takes rows r_lo + w + 32 i (i = 0, 1, ...), 32 rows per batch
+    for (int k0 = r_lo + static_cast<int>(warp); k0 < r_hi; k0 += kBinThreads)
+      ev += stage_rows_jit(conn, out, list, k0, r_hi, staged, n_staged, hist);
+  }
+  return ev;
+}
+
+// k_bin_sorted<true>: the rows are the set bits of spike words [w_begin,
+// w_end) without [skip_b, skip_e) (a partition's remote words on both sides
+// of its own range), bits >= n ignored -- each block lists the rows of its
+// contiguous share of those words itself (no compaction launch, no global
+// list, no count memset).
+struct WordRange {
+  const uint32_t *vec;      // spike vector, word w = neurons 32 w .. 32 w + 31
+  int64_t w_begin, w_end;
+  int64_t skip_b, skip_e;
+  int64_t n;
+};
+
+// Per-event binning of the set bits of a WordRange (dense delivery, or tile
+// tables too large for the block-aggregated kernel): each warp takes `wpw`
+// (<= 32) consecutive words of the range per iteration and delivers the rows
+// of their set bits one by one -- no compaction launch, no list, no memset.
+// (The host picks wpw so that every resident warp gets words: a warp's rows
+// are delivered serially.)
+__global__ void __launch_bounds__(kScatterThreads)
+k_bin_rows_words(ConnArgs conn, BinTarget out, WordRange wr, int wpw,
+                 unsigned long long *events) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const int64_t warp0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t sb = min(max(wr.skip_b, wr.w_begin), wr.w_end);
+  const int64_t se = min(max(wr.skip_e, sb), wr.w_end);
+  const int64_t W1 = sb - wr.w_begin, Wt = W1 + (wr.w_end - se);
+  auto word_of = [&](int64_t v) { return v < W1 ? wr.w_begin + v : se + (v - W1); };
+  unsigned long long ev = 0;
+  for (int64_t v0 = warp0 * wpw; v0 < Wt; v0 += n_warps * wpw) {
+    const int64_t v = v0 + lane;
+    uint32_t w = 0;
+    if (lane < static_cast<uint32_t>(wpw) && v < Wt) {
+      const int64_t wi = word_of(v);
+      w = wr.vec[wi];
+      const int64_t rem = wr.n - wi * 32;
+      if (rem < 32) w &= rem > 0 ? (1u << rem) - 1u : 0u;
+    }
+    uint32_t m = __ballot_sync(0xffffffffu, w != 0u);
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1u;
+      uint32_t bits = __shfl_sync(0xffffffffu, w, src);
+      const int64_t wi = word_of(v0 + src);
+      while (bits) {
+        const int q = __ffs(bits) - 1;
+        bits &= bits - 1u;
+        ev += deliver_row(conn, out, wi * 32 + q);
+      }
+    }
+  }
+  count_events(events, ev);
+}
+
+// Block-wide exclusive scan of one value per thread; *total = the sum.
+__device__ __forceinline__ int32_t block_scan1(int32_t c, int32_t *warp_sums, int32_t *total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t incl = c;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int32_t t = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += t;
+  }
+  if (lane == 31) warp_sums[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int32_t w = warp_sums[lane];
+    int32_t wi = w;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int32_t t = __shfl_up_sync(0xffffffffu, wi, off);
+      if (lane >= off) wi += t;
+    }
+    warp_sums[lane] = wi - w;
+    if (lane == 31) warp_sums[32] = wi;
+  }
+  __syncthreads();
+  *total = warp_sums[32];
+  return warp_sums[warp] + incl - c;
+}
+
+#ifndef BP_WORDS_PT
+#define BP_WORDS_PT 4
+#endif
+constexpr int kWordsPT = BP_WORDS_PT;   // spike words per thread and listing round
+
+template <bool WORDS>
 __global__ void __launch_bounds__(kBinThreads, 1)
 k_bin_sorted(ConnArgs conn, BinTarget out, const int32_t *active, const int32_t *count,
-             unsigned long long *events, uint32_t n_tiles) {
+             WordRange wr, unsigned long long *events, uint32_t n_tiles) {
   extern __shared__ uint32_t smem[];
   uint32_t *staged = smem;                                  // [kBinStage]
   uint32_t *sorted = staged + kBinStage;                    // [kBinStage]
@@ -1330,32 +1439,87 @@ k_bin_sorted(ConnArgs conn, BinTarget out, const int32_t *active, const int32_t 
   __shared__ int32_t warp_sums[33];
   __shared__ unsigned long long block_ev;
   const int tid = threadIdx.x;
-  const uint32_t lane = tid & 31u, warp = tid >> 5;
+  const uint32_t lane = tid & 31u;
   pdl_trigger();
-  pdl_wait();               // the active list of the producing kernel is final
-  const int n_active = *count;
-  // this block's contiguous share of the active rows
-  const int per = (n_active + gridDim.x - 1) / gridDim.x;
-  const int r_lo = min(n_active, static_cast<int>(blockIdx.x) * per);
-  const int r_hi = min(n_active, r_lo + per);
-  BP_BIN_MARK(0);
-  if (r_lo >= r_hi) return;
-  for (uint32_t t = tid; t < n_tiles; t += kBinThreads) hist[t] = 0;
-  if (tid == 0) { n_staged = 0; block_ev = 0; }
-  __syncthreads();
-
-  // A. regenerate this block's rows into shared memory + tile histogram
+  pdl_wait();               // the active list / spike words of the producers are final
   uint32_t ev = 0;
-  if (!conn.all_jit) {
-    for (int k = r_lo + static_cast<int>(warp); k < r_hi; k += kBinThreads / 32)
-      ev += stage_row(conn, out, active[k], staged, &n_staged, hist);
-  } else if (conn.group_lanes < 32) {
-    // few events per (row, segment): 4 lanes per item
-    ev = stage_items<4>(conn, out, active, r_lo, r_hi, conn.n_seg_max, staged, &n_staged, hist);
+  if constexpr (!WORDS) {
+    const int n_active = *count;
+    // this block's contiguous share of the active rows
+    const int per = (n_active + gridDim.x - 1) / gridDim.x;
+    const int r_lo = min(n_active, static_cast<int>(blockIdx.x) * per);
+    const int r_hi = min(n_active, r_lo + per);
+    BP_BIN_MARK(0);
+    if (r_lo >= r_hi) return;
+    for (uint32_t t = tid; t < n_tiles; t += kBinThreads) hist[t] = 0;
+    if (tid == 0) { n_staged = 0; block_ev = 0; }
+    __syncthreads();
+    // A. regenerate this block's rows into shared memory + tile histogram
+    ev = stage_list(conn, out, active, r_lo, r_hi, staged, &n_staged, hist);
   } else {
-    // warp w takes rows r_lo + w + 32 i (i = 0, 1, ...), 32 rows per batch
-    for (int k0 = r_lo + static_cast<int>(warp); k0 < r_hi; k0 += kBinThreads)
-      ev += stage_rows_jit(conn, out, active, k0, r_hi, staged, &n_staged, hist);
+    // the remote words as one virtual range [0, W1 + W2)
+    const int64_t sb = min(max(wr.skip_b, wr.w_begin), wr.w_end);
+    const int64_t se = min(max(wr.skip_e, sb), wr.w_end);
+    const int64_t W1 = sb - wr.w_begin, Wt = W1 + (wr.w_end - se);
+    const int64_t per = (Wt + gridDim.x - 1) / gridDim.x;
+    const int64_t v_lo = min(Wt, static_cast<int64_t>(blockIdx.x) * per);
+    const int64_t v_hi = min(Wt, v_lo + per);
+    BP_BIN_MARK(0);
+    if (v_lo >= v_hi) return;
+    for (uint32_t t = tid; t < n_tiles; t += kBinThreads) hist[t] = 0;
+    if (tid == 0) { n_staged = 0; block_ev = 0; }
+    // A0 + A. list the rows of kWordsPT * 1024 words at a time (all loads in
+    //    flight together) into sorted[] (unused until the sort) and stage
+    //    them whenever the list is full
+    int32_t *list = reinterpret_cast<int32_t *>(sorted);
+    int list_n = 0, rows = 0;                     // block-uniform
+    auto word_of = [&](int64_t v) { return v < W1 ? wr.w_begin + v : se + (v - W1); };
+    for (int64_t v0 = v_lo; v0 < v_hi; v0 += kWordsPT * kBinThreads) {
+      uint32_t w[kWordsPT];
+      int32_t c = 0;
+#pragma unroll
+      for (int j = 0; j < kWordsPT; ++j) {
+        const int64_t v = v0 + tid + j * kBinThreads;
+        w[j] = v < v_hi ? wr.vec[word_of(v)] : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < kWordsPT; ++j) {
+        const int64_t rem = wr.n - word_of(v0 + tid + j * kBinThreads) * 32;
+        if (rem < 32) w[j] &= rem > 0 ? (1u << rem) - 1u : 0u;
+        c += __popc(w[j]);
+      }
+      int32_t total;
+      const int32_t excl = block_scan1(c, warp_sums, &total);
+      rows += total;
+      for (int done = 0; done < total;) {         // (several rounds only for bursts)
+        const int take = min(kBinStage - list_n, total - done);
+        int o = excl;
+#pragma unroll
+        for (int j = 0; j < kWordsPT; ++j) {
+          uint32_t bits = w[j];
+          if (!bits) continue;
+          const int64_t wi = word_of(v0 + tid + j * kBinThreads);
+          while (bits) {
+            const int q = __ffs(bits) - 1;
+            bits &= bits - 1u;
+            if (o >= done && o < done + take)
+              list[list_n + o - done] = static_cast<int32_t>(wi * 32 + q);
+            ++o;
+          }
+        }
+        list_n += take;
+        done += take;
+        __syncthreads();
+        if (list_n == kBinStage) {
+          ev += stage_list(conn, out, list, 0, list_n, staged, &n_staged, hist);
+          list_n = 0;
+          __syncthreads();
+        }
+      }
+      __syncthreads();                            // warp_sums reused by the next scan
+    }
+    if (rows == 0) return;
+    if (list_n) ev += stage_list(conn, out, list, 0, list_n, staged, &n_staged, hist);
   }
   __syncthreads();
   BP_BIN_MARK(1);

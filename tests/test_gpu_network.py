@@ -11,7 +11,7 @@ import pytest
 import torch
 
 from paper_2311_05106_b200 import inputs
-from paper_2311_05106_b200.network import SEED_E, SEED_I, CobaNetwork
+from paper_2311_05106_b200.network import SEED_E, SEED_I, CobaNetwork, partition
 
 pytestmark = pytest.mark.gpu
 
@@ -154,14 +154,20 @@ def test_split_step_equals_fused_step(orc):
     assert np.array_equal(a.state["g_e"].cpu().numpy(), b.state["g_e"].cpu().numpy())
 
 
-def test_partitions_emulated_on_one_gpu_equal_whole(orc):
+@pytest.mark.parametrize("compact", ["0", "1"])
+@pytest.mark.parametrize("n,steps", [(4096, 300), (50_000, 120)])
+def test_partitions_emulated_on_one_gpu_equal_whole(orc, monkeypatch, compact, n, steps):
     """G postsynaptic partitions stepped one after another on one device,
     with the all-gather emulated by sharing one spike vector, give the
-    single-partition network bit for bit."""
-    n, steps, world = 4096, 300, 4
+    single-partition network bit for bit.  The remote
+    rows are listed by the binning blocks themselves (BP_BIN_COMPACT=0) or
+    compacted by a separate launch (1); n = 50 000 has a ragged last word."""
+    monkeypatch.setenv("BP_BIN_COMPACT", compact)
+    world = 4
     whole = CobaNetwork(n, conn="jit", fixed=True, seg_len=1024)
     whole.run(steps)
-    shared = torch.zeros(n // 32, dtype=torch.int32, device="cuda")
+    shared = torch.zeros(partition(n, world, 0, 1024).padded_words, dtype=torch.int32,
+                         device="cuda")
     parts = [CobaNetwork(n, conn="jit", fixed=True, seg_len=1024, rank=r, world=world,
                          spikes=shared) for r in range(world)]
     for _ in range(steps):
@@ -290,3 +296,63 @@ def test_execution_plan_choices():
     assert big.net.describe()["dense"] == 0
     seg8 = CobaNetwork(400_000, conn="jit", fixed=False, seg_len=50_000).net.describe()
     assert seg8["bin_lanes"] == 4
+
+
+def test_remote_listing_burst_matches_compaction(monkeypatch):
+    """Every neuron of a 4 M network spikes at once: rank 0 of 4 bins ~3 M
+    remote rows, ~20 k per binning block -- more than one listing round of
+    the block's shared list and more events than its staging area (the
+    per-event overflow, and the buckets' dense spill).  The in-kernel
+    listing and the compaction launch must give the same conductances and
+    event count bit for bit."""
+    n, world = 4_000_000, 4
+    got = []
+    for compact in ("0", "1"):
+        monkeypatch.setenv("BP_BIN_COMPACT", compact)
+        shared = torch.full(((n + 31) // 32,), -1, dtype=torch.int32, device="cuda")
+        q = CobaNetwork(n, conn="jit", fixed=True, seg_len=n // world, rank=0, world=world,
+                        spikes=shared)
+        q.net.scatter()
+        q.net.update()
+        torch.cuda.synchronize()
+        _, events, _ = q.counters()
+        got.append((q.state["g_e"].cpu().numpy(), q.state["g_i"].cpu().numpy(), events))
+        del q, shared
+    (ge0, gi0, ev0), (ge1, gi1, ev1) = got
+    assert ev0 == ev1 and ev0 > (3 * n // 4) * 15   # ~20 local events per remote row
+    assert np.array_equal(ge0, ge1) and np.array_equal(gi0, gi1)
+    assert ge0.any()
+
+
+@pytest.mark.parametrize("compact", ["0", "1"])
+def test_hh_partitions_emulated_equal_oracle(orc, monkeypatch, compact):
+    """HH network (dense delivery) over 4 postsynaptic partitions with the
+    exchange emulated by a shared spike vector: the remote rows go through
+    the per-event word-listing kernel (BP_BIN_COMPACT=0) or compaction +
+    per-row binning (1); the raster equals the oracle's bit for bit."""
+    monkeypatch.setenv("BP_BIN_COMPACT", compact)
+    n, steps, world = 4000, 300, 4
+    n_exc = 3200
+    ipe, ixe, _ = inputs.random_csr(n_exc, n, 0.02, seed=11)
+    ipi, ixi, _ = inputs.random_csr(n - n_exc, n, 0.02, seed=12)
+    shared = torch.zeros(partition(n, world, 0).padded_words, dtype=torch.int32, device="cuda")
+    parts = [CobaNetwork(n, model="hh", conn="csr", fixed=True, csr=((ipe, ixe), (ipi, ixi)),
+                         rank=r, world=world, spikes=shared) for r in range(world)]
+    raster = np.zeros((steps, n), np.uint8)
+    for t in range(steps):
+        for q in parts:
+            q.net.scatter()
+        for q in parts:
+            q.net.update()
+        torch.cuda.synchronize()
+        raster[t] = inputs.unpack_bits(shared.cpu().numpy().view(np.uint32)[:(n + 31) // 32], n)
+    v, m, h, nk = inputs.hh_init(n)
+    st = dict(v=v, m=m, h=h, n=nk, g_e=np.zeros(n, np.int64), g_i=np.zeros(n, np.int64),
+              spikes=np.zeros(n, np.uint8))
+    pe = orc.Projection(0, n_exc, csr=(ipe, ixe, None), w_homo=6.0)
+    pi = orc.Projection(n_exc, n - n_exc, csr=(ipi, ixi, None), w_homo=67.0)
+    want = orc.run_network("hh", orc.hh_params(), st, pe, pi, steps)
+    assert want.sum() > 0
+    assert np.array_equal(raster, want)
+    v_got = np.concatenate([q.state["v"].cpu().numpy() for q in parts])
+    assert np.array_equal(v_got.view(np.uint32), st["v"].view(np.uint32))

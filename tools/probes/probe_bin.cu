@@ -38,12 +38,12 @@ int main(int argc, char** argv) {
   printf("n %u L %u K %u rows %d S %d tiles %u\n", n, L, K, n_active, group, n_tiles);
   unsigned long long* ev; cudaMalloc(&ev, 8);
   const size_t smem = (2 * (size_t)kBinStage + 2 * n_tiles) * 4;
-  cudaFuncSetAttribute(k_bin_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_bin_sorted<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   for (int r = 0; r < 3; ++r) {
     cudaMemset(bk.cnt, 0, (size_t)n_tiles * kCntStride * 4);
     cudaEventRecord(a);
-    k_bin_sorted<<<148, kBinThreads, smem>>>(c, bt, active, count, ev, n_tiles);
+    k_bin_sorted<false><<<148, kBinThreads, smem>>>(c, bt, active, count, WordRange{}, ev, n_tiles);
     cudaEventRecord(b); cudaEventSynchronize(b);
     float ms; cudaEventElapsedTime(&ms, a, b);
     unsigned long long t[1024][6]; cudaMemcpyFromSymbol(t, g_bin_t, sizeof(t));
