@@ -563,9 +563,15 @@ def run_ours(args):
         ev_step = prof["events"] / nrec
         bytes_per_launch = state_bytes_per_neuron(spec["model"], fixed) * n_local + 4 * ev_step
         achieved = bytes_per_launch / upd_s / 1e9
-        kname = ("k_small_net<%s,%s> (whole time loop in one CTA, state in shared memory)"
-                 if small else "k_step<%s,%s> (fused: bucket counts -> Expon+COBA+neuron -> "
-                 "spike bits + active list)") % (spec["model"].upper(), args.g)
+        if small:
+            kname = "k_small_net<%s,%s> (whole time loop in one CTA, state in shared memory)" % (
+                spec["model"].upper(), args.g)
+        elif spec["model"] == "hh":
+            kname = ("k_hh_dense1<%s> (per-neuron event counts -> Expon+COBA+HH -> spike bits; "
+                     "delivers its own spikes' events as REDs on the next step's counts)" % args.g)
+        else:
+            kname = ("k_step<LIF,%s> (fused: bucket counts -> Expon+COBA+LIF -> spike bits + "
+                     "active list)" % args.g)
         traffic, tsrc = _ncu_traffic_r02(wl, args.g, "k_step")
         roofline = {"kernel": kname, "bound": "hbm", "achieved": achieved,
                     "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
@@ -592,6 +598,12 @@ def run_ours(args):
         if small:
             roofline["note"] = ("latency-bound: the whole state (%d neurons) lives in one SM's "
                                 "shared memory; HBM fraction is not the limiter" % n_local)
+        elif spec["model"] == "hh":
+            roofline["note"] = ("compute-latency-bound: a ~490-instruction dependent fp32 chain "
+                                "per neuron (exponential Euler, 6 rate functions), one neuron per "
+                                "thread; the %.1f MB of state is L2-resident, so the HBM fraction "
+                                "is not the limiter" % (
+                                    state_bytes_per_neuron("hh", fixed) * n_local / 1e6))
         elif spec["conn"] == "jit":
             sm_mhz = clk.summary().get("sm_mhz") or 1965.0
             peak_ops = 148 * 4 * 32 * sm_mhz * 1e6

@@ -1403,6 +1403,7 @@ struct bp_network {
   // blocks (k_step_dense) -- compute-bound networks that fill few tiles
   bool dense = false;
   bool debug_nan = false;         // BP_DEBUG_NAN=1: count non-finite V after every step
+  bool hh_fused = true;           // dense HH kernel delivers its own spikes (BP_HH_FUSED)
   // BP_EXCHANGE_NCCL: the library's own spike all-gather
   bool nccl = false;
   ncclComm_t comm = nullptr;
@@ -1886,6 +1887,10 @@ bp_status launch_step(bp_network *net, uint32_t *raster, cudaStream_t st,
   a.tile_counter = net->count + 4 + cp;           // k_step_persist's tile scheduler
   a.zero_tile_counter = net->count + 4 + (cp ^ 1);
   const int grid = static_cast<int>(net->n_tiles);
+  // dense HH: the update kernel delivers its own spikes (BP_HH_FUSED=0: the
+  // separate binning launch)
+  const bool fused = net->dense && d.model == BP_MODEL_HH && net->hh_fused;
+  if (fused) a.conn = net->conn;
   bp_status s = BP_OK;
   if (net->dense) {
     const int dgrid = static_cast<int>((net->n_local + 4 * bp::kDenseThreads - 1) /
@@ -1897,9 +1902,15 @@ bp_status launch_step(bp_network *net, uint32_t *raster, cudaStream_t st,
     } else {   // HH: one neuron per thread
       const int64_t per_block = static_cast<int64_t>(bp::kHHThreads) * bp::kHHPerThread;
       const int hgrid = static_cast<int>((net->n_local + per_block - 1) / per_block);
-      if (d.g_kind == BP_OUT_FIX64) BP_CUDA(launch_pdl(bp::k_hh_dense1<1>, hgrid, bp::kHHThreads, 0, st, a));
-      else if (d.g_kind == BP_OUT_FIX32) BP_CUDA(launch_pdl(bp::k_hh_dense1<2>, hgrid, bp::kHHThreads, 0, st, a));
-      else BP_CUDA(launch_pdl(bp::k_hh_dense1<0>, hgrid, bp::kHHThreads, 0, st, a));
+      if (fused) {
+        if (d.g_kind == BP_OUT_FIX64) BP_CUDA(launch_pdl(bp::k_hh_dense1<1, true>, hgrid, bp::kHHThreads, 0, st, a));
+        else if (d.g_kind == BP_OUT_FIX32) BP_CUDA(launch_pdl(bp::k_hh_dense1<2, true>, hgrid, bp::kHHThreads, 0, st, a));
+        else BP_CUDA(launch_pdl(bp::k_hh_dense1<0, true>, hgrid, bp::kHHThreads, 0, st, a));
+      } else {
+        if (d.g_kind == BP_OUT_FIX64) BP_CUDA(launch_pdl(bp::k_hh_dense1<1>, hgrid, bp::kHHThreads, 0, st, a));
+        else if (d.g_kind == BP_OUT_FIX32) BP_CUDA(launch_pdl(bp::k_hh_dense1<2>, hgrid, bp::kHHThreads, 0, st, a));
+        else BP_CUDA(launch_pdl(bp::k_hh_dense1<0>, hgrid, bp::kHHThreads, 0, st, a));
+      }
     }
   } else if (d.model == BP_MODEL_LIF) {
     if (d.g_kind == BP_OUT_FIX64) s = launch_k_step_n<0, 1>(a, net->ncls_kernel, grid, st, net->sms);
@@ -1918,8 +1929,10 @@ bp_status launch_step(bp_network *net, uint32_t *raster, cudaStream_t st,
   if (net->debug_nan)
     bp::k_count_nonfinite<<<net->sms * 4, 256, 0, st>>>(d.state.v, net->n_local,
                                                          net->counters + 3);
-  s = launch_bin(net, net->active[1], net->count + 2 + cp, out_par, net->n_local, st);
-  if (s != BP_OK) return s;
+  if (!fused) {
+    s = launch_bin(net, net->active[1], net->count + 2 + cp, out_par, net->n_local, st);
+    if (s != BP_OK) return s;
+  }
   net->steps_done += 1;
   return BP_OK;
 }
@@ -2089,6 +2102,7 @@ bp_status bp_network_create(const bp_network_desc *desc, bp_stream stream,
   net->delay = desc->delay_steps > 0 ? desc->delay_steps : 1;
   net->slots = net->delay + 1;
   net->debug_nan = std::getenv("BP_DEBUG_NAN") && std::atoi(std::getenv("BP_DEBUG_NAN"));
+  if (const char *f = std::getenv("BP_HH_FUSED"); f && *f) net->hh_fused = std::atoi(f) != 0;
   net->n_local = desc->col_end - desc->col_begin;
   net->local_words = (net->n_local + 31) / 32;
   net->global_words = desc->exchange == BP_EXCHANGE_NCCL

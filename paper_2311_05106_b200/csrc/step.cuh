@@ -235,6 +235,7 @@ struct StepArgs {
   int32_t *zero_count;      // set to 0 (the other ping-pong list counter)
   int32_t *tile_counter;    // k_step_persist: next tile index of this step
   int32_t *zero_tile_counter;   // the next step's, set to 0
+  ConnArgs conn;            // FUSED kernels: deliver this step's spikes into `out`
 };
 
 // ---------------------------------------------------------------- helpers
@@ -866,7 +867,16 @@ __device__ __forceinline__ bool hh_dense_one(const StepArgs &a, int64_t i, uint3
 // neurons: 1 -> 14.7 us per step, 2 -> 16.4 us).
 constexpr int kHHPerThread = 1;
 
-template <int KIND>
+// FUSED: the kernel also delivers its own spikes (dense delivery: every
+// event is a fire-and-forget RED on the next step's per-neuron count, so the
+// delivering warp never waits on an atomic) -- the separate binning launch of
+// the ~60 spikes per step of config 4 goes away.  The row delivery is an
+// out-of-line call so its registers do not burden the HH update.
+__device__ __noinline__ uint32_t deliver_row_call(ConnArgs c, BinTarget b, int64_t r) {
+  return deliver_row(c, b, r);
+}
+
+template <int KIND, bool FUSED = false>
 __global__ void __launch_bounds__(kHHThreads, 8) k_hh_dense1(StepArgs a) {
   const NeuronArgs &nr = a.nrn;
   const int64_t base = static_cast<int64_t>(blockIdx.x) * kHHThreads * kHHPerThread;
@@ -895,14 +905,25 @@ __global__ void __launch_bounds__(kHHThreads, 8) k_hh_dense1(StepArgs a) {
       const int c = __popc(ballot);
       int slot = 0;
       if (lane == 0) {
-        if (a.active) slot = atomicAdd(a.active_count, c);
+        if (!FUSED && a.active) slot = atomicAdd(a.active_count, c);
         atomicAdd(a.spikes, static_cast<unsigned long long>(c));
         if (a.step_spikes) atomicAdd(a.step_spikes, c);
       }
-      slot = __shfl_sync(0xffffffffu, slot, 0);
-      if (spike[k] && a.active)
-        a.active[slot + __popc(ballot & ((1u << lane) - 1u))] =
-            nr.active_base + static_cast<int32_t>(i);
+      if constexpr (FUSED) {
+        uint32_t m = ballot, ev = 0;
+        while (m) {
+          const int src = __ffs(m) - 1;
+          m &= m - 1u;
+          ev += deliver_row_call(a.conn, a.out, nr.active_base + w0 + src);
+        }
+        ev = __reduce_add_sync(0xffffffffu, ev);
+        if (lane == 0 && ev && a.events) atomicAdd(a.events, static_cast<unsigned long long>(ev));
+      } else {
+        slot = __shfl_sync(0xffffffffu, slot, 0);
+        if (spike[k] && a.active)
+          a.active[slot + __popc(ballot & ((1u << lane) - 1u))] =
+              nr.active_base + static_cast<int32_t>(i);
+      }
     }
   }
   if (KIND == 2) {
