@@ -415,6 +415,22 @@ def _ncu_traffic_r02(wl, g, kernel_prefix):
     return float(k["dram_bytes"]), os.path.relpath(path, ROOT)
 
 
+def launches_per_step(model: str, n_local: int, n_total: int, world: int,
+                      sms: int = 148) -> int:
+    """libbp kernel launches per network step (bp_api.cu launch_step and
+    remote_scatter): the update kernel; the local binning unless the dense HH
+    update delivers its own spikes (n_local <= 2^21); for world > 1 the
+    remote binning -- one launch when each binning block's share of the
+    remote spike words is <= 1024 words (bin_spike_range's listing rule),
+    else compaction + binning."""
+    dense_hh = model == "hh" and n_local <= (2 << 20)
+    n = 1 if dense_hh else 2
+    if world > 1:
+        remote_words = (n_total - n_local + 31) // 32
+        n += 1 if remote_words <= sms * 1024 else 2
+    return n
+
+
 def settle_default(wl):
     """Untimed pre-roll: the network starts from V0 ~ N(-55, 2),
     every neuron crosses threshold within the first ~30 steps and the
@@ -656,11 +672,10 @@ def run_ours(args):
                    "spikes": spikes_seen, "events": events_total},
         "sim_s_per_wall_s": sim_ratio,
         "events_per_step": events_total / args.steps,
-        # libbp kernels in the timed region: k_step + k_bin per step (world 1),
-        # one k_small_net launch for small networks, and k_step + k_bin +
-        # k_compact + k_bin (remote rows) per step for world > 1 (the memset
-        # and NCCL's all-gather kernel not counted)
-        "gpu_launches": (1 if small else (2 if world == 1 else 4) * args.steps),
+        # libbp kernels in the timed region (launches_per_step; NCCL's
+        # all-gather kernel not counted)
+        "gpu_launches": (1 if small else
+                         launches_per_step(spec["model"], n_local, n_total, world) * args.steps),
         "clocks": clocks,
         "roofline": roofline,
         "cpu_baseline": cpu,

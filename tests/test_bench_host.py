@@ -54,3 +54,14 @@ def test_weak_scaling_segment_is_one_gpu():
 def test_settle_default():
     assert bench.settle_default("coba_lif_jit") == 2000
     assert bench.settle_default("coba4000_csr") == 0
+
+
+def test_launches_per_step():
+    # config 5 at G = 1: k_step + k_bin; G = 8: + compaction + remote binning
+    assert bench.launches_per_step("lif", 12_500_000, 12_500_000, 1) == 2
+    assert bench.launches_per_step("lif", 12_500_000, 100_000_000, 8) == 4
+    # config 3 strong scaling at G = 8: remote words listed by the binning
+    assert bench.launches_per_step("lif", 500_000, 4_000_000, 8) == 3
+    # config 4: the dense HH update delivers its own spikes
+    assert bench.launches_per_step("hh", 400_000, 400_000, 1) == 1
+    assert bench.launches_per_step("hh", 200_000, 400_000, 2) == 2
