@@ -769,14 +769,28 @@ def run_emulated_rank(args):
     slots = net.spikes.view(G, lw)
     local = slots[R].clone()
 
+    comm = torch.cuda.Stream(device=0)
+
     def step(k):
         net.net.scatter()
-        net.net.update()
-        # every slot <- this rank's words (its own slot: the same values)
-        local.copy_(slots[R])
-        slots.copy_(local.expand(G, lw))
+        if args.emu_serial:
+            net.net.update()
+            # every slot <- this rank's words (its own slot: the same values)
+            local.copy_(slots[R])
+            slots.copy_(local.expand(G, lw))
+            return
+        # as CobaNetwork.step_distributed(overlap=True): the exchange stream
+        # waits for this step's spike words only, so the stand-in all-gather
+        # overlaps the local binning, and the next scatter waits for it
+        compute = torch.cuda.current_stream(0)      # (the capture stream inside a graph)
+        net.net.update_overlap(comm)
+        with torch.cuda.stream(comm):
+            local.copy_(slots[R])
+            slots.copy_(local.expand(G, lw))
+        compute.wait_stream(comm)
 
-    for k in range(args.warmup):
+    settle = settle_default(wl) if args.settle is None else args.settle
+    for k in range(settle + args.warmup):
         step(k)
     torch.cuda.synchronize()
     # one period of steps in a CUDA graph, as the N > 1 bench replays it
@@ -814,10 +828,14 @@ def run_emulated_rank(args):
             "config": {"workload": "%s rank %d of %d" % (wl, R, G), "n_total": n,
                        "n_per_gpu": net.part.col_end - net.part.col_begin, "emulated_world": G,
                        "exchange": "replaced by a device copy of this rank's spike words "
-                                   "into the %d remote slots (%.1f MB/step)" % (
-                                       G - 1, (words - lw) * 4 / 1e6),
+                                   "into the %d remote slots (%.1f MB/step), %s" % (
+                                       G - 1, (words - lw) * 4 / 1e6,
+                                       "after the local binning (serial)" if args.emu_serial
+                                       else "on an exchange stream overlapping the local "
+                                            "binning (CobaNetwork.step_distributed's schedule)"),
                        "host_loop": "CUDA graph of %d steps" % period if graph is not None
                                     else "eager",
+                       "settle_steps": settle,
                        "local_spikes_per_step": (sp1 - sp0) / args.steps,
                        "events_per_step": (ev1 - ev0) / args.steps},
             "clocks": clk.summary()}
@@ -1124,6 +1142,9 @@ def main():
                          "replaced by a device copy; not a multi-GPU number)")
     ap.add_argument("--emulate-rank", type=int, default=0,
                     help="--emulate-world: which rank's partition to time")
+    ap.add_argument("--emu-serial", action="store_true",
+                    help="--emulate-world: the stand-in exchange after the local binning "
+                         "instead of overlapping it")
     ap.add_argument("--no-graph", action="store_true",
                     help="--emulate-world: eager per-step calls instead of a CUDA graph")
     ap.add_argument("--fig3-sizes", default="10000,30000,100000,300000,1000000,3000000",
