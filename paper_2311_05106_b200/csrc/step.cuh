@@ -488,9 +488,11 @@ __device__ __forceinline__ void pass_load(Pass<MODEL, KIND> &p, const NeuronArgs
 
 // Update the 4 neurons of pass p (offset j0 in the tile, local index i0);
 // returns their spike nibble.
-template <int MODEL, int KIND, int NCLS>
+// ZERO: the counts this pass consumed are reset to 0 right after the fold
+// (the persistent kernel then needs no zeroing pass and barrier per tile).
+template <int MODEL, int KIND, int NCLS, bool ZERO = false>
 __device__ __forceinline__ uint32_t pass_update(Pass<MODEL, KIND> &p, const StepArgs &a,
-                                                const int32_t *cnt, int stride,
+                                                int32_t *cnt, int stride,
                                                 int j0, int64_t i0, const Policies &pol,
                                                 uint32_t &sat) {
   const NeuronArgs &nr = a.nrn;
@@ -501,6 +503,11 @@ __device__ __forceinline__ uint32_t pass_update(Pass<MODEL, KIND> &p, const Step
 #pragma unroll
     for (int q = 0; q < 4; ++q)
       fold_pair<KIND, NCLS>(a, p.ge.v[q], p.gi.v[q], cnt, stride, j0 + q, sat, gEf[q], gIf[q]);
+    if constexpr (ZERO) {
+#pragma unroll
+      for (int c = 0; c < NCLS; ++c)
+        *reinterpret_cast<int4 *>(cnt + c * stride + j0) = make_int4(0, 0, 0, 0);
+    }
     float V[4] = {p.V.x, p.V.y, p.V.z, p.V.w};
     if constexpr (MODEL == 0) {
       uint32_t Rn = 0;
@@ -538,6 +545,10 @@ __device__ __forceinline__ uint32_t pass_update(Pass<MODEL, KIND> &p, const Step
     G *pi = static_cast<G *>(nr.g_i) + i;
     G ge = *pe, gi = *pi;
     fold_pair<KIND, NCLS>(a, ge, gi, cnt, stride, j0 + q, sat, gEf, gIf);
+    if constexpr (ZERO) {
+#pragma unroll
+      for (int c = 0; c < NCLS; ++c) cnt[c * stride + j0 + q] = 0;
+    }
     *pe = ge;
     *pi = gi;
     float V = nr.v[i];
@@ -677,6 +688,19 @@ k_step(StepArgs a) {
   }
 }
 
+constexpr int kPfRecs = 4 * kStepThreads;   // bucket records prefetched per tile
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // Persistent variant of k_step (LIF): the grid is the resident capacity
 // (4 blocks of 256 threads per SM) and every block takes tiles from a
 // per-step counter, so there is no partial last wave, and while it updates
@@ -690,6 +714,8 @@ k_step_persist(StepArgs a) {
   extern __shared__ __align__(16) int32_t cnt[];   // [NCLS][kTile]
   __shared__ unsigned long long block_sp;
   __shared__ int32_t next_s;
+  __shared__ __align__(16) uint32_t pf_rec[kPfRecs];   // next tile's first records
+  __shared__ int32_t pf_n;                             // next tile's bucket count
   const int tid = threadIdx.x;
   constexpr int nthreads = kStepThreads;
   constexpr int passes = kTile / (4 * nthreads);
@@ -713,24 +739,42 @@ k_step_persist(StepArgs a) {
       *a.zero_tile_counter = 0;
     }
   }
+  // the count arrays are zeroed once; every fold then resets what it read
+  for (int j = tid; j < NCLS * kTile; j += nthreads) cnt[j] = 0;
   __syncthreads();
   int idx = next_s;
   uint32_t my_sp = 0, sat = 0;
   Pass<MODEL, KIND> pa, pb;
+  // The next tile's bucket count and first kPfRecs records are copied into
+  // shared memory (cp.async, no registers) while this tile updates, so the
+  // counting phase waits for no L2 round trip (records beyond kPfRecs, rare,
+  // are read as before).  Needs 16-byte rows of records: cap % 4 == 0.
+  const bool pf_ok = (a.out.cap & 3u) == 0u;
+  auto prefetch = [&](uint32_t t) {
+    if (pf_ok && 4u * tid + 4u <= a.out.cap)
+      cp_async16(&pf_rec[4 * tid], a.in.buf + static_cast<size_t>(t) * a.out.cap + 4 * tid);
+    if (tid == 0) cp_async4(&pf_n, a.in.cnt + t * kCntStride);
+    cp_async_commit();
+  };
   if (idx < n_tiles) {
     const int64_t base0 = static_cast<int64_t>(tile_of(idx)) << kTileShift;
+    prefetch(tile_of(idx));
     pass_load(pa, nr, base0 + 4 * tid, pol);
     pass_load(pb, nr, base0 + pstride + 4 * tid, pol);
   }
   while (idx < n_tiles) {
     const uint32_t tile = tile_of(idx);
     const int64_t base = static_cast<int64_t>(tile) << kTileShift;
-    __syncthreads();                          // the previous tile's counts are consumed
-    for (int j = tid; j < NCLS * kTile; j += nthreads) cnt[j] = 0;
-    __syncthreads();
-    const int32_t n_in = min(static_cast<uint32_t>(a.in.cnt[tile * kCntStride]), a.out.cap);
+    cp_async_wait_all();
+    __syncthreads();        // the previous tile's counts consumed (and reset); prefetch landed
+    const int32_t n_in = min(static_cast<uint32_t>(pf_n), a.out.cap);
+    const int32_t n_pf = pf_ok ? min(n_in, kPfRecs) : 0;
+    for (int k = tid; k < n_pf; k += nthreads) {
+      const uint32_t e = pf_rec[k];
+      atomicAdd(&cnt[(e >> kClsShift) * kTile + (e & (kTile - 1))], 1);
+    }
     const uint32_t *buf = a.in.buf + static_cast<size_t>(tile) * a.out.cap;
-    for (int k = tid; k < n_in; k += nthreads) {
+    for (int k = n_pf + tid; k < n_in; k += nthreads) {
       const uint32_t e = __ldcs(buf + k);
       atomicAdd(&cnt[(e >> kClsShift) * kTile + (e & (kTile - 1))], 1);
     }
@@ -745,19 +789,20 @@ k_step_persist(StepArgs a) {
       }
     }
     if (tid == 0) next_s = atomicAdd(a.tile_counter, 1);
-    __syncthreads();
+    __syncthreads();        // counts complete; every thread is done with pf_rec / pf_n
     const int nxt = next_s;
     if (tid == 0) {
       a.in.cnt[tile * kCntStride] = 0;
       a.in.flag[tile] = 0;
     }
+    if (nxt < n_tiles) prefetch(tile_of(nxt));
     const int64_t nbase = nxt < n_tiles ? static_cast<int64_t>(tile_of(nxt)) << kTileShift : 0;
 #pragma unroll
     for (int p = 0; p < passes; ++p) {
       Pass<MODEL, KIND> &cur = (p & 1) ? pb : pa;
       const int off = p * pstride;
-      const uint32_t nib = pass_update<MODEL, KIND, NCLS>(cur, a, cnt, kTile, off + 4 * tid,
-                                                          base + off + 4 * tid, pol, sat);
+      const uint32_t nib = pass_update<MODEL, KIND, NCLS, true>(cur, a, cnt, kTile, off + 4 * tid,
+                                                                base + off + 4 * tid, pol, sat);
       if (p + 2 < passes) pass_load(cur, nr, base + off + 2 * pstride + 4 * tid, pol);
       else if (nxt < n_tiles) pass_load(cur, nr, nbase + (p + 2 - passes) * pstride + 4 * tid, pol);
       pass_emit(a, nib, base, off, my_sp);
