@@ -1593,6 +1593,17 @@ bp::ConnArgs make_conn(bp_network *net, std::vector<bp::NetProj> *table) {
   // with seg_len n/8) 18.1 vs 21.6 us -> 4 lanes; rows of ~1000 events keep
   // the warp (63 steps of 16 gaps would serialise).
   c.group_lanes = ((e_seg >= 48.0 && e_seg <= 112.0) || e_seg >= 512.0) ? 32 : 4;
+  // rows of several long segments (Fig S3B / S3C with seg_len n/8: ~125 and
+  // ~500 events per item, a few hundred rows per step): a warp per (row,
+  // segment) item, so one row's segments run on different warps instead of
+  // in turn (measured, tools/group_env_ab.sh: S3C binning 34.7 -> 20.6 us,
+  // 46.1 -> 32.5 us per step; S3B 18.4 -> 18.1 us; config 3's ~10 events
+  // per item stay on 4 lanes: 16.5 vs 47 us)
+  if (e_seg >= 112.0 && n_seg_max > 1) c.group_lanes = bp::kWarpPerItem;
+  if (const char *g = std::getenv("BP_BIN_GROUP"); g && *g) {
+    const int v = std::atoi(g);
+    c.group_lanes = v == 4 ? 4 : v == bp::kWarpPerItem ? bp::kWarpPerItem : 32;
+  }
   c.n_seg_max = n_seg_max;
   return c;
 }

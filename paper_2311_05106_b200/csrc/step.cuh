@@ -122,12 +122,17 @@ struct NetProj {
   CsrSide c;                    // CSR: column-sliced rows, indices local
 };
 
+// ConnArgs::group_lanes value: one warp per (row, segment) item
+constexpr int kWarpPerItem = 64;
+
 struct ConnArgs {
   const NetProj *proj;      // device table [n_proj]
   int n_proj;
   int all_jit;              // every projection is JIT (the warp-batched path)
   uint32_t n_cols;          // all neurons (columns of every projection)
-  int group_lanes;          // JIT: lanes per (row, segment) item (4, 8 or 32)
+  int group_lanes;          // JIT binning split: 4 lanes per (row, segment) item,
+                            // 32 = a warp per row (its segments in turn), or
+                            // kWarpPerItem = a warp per (row, segment) item
   uint32_t n_seg_max;       // JIT: most local segments of any projection
 };
 
@@ -1398,6 +1403,10 @@ __device__ __forceinline__ uint32_t stage_list(const ConnArgs &conn, const BinTa
   } else if (conn.group_lanes < 32) {
     // few events per (row, segment): 4 lanes per item
     ev = stage_items<4>(conn, out, list, r_lo, r_hi, conn.n_seg_max, staged, n_staged, hist);
+  } else if (conn.group_lanes == kWarpPerItem) {
+    // long (row, segment) items, few rows: a whole warp per item, so a
+    // row's segments run on different warps
+    ev = stage_items<32>(conn, out, list, r_lo, r_hi, conn.n_seg_max, staged, n_staged, hist);
   } else {
     // warp w takes rows r_lo + w + 32 i (i = 0, 1, ...), 32 rows per batch
     for (int k0 = r_lo + static_cast<int>(warp); k0 < r_hi; k0 += kBinThreads)

@@ -280,6 +280,35 @@ def test_fig_s3_regimes_bit_exact(orc, n, p, steps, mode):
                           st["g_e"].view(np.uint32) if mode == "f32" else st["g_e"])
 
 
+@pytest.mark.parametrize("group", ["", "4", "32", "64"])
+def test_segmented_long_items_bit_exact(orc, monkeypatch, group):
+    """Rows of several long JIT segments (fan-in 1000, seg_len 4992 -> 5
+    segments, the last one 32 columns; ~250 events per (row, segment)):
+    every binning work split -- 4 lanes per item, a warp per row walking its
+    segments, a warp per (row, segment) item (the default here) -- gives the
+    oracle's raster and state bit for bit."""
+    if group:
+        monkeypatch.setenv("BP_BIN_GROUP", group)
+    n, p, steps, L = 20_000, 0.05, 300, 4992
+    scale = 80.0 / (p * n)
+    w = (0.6 * scale, 6.7 * scale)
+    net = CobaNetwork(n, conn="jit", fixed=True, p=p, w_exc=w[0], w_inh=w[1], seg_len=L)
+    if not group:
+        assert net.net.describe()["bin_lanes"] == 64
+    raster = torch.zeros((steps, (n + 31) // 32), dtype=torch.int32, device="cuda")
+    net.run(steps, raster)
+    n_exc = n * 4 // 5
+    K = orc.conn_len(p)
+    pe = orc.Projection(0, n_exc, jit=orc.JitSpec(SEED_E, K, L, orc.LAW_HOMO, w[0]))
+    pi = orc.Projection(n_exc, n - n_exc, jit=orc.JitSpec(SEED_I, K, L, orc.LAW_HOMO, w[1]))
+    st = dict(v=inputs.lif_v0(n), g_e=np.zeros(n, np.int64), g_i=np.zeros(n, np.int64),
+              ref=np.zeros(n, np.uint8), spikes=np.zeros(n, np.uint8))
+    want = orc.run_network("lif", orc.lif_params(), st, pe, pi, steps)
+    assert want.sum() > 0
+    assert np.array_equal(_raster(raster, n), want)
+    assert np.array_equal(net.state["g_e"].cpu().numpy(), st["g_e"])
+
+
 def test_execution_plan_choices():
     """bp_network_describe: the single-CTA loop for <= 4096 neurons, dense
     delivery for HH up to 2 M local neurons and tiles beyond (the

@@ -14,7 +14,7 @@ int main(int argc, char** argv) {
   const uint32_t L = argc > 2 ? (uint32_t)atoll(argv[2]) : n;
   const int n_active = argc > 3 ? atoi(argv[3]) : 27500;
   const int group = argc > 4 ? atoi(argv[4]) : 32;
-  const uint32_t n_exc = n / 5 * 4, K = n / 40 - 1;
+  const uint32_t n_exc = n / 5 * 4, K = argc > 5 ? (uint32_t)atoll(argv[5]) : n / 40 - 1;
   const uint32_t n_tiles = (n + kTile - 1) / kTile, cap = 17408;   // one partition: all n
   int32_t *active, *count; cudaMalloc(&active, n_active * 4); cudaMalloc(&count, 4);
   std::vector<int32_t> h(n_active);
