@@ -15,17 +15,25 @@ int main(int argc, char** argv) {
   const int n_active = argc > 3 ? atoi(argv[3]) : 27500;
   const int group = argc > 4 ? atoi(argv[4]) : 32;
   const uint32_t n_exc = n / 5 * 4, K = argc > 5 ? (uint32_t)atoll(argv[5]) : n / 40 - 1;
-  const uint32_t n_tiles = (n + kTile - 1) / kTile, cap = 17408;   // one partition: all n
+  // LOCAL=1: a rank's partition = the first segment [0, L) only (weak
+  // scaling: the remote rows' events restricted to the local segment)
+  const bool local = getenv("LOCAL") && atoi(getenv("LOCAL"));
+  const uint32_t n_loc = local ? L : n;
+  const uint32_t n_tiles = (n_loc + kTile - 1) / kTile, cap = 17408;
   int32_t *active, *count; cudaMalloc(&active, n_active * 4); cudaMalloc(&count, 4);
   std::vector<int32_t> h(n_active);
   for (int i = 0; i < n_active; ++i) h[i] = (int32_t)(((uint64_t)i * 2654435761u) % n);
+  // the library's lists are (nearly) ascending: compaction of the spike
+  // words in order, k_step's appends tile by tile -- E and I rows do not mix
+  // within a warp's items except at the boundary
+  if (!getenv("UNSORTED")) std::sort(h.begin(), h.end());
   cudaMemcpy(active, h.data(), n_active * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(count, &n_active, 4, cudaMemcpyHostToDevice);
   Buckets bk{}; cudaMalloc(&bk.cnt, (size_t)n_tiles * kCntStride * 4); cudaMalloc(&bk.flag, n_tiles * 4);
   cudaMalloc(&bk.buf, (size_t)n_tiles * cap * 4); cudaMalloc(&bk.spill, (size_t)2 * n * 4);
-  const uint32_t n_seg = (n + L - 1) / L;
+  const uint32_t n_seg = local ? 1u : (n + L - 1) / L;
   cudaMemset(bk.flag, 0, n_tiles * 4); cudaMemset(bk.spill, 0, (size_t)2 * n * 4);
-  BinTarget bt{bk, cap, n, 0};
+  BinTarget bt{bk, cap, n_loc, 0};
   NetProj tab[2] = {};
   tab[0].pre_begin = 0; tab[0].pre_end = n_exc; tab[0].conn = 0; tab[0].cls = 0;
   tab[0].j = JitSide{0x5EED0001, K, L, 0, n_seg, 0.6f, 0.f, 0, nullptr};
