@@ -137,18 +137,18 @@ struct ConnArgs {
 };
 
 __device__ __forceinline__ bool proj_has(const NetProj *P, int64_t r, uint32_t &row) {
-  const uint32_t lo = __ldg(&P->pre_begin), hi = __ldg(&P->pre_end);
+  const uint32_t lo = P->pre_begin, hi = P->pre_end;
   row = static_cast<uint32_t>(r) - lo;
   return static_cast<uint32_t>(r) >= lo && static_cast<uint32_t>(r) < hi;
 }
 
 __device__ __forceinline__ JitSide load_jit(const NetProj *P) {
   JitSide s;
-  s.seed = __ldg(&P->j.seed);
-  s.K = __ldg(&P->j.K);
-  s.L = __ldg(&P->j.L);
-  s.seg_first = __ldg(&P->j.seg_first);
-  s.n_seg = __ldg(&P->j.n_seg);
+  s.seed = P->j.seed;
+  s.K = P->j.K;
+  s.L = P->j.L;
+  s.seg_first = P->j.seg_first;
+  s.n_seg = P->j.n_seg;
   return s;
 }
 
@@ -163,8 +163,8 @@ __device__ __forceinline__ uint32_t deliver_row(const ConnArgs &c, const BinTarg
     const NetProj *P = c.proj + p;
     uint32_t row;
     if (!proj_has(P, r, row)) continue;
-    const uint32_t cls = __ldg(&P->cls);
-    if (__ldg(&P->conn) == 1) {
+    const uint32_t cls = P->cls;
+    if (P->conn == 1) {
       const int64_t *indptr = P->c.indptr;
       const int32_t *indices = P->c.indices;
       const int64_t begin = __ldg(indptr + row), end = __ldg(indptr + row + 1);
@@ -1086,8 +1086,8 @@ __device__ __forceinline__ uint32_t stage_row(const ConnArgs &c, const BinTarget
     const NetProj *P = c.proj + p;
     uint32_t row;
     if (!proj_has(P, r, row)) continue;
-    const uint32_t cls = __ldg(&P->cls);
-    if (__ldg(&P->conn) == 1) {
+    const uint32_t cls = P->cls;
+    if (P->conn == 1) {
       const int64_t *indptr = P->c.indptr;
       const int32_t *indices = P->c.indices;
       const int64_t begin = __ldg(indptr + row), end = __ldg(indptr + row + 1);
@@ -1165,7 +1165,7 @@ __device__ __forceinline__ uint32_t stage_rows_jit(const ConnArgs &c, const BinT
     const uint32_t members = __ballot_sync(0xffffffffu, mem);
     if (!members) continue;
     const JitSide s = load_jit(P);
-    const uint32_t pbit = __ldg(&P->cls) << kClsShift;
+    const uint32_t pbit = P->cls << kClsShift;
     for (uint32_t sidx = 0; sidx < s.n_seg; ++sidx) {
       const uint32_t seg = s.seg_first + sidx;
       const uint32_t seg_end = min(seg * s.L + s.L, c.n_cols);
@@ -1271,7 +1271,7 @@ __device__ __forceinline__ uint32_t stage_items(const ConnArgs &c, const BinTarg
       const JitSide s = load_jit(P);
       const bool mem_l = have_l && proj_has(P, r_l, row_l) && sidx_l < s.n_seg;
       if (!__ballot_sync(0xffffffffu, mem_l)) continue;
-      const uint32_t cbits = __ldg(&P->cls) << kClsShift;
+      const uint32_t cbits = P->cls << kClsShift;
       uint32_t first_l = 0;
       if (mem_l) {
         const uint32_t seg = s.seg_first + sidx_l;
@@ -1503,7 +1503,7 @@ constexpr int kWordsPT = BP_WORDS_PT;   // spike words per thread and listing ro
 
 template <bool WORDS>
 __global__ void __launch_bounds__(kBinThreads, 1)
-k_bin_sorted(ConnArgs conn, BinTarget out, const int32_t *active, const int32_t *count,
+k_bin_sorted(ConnArgs conn_g, BinTarget out, const int32_t *active, const int32_t *count,
              WordRange wr, unsigned long long *events, uint32_t n_tiles) {
   extern __shared__ uint32_t smem[];
   uint32_t *staged = smem;                                  // [kBinStage]
@@ -1513,8 +1513,20 @@ k_bin_sorted(ConnArgs conn, BinTarget out, const int32_t *active, const int32_t 
   __shared__ int32_t n_staged;
   __shared__ int32_t warp_sums[33];
   __shared__ unsigned long long block_ev;
+  __shared__ NetProj proj_s[kMaxProj];
   const int tid = threadIdx.x;
   const uint32_t lane = tid & 31u;
+  // the projection table in shared memory: every row's membership test and
+  // JIT parameters are then one shared load, not an L1/L2 round trip on the
+  // regeneration's dependency chain
+  ConnArgs conn = conn_g;
+  {
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(conn_g.proj);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(proj_s);
+    constexpr int words = static_cast<int>(sizeof(NetProj) / 4);
+    for (int i = tid; i < conn_g.n_proj * words; i += kBinThreads) dst[i] = src[i];
+    conn.proj = proj_s;
+  }
   pdl_trigger();
   pdl_wait();               // the active list / spike words of the producers are final
   uint32_t ev = 0;
@@ -1755,8 +1767,8 @@ k_small_net(SmallArgs a) {
         const NetProj *P = a.conn.proj + pj;
         uint32_t row;
         if (!proj_has(P, r, row)) continue;
-        int32_t *cnt = __ldg(&P->cls) ? cI : cE;       // standard layout: class = receptor
-        if (__ldg(&P->conn) == 1) {
+        int32_t *cnt = P->cls ? cI : cE;       // standard layout: class = receptor
+        if (P->conn == 1) {
           const int64_t *indptr = P->c.indptr;
           const int32_t *indices = P->c.indices;
           const int64_t b = __ldg(indptr + row), e = __ldg(indptr + row + 1);
