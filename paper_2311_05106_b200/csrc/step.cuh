@@ -130,9 +130,9 @@ struct ConnArgs {
   int n_proj;
   int all_jit;              // every projection is JIT (the warp-batched path)
   uint32_t n_cols;          // all neurons (columns of every projection)
-  int group_lanes;          // JIT binning split: 4 lanes per (row, segment) item,
-                            // 32 = a warp per row (its segments in turn), or
-                            // kWarpPerItem = a warp per (row, segment) item
+  int group_lanes;          // JIT binning split: 2 or 4 lanes per (row, segment)
+                            // item, 32 = a warp per row (its segments in turn),
+                            // or kWarpPerItem = a warp per (row, segment) item
   uint32_t n_seg_max;       // JIT: most local segments of any projection
 };
 
@@ -1400,6 +1400,9 @@ __device__ __forceinline__ uint32_t stage_list(const ConnArgs &conn, const BinTa
   if (!conn.all_jit) {
     for (int k = r_lo + static_cast<int>(warp); k < r_hi; k += kBinThreads / 32)
       ev += stage_row(conn, out, list[k], staged, n_staged, hist);
+  } else if (conn.group_lanes == 2) {
+    // ~10 events per item, one segment per row: 2 lanes per item
+    ev = stage_items<2>(conn, out, list, r_lo, r_hi, conn.n_seg_max, staged, n_staged, hist);
   } else if (conn.group_lanes < 32) {
     // few events per (row, segment): 4 lanes per item
     ev = stage_items<4>(conn, out, list, r_lo, r_hi, conn.n_seg_max, staged, n_staged, hist);

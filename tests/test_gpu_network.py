@@ -179,6 +179,45 @@ def test_partitions_emulated_on_one_gpu_equal_whole(orc, monkeypatch, compact, n
     assert np.array_equal(v.view(np.uint32), whole.state["v"].cpu().numpy().view(np.uint32))
 
 
+@pytest.mark.parametrize("group", ["", "2", "4"])
+def test_weak_partitions_item_lanes_equal_whole(orc, monkeypatch, group):
+    """8 partitions whose segment is the whole partition (the weak-scaling
+    layout) with ~10 events per (row, segment): the binning's 2-lanes-per-
+    item split (the default here) and the 4-lane one give the whole
+    network's state bit for bit; the whole network checks against the
+    oracle's raster."""
+    n, world, steps, L = 80_000, 8, 150, 10_016
+    whole = CobaNetwork(n, conn="jit", fixed=True, seg_len=L)
+    raster = torch.zeros((steps, (n + 31) // 32), dtype=torch.int32, device="cuda")
+    whole.run(steps, raster)
+    if group:
+        monkeypatch.setenv("BP_BIN_GROUP", group)
+    shared = torch.zeros(partition(n, world, 0, L).padded_words, dtype=torch.int32,
+                         device="cuda")
+    parts = [CobaNetwork(n, conn="jit", fixed=True, seg_len=L, rank=r, world=world,
+                         spikes=shared) for r in range(world)]
+    if not group:
+        assert parts[0].net.describe()["bin_lanes"] == 2
+    for _ in range(steps):
+        for q in parts:
+            q.net.scatter()
+        for q in parts:
+            q.net.update()
+    v = np.concatenate([q.state["v"].cpu().numpy() for q in parts])[:n]
+    assert np.array_equal(v.view(np.uint32), whole.state["v"].cpu().numpy().view(np.uint32))
+    ge = np.concatenate([q.state["g_e"].cpu().numpy() for q in parts])[:n]
+    assert np.array_equal(ge, whole.state["g_e"].cpu().numpy())
+    n_exc = n * 4 // 5
+    K = orc.conn_len(80.0 / n)
+    pe = orc.Projection(0, n_exc, jit=orc.JitSpec(SEED_E, K, L, orc.LAW_HOMO, 0.6))
+    pi = orc.Projection(n_exc, n - n_exc, jit=orc.JitSpec(SEED_I, K, L, orc.LAW_HOMO, 6.7))
+    st = dict(v=inputs.lif_v0(n), g_e=np.zeros(n, np.int64), g_i=np.zeros(n, np.int64),
+              ref=np.zeros(n, np.uint8), spikes=np.zeros(n, np.uint8))
+    want = orc.run_network("lif", orc.lif_params(), st, pe, pi, steps)
+    assert want.sum() > 0
+    assert np.array_equal(_raster(raster, n), want)
+
+
 @pytest.mark.parametrize("cap", ["1", "8", "64"])
 def test_bucket_overflow_spill_is_exact(orc, monkeypatch, cap):
     """Tiles receiving more events than their bucket holds spill into dense
