@@ -162,7 +162,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 def oracle_sample_steps(n_total: int, n_steps: int, fraction: float, seed: int = 7,
-                        wl: str = "coba_lif_jit"):
+                        wl: str = "coba_lif_jit", count_events: bool = True):
     """Time the oracle on a bounded sample of the same workload: each step
     delivers the spikes of `fraction` of the presynaptic rows (all of their
     events, E and I projections, Bernoulli(22 Hz * dt) activity -- the
@@ -198,6 +198,8 @@ def oracle_sample_steps(n_total: int, n_steps: int, fraction: float, seed: int =
         oracle.jit_event_mv(ji, n_rows_i, n_total, ev_i, out_kind=oracle.OUT_FIX, out=g_i)
         oracle.lif_step(params, v, g_e[:n_upd], g_i[:n_upd], ref)
     secs = time.perf_counter() - t0
+    if not count_events:
+        return secs, None, n_upd * n_steps
     # events delivered (outside the timed region): fan-out of every active row
     per_pattern = []
     for ev_e, ev_i in patterns:
@@ -252,6 +254,16 @@ def oracle_full_network(wl, n_total, csr, n_steps):
     return secs, events
 
 
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(wl, n_total, csr, budget_s: float = 15.0):
     if n_total > 1_000_000:
         fraction = 1.0 / 32
@@ -259,12 +271,30 @@ def cpu_baseline(wl, n_total, csr, budget_s: float = 15.0):
         per_step = max(secs / 2, 1e-3)
         steps = max(2, min(5000, int(budget_s / per_step)))
         secs, events, upd = oracle_sample_steps(n_total, steps, fraction, wl=wl)
-        return {"value": events / secs, "unit": UNIT, "cores": 1, "kind": "oracle",
-                "sample": (f"{steps} steps of the {n_total:,}-neuron network with 1/32 of "
-                           f"presynaptic rows active-eligible (Bernoulli 22 Hz x dt) and 1/32 "
-                           f"of neurons updated per step; {events:,} events in {secs:.1f} s, "
-                           f"single-threaded C oracle"),
-                "sim_s_per_wall_s_equiv": (steps * DT_MS * 1e-3 * fraction) / secs}
+        out = {"value": events / secs, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": (f"{steps} steps of the {n_total:,}-neuron network with 1/32 of "
+                          f"presynaptic rows active-eligible (Bernoulli 22 Hz x dt) and 1/32 "
+                          f"of neurons updated per step; {events:,} events in {secs:.1f} s, "
+                          f"single-threaded C oracle"),
+               "sim_s_per_wall_s_equiv": (steps * DT_MS * 1e-3 * fraction) / secs,
+               "cpu_model": _cpu_model()}
+        # the same sample with the oracle's host threads on every core (its
+        # order-free loops; bit-identical results -- SURVEY 8(d) asks for
+        # both timings)
+        import oracle
+        cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+        if cores and cores > 1:
+            oracle.set_threads(cores)
+            try:
+                secs_t, _, _ = oracle_sample_steps(n_total, steps, fraction, wl=wl,
+                                                   count_events=False)
+            finally:
+                oracle.set_threads(1)
+            out["all_cores"] = {"value": events / secs_t, "unit": UNIT, "cores": cores,
+                                "kind": "oracle (host threads)",
+                                "sample": f"the same {steps} steps; {events:,} events in "
+                                          f"{secs_t:.1f} s"}
+        return out
     secs, _ = oracle_full_network(wl, n_total, csr, 20)                 # calibrate
     steps = max(21, min(10_000, int(budget_s / max(secs / 20, 1e-6))))
     secs, events = oracle_full_network(wl, n_total, csr, steps)
