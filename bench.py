@@ -311,12 +311,21 @@ def run_reference(args):
         return
     n_total = N_PER_GPU * args.gpus
     fraction = 1.0 / 64
-    _, _, _ = oracle_sample_steps(n_total, max(1, args.warmup), fraction)
+    # the oracle with its host threads on every core of the box (its
+    # order-free loops; bit-identical to one thread)
+    import oracle
+    oracle.build()
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    cores = max(1, cores or 1)
+    oracle.set_threads(cores)
+    _, _, _ = oracle_sample_steps(n_total, max(1, args.warmup), fraction, count_events=False)
     secs, events, upd = oracle_sample_steps(n_total, args.steps, fraction)
+    oracle.set_threads(1)
     value = events / secs
     sample = (f"each step: 1/64 of the presynaptic rows (Bernoulli 22 Hz x dt) of the "
               f"{n_total:,}-neuron network delivered through the oracle's Listing S2 "
-              f"loop + 1/64 of the neurons updated (rule N1)")
+              f"loop + 1/64 of the neurons updated (rule N1); {cores} host threads "
+              f"({_cpu_model()})")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
@@ -324,7 +333,7 @@ def run_reference(args):
             "data": "synthetic",
             "config": {"workload": "coba_lif_jit", "n_per_gpu": N_PER_GPU,
                        "n_total": n_total, "fan_in": 80, "dt_ms": DT_MS},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
