@@ -424,3 +424,31 @@ def test_hh_partitions_emulated_equal_oracle(orc, monkeypatch, compact):
     assert np.array_equal(raster, want)
     v_got = np.concatenate([q.state["v"].cpu().numpy() for q in parts])
     assert np.array_equal(v_got.view(np.uint32), st["v"].view(np.uint32))
+
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+@pytest.mark.parametrize("delay", [1, 3])
+def test_hh_dense_delivery_with_delay_bit_exact(orc, monkeypatch, fused, delay):
+    """Dense HH delivery (the update kernel delivering its own spikes, or the
+    separate binning launch) into the bucket ring of reading D1: spikes of
+    step n arrive at step n + D; raster and V equal the oracle's."""
+    monkeypatch.setenv("BP_NO_SMALL_NET", "1")
+    monkeypatch.setenv("BP_HH_FUSED", fused)
+    n, steps = 4000, 300
+    n_exc = 3200
+    ipe, ixe, _ = inputs.random_csr(n_exc, n, 0.02, seed=11)
+    ipi, ixi, _ = inputs.random_csr(n - n_exc, n, 0.02, seed=12)
+    net = CobaNetwork(n, model="hh", conn="csr", fixed=True, csr=((ipe, ixe), (ipi, ixi)),
+                      delay=delay)
+    assert net.net.describe()["dense"] == 1
+    raster = torch.zeros((steps, n // 32), dtype=torch.int32, device="cuda")
+    net.run(steps, raster)
+    v, m, h, nk = inputs.hh_init(n)
+    st = dict(v=v, m=m, h=h, n=nk, g_e=np.zeros(n, np.int64), g_i=np.zeros(n, np.int64),
+              spikes=np.zeros(n, np.uint8))
+    pe = orc.Projection(0, n_exc, csr=(ipe, ixe, None), w_homo=6.0)
+    pi = orc.Projection(n_exc, n - n_exc, csr=(ipi, ixi, None), w_homo=67.0)
+    want = orc.run_network("hh", orc.hh_params(), st, pe, pi, steps, delay=delay)
+    assert want.sum() > 0
+    assert np.array_equal(_raster(raster, n), want)
+    assert np.array_equal(net.state["v"].cpu().numpy().view(np.uint32), st["v"].view(np.uint32))
