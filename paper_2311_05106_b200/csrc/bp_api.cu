@@ -1600,13 +1600,16 @@ bp::ConnArgs make_conn(bp_network *net, std::vector<bp::NetProj> *table) {
   // 46.1 -> 32.5 us per step; S3B 18.4 -> 18.1 us; config 3's ~10 events
   // per item stay on 4 lanes: 16.5 vs 47 us)
   if (e_seg >= 112.0 && n_seg_max > 1) c.group_lanes = bp::kWarpPerItem;
-  // one local segment of ~10 events per row (an 8-GPU weak-scaling rank:
-  // 80 / 8): 2 lanes per item, 16 items per warp in flight -- twice the
-  // rows per warp round, the same gaps per item in 2 steps of 8 (emulated
-  // rank of 8: 112.6 -> 109.9 us per step; at 2 GPUs, ~40 events per item,
-  // 4 lanes stay: 102.3 vs 105.7 us; config 3's 8 segments per row too:
-  // 30.5 vs 30.8 us; tools/group_small_ab.sh)
-  if (e_seg <= 16.0 && n_seg_max == 1) c.group_lanes = 2;
+  // one local segment of ~10 events per row in a LARGE network (an 8-GPU
+  // weak-scaling rank: 80 / 8 events, ~190 k rows per step): 2 lanes per
+  // item, 16 items per warp in flight -- twice the rows per warp round, the
+  // same gaps per item in 2 steps of 8 (emulated rank of 8: 112.6 -> 109.9
+  // us per step).  4 lanes stay at ~40 events per item (2 GPUs: 102.3 vs
+  // 105.7 us), for config 3's 8 segments per row (30.5 vs 30.8 us) and when
+  // the rows are few (config 3 on 8 GPUs, ~8 k rows per step: ~50 per
+  // binning block, 25.5 vs 26.3 us; the 2-lane split would leave warps idle)
+  // -- tools/group_small_ab.sh.  "Large": >= 16 M neurons in all.
+  if (e_seg <= 16.0 && n_seg_max == 1 && d.n >= (int64_t{1} << 24)) c.group_lanes = 2;
   if (const char *g = std::getenv("BP_BIN_GROUP"); g && *g) {
     const int v = std::atoi(g);
     c.group_lanes = (v == 2 || v == 4 || v == bp::kWarpPerItem) ? v : 32;

@@ -183,9 +183,9 @@ def test_partitions_emulated_on_one_gpu_equal_whole(orc, monkeypatch, compact, n
 def test_weak_partitions_item_lanes_equal_whole(orc, monkeypatch, group):
     """8 partitions whose segment is the whole partition (the weak-scaling
     layout) with ~10 events per (row, segment): the binning's 2-lanes-per-
-    item split (the default here) and the 4-lane one give the whole
-    network's state bit for bit; the whole network checks against the
-    oracle's raster."""
+    item split (the default for such networks from 16 M neurons) and the
+    4-lane one (the default at this size) give the whole network's state
+    bit for bit; the whole network checks against the oracle's raster."""
     n, world, steps, L = 80_000, 8, 150, 10_016
     whole = CobaNetwork(n, conn="jit", fixed=True, seg_len=L)
     raster = torch.zeros((steps, (n + 31) // 32), dtype=torch.int32, device="cuda")
@@ -197,7 +197,7 @@ def test_weak_partitions_item_lanes_equal_whole(orc, monkeypatch, group):
     parts = [CobaNetwork(n, conn="jit", fixed=True, seg_len=L, rank=r, world=world,
                          spikes=shared) for r in range(world)]
     if not group:
-        assert parts[0].net.describe()["bin_lanes"] == 2
+        assert parts[0].net.describe()["bin_lanes"] == 4
     for _ in range(steps):
         for q in parts:
             q.net.scatter()
