@@ -479,12 +479,15 @@ bp_status bp_network_counters(bp_network *net, uint64_t *host_out,
 size_t bp_network_device_bytes(const bp_network *net);
 /* The execution plan chosen at create, into out[0 .. n) (host int32, up to
  * 8): [0] single-CTA time loop, [1] dense delivery, [2] tiles, [3] bucket
- * capacity per tile, [4] weight-class fold (2 or 4), [5] binning lanes per
- * (row, segment) item, [6] library NCCL exchange, [7] weight classes. */
+ * capacity per tile, [4] weight-class fold (2 or 4), [5] JIT binning split
+ * (2 or 4 lanes per (row, segment) item, 32 = a warp per row, 64 = a warp
+ * per (row, segment) item), [6] library NCCL exchange, [7] weight classes. */
 bp_status bp_network_describe(const bp_network *net, int32_t *out, int32_t n);
 /* Per-kernel timing of the next bp_network_step calls (at most max_steps
  * steps): CUDA events are recorded on `stream` before the neuron-update
- * kernel, between it and the event-binning kernel, and after the latter.
+ * kernel, between it and the event-binning kernel, and after the latter
+ * (a step without a binning launch -- the dense HH update delivers its own
+ * spikes -- records an empty binning interval).
  * _end synchronises and returns the summed device milliseconds of the
  * update kernels (update_ms) and of the binning kernels (scatter_ms) and
  * the number of steps recorded. */
